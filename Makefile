@@ -1,0 +1,60 @@
+# Builds the product library (libvcs_gpu.so, sm_100a), the C++ drop-in shim, and the oracle
+# (test infrastructure: oracle/liboracle.so + oracle/_ref/libvcsref.so when /root/reference exists).
+CUDA      ?= /usr/local/cuda
+NVCC      ?= $(CUDA)/bin/nvcc
+CXX       ?= g++
+CC        ?= gcc
+PKG       := paper_2012_12419_b200
+SRC       := $(PKG)/csrc
+OBJ       := build/obj
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+CXXFLAGS  := -O2 -std=c++17 -fPIC -Wall -Wextra -I$(CUDA)/include
+REF       ?= /root/reference/proj
+JSON_INC  ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
+
+CU_SRCS   := $(SRC)/vcs_space.cu $(SRC)/vcs_solve.cu $(SRC)/vcs_greedy.cu
+CU_OBJS   := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU_SRCS))
+HOST_OBJS := $(OBJ)/vcs_host.o
+HDRS      := include/vcs_gpu.h $(SRC)/vcs_internal.h $(SRC)/vcs_device.cuh
+
+LIB       := $(PKG)/libvcs_gpu.so
+SHIM      := $(PKG)/libvcsched_b200.so
+ORACLE    := oracle/liboracle.so
+REFLIB    := oracle/_ref/libvcsref.so
+
+all: $(LIB) $(SHIM) $(ORACLE) ref
+
+$(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJ)/$*.ptxas.log || (cat $(OBJ)/$*.ptxas.log; false)
+
+$(OBJ)/vcs_host.o: $(SRC)/vcs_host.cpp $(HDRS)
+	@mkdir -p $(OBJ)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(LIB): $(CU_OBJS) $(HOST_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $^ -Xlinker -soname=libvcs_gpu.so
+
+$(SHIM): $(SRC)/vcsched_b200.cpp $(SRC)/vcsched_b200.hpp include/vcs_gpu.h $(LIB)
+	$(CXX) -O2 -std=c++20 -fPIC -shared -I$(SRC) -o $@ $(SRC)/vcsched_b200.cpp \
+	    -L$(PKG) -lvcs_gpu -Wl,-rpath,'$$ORIGIN'
+
+$(ORACLE): oracle/vcs_oracle.c include/vcs_gpu.h
+	$(CC) -O2 -std=gnu11 -fPIC -shared -ffp-contract=off -pthread -o $@ $< -lm
+
+# The unmodified reference, compiled from its own sources where they lie (never copied), with
+# the reference's Release flags (-O3 -DNDEBUG, no -march), plus the C shim of oracle/ref_capi.cpp.
+ref:
+	@if [ -d $(REF)/core/src ]; then $(MAKE) --no-print-directory $(REFLIB); \
+	 else echo "reference sources absent: using the prebuilt $(REFLIB) if present"; fi
+
+$(REFLIB): oracle/ref_capi.cpp include/vcs_gpu.h
+	@mkdir -p oracle/_ref
+	$(CXX) -std=c++20 -O3 -DNDEBUG -fPIC -shared -pthread -I$(REF)/core/include -I$(JSON_INC) \
+	    -o $@ $(REF)/core/src/*.cpp oracle/ref_capi.cpp
+
+clean:
+	rm -rf build $(LIB) $(SHIM) $(ORACLE) oracle/_ref
+
+.PHONY: all ref clean

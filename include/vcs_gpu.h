@@ -1,0 +1,240 @@
+/*
+ * vcs_gpu.h — C ABI of the B200-native vehicular-cloud placement solver.
+ *
+ * This is the drop-in boundary for the reference's solver path
+ * (reference: /root/reference/proj/core/include/vcsched/{workload,mdp,parallel_vi,greedy}.hpp).
+ * Every entry point below names the reference interface it replaces (file:line, relative to
+ * /root/reference/proj).  Plain C types only: the caller owns every input and output buffer,
+ * the library owns the device memory behind a `vcs_space` handle.
+ *
+ * Status codes mirror the reference CLI exit codes (tools/cli.hpp:30-33, tools/cli.cpp:225-240):
+ *   VCS_OK 0, VCS_EINVAL 2 (std::invalid_argument / ConfigError), VCS_ECAP 3 (StateCapacityError),
+ *   VCS_EIO 4 (IoError), VCS_ECUDA 5 (CUDA runtime / device failure), VCS_ERANGE 6 (std::out_of_range).
+ * The message of the last failure on the calling thread is returned by vcs_last_error(); the
+ * messages of the reference exceptions are reproduced verbatim (e.g. "reachable state space
+ * exceeds cap of N states", mdp.hpp:58-68).
+ *
+ * Threading: every call is synchronous and re-entrant; one handle must not be used by two host
+ * threads at once.  There is no global mutable state apart from the per-thread error message.
+ */
+#ifndef VCS_GPU_H
+#define VCS_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VCS_OK 0
+#define VCS_EINVAL 2
+#define VCS_ECAP 3
+#define VCS_EIO 4
+#define VCS_ECUDA 5
+#define VCS_ERANGE 6
+
+/* Sentinel target for the paid traditional cloud (workload.hpp:46 kPaidCloud). */
+#define VCS_PAID_CLOUD (-1)
+
+/*
+ * A placement problem in canonical order (mdp.hpp:18-23 MdpInstance; workload.hpp:12-43).
+ * Structure-of-arrays view; nothing is copied until a call needs it.
+ *   clouds: VehicularCloud{id, vm_total, vm_free, vm_throughput_kbps, v2i_delay_ms}
+ *   tasks : the FLATTENED task sequence (workload.cpp:28-33 flatten_tasks): bags in order,
+ *           tasks in order.  bot_task_offset (n_bots+1 entries, may be NULL) records the bag
+ *           boundaries for round trips; the solver and greedy only need the flat order.
+ *   beta_vc / beta_tc / gamma_vc: reward_per_vc_vm, cost_per_tcc_vm, penalty_per_idle_vm.
+ */
+typedef struct vcs_instance {
+    int32_t n_clouds;
+    const int32_t* cloud_id;
+    const int32_t* cloud_vm_total;
+    const int32_t* cloud_vm_free;
+    const double* cloud_thr_kbps;
+    const double* cloud_delay_ms;
+    int32_t n_tasks;
+    const int32_t* task_id;
+    const int32_t* task_demand;
+    const double* task_max_delay_ms;
+    const double* task_min_thr_kbps;
+    int32_t n_bots;
+    const int32_t* bot_id;          /* may be NULL when n_bots == 0 */
+    const int32_t* bot_task_offset; /* n_bots + 1 entries, may be NULL when n_bots == 0 */
+    double beta_vc;
+    double beta_tc;
+    double gamma_vc;
+} vcs_instance;
+
+/* ------------------------------------------------------------------------------------------ */
+/* Instance ingestion (host)                                                                   */
+/* ------------------------------------------------------------------------------------------ */
+
+/* An instance owned by the library (parsed or generated).  vcs_instance_view() returns a view
+ * whose pointers stay valid until vcs_instance_free(). */
+typedef struct vcs_instance_owned vcs_instance_owned;
+
+/* Replaces io.cpp:51-95 parse_instance (grammar of io.hpp:33-40; vm_free = vm_total, io.cpp:71;
+ * validate() of workload.cpp:35-57).  Errors: VCS_EINVAL with the ConfigError text. */
+int vcs_instance_parse(const char* text, vcs_instance_owned** out);
+/* Replaces io.cpp:97-101 load_instance.  Errors: VCS_EIO "cannot read instance file: <path>". */
+int vcs_instance_load(const char* path, vcs_instance_owned** out);
+/* Build an owned copy of a caller view (runs validate()). */
+int vcs_instance_copy(const vcs_instance* in, vcs_instance_owned** out);
+const vcs_instance* vcs_instance_view(const vcs_instance_owned* inst);
+void vcs_instance_free(vcs_instance_owned* inst);
+
+/* Seeded synthetic instances (std::mt19937_64 + libstdc++ uniform_int_distribution, so the
+ * same seed yields the same instance as the reference's generators).
+ *   kind VCS_GEN_RANDOM : tests/testutil.hpp:28-65 random_instance(rng, {a,b,c,d}); the
+ *                         `trial`-th instance drawn from one rng seeded with `seed`.
+ *   kind VCS_GEN_HOMOG  : SURVEY §8(d) C3/C4 family: a clouds {vm_total b, thr 100, delay 10},
+ *                         c tasks {demand U[1,d], max_delay 100, min_thr 50}, a bags round-robin.
+ *   kind VCS_GEN_GREEDY : SURVEY §8(d) C2: a clouds {U[50,150] VMs, thr U[60,160], delay U[5,50]},
+ *                         b bags x c tasks {demand U[1,d], max_delay U[5,60], min_thr U[50,170]}. */
+#define VCS_GEN_RANDOM 0
+#define VCS_GEN_HOMOG 1
+#define VCS_GEN_GREEDY 2
+int vcs_instance_generate(int kind, uint64_t seed, int32_t trial, int32_t a, int32_t b, int32_t c,
+                          int32_t d, vcs_instance_owned** out);
+
+/* ------------------------------------------------------------------------------------------ */
+/* State space (device)                                                                        */
+/* ------------------------------------------------------------------------------------------ */
+
+typedef struct vcs_space vcs_space;
+
+typedef struct vcs_space_info {
+    uint64_t n_states;  /* StateSpace::size() (mdp.hpp:88) */
+    uint64_t n_edges;
+    int32_t horizon;    /* StateSpace::task_count() (mdp.hpp:89) */
+    int32_t key_words;  /* 64-bit words per packed reduced key */
+    uint64_t max_layer; /* largest layer, states */
+    int32_t max_degree; /* largest out-degree */
+    int32_t device;
+    double build_ms;    /* device build time (CUDA events) */
+    uint64_t device_bytes; /* resident bytes of the CSR + value buffers */
+} vcs_space_info;
+
+/* Replaces mdp.cpp:81-214 StateSpace::build.  The layered reachable-state enumeration runs on
+ * `device`; the CSR (row_ptr, succ, reward, action) and the per-layer packed keys stay resident
+ * in HBM.  Enumeration order, edge order (clouds ascending then paid), successor indices and
+ * fp64 reward bits equal the reference's.  Errors: VCS_ECAP "reachable state space exceeds cap
+ * of N states"; VCS_EINVAL "cloud free counts above 65535 are not supported". */
+int vcs_space_build(const vcs_instance* inst, uint64_t state_cap, int device, vcs_space** out);
+/* Test seam: upload an externally built CSR (e.g. the oracle's) instead of building it, so the
+ * solver can be validated independently of the builder.  row_ptr has n_states+1 entries,
+ * layer_offset horizon+2 entries (mdp.hpp:119-128 layout). */
+int vcs_space_from_csr(uint64_t n_states, uint64_t n_edges, int32_t horizon,
+                       const uint64_t* layer_offset, const uint64_t* row_ptr, const uint32_t* succ,
+                       const double* reward, const int32_t* action, int device, vcs_space** out);
+int vcs_space_info_get(const vcs_space* sp, vcs_space_info* info);
+/* layer_offset: horizon+2 entries (StateSpace::layer_begin/layer_end, mdp.hpp:90-91). */
+int vcs_space_layer_offsets(const vcs_space* sp, uint64_t* layer_offset);
+/* Download the CSR (any pointer may be NULL to skip that array). */
+int vcs_space_csr(const vcs_space* sp, uint64_t* row_ptr, uint32_t* succ, double* reward,
+                  int32_t* action);
+/* Replaces mdp.cpp:227-234 StateSpace::locate for a batch of full states.  free_vms is
+ * n x n_clouds (row-major), task_index the next_task_index, terminal 0/1.  idx_out[i] receives
+ * the flat state index, or -1 when the state is not reachable (the reference throws
+ * std::out_of_range "state not reachable in enumerated space"). */
+int vcs_space_locate(vcs_space* sp, int64_t n, const int32_t* free_vms, const int32_t* task_index,
+                     const uint8_t* terminal, int64_t* idx_out);
+/* Replaces mdp.cpp:236-243 StateSpace::hidden_penalty for a batch of full states. */
+int vcs_space_hidden_penalty(const vcs_space* sp, int64_t n, const int32_t* free_vms,
+                             const int32_t* task_index, const uint8_t* terminal, double* out);
+void vcs_space_free(vcs_space* sp);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Value iteration (device)                                                                    */
+/* ------------------------------------------------------------------------------------------ */
+
+typedef struct vcs_solve_opts {
+    double epsilon;         /* ViOptions::epsilon (mdp.hpp:131-134), default 1e-6 */
+    int32_t skip_converged; /* 1: skip layers proven exact (bit-identical) */
+    int32_t max_sweeps;     /* 0 = no cap (the reference has none) */
+    double discount;        /* 1.0 = the reference's undiscounted backup (mdp.cpp:255).  Any
+                               other value is the labelled EXTENSION q = r + discount*V(s')
+                               (BASELINE.json configs[0] "gamma=0.9"); it has no reference
+                               counterpart and is checked against the C oracle only. */
+} vcs_solve_opts;
+
+typedef struct vcs_solve_report {
+    int32_t sweeps;            /* ValueTable::sweeps() */
+    int32_t launches;          /* device kernel launches issued by the solve */
+    uint64_t backups_ref;      /* reference-equivalent backups = n_states * sweeps */
+    uint64_t backups_done;     /* backups actually performed (layer skip) */
+    double sweep_ms;           /* sweeps only, CUDA events */
+    double extract_ms;         /* policy extraction, CUDA events */
+    double alg_bytes;          /* SURVEY §8(d) algorithmic bytes of the sweeps: (24+12 d) per backup_ref */
+    double alg_bytes_done;     /* same formula over the performed backups */
+} vcs_solve_report;
+
+/* Replaces parallel_vi.cpp:48-116 detail::run_value_iteration (the sweep loop, the sup-norm
+ * residual `delta < epsilon`, buffer parity, and the argmax extraction of
+ * parallel_vi.cpp:109-111).  values_out (n_states f64) and actions_out (n_states i32) may be
+ * NULL.  Bit-identical to the reference for every epsilon (same sweep count). */
+int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int32_t* actions_out,
+              vcs_solve_report* report);
+
+/* Sharded (multi-GPU) building blocks.  One process per GPU; the host runtime owns the value
+ * buffers and the collectives (torch.distributed / NCCL over NVLink), these calls only enqueue
+ * device work on `stream` (a cudaStream_t; NULL = the space's own stream) and never synchronise
+ * except vcs_shard_finish.  Together they replace the block-parallel worker of
+ * parallel_vi.cpp:68-107 (BlockPartition + SweepBarrier + per-block residual fold).
+ *   vcs_shard_plan   : host-only.  Row block [row_begin,row_end) of `rank` (contiguous, balanced
+ *                      on the per-layer edge/state cost; skip_weighted also weights a layer by
+ *                      the number of sweeps that visit it) and the forward halo
+ *                      [halo_begin,halo_end) of successor rows owned by later ranks.
+ *   vcs_shard_begin  : adopt caller-owned device buffers v0/v1 (n_states f64 each) and delta
+ *                      (n_delta >= horizon+3 f64: slot k = residual of sweep k); zero them.
+ *   vcs_shard_sweep  : sweep k (1-based) over [row_begin,row_end) reading v[(k-1)&1], writing
+ *                      v[k&1] and the block residual into delta[k] (atomic max).  The host
+ *                      all-reduces delta[k] (MAX) and exchanges the halo before sweep k+1, whose
+ *                      prologue evaluates `delta[k] < eps` on the device (no host round trip).
+ *   vcs_shard_finish : policy extraction over [row_begin,row_end) from the converged buffer and
+ *                      download of that block's values/actions into the host arrays (indexed by
+ *                      flat state); *sweeps_out = the converged sweep count. */
+int vcs_shard_plan(const uint64_t* layer_offset, const uint64_t* layer_edges, int32_t horizon,
+                   int32_t world, int32_t rank, int32_t skip_weighted, uint64_t* row_begin,
+                   uint64_t* row_end, uint64_t* halo_begin, uint64_t* halo_end);
+int vcs_space_layer_edges(const vcs_space* sp, uint64_t* layer_edges); /* horizon+1 entries */
+int vcs_shard_begin(vcs_space* sp, double* v0, double* v1, double* delta, int32_t n_delta,
+                    void* stream);
+int vcs_shard_sweep(vcs_space* sp, int32_t k, uint64_t row_begin, uint64_t row_end,
+                    const vcs_solve_opts* opts, void* stream);
+int vcs_shard_finish(vcs_space* sp, int32_t n_sweeps, uint64_t row_begin, uint64_t row_end,
+                     const vcs_solve_opts* opts, double* values_out, int32_t* actions_out,
+                     int32_t* sweeps_out, void* stream);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Greedy placement (device)                                                                   */
+/* ------------------------------------------------------------------------------------------ */
+
+/* Replaces greedy.cpp:5-30 greedy_schedule (Alg. 2 first-fit).  target_per_task[i] receives the
+ * cloud INDEX (position in the cloud list) of flattened task i, or VCS_PAID_CLOUD;
+ * per_cloud_used (n_clouds entries, may be NULL) the VMs placed per cloud index; *paid and
+ * *unused as ScheduleResult::paid_vms / unused_vms (unused = total_capacity - placed,
+ * greedy.cpp:28).  Placements are bit-exact against the reference. */
+int vcs_greedy(const vcs_instance* inst, int device, int32_t* target_per_task,
+               int64_t* per_cloud_used, int64_t* paid, int64_t* unused);
+/* n independent instances in one launch (one warp each). */
+int vcs_greedy_batch(int32_t n, const vcs_instance* insts, int device, int32_t** target_per_task,
+                     int64_t* paid, int64_t* unused);
+/* greedy.cpp:32-36 greedy_reward. */
+double vcs_greedy_reward(const vcs_instance* inst, int64_t placed, int64_t paid, int64_t unused);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Diagnostics                                                                                 */
+/* ------------------------------------------------------------------------------------------ */
+
+const char* vcs_last_error(void);
+/* Number of device kernels this library launched on the calling process so far. */
+uint64_t vcs_kernel_launches(void);
+/* 1 when a CUDA device is usable, else 0 (no kernel is launched). */
+int vcs_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VCS_GPU_H */

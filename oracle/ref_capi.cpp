@@ -1,0 +1,270 @@
+// oracle/ref_capi.cpp — TEST INFRASTRUCTURE ONLY (never linked into the product).
+//
+// A plain-C shim over the UNMODIFIED reference C++ library (compiled from
+// /root/reference/proj/core/src/*.cpp by oracle/Makefile into oracle/_ref/libvcsref.so).
+// It lets the Python tests and bench.py's reference arm drive the reference solver through
+// its own public API:
+//   StateSpace::build            core/src/mdp.cpp:81-214
+//   detail::run_value_iteration  core/src/parallel_vi.cpp:48-116
+//   ValueTable / Policy / rollout core/src/mdp.cpp:269-324
+//   greedy_schedule / greedy_reward core/src/greedy.cpp:5-36
+// Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline / --impl reference) load it.
+#include "vcsched/greedy.hpp"
+#include "vcsched/io.hpp"
+#include "vcsched/mdp.hpp"
+#include "vcsched/parallel_vi.hpp"
+
+#include "../include/vcs_gpu.h"
+
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+using namespace vcsched;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        return f();
+    } catch (const StateCapacityError& e) {
+        return fail(VCS_ECAP, e.what());
+    } catch (const std::invalid_argument& e) {
+        return fail(VCS_EINVAL, e.what());
+    } catch (const ConfigError& e) {
+        return fail(VCS_EINVAL, e.what());
+    } catch (const IoError& e) {
+        return fail(VCS_EIO, e.what());
+    } catch (const std::out_of_range& e) {
+        return fail(VCS_ERANGE, e.what());
+    } catch (const std::exception& e) {
+        return fail(1, e.what());
+    }
+}
+
+struct Converted {
+    VccModel vcc;
+    std::vector<BagOfTasks> bots;
+};
+
+Converted convert(const vcs_instance* in) {
+    Converted c;
+    for (int i = 0; i < in->n_clouds; ++i) {
+        VehicularCloud cl;
+        cl.id = in->cloud_id[i];
+        cl.vm_total = in->cloud_vm_total[i];
+        cl.vm_free = in->cloud_vm_free[i];
+        cl.vm_throughput_kbps = in->cloud_thr_kbps[i];
+        cl.v2i_delay_ms = in->cloud_delay_ms[i];
+        c.vcc.clouds.push_back(cl);
+    }
+    c.vcc.reward_per_vc_vm = in->beta_vc;
+    c.vcc.cost_per_tcc_vm = in->beta_tc;
+    c.vcc.penalty_per_idle_vm = in->gamma_vc;
+    auto task_at = [&](int j) {
+        Task t;
+        t.id = in->task_id[j];
+        t.vm_demand = in->task_demand[j];
+        t.max_delay_ms = in->task_max_delay_ms[j];
+        t.min_vm_throughput_kbps = in->task_min_thr_kbps[j];
+        return t;
+    };
+    if (in->n_bots > 0 && in->bot_task_offset) {
+        for (int b = 0; b < in->n_bots; ++b) {
+            BagOfTasks bot;
+            bot.id = in->bot_id ? in->bot_id[b] : b + 1;
+            for (int j = in->bot_task_offset[b]; j < in->bot_task_offset[b + 1]; ++j)
+                bot.tasks.push_back(task_at(j));
+            c.bots.push_back(std::move(bot));
+        }
+    } else if (in->n_tasks > 0) {
+        BagOfTasks bot;
+        bot.id = 1;
+        for (int j = 0; j < in->n_tasks; ++j) bot.tasks.push_back(task_at(j));
+        c.bots.push_back(std::move(bot));
+    }
+    return c;
+}
+
+struct RefSpace {
+    MdpInstance inst;
+    std::shared_ptr<const StateSpace> space;
+};
+
+struct RefResult {
+    MdpInstance inst;
+    ViResult vi;
+};
+
+MdpState make_state(const int32_t* free_vms, int n_clouds, int32_t t, uint8_t terminal) {
+    MdpState s;
+    s.free_vms.assign(free_vms, free_vms + n_clouds);
+    s.next_task_index = t;
+    s.terminal = terminal != 0;
+    return s;
+}
+
+} // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+int ref_hardware_threads(void) {
+    const unsigned n = std::thread::hardware_concurrency();
+    return n == 0 ? 1 : static_cast<int>(n);
+}
+
+int ref_space_build(const vcs_instance* in, uint64_t cap, void** out, double* build_ms) {
+    return guarded([&] {
+        auto c = convert(in);
+        auto h = std::make_unique<RefSpace>();
+        h->inst = MdpInstance::from_workload(c.vcc, c.bots);
+        const auto t0 = std::chrono::steady_clock::now();
+        h->space = StateSpace::build(h->inst, static_cast<std::size_t>(cap));
+        const auto t1 = std::chrono::steady_clock::now();
+        if (build_ms) *build_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        *out = h.release();
+        return VCS_OK;
+    });
+}
+
+void ref_space_free(void* h) { delete static_cast<RefSpace*>(h); }
+
+uint64_t ref_space_size(void* h) { return static_cast<RefSpace*>(h)->space->size(); }
+
+int32_t ref_space_horizon(void* h) { return static_cast<RefSpace*>(h)->space->task_count(); }
+
+void ref_space_layers(void* h, uint64_t* off) {
+    const auto& sp = *static_cast<RefSpace*>(h)->space;
+    for (int t = 0; t <= sp.task_count(); ++t) off[t] = sp.layer_begin(t);
+    off[sp.task_count() + 1] = sp.layer_end(sp.task_count());
+}
+
+// detail::run_value_iteration on the prebuilt space (the reference's own timing convention,
+// parallel_vi.cpp:126-147: build excluded, sweeps + extraction timed with steady_clock).
+int ref_vi(void* h, double eps, int workers, void** res_out, int32_t* sweeps, double* ms) {
+    return guarded([&] {
+        auto* rs = static_cast<RefSpace*>(h);
+        ViOptions opts;
+        opts.epsilon = eps;
+        const auto t0 = std::chrono::steady_clock::now();
+        ViResult r = detail::run_value_iteration(rs->space, opts, workers);
+        const auto t1 = std::chrono::steady_clock::now();
+        if (ms) *ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        if (sweeps) *sweeps = r.values.sweeps();
+        *res_out = new RefResult{rs->inst, std::move(r)};
+        return VCS_OK;
+    });
+}
+
+void ref_res_free(void* r) { delete static_cast<RefResult*>(r); }
+
+void ref_res_values(void* r, double* out) {
+    const auto v = static_cast<RefResult*>(r)->vi.values.raw_values();
+    std::memcpy(out, v.data(), v.size() * sizeof(double));
+}
+
+void ref_res_actions(void* r, int32_t* out) {
+    const auto a = static_cast<RefResult*>(r)->vi.policy.raw_actions();
+    std::memcpy(out, a.data(), a.size() * sizeof(int32_t));
+}
+
+int ref_res_initial_value(void* r, double* out) {
+    return guarded([&] {
+        *out = static_cast<RefResult*>(r)->vi.values.initial_value();
+        return VCS_OK;
+    });
+}
+
+int ref_res_value_of(void* r, const int32_t* free_vms, int32_t t, uint8_t terminal, double* out) {
+    return guarded([&] {
+        auto* rr = static_cast<RefResult*>(r);
+        const int n = static_cast<int>(rr->inst.vcc.clouds.size());
+        *out = rr->vi.values.value_of(make_state(free_vms, n, t, terminal));
+        return VCS_OK;
+    });
+}
+
+int ref_res_action_for(void* r, const int32_t* free_vms, int32_t t, uint8_t terminal,
+                       int32_t* out) {
+    return guarded([&] {
+        auto* rr = static_cast<RefResult*>(r);
+        const int n = static_cast<int>(rr->inst.vcc.clouds.size());
+        *out = rr->vi.policy.action_for(make_state(free_vms, n, t, terminal)).target;
+        return VCS_OK;
+    });
+}
+
+// rollout (mdp.cpp:305-324); targets are cloud INDICES (or -1) so they compare with the
+// product's vcs_greedy/rollout output; per_cloud_used is indexed by cloud position.
+int ref_res_rollout(void* r, int32_t* targets, int64_t* per_cloud_used, int64_t* paid,
+                    int64_t* unused, double* reward) {
+    return guarded([&] {
+        auto* rr = static_cast<RefResult*>(r);
+        const auto res = rollout(rr->vi.policy, rr->inst);
+        const auto& clouds = rr->inst.vcc.clouds;
+        // The reference reports cloud ids; re-derive the index by replaying the policy.
+        MdpState s = initial_state(rr->inst);
+        std::size_t i = 0;
+        while (!s.terminal) {
+            const MdpAction a = rr->vi.policy.action_for(s);
+            targets[i++] = a.target;
+            s = transition(s, a, rr->inst);
+        }
+        if (per_cloud_used)
+            for (std::size_t c = 0; c < clouds.size(); ++c)
+                per_cloud_used[c] = res.per_vc_used.at(clouds[c].id);
+        *paid = res.paid_vms;
+        *unused = res.unused_vms;
+        *reward = greedy_reward(res, rr->inst.vcc);
+        return VCS_OK;
+    });
+}
+
+// greedy_schedule + greedy_reward (greedy.cpp:5-36).  targets receive cloud IDS as the
+// reference's PlacementRecord::target does (kPaidCloud for paid).
+int ref_greedy(const vcs_instance* in, int32_t* target_ids, int32_t* vms_used, int64_t* paid,
+               int64_t* unused, int64_t* placed, double* reward, double* ms) {
+    return guarded([&] {
+        auto c = convert(in);
+        const auto t0 = std::chrono::steady_clock::now();
+        const auto r = greedy_schedule(c.vcc, c.bots);
+        const auto t1 = std::chrono::steady_clock::now();
+        if (ms) *ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        for (std::size_t i = 0; i < r.placements.size(); ++i) {
+            target_ids[i] = r.placements[i].target;
+            if (vms_used) vms_used[i] = r.placements[i].vms_used;
+        }
+        *paid = r.paid_vms;
+        *unused = r.unused_vms;
+        *placed = r.vc_placed_vms();
+        *reward = greedy_reward(r, c.vcc);
+        return VCS_OK;
+    });
+}
+
+// The reference's own parser (io.cpp:51-101), for cross-checking the product parser.
+int ref_load_counts(const char* path, int32_t* n_clouds, int32_t* n_tasks, int32_t* n_bots) {
+    return guarded([&] {
+        const auto p = load_instance(path);
+        *n_clouds = static_cast<int32_t>(p.vcc.clouds.size());
+        *n_tasks = static_cast<int32_t>(flatten_tasks(p.bots).size());
+        *n_bots = static_cast<int32_t>(p.bots.size());
+        return VCS_OK;
+    });
+}
+
+} // extern "C"

@@ -1,0 +1,138 @@
+// vcs_device.cuh — device-side internals shared by the builder, solver and greedy units.
+#pragma once
+
+#include "vcs_internal.h"
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <tuple>
+
+#define VCS_CUDA(call)                                                                         \
+    do {                                                                                       \
+        cudaError_t err_ = (call);                                                             \
+        if (err_ != cudaSuccess)                                                               \
+            ::vcs::raise(VCS_ECUDA, std::string(#call) + ": " + cudaGetErrorString(err_));     \
+    } while (0)
+
+#define VCS_LAUNCHED()                                                                         \
+    do {                                                                                       \
+        cudaError_t err_ = cudaGetLastError();                                                 \
+        if (err_ != cudaSuccess)                                                               \
+            ::vcs::raise(VCS_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(err_)); \
+        ::vcs::note_launch();                                                                  \
+    } while (0)
+
+namespace vcs {
+
+constexpr uint32_t kEmpty32 = 0xffffffffu;
+
+// RAII device buffer (cudaMalloc / cudaFree), growable with copy.
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0; // capacity in elements
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    // Ensure capacity >= want; keeps the first `keep` elements when it must reallocate.
+    void reserve(size_t want, size_t keep, cudaStream_t s, double growth = 1.5) {
+        if (want <= n) return;
+        size_t cap = n ? static_cast<size_t>(static_cast<double>(n) * growth) : want;
+        if (cap < want) cap = want;
+        T* np = nullptr;
+        VCS_CUDA(cudaMalloc(&np, cap * sizeof(T)));
+        if (p && keep)
+            VCS_CUDA(cudaMemcpyAsync(np, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, s));
+        if (p) {
+            VCS_CUDA(cudaStreamSynchronize(s));
+            cudaFree(p);
+        }
+        p = np;
+        n = cap;
+    }
+    void exact(size_t want) { // discard contents, capacity exactly `want` if it must grow
+        if (want <= n) return;
+        release();
+        VCS_CUDA(cudaMalloc(&p, (want ? want : 1) * sizeof(T)));
+        n = want ? want : 1;
+    }
+};
+
+// Device-side control block of one solve.
+struct SolveCtrl {
+    int32_t stop;   // sticky: set by the first sweep that sees delta[k-1] < eps
+    int32_t sweeps; // K*: the converged sweep count
+};
+
+struct GraphKey {
+    double eps;
+    double discount;
+    int skip;
+    int max_sweeps;
+    bool operator<(const GraphKey& o) const {
+        return std::tie(eps, discount, skip, max_sweeps) <
+               std::tie(o.eps, o.discount, o.skip, o.max_sweeps);
+    }
+};
+
+struct CachedGraph {
+    cudaGraphExec_t exec = nullptr;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    int n_sweeps = 0; // sweep kernels in the graph
+    int launches = 0;
+};
+
+} // namespace vcs
+
+struct vcs_space {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint64_t S = 0, E = 0;
+    int H = 0;
+    int max_degree = 1;
+    uint64_t max_layer = 0;
+    double build_ms = 0.0;
+    std::vector<uint64_t> layer_off;   // H+2
+    std::vector<uint64_t> layer_edges; // H+1: edges leaving layer t
+    bool has_plan = false;
+    vcs::LayerPlan plan;
+    std::vector<uint64_t> key_off;     // H+2: offset (u64 words) of layer t's packed keys
+
+    // CSR in HBM (row_ptr u32 since E < 2^32 is enforced; succ u32 as mdp.hpp:126)
+    vcs::DevBuf<uint32_t> row_ptr;
+    vcs::DevBuf<uint32_t> succ;
+    vcs::DevBuf<double> reward;
+    vcs::DevBuf<int32_t> action;
+    vcs::DevBuf<uint64_t> keys;
+
+    // value iteration state
+    vcs::DevBuf<double> v[2];
+    vcs::DevBuf<double> delta;   // residual per sweep (index k = sweep k)
+    vcs::DevBuf<vcs::SolveCtrl> ctrl;
+    vcs::DevBuf<int32_t> actions_dev;
+    std::map<vcs::GraphKey, vcs::CachedGraph> graphs;
+    double* shard_v0 = nullptr; // caller-owned device buffers of the sharded driver
+    double* shard_v1 = nullptr;
+    double* shard_delta = nullptr;
+    int shard_n_delta = 0;
+
+    // lazily built device index for locate (hash over (layer, key) -> state)
+    vcs::DevBuf<uint32_t> loc_table;
+    uint64_t loc_cap = 0;
+
+    int num_sms = 148;
+    ~vcs_space();
+};
+
+namespace vcs {
+void bind_device(int device);
+int sm_count(int device);
+}

@@ -1,0 +1,352 @@
+// vcs_greedy.cu — Alg. 2 first-fit placement on the device (replaces greedy_schedule,
+// greedy.cpp:5-30, with feasible() of workload.cpp:22-26).
+//
+// The scan is inherently sequential through vm_free, so the work is split in two:
+//   1. k_attr_mask (all SMs): the batched feasibility scoring.  For every (task, cloud) pair the
+//      link test `delay <= max_delay && thr >= min_thr` becomes one bit; a warp covers 32 clouds
+//      and emits one 32-bit word with a ballot.  T x ceil(K/32) words.
+//   2. k_first_fit (one warp per instance): per task, lane l ANDs its attribute word(s) with the
+//      capacity word "free >= demand" (kept incrementally per distinct demand value in shared
+//      memory), a ballot finds the lowest word with a candidate and ffs the lowest cloud —
+//      exactly the first cloud in list order that feasible() accepts.  The next tasks'
+//      attribute words are prefetched into registers while the current batch is scanned.
+// Placements are bit-exact against the reference (same first feasible cloud, same paid set).
+#include "vcs_device.cuh"
+
+#include <algorithm>
+#include <set>
+
+namespace vcs {
+
+namespace {
+
+constexpr int kMaxLevels = 16;
+constexpr int kPrefetch = 16;
+
+struct GreedyDesc {
+    int32_t K, T, W, n_levels; // n_levels == 0: generic capacity test from free counts
+    const uint32_t* mask;      // T x W attribute words
+    const int2* task;          // T: {level, demand}
+    const int32_t* levels;     // n_levels distinct demands (ascending)
+    int32_t* free_vms;         // K: in = vm_free, out = remaining free VMs
+    int32_t* target;           // T: cloud index or -1
+    long long* paid;           // 1
+};
+
+__global__ void k_attr_mask(int32_t K, int32_t T, int32_t W, const double* __restrict__ c_delay,
+                            const double* __restrict__ c_thr, const double* __restrict__ t_delay,
+                            const double* __restrict__ t_thr, uint32_t* __restrict__ mask) {
+    const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint64_t total = static_cast<uint64_t>(T) * static_cast<uint64_t>(W);
+    for (uint64_t item = warp; item < total; item += n_warps) {
+        const uint64_t j = item / static_cast<uint64_t>(W);
+        const int w = static_cast<int>(item - j * static_cast<uint64_t>(W));
+        const int c = w * 32 + lane;
+        bool ok = false;
+        if (c < K) ok = c_delay[c] <= t_delay[j] && c_thr[c] >= t_thr[j];
+        const uint32_t bits = __ballot_sync(0xffffffffu, ok);
+        if (lane == 0) mask[item] = bits;
+    }
+}
+
+__device__ __forceinline__ uint32_t cap_bits_generic(const int32_t* __restrict__ fr, int K, int w,
+                                                     int d) {
+    uint32_t bits = 0;
+    const int c0 = w * 32;
+#pragma unroll 8
+    for (int b = 0; b < 32; ++b) {
+        const int c = c0 + b;
+        if (c < K && fr[c] >= d) bits |= 1u << b;
+    }
+    return bits;
+}
+
+// One warp per instance.  Shared memory: free[K] then cap[n_levels][W].
+__global__ void __launch_bounds__(32) k_first_fit(const GreedyDesc* __restrict__ descs) {
+    extern __shared__ int32_t sm[];
+    const GreedyDesc D = descs[blockIdx.x];
+    const int lane = threadIdx.x;
+    int32_t* fr = sm;
+    uint32_t* cap = reinterpret_cast<uint32_t*>(sm + D.K);
+    for (int c = lane; c < D.K; c += 32) fr[c] = D.free_vms[c];
+    __syncwarp();
+    for (int L = 0; L < D.n_levels; ++L)
+        for (int w = lane; w < D.W; w += 32) {
+            uint32_t bits = 0;
+            for (int b = 0; b < 32; ++b) {
+                const int c = w * 32 + b;
+                if (c < D.K && fr[c] >= D.levels[L]) bits |= 1u << b;
+            }
+            cap[L * D.W + w] = bits;
+        }
+    __syncwarp();
+    long long paid = 0;
+    const bool one_round = D.W <= 32;
+    uint32_t cur[kPrefetch], nxt[kPrefetch];
+    int2 tcur[kPrefetch], tnxt[kPrefetch];
+    auto load_batch = [&](int j0, uint32_t (&m)[kPrefetch], int2 (&tk)[kPrefetch]) {
+#pragma unroll
+        for (int u = 0; u < kPrefetch; ++u) {
+            const int j = j0 + u;
+            m[u] = (one_round && j < D.T && lane < D.W) ? __ldg(D.mask + static_cast<size_t>(j) * D.W + lane) : 0u;
+            tk[u] = j < D.T ? __ldg(D.task + j) : make_int2(0, 0);
+        }
+    };
+    load_batch(0, cur, tcur);
+    for (int j0 = 0; j0 < D.T; j0 += kPrefetch) {
+        load_batch(j0 + kPrefetch, nxt, tnxt);
+#pragma unroll
+        for (int u = 0; u < kPrefetch; ++u) {
+            const int j = j0 + u;
+            if (j >= D.T) break;
+            const int level = tcur[u].x, d = tcur[u].y;
+            int winner = -1;
+            if (one_round) {
+                uint32_t m = cur[u];
+                if (m) m &= D.n_levels ? cap[level * D.W + lane] : cap_bits_generic(fr, D.K, lane, d);
+                const uint32_t any = __ballot_sync(0xffffffffu, m != 0);
+                if (any) {
+                    const int src = __ffs(any) - 1;
+                    const uint32_t ms = __shfl_sync(0xffffffffu, m, src);
+                    winner = src * 32 + __ffs(ms) - 1;
+                }
+            } else {
+                for (int base = 0; base < D.W && winner < 0; base += 32) {
+                    const int w = base + lane;
+                    uint32_t m = w < D.W ? __ldg(D.mask + static_cast<size_t>(j) * D.W + w) : 0u;
+                    if (m) m &= D.n_levels ? cap[level * D.W + w] : cap_bits_generic(fr, D.K, w, d);
+                    const uint32_t any = __ballot_sync(0xffffffffu, m != 0);
+                    if (any) {
+                        const int src = __ffs(any) - 1;
+                        const uint32_t ms = __shfl_sync(0xffffffffu, m, src);
+                        winner = (base + src) * 32 + __ffs(ms) - 1;
+                    }
+                }
+            }
+            if (winner >= 0) {
+                if (lane == 0) {
+                    const int f = fr[winner] - d;
+                    fr[winner] = f;
+                    const int w = winner >> 5;
+                    const uint32_t bit = 1u << (winner & 31);
+                    for (int L = 0; L < D.n_levels; ++L) {
+                        uint32_t& word = cap[L * D.W + w];
+                        word = f >= D.levels[L] ? (word | bit) : (word & ~bit);
+                    }
+                    D.target[j] = winner;
+                }
+            } else {
+                paid += d;
+                if (lane == 0) D.target[j] = -1;
+            }
+            __syncwarp();
+        }
+#pragma unroll
+        for (int u = 0; u < kPrefetch; ++u) {
+            cur[u] = nxt[u];
+            tcur[u] = tnxt[u];
+        }
+    }
+    for (int c = lane; c < D.K; c += 32) D.free_vms[c] = fr[c];
+    if (lane == 0) *D.paid = paid;
+}
+
+struct HostGreedy {
+    int K, T, W, n_levels;
+    std::vector<int2> task;
+    std::vector<int32_t> levels;
+    size_t smem;
+};
+
+HostGreedy plan_greedy(const vcs_instance* in) {
+    HostGreedy h{};
+    h.K = in->n_clouds;
+    h.T = in->n_tasks;
+    h.W = std::max(1, (h.K + 31) / 32);
+    std::set<int32_t> distinct(in->task_demand, in->task_demand + h.T);
+    if (static_cast<int>(distinct.size()) <= kMaxLevels) {
+        h.levels.assign(distinct.begin(), distinct.end());
+        h.n_levels = static_cast<int>(h.levels.size());
+    }
+    h.task.resize(static_cast<size_t>(h.T));
+    for (int j = 0; j < h.T; ++j) {
+        int level = 0;
+        if (h.n_levels)
+            level = static_cast<int>(std::lower_bound(h.levels.begin(), h.levels.end(),
+                                                      in->task_demand[j]) -
+                                     h.levels.begin());
+        h.task[static_cast<size_t>(j)] = make_int2(level, in->task_demand[j]);
+    }
+    h.smem = static_cast<size_t>(h.K) * 4 + static_cast<size_t>(h.n_levels) * h.W * 4;
+    if (h.smem > 200 * 1024)
+        raise(VCS_EINVAL, "too many clouds for the device first-fit (shared-memory bound)");
+    return h;
+}
+
+// Device staging of one instance for the greedy kernels.
+struct GreedyDev {
+    DevBuf<double> c_delay, c_thr, t_delay, t_thr;
+    DevBuf<uint32_t> mask;
+    DevBuf<int2> task;
+    DevBuf<int32_t> levels, free_vms, target;
+    DevBuf<long long> paid;
+};
+
+void stage(const vcs_instance* in, const HostGreedy& h, GreedyDev& g, cudaStream_t s) {
+    const size_t K = static_cast<size_t>(h.K), T = static_cast<size_t>(h.T);
+    g.c_delay.exact(K);
+    g.c_thr.exact(K);
+    g.t_delay.exact(T);
+    g.t_thr.exact(T);
+    g.mask.exact(T * static_cast<size_t>(h.W));
+    g.task.exact(T);
+    g.levels.exact(std::max<size_t>(1, h.levels.size()));
+    g.free_vms.exact(K);
+    g.target.exact(T);
+    g.paid.exact(1);
+    if (K) {
+        VCS_CUDA(cudaMemcpyAsync(g.c_delay.p, in->cloud_delay_ms, K * 8, cudaMemcpyHostToDevice, s));
+        VCS_CUDA(cudaMemcpyAsync(g.c_thr.p, in->cloud_thr_kbps, K * 8, cudaMemcpyHostToDevice, s));
+        VCS_CUDA(cudaMemcpyAsync(g.free_vms.p, in->cloud_vm_free, K * 4, cudaMemcpyHostToDevice, s));
+    }
+    if (T) {
+        VCS_CUDA(cudaMemcpyAsync(g.t_delay.p, in->task_max_delay_ms, T * 8, cudaMemcpyHostToDevice, s));
+        VCS_CUDA(cudaMemcpyAsync(g.t_thr.p, in->task_min_thr_kbps, T * 8, cudaMemcpyHostToDevice, s));
+        VCS_CUDA(cudaMemcpyAsync(g.task.p, h.task.data(), T * sizeof(int2), cudaMemcpyHostToDevice, s));
+    }
+    if (!h.levels.empty())
+        VCS_CUDA(cudaMemcpyAsync(g.levels.p, h.levels.data(), h.levels.size() * 4,
+                                 cudaMemcpyHostToDevice, s));
+}
+
+void launch_mask(const HostGreedy& h, GreedyDev& g, int sms, cudaStream_t s) {
+    if (!h.T) return;
+    const uint64_t items = static_cast<uint64_t>(h.T) * static_cast<uint64_t>(h.W);
+    const uint64_t blocks = std::min<uint64_t>((items + 7) / 8, static_cast<uint64_t>(sms) * 16);
+    k_attr_mask<<<static_cast<unsigned>(std::max<uint64_t>(1, blocks)), 256, 0, s>>>(
+        h.K, h.T, h.W, g.c_delay.p, g.c_thr.p, g.t_delay.p, g.t_thr.p, g.mask.p);
+    VCS_LAUNCHED();
+}
+
+GreedyDesc desc_of(const HostGreedy& h, GreedyDev& g) {
+    return GreedyDesc{h.K, h.T, h.W, h.n_levels, g.mask.p, g.task.p, g.levels.p,
+                      g.free_vms.p, g.target.p, g.paid.p};
+}
+
+void launch_first_fit(const GreedyDesc* d_descs, int n, size_t smem, cudaStream_t s) {
+    VCS_CUDA(cudaFuncSetAttribute(k_first_fit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(std::max<size_t>(smem, 1))));
+    k_first_fit<<<n, 32, std::max<size_t>(smem, 4), s>>>(d_descs);
+    VCS_LAUNCHED();
+}
+
+} // namespace
+} // namespace vcs
+
+using vcs::guarded;
+using vcs::raise;
+
+extern "C" {
+
+int vcs_greedy(const vcs_instance* in, int device, int32_t* target_per_task,
+               int64_t* per_cloud_used, int64_t* paid, int64_t* unused) {
+    return guarded([&] {
+        vcs::bind_device(device);
+        const vcs::HostGreedy h = vcs::plan_greedy(in);
+        cudaStream_t s = nullptr;
+        VCS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        struct StreamGuard {
+            cudaStream_t s;
+            ~StreamGuard() { cudaStreamDestroy(s); }
+        } guard{s};
+        vcs::GreedyDev g;
+        vcs::stage(in, h, g, s);
+        vcs::launch_mask(h, g, vcs::sm_count(device), s);
+        vcs::DevBuf<vcs::GreedyDesc> dd;
+        dd.exact(1);
+        const vcs::GreedyDesc desc = vcs::desc_of(h, g);
+        VCS_CUDA(cudaMemcpyAsync(dd.p, &desc, sizeof desc, cudaMemcpyHostToDevice, s));
+        vcs::launch_first_fit(dd.p, 1, h.smem, s);
+        std::vector<int32_t> free_out(static_cast<size_t>(h.K));
+        long long p = 0;
+        if (h.T)
+            VCS_CUDA(cudaMemcpyAsync(target_per_task, g.target.p, static_cast<size_t>(h.T) * 4,
+                                     cudaMemcpyDeviceToHost, s));
+        if (h.K)
+            VCS_CUDA(cudaMemcpyAsync(free_out.data(), g.free_vms.p, static_cast<size_t>(h.K) * 4,
+                                     cudaMemcpyDeviceToHost, s));
+        VCS_CUDA(cudaMemcpyAsync(&p, g.paid.p, sizeof p, cudaMemcpyDeviceToHost, s));
+        VCS_CUDA(cudaStreamSynchronize(s));
+        int64_t placed = 0, capacity = 0;
+        for (int c = 0; c < h.K; ++c) {
+            const int64_t used = static_cast<int64_t>(in->cloud_vm_free[c]) - free_out[c];
+            if (per_cloud_used) per_cloud_used[c] = used;
+            placed += used;
+            capacity += in->cloud_vm_total[c];
+        }
+        *paid = h.T ? p : 0;
+        *unused = capacity - placed; // greedy.cpp:28: total_capacity - vc_placed
+        return VCS_OK;
+    });
+}
+
+int vcs_greedy_batch(int32_t n, const vcs_instance* insts, int device, int32_t** target_per_task,
+                     int64_t* paid, int64_t* unused) {
+    return guarded([&] {
+        if (n <= 0) return VCS_OK;
+        vcs::bind_device(device);
+        cudaStream_t s = nullptr;
+        VCS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        struct StreamGuard {
+            cudaStream_t s;
+            ~StreamGuard() { cudaStreamDestroy(s); }
+        } guard{s};
+        std::vector<vcs::HostGreedy> hs;
+        std::vector<std::unique_ptr<vcs::GreedyDev>> gs;
+        std::vector<vcs::GreedyDesc> descs;
+        size_t smem = 4;
+        const int sms = vcs::sm_count(device);
+        for (int i = 0; i < n; ++i) {
+            hs.push_back(vcs::plan_greedy(&insts[i]));
+            gs.push_back(std::make_unique<vcs::GreedyDev>());
+            vcs::stage(&insts[i], hs.back(), *gs.back(), s);
+            vcs::launch_mask(hs.back(), *gs.back(), sms, s);
+            descs.push_back(vcs::desc_of(hs.back(), *gs.back()));
+            smem = std::max(smem, hs.back().smem);
+        }
+        vcs::DevBuf<vcs::GreedyDesc> dd;
+        dd.exact(static_cast<size_t>(n));
+        VCS_CUDA(cudaMemcpyAsync(dd.p, descs.data(), descs.size() * sizeof(vcs::GreedyDesc),
+                                 cudaMemcpyHostToDevice, s));
+        vcs::launch_first_fit(dd.p, n, smem, s);
+        std::vector<std::vector<int32_t>> frees(static_cast<size_t>(n));
+        std::vector<long long> ps(static_cast<size_t>(n), 0);
+        for (int i = 0; i < n; ++i) {
+            const auto& h = hs[static_cast<size_t>(i)];
+            frees[i].resize(static_cast<size_t>(h.K));
+            if (h.T)
+                VCS_CUDA(cudaMemcpyAsync(target_per_task[i], gs[i]->target.p,
+                                         static_cast<size_t>(h.T) * 4, cudaMemcpyDeviceToHost, s));
+            if (h.K)
+                VCS_CUDA(cudaMemcpyAsync(frees[i].data(), gs[i]->free_vms.p,
+                                         static_cast<size_t>(h.K) * 4, cudaMemcpyDeviceToHost, s));
+            VCS_CUDA(cudaMemcpyAsync(&ps[i], gs[i]->paid.p, sizeof(long long), cudaMemcpyDeviceToHost, s));
+        }
+        VCS_CUDA(cudaStreamSynchronize(s));
+        for (int i = 0; i < n; ++i) {
+            const vcs_instance& in = insts[i];
+            int64_t placed = 0, capacity = 0;
+            for (int c = 0; c < in.n_clouds; ++c) {
+                placed += static_cast<int64_t>(in.cloud_vm_free[c]) - frees[i][c];
+                capacity += in.cloud_vm_total[c];
+            }
+            paid[i] = in.n_tasks ? ps[i] : 0;
+            unused[i] = capacity - placed;
+        }
+        return VCS_OK;
+    });
+}
+
+} // extern "C"

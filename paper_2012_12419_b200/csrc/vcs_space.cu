@@ -1,0 +1,673 @@
+// vcs_space.cu — the GPU state-space builder (replaces StateSpace::build, mdp.cpp:81-214),
+// the device key index behind locate (mdp.cpp:227-234), and the space handle.
+//
+// Layered frontier expansion, one layer (decision epoch) at a time:
+//   1. k_count     out-degree of every frontier state (feasible active clouds + paid)
+//   2. scan        exclusive sum -> CSR row offsets (edge order of the reference: clouds
+//                  ascending, paid last, mdp.cpp:169-204)
+//   3. k_emit      per edge: packed successor key, fp64 reward (separate mul/sub, no FMA,
+//                  = mdp.cpp:191/202 bits), action
+//   4. k_insert    hash every successor key; each slot keeps the MINIMUM edge index carrying
+//                  that key (atomicMin) = its first occurrence in the reference's BFS
+//   5. k_mark/scan a successor's layer-local index is the rank of its first edge among all
+//                  first edges -> exactly the reference's first-insertion order (mdp.cpp:157-165)
+//   6. k_finalize  successor indices + next-frontier keys
+// Keys are the reference's reduced keys (free counts of still-eligible clouds, mdp.hpp:70-79)
+// packed into 64-bit words, ceil(log2(vm_free+1)) bits per cloud.
+#include "vcs_device.cuh"
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+
+namespace vcs {
+
+namespace {
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ull;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebull;
+    x ^= x >> 31;
+    return x;
+}
+
+template <int WM>
+__device__ __forceinline__ uint64_t hash_key(const uint64_t (&k)[WM], int words, uint64_t salt) {
+    uint64_t h = mix64(salt * 0x9e3779b97f4a7c15ull + 0x632be59bd9b4e019ull);
+#pragma unroll
+    for (int i = 0; i < WM; ++i)
+        if (i < words) h = mix64(h ^ k[i]);
+    return h;
+}
+
+template <int WM>
+__device__ __forceinline__ void load_key(const uint64_t* __restrict__ p, int words,
+                                         uint64_t (&k)[WM]) {
+#pragma unroll
+    for (int i = 0; i < WM; ++i) k[i] = i < words ? p[i] : 0ull;
+}
+
+template <int WM>
+__device__ __forceinline__ bool key_equal(const uint64_t* __restrict__ p, int words,
+                                          const uint64_t (&k)[WM]) {
+    bool eq = true;
+#pragma unroll
+    for (int i = 0; i < WM; ++i)
+        if (i < words) eq &= (p[i] == k[i]);
+    return eq;
+}
+
+template <int WM>
+__device__ __forceinline__ int get_field(const uint64_t (&k)[WM], int off, int width) {
+    const int w = off >> 6;
+    uint64_t word = k[0];
+#pragma unroll
+    for (int i = 1; i < WM; ++i)
+        if (i == w) word = k[i];
+    return static_cast<int>((word >> (off & 63)) & ((1ull << width) - 1ull));
+}
+
+template <int WM>
+__device__ __forceinline__ void put_field(uint64_t (&k)[WM], int off, uint64_t v) {
+    const int w = off >> 6;
+#pragma unroll
+    for (int i = 0; i < WM; ++i)
+        if (i == w) k[i] |= v << (off & 63);
+}
+
+template <int WM>
+__global__ void k_count(uint32_t n, const uint64_t* __restrict__ keys, const LayerParam L,
+                        uint32_t* __restrict__ deg) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    if (i == n) {
+        deg[n] = 0;
+        return;
+    }
+    uint64_t k[WM];
+    load_key<WM>(keys + static_cast<uint64_t>(i) * L.words, L.words, k);
+    uint32_t d = 1; // the paid edge always exists
+    for (int p = 0; p < L.n_active; ++p)
+        if (L.attr[p] && get_field<WM>(k, L.bit_off[p], L.width[p]) >= L.demand) ++d;
+    deg[i] = d;
+}
+
+// One edge: successor key in the layer-(t+1) packing, reward, action.  `p` = key position of
+// the chosen cloud, or -1 for the paid cloud.
+template <int WM>
+__device__ __forceinline__ void emit_edge(const uint64_t (&k)[WM], int p, const LayerParam& L,
+                                          uint64_t* __restrict__ ekey, double* __restrict__ rw,
+                                          int32_t* __restrict__ act) {
+    uint64_t nk[WM];
+#pragma unroll
+    for (int i = 0; i < WM; ++i) nk[i] = 0ull;
+    double retired = 0.0; // mdp.cpp:179-185 / :196-197, summed in key-position order
+    for (int q = 0; q < L.n_active; ++q) {
+        int v = get_field<WM>(k, L.bit_off[q], L.width[q]);
+        if (q == p) v -= L.demand;
+        if (L.keep_idx[q] >= 0)
+            put_field<WM>(nk, L.next_bit_off[q], static_cast<uint64_t>(v));
+        else
+            retired = __dadd_rn(retired, static_cast<double>(v));
+    }
+#pragma unroll
+    for (int i = 0; i < WM; ++i)
+        if (i < L.next_words) ekey[i] = nk[i];
+    // beta*n - gamma*retired as two rounded operations (the reference's -O3 x86-64 code has no
+    // FMA; nvcc would contract a*b-c*d, so the intrinsics pin the rounding).
+    const double base = p < 0 ? L.r_paid : L.r_cloud;
+    *rw = __dsub_rn(base, __dmul_rn(L.gamma, retired));
+    *act = p < 0 ? -1 : L.cloud[p];
+}
+
+template <int WM>
+__global__ void k_emit(uint32_t n, const uint64_t* __restrict__ keys,
+                       const uint32_t* __restrict__ off, const LayerParam L, uint32_t edge_base,
+                       uint32_t* __restrict__ row_ptr_layer, uint64_t* __restrict__ ekeys,
+                       double* __restrict__ reward, int32_t* __restrict__ action) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint64_t k[WM];
+    load_key<WM>(keys + static_cast<uint64_t>(i) * L.words, L.words, k);
+    uint32_t j = off[i];
+    row_ptr_layer[i] = edge_base + j;
+    for (int p = 0; p < L.n_active; ++p) {
+        if (!L.attr[p] || get_field<WM>(k, L.bit_off[p], L.width[p]) < L.demand) continue;
+        emit_edge<WM>(k, p, L, ekeys + static_cast<uint64_t>(j) * L.next_words,
+                      reward + edge_base + j, action + edge_base + j);
+        ++j;
+    }
+    emit_edge<WM>(k, -1, L, ekeys + static_cast<uint64_t>(j) * L.next_words,
+                  reward + edge_base + j, action + edge_base + j);
+}
+
+template <int WM>
+__global__ void k_insert(uint32_t n_edges, const uint64_t* __restrict__ ekeys, int words,
+                         uint32_t* __restrict__ table, uint32_t mask,
+                         uint32_t* __restrict__ slot_of) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_edges) return;
+    uint64_t k[WM];
+    load_key<WM>(ekeys + static_cast<uint64_t>(j) * words, words, k);
+    uint32_t h = static_cast<uint32_t>(hash_key<WM>(k, words, 0)) & mask;
+    for (;;) {
+        uint32_t cur = table[h];
+        if (cur == kEmpty32) {
+            const uint32_t prev = atomicCAS(&table[h], kEmpty32, j);
+            if (prev == kEmpty32) {
+                slot_of[j] = h;
+                return;
+            }
+            cur = prev;
+        }
+        if (key_equal<WM>(ekeys + static_cast<uint64_t>(cur) * words, words, k)) {
+            atomicMin(&table[h], j); // keep the first occurrence (lowest edge index)
+            slot_of[j] = h;
+            return;
+        }
+        h = (h + 1) & mask;
+    }
+}
+
+__global__ void k_mark(uint32_t n_edges, const uint32_t* __restrict__ table,
+                       const uint32_t* __restrict__ slot_of, uint32_t* __restrict__ flag) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j > n_edges) return;
+    flag[j] = j < n_edges ? (table[slot_of[j]] == j ? 1u : 0u) : 0u;
+}
+
+__global__ void k_finalize(uint32_t n_edges, const uint32_t* __restrict__ table,
+                           const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ rank,
+                           const uint64_t* __restrict__ ekeys, int words, uint32_t next_base,
+                           uint32_t* __restrict__ succ, uint64_t* __restrict__ next_keys) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_edges) return;
+    const uint32_t first = table[slot_of[j]];
+    succ[j] = next_base + rank[first];
+    if (first == j) {
+        const uint64_t* src = ekeys + static_cast<uint64_t>(j) * words;
+        uint64_t* dst = next_keys + static_cast<uint64_t>(rank[j]) * words;
+        for (int w = 0; w < words; ++w) dst[w] = src[w];
+    }
+}
+
+__global__ void k_fill_u32(uint32_t* __restrict__ p, uint64_t n, uint32_t v) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+// ---- locate index: one open-addressing table over (layer, key) -> flat state index ----------
+template <int WM>
+__global__ void k_loc_insert(uint32_t n, const uint64_t* __restrict__ keys, int words, int layer,
+                             uint32_t base, uint32_t* __restrict__ table, uint32_t mask) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint64_t k[WM];
+    load_key<WM>(keys + static_cast<uint64_t>(i) * words, words, k);
+    uint32_t h = static_cast<uint32_t>(hash_key<WM>(k, words, static_cast<uint64_t>(layer) + 1)) &
+                 mask;
+    while (atomicCAS(&table[h], kEmpty32, base + i) != kEmpty32) h = (h + 1) & mask;
+}
+
+struct LocQuery {
+    int32_t layer;
+    int32_t words;
+    int32_t valid;
+    int32_t pad;
+    uint64_t key[kMaxKeyWords];
+};
+
+template <int WM>
+__global__ void k_loc_lookup(int64_t n, const LocQuery* __restrict__ q,
+                             const uint64_t* __restrict__ keys,
+                             const uint64_t* __restrict__ layer_off,
+                             const uint64_t* __restrict__ key_off,
+                             const uint32_t* __restrict__ table, uint32_t mask,
+                             int64_t* __restrict__ out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const LocQuery& Q = q[i];
+    if (!Q.valid) {
+        out[i] = -1;
+        return;
+    }
+    uint64_t k[WM];
+#pragma unroll
+    for (int w = 0; w < WM; ++w) k[w] = Q.key[w];
+    const int t = Q.layer;
+    uint32_t h = static_cast<uint32_t>(hash_key<WM>(k, Q.words, static_cast<uint64_t>(t) + 1)) &
+                 mask;
+    const uint64_t lo = layer_off[t], hi = layer_off[t + 1];
+    for (;;) {
+        const uint32_t cur = table[h];
+        if (cur == kEmpty32) {
+            out[i] = -1;
+            return;
+        }
+        if (cur >= lo && cur < hi &&
+            key_equal<WM>(keys + key_off[t] + (cur - lo) * static_cast<uint64_t>(Q.words),
+                          Q.words, k)) {
+            out[i] = cur;
+            return;
+        }
+        h = (h + 1) & mask;
+    }
+}
+
+uint32_t blocks_for(uint64_t n, uint32_t threads) {
+    return static_cast<uint32_t>((n + threads - 1) / threads);
+}
+
+uint64_t pow2_at_least(uint64_t n) {
+    uint64_t c = 1024;
+    while (c < n) c <<= 1;
+    return c;
+}
+
+struct Scratch {
+    DevBuf<uint32_t> deg, off, slot, flag, rank, table;
+    DevBuf<uint64_t> ekeys;
+    DevBuf<uint8_t> cub_tmp;
+    uint32_t* host_word = nullptr;
+    ~Scratch() {
+        if (host_word) cudaFreeHost(host_word);
+    }
+};
+
+void exclusive_scan(Scratch& sc, const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t s) {
+    size_t bytes = 0;
+    VCS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, static_cast<int64_t>(n), s));
+    sc.cub_tmp.exact(bytes);
+    VCS_CUDA(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.p, bytes, in, out, static_cast<int64_t>(n), s));
+    note_launch();
+}
+
+uint32_t read_word(Scratch& sc, const uint32_t* dev, cudaStream_t s) {
+    VCS_CUDA(cudaMemcpyAsync(sc.host_word, dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    VCS_CUDA(cudaStreamSynchronize(s));
+    return *sc.host_word;
+}
+
+template <int WM>
+void build_layers(vcs_space* sp, uint64_t state_cap) {
+    const LayerPlan& pl = sp->plan;
+    const int H = pl.horizon;
+    cudaStream_t s = sp->stream;
+    Scratch sc;
+    VCS_CUDA(cudaMallocHost(&sc.host_word, sizeof(uint32_t)));
+
+    sp->layer_off.assign(static_cast<size_t>(H) + 2, 0);
+    sp->layer_edges.assign(static_cast<size_t>(H) + 1, 0);
+    sp->key_off.assign(static_cast<size_t>(H) + 2, 0);
+    sp->keys.reserve(1u << 16, 0, s);
+    VCS_CUDA(cudaMemcpyAsync(sp->keys.p, pl.init_key.data(), pl.words[0] * sizeof(uint64_t),
+                             cudaMemcpyHostToDevice, s));
+    sp->row_ptr.reserve(1u << 16, 0, s);
+    sp->succ.reserve(1u << 16, 0, s);
+    sp->reward.reserve(1u << 16, 0, s);
+    sp->action.reserve(1u << 16, 0, s);
+
+    uint64_t S = 1, E = 0, n_t = 1;
+    sp->max_layer = 1;
+    constexpr uint32_t T = 256;
+    for (int t = 0; t < H; ++t) {
+        const LayerParam& L = pl.layers[static_cast<size_t>(t)];
+        sp->layer_off[static_cast<size_t>(t) + 1] = S;
+        const uint64_t key_t = sp->key_off[static_cast<size_t>(t)];
+        sp->key_off[static_cast<size_t>(t) + 1] = key_t + n_t * static_cast<uint64_t>(L.words);
+
+        sc.deg.exact(n_t + 1);
+        sc.off.exact(n_t + 1);
+        k_count<WM><<<blocks_for(n_t + 1, T), T, 0, s>>>(static_cast<uint32_t>(n_t),
+                                                         sp->keys.p + key_t, L, sc.deg.p);
+        VCS_LAUNCHED();
+        exclusive_scan(sc, sc.deg.p, sc.off.p, n_t + 1, s);
+        const uint64_t E_t = read_word(sc, sc.off.p + n_t, s);
+        if (E + E_t >= 0xffffffffull)
+            raise(VCS_EINVAL, "more than 2^32-1 transitions are not supported");
+
+        const uint64_t row0 = sp->layer_off[static_cast<size_t>(t)];
+        sp->row_ptr.reserve(row0 + n_t + 1, row0, s);
+        sp->succ.reserve(E + E_t, E, s);
+        sp->reward.reserve(E + E_t, E, s);
+        sp->action.reserve(E + E_t, E, s);
+        sc.ekeys.exact(E_t * static_cast<uint64_t>(L.next_words));
+        k_emit<WM><<<blocks_for(n_t, T), T, 0, s>>>(
+            static_cast<uint32_t>(n_t), sp->keys.p + key_t, sc.off.p, L, static_cast<uint32_t>(E),
+            sp->row_ptr.p + row0, sc.ekeys.p, sp->reward.p, sp->action.p);
+        VCS_LAUNCHED();
+
+        const uint64_t cap = pow2_at_least(2 * E_t);
+        sc.table.exact(cap);
+        sc.slot.exact(E_t);
+        sc.flag.exact(E_t + 1);
+        sc.rank.exact(E_t + 1);
+        VCS_CUDA(cudaMemsetAsync(sc.table.p, 0xff, cap * sizeof(uint32_t), s));
+        k_insert<WM><<<blocks_for(E_t, T), T, 0, s>>>(static_cast<uint32_t>(E_t), sc.ekeys.p,
+                                                      L.next_words, sc.table.p,
+                                                      static_cast<uint32_t>(cap - 1), sc.slot.p);
+        VCS_LAUNCHED();
+        k_mark<<<blocks_for(E_t + 1, T), T, 0, s>>>(static_cast<uint32_t>(E_t), sc.table.p,
+                                                    sc.slot.p, sc.flag.p);
+        VCS_LAUNCHED();
+        exclusive_scan(sc, sc.flag.p, sc.rank.p, E_t + 1, s);
+        const uint64_t n_next = read_word(sc, sc.rank.p + E_t, s);
+        if (S + n_next > state_cap)
+            raise(VCS_ECAP, "reachable state space exceeds cap of " + std::to_string(state_cap) +
+                                " states");
+        if (S + n_next >= 0xffffffffull)
+            raise(VCS_EINVAL, "more than 2^32-1 states are not supported");
+        const uint64_t key_next = sp->key_off[static_cast<size_t>(t) + 1];
+        sp->keys.reserve(key_next + n_next * static_cast<uint64_t>(L.next_words), key_next, s);
+        k_finalize<<<blocks_for(E_t, T), T, 0, s>>>(
+            static_cast<uint32_t>(E_t), sc.table.p, sc.slot.p, sc.rank.p, sc.ekeys.p,
+            L.next_words, static_cast<uint32_t>(S), sp->succ.p + E, sp->keys.p + key_next);
+        VCS_LAUNCHED();
+
+        sp->layer_edges[static_cast<size_t>(t)] = E_t;
+        E += E_t;
+        S += n_next;
+        n_t = n_next;
+        sp->max_layer = std::max<uint64_t>(sp->max_layer, n_t);
+    }
+    sp->layer_off[static_cast<size_t>(H) + 1] = S;
+    sp->key_off[static_cast<size_t>(H) + 1] =
+        sp->key_off[static_cast<size_t>(H)] + n_t * static_cast<uint64_t>(pl.words[H]);
+    // Terminal layer: no outgoing edges (mdp.cpp:207-209).
+    const uint64_t rowH = sp->layer_off[static_cast<size_t>(H)];
+    sp->row_ptr.reserve(S + 1, rowH, s);
+    k_fill_u32<<<blocks_for(S + 1 - rowH, T), T, 0, s>>>(sp->row_ptr.p + rowH, S + 1 - rowH,
+                                                         static_cast<uint32_t>(E));
+    VCS_LAUNCHED();
+    VCS_CUDA(cudaStreamSynchronize(s));
+    sp->S = S;
+    sp->E = E;
+}
+
+int words_template(int w) {
+    if (w <= 1) return 1;
+    if (w <= 2) return 2;
+    if (w <= 4) return 4;
+    return 8;
+}
+
+template <class F>
+void dispatch_words(int wm, F&& f) {
+    switch (words_template(wm)) {
+    case 1: f(std::integral_constant<int, 1>{}); break;
+    case 2: f(std::integral_constant<int, 2>{}); break;
+    case 4: f(std::integral_constant<int, 4>{}); break;
+    default: f(std::integral_constant<int, 8>{}); break;
+    }
+}
+
+int max_words(const vcs_space* sp) {
+    int wm = 1;
+    for (int w : sp->plan.words) wm = std::max(wm, w);
+    return wm;
+}
+
+void ensure_locate_index(vcs_space* sp) {
+    if (sp->loc_cap) return;
+    const uint64_t cap = pow2_at_least(2 * sp->S);
+    if (cap > 0xffffffffull) raise(VCS_EINVAL, "state space too large for the locate index");
+    sp->loc_table.exact(cap);
+    cudaStream_t s = sp->stream;
+    VCS_CUDA(cudaMemsetAsync(sp->loc_table.p, 0xff, cap * sizeof(uint32_t), s));
+    dispatch_words(max_words(sp), [&](auto wm) {
+        constexpr int WM = decltype(wm)::value;
+        for (int t = 0; t <= sp->H; ++t) {
+            const uint64_t n = sp->layer_off[t + 1] - sp->layer_off[t];
+            if (!n) continue;
+            k_loc_insert<WM><<<blocks_for(n, 256), 256, 0, s>>>(
+                static_cast<uint32_t>(n), sp->keys.p + sp->key_off[t], sp->plan.words[t], t,
+                static_cast<uint32_t>(sp->layer_off[t]), sp->loc_table.p,
+                static_cast<uint32_t>(cap - 1));
+            VCS_LAUNCHED();
+        }
+    });
+    VCS_CUDA(cudaStreamSynchronize(s));
+    sp->loc_cap = cap;
+}
+
+} // namespace
+
+void bind_device(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        raise(VCS_ECUDA, "no CUDA device available (the solver has no CPU fallback)");
+    if (device < 0 || device >= n) raise(VCS_EINVAL, "device ordinal out of range");
+    VCS_CUDA(cudaSetDevice(device));
+}
+
+int sm_count(int device) {
+    int v = 0;
+    VCS_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
+    return v;
+}
+
+} // namespace vcs
+
+vcs_space::~vcs_space() {
+    cudaSetDevice(device);
+    for (auto& [k, g] : graphs) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        for (auto& e : g.ev)
+            if (e) cudaEventDestroy(e);
+    }
+    if (stream) cudaStreamDestroy(stream);
+}
+
+using vcs::guarded;
+using vcs::raise;
+
+namespace {
+std::unique_ptr<vcs_space> new_space(int device) {
+    vcs::bind_device(device);
+    auto sp = std::make_unique<vcs_space>();
+    sp->device = device;
+    sp->num_sms = vcs::sm_count(device);
+    VCS_CUDA(cudaStreamCreateWithFlags(&sp->stream, cudaStreamNonBlocking));
+    return sp;
+}
+} // namespace
+
+extern "C" {
+
+int vcs_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int vcs_space_build(const vcs_instance* inst, uint64_t state_cap, int device, vcs_space** out) {
+    return guarded([&] {
+        if (!inst || !out) raise(VCS_EINVAL, "null argument");
+        for (int j = 0; j < inst->n_tasks; ++j)
+            if (inst->task_demand[j] < 0)
+                raise(VCS_EINVAL, "negative vm_demand is not supported by the device builder");
+        vcs::LayerPlan plan = vcs::make_layer_plan(inst); // throws the 65535 error first
+        auto sp = new_space(device);
+        sp->plan = std::move(plan);
+        sp->has_plan = true;
+        sp->H = sp->plan.horizon;
+        int maxdeg = 1;
+        for (const auto& L : sp->plan.layers) {
+            int d = 1;
+            for (int p = 0; p < L.n_active; ++p) d += L.attr[p] ? 1 : 0;
+            maxdeg = std::max(maxdeg, d);
+        }
+        sp->max_degree = maxdeg;
+        const auto t0 = std::chrono::steady_clock::now();
+        vcs::dispatch_words(vcs::max_words(sp.get()), [&](auto wm) {
+            vcs::build_layers<decltype(wm)::value>(sp.get(), state_cap);
+        });
+        const auto t1 = std::chrono::steady_clock::now();
+        sp->build_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        *out = sp.release();
+        return VCS_OK;
+    });
+}
+
+int vcs_space_from_csr(uint64_t n_states, uint64_t n_edges, int32_t horizon,
+                       const uint64_t* layer_offset, const uint64_t* row_ptr, const uint32_t* succ,
+                       const double* reward, const int32_t* action, int device, vcs_space** out) {
+    return guarded([&] {
+        if (n_edges >= 0xffffffffull || n_states >= 0xffffffffull)
+            raise(VCS_EINVAL, "more than 2^32-1 states or transitions are not supported");
+        if (n_states < 1 || horizon < 0) raise(VCS_EINVAL, "empty state space");
+        auto sp = new_space(device);
+        sp->S = n_states;
+        sp->E = n_edges;
+        sp->H = horizon;
+        sp->layer_off.assign(layer_offset, layer_offset + horizon + 2);
+        sp->layer_edges.assign(static_cast<size_t>(horizon) + 1, 0);
+        std::vector<uint32_t> rp32(n_states + 1);
+        int maxdeg = 1;
+        for (uint64_t i = 0; i <= n_states; ++i) {
+            rp32[i] = static_cast<uint32_t>(row_ptr[i]);
+            if (i < n_states)
+                maxdeg = std::max<int>(maxdeg, static_cast<int>(row_ptr[i + 1] - row_ptr[i]));
+        }
+        for (int t = 0; t <= horizon; ++t) {
+            sp->layer_edges[t] = row_ptr[sp->layer_off[t + 1]] - row_ptr[sp->layer_off[t]];
+            sp->max_layer = std::max(sp->max_layer, sp->layer_off[t + 1] - sp->layer_off[t]);
+        }
+        sp->max_degree = maxdeg;
+        cudaStream_t s = sp->stream;
+        sp->row_ptr.exact(n_states + 1);
+        sp->succ.exact(n_edges);
+        sp->reward.exact(n_edges);
+        sp->action.exact(n_edges);
+        VCS_CUDA(cudaMemcpyAsync(sp->row_ptr.p, rp32.data(), rp32.size() * 4, cudaMemcpyHostToDevice, s));
+        if (n_edges) {
+            VCS_CUDA(cudaMemcpyAsync(sp->succ.p, succ, n_edges * 4, cudaMemcpyHostToDevice, s));
+            VCS_CUDA(cudaMemcpyAsync(sp->reward.p, reward, n_edges * 8, cudaMemcpyHostToDevice, s));
+            VCS_CUDA(cudaMemcpyAsync(sp->action.p, action, n_edges * 4, cudaMemcpyHostToDevice, s));
+        }
+        VCS_CUDA(cudaStreamSynchronize(s));
+        *out = sp.release();
+        return VCS_OK;
+    });
+}
+
+int vcs_space_info_get(const vcs_space* sp, vcs_space_info* info) {
+    return guarded([&] {
+        info->n_states = sp->S;
+        info->n_edges = sp->E;
+        info->horizon = sp->H;
+        int wm = 0;
+        for (int w : sp->plan.words) wm = std::max(wm, w);
+        info->key_words = wm;
+        info->max_layer = sp->max_layer;
+        info->max_degree = sp->max_degree;
+        info->device = sp->device;
+        info->build_ms = sp->build_ms;
+        info->device_bytes = (sp->S + 1) * 4 + sp->E * (4 + 8 + 4) + sp->S * 16;
+        return VCS_OK;
+    });
+}
+
+int vcs_space_layer_offsets(const vcs_space* sp, uint64_t* layer_offset) {
+    return guarded([&] {
+        std::copy(sp->layer_off.begin(), sp->layer_off.end(), layer_offset);
+        return VCS_OK;
+    });
+}
+
+int vcs_space_layer_edges(const vcs_space* sp, uint64_t* layer_edges) {
+    return guarded([&] {
+        std::copy(sp->layer_edges.begin(), sp->layer_edges.end(), layer_edges);
+        return VCS_OK;
+    });
+}
+
+int vcs_space_csr(const vcs_space* sp, uint64_t* row_ptr, uint32_t* succ, double* reward,
+                  int32_t* action) {
+    return guarded([&] {
+        vcs::bind_device(sp->device);
+        cudaStream_t s = sp->stream;
+        if (row_ptr) {
+            std::vector<uint32_t> rp(sp->S + 1);
+            VCS_CUDA(cudaMemcpyAsync(rp.data(), sp->row_ptr.p, rp.size() * 4, cudaMemcpyDeviceToHost, s));
+            VCS_CUDA(cudaStreamSynchronize(s));
+            for (size_t i = 0; i < rp.size(); ++i) row_ptr[i] = rp[i];
+        }
+        if (sp->E) {
+            if (succ) VCS_CUDA(cudaMemcpyAsync(succ, sp->succ.p, sp->E * 4, cudaMemcpyDeviceToHost, s));
+            if (reward) VCS_CUDA(cudaMemcpyAsync(reward, sp->reward.p, sp->E * 8, cudaMemcpyDeviceToHost, s));
+            if (action) VCS_CUDA(cudaMemcpyAsync(action, sp->action.p, sp->E * 4, cudaMemcpyDeviceToHost, s));
+        }
+        VCS_CUDA(cudaStreamSynchronize(s));
+        return VCS_OK;
+    });
+}
+
+int vcs_space_locate(vcs_space* sp, int64_t n, const int32_t* free_vms, const int32_t* task_index,
+                     const uint8_t* terminal, int64_t* idx_out) {
+    return guarded([&] {
+        if (!sp->has_plan) raise(VCS_EINVAL, "space was not built from an instance");
+        if (n <= 0) return VCS_OK;
+        vcs::bind_device(sp->device);
+        const int K = sp->plan.n_clouds;
+        std::vector<vcs::LocQuery> q(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) {
+            const int t = terminal[i] ? sp->H : task_index[i];
+            if (t < 0 || t > sp->H) raise(VCS_EINVAL, "task index outside horizon");
+            auto& Q = q[static_cast<size_t>(i)];
+            std::memset(&Q, 0, sizeof Q);
+            Q.layer = t;
+            Q.words = sp->plan.words[t];
+            Q.valid = vcs::pack_key(sp->plan, t, free_vms + i * K, Q.key) ? 1 : 0;
+        }
+        vcs::ensure_locate_index(sp);
+        cudaStream_t s = sp->stream;
+        vcs::DevBuf<vcs::LocQuery> dq;
+        vcs::DevBuf<int64_t> dout;
+        vcs::DevBuf<uint64_t> dmeta;
+        dq.exact(static_cast<size_t>(n));
+        dout.exact(static_cast<size_t>(n));
+        dmeta.exact(2 * (static_cast<size_t>(sp->H) + 2));
+        VCS_CUDA(cudaMemcpyAsync(dq.p, q.data(), q.size() * sizeof(vcs::LocQuery), cudaMemcpyHostToDevice, s));
+        VCS_CUDA(cudaMemcpyAsync(dmeta.p, sp->layer_off.data(), (sp->H + 2) * 8, cudaMemcpyHostToDevice, s));
+        VCS_CUDA(cudaMemcpyAsync(dmeta.p + sp->H + 2, sp->key_off.data(), (sp->H + 2) * 8, cudaMemcpyHostToDevice, s));
+        vcs::dispatch_words(vcs::max_words(sp), [&](auto wm) {
+            constexpr int WM = decltype(wm)::value;
+            vcs::k_loc_lookup<WM><<<vcs::blocks_for(static_cast<uint64_t>(n), 128), 128, 0, s>>>(
+                n, dq.p, sp->keys.p, dmeta.p, dmeta.p + sp->H + 2, sp->loc_table.p,
+                static_cast<uint32_t>(sp->loc_cap - 1), dout.p);
+            VCS_LAUNCHED();
+        });
+        VCS_CUDA(cudaMemcpyAsync(idx_out, dout.p, n * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        VCS_CUDA(cudaStreamSynchronize(s));
+        return VCS_OK;
+    });
+}
+
+int vcs_space_hidden_penalty(const vcs_space* sp, int64_t n, const int32_t* free_vms,
+                             const int32_t* task_index, const uint8_t* terminal, double* out) {
+    return guarded([&] {
+        if (!sp->has_plan) raise(VCS_EINVAL, "space was not built from an instance");
+        const int K = sp->plan.n_clouds;
+        for (int64_t i = 0; i < n; ++i) {
+            if (sp->H == 0) { // mdp.cpp:237: nothing was ever schedulable
+                out[i] = 0.0;
+                continue;
+            }
+            const int t = terminal[i] ? sp->H : task_index[i];
+            double retired = 0.0;
+            for (int c = 0; c < K; ++c)
+                if (sp->plan.last_use[c] < t) retired += free_vms[i * K + c];
+            out[i] = sp->plan.layers.empty() ? 0.0 : sp->plan.layers[0].gamma * retired;
+        }
+        return VCS_OK;
+    });
+}
+
+void vcs_space_free(vcs_space* sp) { delete sp; }
+
+} // extern "C"
