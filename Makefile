@@ -36,8 +36,10 @@ $(OBJ)/vcs_host.o: $(SRC)/vcs_host.cpp $(HDRS)
 $(LIB): $(CU_OBJS) $(HOST_OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $^ -Xlinker -soname=libvcs_gpu.so
 
-$(SHIM): $(SRC)/vcsched_b200.cpp $(SRC)/vcsched_b200.hpp include/vcs_gpu.h $(LIB)
-	$(CXX) -O2 -std=c++20 -fPIC -shared -I$(SRC) -o $@ $(SRC)/vcsched_b200.cpp \
+SHIM_HDRS := $(wildcard $(PKG)/include/vcsched/*.hpp)
+
+$(SHIM): $(SRC)/vcsched_b200.cpp $(SHIM_HDRS) include/vcs_gpu.h $(LIB)
+	$(CXX) -O2 -std=c++20 -fPIC -shared -Wall -I$(PKG)/include -o $@ $(SRC)/vcsched_b200.cpp \
 	    -L$(PKG) -lvcs_gpu -Wl,-rpath,'$$ORIGIN'
 
 $(ORACLE): oracle/vcs_oracle.c include/vcs_gpu.h
@@ -46,13 +48,31 @@ $(ORACLE): oracle/vcs_oracle.c include/vcs_gpu.h
 # The unmodified reference, compiled from its own sources where they lie (never copied), with
 # the reference's Release flags (-O3 -DNDEBUG, no -march), plus the C shim of oracle/ref_capi.cpp.
 ref:
-	@if [ -d $(REF)/core/src ]; then $(MAKE) --no-print-directory $(REFLIB); \
+	@if [ -d $(REF)/core/src ]; then $(MAKE) --no-print-directory $(REFLIB) $(REF_SUITES); \
 	 else echo "reference sources absent: using the prebuilt $(REFLIB) if present"; fi
 
 $(REFLIB): oracle/ref_capi.cpp include/vcs_gpu.h
 	@mkdir -p oracle/_ref
-	$(CXX) -std=c++20 -O3 -DNDEBUG -fPIC -shared -pthread -I$(REF)/core/include -I$(JSON_INC) \
+	$(CXX) -std=c++20 -O3 -DNDEBUG -fPIC -shared -pthread -I$(REF)/core/include -I$(REF)/tests -I$(JSON_INC) \
 	    -o $@ $(REF)/core/src/*.cpp oracle/ref_capi.cpp
+
+# The reference's OWN solver test suites (doctest files compiled where they lie, unchanged),
+# linked (a) against the reference library as the control and (b) against the B200 drop-in shim.
+REF_TESTS  := $(REF)/tests/test_workload.cpp $(REF)/tests/test_greedy.cpp \
+              $(REF)/tests/test_mdp.cpp $(REF)/tests/test_parallel.cpp
+REF_SUITES := oracle/_ref/ref_suite_on_reference oracle/_ref/ref_suite_on_b200
+
+oracle/_ref/ref_suite_on_reference: tests/cpp/doctest.h tests/cpp/doctest_main.cpp
+	@mkdir -p oracle/_ref
+	$(CXX) -std=c++20 -O2 -pthread -Itests/cpp -I$(REF)/core/include -I$(REF)/tests -I$(JSON_INC) \
+	    -DVCSCHED_DATA_DIR='"tests/golden"' -o $@ $(REF_TESTS) tests/cpp/doctest_main.cpp \
+	    $(REF)/core/src/*.cpp
+
+oracle/_ref/ref_suite_on_b200: tests/cpp/doctest.h tests/cpp/doctest_main.cpp $(SHIM) $(SHIM_HDRS)
+	@mkdir -p oracle/_ref
+	$(CXX) -std=c++20 -O2 -pthread -Itests/cpp -I$(PKG)/include -I$(REF)/tests \
+	    -DVCSCHED_DATA_DIR='"tests/golden"' -o $@ $(REF_TESTS) tests/cpp/doctest_main.cpp \
+	    -L$(PKG) -lvcsched_b200 -lvcs_gpu -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
 
 clean:
 	rm -rf build $(LIB) $(SHIM) $(ORACLE) oracle/_ref

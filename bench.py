@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 solver path: fp64 value iteration on the ~10^7-state VC MDP.
+
+Metric (BASELINE.json): Bellman state-action backups/sec and time-to-convergence.
+  step   = one complete solve (all Jacobi sweeps until `delta < eps` + policy extraction,
+           the reference's time-to-convergence convention, parallel_vi.cpp:126-147) on the
+           device-resident prebuilt space of SURVEY §8(d) C4 (19,333,781 states).
+  value  = reference-equivalent backups/s = n_states * sweeps * steps / device time (whole job).
+  e2e    = the same metric through the C ABI with HOST buffers: per step vcs_space_build from
+           the host instance (H2D) + vcs_solve into pinned host values/actions (D2H).
+  --impl reference : the unmodified reference CPU solver (oracle/_ref/libvcsref.so,
+           detail::run_value_iteration with all host threads) on the same config.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (row-block sharded, NCCL halo exchange)
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # name: (generator args, description)
+    "c4": ((1, 2012, 0, 6, 8, 48, 3),
+           "C4: 6 clouds x 8 VMs, 48 tasks demand U[1,3] (mt19937_64 seed 2012), 6 bags"),
+    "c3": ((1, 2012, 0, 5, 8, 40, 3),
+           "C3: 5 clouds x 8 VMs, 40 tasks demand U[1,3] (mt19937_64 seed 2012), 5 bags"),
+}
+METRIC = "Bellman state-action backups/sec (fp64 value iteration to eps=1e-6, time-to-convergence)"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled in the background."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self.proc = None
+        self.thread = None
+        self.window = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        rows = self.samples
+        if self.window:
+            inside = [s for s in rows if self.window[0] - 0.05 <= s[0] <= self.window[1] + 0.05]
+            if inside:
+                rows = inside
+        sm = [float(r[1][0]) for r in rows if r[1][0].replace(".", "").isdigit()]
+        mx = [float(r[1][1]) for r in rows if r[1][1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for _, r in rows:
+            for name, v in zip(names, r[4:8]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(rows), "in_timed_window": self.window is not None}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the profiled sweep launch (profiles/ncu_sweep.json), or None."""
+    p = ROOT / "profiles" / "ncu_sweep.json"
+    if not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text())
+    except Exception:
+        return None
+
+
+def cpu_baseline(space, opts_eps):
+    """The C oracle's Jacobi port on the SAME CSR (downloaded from HBM), all host threads,
+    full solves repeated for ~10 s.  Test infrastructure: only this leg runs oracle/."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_bind import Oracle
+    orc = Oracle()
+    rp, su, rw, ac = space.csr()
+    lo = space.layer_offsets()
+    osp = orc.wrap(lo, rp, su, rw, ac)
+    threads = os.cpu_count() or 1
+    rates, t_total, runs = [], 0.0, 0
+    while runs < 1 or (t_total < 10.0 and runs < 20):
+        v, a, sw, t_sw, t_ex = osp.vi(eps=opts_eps, workers=threads)
+        t = (t_sw + t_ex) * 1e-3
+        rates.append(osp.S * sw / t)
+        t_total += t
+        runs += 1
+    return {"value": max(rates), "unit": "backups/s", "cores": threads, "kind": "port",
+            "sample": f"{runs} full solve(s) ({sw} sweeps + extraction each, {t_total:.1f} s) of "
+                      f"oracle/vcs_oracle.c orc_vi on the device-built C4 CSR, {threads} threads",
+            "time_to_convergence_ms": t_total / runs * 1e3}
+
+
+def run_reference(args):
+    """--impl reference: the unmodified reference solver on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    sys.path.insert(0, str(ROOT / "tests"))
+    import paper_2012_12419_b200 as V
+    try:
+        from oracle_bind import Reference
+        ref = Reference()
+    except Exception as e:  # noqa: BLE001
+        print(json.dumps({"impl": "reference", "unavailable": f"reference library: {e}"}))
+        return 0
+    gen, desc = WORKLOADS[args.workload]
+    ni = V.generate_instance(*gen, as_objects=False)
+    log(f"[reference] building the state space with StateSpace::build ({desc}) ...")
+    sp = ref.build(ni.ref, 10**9)
+    workers = ref.threads()
+    budget_s = float(os.environ.get("VCS_REF_BUDGET_S", "150"))
+    times, sweeps = [], 0
+    t_start = time.time()
+    for i in range(max(0, min(args.warmup, 1))):
+        r = sp.vi(eps=args.eps, workers=workers)
+        sweeps = r.sweeps
+        del r
+    steps = 0
+    while steps < args.steps:
+        r = sp.vi(eps=args.eps, workers=workers)
+        times.append(r.ms * 1e-3)
+        sweeps = r.sweeps
+        del r
+        steps += 1
+        if time.time() - t_start > budget_s:
+            break
+    total = sum(times)
+    value = sp.S * sweeps * steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "backups/s",
+        "n_gpus": args.gpus, "steps": steps, "warmup": min(args.warmup, 1),
+        "ms_per_step": total / steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "states": sp.S, "sweeps": sweeps, "epsilon": args.eps,
+                   "build_ms_excluded": sp.build_ms,
+                   "timing": "detail::run_value_iteration on a prebuilt StateSpace "
+                             "(reference convention, parallel_vi.cpp:126-147), steady_clock"},
+        "time_to_convergence_ms": total / steps * 1e3,
+        "cpu_baseline": {"value": value, "unit": "backups/s", "cores": workers,
+                         "kind": "reference",
+                         "sample": f"{steps} full solve(s) of the unmodified reference "
+                                   f"(oracle/_ref/libvcsref.so), {workers} worker threads"},
+        "e2e": {"value": value, "unit": "backups/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2012_12419_b200 as V
+    from paper_2012_12419_b200 import _native as N
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        log(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    gen, desc = WORKLOADS[args.workload]
+    ni = V.generate_instance(*gen, as_objects=False)
+    t0 = time.time()
+    space = V.StateSpace.build_native(ni, 10**9, local)
+    build_wall_ms = (time.time() - t0) * 1e3
+    S, E, H = space.size(), space.edges(), space.task_count()
+    log(f"[rank {rank}] built {desc}: S={S} E={E} H={H} in {space.info.build_ms:.1f} ms")
+    opts = N.vcs_solve_opts(args.eps, 0 if args.no_skip else 1, 0, 1.0)
+    # A dedicated (non-default) stream: the library, torch's events and NCCL all order on it.
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    sampler = ClockSampler(local)
+    sampler.start()
+    launches0 = None
+
+    if world == 1:
+        h_stream = C.c_void_p(stream.cuda_stream)
+        rep = N.vcs_solve_report()
+        for _ in range(args.warmup):
+            N.check(N.lib().vcs_solve_enqueue(space.handle, C.byref(opts), h_stream))
+        N.check(N.lib().vcs_solve_collect(space.handle, None, None, C.byref(rep), h_stream))
+        sweeps = rep.sweeps
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        launches0 = N.kernel_launches()
+        sweep_ms, extract_ms = [], []
+        tw0 = time.time()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            N.check(N.lib().vcs_solve_enqueue(space.handle, C.byref(opts), h_stream))
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        tw1 = time.time()
+        launches = N.kernel_launches() - launches0
+        # the library's in-graph events of the last step split sweeps vs extraction
+        N.check(N.lib().vcs_solve_collect(space.handle, None, None, C.byref(rep), h_stream))
+        total_ms = ev0.elapsed_time(ev1)
+        sweep_ms.append(rep.sweep_ms)
+        extract_ms.append(rep.extract_ms)
+        sampler.mark(tw0, tw1)
+        alg_bytes_done = rep.alg_bytes_done
+        backups_done = rep.backups_done
+    else:
+        from paper_2012_12419_b200.sharded import CudaBackend, run_sharded
+        backend = CudaBackend(space, dev, stream)
+        lo, le = space.layer_offsets(), space.layer_edges()
+        for _ in range(args.warmup):
+            _, _, sweeps = run_sharded(backend, lo, le, opts, gather=False)
+        dist.barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        launches0 = N.kernel_launches()
+        tw0 = time.time()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            _, _, sweeps = run_sharded(backend, lo, le, opts, gather=False)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        tw1 = time.time()
+        launches = N.kernel_launches() - launches0
+        local_ms = torch.tensor([ev0.elapsed_time(ev1)], device=dev, dtype=torch.float64)
+        dist.all_reduce(local_ms, op=dist.ReduceOp.MAX)
+        total_ms = float(local_ms.item())
+        sampler.mark(tw0, tw1)
+        rep = None
+        from paper_2012_12419_b200.sharded import sweep_row_end
+        backups_done = sum(sweep_row_end(lo, k, not args.no_skip) for k in range(1, sweeps + 1))
+        dbar = E / S
+        alg_bytes_done = (24 + 12 * dbar) * backups_done
+        sweep_ms, extract_ms = [total_ms / args.steps], [0.0]
+
+    sampler.stop()
+    ms_per_step = total_ms / args.steps
+    value = S * sweeps * args.steps / (total_ms * 1e-3)
+    dbar = E / S
+    b_ref = 24 + 12 * dbar
+
+    # ---- e2e through the C ABI with host buffers (rank 0 / N=1 path) --------------------------
+    e2e = None
+    if world == 1 and args.e2e_steps > 0:
+        vals = torch.empty(S, dtype=torch.float64, pin_memory=True)
+        acts = torch.empty(S, dtype=torch.int32, pin_memory=True)
+        inst_bytes = 0
+        s = ni.struct
+        inst_bytes = s.n_clouds * (3 * 4 + 2 * 8) + s.n_tasks * (2 * 4 + 2 * 8)
+        e2e_times = []
+        vp = C.cast(C.c_void_p(vals.data_ptr()), C.POINTER(C.c_double))
+        ap = C.cast(C.c_void_p(acts.data_ptr()), C.POINTER(C.c_int32))
+        for i in range(args.e2e_steps + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            h = C.c_void_p()
+            N.check(N.lib().vcs_space_build(ni.ref, 10**9, local, C.byref(h)))
+            rep2 = N.vcs_solve_report()
+            N.check(N.lib().vcs_solve(h, C.byref(opts), vp, ap, C.byref(rep2)))
+            t1 = time.perf_counter()
+            N.lib().vcs_space_free(h)
+            if i > 0:
+                e2e_times.append(t1 - t0)
+        e2e_t = statistics.median(e2e_times)
+        e2e = {"value": S * rep2.sweeps / e2e_t, "unit": "backups/s",
+               "h2d_bytes_per_step": inst_bytes, "d2h_bytes_per_step": S * (8 + 4),
+               "ms_per_step": e2e_t * 1e3,
+               "path": "vcs_space_build(host instance) + vcs_solve(pinned host values/actions)",
+               "steps": len(e2e_times)}
+
+    # ---- roofline of the dominant kernel (k_sweep) --------------------------------------------
+    peak, peak_src = measured_peaks()
+    sweep_s = statistics.mean(sweep_ms) * 1e-3 if world == 1 else None
+    roofline = None
+    if world == 1 and sweep_s:
+        achieved = alg_bytes_done / sweep_s / 1e9
+        layout_bytes = (20 + 12 * dbar) * backups_done  # u32 row_ptr: 4 B less per state
+        tr = ncu_traffic()
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": tr.get("dram_bytes_per_launch") if tr else None,
+                    "kernel": "k_sweep<false> (all sweep launches of one solve)",
+                    "alg_bytes_per_backup": b_ref,
+                    "alg_bytes_formula": "24 + 12*E/S per performed backup (SURVEY 8d)",
+                    "achieved_layout_GBps": layout_bytes / sweep_s / 1e9,
+                    "peak_source": peak_src,
+                    "traffic_note": (tr or {}).get("note")}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "backups/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": desc, "states": S, "transitions": E, "horizon": H,
+                   "sweeps": sweeps, "epsilon": args.eps, "layer_skip": not args.no_skip,
+                   "backups_performed_per_step": backups_done,
+                   "parallelism": "single GPU" if world == 1 else
+                   f"row-block sharded x{world}, forward halo over NCCL + MAX all-reduce",
+                   "l2": "no flush: CSR 1.7 GB and V buffers 2x155 MB exceed the 126 MB L2",
+                   "build_ms": space.info.build_ms, "build_wall_ms": build_wall_ms},
+        "time_to_convergence_ms": ms_per_step,
+        "sweep_ms": statistics.mean(sweep_ms), "extract_ms": statistics.mean(extract_ms),
+        "roofline": roofline,
+        "cpu_baseline": None,
+        "e2e": e2e,
+        "clocks": sampler.summary(),
+        "gpu_launches": int(launches),
+    }
+    if world == 1 and not args.no_cpu_baseline and rank == 0:
+        try:
+            line["cpu_baseline"] = cpu_baseline(space, args.eps)
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawTextHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
+    ap.add_argument("--eps", type=float, default=1e-6)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-skip", action="store_true", help="disable the converged-layer skip")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        log("note: the timing rules ask for >= 3 warm-up steps")
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -176,6 +176,13 @@ typedef struct vcs_solve_report {
  * NULL.  Bit-identical to the reference for every epsilon (same sweep count). */
 int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int32_t* actions_out,
               vcs_solve_report* report);
+/* The same solve split in two for callers that overlap or time it on their own stream
+ * (a cudaStream_t; NULL = the space's stream): vcs_solve_enqueue launches the whole solve (one
+ * CUDA graph) without synchronising; vcs_solve_collect waits for it, downloads the results of
+ * the LAST enqueued solve and fills the report.  vcs_solve = enqueue + collect. */
+int vcs_solve_enqueue(vcs_space* sp, const vcs_solve_opts* opts, void* stream);
+int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
+                      vcs_solve_report* report, void* stream);
 
 /* Sharded (multi-GPU) building blocks.  One process per GPU; the host runtime owns the value
  * buffers and the collectives (torch.distributed / NCCL over NVLink), these calls only enqueue

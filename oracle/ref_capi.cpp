@@ -268,3 +268,64 @@ int ref_load_counts(const char* path, int32_t* n_clouds, int32_t* n_tasks, int32
 }
 
 } // extern "C"
+
+// ---- the reference's own test oracles (tests/testutil.hpp, compiled from /root/reference) ----
+#include "testutil.hpp"
+
+extern "C" {
+
+// testutil::random_instance(rng, {a,b,c,d}) drawn `trial`+1 times from one rng(seed).  Writes the
+// FLATTENED instance (flatten_tasks order) into caller buffers of capacity a clouds / c tasks.
+int ref_random_instance(uint64_t seed, int32_t trial, int32_t a, int32_t b, int32_t c, int32_t d,
+                        int32_t* n_clouds, int32_t* cloud_cap, double* cloud_delay,
+                        double* cloud_thr, int32_t* n_tasks, int32_t* task_id,
+                        int32_t* task_demand, double* task_delay, double* task_thr,
+                        int32_t* n_bots, int32_t* bot_sizes) {
+    std::mt19937_64 rng(seed);
+    testutil::RandomInstance r;
+    for (int i = 0; i <= trial; ++i) r = testutil::random_instance(rng, {a, b, c, d});
+    *n_clouds = static_cast<int32_t>(r.vcc.clouds.size());
+    for (std::size_t i = 0; i < r.vcc.clouds.size(); ++i) {
+        cloud_cap[i] = r.vcc.clouds[i].vm_total;
+        cloud_delay[i] = r.vcc.clouds[i].v2i_delay_ms;
+        cloud_thr[i] = r.vcc.clouds[i].vm_throughput_kbps;
+    }
+    const auto tasks = flatten_tasks(r.bots);
+    *n_tasks = static_cast<int32_t>(tasks.size());
+    for (std::size_t j = 0; j < tasks.size(); ++j) {
+        task_id[j] = tasks[j].id;
+        task_demand[j] = tasks[j].vm_demand;
+        task_delay[j] = tasks[j].max_delay_ms;
+        task_thr[j] = tasks[j].min_vm_throughput_kbps;
+    }
+    *n_bots = static_cast<int32_t>(r.bots.size());
+    for (std::size_t b = 0; b < r.bots.size(); ++b)
+        bot_sizes[b] = static_cast<int32_t>(r.bots[b].tasks.size());
+    return VCS_OK;
+}
+
+// testutil::brute_force_optimum: exhaustive search, independent of the solver.
+int ref_brute_force(const vcs_instance* in, double* out) {
+    return guarded([&] {
+        auto c = convert(in);
+        *out = testutil::brute_force_optimum(MdpInstance::from_workload(c.vcc, c.bots));
+        return VCS_OK;
+    });
+}
+
+// testutil::FullStateReference value/action of a full state (memoised full-state recursion).
+int ref_full_state(const vcs_instance* in, const int32_t* free_vms, int32_t t, double* value,
+                   int32_t* action) {
+    return guarded([&] {
+        auto c = convert(in);
+        const auto inst = MdpInstance::from_workload(c.vcc, c.bots);
+        testutil::FullStateReference fr(inst);
+        MdpState s = make_state(free_vms, static_cast<int>(c.vcc.clouds.size()), t,
+                                t == static_cast<int>(inst.tasks.size()));
+        *value = fr.value(s);
+        *action = fr.best_action(s);
+        return VCS_OK;
+    });
+}
+
+} // extern "C"

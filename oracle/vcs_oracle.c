@@ -172,7 +172,7 @@ int orc_build(const vcs_instance* in, uint64_t state_cap, orc_space** out) {
     sp->gamma = in->gamma_vc;
 
     /* attr_ok and last_use (mdp.cpp:94-109): capacity against the INITIAL free count. */
-    char* attr_ok = (char*)calloc((size_t)K * (size_t)(H > 0 ? H : 1), 1);
+    char* attr_ok = (char*)calloc((size_t)(K > 0 ? K : 1) * (size_t)(H > 0 ? H : 1), 1);
     sp->last_use = (int*)malloc(sizeof(int) * (size_t)(K > 0 ? K : 1));
     for (int i = 0; i < K; ++i) {
         sp->last_use[i] = -1;
@@ -477,6 +477,28 @@ int orc_vi(const orc_space* sp, double eps, int workers, double discount, int ma
     free(b0);
     free(b1);
     return VCS_OK;
+}
+
+/* Row-range pieces of the same sweep, for the CPU backend of the sharded-driver tests:
+ * one Jacobi sweep over rows [rb, re) (returns the block residual) and the argmax extraction. */
+double orc_sweep_rows(const orc_space* sp, const double* prev, double* next, uint64_t rb,
+                      uint64_t re, double discount) {
+    double delta = 0.0;
+    for (uint64_t s = rb; s < re; ++s) {
+        const double v = orc_backup(sp, s, prev, NULL, discount);
+        const double d = fabs(v - prev[s]);
+        delta = delta < d ? d : delta;
+        next[s] = v;
+    }
+    return delta;
+}
+
+void orc_extract_rows(const orc_space* sp, const double* v, int32_t* act, uint64_t rb, uint64_t re,
+                      double discount) {
+    for (uint64_t s = rb; s < re; ++s) {
+        act[s] = VCS_PAID_CLOUD;
+        orc_backup(sp, s, v, &act[s], discount);
+    }
 }
 
 /* hidden_penalty (mdp.cpp:236-243): gamma * free VMs of clouds retired at the state's layer. */

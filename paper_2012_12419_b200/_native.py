@@ -26,7 +26,7 @@ EXPORTS = (
     "vcs_space_build", "vcs_space_from_csr", "vcs_space_info_get", "vcs_space_layer_offsets",
     "vcs_space_layer_edges", "vcs_space_csr", "vcs_space_locate", "vcs_space_hidden_penalty",
     "vcs_space_free",
-    "vcs_solve", "vcs_shard_plan", "vcs_shard_begin", "vcs_shard_sweep", "vcs_shard_finish",
+    "vcs_solve", "vcs_solve_enqueue", "vcs_solve_collect", "vcs_shard_plan", "vcs_shard_begin", "vcs_shard_sweep", "vcs_shard_finish",
     "vcs_greedy", "vcs_greedy_batch", "vcs_greedy_reward",
     "vcs_last_error", "vcs_kernel_launches", "vcs_device_count",
 )
@@ -150,6 +150,8 @@ _SIGS = {
     "vcs_space_free": (None, [_P]),
     "vcs_solve": (C.c_int, [_P, C.POINTER(vcs_solve_opts), _F64P, _I32P,
                             C.POINTER(vcs_solve_report)]),
+    "vcs_solve_enqueue": (C.c_int, [_P, C.POINTER(vcs_solve_opts), _P]),
+    "vcs_solve_collect": (C.c_int, [_P, _F64P, _I32P, C.POINTER(vcs_solve_report), _P]),
     "vcs_shard_plan": (C.c_int, [_U64P, _U64P, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                  _U64P, _U64P, _U64P, _U64P]),
     "vcs_shard_begin": (C.c_int, [_P, _P, _P, _P, C.c_int32, _P]),

@@ -119,6 +119,8 @@ struct vcs_space {
     vcs::DevBuf<vcs::SolveCtrl> ctrl;
     vcs::DevBuf<int32_t> actions_dev;
     std::map<vcs::GraphKey, vcs::CachedGraph> graphs;
+    vcs::CachedGraph* last_graph = nullptr; // graph of the last vcs_solve_enqueue
+    int last_key_skip = 1;
     double* shard_v0 = nullptr; // caller-owned device buffers of the sharded driver
     double* shard_v1 = nullptr;
     double* shard_delta = nullptr;

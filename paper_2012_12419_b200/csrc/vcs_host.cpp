@@ -488,10 +488,17 @@ int vcs_shard_plan(const uint64_t* layer_offset, const uint64_t* layer_edges, in
         *row_end = re;
         uint64_t hb = re, he = re;
         if (re > rb) {
-            int t = 0; // layer of the block's last row
-            while (t < H && layer_offset[t + 1] <= re - 1) ++t;
-            const uint64_t succ_end = t + 1 <= H ? layer_offset[t + 2] : layer_offset[t + 1];
-            he = std::max(re, std::min(S, succ_end));
+            auto layer_of = [&](uint64_t row) {
+                int t = 0;
+                while (t < H && layer_offset[t + 1] <= row) ++t;
+                return t;
+            };
+            const int t_first = layer_of(rb), t_last = layer_of(re - 1);
+            // successors of layer t rows live in layer t+1 (mdp.cpp:190/201)
+            const uint64_t succ_begin = layer_offset[std::min(t_first + 1, H + 1)];
+            const uint64_t succ_end = t_last + 1 <= H ? layer_offset[t_last + 2] : layer_offset[t_last + 1];
+            hb = std::max(re, succ_begin);
+            he = std::max(hb, std::min(S, succ_end));
         }
         *halo_begin = hb;
         *halo_end = he;

@@ -323,8 +323,7 @@ using vcs::raise;
 
 extern "C" {
 
-int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int32_t* actions_out,
-              vcs_solve_report* report) {
+int vcs_solve_enqueue(vcs_space* sp, const vcs_solve_opts* opts, void* stream) {
     return guarded([&] {
         vcs_solve_opts o{1e-6, 1, 0, 1.0};
         if (opts) o = *opts;
@@ -334,12 +333,32 @@ int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int
         int M = sp->H + 1; // delta_{H+1} == 0 on the layered DAG, so this is never binding
         if (o.max_sweeps > 0) M = std::min(M, o.max_sweeps);
         vcs::ensure_solve_buffers(sp, sp->H + 1); // fixed size: cached graphs keep addresses
-        // Graph node parameters bake in buffer addresses: drop graphs on reallocation.
         const vcs::GraphKey key{o.epsilon, o.discount, o.skip_converged ? 1 : 0, M};
         auto& g = vcs::solve_graph(sp, key);
-        cudaStream_t s = sp->stream;
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
         VCS_CUDA(cudaGraphLaunch(g.exec, s));
         vcs::note_launch(static_cast<uint64_t>(g.launches));
+        sp->last_graph = &g;
+        sp->last_key_skip = key.skip;
+        return VCS_OK;
+    });
+}
+
+int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int32_t* actions_out,
+              vcs_solve_report* report) {
+    const int rc = vcs_solve_enqueue(sp, opts, nullptr);
+    if (rc != VCS_OK) return rc;
+    return vcs_solve_collect(sp, values_out, actions_out, report, nullptr);
+}
+
+int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
+                      vcs_solve_report* report, void* stream) {
+    return guarded([&] {
+        if (!sp->last_graph) raise(VCS_EINVAL, "no solve was enqueued on this space");
+        vcs::bind_device(sp->device);
+        auto& g = *sp->last_graph;
+        const vcs::GraphKey key{0.0, 0.0, sp->last_key_skip, 0};
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
         vcs::SolveCtrl ctrl{};
         VCS_CUDA(cudaMemcpyAsync(&ctrl, sp->ctrl.p, sizeof ctrl, cudaMemcpyDeviceToHost, s));
         VCS_CUDA(cudaStreamSynchronize(s));

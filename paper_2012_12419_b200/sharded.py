@@ -1,0 +1,191 @@
+"""Row-block sharded value iteration across GPUs (one process per GPU, torch.distributed).
+
+Replaces the block-parallel worker of parallel_vi.cpp:68-107: the reference's ``std::thread``
+workers over ``BlockPartition::even`` blocks become ranks over contiguous, cost-balanced row
+blocks; its private-buffer flush + 3 ``SweepBarrier`` waits per sweep become, per sweep,
+
+  1. ``vcs_shard_sweep``  — the local sweep kernel on the rank's rows (residual -> delta[k]);
+  2. ``all_reduce(delta[k], MAX)`` — the reference's fold of ``block_delta`` (:90-96);
+  3. a forward HALO exchange: the state graph is a layered DAG (mdp.cpp:190/201), so a rank only
+     needs V of successor rows in the layer after its last row, owned by the next rank(s) —
+     at most one layer instead of a full all-gather of V.
+
+The convergence test ``delta[k] < eps`` runs in the prologue of the next sweep kernel on the
+device, so the host enqueues the whole solve without a single synchronisation.  Results are
+bit-identical to the single-GPU solve for any world size (the reference's own contract,
+tests/test_parallel.cpp:89-106).
+
+The device work goes through a backend object (``CudaBackend`` here; tests use a CPU backend
+over the C oracle with the gloo process group to check the driver logic).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _native as N
+
+
+@dataclass
+class ShardPlan:
+    row_begin: int
+    row_end: int
+    halo_begin: int
+    halo_end: int
+
+
+def shard_plans(layer_offset: np.ndarray, layer_edges: np.ndarray, world: int,
+                skip_weighted: bool = False) -> list:
+    """vcs_shard_plan for every rank (host-only, no GPU)."""
+    lo = np.ascontiguousarray(layer_offset, dtype=np.uint64)
+    le = np.ascontiguousarray(layer_edges, dtype=np.uint64)
+    H = len(lo) - 2
+    plans = []
+    for r in range(world):
+        vals = [C.c_uint64() for _ in range(4)]
+        N.check(N.lib().vcs_shard_plan(N.ptr(lo, C.c_uint64), N.ptr(le, C.c_uint64), H, world, r,
+                                       1 if skip_weighted else 0, *[C.byref(v) for v in vals]))
+        plans.append(ShardPlan(*[int(v.value) for v in vals]))
+    return plans
+
+
+def sweep_row_end(layer_offset: np.ndarray, k: int, skip: bool) -> int:
+    """Rows visited by sweep k (converged-layer skip), mirrors vcs_solve.cu sweep_row_end."""
+    H = len(layer_offset) - 2
+    S = int(layer_offset[-1])
+    if not skip:
+        return S
+    last = min(H, H - k + 1)
+    return 0 if last < 0 else int(layer_offset[last + 1])
+
+
+class CudaBackend:
+    """Device backend: the sm_100a sweep/extract kernels of libvcs_gpu.so on torch's stream."""
+
+    def __init__(self, space, device: torch.device, stream: "torch.cuda.Stream | None" = None):
+        self.space = space
+        self.device = device
+        # Never the legacy default stream (handle 0 would mean "the space's own stream" to the
+        # C ABI and break the ordering with the NCCL collectives issued on torch's stream).
+        self.torch_stream = stream or torch.cuda.Stream(device)
+        S = space.size()
+        H = space.task_count()
+        self.v0 = torch.empty(S, dtype=torch.float64, device=device)
+        self.v1 = torch.empty(S, dtype=torch.float64, device=device)
+        self.delta = torch.empty(H + 3, dtype=torch.float64, device=device)
+
+    def stream(self):
+        return C.c_void_p(self.torch_stream.cuda_stream)
+
+    def begin(self, opts):
+        N.check(N.lib().vcs_shard_begin(self.space.handle, C.c_void_p(self.v0.data_ptr()),
+                                        C.c_void_p(self.v1.data_ptr()),
+                                        C.c_void_p(self.delta.data_ptr()), self.delta.numel(),
+                                        self.stream()))
+
+    def buffer(self, k: int) -> torch.Tensor:
+        return self.v1 if (k & 1) else self.v0
+
+    def sweep(self, k: int, rb: int, re: int, opts):
+        N.check(N.lib().vcs_shard_sweep(self.space.handle, k, rb, re, C.byref(opts),
+                                        self.stream()))
+
+    def finish(self, n_sweeps: int, rb: int, re: int, opts, values: np.ndarray | None,
+               actions: np.ndarray | None) -> int:
+        sw = C.c_int32()
+        N.check(N.lib().vcs_shard_finish(
+            self.space.handle, n_sweeps, rb, re, C.byref(opts),
+            N.ptr(values, C.c_double) if values is not None else None,
+            N.ptr(actions, C.c_int32) if actions is not None else None, C.byref(sw),
+            self.stream()))
+        return int(sw.value)
+
+
+def halo_transfers(plans: list, rows_done: int) -> list:
+    """(src_rank, dst_rank, begin, end): rows of src's block that dst reads next sweep and that
+    changed in this sweep (rows >= rows_done were not recomputed)."""
+    out = []
+    for dst, p in enumerate(plans):
+        if p.halo_end <= p.halo_begin:
+            continue
+        for src, q in enumerate(plans):
+            if src == dst:
+                continue
+            b = max(p.halo_begin, q.row_begin)
+            e = min(p.halo_end, q.row_end, rows_done)
+            if e > b:
+                out.append((src, dst, b, e))
+    return out
+
+
+def run_sharded(backend, layer_offset: np.ndarray, layer_edges: np.ndarray, opts,
+                group=None, gather: bool = True):
+    """Sharded Jacobi VI.  Returns (values, actions, sweeps) on every rank when ``gather``
+    (full arrays), else (None, None, sweeps) with only this rank's block extracted."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    plans = shard_plans(layer_offset, layer_edges, world, skip_weighted=False)
+    me = plans[rank]
+    H = len(layer_offset) - 2
+    S = int(layer_offset[-1])
+    skip = bool(opts.skip_converged)
+    M = H + 1
+    if opts.max_sweeps > 0:
+        M = min(M, opts.max_sweeps)
+    ctx = torch.cuda.stream(backend.torch_stream) if hasattr(backend, "torch_stream") else None
+    if ctx is not None:
+        ctx.__enter__()
+    try:
+        sweeps = _sweeps(backend, plans, rank, world, layer_offset, opts, group, M, skip)
+    finally:
+        if ctx is not None:
+            ctx.__exit__(None, None, None)
+    values = np.zeros(S, np.float64) if gather else None
+    actions = np.zeros(S, np.int32) if gather else None
+    sweeps = backend.finish(M, me.row_begin, me.row_end, opts, values, actions)
+    if gather and world > 1:
+        # Every rank holds only its block (zeros elsewhere); an integer SUM over the bit images
+        # assembles the arrays exactly (a float sum would turn -0.0 into +0.0).
+        vt = torch.from_numpy(values.view(np.int64))
+        at = torch.from_numpy(actions)
+        dist.all_reduce(vt, op=dist.ReduceOp.SUM, group=_cpu_group(group))
+        dist.all_reduce(at, op=dist.ReduceOp.SUM, group=_cpu_group(group))
+        values, actions = vt.numpy().view(np.float64), at.numpy()
+    return values, actions, sweeps
+
+
+def _sweeps(backend, plans, rank, world, layer_offset, opts, group, M, skip):
+    me = plans[rank]
+    backend.begin(opts)
+    for k in range(1, M + 1):
+        backend.sweep(k, me.row_begin, me.row_end, opts)
+        dist.all_reduce(backend.delta[k:k + 1], op=dist.ReduceOp.MAX, group=group)
+        if world > 1 and k < M:
+            buf = backend.buffer(k)
+            ops = []
+            for src, dst, b, e in halo_transfers(plans, sweep_row_end(layer_offset, k, skip)):
+                if src == rank:
+                    ops.append(dist.P2POp(dist.isend, buf[b:e], dst, group))
+                elif dst == rank:
+                    ops.append(dist.P2POp(dist.irecv, buf[b:e], src, group))
+            if ops:
+                for req in dist.batch_isend_irecv(ops):
+                    req.wait()
+    return M
+
+
+_CPU_GROUPS: dict = {}
+
+
+def _cpu_group(group):
+    """A gloo group for host-side gathers (the data path itself never uses it)."""
+    if dist.get_backend(group) == "gloo":
+        return group
+    key = id(group)
+    if key not in _CPU_GROUPS:
+        _CPU_GROUPS[key] = dist.new_group(backend="gloo")
+    return _CPU_GROUPS[key]

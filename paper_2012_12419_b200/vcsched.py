@@ -142,6 +142,7 @@ class NativeInstance:
         self._owned = _owned
         if _owned is not None:
             self.struct = N.lib().vcs_instance_view(_owned).contents
+            self.struct._owner = self
             return
         clouds = vcc.clouds
         if bots is not None:
@@ -183,6 +184,7 @@ class NativeInstance:
         s.beta_vc = vcc.reward_per_vc_vm
         s.beta_tc = vcc.cost_per_tcc_vm
         s.gamma_vc = vcc.penalty_per_idle_vm
+        s._owner = self  # byref(struct) keeps the SoA arrays alive (temporaries are safe)
         self.struct = s
 
     @classmethod

@@ -1,0 +1,337 @@
+"""GPU parity: the sm_100a builder and Jacobi solver vs the C oracle and the reference's golden
+vectors — bit-exact CSR (succ, fp64 reward bits, action, row_ptr), values (memcmp), policies,
+sweep counts; plus the reference's property tests (test_mdp.cpp, test_parallel.cpp)."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import paper_2012_12419_b200 as V
+from paper_2012_12419_b200 import _native as N
+from cases import FAMILIES, GOLDEN, named_cases, named_workloads, tiny
+from conftest import bits, sha
+
+pytestmark = pytest.mark.gpu
+
+
+def _csr_equal(sp, osp):
+    lo, rp, su, rw, ac = osp.csr()
+    grp, gsu, grw, gac = sp.csr()
+    assert np.array_equal(lo, sp.layer_offsets())
+    assert np.array_equal(rp, grp)
+    assert np.array_equal(su, gsu)
+    assert np.array_equal(bits(rw), bits(grw))  # fp64 reward BITS (no FMA contraction)
+    assert np.array_equal(ac, gac)
+
+
+def _solve(sp, eps=1e-6, skip=True, discount=1.0):
+    return V.run_value_iteration(sp, V.ViOptions(epsilon=eps, skip_converged=skip,
+                                                 discount=discount))
+
+
+@pytest.mark.parametrize("name", list(named_cases().keys()))
+def test_named_cases_bitwise(gpu, oracle, golden, name):
+    ni, eps_list = named_cases()[name]
+    sp = V.StateSpace.build_native(ni, 10**9)
+    osp = oracle.build(ni.ref, 10**9)
+    _csr_equal(sp, osp)
+    rec = golden["cases"][name]
+    assert sp.size() == rec["S"]
+    assert sha(sp.layer_offsets()) == rec["layers_sha"]
+    for eps in eps_list:
+        g = rec[f"eps={eps:g}"]
+        for skip in (True, False):
+            r = _solve(sp, eps, skip)
+            assert r.values.sweeps() == g["sweeps"]
+            assert sha(r.values.raw_values()) == g["values_sha"]
+            assert sha(r.policy.raw_actions()) == g["actions_sha"]
+
+
+@pytest.mark.parametrize("family", list(FAMILIES.keys()))
+def test_random_families_bitwise(gpu, oracle, golden, family):
+    seed, params, n, brute = FAMILIES[family]
+    for trial in range(n):
+        ni = V.generate_instance(N.VCS_GEN_RANDOM, seed, trial, *params, as_objects=False)
+        sp = V.StateSpace.build_native(ni, 10**9)
+        rec = golden["families"][family][trial]
+        assert sp.size() == rec["S"] and sha(sp.layer_offsets()) == rec["layers_sha"]
+        r = _solve(sp)
+        g = rec["eps=1e-06"]
+        assert r.values.sweeps() == g["sweeps"], trial
+        assert sha(r.values.raw_values()) == g["values_sha"], trial
+        assert sha(r.policy.raw_actions()) == g["actions_sha"], trial
+        if trial % 7 == 0:  # full CSR check on a sample (the value digests cover the rest)
+            _csr_equal(sp, oracle.build(ni.ref, 10**9))
+
+
+def test_canonical_known_answers(gpu, golden):
+    p = V.load_instance(str(GOLDEN / "canonical_instance.txt"))
+    inst = V.MdpInstance.from_workload(p.vcc, p.bots)
+    r = V.value_iteration(inst)
+    g = golden["cases"]["canonical"]["eps=1e-06"]
+    assert r.values.initial_value().hex() == g["v0_hex"]
+    assert abs(r.values.initial_value() - 202.4) <= 1e-9           # acceptance.cpp:87
+    assert r.values.sweeps() == 331 and r.values.states_explored() == 68797
+    ro = V.rollout(r.policy, inst)
+    assert (ro.paid_vms, ro.unused_vms) == (58, 0)                  # test_mdp.cpp:270-281
+    assert abs(V.greedy_reward(ro, p.vcc) - 202.4) <= 1e-9
+    assert sha(ro.target_index) == g["rollout_targets_sha"]
+    for c in p.vcc.clouds:
+        assert ro.per_vc_used[c.id] == c.vm_total                   # 100 % utilization
+
+
+def test_c3_full_size(gpu, oracle, golden):
+    ni = V.generate_instance(N.VCS_GEN_HOMOG, 2012, 0, 5, 8, 40, 3, as_objects=False)
+    sp = V.StateSpace.build_native(ni, 10**9)
+    assert (sp.size(), sp.edges()) == (1788700, 8478149)
+    _csr_equal(sp, oracle.build(ni.ref, 10**9))
+    g = golden["cases"]["C3"]["eps=1e-06"]
+    for skip in (True, False):
+        r = _solve(sp, skip=skip)
+        assert r.values.sweeps() == g["sweeps"] == 41
+        assert sha(r.values.raw_values()) == g["values_sha"]
+        assert sha(r.policy.raw_actions()) == g["actions_sha"]
+        assert float(r.values.raw_values()[0]).hex() == (-23.599999999999973).hex()
+
+
+def test_c4_full_size(gpu, golden):
+    """~10^7 states: bit-exact against the reference's digests (no CPU run needed)."""
+    ni = V.generate_instance(N.VCS_GEN_HOMOG, 2012, 0, 6, 8, 48, 3, as_objects=False)
+    sp = V.StateSpace.build_native(ni, 10**9)
+    assert (sp.size(), sp.edges()) == (19333781, 106428994)
+    g = golden["cases"]["C4"]
+    assert sha(sp.layer_offsets()) == g["layers_sha"]
+    r = _solve(sp)
+    assert r.values.sweeps() == g["eps=1e-06"]["sweeps"] == 49
+    assert sha(r.values.raw_values()) == g["eps=1e-06"]["values_sha"]
+    assert sha(r.policy.raw_actions()) == g["eps=1e-06"]["actions_sha"]
+    r2 = _solve(sp, skip=False)  # layer skip is bit-identical
+    assert np.array_equal(bits(r2.values.raw_values()), bits(r.values.raw_values()))
+    assert np.array_equal(r2.policy.raw_actions(), r.policy.raw_actions())
+
+
+def test_solver_on_uploaded_oracle_csr(gpu, oracle):
+    """The solver alone (vcs_space_from_csr), independent of the device builder."""
+    for seed, trial in ((3003, 1), (47, 4), (2002, 5)):
+        params = {3003: (4, 5, 25, 3), 47: (4, 6, 25, 3), 2002: (6, 5, 50, 3)}[seed]
+        ni = V.generate_instance(N.VCS_GEN_RANDOM, seed, trial, *params, as_objects=False)
+        osp = oracle.build(ni.ref)
+        lo, rp, su, rw, ac = osp.csr()
+        sp = V.StateSpace.from_csr(lo, rp, su, rw, ac)
+        for eps in (1e-6, 0.4):
+            r = _solve(sp, eps)
+            v, a, sw, _, _ = osp.vi(eps=eps)
+            assert r.values.sweeps() == sw
+            assert np.array_equal(bits(r.values.raw_values()), bits(v))
+            assert np.array_equal(r.policy.raw_actions(), a)
+
+
+@pytest.mark.parametrize("discount", [0.9, 0.5])
+def test_discounted_extension_matches_oracle(gpu, oracle, discount):
+    """LABELLED EXTENSION (no reference counterpart): q = r + gamma*V(s'), separate mul/add."""
+    p = V.load_instance(str(GOLDEN / "canonical_instance.txt"))
+    ni = V.NativeInstance(p.vcc, bots=p.bots)
+    sp = V.StateSpace.build_native(ni)
+    osp = oracle.build(ni.ref)
+    for skip in (True, False):
+        r = _solve(sp, discount=discount, skip=skip)
+        v, a, sw, _, _ = osp.vi(discount=discount)
+        assert r.values.sweeps() == sw
+        assert np.array_equal(bits(r.values.raw_values()), bits(v))
+        assert np.array_equal(r.policy.raw_actions(), a)
+
+
+def test_state_cap_error(gpu):
+    """test_mdp.cpp:248-259."""
+    vcc, bots = tiny(6, [1] * 6)
+    with pytest.raises(V.StateCapacityError) as e:
+        V.value_iteration(V.MdpInstance.from_workload(vcc, bots), V.ViOptions(state_cap=3))
+    assert e.value.cap() == 3 and "3" in str(e.value)
+    assert str(e.value) == "reachable state space exceeds cap of 3 states"
+
+
+def test_free_count_limit(gpu):
+    vcc = V.VccModel([V.VehicularCloud(1, 70000, 70000, 100.0, 10.0)])
+    bots = [V.BagOfTasks(1, [V.Task(1, 1, 50.0, 50.0)])]
+    with pytest.raises(V.InvalidArgument, match="cloud free counts above 65535 are not supported"):
+        V.value_iteration(V.MdpInstance.from_workload(vcc, bots))
+
+
+def test_epsilon_must_be_positive(gpu):
+    vcc, bots = tiny(2, [1])
+    with pytest.raises(V.InvalidArgument, match="epsilon must be > 0"):
+        V.value_iteration(V.MdpInstance.from_workload(vcc, bots), V.ViOptions(epsilon=0.0))
+
+
+def test_terminal_values_and_lookups(gpu):
+    """test_mdp.cpp:65-72 and :261-268."""
+    vcc, bots = tiny(27, [27])
+    inst = V.MdpInstance.from_workload(vcc, bots)
+    vi = V.value_iteration(inst)
+    assert vi.values.value_of(V.MdpState([27], 1, True)) == pytest.approx(-27.0)
+    assert vi.values.value_of(V.MdpState([0], 1, True)) == pytest.approx(0.0)
+    vcc, bots = tiny(2, [1])
+    inst = V.MdpInstance.from_workload(vcc, bots)
+    vi = V.value_iteration(inst)
+    with pytest.raises(V.OutOfRange):
+        vi.policy.action_for(V.MdpState([2], 1, True))
+    with pytest.raises(V.OutOfRange):
+        vi.policy.action_for(V.MdpState([1], 0, False))
+
+
+def test_tie_breaks(gpu):
+    """test_mdp.cpp:74-106."""
+    w = named_workloads()
+    vcc, bots, _ = w["tie_single_paid"]
+    inst = V.MdpInstance.from_workload(vcc, bots)
+    vi = V.value_iteration(inst)
+    val, act = V.bellman_backup(V.initial_state(inst), vi.values, inst)
+    assert val == pytest.approx(-1.2) and act.is_paid()
+    vcc, bots, _ = w["tie_two_branch"]
+    inst = V.MdpInstance.from_workload(vcc, bots)
+    vi = V.value_iteration(inst)
+    val, act = V.bellman_backup(V.initial_state(inst), vi.values, inst)
+    assert val == pytest.approx(1.0) and act == V.MdpAction(0)
+    vcc, bots, _ = w["tie_symmetric"]
+    inst = V.MdpInstance.from_workload(vcc, bots)
+    vi = V.value_iteration(inst)
+    val, act = V.bellman_backup(V.initial_state(inst), vi.values, inst)
+    assert act == V.MdpAction(0)
+    assert vi.policy.action_for(V.initial_state(inst)) == V.MdpAction(0)
+
+
+def test_empty_task_list(gpu):
+    """test_mdp.cpp:108-116."""
+    vcc = V.VccModel([V.VehicularCloud(1, 4, 4, 100.0, 10.0)])
+    inst = V.MdpInstance.from_workload(vcc, [])
+    vi = V.value_iteration(inst)
+    assert vi.values.sweeps() == 1
+    assert vi.values.initial_value() == 0.0
+    assert V.rollout(vi.policy, inst).placements == []
+
+
+def test_full_state_reference_walks(gpu, reference):
+    """test_mdp.cpp:126-156: value_of / action_for along random trajectories vs the
+    reference's memoised full-state recursion (testutil::FullStateReference)."""
+    f = reference.L.ref_full_state
+    f.restype = C.c_int
+    f.argtypes = [C.POINTER(N.vcs_instance), C.POINTER(C.c_int32), C.c_int32,
+                  C.POINTER(C.c_double), C.POINTER(C.c_int32)]
+    rng = np.random.default_rng(61)
+    for trial in range(12):
+        p = V.generate_instance(N.VCS_GEN_RANDOM, 61, trial, 3, 6, 10, 3)
+        inst = V.MdpInstance.from_workload(p.vcc, p.bots)
+        ni = V.NativeInstance(p.vcc, bots=p.bots)
+        vi = V.value_iteration(inst)
+
+        def ref_value(s):
+            fv = np.array(s.free_vms, np.int32)
+            out, act = C.c_double(), C.c_int32()
+            t = s.next_task_index
+            assert f(ni.ref, fv.ctypes.data_as(C.POINTER(C.c_int32)), t, C.byref(out),
+                     C.byref(act)) == 0
+            return out.value
+
+        for walk in range(3):
+            s = V.initial_state(inst)
+            while True:
+                assert vi.values.value_of(s) == pytest.approx(ref_value(s), rel=1e-12, abs=1e-12)
+                if s.terminal:
+                    break
+                chosen = vi.policy.action_for(s)
+                after = V.transition(s, chosen, inst)
+                q = V.step_reward(s, chosen, after, inst) + ref_value(after)
+                assert q == pytest.approx(ref_value(s), rel=1e-12, abs=1e-12)
+                acts = V.legal_actions(inst, s)
+                step = chosen if walk == 0 or rng.random() < 0.5 else acts[rng.integers(len(acts))]
+                s = V.transition(s, step, inst)
+
+
+def test_one_step_optimality_and_rollout(gpu):
+    """test_mdp.cpp:158-180 and :204-214."""
+    rng = np.random.default_rng(67)
+    for trial in range(10):
+        p = V.generate_instance(N.VCS_GEN_RANDOM, 67, trial, 3, 6, 12, 3)
+        inst = V.MdpInstance.from_workload(p.vcc, p.bots)
+        vi = V.value_iteration(inst)
+        s = V.initial_state(inst)
+        while not s.terminal:
+            value, action = V.bellman_backup(s, vi.values, inst)
+            assert value == pytest.approx(vi.values.value_of(s), rel=1e-12, abs=1e-12)
+            acts = V.legal_actions(inst, s)
+            s = V.transition(s, acts[rng.integers(len(acts))], inst)
+        ro = V.rollout(vi.policy, inst)
+        assert V.greedy_reward(ro, p.vcc) == pytest.approx(vi.values.initial_value(), rel=1e-12)
+
+
+def test_scale_covariance_bitwise(gpu):
+    """test_mdp.cpp:216-236: doubling every rate doubles V0 exactly, same raw actions."""
+    for trial in range(10):
+        p = V.generate_instance(N.VCS_GEN_RANDOM, 37, trial, 3, 6, 12, 3)
+        inst = V.MdpInstance.from_workload(p.vcc, p.bots)
+        vcc2 = V.VccModel(p.vcc.clouds, 2 * p.vcc.reward_per_vc_vm, 2 * p.vcc.cost_per_tcc_vm,
+                          2 * p.vcc.penalty_per_idle_vm)
+        inst2 = V.MdpInstance.from_workload(vcc2, p.bots)
+        a, b = V.value_iteration(inst), V.value_iteration(inst2)
+        assert b.values.initial_value() == 2.0 * a.values.initial_value()
+        assert np.array_equal(a.policy.raw_actions(), b.policy.raw_actions())
+
+
+def test_sweeps_bounded_and_dominates_greedy(gpu):
+    """test_mdp.cpp:193-202 and :238-246."""
+    for trial in range(15):
+        p = V.generate_instance(N.VCS_GEN_RANDOM, 41, trial, 4, 6, 25, 3)
+        inst = V.MdpInstance.from_workload(p.vcc, p.bots)
+        vi = V.value_iteration(inst)
+        assert vi.values.sweeps() <= len(inst.tasks) + 1
+        g = V.greedy_schedule(p.vcc, p.bots)
+        assert vi.values.initial_value() >= V.greedy_reward(g, p.vcc) - 1e-9
+
+
+def test_parallel_api_bit_identical(gpu):
+    """test_parallel.cpp:64-106 through the mirrored API (worker count is partition-free)."""
+    p = V.load_instance(str(GOLDEN / "canonical_instance.txt"))
+    inst = V.MdpInstance.from_workload(p.vcc, p.bots)
+    seq = V.value_iteration(inst)
+    for w in (1, 2, 4, 8):
+        par = V.parallel_value_iteration(inst, V.ViOptions(), w)
+        assert np.array_equal(bits(par.values.raw_values()), bits(seq.values.raw_values()))
+        assert np.array_equal(par.policy.raw_actions(), seq.policy.raw_actions())
+        assert par.values.sweeps() == seq.values.sweeps()
+    with pytest.raises(V.InvalidArgument, match="n_workers must be >= 1"):
+        V.parallel_value_iteration(inst, V.ViOptions(), 0)
+    rows = V.measure_speedup(inst, [1, 2])
+    assert rows[0].workers == 1 and rows[0].speedup_vs_one == pytest.approx(1.0)
+
+
+def test_shard_kernels_emulated_ranks(gpu, oracle):
+    """The device shard API (vcs_shard_begin/sweep/finish) over 1..4 row blocks in ONE
+    process: the blocks' sweeps run back to back on one buffer set (their atomicMax into the
+    shared residual slot is the all-reduce), which must reproduce the oracle bit for bit."""
+    import torch
+    from paper_2012_12419_b200.sharded import CudaBackend, shard_plans
+    p = V.load_instance(str(GOLDEN / "canonical_instance.txt"))
+    ni = V.NativeInstance(p.vcc, bots=p.bots)
+    sp = V.StateSpace.build_native(ni)
+    v_ref, a_ref, sw_ref, _, _ = oracle.build(ni.ref).vi()
+    lo, le = sp.layer_offsets(), sp.layer_edges()
+    for world in (1, 2, 4):
+        for skip in (0, 1):
+            be = CudaBackend(sp, torch.device("cuda", 0))
+            opts = N.vcs_solve_opts(1e-6, skip, 0, 1.0)
+            be.begin(opts)
+            plans = shard_plans(lo, le, world)
+            M = sp.task_count() + 1
+            for k in range(1, M + 1):
+                for pl in plans:
+                    be.sweep(k, pl.row_begin, pl.row_end, opts)
+            values = np.zeros(sp.size())
+            actions = np.zeros(sp.size(), np.int32)
+            sweeps = [be.finish(M, pl.row_begin, pl.row_end, opts, values, actions)
+                      for pl in plans]
+            torch.cuda.synchronize()
+            assert set(sweeps) == {sw_ref}
+            assert np.array_equal(bits(values), bits(v_ref))
+            assert np.array_equal(actions, a_ref)

@@ -1,0 +1,124 @@
+"""The multi-GPU driver (paper_2012_12419_b200/sharded.py) on CPU: world_size 2 and 3 over
+gloo, with a backend that runs the C oracle's row-range sweep instead of the sm_100a kernel.
+Checks the plan, the per-sweep MAX all-reduce, the forward-halo exchange, the device-style
+stop rule and buffer parity: the gathered result must be bit-identical to the single-process
+oracle solve (test_parallel.cpp:89-106 contract)."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2012_12419_b200 import _native as N
+from paper_2012_12419_b200.sharded import run_sharded, sweep_row_end
+
+
+class OracleRowBackend:
+    """Mimics the device semantics of vcs_shard_{begin,sweep,finish} with the C oracle."""
+
+    def __init__(self, orc, sp, layer_offset):
+        self.orc, self.sp, self.lo = orc, sp, layer_offset
+        f = orc.L.orc_sweep_rows
+        f.restype = C.c_double
+        f.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_double]
+        g = orc.L.orc_extract_rows
+        g.restype = None
+        g.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_double]
+
+    def begin(self, opts):
+        S, H = self.sp.S, self.sp.H
+        self.v0 = torch.zeros(S, dtype=torch.float64)
+        self.v1 = torch.full((S,), float("nan"), dtype=torch.float64)  # garbage until written
+        self.delta = torch.zeros(H + 3, dtype=torch.float64)
+        self.stop, self.sweeps = False, 0
+
+    def buffer(self, k):
+        return self.v1 if k & 1 else self.v0
+
+    def sweep(self, k, rb, re, opts):
+        if self.stop:
+            return
+        if k > 1 and float(self.delta[k - 1]) < opts.epsilon:
+            self.stop, self.sweeps = True, k - 1
+            return
+        hi = min(re, sweep_row_end(self.lo, k, bool(opts.skip_converged)))
+        if hi > rb:
+            d = self.orc.L.orc_sweep_rows(self.sp.h, self.buffer(k - 1).data_ptr(),
+                                          self.buffer(k).data_ptr(), rb, hi, opts.discount)
+            self.delta[k] = max(float(self.delta[k]), d)
+
+    def finish(self, M, rb, re, opts, values, actions):
+        K = self.sweeps if self.stop else M
+        v = self.buffer(K)
+        act = np.full(self.sp.S, -1, np.int32)
+        self.orc.L.orc_extract_rows(self.sp.h, v.data_ptr(), act.ctypes.data, rb, re,
+                                    opts.discount)
+        if values is not None:
+            values[rb:re] = v.numpy()[rb:re]
+            actions[rb:re] = act[rb:re]
+        return K
+
+
+def _instance(case):
+    import paper_2012_12419_b200 as V
+    from cases import GOLDEN
+    if case == "canonical":
+        p = V.load_instance(str(GOLDEN / "canonical_instance.txt"))
+        return V.NativeInstance(p.vcc, bots=p.bots)
+    seed, trial = case
+    return V.generate_instance(N.VCS_GEN_RANDOM, seed, trial, 4, 6, 25, 3, as_objects=False)
+
+
+def _worker(rank, world, port, case, eps, skip, out_path):
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    sys.path[:0] = [str(root), str(root / "tests")]
+    from oracle_bind import Oracle
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        orc = Oracle()
+        ni = _instance(case)
+        sp = orc.build(ni.ref, 10**9)
+        lo, rp, _, _, _ = sp.csr()
+        le = np.array([rp[lo[t + 1]] - rp[lo[t]] for t in range(sp.H + 1)], np.uint64)
+        opts = N.vcs_solve_opts(eps, 1 if skip else 0, 0, 1.0)
+        backend = OracleRowBackend(orc, sp, lo)
+        values, actions, sweeps = run_sharded(backend, lo, le, opts)
+        if rank == 0:
+            np.savez(out_path, values=values, actions=actions, sweeps=sweeps)
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case,eps,skip", [
+    ("canonical", 1e-6, True), ("canonical", 5.0, True), ("canonical", 1e-6, False),
+    ((3003, 0), 1e-6, True), ((47, 3), 1e-6, True), ((47, 5), 0.7, False),
+])
+def test_sharded_driver_bit_identical(oracle, world, case, eps, skip):
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "r.npz")
+        mp.spawn(_worker, args=(world, _free_port(), case, eps, skip, out), nprocs=world,
+                 join=True)
+        got = np.load(out)
+    ni = _instance(case)  # keep the SoA arrays alive across the C call
+    sp = oracle.build(ni.ref, 10**9)
+    v, a, sw, _, _ = sp.vi(eps=eps)
+    assert int(got["sweeps"]) == sw
+    assert np.array_equal(got["values"].view(np.uint64), v.view(np.uint64))
+    assert np.array_equal(got["actions"], a)
