@@ -117,9 +117,12 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """dram bytes per launch of the profiled sweep launch (profiles/ncu_sweep.json), or None."""
-    p = ROOT / "profiles" / "ncu_sweep.json"
+def ncu_traffic(method):
+    """DRAM bytes per launch of the profiled launch of the dominant kernel (from the committed
+    ncu capture summary under profiles/), or None."""
+    from paper_2012_12419_b200 import _native as N
+    name = "ncu_wave.json" if method == N.VCS_METHOD_WAVEFRONT else "ncu_sweep.json"
+    p = ROOT / "profiles" / name
     if not p.exists():
         return None
     try:
@@ -230,7 +233,9 @@ def run_b200(args):
     build_wall_ms = (time.time() - t0) * 1e3
     S, E, H = space.size(), space.edges(), space.task_count()
     log(f"[rank {rank}] built {desc}: S={S} E={E} H={H} in {space.info.build_ms:.1f} ms")
-    opts = N.vcs_solve_opts(args.eps, 0 if args.no_skip else 1, 0, 1.0)
+    method = {"auto": N.VCS_METHOD_AUTO, "jacobi": N.VCS_METHOD_JACOBI,
+              "wavefront": N.VCS_METHOD_WAVEFRONT}[args.method]
+    opts = N.vcs_solve_opts(args.eps, 0 if args.no_skip else 1, 0, 1.0, method)
     # A dedicated (non-default) stream: the library, torch's events and NCCL all order on it.
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
@@ -265,6 +270,8 @@ def run_b200(args):
         sampler.mark(tw0, tw1)
         alg_bytes_done = rep.alg_bytes_done
         backups_done = rep.backups_done
+        method = rep.method
+        model_bytes = rep.model_bytes
     else:
         from paper_2012_12419_b200.sharded import CudaBackend, run_sharded
         backend = CudaBackend(space, dev, stream)
@@ -293,6 +300,7 @@ def run_b200(args):
         backups_done = sum(sweep_row_end(lo, k, not args.no_skip) for k in range(1, sweeps + 1))
         dbar = E / S
         alg_bytes_done = (24 + 12 * dbar) * backups_done
+        method, model_bytes = N.VCS_METHOD_JACOBI, (20 + 12 * dbar) * backups_done
         sweep_ms, extract_ms = [total_ms / args.steps], [0.0]
 
     sampler.stop()
@@ -330,20 +338,34 @@ def run_b200(args):
                "path": "vcs_space_build(host instance) + vcs_solve(pinned host values/actions)",
                "steps": len(e2e_times)}
 
-    # ---- roofline of the dominant kernel (k_sweep) --------------------------------------------
+    # ---- roofline of the dominant kernel ----------------------------------------------------
     peak, peak_src = measured_peaks()
     sweep_s = statistics.mean(sweep_ms) * 1e-3 if world == 1 else None
     roofline = None
     if world == 1 and sweep_s:
-        achieved = alg_bytes_done / sweep_s / 1e9
-        layout_bytes = (20 + 12 * dbar) * backups_done  # u32 row_ptr: 4 B less per state
-        tr = ncu_traffic()
+        tr = ncu_traffic(method)
+        survey_equiv = b_ref * S * sweeps / sweep_s / 1e9  # SURVEY 8d bytes of the Jacobi sweeps
+        if method == N.VCS_METHOD_WAVEFRONT:
+            # k_wave_layer (all H launches of one solve, extraction fused): per state row_ptr 4
+            # + value 8 + action 4 + winner's action 4, per edge succ 4 + reward 8, per
+            # performed backup (state, version) 16 (written once, read once by layer t-1)
+            alg = model_bytes
+            formula = "20*S + 12*E + 16*backups_performed per solve (DESIGN.md 3.3)"
+            kernel = "k_wave_layer<false> (all H layer launches of one solve)"
+        else:
+            alg = alg_bytes_done
+            formula = "24 + 12*E/S per performed backup (SURVEY 8d)"
+            kernel = "k_sweep<false> (all sweep launches of one solve)"
+        achieved = alg / sweep_s / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": tr.get("dram_bytes_per_launch") if tr else None,
-                    "kernel": "k_sweep<false> (all sweep launches of one solve)",
-                    "alg_bytes_per_backup": b_ref,
-                    "alg_bytes_formula": "24 + 12*E/S per performed backup (SURVEY 8d)",
-                    "achieved_layout_GBps": layout_bytes / sweep_s / 1e9,
+                    "frac": achieved / peak,
+                    "traffic": tr.get("dram_bytes_per_launch") if tr else None,
+                    "traffic_alg_bytes_per_launch": tr.get("alg_bytes_per_launch") if tr else None,
+                    "kernel": kernel, "alg_bytes_per_solve": alg, "alg_bytes_formula": formula,
+                    "survey_B_equivalent_GBps": survey_equiv,
+                    "survey_B_note": "SURVEY 8d Jacobi bytes (24+12*E/S per backup x S x sweeps) "
+                                     "over the same time: the traffic a per-sweep solver would "
+                                     "need to stream for this result",
                     "peak_source": peak_src,
                     "traffic_note": (tr or {}).get("note")}
 
@@ -354,6 +376,7 @@ def run_b200(args):
         "data": "synthetic",
         "config": {"workload": desc, "states": S, "transitions": E, "horizon": H,
                    "sweeps": sweeps, "epsilon": args.eps, "layer_skip": not args.no_skip,
+                   "method": {1: "jacobi", 2: "layer-wavefront"}.get(method, str(method)),
                    "backups_performed_per_step": backups_done,
                    "parallelism": "single GPU" if world == 1 else
                    f"row-block sharded x{world}, forward halo over NCCL + MAX all-reduce",
@@ -389,6 +412,8 @@ def main():
     ap.add_argument("--eps", type=float, default=1e-6)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-skip", action="store_true", help="disable the converged-layer skip")
+    ap.add_argument("--method", choices=["auto", "jacobi", "wavefront"], default="auto",
+                    help="single-GPU solver (auto = layer wavefront when it fits in HBM)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":

@@ -16,6 +16,7 @@ import numpy as np
 VCS_OK, VCS_EINVAL, VCS_ECAP, VCS_EIO, VCS_ECUDA, VCS_ERANGE = 0, 2, 3, 4, 5, 6
 VCS_PAID_CLOUD = -1
 VCS_GEN_RANDOM, VCS_GEN_HOMOG, VCS_GEN_GREEDY = 0, 1, 2
+VCS_METHOD_AUTO, VCS_METHOD_JACOBI, VCS_METHOD_WAVEFRONT = 0, 1, 2
 
 LIB_PATH = Path(__file__).resolve().parent / "libvcs_gpu.so"
 
@@ -105,6 +106,7 @@ class vcs_solve_opts(C.Structure):
         ("skip_converged", C.c_int32),
         ("max_sweeps", C.c_int32),
         ("discount", C.c_double),
+        ("method", C.c_int32),
     ]
 
 
@@ -118,6 +120,9 @@ class vcs_solve_report(C.Structure):
         ("extract_ms", C.c_double),
         ("alg_bytes", C.c_double),
         ("alg_bytes_done", C.c_double),
+        ("method", C.c_int32),
+        ("pad", C.c_int32),
+        ("model_bytes", C.c_double),
     ]
 
 

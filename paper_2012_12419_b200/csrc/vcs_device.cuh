@@ -5,8 +5,10 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <tuple>
 
 #define VCS_CUDA(call)                                                                         \
@@ -28,41 +30,49 @@ namespace vcs {
 
 constexpr uint32_t kEmpty32 = 0xffffffffu;
 
-// RAII device buffer (cudaMalloc / cudaFree), growable with copy.
+// Configure the device's default memory pool once so freed blocks stay cached for reuse
+// (building and freeing spaces repeatedly then costs no cudaMalloc / implicit device sync).
+void init_pool(int device);
+
+// RAII device buffer on the stream-ordered allocator (cudaMallocAsync / cudaFreeAsync on the
+// owner's stream), growable with copy.
 template <class T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0; // capacity in elements
+    cudaStream_t st = nullptr;
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, st);
         p = nullptr;
         n = 0;
     }
     // Ensure capacity >= want; keeps the first `keep` elements when it must reallocate.
-    void reserve(size_t want, size_t keep, cudaStream_t s, double growth = 1.5) {
+    void reserve(size_t want, size_t keep, cudaStream_t s, double growth = 2.0) {
         if (want <= n) return;
         size_t cap = n ? static_cast<size_t>(static_cast<double>(n) * growth) : want;
         if (cap < want) cap = want;
         T* np = nullptr;
-        VCS_CUDA(cudaMalloc(&np, cap * sizeof(T)));
+        VCS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&np), cap * sizeof(T), s));
         if (p && keep)
             VCS_CUDA(cudaMemcpyAsync(np, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, s));
-        if (p) {
-            VCS_CUDA(cudaStreamSynchronize(s));
-            cudaFree(p);
-        }
+        if (p) VCS_CUDA(cudaFreeAsync(p, s));
         p = np;
         n = cap;
+        st = s;
     }
-    void exact(size_t want) { // discard contents, capacity exactly `want` if it must grow
+    // Discard contents; capacity >= `want` (grows geometrically to amortise re-allocation).
+    void exact(size_t want, cudaStream_t s) {
         if (want <= n) return;
-        release();
-        VCS_CUDA(cudaMalloc(&p, (want ? want : 1) * sizeof(T)));
-        n = want ? want : 1;
+        if (p) VCS_CUDA(cudaFreeAsync(p, s));
+        p = nullptr;
+        const size_t cap = std::max<size_t>(want ? want : 1, n + n / 2);
+        VCS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), cap * sizeof(T), s));
+        n = cap;
+        st = s;
     }
 };
 
@@ -72,14 +82,19 @@ struct SolveCtrl {
     int32_t sweeps; // K*: the converged sweep count
 };
 
+constexpr int kMethodAuto = 0;
+constexpr int kMethodJacobi = 1;
+constexpr int kMethodWavefront = 2;
+
 struct GraphKey {
     double eps;
     double discount;
     int skip;
     int max_sweeps;
+    int method;
     bool operator<(const GraphKey& o) const {
-        return std::tie(eps, discount, skip, max_sweeps) <
-               std::tie(o.eps, o.discount, o.skip, o.max_sweeps);
+        return std::tie(eps, discount, skip, max_sweeps, method) <
+               std::tie(o.eps, o.discount, o.skip, o.max_sweeps, o.method);
     }
 };
 
@@ -88,6 +103,7 @@ struct CachedGraph {
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     int n_sweeps = 0; // sweep kernels in the graph
     int launches = 0;
+    int method = kMethodJacobi;
 };
 
 } // namespace vcs
@@ -118,6 +134,11 @@ struct vcs_space {
     vcs::DevBuf<double> delta;   // residual per sweep (index k = sweep k)
     vcs::DevBuf<vcs::SolveCtrl> ctrl;
     vcs::DevBuf<int32_t> actions_dev;
+    // layer-wavefront solver: version vectors of every layer + offsets
+    vcs::DevBuf<double> ver;
+    vcs::DevBuf<uint64_t> ver_off;
+    vcs::DevBuf<uint64_t> layer_off_dev;
+    std::vector<uint64_t> ver_off_host;
     std::map<vcs::GraphKey, vcs::CachedGraph> graphs;
     vcs::CachedGraph* last_graph = nullptr; // graph of the last vcs_solve_enqueue
     int last_key_skip = 1;

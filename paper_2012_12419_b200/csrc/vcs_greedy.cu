@@ -196,16 +196,16 @@ struct GreedyDev {
 
 void stage(const vcs_instance* in, const HostGreedy& h, GreedyDev& g, cudaStream_t s) {
     const size_t K = static_cast<size_t>(h.K), T = static_cast<size_t>(h.T);
-    g.c_delay.exact(K);
-    g.c_thr.exact(K);
-    g.t_delay.exact(T);
-    g.t_thr.exact(T);
-    g.mask.exact(T * static_cast<size_t>(h.W));
-    g.task.exact(T);
-    g.levels.exact(std::max<size_t>(1, h.levels.size()));
-    g.free_vms.exact(K);
-    g.target.exact(T);
-    g.paid.exact(1);
+    g.c_delay.exact(K, s);
+    g.c_thr.exact(K, s);
+    g.t_delay.exact(T, s);
+    g.t_thr.exact(T, s);
+    g.mask.exact(T * static_cast<size_t>(h.W), s);
+    g.task.exact(T, s);
+    g.levels.exact(std::max<size_t>(1, h.levels.size()), s);
+    g.free_vms.exact(K, s);
+    g.target.exact(T, s);
+    g.paid.exact(1, s);
     if (K) {
         VCS_CUDA(cudaMemcpyAsync(g.c_delay.p, in->cloud_delay_ms, K * 8, cudaMemcpyHostToDevice, s));
         VCS_CUDA(cudaMemcpyAsync(g.c_thr.p, in->cloud_thr_kbps, K * 8, cudaMemcpyHostToDevice, s));
@@ -265,7 +265,7 @@ int vcs_greedy(const vcs_instance* in, int device, int32_t* target_per_task,
         vcs::stage(in, h, g, s);
         vcs::launch_mask(h, g, vcs::sm_count(device), s);
         vcs::DevBuf<vcs::GreedyDesc> dd;
-        dd.exact(1);
+        dd.exact(1, s);
         const vcs::GreedyDesc desc = vcs::desc_of(h, g);
         VCS_CUDA(cudaMemcpyAsync(dd.p, &desc, sizeof desc, cudaMemcpyHostToDevice, s));
         vcs::launch_first_fit(dd.p, 1, h.smem, s);
@@ -317,7 +317,7 @@ int vcs_greedy_batch(int32_t n, const vcs_instance* insts, int device, int32_t**
             smem = std::max(smem, hs.back().smem);
         }
         vcs::DevBuf<vcs::GreedyDesc> dd;
-        dd.exact(static_cast<size_t>(n));
+        dd.exact(static_cast<size_t>(n), s);
         VCS_CUDA(cudaMemcpyAsync(dd.p, descs.data(), descs.size() * sizeof(vcs::GreedyDesc),
                                  cudaMemcpyHostToDevice, s));
         vcs::launch_first_fit(dd.p, n, smem, s);

@@ -262,10 +262,400 @@ SweepArgs base_args(vcs_space* sp, const double* v0, double* v1, double* delta, 
 
 bool is_discounted(double d) { return !(d == 0.0 || d == 1.0); }
 
+// =============================================================================================
+// Layer wavefront ("all truncation horizons") solver.
+//
+// On the layered DAG the Jacobi iterate of a layer-t state is the optimal k-step truncated
+// return: V_k(s) = max_e ( r_e + V_{k-1}(succ_e) ), succ_e in layer t+1, V_0 = 0, and it is
+// exact (constant) for k >= m_t = H - t.  So every Jacobi iterate V_1..V_{H+1} of every state is
+// determined by the version vectors  W_t(s) = (V_1(s), ..., V_{m_t}(s)).  Processing the layers
+// from t = H-1 down to 0, layer t's version vectors need only layer t+1's — the CSR is streamed
+// ONCE per solve instead of once per sweep, and each V_k(s) is computed with exactly the
+// reference's arithmetic (same adds, same strict '>' edge order), so the bits are identical.
+// The residual of Jacobi sweep k is max over (s,k) of |V_k(s) - V_{k-1}(s)|, reduced per k
+// (shared-memory atomics, then one global atomicMax per block and k).  The convergence sweep
+// K* = min{k : delta_k < eps} is then known on the device; the extraction kernel outputs
+// V_{K*} = W_t(s)[min(K*, m_t)] and the argmax action against V_{K*} of the successors — the
+// reference's extraction (parallel_vi.cpp:109-111) bit for bit.
+// Layout: W_t is state-major (state i of layer t at ver + ver_off[t] + i*m_t), so the lanes
+// that compute the versions of one state read the successor's version vector contiguously.
+// =============================================================================================
+
+constexpr int kWaveWarps = 8;
+
+struct WaveArgs {
+    const uint32_t* __restrict__ row_ptr;
+    const uint32_t* __restrict__ succ;
+    const double* __restrict__ reward;
+    const int32_t* __restrict__ action;
+    double* ver;               // all version vectors
+    const uint64_t* ver_off;   // per layer (H+2)
+    const uint64_t* layer_off; // per layer (H+2), flat state index
+    double* delta;             // delta[k], k = 1..H+1
+    SolveCtrl* ctrl;
+    double* values_out;        // extraction: V_{K*} in reference order
+    int32_t* act_out;          // extraction: argmax action
+    double eps;
+    double discount;
+    uint64_t row0, n, next_row0; // layer t: first flat state, size; layer t+1 first state
+    uint64_t voff, voff_next;    // version offsets of layers t and t+1
+    int m;                       // versions of layer t  (H - t)
+    int tile;                    // states per block tile
+    int max_deg;                 // edge slots per state in the tile's shared-memory CSR
+    int H;
+    int max_sweeps;              // K* cap (H+1, or the caller's max_sweeps)
+};
+
+// One block per tile of T consecutive states of layer t (T*m ~ 2048 (state, version) items):
+//   phase 1: the tile's CSR rows (row_ptr, succ, reward) -> shared memory, coalesced;
+//   phase 2: every item (s, k) gathers V_{k-1}(succ) of its row's successors (the indices come
+//            from shared memory, so the only global round trip is the gather itself) and takes
+//            the strict first maximum; the item with k = m_t (the exact value) also records the
+//            argmax — that IS the extraction of s whenever K* >= m_t;
+//   phase 3: residuals |V_k - V_{k-1}| per k (shared-memory atomics) and coalesced stores.
+template <bool DISC>
+__global__ void __launch_bounds__(kWaveWarps * 32) k_wave_layer(WaveArgs a) {
+    extern __shared__ unsigned long long smem_u64[];
+    const int m = a.m;
+    const int T = a.tile;
+    unsigned long long* sdelta = smem_u64;                           // [m]
+    double* sout = reinterpret_cast<double*>(smem_u64 + m);          // [T*m]
+    double* srew = sout + static_cast<size_t>(T) * m;                // [T*max_deg]
+    uint32_t* ssucc = reinterpret_cast<uint32_t*>(srew + static_cast<size_t>(T) * a.max_deg);
+    uint32_t* srp = ssucc + static_cast<size_t>(T) * a.max_deg;       // [T+1]
+    for (int k = threadIdx.x; k < m; k += blockDim.x) sdelta[k] = 0ull;
+    constexpr int U = 8;
+    const uint32_t mu = static_cast<uint32_t>(m);
+    const int mn = m - 1; // versions stored for layer t+1
+    const double* vn = a.ver + a.voff_next;
+    const uint32_t nbase = static_cast<uint32_t>(a.next_row0);
+    const uint64_t n_tiles = (a.n + T - 1) / T;
+    for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const uint64_t s0 = tile * static_cast<uint64_t>(T);
+        const int nt = static_cast<int>(a.n - s0 < static_cast<uint64_t>(T) ? a.n - s0 : T);
+        __syncthreads(); // previous tile's smem readers are done
+        for (int j = threadIdx.x; j <= nt; j += blockDim.x) srp[j] = __ldg(a.row_ptr + a.row0 + s0 + j);
+        __syncthreads();
+        const uint32_t e0 = srp[0];
+        const int ne = static_cast<int>(srp[nt] - e0);
+        for (int j = threadIdx.x; j < ne; j += blockDim.x) {
+            ssucc[j] = __ldcs(a.succ + e0 + j) - nbase;
+            srew[j] = __ldcs(a.reward + e0 + j);
+        }
+        __syncthreads();
+        const int items = nt * m;
+        for (int i = threadIdx.x; i < items; i += blockDim.x) {
+            const int sl = static_cast<int>(static_cast<uint32_t>(i) / mu);
+            const int k = i - sl * m + 1;
+            const int eb = static_cast<int>(srp[sl] - e0), ee = static_cast<int>(srp[sl + 1] - e0);
+            double best = -INFINITY;
+            int best_e = -1;
+            for (int eo = eb; eo < ee; eo += U) {
+                double v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) // all gathers of the round in flight together
+                    if (eo + u < ee) // V_{k-1}(succ): version 0 is the initial iterate +0.0
+                        v[u] = k >= 2 ? __ldg(vn + static_cast<uint64_t>(ssucc[eo + u]) * mn + (k - 2)) : 0.0;
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (eo + u < ee) {
+                        const double r = srew[eo + u];
+                        const double q = DISC ? __dadd_rn(r, __dmul_rn(a.discount, v[u]))
+                                              : __dadd_rn(r, v[u]);
+                        if (q > best) { // strict: the first maximal edge wins
+                            best = q;
+                            best_e = eo + u;
+                        }
+                    }
+            }
+            sout[i] = best;
+            if (k == m) { // exact value: V_{K*}(s) and the policy whenever K* >= m_t
+                const uint64_t s = a.row0 + s0 + sl;
+                a.values_out[s] = best;
+                a.act_out[s] = best_e >= 0 ? __ldg(a.action + e0 + best_e) : -1;
+            }
+        }
+        __syncthreads();
+        double* out = a.ver + a.voff + s0 * static_cast<uint64_t>(m);
+        for (int i = threadIdx.x; i < items; i += blockDim.x) {
+            const int sl = static_cast<int>(static_cast<uint32_t>(i) / mu);
+            const int k = i - sl * m + 1;
+            const double vk = sout[i];
+            const double d = fabs(vk - (k >= 2 ? sout[i - 1] : 0.0)); // |V_k - V_{k-1}|, V_0 = 0
+            if (d > 0.0)
+                atomicMax(&sdelta[k - 1], static_cast<unsigned long long>(__double_as_longlong(d)));
+            out[i] = vk;
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < m; k += blockDim.x)
+        if (sdelta[k]) atomicMax(reinterpret_cast<unsigned long long*>(a.delta + k + 1), sdelta[k]);
+}
+
+// K* from the residuals, then V_{K*} and the argmax policy for every state.  Warp-cooperative
+// like the Jacobi kernel: 32 consecutive rows per warp, the rows' edge range staged with
+// coalesced loads (q = r + V_{K*}(succ) into shared memory), then each lane scans its row.
+__device__ __forceinline__ int layer_of(const uint64_t* s_layer, int H, uint64_t s) {
+    int lo = 0, hi = H; // largest t with layer_off[t] <= s
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_layer[mid] <= s) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+template <bool DISC>
+__global__ void __launch_bounds__(kWaveWarps * 32) k_wave_extract(WaveArgs a, int qcap) {
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int U = 8;
+    __shared__ int s_kstar;
+    extern __shared__ uint64_t s_dyn[];
+    const int H = a.H;
+    uint64_t* s_layer = s_dyn;           // H+2 layer offsets
+    uint64_t* s_voff = s_dyn + (H + 2);  // H+2 version offsets
+    double* qw = reinterpret_cast<double*>(s_dyn + 2 * (H + 2)) + (threadIdx.x >> 5) * 32 * qcap;
+    for (int t = threadIdx.x; t < H + 2; t += blockDim.x) {
+        s_layer[t] = a.layer_off[t];
+        s_voff[t] = a.ver_off[t];
+    }
+    if (threadIdx.x == 0) {
+        int K = a.max_sweeps;
+        for (int k = 1; k <= a.max_sweeps; ++k)
+            if (a.delta[k] < a.eps) { // parallel_vi.cpp:66: first sweep whose residual < eps
+                K = k;
+                break;
+            }
+        s_kstar = K;
+        if (blockIdx.x == 0) {
+            a.ctrl->sweeps = K;
+            a.ctrl->stop = 1;
+        }
+    }
+    __syncthreads();
+    const int K = s_kstar;
+    // The layer pass already wrote the exact value and its argmax for every state; they are the
+    // extraction against V_{K*} for layers t >= H - K* (min(K*, m_t) = m_t).  Only the prefix
+    // of layers t < H - K* (an early stop) is recomputed here; usually it is empty.
+    const uint64_t S = H - K > 0 ? s_layer[H - K] : 0;
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t r0 = warp * 32; r0 < S; r0 += n_warps * 32) {
+        const uint64_t r = r0 + lane;
+        const bool valid = r < S;
+        const uint64_t rr = valid ? r : S;
+        const uint32_t eb = __ldg(a.row_ptr + rr);
+        uint32_t ee = __shfl_down_sync(FULL, eb, 1);
+        if (lane == 31) ee = valid ? __ldg(a.row_ptr + r + 1) : eb;
+        const uint32_t w0 = __shfl_sync(FULL, eb, 0);
+        const uint32_t w1 = __shfl_sync(FULL, ee, 31);
+        const int t_r = layer_of(s_layer, H, valid ? r : S - 1);
+        // successor layer: t+1 of the source row; when the warp's rows share one layer (the
+        // common case) every staged edge has the same successor layer
+        const int t_first = __shfl_sync(FULL, t_r, 0);
+        const int t_lastv = __shfl_sync(FULL, t_r, 31);
+        const bool one_layer = t_first == t_lastv;
+        for (uint32_t base = w0; base < w1; base += 32 * U) {
+            uint32_t sidx[U];
+            double rw[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t e = base + u * 32 + lane;
+                if (e < w1) {
+                    sidx[u] = __ldcs(a.succ + e);
+                    rw[u] = __ldcs(a.reward + e);
+                }
+            }
+            double v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t e = base + u * 32 + lane;
+                if (e < w1) {
+                    const int ts = one_layer ? t_first + 1 : layer_of(s_layer, H, sidx[u]);
+                    const int ms = H - ts;
+                    const int j = K < ms ? K : ms;
+                    v[u] = j == 0 ? 0.0
+                                  : __ldg(a.ver + s_voff[ts] + (sidx[u] - s_layer[ts]) * ms + (j - 1));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t e = base + u * 32 + lane;
+                if (e < w1)
+                    qw[e - w0] = DISC ? __dadd_rn(rw[u], __dmul_rn(a.discount, v[u]))
+                                      : __dadd_rn(rw[u], v[u]);
+            }
+        }
+        __syncwarp();
+        if (valid) {
+            const int m_t = H - t_r;
+            const int jv = K < m_t ? K : m_t; // V_{K*}(r) = version min(K*, m_t)
+            a.values_out[r] =
+                jv == 0 ? 0.0 : a.ver[s_voff[t_r] + (r - s_layer[t_r]) * m_t + (jv - 1)];
+            int32_t act = -1;
+            double best = -INFINITY;
+            uint32_t best_e = 0xffffffffu;
+            for (uint32_t e = eb; e < ee; ++e) {
+                const double q = qw[e - w0];
+                if (q > best) {
+                    best = q;
+                    best_e = e;
+                }
+            }
+            if (best_e != 0xffffffffu) act = __ldg(a.action + best_e);
+            a.act_out[r] = act;
+        }
+        __syncwarp();
+    }
+}
+
+uint64_t wave_versions(const vcs_space* sp, std::vector<uint64_t>* off = nullptr) {
+    uint64_t tot = 0;
+    if (off) off->assign(static_cast<size_t>(sp->H) + 2, 0);
+    for (int t = 0; t <= sp->H; ++t) {
+        if (off) (*off)[static_cast<size_t>(t)] = tot;
+        tot += (sp->layer_off[t + 1] - sp->layer_off[t]) * static_cast<uint64_t>(sp->H - t);
+    }
+    if (off) (*off)[static_cast<size_t>(sp->H) + 1] = tot;
+    return tot;
+}
+
+bool wavefront_fits(const vcs_space* sp) {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return false;
+    const uint64_t need = wave_versions(sp) * sizeof(double) + (sp->H + 2) * 16;
+    return sp->ver.n >= wave_versions(sp) || need < free_b / 2;
+}
+
+void ensure_wave_buffers(vcs_space* sp) {
+    std::vector<uint64_t> off;
+    const uint64_t nv = wave_versions(sp, &off);
+    sp->ver.exact(std::max<uint64_t>(nv, 1), sp->stream);
+    sp->ver_off.exact(off.size(), sp->stream);
+    sp->layer_off_dev.exact(sp->layer_off.size(), sp->stream);
+    VCS_CUDA(cudaMemcpy(sp->ver_off.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
+    VCS_CUDA(cudaMemcpy(sp->layer_off_dev.p, sp->layer_off.data(), sp->layer_off.size() * 8,
+                        cudaMemcpyHostToDevice));
+    sp->ver_off_host = off;
+}
+
+void capture_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaStream_t s) {
+    const bool disc = is_discounted(key.discount);
+    WaveArgs a{};
+    a.row_ptr = sp->row_ptr.p;
+    a.succ = sp->succ.p;
+    a.reward = sp->reward.p;
+    a.action = sp->action.p;
+    a.ver = sp->ver.p;
+    a.ver_off = sp->ver_off.p;
+    a.layer_off = sp->layer_off_dev.p;
+    a.delta = sp->delta.p;
+    a.ctrl = sp->ctrl.p;
+    a.values_out = sp->v[0].p;
+    a.act_out = sp->actions_dev.p;
+    a.eps = key.eps;
+    a.discount = key.discount;
+    a.H = sp->H;
+    a.max_sweeps = key.max_sweeps;
+    const void* fn_layer = disc ? reinterpret_cast<const void*>(k_wave_layer<true>)
+                                : reinterpret_cast<const void*>(k_wave_layer<false>);
+    const void* fn_ext = disc ? reinterpret_cast<const void*>(k_wave_extract<true>)
+                              : reinterpret_cast<const void*>(k_wave_extract<false>);
+    const int qcap = std::max(1, sp->max_degree);
+    const size_t smem_ext = static_cast<size_t>(sp->H + 2) * 16 +
+                            static_cast<size_t>(kWaveWarps) * 32 * qcap * sizeof(double);
+    if (smem_ext > 200 * 1024) raise(VCS_EINVAL, "out-degree too large for the extraction kernel");
+    // per-layer tile: ~2048 (state, version) items per block tile
+    auto tile_of = [](int m) { return std::max(1, std::min(512, 2048 / std::max(1, m))); };
+    auto smem_of = [&](int m, int T) {
+        return static_cast<size_t>(m) * 8 + static_cast<size_t>(T) * m * 8 +
+               static_cast<size_t>(T) * qcap * 12 + static_cast<size_t>(T + 1) * 4;
+    };
+    size_t smem_layer_max = 1024;
+    for (int t = 0; t < sp->H; ++t)
+        smem_layer_max = std::max(smem_layer_max, smem_of(sp->H - t, tile_of(sp->H - t)));
+    if (smem_layer_max > 200 * 1024)
+        raise(VCS_EINVAL, "horizon/out-degree too large for the wavefront tile");
+    VCS_CUDA(cudaFuncSetAttribute(fn_layer, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem_layer_max)));
+    VCS_CUDA(cudaFuncSetAttribute(fn_ext, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(std::max<size_t>(smem_ext, 1024))));
+    VCS_CUDA(cudaMemsetAsync(sp->delta.p, 0, (sp->H + 3) * sizeof(double), s));
+    VCS_CUDA(cudaMemsetAsync(sp->ctrl.p, 0, sizeof(SolveCtrl), s));
+    VCS_CUDA(cudaEventRecordWithFlags(g.ev[0], s, cudaEventRecordExternal));
+    // terminal layer: V = 0.0 (+0), action = kPaidCloud (mdp.cpp:248-251)
+    {
+        const uint64_t rH = sp->layer_off[sp->H], nH = sp->S - rH;
+        VCS_CUDA(cudaMemsetAsync(sp->v[0].p + rH, 0, nH * sizeof(double), s));
+        VCS_CUDA(cudaMemsetAsync(sp->actions_dev.p + rH, 0xff, nH * sizeof(int32_t), s));
+    }
+    int launches = 0;
+    for (int t = sp->H - 1; t >= 0; --t) {
+        a.row0 = sp->layer_off[t];
+        a.n = sp->layer_off[t + 1] - sp->layer_off[t];
+        a.next_row0 = sp->layer_off[t + 1];
+        a.voff = sp->ver_off_host[t];
+        a.voff_next = sp->ver_off_host[t + 1];
+        a.m = sp->H - t;
+        a.tile = tile_of(a.m);
+        a.max_deg = qcap;
+        const size_t smem = smem_of(a.m, a.tile);
+        int per_sm = 0;
+        VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn_layer,
+                                                               kWaveWarps * 32, smem));
+        const uint64_t tiles = (a.n + a.tile - 1) / a.tile;
+        const uint64_t blocks = std::max<uint64_t>(
+            1, std::min<uint64_t>(tiles, static_cast<uint64_t>(std::max(1, per_sm)) * sp->num_sms));
+        if (disc)
+            k_wave_layer<true><<<static_cast<unsigned>(blocks), kWaveWarps * 32, smem, s>>>(a);
+        else
+            k_wave_layer<false><<<static_cast<unsigned>(blocks), kWaveWarps * 32, smem, s>>>(a);
+        VCS_LAUNCHED();
+        ++launches;
+    }
+    VCS_CUDA(cudaEventRecordWithFlags(g.ev[1], s, cudaEventRecordExternal));
+    int per_sm_ext = 0;
+    VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_ext, fn_ext, kWaveWarps * 32,
+                                                           smem_ext));
+    const uint64_t eblocks = std::max<uint64_t>(
+        1, std::min<uint64_t>((sp->S + 255) / 256,
+                              static_cast<uint64_t>(std::max(1, per_sm_ext)) * sp->num_sms));
+    if (disc)
+        k_wave_extract<true><<<static_cast<unsigned>(eblocks), kWaveWarps * 32, smem_ext, s>>>(a, qcap);
+    else
+        k_wave_extract<false><<<static_cast<unsigned>(eblocks), kWaveWarps * 32, smem_ext, s>>>(a, qcap);
+    VCS_LAUNCHED();
+    VCS_CUDA(cudaEventRecordWithFlags(g.ev[2], s, cudaEventRecordExternal));
+    g.launches = launches + 1;
+}
+
 CachedGraph& solve_graph(vcs_space* sp, const GraphKey& key) {
     auto it = sp->graphs.find(key);
     if (it != sp->graphs.end()) return it->second;
     CachedGraph g;
+    g.method = key.method;
+    if (key.method == kMethodWavefront) {
+        cudaStream_t s = sp->stream;
+        for (auto& e : g.ev) VCS_CUDA(cudaEventCreate(&e));
+        VCS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        try {
+            capture_wavefront(sp, key, g, s);
+        } catch (...) {
+            cudaGraph_t dummy = nullptr;
+            cudaStreamEndCapture(s, &dummy);
+            if (dummy) cudaGraphDestroy(dummy);
+            throw;
+        }
+        cudaGraph_t graph = nullptr;
+        VCS_CUDA(cudaStreamEndCapture(s, &graph));
+        const cudaError_t ierr = cudaGraphInstantiate(&g.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ierr != cudaSuccess)
+            raise(VCS_ECUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ierr));
+        g.n_sweeps = key.max_sweeps;
+        return sp->graphs.emplace(key, g).first->second;
+    }
     cudaStream_t s = sp->stream;
     const bool disc = is_discounted(key.discount);
     const LaunchShape sw = shape_for(sp, disc, false);
@@ -308,11 +698,12 @@ CachedGraph& solve_graph(vcs_space* sp, const GraphKey& key) {
 }
 
 void ensure_solve_buffers(vcs_space* sp, int max_sweeps) {
-    sp->v[0].exact(sp->S);
-    sp->v[1].exact(sp->S);
-    sp->delta.exact(static_cast<size_t>(max_sweeps) + 2);
-    sp->ctrl.exact(1);
-    sp->actions_dev.exact(sp->S);
+    sp->v[0].exact(sp->S, sp->stream);
+    sp->v[1].exact(sp->S, sp->stream);
+    sp->delta.exact(static_cast<size_t>(max_sweeps) + 2, sp->stream);
+    sp->ctrl.exact(1, sp->stream);
+    sp->actions_dev.exact(sp->S, sp->stream);
+    VCS_CUDA(cudaStreamSynchronize(sp->stream)); // pool allocations ready for any stream
 }
 
 } // namespace
@@ -325,15 +716,24 @@ extern "C" {
 
 int vcs_solve_enqueue(vcs_space* sp, const vcs_solve_opts* opts, void* stream) {
     return guarded([&] {
-        vcs_solve_opts o{1e-6, 1, 0, 1.0};
+        vcs_solve_opts o{1e-6, 1, 0, 1.0, VCS_METHOD_AUTO};
         if (opts) o = *opts;
         if (!(o.epsilon > 0.0))
             raise(VCS_EINVAL, "epsilon must be > 0 (value iteration would never terminate)");
+        if (o.method < VCS_METHOD_AUTO || o.method > VCS_METHOD_WAVEFRONT)
+            raise(VCS_EINVAL, "unknown solve method");
         vcs::bind_device(sp->device);
         int M = sp->H + 1; // delta_{H+1} == 0 on the layered DAG, so this is never binding
         if (o.max_sweeps > 0) M = std::min(M, o.max_sweeps);
         vcs::ensure_solve_buffers(sp, sp->H + 1); // fixed size: cached graphs keep addresses
-        const vcs::GraphKey key{o.epsilon, o.discount, o.skip_converged ? 1 : 0, M};
+        int method = o.method;
+        if (method == VCS_METHOD_AUTO)
+            method = vcs::wavefront_fits(sp) ? VCS_METHOD_WAVEFRONT : VCS_METHOD_JACOBI;
+        if (method == VCS_METHOD_WAVEFRONT && sp->ver_off_host.empty())
+            vcs::ensure_wave_buffers(sp);
+        const vcs::GraphKey key{o.epsilon, o.discount,
+                                method == VCS_METHOD_JACOBI && o.skip_converged ? 1 : 0, M,
+                                method};
         auto& g = vcs::solve_graph(sp, key);
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
         VCS_CUDA(cudaGraphLaunch(g.exec, s));
@@ -357,14 +757,16 @@ int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
         if (!sp->last_graph) raise(VCS_EINVAL, "no solve was enqueued on this space");
         vcs::bind_device(sp->device);
         auto& g = *sp->last_graph;
-        const vcs::GraphKey key{0.0, 0.0, sp->last_key_skip, 0};
+        const bool wave = g.method == vcs::kMethodWavefront;
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
         vcs::SolveCtrl ctrl{};
         VCS_CUDA(cudaMemcpyAsync(&ctrl, sp->ctrl.p, sizeof ctrl, cudaMemcpyDeviceToHost, s));
         VCS_CUDA(cudaStreamSynchronize(s));
         const int K = ctrl.sweeps;
+        // Jacobi leaves V_{K*} in ping-pong buffer K*&1; the wavefront extraction writes it to v[0]
+        const double* vsrc = wave ? sp->v[0].p : sp->v[K & 1].p;
         if (values_out)
-            VCS_CUDA(cudaMemcpyAsync(values_out, sp->v[K & 1].p, sp->S * sizeof(double),
+            VCS_CUDA(cudaMemcpyAsync(values_out, vsrc, sp->S * sizeof(double),
                                      cudaMemcpyDeviceToHost, s));
         if (actions_out)
             VCS_CUDA(cudaMemcpyAsync(actions_out, sp->actions_dev.p, sp->S * sizeof(int32_t),
@@ -377,12 +779,21 @@ int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
             report->sweeps = K;
             report->launches = g.launches;
             report->backups_ref = sp->S * static_cast<uint64_t>(K);
+            const double dbar = sp->S ? static_cast<double>(sp->E) / static_cast<double>(sp->S) : 0.0;
             uint64_t done = 0;
-            for (int k = 1; k <= K; ++k) done += vcs::sweep_row_end(sp, k, key.skip != 0);
+            if (wave) {
+                done = vcs::wave_versions(sp); // every version of every state, once
+                // per state: row_ptr 4 + value out 8 + action out 4 + winning action 4; per
+                // edge: succ 4 + reward 8; per version: written once + read back once (8 + 8)
+                report->model_bytes = 20.0 * sp->S + 12.0 * sp->E + 16.0 * done;
+            } else {
+                for (int k = 1; k <= K; ++k) done += vcs::sweep_row_end(sp, k, sp->last_key_skip != 0);
+                report->model_bytes = (20.0 + 12.0 * dbar) * static_cast<double>(done);
+            }
             report->backups_done = done;
             report->sweep_ms = ms_sweep;
             report->extract_ms = ms_ext;
-            const double dbar = sp->S ? static_cast<double>(sp->E) / static_cast<double>(sp->S) : 0.0;
+            report->method = g.method;
             report->alg_bytes = (24.0 + 12.0 * dbar) * static_cast<double>(report->backups_ref);
             report->alg_bytes_done = (24.0 + 12.0 * dbar) * static_cast<double>(done);
         }
@@ -395,8 +806,9 @@ int vcs_shard_begin(vcs_space* sp, double* v0, double* v1, double* delta, int32_
     return guarded([&] {
         vcs::bind_device(sp->device);
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
-        sp->ctrl.exact(1);
-        sp->actions_dev.exact(sp->S);
+        sp->ctrl.exact(1, sp->stream);
+        sp->actions_dev.exact(sp->S, sp->stream);
+        VCS_CUDA(cudaStreamSynchronize(sp->stream));
         sp->shard_v0 = v0;
         sp->shard_v1 = v1;
         sp->shard_delta = delta;
@@ -413,7 +825,7 @@ int vcs_shard_sweep(vcs_space* sp, int32_t k, uint64_t row_begin, uint64_t row_e
     return guarded([&] {
         if (!sp->shard_v0) raise(VCS_EINVAL, "vcs_shard_begin was not called");
         if (k < 1 || k + 1 > sp->shard_n_delta) raise(VCS_EINVAL, "sweep index out of range");
-        vcs_solve_opts o{1e-6, 1, 0, 1.0};
+        vcs_solve_opts o{1e-6, 1, 0, 1.0, VCS_METHOD_JACOBI};
         if (opts) o = *opts;
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
         const bool disc = vcs::is_discounted(o.discount);
@@ -434,7 +846,7 @@ int vcs_shard_finish(vcs_space* sp, int32_t n_sweeps, uint64_t row_begin, uint64
                      int32_t* sweeps_out, void* stream) {
     return guarded([&] {
         if (!sp->shard_v0) raise(VCS_EINVAL, "vcs_shard_begin was not called");
-        vcs_solve_opts o{1e-6, 1, 0, 1.0};
+        vcs_solve_opts o{1e-6, 1, 0, 1.0, VCS_METHOD_JACOBI};
         if (opts) o = *opts;
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
         const bool disc = vcs::is_discounted(o.discount);

@@ -281,7 +281,7 @@ struct Scratch {
 void exclusive_scan(Scratch& sc, const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t s) {
     size_t bytes = 0;
     VCS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, static_cast<int64_t>(n), s));
-    sc.cub_tmp.exact(bytes);
+    sc.cub_tmp.exact(bytes, s);
     VCS_CUDA(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.p, bytes, in, out, static_cast<int64_t>(n), s));
     note_launch();
 }
@@ -320,8 +320,8 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
         const uint64_t key_t = sp->key_off[static_cast<size_t>(t)];
         sp->key_off[static_cast<size_t>(t) + 1] = key_t + n_t * static_cast<uint64_t>(L.words);
 
-        sc.deg.exact(n_t + 1);
-        sc.off.exact(n_t + 1);
+        sc.deg.exact(n_t + 1, s);
+        sc.off.exact(n_t + 1, s);
         k_count<WM><<<blocks_for(n_t + 1, T), T, 0, s>>>(static_cast<uint32_t>(n_t),
                                                          sp->keys.p + key_t, L, sc.deg.p);
         VCS_LAUNCHED();
@@ -335,17 +335,17 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
         sp->succ.reserve(E + E_t, E, s);
         sp->reward.reserve(E + E_t, E, s);
         sp->action.reserve(E + E_t, E, s);
-        sc.ekeys.exact(E_t * static_cast<uint64_t>(L.next_words));
+        sc.ekeys.exact(E_t * static_cast<uint64_t>(L.next_words), s);
         k_emit<WM><<<blocks_for(n_t, T), T, 0, s>>>(
             static_cast<uint32_t>(n_t), sp->keys.p + key_t, sc.off.p, L, static_cast<uint32_t>(E),
             sp->row_ptr.p + row0, sc.ekeys.p, sp->reward.p, sp->action.p);
         VCS_LAUNCHED();
 
         const uint64_t cap = pow2_at_least(2 * E_t);
-        sc.table.exact(cap);
-        sc.slot.exact(E_t);
-        sc.flag.exact(E_t + 1);
-        sc.rank.exact(E_t + 1);
+        sc.table.exact(cap, s);
+        sc.slot.exact(E_t, s);
+        sc.flag.exact(E_t + 1, s);
+        sc.rank.exact(E_t + 1, s);
         VCS_CUDA(cudaMemsetAsync(sc.table.p, 0xff, cap * sizeof(uint32_t), s));
         k_insert<WM><<<blocks_for(E_t, T), T, 0, s>>>(static_cast<uint32_t>(E_t), sc.ekeys.p,
                                                       L.next_words, sc.table.p,
@@ -415,7 +415,7 @@ void ensure_locate_index(vcs_space* sp) {
     if (sp->loc_cap) return;
     const uint64_t cap = pow2_at_least(2 * sp->S);
     if (cap > 0xffffffffull) raise(VCS_EINVAL, "state space too large for the locate index");
-    sp->loc_table.exact(cap);
+    sp->loc_table.exact(cap, sp->stream);
     cudaStream_t s = sp->stream;
     VCS_CUDA(cudaMemsetAsync(sp->loc_table.p, 0xff, cap * sizeof(uint32_t), s));
     dispatch_words(max_words(sp), [&](auto wm) {
@@ -442,6 +442,18 @@ void bind_device(int device) {
         raise(VCS_ECUDA, "no CUDA device available (the solver has no CPU fallback)");
     if (device < 0 || device >= n) raise(VCS_EINVAL, "device ordinal out of range");
     VCS_CUDA(cudaSetDevice(device));
+    init_pool(device);
+}
+
+void init_pool(int device) {
+    static std::once_flag once[64];
+    if (device < 0 || device >= 64) return;
+    std::call_once(once[device], [device] {
+        cudaMemPool_t pool = nullptr;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return;
+        uint64_t keep = ~0ull; // keep freed blocks cached in the pool (no trim at sync points)
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    });
 }
 
 int sm_count(int device) {
@@ -454,12 +466,31 @@ int sm_count(int device) {
 
 vcs_space::~vcs_space() {
     cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
     for (auto& [k, g] : graphs) {
         if (g.exec) cudaGraphExecDestroy(g.exec);
         for (auto& e : g.ev)
             if (e) cudaEventDestroy(e);
     }
-    if (stream) cudaStreamDestroy(stream);
+    // stream-ordered frees must be issued while the stream is alive
+    row_ptr.release();
+    succ.release();
+    reward.release();
+    action.release();
+    keys.release();
+    v[0].release();
+    v[1].release();
+    delta.release();
+    ctrl.release();
+    actions_dev.release();
+    ver.release();
+    ver_off.release();
+    layer_off_dev.release();
+    loc_table.release();
+    if (stream) {
+        cudaStreamSynchronize(stream);
+        cudaStreamDestroy(stream);
+    }
 }
 
 using vcs::guarded;
@@ -539,10 +570,10 @@ int vcs_space_from_csr(uint64_t n_states, uint64_t n_edges, int32_t horizon,
         }
         sp->max_degree = maxdeg;
         cudaStream_t s = sp->stream;
-        sp->row_ptr.exact(n_states + 1);
-        sp->succ.exact(n_edges);
-        sp->reward.exact(n_edges);
-        sp->action.exact(n_edges);
+        sp->row_ptr.exact(n_states + 1, sp->stream);
+        sp->succ.exact(n_edges, sp->stream);
+        sp->reward.exact(n_edges, sp->stream);
+        sp->action.exact(n_edges, sp->stream);
         VCS_CUDA(cudaMemcpyAsync(sp->row_ptr.p, rp32.data(), rp32.size() * 4, cudaMemcpyHostToDevice, s));
         if (n_edges) {
             VCS_CUDA(cudaMemcpyAsync(sp->succ.p, succ, n_edges * 4, cudaMemcpyHostToDevice, s));
@@ -629,9 +660,9 @@ int vcs_space_locate(vcs_space* sp, int64_t n, const int32_t* free_vms, const in
         vcs::DevBuf<vcs::LocQuery> dq;
         vcs::DevBuf<int64_t> dout;
         vcs::DevBuf<uint64_t> dmeta;
-        dq.exact(static_cast<size_t>(n));
-        dout.exact(static_cast<size_t>(n));
-        dmeta.exact(2 * (static_cast<size_t>(sp->H) + 2));
+        dq.exact(static_cast<size_t>(n), sp->stream);
+        dout.exact(static_cast<size_t>(n), sp->stream);
+        dmeta.exact(2 * (static_cast<size_t>(sp->H) + 2), sp->stream);
         VCS_CUDA(cudaMemcpyAsync(dq.p, q.data(), q.size() * sizeof(vcs::LocQuery), cudaMemcpyHostToDevice, s));
         VCS_CUDA(cudaMemcpyAsync(dmeta.p, sp->layer_off.data(), (sp->H + 2) * 8, cudaMemcpyHostToDevice, s));
         VCS_CUDA(cudaMemcpyAsync(dmeta.p + sp->H + 2, sp->key_off.data(), (sp->H + 2) * 8, cudaMemcpyHostToDevice, s));

@@ -362,6 +362,7 @@ class ViOptions:
     skip_converged: bool = True
     discount: float = 1.0
     device: int = 0
+    method: int = 0  # 0 auto (wavefront if it fits), 1 Jacobi sweeps, 2 layer wavefront
 
 
 class StateSpace:
@@ -566,7 +567,7 @@ def run_value_iteration(space: StateSpace, options: ViOptions | None = None,
     values = np.empty(S, dtype=np.float64)
     actions = np.empty(S, dtype=np.int32)
     opts = N.vcs_solve_opts(options.epsilon, 1 if options.skip_converged else 0, 0,
-                            options.discount)
+                            options.discount, options.method)
     rep = N.vcs_solve_report()
     N.check(N.lib().vcs_solve(space.handle, C.byref(opts), N.ptr(values, C.c_double),
                               N.ptr(actions, C.c_int32), C.byref(rep)))

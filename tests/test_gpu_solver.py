@@ -26,9 +26,14 @@ def _csr_equal(sp, osp):
     assert np.array_equal(ac, gac)
 
 
-def _solve(sp, eps=1e-6, skip=True, discount=1.0):
+# (method, skip): every solver path must give the same bits
+METHODS = [(N.VCS_METHOD_JACOBI, True), (N.VCS_METHOD_JACOBI, False),
+           (N.VCS_METHOD_WAVEFRONT, True)]
+
+
+def _solve(sp, eps=1e-6, skip=True, discount=1.0, method=N.VCS_METHOD_AUTO):
     return V.run_value_iteration(sp, V.ViOptions(epsilon=eps, skip_converged=skip,
-                                                 discount=discount))
+                                                 discount=discount, method=method))
 
 
 @pytest.mark.parametrize("name", list(named_cases().keys()))
@@ -42,8 +47,9 @@ def test_named_cases_bitwise(gpu, oracle, golden, name):
     assert sha(sp.layer_offsets()) == rec["layers_sha"]
     for eps in eps_list:
         g = rec[f"eps={eps:g}"]
-        for skip in (True, False):
-            r = _solve(sp, eps, skip)
+        for method, skip in METHODS:
+            r = _solve(sp, eps, skip, method=method)
+            assert r.values.report.method == method
             assert r.values.sweeps() == g["sweeps"]
             assert sha(r.values.raw_values()) == g["values_sha"]
             assert sha(r.policy.raw_actions()) == g["actions_sha"]
@@ -57,11 +63,12 @@ def test_random_families_bitwise(gpu, oracle, golden, family):
         sp = V.StateSpace.build_native(ni, 10**9)
         rec = golden["families"][family][trial]
         assert sp.size() == rec["S"] and sha(sp.layer_offsets()) == rec["layers_sha"]
-        r = _solve(sp)
         g = rec["eps=1e-06"]
-        assert r.values.sweeps() == g["sweeps"], trial
-        assert sha(r.values.raw_values()) == g["values_sha"], trial
-        assert sha(r.policy.raw_actions()) == g["actions_sha"], trial
+        for method, skip in METHODS:
+            r = _solve(sp, method=method, skip=skip)
+            assert r.values.sweeps() == g["sweeps"], (trial, method)
+            assert sha(r.values.raw_values()) == g["values_sha"], (trial, method)
+            assert sha(r.policy.raw_actions()) == g["actions_sha"], (trial, method)
         if trial % 7 == 0:  # full CSR check on a sample (the value digests cover the rest)
             _csr_equal(sp, oracle.build(ni.ref, 10**9))
 
@@ -88,8 +95,8 @@ def test_c3_full_size(gpu, oracle, golden):
     assert (sp.size(), sp.edges()) == (1788700, 8478149)
     _csr_equal(sp, oracle.build(ni.ref, 10**9))
     g = golden["cases"]["C3"]["eps=1e-06"]
-    for skip in (True, False):
-        r = _solve(sp, skip=skip)
+    for method, skip in METHODS:
+        r = _solve(sp, skip=skip, method=method)
         assert r.values.sweeps() == g["sweeps"] == 41
         assert sha(r.values.raw_values()) == g["values_sha"]
         assert sha(r.policy.raw_actions()) == g["actions_sha"]
@@ -103,13 +110,11 @@ def test_c4_full_size(gpu, golden):
     assert (sp.size(), sp.edges()) == (19333781, 106428994)
     g = golden["cases"]["C4"]
     assert sha(sp.layer_offsets()) == g["layers_sha"]
-    r = _solve(sp)
-    assert r.values.sweeps() == g["eps=1e-06"]["sweeps"] == 49
-    assert sha(r.values.raw_values()) == g["eps=1e-06"]["values_sha"]
-    assert sha(r.policy.raw_actions()) == g["eps=1e-06"]["actions_sha"]
-    r2 = _solve(sp, skip=False)  # layer skip is bit-identical
-    assert np.array_equal(bits(r2.values.raw_values()), bits(r.values.raw_values()))
-    assert np.array_equal(r2.policy.raw_actions(), r.policy.raw_actions())
+    for method, skip in METHODS:
+        r = _solve(sp, skip=skip, method=method)
+        assert r.values.sweeps() == g["eps=1e-06"]["sweeps"] == 49
+        assert sha(r.values.raw_values()) == g["eps=1e-06"]["values_sha"]
+        assert sha(r.policy.raw_actions()) == g["eps=1e-06"]["actions_sha"]
 
 
 def test_solver_on_uploaded_oracle_csr(gpu, oracle):
@@ -121,11 +126,12 @@ def test_solver_on_uploaded_oracle_csr(gpu, oracle):
         lo, rp, su, rw, ac = osp.csr()
         sp = V.StateSpace.from_csr(lo, rp, su, rw, ac)
         for eps in (1e-6, 0.4):
-            r = _solve(sp, eps)
             v, a, sw, _, _ = osp.vi(eps=eps)
-            assert r.values.sweeps() == sw
-            assert np.array_equal(bits(r.values.raw_values()), bits(v))
-            assert np.array_equal(r.policy.raw_actions(), a)
+            for method, skip in METHODS:
+                r = _solve(sp, eps, skip=skip, method=method)
+                assert r.values.sweeps() == sw
+                assert np.array_equal(bits(r.values.raw_values()), bits(v))
+                assert np.array_equal(r.policy.raw_actions(), a)
 
 
 @pytest.mark.parametrize("discount", [0.9, 0.5])
@@ -135,12 +141,33 @@ def test_discounted_extension_matches_oracle(gpu, oracle, discount):
     ni = V.NativeInstance(p.vcc, bots=p.bots)
     sp = V.StateSpace.build_native(ni)
     osp = oracle.build(ni.ref)
-    for skip in (True, False):
-        r = _solve(sp, discount=discount, skip=skip)
-        v, a, sw, _, _ = osp.vi(discount=discount)
+    v, a, sw, _, _ = osp.vi(discount=discount)
+    for method, skip in METHODS:
+        r = _solve(sp, discount=discount, skip=skip, method=method)
         assert r.values.sweeps() == sw
         assert np.array_equal(bits(r.values.raw_values()), bits(v))
         assert np.array_equal(r.policy.raw_actions(), a)
+
+
+def test_capped_sweeps_match_oracle(gpu, oracle):
+    """max_sweeps caps (bench sampling): both methods return V_M of the capped Jacobi run."""
+    p = V.load_instance(str(GOLDEN / "canonical_instance.txt"))
+    ni = V.NativeInstance(p.vcc, bots=p.bots)
+    sp = V.StateSpace.build_native(ni)
+    osp = oracle.build(ni.ref)
+    import ctypes as C
+    for cap in (1, 7, 150):
+        v, a, sw, _, _ = osp.vi(max_sweeps=cap)
+        for method, skip in METHODS:
+            opts = N.vcs_solve_opts(1e-6, 1 if skip else 0, cap, 1.0, method)
+            vals = np.empty(sp.size())
+            acts = np.empty(sp.size(), np.int32)
+            rep = N.vcs_solve_report()
+            N.check(N.lib().vcs_solve(sp.handle, C.byref(opts), N.ptr(vals, C.c_double),
+                                      N.ptr(acts, C.c_int32), C.byref(rep)))
+            assert rep.sweeps == sw == cap
+            assert np.array_equal(bits(vals), bits(v)), (cap, method, skip)
+            assert np.array_equal(acts, a)
 
 
 def test_state_cap_error(gpu):
