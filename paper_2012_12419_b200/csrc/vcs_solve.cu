@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 namespace vcs {
 
@@ -283,6 +284,10 @@ bool is_discounted(double d) { return !(d == 0.0 || d == 1.0); }
 
 constexpr int kWaveWarps = 8;
 
+// Version vectors are stored as V_0..V_m (V_0 = 0, the initial iterate) with the stride padded
+// to a multiple of 4 doubles, so a thread's 4 consecutive versions load as two aligned double2.
+__host__ __device__ __forceinline__ int wave_stride(int m) { return (m + 1 + 3) & ~3; }
+
 struct WaveArgs {
     const uint32_t* __restrict__ row_ptr;
     const uint32_t* __restrict__ succ;
@@ -301,94 +306,171 @@ struct WaveArgs {
     uint64_t voff, voff_next;    // version offsets of layers t and t+1
     int m;                       // versions of layer t  (H - t)
     int tile;                    // states per block tile
+    int stride, stride_next;     // stored version-vector strides of layers t and t+1
     int max_deg;                 // edge slots per state in the tile's shared-memory CSR
     int H;
     int max_sweeps;              // K* cap (H+1, or the caller's max_sweeps)
 };
 
-// One block per tile of T consecutive states of layer t (T*m ~ 2048 (state, version) items):
+// One block per tile of T consecutive states of layer t:
 //   phase 1: the tile's CSR rows (row_ptr, succ, reward) -> shared memory, coalesced;
-//   phase 2: every item (s, k) gathers V_{k-1}(succ) of its row's successors (the indices come
-//            from shared memory, so the only global round trip is the gather itself) and takes
-//            the strict first maximum; the item with k = m_t (the exact value) also records the
-//            argmax — that IS the extraction of s whenever K* >= m_t;
-//   phase 3: residuals |V_k - V_{k-1}| per k (shared-memory atomics) and coalesced stores.
-template <bool DISC>
-__global__ void __launch_bounds__(kWaveWarps * 32) k_wave_layer(WaveArgs a) {
+//   phase 2: thread (j, g) of a pass computes versions k = 2g+1, 2g+2 of state j of the pass:
+//            per edge one shared-memory read of (succ, reward) and ONE aligned 16-byte load of
+//            the successor's V_{2g}, V_{2g+1} (version vectors are stored V_0..V_m with an even
+//            stride); the gathers of up to 8 edges are in flight together; then the strict
+//            first maximum per version.  The thread holding k = m_t (the exact value) also records the argmax —
+//            that IS the extraction of s whenever K* >= m_t;
+//   phase 3: residuals |V_k - V_{k-1}| (a thread's k's are fixed: register running maxima).
+template <bool DISC, int U, int MINB>
+__global__ void __launch_bounds__(kWaveWarps * 32, MINB) k_wave_layer(WaveArgs a) {
+    constexpr int P = 2; // versions per thread (one aligned double2 gather per edge)
+    // U: edges whose gathers are issued together; MINB: resident blocks per SM (register cap)
     extern __shared__ unsigned long long smem_u64[];
     const int m = a.m;
     const int T = a.tile;
+    const int m1 = m + 1;                                            // V_0..V_m per state
     unsigned long long* sdelta = smem_u64;                           // [m]
-    double* sout = reinterpret_cast<double*>(smem_u64 + m);          // [T*m]
-    double* srew = sout + static_cast<size_t>(T) * m;                // [T*max_deg]
+    double* sout = reinterpret_cast<double*>(smem_u64 + m);          // [T*(m+1)]
+    double* srew = sout + static_cast<size_t>(T) * m1;               // [T*max_deg]
     uint32_t* ssucc = reinterpret_cast<uint32_t*>(srew + static_cast<size_t>(T) * a.max_deg);
-    uint32_t* srp = ssucc + static_cast<size_t>(T) * a.max_deg;       // [T+1]
-    for (int k = threadIdx.x; k < m; k += blockDim.x) sdelta[k] = 0ull;
-    constexpr int U = 8;
-    const uint32_t mu = static_cast<uint32_t>(m);
-    const int mn = m - 1; // versions stored for layer t+1
+    int32_t* sact = reinterpret_cast<int32_t*>(ssucc + static_cast<size_t>(T) * a.max_deg);
+    uint32_t* srp = reinterpret_cast<uint32_t*>(sact + static_cast<size_t>(T) * a.max_deg); // [T+1]
+    const int tid = threadIdx.x;
+    const int nthr = blockDim.x;
+    for (int k = tid; k < m; k += nthr) sdelta[k] = 0ull;
+    const int G = (m + P - 1) / P;                 // thread groups per state (P versions each)
+    const bool wide = G > nthr;                    // groups loop in strides of nthr
+    const int spp = wide ? 1 : nthr / G;           // states per pass
+    const int my_s = wide ? 0 : tid / G;
+    const int my_g0 = wide ? tid : tid - my_s * G;
+    const bool active = wide || my_s < spp;
+    const uint32_t sn = static_cast<uint32_t>(a.stride_next); // stored stride of layer t+1
+    const uint64_t st = static_cast<uint64_t>(a.stride);       // stored stride of layer t
     const double* vn = a.ver + a.voff_next;
     const uint32_t nbase = static_cast<uint32_t>(a.next_row0);
     const uint64_t n_tiles = (a.n + T - 1) / T;
+    double dmax[P] = {0.0, 0.0}; // narrow case: the thread's k's never change
+    // row_ptr of the block's NEXT tile is prefetched into registers while the current tile
+    // computes (T+1 <= 513 entries: up to 3 per thread)
+    uint32_t rp_next[3];
+    auto prefetch_rp = [&](uint64_t tl) {
+        if (tl >= n_tiles) return;
+        const uint64_t b0 = tl * static_cast<uint64_t>(T);
+        const int cnt = static_cast<int>(a.n - b0 < static_cast<uint64_t>(T) ? a.n - b0 : T);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const int j = tid + q * nthr;
+            if (j <= cnt) rp_next[q] = __ldg(a.row_ptr + a.row0 + b0 + j);
+        }
+    };
+    prefetch_rp(blockIdx.x);
     for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const uint64_t s0 = tile * static_cast<uint64_t>(T);
         const int nt = static_cast<int>(a.n - s0 < static_cast<uint64_t>(T) ? a.n - s0 : T);
-        __syncthreads(); // previous tile's smem readers are done
-        for (int j = threadIdx.x; j <= nt; j += blockDim.x) srp[j] = __ldg(a.row_ptr + a.row0 + s0 + j);
+        __syncthreads(); // previous tile's shared-memory readers are done
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const int j = tid + q * nthr;
+            if (j <= nt) srp[j] = rp_next[q];
+        }
         __syncthreads();
+        prefetch_rp(tile + gridDim.x);
         const uint32_t e0 = srp[0];
         const int ne = static_cast<int>(srp[nt] - e0);
-        for (int j = threadIdx.x; j < ne; j += blockDim.x) {
+        for (int j = tid; j < ne; j += nthr) {
             ssucc[j] = __ldcs(a.succ + e0 + j) - nbase;
             srew[j] = __ldcs(a.reward + e0 + j);
+            sact[j] = __ldcs(a.action + e0 + j); // the winner's action, without a dependent load
         }
         __syncthreads();
-        const int items = nt * m;
-        for (int i = threadIdx.x; i < items; i += blockDim.x) {
-            const int sl = static_cast<int>(static_cast<uint32_t>(i) / mu);
-            const int k = i - sl * m + 1;
-            const int eb = static_cast<int>(srp[sl] - e0), ee = static_cast<int>(srp[sl + 1] - e0);
-            double best = -INFINITY;
-            int best_e = -1;
-            for (int eo = eb; eo < ee; eo += U) {
-                double v[U];
+        double* out = a.ver + a.voff + s0 * st;
+        if (active) {
+            for (int sl = my_s; sl < nt; sl += spp) {
+                const int eb = static_cast<int>(srp[sl] - e0), ee = static_cast<int>(srp[sl + 1] - e0);
+                for (int g = my_g0; g < G; g += nthr) {
+                    double best[P];
+                    int best_e[P];
 #pragma unroll
-                for (int u = 0; u < U; ++u) // all gathers of the round in flight together
-                    if (eo + u < ee) // V_{k-1}(succ): version 0 is the initial iterate +0.0
-                        v[u] = k >= 2 ? __ldg(vn + static_cast<uint64_t>(ssucc[eo + u]) * mn + (k - 2)) : 0.0;
+                    for (int p = 0; p < P; ++p) {
+                        best[p] = -INFINITY;
+                        best_e[p] = -1;
+                    }
+                    for (int eo = eb; eo < ee; eo += U) {
+                        double2 x[U]; // all of the round's gathers in flight together
 #pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (eo + u < ee) {
-                        const double r = srew[eo + u];
-                        const double q = DISC ? __dadd_rn(r, __dmul_rn(a.discount, v[u]))
-                                              : __dadd_rn(r, v[u]);
-                        if (q > best) { // strict: the first maximal edge wins
-                            best = q;
-                            best_e = eo + u;
+                        for (int u = 0; u < U; ++u)
+                            if (eo + u < ee)
+                                x[u] = __ldg(reinterpret_cast<const double2*>(
+                                    vn + (ssucc[eo + u] * sn + static_cast<uint32_t>(g * P))));
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+                            if (eo + u < ee) {
+                                const double r = srew[eo + u];
+                                const double v[P] = {x[u].x, x[u].y}; // V_{2g}, V_{2g+1}
+#pragma unroll
+                                for (int p = 0; p < P; ++p) {
+                                    const double q = DISC ? __dadd_rn(r, __dmul_rn(a.discount, v[p]))
+                                                          : __dadd_rn(r, v[p]);
+                                    if (q > best[p]) { // strict: the first maximal edge wins
+                                        best[p] = q;
+                                        best_e[p] = eo + u;
+                                    }
+                                }
+                            }
+                    }
+                    double* o = out + sl * st;
+                    double* so = sout + sl * m1;
+                    if (g == 0) {
+                        o[0] = 0.0; // V_0 (the initial iterate) is stored for aligned reads
+                        so[0] = 0.0;
+                    }
+#pragma unroll
+                    for (int p = 0; p < P; ++p) {
+                        const int k = g * P + 1 + p;
+                        if (k <= m) {
+                            o[k] = best[p];
+                            so[k] = best[p];
+                            if (k == m) { // exact value: V_{K*}(s) and the policy if K* >= m_t
+                                const uint64_t s = a.row0 + s0 + sl;
+                                a.values_out[s] = best[p];
+                                a.act_out[s] = best_e[p] >= 0 ? sact[best_e[p]] : -1;
+                            }
                         }
                     }
-            }
-            sout[i] = best;
-            if (k == m) { // exact value: V_{K*}(s) and the policy whenever K* >= m_t
-                const uint64_t s = a.row0 + s0 + sl;
-                a.values_out[s] = best;
-                a.act_out[s] = best_e >= 0 ? __ldg(a.action + e0 + best_e) : -1;
+                }
             }
         }
         __syncthreads();
-        double* out = a.ver + a.voff + s0 * static_cast<uint64_t>(m);
-        for (int i = threadIdx.x; i < items; i += blockDim.x) {
-            const int sl = static_cast<int>(static_cast<uint32_t>(i) / mu);
-            const int k = i - sl * m + 1;
-            const double vk = sout[i];
-            const double d = fabs(vk - (k >= 2 ? sout[i - 1] : 0.0)); // |V_k - V_{k-1}|, V_0 = 0
-            if (d > 0.0)
-                atomicMax(&sdelta[k - 1], static_cast<unsigned long long>(__double_as_longlong(d)));
-            out[i] = vk;
+        if (active) {
+            for (int sl = my_s; sl < nt; sl += spp)
+                for (int g = my_g0; g < G; g += nthr) {
+                    const double* so = sout + sl * m1;
+#pragma unroll
+                    for (int p = 0; p < P; ++p) {
+                        const int k = g * P + 1 + p;
+                        if (k <= m) {
+                            const double d = fabs(so[k] - so[k - 1]);
+                            if (!wide) {
+                                dmax[p] = dmax[p] < d ? d : dmax[p];
+                            } else if (d > 0.0) {
+                                atomicMax(&sdelta[k - 1],
+                                          static_cast<unsigned long long>(__double_as_longlong(d)));
+                            }
+                        }
+                    }
+                }
+        }
+    }
+    if (!wide && active) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const int k = my_g0 * P + 1 + p;
+            if (k <= m && dmax[p] > 0.0)
+                atomicMax(&sdelta[k - 1], static_cast<unsigned long long>(__double_as_longlong(dmax[p])));
         }
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < m; k += blockDim.x)
+    for (int k = tid; k < m; k += nthr)
         if (sdelta[k]) atomicMax(reinterpret_cast<unsigned long long*>(a.delta + k + 1), sdelta[k]);
 }
 
@@ -474,9 +556,8 @@ __global__ void __launch_bounds__(kWaveWarps * 32) k_wave_extract(WaveArgs a, in
                 if (e < w1) {
                     const int ts = one_layer ? t_first + 1 : layer_of(s_layer, H, sidx[u]);
                     const int ms = H - ts;
-                    const int j = K < ms ? K : ms;
-                    v[u] = j == 0 ? 0.0
-                                  : __ldg(a.ver + s_voff[ts] + (sidx[u] - s_layer[ts]) * ms + (j - 1));
+                    const int j = K < ms ? K : ms; // V_{K*}(succ) = stored version min(K*, m)
+                    v[u] = __ldg(a.ver + s_voff[ts] + (sidx[u] - s_layer[ts]) * wave_stride(ms) + j);
                 }
             }
 #pragma unroll
@@ -491,8 +572,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32) k_wave_extract(WaveArgs a, in
         if (valid) {
             const int m_t = H - t_r;
             const int jv = K < m_t ? K : m_t; // V_{K*}(r) = version min(K*, m_t)
-            a.values_out[r] =
-                jv == 0 ? 0.0 : a.ver[s_voff[t_r] + (r - s_layer[t_r]) * m_t + (jv - 1)];
+            a.values_out[r] = a.ver[s_voff[t_r] + (r - s_layer[t_r]) * wave_stride(m_t) + jv];
             int32_t act = -1;
             double best = -INFINITY;
             uint32_t best_e = 0xffffffffu;
@@ -510,14 +590,23 @@ __global__ void __launch_bounds__(kWaveWarps * 32) k_wave_extract(WaveArgs a, in
     }
 }
 
+// Stored doubles of the version store (V_0..V_{m_t} per state, stride wave_stride(m_t)).
 uint64_t wave_versions(const vcs_space* sp, std::vector<uint64_t>* off = nullptr) {
     uint64_t tot = 0;
     if (off) off->assign(static_cast<size_t>(sp->H) + 2, 0);
     for (int t = 0; t <= sp->H; ++t) {
         if (off) (*off)[static_cast<size_t>(t)] = tot;
-        tot += (sp->layer_off[t + 1] - sp->layer_off[t]) * static_cast<uint64_t>(sp->H - t);
+        tot += (sp->layer_off[t + 1] - sp->layer_off[t]) * static_cast<uint64_t>(wave_stride(sp->H - t));
     }
     if (off) (*off)[static_cast<size_t>(sp->H) + 1] = tot;
+    return tot;
+}
+
+// Backups the wavefront performs: one per (state, version k = 1..m_t).
+uint64_t wave_backups(const vcs_space* sp) {
+    uint64_t tot = 0;
+    for (int t = 0; t <= sp->H; ++t)
+        tot += (sp->layer_off[t + 1] - sp->layer_off[t]) * static_cast<uint64_t>(sp->H - t);
     return tot;
 }
 
@@ -558,19 +647,34 @@ void capture_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaS
     a.discount = key.discount;
     a.H = sp->H;
     a.max_sweeps = key.max_sweeps;
-    const void* fn_layer = disc ? reinterpret_cast<const void*>(k_wave_layer<true>)
-                                : reinterpret_cast<const void*>(k_wave_layer<false>);
+    // kernel variant (gathers in flight per thread vs occupancy); VCS_WAVE_VARIANT overrides
+    static const int variant = [] {
+        const char* e = std::getenv("VCS_WAVE_VARIANT");
+        return e ? std::atoi(e) : 1;
+    }();
+    using LayerFn = void (*)(WaveArgs);
+    static const LayerFn fns[2][4] = {
+        {k_wave_layer<false, 8, 3>, k_wave_layer<false, 4, 4>, k_wave_layer<false, 4, 5>,
+         k_wave_layer<false, 2, 6>},
+        {k_wave_layer<true, 8, 3>, k_wave_layer<true, 4, 4>, k_wave_layer<true, 4, 5>,
+         k_wave_layer<true, 2, 6>}};
+    const LayerFn layer_fn = fns[disc ? 1 : 0][std::min(3, std::max(0, variant))];
+    const void* fn_layer = reinterpret_cast<const void*>(layer_fn);
     const void* fn_ext = disc ? reinterpret_cast<const void*>(k_wave_extract<true>)
                               : reinterpret_cast<const void*>(k_wave_extract<false>);
     const int qcap = std::max(1, sp->max_degree);
     const size_t smem_ext = static_cast<size_t>(sp->H + 2) * 16 +
                             static_cast<size_t>(kWaveWarps) * 32 * qcap * sizeof(double);
     if (smem_ext > 200 * 1024) raise(VCS_EINVAL, "out-degree too large for the extraction kernel");
-    // per-layer tile: ~2048 (state, version) items per block tile
-    auto tile_of = [](int m) { return std::max(1, std::min(512, 2048 / std::max(1, m))); };
+    // per-layer tile: whole passes of (states x 2-version groups) threads, ~8 passes per tile
+    auto tile_of = [](int m) {
+        const int G = (m + 1) / 2;
+        const int spp = G > kWaveWarps * 32 ? 1 : (kWaveWarps * 32) / G;
+        return G > kWaveWarps * 32 ? 2 : std::min(512, spp * 8);
+    };
     auto smem_of = [&](int m, int T) {
-        return static_cast<size_t>(m) * 8 + static_cast<size_t>(T) * m * 8 +
-               static_cast<size_t>(T) * qcap * 12 + static_cast<size_t>(T + 1) * 4;
+        return static_cast<size_t>(m) * 8 + static_cast<size_t>(T) * (m + 1) * 8 +
+               static_cast<size_t>(T) * qcap * 16 + static_cast<size_t>(T + 1) * 4;
     };
     size_t smem_layer_max = 1024;
     for (int t = 0; t < sp->H; ++t)
@@ -584,11 +688,13 @@ void capture_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaS
     VCS_CUDA(cudaMemsetAsync(sp->delta.p, 0, (sp->H + 3) * sizeof(double), s));
     VCS_CUDA(cudaMemsetAsync(sp->ctrl.p, 0, sizeof(SolveCtrl), s));
     VCS_CUDA(cudaEventRecordWithFlags(g.ev[0], s, cudaEventRecordExternal));
-    // terminal layer: V = 0.0 (+0), action = kPaidCloud (mdp.cpp:248-251)
+    // terminal layer: V = 0.0 (+0), action = kPaidCloud (mdp.cpp:248-251); its stored V_0 = 0
     {
         const uint64_t rH = sp->layer_off[sp->H], nH = sp->S - rH;
         VCS_CUDA(cudaMemsetAsync(sp->v[0].p + rH, 0, nH * sizeof(double), s));
         VCS_CUDA(cudaMemsetAsync(sp->actions_dev.p + rH, 0xff, nH * sizeof(int32_t), s));
+        VCS_CUDA(cudaMemsetAsync(sp->ver.p + sp->ver_off_host[sp->H], 0,
+                                 nH * wave_stride(0) * sizeof(double), s));
     }
     int launches = 0;
     for (int t = sp->H - 1; t >= 0; --t) {
@@ -598,6 +704,8 @@ void capture_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaS
         a.voff = sp->ver_off_host[t];
         a.voff_next = sp->ver_off_host[t + 1];
         a.m = sp->H - t;
+        a.stride = wave_stride(a.m);
+        a.stride_next = wave_stride(a.m - 1);
         a.tile = tile_of(a.m);
         a.max_deg = qcap;
         const size_t smem = smem_of(a.m, a.tile);
@@ -607,10 +715,7 @@ void capture_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaS
         const uint64_t tiles = (a.n + a.tile - 1) / a.tile;
         const uint64_t blocks = std::max<uint64_t>(
             1, std::min<uint64_t>(tiles, static_cast<uint64_t>(std::max(1, per_sm)) * sp->num_sms));
-        if (disc)
-            k_wave_layer<true><<<static_cast<unsigned>(blocks), kWaveWarps * 32, smem, s>>>(a);
-        else
-            k_wave_layer<false><<<static_cast<unsigned>(blocks), kWaveWarps * 32, smem, s>>>(a);
+        layer_fn<<<static_cast<unsigned>(blocks), kWaveWarps * 32, smem, s>>>(a);
         VCS_LAUNCHED();
         ++launches;
     }
@@ -782,7 +887,7 @@ int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
             const double dbar = sp->S ? static_cast<double>(sp->E) / static_cast<double>(sp->S) : 0.0;
             uint64_t done = 0;
             if (wave) {
-                done = vcs::wave_versions(sp); // every version of every state, once
+                done = vcs::wave_backups(sp); // every version of every state, once
                 // per state: row_ptr 4 + value out 8 + action out 4 + winning action 4; per
                 // edge: succ 4 + reward 8; per version: written once + read back once (8 + 8)
                 report->model_bytes = 20.0 * sp->S + 12.0 * sp->E + 16.0 * done;

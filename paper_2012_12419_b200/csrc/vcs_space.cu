@@ -20,6 +20,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 namespace vcs {
@@ -258,6 +260,17 @@ __global__ void k_loc_lookup(int64_t n, const LocQuery* __restrict__ q,
     }
 }
 
+bool trace_enabled() {
+    static const bool on = std::getenv("VCS_TRACE") != nullptr;
+    return on;
+}
+
+double host_ms() {
+    return std::chrono::duration<double, std::milli>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
 uint32_t blocks_for(uint64_t n, uint32_t threads) {
     return static_cast<uint32_t>((n + threads - 1) / threads);
 }
@@ -314,6 +327,7 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
     uint64_t S = 1, E = 0, n_t = 1;
     sp->max_layer = 1;
     constexpr uint32_t T = 256;
+    double t_last = host_ms();
     for (int t = 0; t < H; ++t) {
         const LayerParam& L = pl.layers[static_cast<size_t>(t)];
         sp->layer_off[static_cast<size_t>(t) + 1] = S;
@@ -373,6 +387,14 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
         S += n_next;
         n_t = n_next;
         sp->max_layer = std::max<uint64_t>(sp->max_layer, n_t);
+        if (trace_enabled()) {
+            VCS_CUDA(cudaStreamSynchronize(s));
+            const double now = host_ms();
+            std::fprintf(stderr, "[vcs build] layer %d: n=%llu E_t=%llu  %.3f ms\n", t,
+                         static_cast<unsigned long long>(n_t),
+                         static_cast<unsigned long long>(E_t), now - t_last);
+            t_last = now;
+        }
     }
     sp->layer_off[static_cast<size_t>(H) + 1] = S;
     sp->key_off[static_cast<size_t>(H) + 1] =
