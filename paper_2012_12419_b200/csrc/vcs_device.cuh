@@ -104,6 +104,7 @@ struct CachedGraph {
     int n_sweeps = 0; // sweep kernels in the graph
     int launches = 0;
     int method = kMethodJacobi;
+    int uses = 0; // solves enqueued so far (the first runs without a graph)
 };
 
 } // namespace vcs

@@ -33,6 +33,7 @@ std::atomic<uint64_t>* launches() {
 void raise(int code, const std::string& msg) { throw Error{code, msg}; }
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 void note_launch(uint64_t n) { launches()->fetch_add(n, std::memory_order_relaxed); }
+void unnote_launch(uint64_t n) { launches()->fetch_sub(n, std::memory_order_relaxed); }
 
 void OwnedInstance::refresh_view() {
     view.n_clouds = static_cast<int32_t>(cloud_id.size());

@@ -19,6 +19,7 @@ struct Error {
 [[noreturn]] void raise(int code, const std::string& msg);
 void set_last_error(const std::string& msg);
 void note_launch(uint64_t n = 1);
+void unnote_launch(uint64_t n);
 
 template <class F>
 int guarded(F&& f) {

@@ -629,7 +629,16 @@ void ensure_wave_buffers(vcs_space* sp) {
     sp->ver_off_host = off;
 }
 
-void capture_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaStream_t s) {
+void record_event(cudaEvent_t ev, cudaStream_t s, bool capturing) {
+    if (capturing)
+        VCS_CUDA(cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal));
+    else
+        VCS_CUDA(cudaEventRecord(ev, s));
+}
+
+// Enqueue one wavefront solve on `s` (directly, or into a stream capture).
+void record_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaStream_t s,
+                      bool capturing) {
     const bool disc = is_discounted(key.discount);
     WaveArgs a{};
     a.row_ptr = sp->row_ptr.p;
@@ -687,7 +696,7 @@ void capture_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaS
                                   static_cast<int>(std::max<size_t>(smem_ext, 1024))));
     VCS_CUDA(cudaMemsetAsync(sp->delta.p, 0, (sp->H + 3) * sizeof(double), s));
     VCS_CUDA(cudaMemsetAsync(sp->ctrl.p, 0, sizeof(SolveCtrl), s));
-    VCS_CUDA(cudaEventRecordWithFlags(g.ev[0], s, cudaEventRecordExternal));
+    record_event(g.ev[0], s, capturing);
     // terminal layer: V = 0.0 (+0), action = kPaidCloud (mdp.cpp:248-251); its stored V_0 = 0
     {
         const uint64_t rH = sp->layer_off[sp->H], nH = sp->S - rH;
@@ -719,7 +728,7 @@ void capture_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaS
         VCS_LAUNCHED();
         ++launches;
     }
-    VCS_CUDA(cudaEventRecordWithFlags(g.ev[1], s, cudaEventRecordExternal));
+    record_event(g.ev[1], s, capturing);
     int per_sm_ext = 0;
     VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_ext, fn_ext, kWaveWarps * 32,
                                                            smem_ext));
@@ -731,75 +740,83 @@ void capture_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaS
     else
         k_wave_extract<false><<<static_cast<unsigned>(eblocks), kWaveWarps * 32, smem_ext, s>>>(a, qcap);
     VCS_LAUNCHED();
-    VCS_CUDA(cudaEventRecordWithFlags(g.ev[2], s, cudaEventRecordExternal));
+    record_event(g.ev[2], s, capturing);
     g.launches = launches + 1;
 }
 
-CachedGraph& solve_graph(vcs_space* sp, const GraphKey& key) {
+// Enqueue one Jacobi solve on `s`: zeroing, up to max_sweeps sweep kernels, extraction.
+void record_jacobi(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaStream_t s,
+                   bool capturing) {
+    const bool disc = is_discounted(key.discount);
+    const LaunchShape sw = shape_for(sp, disc, false);
+    const LaunchShape ex = shape_for(sp, disc, true);
+    SweepArgs a = base_args(sp, sp->v[0].p, sp->v[1].p, sp->delta.p, key.eps, key.discount);
+    VCS_CUDA(cudaMemsetAsync(sp->v[0].p, 0, sp->S * sizeof(double), s));
+    VCS_CUDA(cudaMemsetAsync(sp->delta.p, 0, (key.max_sweeps + 2) * sizeof(double), s));
+    VCS_CUDA(cudaMemsetAsync(sp->ctrl.p, 0, sizeof(SolveCtrl), s));
+    record_event(g.ev[0], s, capturing);
+    for (int k = 1; k <= key.max_sweeps; ++k) {
+        a.k = k;
+        a.row_begin = 0;
+        a.row_end = static_cast<uint32_t>(sweep_row_end(sp, k, key.skip != 0));
+        launch_sweep(sp, a, sw, disc, s);
+    }
+    record_event(g.ev[1], s, capturing);
+    a.k = key.max_sweeps;
+    a.row_begin = 0;
+    a.row_end = static_cast<uint32_t>(sp->S);
+    launch_extract(sp, a, ex, disc, s);
+    record_event(g.ev[2], s, capturing);
+    g.launches = key.max_sweeps + 1;
+}
+
+void record_solve(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaStream_t s,
+                  bool capturing) {
+    if (key.method == kMethodWavefront)
+        record_wavefront(sp, key, g, s, capturing);
+    else
+        record_jacobi(sp, key, g, s, capturing);
+}
+
+// Launch one solve on `s`: the first solve of a (space, options) pair captures the kernel
+// sequence into a CUDA graph, every solve replays it with one launch.
+CachedGraph& enqueue_solve(vcs_space* sp, const GraphKey& key, cudaStream_t s) {
     auto it = sp->graphs.find(key);
-    if (it != sp->graphs.end()) return it->second;
-    CachedGraph g;
-    g.method = key.method;
-    if (key.method == kMethodWavefront) {
-        cudaStream_t s = sp->stream;
+    if (it == sp->graphs.end()) {
+        CachedGraph g;
+        g.method = key.method;
+        g.n_sweeps = key.max_sweeps;
         for (auto& e : g.ev) VCS_CUDA(cudaEventCreate(&e));
-        VCS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        it = sp->graphs.emplace(key, g).first;
+    }
+    CachedGraph& g = it->second;
+    // (Measured on C4: capture + instantiate + replay of the 49-node solve costs less than
+    // enqueueing it directly, whose host work between short layer kernels idles the GPU, so
+    // even a one-shot solve goes through the graph.)
+    if (!g.exec) {
+        cudaStream_t cs = sp->stream;
+        if (cs != s) VCS_CUDA(cudaStreamSynchronize(s)); // no cross-stream work pending
+        VCS_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
         try {
-            capture_wavefront(sp, key, g, s);
+            record_solve(sp, key, g, cs, true);
+            unnote_launch(static_cast<uint64_t>(g.launches)); // captured, not launched
         } catch (...) {
             cudaGraph_t dummy = nullptr;
-            cudaStreamEndCapture(s, &dummy);
+            cudaStreamEndCapture(cs, &dummy);
             if (dummy) cudaGraphDestroy(dummy);
             throw;
         }
         cudaGraph_t graph = nullptr;
-        VCS_CUDA(cudaStreamEndCapture(s, &graph));
+        VCS_CUDA(cudaStreamEndCapture(cs, &graph));
         const cudaError_t ierr = cudaGraphInstantiate(&g.exec, graph, 0);
         cudaGraphDestroy(graph);
         if (ierr != cudaSuccess)
             raise(VCS_ECUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ierr));
-        g.n_sweeps = key.max_sweeps;
-        return sp->graphs.emplace(key, g).first->second;
     }
-    cudaStream_t s = sp->stream;
-    const bool disc = is_discounted(key.discount);
-    const LaunchShape sw = shape_for(sp, disc, false);
-    const LaunchShape ex = shape_for(sp, disc, true);
-    for (auto& e : g.ev) VCS_CUDA(cudaEventCreate(&e));
-    SweepArgs a = base_args(sp, sp->v[0].p, sp->v[1].p, sp->delta.p, key.eps, key.discount);
-    VCS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    try {
-        VCS_CUDA(cudaMemsetAsync(sp->v[0].p, 0, sp->S * sizeof(double), s));
-        VCS_CUDA(cudaMemsetAsync(sp->delta.p, 0, (key.max_sweeps + 2) * sizeof(double), s));
-        VCS_CUDA(cudaMemsetAsync(sp->ctrl.p, 0, sizeof(SolveCtrl), s));
-        VCS_CUDA(cudaEventRecordWithFlags(g.ev[0], s, cudaEventRecordExternal));
-        for (int k = 1; k <= key.max_sweeps; ++k) {
-            a.k = k;
-            a.row_begin = 0;
-            a.row_end = static_cast<uint32_t>(sweep_row_end(sp, k, key.skip != 0));
-            launch_sweep(sp, a, sw, disc, s);
-        }
-        VCS_CUDA(cudaEventRecordWithFlags(g.ev[1], s, cudaEventRecordExternal));
-        a.k = key.max_sweeps;
-        a.row_begin = 0;
-        a.row_end = static_cast<uint32_t>(sp->S);
-        launch_extract(sp, a, ex, disc, s);
-        VCS_CUDA(cudaEventRecordWithFlags(g.ev[2], s, cudaEventRecordExternal));
-    } catch (...) {
-        cudaGraph_t dummy = nullptr;
-        cudaStreamEndCapture(s, &dummy);
-        if (dummy) cudaGraphDestroy(dummy);
-        throw;
-    }
-    cudaGraph_t graph = nullptr;
-    VCS_CUDA(cudaStreamEndCapture(s, &graph));
-    const cudaError_t ierr = cudaGraphInstantiate(&g.exec, graph, 0);
-    cudaGraphDestroy(graph);
-    if (ierr != cudaSuccess)
-        raise(VCS_ECUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ierr));
-    g.n_sweeps = key.max_sweeps;
-    g.launches = key.max_sweeps + 1;
-    return sp->graphs.emplace(key, g).first->second;
+    VCS_CUDA(cudaGraphLaunch(g.exec, s));
+    note_launch(static_cast<uint64_t>(g.launches));
+    ++g.uses;
+    return g;
 }
 
 void ensure_solve_buffers(vcs_space* sp, int max_sweeps) {
@@ -839,10 +856,8 @@ int vcs_solve_enqueue(vcs_space* sp, const vcs_solve_opts* opts, void* stream) {
         const vcs::GraphKey key{o.epsilon, o.discount,
                                 method == VCS_METHOD_JACOBI && o.skip_converged ? 1 : 0, M,
                                 method};
-        auto& g = vcs::solve_graph(sp, key);
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
-        VCS_CUDA(cudaGraphLaunch(g.exec, s));
-        vcs::note_launch(static_cast<uint64_t>(g.launches));
+        auto& g = vcs::enqueue_solve(sp, key, s);
         sp->last_graph = &g;
         sp->last_key_skip = key.skip;
         return VCS_OK;

@@ -148,11 +148,11 @@ __global__ void k_emit(uint32_t n, const uint64_t* __restrict__ keys,
 }
 
 template <int WM>
-__global__ void k_insert(uint32_t n_edges, const uint64_t* __restrict__ ekeys, int words,
-                         uint32_t* __restrict__ table, uint32_t mask,
+__global__ void k_insert(const uint32_t* __restrict__ n_edges_dev, const uint64_t* __restrict__ ekeys,
+                         int words, uint32_t* __restrict__ table, uint32_t mask,
                          uint32_t* __restrict__ slot_of) {
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n_edges) return;
+    if (j >= *n_edges_dev) return;
     uint64_t k[WM];
     load_key<WM>(ekeys + static_cast<uint64_t>(j) * words, words, k);
     uint32_t h = static_cast<uint32_t>(hash_key<WM>(k, words, 0)) & mask;
@@ -167,7 +167,10 @@ __global__ void k_insert(uint32_t n_edges, const uint64_t* __restrict__ ekeys, i
             cur = prev;
         }
         if (key_equal<WM>(ekeys + static_cast<uint64_t>(cur) * words, words, k)) {
-            atomicMin(&table[h], j); // keep the first occurrence (lowest edge index)
+            // keep the first occurrence (lowest edge index); skip the atomic when a smaller
+            // index is already there (heavily shared successors, e.g. the single terminal
+            // state, would otherwise serialise on one address)
+            if (cur > j) atomicMin(&table[h], j);
             slot_of[j] = h;
             return;
         }
@@ -175,19 +178,23 @@ __global__ void k_insert(uint32_t n_edges, const uint64_t* __restrict__ ekeys, i
     }
 }
 
-__global__ void k_mark(uint32_t n_edges, const uint32_t* __restrict__ table,
-                       const uint32_t* __restrict__ slot_of, uint32_t* __restrict__ flag) {
+// flag[j] = 1 iff edge j is the first occurrence of its successor; zeros past E_t up to the
+// launch bound so the scan over the bound yields rank[E_t] = n_{t+1}
+__global__ void k_mark(const uint32_t* __restrict__ n_edges_dev, uint32_t bound,
+                       const uint32_t* __restrict__ table, const uint32_t* __restrict__ slot_of,
+                       uint32_t* __restrict__ flag) {
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j > n_edges) return;
+    if (j > bound) return;
+    const uint32_t n_edges = *n_edges_dev;
     flag[j] = j < n_edges ? (table[slot_of[j]] == j ? 1u : 0u) : 0u;
 }
 
-__global__ void k_finalize(uint32_t n_edges, const uint32_t* __restrict__ table,
+__global__ void k_finalize(const uint32_t* __restrict__ n_edges_dev, const uint32_t* __restrict__ table,
                            const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ rank,
                            const uint64_t* __restrict__ ekeys, int words, uint32_t next_base,
                            uint32_t* __restrict__ succ, uint64_t* __restrict__ next_keys) {
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n_edges) return;
+    if (j >= *n_edges_dev) return;
     const uint32_t first = table[slot_of[j]];
     succ[j] = next_base + rank[first];
     if (first == j) {
@@ -281,13 +288,28 @@ uint64_t pow2_at_least(uint64_t n) {
     return c;
 }
 
+// Device-side layer counters written by k_counters into mapped pinned host memory, so a layer
+// needs exactly one host synchronisation (to size the next layer's launches and buffers).
+struct LayerCounters {
+    uint32_t n_edges; // E_t
+    uint32_t n_next;  // n_{t+1}
+};
+
+__global__ void k_counters(const uint32_t* __restrict__ off_end, const uint32_t* __restrict__ rank,
+                           LayerCounters* __restrict__ out) {
+    const uint32_t e = *off_end;
+    out->n_edges = e;
+    out->n_next = rank[e];
+}
+
 struct Scratch {
     DevBuf<uint32_t> deg, off, slot, flag, rank, table;
     DevBuf<uint64_t> ekeys;
     DevBuf<uint8_t> cub_tmp;
-    uint32_t* host_word = nullptr;
+    LayerCounters* counters = nullptr;     // mapped pinned host memory
+    LayerCounters* counters_dev = nullptr; // its device alias
     ~Scratch() {
-        if (host_word) cudaFreeHost(host_word);
+        if (counters) cudaFreeHost(counters);
     }
 };
 
@@ -299,30 +321,28 @@ void exclusive_scan(Scratch& sc, const uint32_t* in, uint32_t* out, uint64_t n, 
     note_launch();
 }
 
-uint32_t read_word(Scratch& sc, const uint32_t* dev, cudaStream_t s) {
-    VCS_CUDA(cudaMemcpyAsync(sc.host_word, dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    VCS_CUDA(cudaStreamSynchronize(s));
-    return *sc.host_word;
-}
-
+// Per layer: count -> scan -> emit -> insert -> mark -> scan -> finalize -> counters, with the
+// edge-side launches sized by the host-known bound E_t <= n_t * max_degree_t (the kernels read
+// the exact E_t from device memory), and ONE stream synchronisation at the end of the layer.
 template <int WM>
 void build_layers(vcs_space* sp, uint64_t state_cap) {
     const LayerPlan& pl = sp->plan;
     const int H = pl.horizon;
     cudaStream_t s = sp->stream;
     Scratch sc;
-    VCS_CUDA(cudaMallocHost(&sc.host_word, sizeof(uint32_t)));
+    VCS_CUDA(cudaHostAlloc(&sc.counters, sizeof(LayerCounters), cudaHostAllocMapped));
+    VCS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&sc.counters_dev), sc.counters, 0));
 
     sp->layer_off.assign(static_cast<size_t>(H) + 2, 0);
     sp->layer_edges.assign(static_cast<size_t>(H) + 1, 0);
     sp->key_off.assign(static_cast<size_t>(H) + 2, 0);
-    sp->keys.reserve(1u << 16, 0, s);
+    sp->keys.reserve(1u << 20, 0, s);
     VCS_CUDA(cudaMemcpyAsync(sp->keys.p, pl.init_key.data(), pl.words[0] * sizeof(uint64_t),
                              cudaMemcpyHostToDevice, s));
-    sp->row_ptr.reserve(1u << 16, 0, s);
-    sp->succ.reserve(1u << 16, 0, s);
-    sp->reward.reserve(1u << 16, 0, s);
-    sp->action.reserve(1u << 16, 0, s);
+    sp->row_ptr.reserve(1u << 20, 0, s);
+    sp->succ.reserve(1u << 20, 0, s);
+    sp->reward.reserve(1u << 20, 0, s);
+    sp->action.reserve(1u << 20, 0, s);
 
     uint64_t S = 1, E = 0, n_t = 1;
     sp->max_layer = 1;
@@ -333,6 +353,11 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
         sp->layer_off[static_cast<size_t>(t) + 1] = S;
         const uint64_t key_t = sp->key_off[static_cast<size_t>(t)];
         sp->key_off[static_cast<size_t>(t) + 1] = key_t + n_t * static_cast<uint64_t>(L.words);
+        int maxdeg = 1;
+        for (int p = 0; p < L.n_active; ++p) maxdeg += L.attr[p] ? 1 : 0;
+        const uint64_t e_ub = n_t * static_cast<uint64_t>(maxdeg); // E_t <= e_ub
+        if (E + e_ub >= 0xffffffffull)
+            raise(VCS_EINVAL, "more than 2^32-1 transitions are not supported");
 
         sc.deg.exact(n_t + 1, s);
         sc.off.exact(n_t + 1, s);
@@ -340,47 +365,49 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
                                                          sp->keys.p + key_t, L, sc.deg.p);
         VCS_LAUNCHED();
         exclusive_scan(sc, sc.deg.p, sc.off.p, n_t + 1, s);
-        const uint64_t E_t = read_word(sc, sc.off.p + n_t, s);
-        if (E + E_t >= 0xffffffffull)
-            raise(VCS_EINVAL, "more than 2^32-1 transitions are not supported");
+        const uint32_t* e_dev = sc.off.p + n_t; // exact E_t on the device
 
         const uint64_t row0 = sp->layer_off[static_cast<size_t>(t)];
         sp->row_ptr.reserve(row0 + n_t + 1, row0, s);
-        sp->succ.reserve(E + E_t, E, s);
-        sp->reward.reserve(E + E_t, E, s);
-        sp->action.reserve(E + E_t, E, s);
-        sc.ekeys.exact(E_t * static_cast<uint64_t>(L.next_words), s);
+        sp->succ.reserve(E + e_ub, E, s);
+        sp->reward.reserve(E + e_ub, E, s);
+        sp->action.reserve(E + e_ub, E, s);
+        sc.ekeys.exact(e_ub * static_cast<uint64_t>(L.next_words), s);
         k_emit<WM><<<blocks_for(n_t, T), T, 0, s>>>(
             static_cast<uint32_t>(n_t), sp->keys.p + key_t, sc.off.p, L, static_cast<uint32_t>(E),
             sp->row_ptr.p + row0, sc.ekeys.p, sp->reward.p, sp->action.p);
         VCS_LAUNCHED();
 
-        const uint64_t cap = pow2_at_least(2 * E_t);
+        const uint64_t cap = pow2_at_least(2 * e_ub);
         sc.table.exact(cap, s);
-        sc.slot.exact(E_t, s);
-        sc.flag.exact(E_t + 1, s);
-        sc.rank.exact(E_t + 1, s);
+        sc.slot.exact(e_ub, s);
+        sc.flag.exact(e_ub + 1, s);
+        sc.rank.exact(e_ub + 1, s);
         VCS_CUDA(cudaMemsetAsync(sc.table.p, 0xff, cap * sizeof(uint32_t), s));
-        k_insert<WM><<<blocks_for(E_t, T), T, 0, s>>>(static_cast<uint32_t>(E_t), sc.ekeys.p,
-                                                      L.next_words, sc.table.p,
-                                                      static_cast<uint32_t>(cap - 1), sc.slot.p);
+        k_insert<WM><<<blocks_for(e_ub, T), T, 0, s>>>(e_dev, sc.ekeys.p, L.next_words,
+                                                       sc.table.p, static_cast<uint32_t>(cap - 1),
+                                                       sc.slot.p);
         VCS_LAUNCHED();
-        k_mark<<<blocks_for(E_t + 1, T), T, 0, s>>>(static_cast<uint32_t>(E_t), sc.table.p,
-                                                    sc.slot.p, sc.flag.p);
+        k_mark<<<blocks_for(e_ub + 1, T), T, 0, s>>>(e_dev, static_cast<uint32_t>(e_ub), sc.table.p,
+                                                     sc.slot.p, sc.flag.p);
         VCS_LAUNCHED();
-        exclusive_scan(sc, sc.flag.p, sc.rank.p, E_t + 1, s);
-        const uint64_t n_next = read_word(sc, sc.rank.p + E_t, s);
+        exclusive_scan(sc, sc.flag.p, sc.rank.p, e_ub + 1, s); // zeros past E_t: rank[E_t] = n_{t+1}
+        const uint64_t key_next = sp->key_off[static_cast<size_t>(t) + 1];
+        sp->keys.reserve(key_next + e_ub * static_cast<uint64_t>(L.next_words), key_next, s);
+        k_finalize<<<blocks_for(e_ub, T), T, 0, s>>>(
+            e_dev, sc.table.p, sc.slot.p, sc.rank.p, sc.ekeys.p, L.next_words,
+            static_cast<uint32_t>(S), sp->succ.p + E, sp->keys.p + key_next);
+        VCS_LAUNCHED();
+        k_counters<<<1, 1, 0, s>>>(e_dev, sc.rank.p, sc.counters_dev);
+        VCS_LAUNCHED();
+        VCS_CUDA(cudaStreamSynchronize(s)); // the layer's single host round trip
+        const uint64_t E_t = sc.counters->n_edges;
+        const uint64_t n_next = sc.counters->n_next;
         if (S + n_next > state_cap)
             raise(VCS_ECAP, "reachable state space exceeds cap of " + std::to_string(state_cap) +
                                 " states");
         if (S + n_next >= 0xffffffffull)
             raise(VCS_EINVAL, "more than 2^32-1 states are not supported");
-        const uint64_t key_next = sp->key_off[static_cast<size_t>(t) + 1];
-        sp->keys.reserve(key_next + n_next * static_cast<uint64_t>(L.next_words), key_next, s);
-        k_finalize<<<blocks_for(E_t, T), T, 0, s>>>(
-            static_cast<uint32_t>(E_t), sc.table.p, sc.slot.p, sc.rank.p, sc.ekeys.p,
-            L.next_words, static_cast<uint32_t>(S), sp->succ.p + E, sp->keys.p + key_next);
-        VCS_LAUNCHED();
 
         sp->layer_edges[static_cast<size_t>(t)] = E_t;
         E += E_t;
@@ -388,7 +415,6 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
         n_t = n_next;
         sp->max_layer = std::max<uint64_t>(sp->max_layer, n_t);
         if (trace_enabled()) {
-            VCS_CUDA(cudaStreamSynchronize(s));
             const double now = host_ms();
             std::fprintf(stderr, "[vcs build] layer %d: n=%llu E_t=%llu  %.3f ms\n", t,
                          static_cast<unsigned long long>(n_t),

@@ -1,0 +1,55 @@
+"""Summarise an ncu --set full capture of k_wave_layer (C4, tools/prof_sweep.py) into
+profiles/ncu_wave.json: per captured launch, DRAM traffic vs the algorithmic bytes of that layer.
+
+    python tools/ncu_summary.py gpurun_out/prof_wave.ncu-rep <first_skip> [out.json]
+
+`first_skip` is the -s value used for the capture: k_wave_layer launches are numbered over
+two solves of H=48 layer launches each, layers descending (t = H-1 .. 0)."""
+import csv
+import io
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def main(rep, skip, out=None):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    lay = json.loads((ROOT / "tools" / "c4_layers.json").read_text())
+    H = lay["H"]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    launches = []
+    for j, r in enumerate(rows[2:]):
+        idx = (skip + j) % H
+        t = H - 1 - idx
+        n, e = lay["layers"][t]["n"], lay["layers"][t]["edges"]
+        n_next = lay["layers"][t + 1]["n"]
+        m = H - t
+        # per layer: row_ptr 4 + value 8 + action 4 + winner's action 4 per state, succ 4 +
+        # reward 8 per edge, versions written (8 per backup) and the successor versions read
+        # once (8 * n_{t+1} * (m-1))
+        alg = 20 * n + 12 * e + 8 * n * m + 8 * n_next * (m - 1)
+        g = lambda k: float(r[hdr.index(k)]) * scale.get(units[hdr.index(k)], 1)
+        dram = g("dram__bytes_read.sum") + g("dram__bytes_write.sum")
+        tt = float(r[hdr.index("gpu__time_duration.sum")]) * (1e-6 if units[hdr.index("gpu__time_duration.sum")] == "us" else 1e-9)
+        launches.append({"layer": t, "states": n, "edges": e, "versions": m,
+                         "alg_bytes": alg, "dram_bytes": dram, "dram_over_alg": dram / alg,
+                         "ncu_time_us": tt * 1e6, "dram_GBps": dram / tt / 1e9,
+                         "l2_hit_pct": float(r[hdr.index("lts__t_sector_hit_rate.pct")]),
+                         "warps_active_pct": float(r[hdr.index("sm__warps_active.avg.pct_of_peak_sustained_active")]),
+                         "issue_active_pct": float(r[hdr.index("smsp__issue_active.avg.pct_of_peak_sustained_active")])})
+    summary = {"kernel": "k_wave_layer<false>", "capture": f"ncu --set full, C4, launches {skip}..{skip + len(launches) - 1} of tools/prof_sweep.py",
+               "dram_bytes_per_launch": launches[0]["dram_bytes"],
+               "alg_bytes_per_launch": launches[0]["alg_bytes"], "launches": launches,
+               "note": "dram/alg = %.2f on layer %d" % (launches[0]["dram_over_alg"], launches[0]["layer"])}
+    Path(out or ROOT / "profiles" / "ncu_wave.json").write_text(json.dumps(summary, indent=1))
+    print(json.dumps(summary, indent=1)[:1500])
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], int(sys.argv[2]), sys.argv[3] if len(sys.argv) > 3 else None)
