@@ -153,6 +153,94 @@ __global__ void __launch_bounds__(32) k_first_fit(const GreedyDesc* __restrict__
     if (lane == 0) *D.paid = paid;
 }
 
+// Fast path: <= 1024 clouds (lane l owns word l: clouds 32l..32l+31) and <= 8 distinct demands.
+// The capacity words "free >= level_L" live in REGISTERS of the owning lane; per task the
+// critical path is AND -> ballot -> ffs, and only the winning lane updates its free count (in
+// shared memory, touched by that lane only) and its capacity bits.  Targets are gathered in
+// registers (lane j%32 keeps task j's) and stored 32 at a time, coalesced.
+constexpr int kFastLevels = 8;
+
+__global__ void __launch_bounds__(32) k_first_fit_fast(const GreedyDesc* __restrict__ descs) {
+    extern __shared__ int32_t sm[];
+    const GreedyDesc D = descs[blockIdx.x];
+    const int lane = threadIdx.x;
+    int32_t* fr = sm; // free counts, word-major: cloud c at fr[c]
+    for (int c = lane; c < D.K; c += 32) fr[c] = D.free_vms[c];
+    __syncwarp();
+    int lvl[kFastLevels];
+    uint32_t capw[kFastLevels];
+#pragma unroll
+    for (int L = 0; L < kFastLevels; ++L) {
+        lvl[L] = L < D.n_levels ? D.levels[L] : 0x7fffffff;
+        uint32_t bits = 0;
+        if (L < D.n_levels)
+            for (int b = 0; b < 32; ++b) {
+                const int c = lane * 32 + b;
+                if (c < D.K && fr[c] >= lvl[L]) bits |= 1u << b;
+            }
+        capw[L] = bits;
+    }
+    long long paid = 0;
+    int my_target = -1;
+    uint32_t cur[kPrefetch], nxt[kPrefetch];
+    int2 tcur[kPrefetch], tnxt[kPrefetch];
+#pragma unroll
+    for (int u = 0; u < kPrefetch; ++u) {
+        cur[u] = (u < D.T && lane < D.W) ? __ldg(D.mask + static_cast<size_t>(u) * D.W + lane) : 0u;
+        tcur[u] = u < D.T ? __ldg(D.task + u) : make_int2(0, 0);
+    }
+    for (int j0 = 0; j0 < D.T; j0 += kPrefetch) {
+#pragma unroll
+        for (int u = 0; u < kPrefetch; ++u) { // next batch in flight while this one is scanned
+            const int j = j0 + kPrefetch + u;
+            nxt[u] = (j < D.T && lane < D.W) ? __ldg(D.mask + static_cast<size_t>(j) * D.W + lane) : 0u;
+            tnxt[u] = j < D.T ? __ldg(D.task + j) : make_int2(0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < kPrefetch; ++u) {
+            const int j = j0 + u;
+            if (j < D.T) {
+                const int level = tcur[u].x, d = tcur[u].y;
+                uint32_t c = 0;
+#pragma unroll
+                for (int L = 0; L < kFastLevels; ++L) c = L == level ? capw[L] : c;
+                const uint32_t m = cur[u] & c;
+                const uint32_t any = __ballot_sync(0xffffffffu, m != 0);
+                int winner = -1;
+                if (any) {
+                    const int src = __ffs(any) - 1;
+                    if (lane == src) { // the owning lane updates its free count and bits
+                        const int b = __ffs(m) - 1;
+                        const int cloud = lane * 32 + b;
+                        const int f = fr[cloud] - d;
+                        fr[cloud] = f;
+                        const uint32_t bit = 1u << b;
+#pragma unroll
+                        for (int L = 0; L < kFastLevels; ++L)
+                            capw[L] = f >= lvl[L] ? (capw[L] | bit) : (capw[L] & ~bit);
+                        winner = cloud;
+                    }
+                    winner = __shfl_sync(0xffffffffu, winner, src);
+                } else {
+                    paid += d;
+                }
+                if (lane == (j & 31)) my_target = winner;
+                if ((j & 31) == 31) D.target[j - 31 + lane] = my_target;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kPrefetch; ++u) {
+            cur[u] = nxt[u];
+            tcur[u] = tnxt[u];
+        }
+    }
+    const int tail = D.T & 31; // the last partial group of 32 targets
+    if (tail && lane < tail) D.target[D.T - tail + lane] = my_target;
+    __syncwarp();
+    for (int c = lane; c < D.K; c += 32) D.free_vms[c] = fr[c];
+    if (lane == 0) *D.paid = paid;
+}
+
 struct HostGreedy {
     int K, T, W, n_levels;
     std::vector<int2> task;
@@ -235,10 +323,22 @@ GreedyDesc desc_of(const HostGreedy& h, GreedyDev& g) {
                       g.free_vms.p, g.target.p, g.paid.p};
 }
 
-void launch_first_fit(const GreedyDesc* d_descs, int n, size_t smem, cudaStream_t s) {
-    VCS_CUDA(cudaFuncSetAttribute(k_first_fit, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(std::max<size_t>(smem, 1))));
-    k_first_fit<<<n, 32, std::max<size_t>(smem, 4), s>>>(d_descs);
+bool fast_path(const HostGreedy& h) {
+    return h.W <= 32 && h.n_levels > 0 && h.n_levels <= kFastLevels;
+}
+
+void launch_first_fit(const GreedyDesc* d_descs, int n, size_t smem, bool fast, size_t max_k,
+                      cudaStream_t s) {
+    if (fast) {
+        const size_t fs = std::max<size_t>(max_k * 4, 4);
+        VCS_CUDA(cudaFuncSetAttribute(k_first_fit_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(fs)));
+        k_first_fit_fast<<<n, 32, fs, s>>>(d_descs);
+    } else {
+        VCS_CUDA(cudaFuncSetAttribute(k_first_fit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(std::max<size_t>(smem, 1))));
+        k_first_fit<<<n, 32, std::max<size_t>(smem, 4), s>>>(d_descs);
+    }
     VCS_LAUNCHED();
 }
 
@@ -268,7 +368,7 @@ int vcs_greedy(const vcs_instance* in, int device, int32_t* target_per_task,
         dd.exact(1, s);
         const vcs::GreedyDesc desc = vcs::desc_of(h, g);
         VCS_CUDA(cudaMemcpyAsync(dd.p, &desc, sizeof desc, cudaMemcpyHostToDevice, s));
-        vcs::launch_first_fit(dd.p, 1, h.smem, s);
+        vcs::launch_first_fit(dd.p, 1, h.smem, vcs::fast_path(h), static_cast<size_t>(h.K), s);
         std::vector<int32_t> free_out(static_cast<size_t>(h.K));
         long long p = 0;
         if (h.T)
@@ -306,7 +406,8 @@ int vcs_greedy_batch(int32_t n, const vcs_instance* insts, int device, int32_t**
         std::vector<vcs::HostGreedy> hs;
         std::vector<std::unique_ptr<vcs::GreedyDev>> gs;
         std::vector<vcs::GreedyDesc> descs;
-        size_t smem = 4;
+        size_t smem = 4, max_k = 1;
+        bool fast = true;
         const int sms = vcs::sm_count(device);
         for (int i = 0; i < n; ++i) {
             hs.push_back(vcs::plan_greedy(&insts[i]));
@@ -315,12 +416,14 @@ int vcs_greedy_batch(int32_t n, const vcs_instance* insts, int device, int32_t**
             vcs::launch_mask(hs.back(), *gs.back(), sms, s);
             descs.push_back(vcs::desc_of(hs.back(), *gs.back()));
             smem = std::max(smem, hs.back().smem);
+            max_k = std::max(max_k, static_cast<size_t>(hs.back().K));
+            fast = fast && vcs::fast_path(hs.back());
         }
         vcs::DevBuf<vcs::GreedyDesc> dd;
         dd.exact(static_cast<size_t>(n), s);
         VCS_CUDA(cudaMemcpyAsync(dd.p, descs.data(), descs.size() * sizeof(vcs::GreedyDesc),
                                  cudaMemcpyHostToDevice, s));
-        vcs::launch_first_fit(dd.p, n, smem, s);
+        vcs::launch_first_fit(dd.p, n, smem, fast, max_k, s);
         std::vector<std::vector<int32_t>> frees(static_cast<size_t>(n));
         std::vector<long long> ps(static_cast<size_t>(n), 0);
         for (int i = 0; i < n; ++i) {
