@@ -101,6 +101,7 @@ struct GraphKey {
 struct CachedGraph {
     cudaGraphExec_t exec = nullptr;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    std::vector<cudaEvent_t> layer_ev; // wavefront: after layer t's kernel (timing disabled)
     int n_sweeps = 0; // sweep kernels in the graph
     int launches = 0;
     int method = kMethodJacobi;
@@ -112,6 +113,7 @@ struct CachedGraph {
 struct vcs_space {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t d2h_stream = nullptr; // result copies overlapped with the layer pass
     uint64_t S = 0, E = 0;
     int H = 0;
     int max_degree = 1;

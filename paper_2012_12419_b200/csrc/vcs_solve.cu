@@ -727,6 +727,9 @@ void record_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
         layer_fn<<<static_cast<unsigned>(blocks), kWaveWarps * 32, smem, s>>>(a);
         VCS_LAUNCHED();
         ++launches;
+        // layer t's values/actions are final here (unless an early stop needs the fix-up):
+        // lets vcs_solve stream them to the host while the remaining layers compute
+        record_event(g.layer_ev[static_cast<size_t>(t)], s, capturing);
     }
     record_event(g.ev[1], s, capturing);
     int per_sm_ext = 0;
@@ -787,6 +790,8 @@ CachedGraph& enqueue_solve(vcs_space* sp, const GraphKey& key, cudaStream_t s) {
         g.method = key.method;
         g.n_sweeps = key.max_sweeps;
         for (auto& e : g.ev) VCS_CUDA(cudaEventCreate(&e));
+        g.layer_ev.assign(static_cast<size_t>(std::max(0, sp->H)), nullptr);
+        for (auto& e : g.layer_ev) VCS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         it = sp->graphs.emplace(key, g).first;
     }
     CachedGraph& g = it->second;
@@ -864,11 +869,63 @@ int vcs_solve_enqueue(vcs_space* sp, const vcs_solve_opts* opts, void* stream) {
     });
 }
 
+namespace {
+bool is_pinned(const void* p) {
+    if (!p) return true;
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return attr.type == cudaMemoryTypeHost;
+}
+} // namespace
+
 int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int32_t* actions_out,
               vcs_solve_report* report) {
     const int rc = vcs_solve_enqueue(sp, opts, nullptr);
     if (rc != VCS_OK) return rc;
-    return vcs_solve_collect(sp, values_out, actions_out, report, nullptr);
+    const vcs::CachedGraph& g = *sp->last_graph;
+    const bool overlap = g.method == vcs::kMethodWavefront && !g.layer_ev.empty() &&
+                         (values_out || actions_out) && is_pinned(values_out) &&
+                         is_pinned(actions_out);
+    if (!overlap) return vcs_solve_collect(sp, values_out, actions_out, report, nullptr);
+    // Stream each layer's values/actions to the (pinned) host buffers as soon as its layer
+    // kernel finished — the 12 B/state download overlaps the rest of the layer pass.
+    const int rc2 = guarded([&] {
+        if (!sp->d2h_stream)
+            VCS_CUDA(cudaStreamCreateWithFlags(&sp->d2h_stream, cudaStreamNonBlocking));
+        cudaStream_t d = sp->d2h_stream;
+        auto copy_rows = [&](uint64_t r0, uint64_t r1, cudaStream_t st) {
+            if (r1 <= r0) return;
+            if (values_out)
+                VCS_CUDA(cudaMemcpyAsync(values_out + r0, sp->v[0].p + r0, (r1 - r0) * sizeof(double),
+                                         cudaMemcpyDeviceToHost, st));
+            if (actions_out)
+                VCS_CUDA(cudaMemcpyAsync(actions_out + r0, sp->actions_dev.p + r0,
+                                         (r1 - r0) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        };
+        VCS_CUDA(cudaStreamWaitEvent(d, g.ev[0], 0)); // terminal layer: set at the solve's start
+        copy_rows(sp->layer_off[sp->H], sp->S, d);
+        for (int t = sp->H - 1; t >= 0; --t) {
+            VCS_CUDA(cudaStreamWaitEvent(d, g.layer_ev[static_cast<size_t>(t)], 0));
+            copy_rows(sp->layer_off[t], sp->layer_off[t + 1], d);
+        }
+        vcs_solve_report local{};
+        vcs_solve_report* rep = report ? report : &local;
+        const int rc3 = vcs_solve_collect(sp, nullptr, nullptr, rep, nullptr);
+        if (rc3 != VCS_OK) vcs::raise(rc3, vcs_last_error());
+        // an early stop (K* < H) rewrote the prefix of layers t < H - K* after their events
+        const int K = rep->sweeps;
+        if (sp->H - K > 0) {
+            VCS_CUDA(cudaStreamSynchronize(d));
+            copy_rows(0, sp->layer_off[sp->H - K], sp->stream);
+            VCS_CUDA(cudaStreamSynchronize(sp->stream));
+        }
+        VCS_CUDA(cudaStreamSynchronize(d));
+        return VCS_OK;
+    });
+    return rc2;
 }
 
 int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,

@@ -519,7 +519,10 @@ vcs_space::~vcs_space() {
         if (g.exec) cudaGraphExecDestroy(g.exec);
         for (auto& e : g.ev)
             if (e) cudaEventDestroy(e);
+        for (auto& e : g.layer_ev)
+            if (e) cudaEventDestroy(e);
     }
+    if (d2h_stream) cudaStreamDestroy(d2h_stream);
     // stream-ordered frees must be issued while the stream is alive
     row_ptr.release();
     succ.release();

@@ -170,6 +170,31 @@ def test_capped_sweeps_match_oracle(gpu, oracle):
             assert np.array_equal(acts, a)
 
 
+def test_pinned_outputs_overlapped_download(gpu, golden):
+    """vcs_solve into PINNED host buffers streams each layer's results while the wavefront
+    runs; an early stop (eps = 5, 0.5) rewrites a prefix afterwards — both must be exact."""
+    import torch
+    p = V.load_instance(str(GOLDEN / "canonical_instance.txt"))
+    ni = V.NativeInstance(p.vcc, bots=p.bots)
+    sp = V.StateSpace.build_native(ni)
+    S = sp.size()
+    vals = torch.empty(S, dtype=torch.float64, pin_memory=True)
+    acts = torch.empty(S, dtype=torch.int32, pin_memory=True)
+    vp = C.cast(C.c_void_p(vals.data_ptr()), C.POINTER(C.c_double))
+    ap = C.cast(C.c_void_p(acts.data_ptr()), C.POINTER(C.c_int32))
+    for eps in (1e-6, 5.0, 0.5):
+        g = golden["cases"]["canonical"][f"eps={eps:g}"]
+        for _ in range(2):  # first solve captures the graph, the second replays it
+            vals.fill_(float("nan"))
+            acts.fill_(-7)
+            opts = N.vcs_solve_opts(eps, 1, 0, 1.0, N.VCS_METHOD_WAVEFRONT)
+            rep = N.vcs_solve_report()
+            N.check(N.lib().vcs_solve(sp.handle, C.byref(opts), vp, ap, C.byref(rep)))
+            assert rep.sweeps == g["sweeps"]
+            assert sha(vals.numpy()) == g["values_sha"]
+            assert sha(acts.numpy()) == g["actions_sha"]
+
+
 def test_state_cap_error(gpu):
     """test_mdp.cpp:248-259."""
     vcc, bots = tiny(6, [1] * 6)
