@@ -9,7 +9,7 @@ SRC       := $(PKG)/csrc
 OBJ       := build/obj
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
-CXXFLAGS  := -O2 -std=c++17 -fPIC -Wall -Wextra -I$(CUDA)/include
+CXXFLAGS  := -O2 -std=c++17 -fPIC -Wall -Wextra -ffp-contract=off -I$(CUDA)/include
 REF       ?= /root/reference/proj
 JSON_INC  ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
 

@@ -297,6 +297,7 @@ LayerPlan make_layer_plan(const vcs_instance* in) {
             cur += w;
         }
         const int words = std::max(1, (cur + 63) / 64);
+        pl.key_bits.push_back(cur);
         if (words > kMaxKeyWords)
             raise(VCS_EINVAL, "reduced state key wider than " + std::to_string(kMaxKeyWords * 64) +
                                   " bits is not supported");
@@ -316,6 +317,9 @@ LayerPlan make_layer_plan(const vcs_instance* in) {
         L.r_cloud = in->beta_vc * n;  // mdp.cpp:191 first product
         L.r_paid = -in->beta_tc * n;  // mdp.cpp:202 first product
         L.gamma = in->gamma_vc;
+        // the full reward expression with nothing retired (same two rounded operations)
+        L.r_cloud_kept = L.r_cloud - L.gamma * 0.0;
+        L.r_paid_kept = L.r_paid - L.gamma * 0.0;
         int kept = 0;
         for (std::size_t p = 0; p < act.size(); ++p) {
             const int c = act[p];

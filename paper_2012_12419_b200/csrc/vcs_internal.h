@@ -65,6 +65,8 @@ struct LayerParam {
     double r_cloud;              // beta_vc * demand      (host IEEE multiply, = reference bits)
     double r_paid;               // -beta_tc * demand
     double gamma;                // penalty_per_idle_vm
+    double r_cloud_kept;         // r_cloud - gamma * 0.0: reward when nothing retires
+    double r_paid_kept;          // r_paid  - gamma * 0.0
     int32_t cloud[kMaxActive];   // cloud index of key position p
     int8_t attr[kMaxActive];     // attr_ok[cloud[p]][t]
     int8_t keep_idx[kMaxActive]; // position in the next key, -1 = retired at this transition
@@ -80,6 +82,7 @@ struct LayerPlan {
     std::vector<std::vector<int>> active; // per layer 0..H
     std::vector<LayerParam> layers;       // per layer 0..H-1 (transition t -> t+1)
     std::vector<int> words;               // packed key words per layer 0..H
+    std::vector<int> key_bits;            // used bits of the packed key per layer 0..H
     std::vector<std::vector<uint16_t>> bit_off; // per layer: bit offsets of active fields
     std::vector<int> width_of_cloud;      // bit width per cloud
     std::vector<uint64_t> init_key;       // packed layer-0 key

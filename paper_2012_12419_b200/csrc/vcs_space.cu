@@ -137,6 +137,30 @@ __global__ void k_emit(uint32_t n, const uint64_t* __restrict__ keys,
     load_key<WM>(keys + static_cast<uint64_t>(i) * L.words, L.words, k);
     uint32_t j = off[i];
     row_ptr_layer[i] = edge_base + j;
+    if (L.n_keep == L.n_active) {
+        // No cloud retires at this transition (the common case): the next key has the same
+        // layout, a cloud action subtracts the demand from its own field, nothing is charged
+        // (reward = base - gamma * 0.0, evaluated on the host with the same two IEEE ops).
+        for (int p = 0; p < L.n_active; ++p) {
+            if (!L.attr[p] || get_field<WM>(k, L.bit_off[p], L.width[p]) < L.demand) continue;
+            uint64_t* ek = ekeys + static_cast<uint64_t>(j) * L.next_words;
+            const int w = L.bit_off[p] >> 6;
+            const uint64_t sub = static_cast<uint64_t>(L.demand) << (L.bit_off[p] & 63);
+#pragma unroll
+            for (int q = 0; q < WM; ++q)
+                if (q < L.next_words) ek[q] = q == w ? k[q] - sub : k[q];
+            reward[edge_base + j] = L.r_cloud_kept;
+            action[edge_base + j] = L.cloud[p];
+            ++j;
+        }
+        uint64_t* ek = ekeys + static_cast<uint64_t>(j) * L.next_words;
+#pragma unroll
+        for (int q = 0; q < WM; ++q)
+            if (q < L.next_words) ek[q] = k[q];
+        reward[edge_base + j] = L.r_paid_kept;
+        action[edge_base + j] = -1;
+        return;
+    }
     for (int p = 0; p < L.n_active; ++p) {
         if (!L.attr[p] || get_field<WM>(k, L.bit_off[p], L.width[p]) < L.demand) continue;
         emit_edge<WM>(k, p, L, ekeys + static_cast<uint64_t>(j) * L.next_words,
@@ -176,6 +200,29 @@ __global__ void k_insert(const uint32_t* __restrict__ n_edges_dev, const uint64_
         }
         h = (h + 1) & mask;
     }
+}
+
+// Single-word keys narrower than 64 bits (so ~0 is never a key): the table stores the key next
+// to the first-edge index, so an insert never re-reads another edge's key.
+constexpr uint64_t kEmptyKey = ~0ull;
+
+__global__ void k_insert_kv(const uint32_t* __restrict__ n_edges_dev,
+                            const uint64_t* __restrict__ ekeys, unsigned long long* __restrict__ tkey,
+                            uint32_t* __restrict__ tidx, uint32_t mask,
+                            uint32_t* __restrict__ slot_of) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= *n_edges_dev) return;
+    const uint64_t k = ekeys[j];
+    uint64_t kk[1] = {k};
+    uint32_t h = static_cast<uint32_t>(hash_key<1>(kk, 1, 0)) & mask;
+    for (;;) {
+        unsigned long long cur = tkey[h];
+        if (cur == kEmptyKey) cur = atomicCAS(&tkey[h], kEmptyKey, static_cast<unsigned long long>(k));
+        if (cur == kEmptyKey || cur == k) break; // claimed the slot, or the key is already there
+        h = (h + 1) & mask;
+    }
+    if (tidx[h] > j) atomicMin(&tidx[h], j); // the first occurrence (lowest edge index) wins
+    slot_of[j] = h;
 }
 
 // flag[j] = 1 iff edge j is the first occurrence of its successor; zeros past E_t up to the
@@ -304,7 +351,7 @@ __global__ void k_counters(const uint32_t* __restrict__ off_end, const uint32_t*
 
 struct Scratch {
     DevBuf<uint32_t> deg, off, slot, flag, rank, table;
-    DevBuf<uint64_t> ekeys;
+    DevBuf<uint64_t> ekeys, tkey;
     DevBuf<uint8_t> cub_tmp;
     LayerCounters* counters = nullptr;     // mapped pinned host memory
     LayerCounters* counters_dev = nullptr; // its device alias
@@ -384,9 +431,17 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
         sc.flag.exact(e_ub + 1, s);
         sc.rank.exact(e_ub + 1, s);
         VCS_CUDA(cudaMemsetAsync(sc.table.p, 0xff, cap * sizeof(uint32_t), s));
-        k_insert<WM><<<blocks_for(e_ub, T), T, 0, s>>>(e_dev, sc.ekeys.p, L.next_words,
-                                                       sc.table.p, static_cast<uint32_t>(cap - 1),
-                                                       sc.slot.p);
+        if (L.next_words == 1 && pl.key_bits[static_cast<size_t>(t) + 1] < 64) {
+            sc.tkey.exact(cap, s);
+            VCS_CUDA(cudaMemsetAsync(sc.tkey.p, 0xff, cap * sizeof(uint64_t), s));
+            k_insert_kv<<<blocks_for(e_ub, T), T, 0, s>>>(
+                e_dev, sc.ekeys.p, reinterpret_cast<unsigned long long*>(sc.tkey.p), sc.table.p,
+                static_cast<uint32_t>(cap - 1), sc.slot.p);
+        } else {
+            k_insert<WM><<<blocks_for(e_ub, T), T, 0, s>>>(e_dev, sc.ekeys.p, L.next_words,
+                                                           sc.table.p, static_cast<uint32_t>(cap - 1),
+                                                           sc.slot.p);
+        }
         VCS_LAUNCHED();
         k_mark<<<blocks_for(e_ub + 1, T), T, 0, s>>>(e_dev, static_cast<uint32_t>(e_ub), sc.table.p,
                                                      sc.slot.p, sc.flag.p);
