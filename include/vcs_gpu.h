@@ -226,6 +226,31 @@ int vcs_shard_finish(vcs_space* sp, int32_t n_sweeps, uint64_t row_begin, uint64
                      const vcs_solve_opts* opts, double* values_out, int32_t* actions_out,
                      int32_t* sweeps_out, void* stream);
 
+/* Version-band sharding of the layer wavefront (the multi-GPU form of VCS_METHOD_WAVEFRONT).
+ * Rank r of `world` computes versions [lo_t, hi_t) = [1 + r*m_t/world, 1 + (r+1)*m_t/world) of
+ * every layer t (m_t = horizon - t, integer division).  Its band of layer t needs only its own
+ * band of layer t+1 plus ONE column below it (version lo_{t+1}-1, owned by a lower rank), so
+ * the per-layer exchange is one n_t-double column per rank.  Host driver (one process per GPU):
+ *   begin(world, rank, opts, delta)      delta: caller-owned device array of horizon+3 doubles
+ *   for t = horizon-1 .. 0:
+ *       layer(t)                          the rank's band of layer t
+ *       for every rank d with lo_t(d) > 1: owner q of version lo_t(d)-1 packs it (pack) and
+ *                                         sends n_t doubles to d, which unpacks it (unpack)
+ *   all-reduce(delta, MAX); K* = first k with delta[k] < eps (else horizon+1)
+ *   finish(K*)                            early-stop fix-up + this rank's rows to the host
+ * The results are bit-identical to vcs_solve for every world size.  Replaces the same
+ * block-parallel worker (parallel_vi.cpp:68-107) as vcs_shard_*, with the wavefront's work. */
+int vcs_wave_shard_begin(vcs_space* sp, int32_t world, int32_t rank, const vcs_solve_opts* opts,
+                         double* delta, void* stream);
+int vcs_wave_shard_band(const vcs_space* sp, int32_t t, int32_t* lo, int32_t* hi);
+int vcs_wave_shard_layer(vcs_space* sp, int32_t t, void* stream);
+int vcs_wave_shard_pack(vcs_space* sp, int32_t t, int32_t version, double* dst, void* stream);
+int vcs_wave_shard_unpack(vcs_space* sp, int32_t t, const double* src, void* stream);
+/* values_out / actions_out: host arrays of n_states; this rank writes exactly the rows it is
+ * responsible for (every row is written by one rank), the rest is left untouched. */
+int vcs_wave_shard_finish(vcs_space* sp, int32_t K, double* values_out, int32_t* actions_out,
+                          void* stream);
+
 /* ------------------------------------------------------------------------------------------ */
 /* Greedy placement (device)                                                                   */
 /* ------------------------------------------------------------------------------------------ */

@@ -28,6 +28,8 @@ EXPORTS = (
     "vcs_space_layer_edges", "vcs_space_csr", "vcs_space_locate", "vcs_space_hidden_penalty",
     "vcs_space_free",
     "vcs_solve", "vcs_solve_enqueue", "vcs_solve_collect", "vcs_shard_plan", "vcs_shard_begin", "vcs_shard_sweep", "vcs_shard_finish",
+    "vcs_wave_shard_begin", "vcs_wave_shard_band", "vcs_wave_shard_layer", "vcs_wave_shard_pack",
+    "vcs_wave_shard_unpack", "vcs_wave_shard_finish",
     "vcs_greedy", "vcs_greedy_batch", "vcs_greedy_reward",
     "vcs_last_error", "vcs_kernel_launches", "vcs_device_count",
 )
@@ -164,6 +166,13 @@ _SIGS = {
                                   C.POINTER(vcs_solve_opts), _P]),
     "vcs_shard_finish": (C.c_int, [_P, C.c_int32, C.c_uint64, C.c_uint64,
                                    C.POINTER(vcs_solve_opts), _F64P, _I32P, _I32P, _P]),
+    "vcs_wave_shard_begin": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(vcs_solve_opts), _P,
+                                       _P]),
+    "vcs_wave_shard_band": (C.c_int, [_P, C.c_int32, _I32P, _I32P]),
+    "vcs_wave_shard_layer": (C.c_int, [_P, C.c_int32, _P]),
+    "vcs_wave_shard_pack": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P]),
+    "vcs_wave_shard_unpack": (C.c_int, [_P, C.c_int32, _P, _P]),
+    "vcs_wave_shard_finish": (C.c_int, [_P, C.c_int32, _F64P, _I32P, _P]),
     "vcs_greedy": (C.c_int, [_INSTP, C.c_int, _I32P, _I64P, _I64P, _I64P]),
     "vcs_greedy_batch": (C.c_int, [C.c_int32, _INSTP, C.c_int, C.POINTER(_I32P), _I64P, _I64P]),
     "vcs_greedy_reward": (C.c_double, [_INSTP, C.c_int64, C.c_int64, C.c_int64]),

@@ -145,6 +145,13 @@ struct vcs_space {
     std::map<vcs::GraphKey, vcs::CachedGraph> graphs;
     vcs::CachedGraph* last_graph = nullptr; // graph of the last vcs_solve_enqueue
     int last_key_skip = 1;
+    // version-band sharded wavefront (vcs_wave_shard_*): this rank's band per layer
+    int wave_world = 0, wave_rank = 0;
+    double wave_eps = 1e-6, wave_discount = 1.0;
+    std::vector<int> band_lo, band_hi, band_base, band_stride; // per layer 0..H
+    std::vector<uint64_t> band_off;                             // per layer 0..H+1 (doubles)
+    vcs::DevBuf<double> band_ver;                               // the rank's band store
+    double* wave_delta = nullptr;                               // caller-owned residuals (H+3)
     double* shard_v0 = nullptr; // caller-owned device buffers of the sharded driver
     double* shard_v1 = nullptr;
     double* shard_delta = nullptr;

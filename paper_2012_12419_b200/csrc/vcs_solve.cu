@@ -305,6 +305,10 @@ struct WaveArgs {
     uint64_t row0, n, next_row0; // layer t: first flat state, size; layer t+1 first state
     uint64_t voff, voff_next;    // version offsets of layers t and t+1
     int m;                       // versions of layer t  (H - t)
+    int band_lo, band_hi;        // versions [band_lo, band_hi) computed for layer t
+    int next_lo;                 // band_lo of layer t+1
+    int base, base_next;         // storage slot of version v in layer t (t+1) is v - base;
+                                 // the bases keep the consumer's double2 loads 16B-aligned
     int tile;                    // states per block tile
     int stride, stride_next;     // stored version-vector strides of layers t and t+1
     int max_deg;                 // edge slots per state in the tile's shared-memory CSR
@@ -313,32 +317,37 @@ struct WaveArgs {
 };
 
 // One block per tile of T consecutive states of layer t:
-//   phase 1: the tile's CSR rows (row_ptr, succ, reward) -> shared memory, coalesced;
-//   phase 2: thread (j, g) of a pass computes versions k = 2g+1, 2g+2 of state j of the pass:
-//            per edge one shared-memory read of (succ, reward) and ONE aligned 16-byte load of
-//            the successor's V_{2g}, V_{2g+1} (version vectors are stored V_0..V_m with an even
-//            stride); the gathers of up to 8 edges are in flight together; then the strict
-//            first maximum per version.  The thread holding k = m_t (the exact value) also records the argmax —
-//            that IS the extraction of s whenever K* >= m_t;
+//   phase 1: the tile's CSR rows (row_ptr, succ, reward, action) -> shared memory, coalesced;
+//   phase 2: thread (j, g) of a pass computes versions k = a+2g, a+2g+1 of state j of the pass
+//            (the rank's version band [a, b) of this layer; single GPU: [1, m_t+1)): per edge
+//            one shared-memory read of (succ, reward) and ONE aligned 16-byte load of the
+//            successor's V_{k-1}, V_k (band vectors are stored from version a-1 with an even
+//            stride, band starts are odd); the gathers of up to U edges are in flight
+//            together; then the strict first maximum per version.  The thread holding k = m_t
+//            (the exact value) also records the argmax — that IS the extraction of s whenever
+//            K* >= m_t;
 //   phase 3: residuals |V_k - V_{k-1}| (a thread's k's are fixed: register running maxima).
+//            For k = a the predecessor V_{a-1} is V_0 = 0 when a = 1; otherwise it is the
+//            halo column another rank computes, and k_band_low_delta folds it in later.
 template <bool DISC, int U, int MINB>
 __global__ void __launch_bounds__(kWaveWarps * 32, MINB) k_wave_layer(WaveArgs a) {
     constexpr int P = 2; // versions per thread (one aligned double2 gather per edge)
     // U: edges whose gathers are issued together; MINB: resident blocks per SM (register cap)
     extern __shared__ unsigned long long smem_u64[];
-    const int m = a.m;
+    const int lo = a.band_lo;                    // first version computed (odd)
+    const int nb = a.band_hi - a.band_lo;        // versions computed per state
     const int T = a.tile;
-    const int m1 = m + 1;                                            // V_0..V_m per state
-    unsigned long long* sdelta = smem_u64;                           // [m]
-    double* sout = reinterpret_cast<double*>(smem_u64 + m);          // [T*(m+1)]
-    double* srew = sout + static_cast<size_t>(T) * m1;               // [T*max_deg]
+    const int w1 = nb + 1;                       // shared slots per state: V_{lo-1} .. V_{hi-1}
+    unsigned long long* sdelta = smem_u64;                           // [nb]
+    double* sout = reinterpret_cast<double*>(smem_u64 + nb);         // [T*(nb+1)]
+    double* srew = sout + static_cast<size_t>(T) * w1;               // [T*max_deg]
     uint32_t* ssucc = reinterpret_cast<uint32_t*>(srew + static_cast<size_t>(T) * a.max_deg);
     int32_t* sact = reinterpret_cast<int32_t*>(ssucc + static_cast<size_t>(T) * a.max_deg);
     uint32_t* srp = reinterpret_cast<uint32_t*>(sact + static_cast<size_t>(T) * a.max_deg); // [T+1]
     const int tid = threadIdx.x;
     const int nthr = blockDim.x;
-    for (int k = tid; k < m; k += nthr) sdelta[k] = 0ull;
-    const int G = (m + P - 1) / P;                 // thread groups per state (P versions each)
+    for (int j = tid; j < nb; j += nthr) sdelta[j] = 0ull;
+    const int G = (nb + P - 1) / P;                // thread groups per state (P versions each)
     const bool wide = G > nthr;                    // groups loop in strides of nthr
     const int spp = wide ? 1 : nthr / G;           // states per pass
     const int my_s = wide ? 0 : tid / G;
@@ -346,6 +355,9 @@ __global__ void __launch_bounds__(kWaveWarps * 32, MINB) k_wave_layer(WaveArgs a
     const bool active = wide || my_s < spp;
     const uint32_t sn = static_cast<uint32_t>(a.stride_next); // stored stride of layer t+1
     const uint64_t st = static_cast<uint64_t>(a.stride);       // stored stride of layer t
+    // successor slot of version (k-1) is k-1-base_next; for k = lo + gP it is even (aligned)
+    const uint32_t nshift = static_cast<uint32_t>(lo - 1 - a.base_next);
+    const int oshift = lo - a.base; // own storage slot of version lo + j is j + oshift
     const double* vn = a.ver + a.voff_next;
     const uint32_t nbase = static_cast<uint32_t>(a.next_row0);
     const uint64_t n_tiles = (a.n + T - 1) / T;
@@ -395,18 +407,19 @@ __global__ void __launch_bounds__(kWaveWarps * 32, MINB) k_wave_layer(WaveArgs a
                         best[p] = -INFINITY;
                         best_e[p] = -1;
                     }
+                    const uint32_t nslot = nshift + static_cast<uint32_t>(g * P);
                     for (int eo = eb; eo < ee; eo += U) {
                         double2 x[U]; // all of the round's gathers in flight together
 #pragma unroll
                         for (int u = 0; u < U; ++u)
                             if (eo + u < ee)
                                 x[u] = __ldg(reinterpret_cast<const double2*>(
-                                    vn + (ssucc[eo + u] * sn + static_cast<uint32_t>(g * P))));
+                                    vn + (ssucc[eo + u] * sn + nslot)));
 #pragma unroll
                         for (int u = 0; u < U; ++u)
                             if (eo + u < ee) {
                                 const double r = srew[eo + u];
-                                const double v[P] = {x[u].x, x[u].y}; // V_{2g}, V_{2g+1}
+                                const double v[P] = {x[u].x, x[u].y}; // V_{k-1} of both versions
 #pragma unroll
                                 for (int p = 0; p < P; ++p) {
                                     const double q = DISC ? __dadd_rn(r, __dmul_rn(a.discount, v[p]))
@@ -419,18 +432,18 @@ __global__ void __launch_bounds__(kWaveWarps * 32, MINB) k_wave_layer(WaveArgs a
                             }
                     }
                     double* o = out + sl * st;
-                    double* so = sout + sl * m1;
-                    if (g == 0) {
-                        o[0] = 0.0; // V_0 (the initial iterate) is stored for aligned reads
+                    double* so = sout + sl * w1;
+                    if (g == 0 && lo == 1) {
+                        o[oshift - 1] = 0.0; // V_0 (the initial iterate), stored for aligned reads
                         so[0] = 0.0;
                     }
 #pragma unroll
                     for (int p = 0; p < P; ++p) {
-                        const int k = g * P + 1 + p;
-                        if (k <= m) {
-                            o[k] = best[p];
-                            so[k] = best[p];
-                            if (k == m) { // exact value: V_{K*}(s) and the policy if K* >= m_t
+                        const int j = g * P + p; // version k = lo + j
+                        if (j < nb) {
+                            o[j + oshift] = best[p];
+                            so[j + 1] = best[p];
+                            if (lo + j == a.m) { // exact value: V_{K*}(s) and the policy
                                 const uint64_t s = a.row0 + s0 + sl;
                                 a.values_out[s] = best[p];
                                 a.act_out[s] = best_e[p] >= 0 ? sact[best_e[p]] : -1;
@@ -444,16 +457,16 @@ __global__ void __launch_bounds__(kWaveWarps * 32, MINB) k_wave_layer(WaveArgs a
         if (active) {
             for (int sl = my_s; sl < nt; sl += spp)
                 for (int g = my_g0; g < G; g += nthr) {
-                    const double* so = sout + sl * m1;
+                    const double* so = sout + sl * w1;
 #pragma unroll
                     for (int p = 0; p < P; ++p) {
-                        const int k = g * P + 1 + p;
-                        if (k <= m) {
-                            const double d = fabs(so[k] - so[k - 1]);
+                        const int j = g * P + p;
+                        if (j < nb && (j > 0 || lo == 1)) {
+                            const double d = fabs(so[j + 1] - so[j]);
                             if (!wide) {
                                 dmax[p] = dmax[p] < d ? d : dmax[p];
                             } else if (d > 0.0) {
-                                atomicMax(&sdelta[k - 1],
+                                atomicMax(&sdelta[j],
                                           static_cast<unsigned long long>(__double_as_longlong(d)));
                             }
                         }
@@ -464,14 +477,14 @@ __global__ void __launch_bounds__(kWaveWarps * 32, MINB) k_wave_layer(WaveArgs a
     if (!wide && active) {
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-            const int k = my_g0 * P + 1 + p;
-            if (k <= m && dmax[p] > 0.0)
-                atomicMax(&sdelta[k - 1], static_cast<unsigned long long>(__double_as_longlong(dmax[p])));
+            const int j = my_g0 * P + p;
+            if (j < nb && dmax[p] > 0.0)
+                atomicMax(&sdelta[j], static_cast<unsigned long long>(__double_as_longlong(dmax[p])));
         }
     }
     __syncthreads();
-    for (int k = tid; k < m; k += nthr)
-        if (sdelta[k]) atomicMax(reinterpret_cast<unsigned long long*>(a.delta + k + 1), sdelta[k]);
+    for (int j = tid; j < nb; j += nthr)
+        if (sdelta[j]) atomicMax(reinterpret_cast<unsigned long long*>(a.delta + lo + j), sdelta[j]);
 }
 
 // K* from the residuals, then V_{K*} and the argmax policy for every state.  Warp-cooperative
@@ -637,6 +650,45 @@ void record_event(cudaEvent_t ev, cudaStream_t s, bool capturing) {
 }
 
 // Enqueue one wavefront solve on `s` (directly, or into a stream capture).
+// Launch k_wave_layer for the band [a.band_lo, a.band_hi) of one layer (a.row0 / n / m /
+// strides / bases set by the caller): tile size, shared memory, grid.
+void launch_layer(vcs_space* sp, WaveArgs& a, bool disc, cudaStream_t s) {
+    // kernel variant (gathers in flight per thread vs occupancy); VCS_WAVE_VARIANT overrides
+    static const int variant = [] {
+        const char* e = std::getenv("VCS_WAVE_VARIANT");
+        return e ? std::atoi(e) : 1;
+    }();
+    using LayerFn = void (*)(WaveArgs);
+    static const LayerFn fns[2][4] = {
+        {k_wave_layer<false, 8, 3>, k_wave_layer<false, 4, 4>, k_wave_layer<false, 4, 5>,
+         k_wave_layer<false, 2, 6>},
+        {k_wave_layer<true, 8, 3>, k_wave_layer<true, 4, 4>, k_wave_layer<true, 4, 5>,
+         k_wave_layer<true, 2, 6>}};
+    const LayerFn layer_fn = fns[disc ? 1 : 0][std::min(3, std::max(0, variant))];
+    const void* fn = reinterpret_cast<const void*>(layer_fn);
+    const int nb = a.band_hi - a.band_lo;
+    if (nb <= 0 || a.n == 0) return;
+    const int qcap = std::max(1, sp->max_degree);
+    // tile: whole passes of (states x 2-version groups) threads, ~8 passes per tile
+    const int G = (nb + 1) / 2;
+    const int spp = G > kWaveWarps * 32 ? 1 : (kWaveWarps * 32) / G;
+    a.tile = G > kWaveWarps * 32 ? 2 : std::min(512, spp * 8);
+    a.max_deg = qcap;
+    const size_t smem = static_cast<size_t>(nb) * 8 + static_cast<size_t>(a.tile) * (nb + 1) * 8 +
+                        static_cast<size_t>(a.tile) * qcap * 16 + static_cast<size_t>(a.tile + 1) * 4;
+    if (smem > 200 * 1024) raise(VCS_EINVAL, "horizon/out-degree too large for the wavefront tile");
+    // (per device context, so set on every launch rather than cached per process)
+    VCS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(std::max<size_t>(smem, 48 * 1024))));
+    int per_sm = 0;
+    VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kWaveWarps * 32, smem));
+    const uint64_t tiles = (a.n + a.tile - 1) / a.tile;
+    const uint64_t blocks = std::max<uint64_t>(
+        1, std::min<uint64_t>(tiles, static_cast<uint64_t>(std::max(1, per_sm)) * sp->num_sms));
+    layer_fn<<<static_cast<unsigned>(blocks), kWaveWarps * 32, smem, s>>>(a);
+    VCS_LAUNCHED();
+}
+
 void record_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaStream_t s,
                       bool capturing) {
     const bool disc = is_discounted(key.discount);
@@ -656,42 +708,12 @@ void record_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
     a.discount = key.discount;
     a.H = sp->H;
     a.max_sweeps = key.max_sweeps;
-    // kernel variant (gathers in flight per thread vs occupancy); VCS_WAVE_VARIANT overrides
-    static const int variant = [] {
-        const char* e = std::getenv("VCS_WAVE_VARIANT");
-        return e ? std::atoi(e) : 1;
-    }();
-    using LayerFn = void (*)(WaveArgs);
-    static const LayerFn fns[2][4] = {
-        {k_wave_layer<false, 8, 3>, k_wave_layer<false, 4, 4>, k_wave_layer<false, 4, 5>,
-         k_wave_layer<false, 2, 6>},
-        {k_wave_layer<true, 8, 3>, k_wave_layer<true, 4, 4>, k_wave_layer<true, 4, 5>,
-         k_wave_layer<true, 2, 6>}};
-    const LayerFn layer_fn = fns[disc ? 1 : 0][std::min(3, std::max(0, variant))];
-    const void* fn_layer = reinterpret_cast<const void*>(layer_fn);
     const void* fn_ext = disc ? reinterpret_cast<const void*>(k_wave_extract<true>)
                               : reinterpret_cast<const void*>(k_wave_extract<false>);
     const int qcap = std::max(1, sp->max_degree);
     const size_t smem_ext = static_cast<size_t>(sp->H + 2) * 16 +
                             static_cast<size_t>(kWaveWarps) * 32 * qcap * sizeof(double);
     if (smem_ext > 200 * 1024) raise(VCS_EINVAL, "out-degree too large for the extraction kernel");
-    // per-layer tile: whole passes of (states x 2-version groups) threads, ~8 passes per tile
-    auto tile_of = [](int m) {
-        const int G = (m + 1) / 2;
-        const int spp = G > kWaveWarps * 32 ? 1 : (kWaveWarps * 32) / G;
-        return G > kWaveWarps * 32 ? 2 : std::min(512, spp * 8);
-    };
-    auto smem_of = [&](int m, int T) {
-        return static_cast<size_t>(m) * 8 + static_cast<size_t>(T) * (m + 1) * 8 +
-               static_cast<size_t>(T) * qcap * 16 + static_cast<size_t>(T + 1) * 4;
-    };
-    size_t smem_layer_max = 1024;
-    for (int t = 0; t < sp->H; ++t)
-        smem_layer_max = std::max(smem_layer_max, smem_of(sp->H - t, tile_of(sp->H - t)));
-    if (smem_layer_max > 200 * 1024)
-        raise(VCS_EINVAL, "horizon/out-degree too large for the wavefront tile");
-    VCS_CUDA(cudaFuncSetAttribute(fn_layer, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem_layer_max)));
     VCS_CUDA(cudaFuncSetAttribute(fn_ext, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(std::max<size_t>(smem_ext, 1024))));
     VCS_CUDA(cudaMemsetAsync(sp->delta.p, 0, (sp->H + 3) * sizeof(double), s));
@@ -713,19 +735,14 @@ void record_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
         a.voff = sp->ver_off_host[t];
         a.voff_next = sp->ver_off_host[t + 1];
         a.m = sp->H - t;
+        a.band_lo = 1; // single GPU: every version of the layer
+        a.band_hi = a.m + 1;
+        a.next_lo = 1;
+        a.base = 0;
+        a.base_next = 0;
         a.stride = wave_stride(a.m);
         a.stride_next = wave_stride(a.m - 1);
-        a.tile = tile_of(a.m);
-        a.max_deg = qcap;
-        const size_t smem = smem_of(a.m, a.tile);
-        int per_sm = 0;
-        VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn_layer,
-                                                               kWaveWarps * 32, smem));
-        const uint64_t tiles = (a.n + a.tile - 1) / a.tile;
-        const uint64_t blocks = std::max<uint64_t>(
-            1, std::min<uint64_t>(tiles, static_cast<uint64_t>(std::max(1, per_sm)) * sp->num_sms));
-        layer_fn<<<static_cast<unsigned>(blocks), kWaveWarps * 32, smem, s>>>(a);
-        VCS_LAUNCHED();
+        launch_layer(sp, a, disc, s);
         ++launches;
         // layer t's values/actions are final here (unless an early stop needs the fix-up):
         // lets vcs_solve stream them to the host while the remaining layers compute
@@ -831,6 +848,95 @@ void ensure_solve_buffers(vcs_space* sp, int max_sweeps) {
     sp->ctrl.exact(1, sp->stream);
     sp->actions_dev.exact(sp->S, sp->stream);
     VCS_CUDA(cudaStreamSynchronize(sp->stream)); // pool allocations ready for any stream
+}
+
+// ---- version-band sharding of the wavefront (multi-GPU) ---------------------------------------
+// Rank r of N owns versions [lo_t, hi_t) = [1 + r*m_t/N, 1 + (r+1)*m_t/N) of every layer t
+// (m_t = H - t; floor division: balanced to one version per layer).  Since lo_{t+1} <= lo_t and
+// hi_t - 1 <= hi_{t+1}, computing its band of layer t needs only its own band of layer t+1 plus
+// ONE column below it (version lo_{t+1} - 1, owned by the rank below): the per-layer exchange is
+// a single n_{t+1}-double column.  Storage of layer t holds versions [base_t, hi_t) with
+// base_t = lo_t - 1 - pad_t; pad_t = (lo_t - lo_{t-1}) & 1 keeps the consumer's (layer t-1)
+// double2 loads 16-byte aligned.
+
+__global__ void k_band_pack(const double* __restrict__ src, uint64_t n, uint32_t stride,
+                            uint32_t slot, double* __restrict__ dst) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[i * stride + slot];
+}
+
+// Receive the halo column (version lo_t - 1) of layer t, and fold in the residual of the band's
+// lowest version, |V_lo - V_{lo-1}|, that the layer kernel could not compute without it.
+__global__ void k_band_unpack(double* __restrict__ store, uint64_t n, uint32_t stride,
+                              uint32_t slot, const double* __restrict__ src, int has_low,
+                              double* __restrict__ delta_lo) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    double d = 0.0;
+    if (i < n) {
+        const double h = src[i];
+        store[i * stride + slot] = h;
+        if (has_low) d = fabs(store[i * stride + slot + 1] - h);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double other = __shfl_xor_sync(0xffffffffu, d, o);
+        d = d < other ? other : d;
+    }
+    if ((threadIdx.x & 31) == 0 && d > 0.0)
+        atomicMax(reinterpret_cast<unsigned long long*>(delta_lo),
+                  static_cast<unsigned long long>(__double_as_longlong(d)));
+}
+
+// Early-stop fix-up of layer t (t < H - K): V_K(s) on the rank owning version K of layer t
+// (ver_t != nullptr), the argmax against V_K of the successors on the rank owning version K of
+// layer t+1 (ver_n != nullptr).
+template <bool DISC>
+__global__ void k_band_fixup(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ succ,
+                             const double* __restrict__ reward, const int32_t* __restrict__ action,
+                             const double* __restrict__ ver_t, uint32_t stride_t, uint32_t slot_t,
+                             const double* __restrict__ ver_n, uint32_t stride_n, uint32_t slot_n,
+                             uint64_t row0, uint64_t n, uint64_t next_row0, double discount,
+                             double* __restrict__ values_out, int32_t* __restrict__ act_out) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t s = row0 + i;
+    if (ver_t) values_out[s] = ver_t[i * stride_t + slot_t];
+    if (!ver_n) return;
+    double best = -INFINITY;
+    int32_t act = -1;
+    for (uint32_t e = row_ptr[s]; e < row_ptr[s + 1]; ++e) {
+        const double v = ver_n[(succ[e] - next_row0) * stride_n + slot_n];
+        const double q = DISC ? __dadd_rn(reward[e], __dmul_rn(discount, v)) : __dadd_rn(reward[e], v);
+        if (q > best) {
+            best = q;
+            act = action[e];
+        }
+    }
+    act_out[s] = act;
+}
+
+void band_plan(vcs_space* sp, int world, int rank) {
+    const int H = sp->H;
+    sp->band_lo.assign(static_cast<size_t>(H) + 1, 1);
+    sp->band_hi.assign(static_cast<size_t>(H) + 1, 1);
+    sp->band_base.assign(static_cast<size_t>(H) + 1, 0);
+    sp->band_stride.assign(static_cast<size_t>(H) + 1, 2);
+    sp->band_off.assign(static_cast<size_t>(H) + 2, 0);
+    for (int t = 0; t <= H; ++t) {
+        const long m = H - t;
+        sp->band_lo[t] = static_cast<int>(1 + rank * m / world);
+        sp->band_hi[t] = static_cast<int>(1 + (rank + 1) * m / world);
+    }
+    uint64_t off = 0;
+    for (int t = 0; t <= H; ++t) {
+        const int pad = t == 0 ? 0 : ((sp->band_lo[t] - sp->band_lo[t - 1]) & 1);
+        sp->band_base[t] = sp->band_lo[t] - 1 - pad;
+        const int width = sp->band_hi[t] - sp->band_base[t];
+        sp->band_stride[t] = (width + 2 + 1) & ~1; // consumer pairs may read one version past hi
+        sp->band_off[t] = off;
+        off += (sp->layer_off[t + 1] - sp->layer_off[t]) * static_cast<uint64_t>(sp->band_stride[t]);
+    }
+    sp->band_off[static_cast<size_t>(H) + 1] = off;
 }
 
 } // namespace
@@ -1048,6 +1154,183 @@ int vcs_shard_finish(vcs_space* sp, int32_t n_sweeps, uint64_t row_begin, uint64
                                      n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         VCS_CUDA(cudaStreamSynchronize(s));
         if (sweeps_out) *sweeps_out = K;
+        return VCS_OK;
+    });
+}
+
+// ---- version-band sharded wavefront --------------------------------------------------------
+
+int vcs_wave_shard_begin(vcs_space* sp, int32_t world, int32_t rank, const vcs_solve_opts* opts,
+                         double* delta, void* stream) {
+    return guarded([&] {
+        if (world < 1 || rank < 0 || rank >= world) raise(VCS_EINVAL, "bad world/rank");
+        vcs_solve_opts o{1e-6, 1, 0, 1.0, VCS_METHOD_WAVEFRONT};
+        if (opts) o = *opts;
+        if (!(o.epsilon > 0.0))
+            raise(VCS_EINVAL, "epsilon must be > 0 (value iteration would never terminate)");
+        vcs::bind_device(sp->device);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
+        sp->wave_world = world;
+        sp->wave_rank = rank;
+        sp->wave_eps = o.epsilon;
+        sp->wave_discount = o.discount;
+        vcs::band_plan(sp, world, rank);
+        const uint64_t total = sp->band_off[static_cast<size_t>(sp->H) + 1];
+        if (!delta) raise(VCS_EINVAL, "delta buffer (horizon+3 doubles) required");
+        sp->wave_delta = delta;
+        sp->band_ver.exact(total + 4, sp->stream); // +4: a consumer pair may read past the end
+        sp->v[0].exact(sp->S, sp->stream);
+        sp->actions_dev.exact(sp->S, sp->stream);
+        VCS_CUDA(cudaStreamSynchronize(sp->stream));
+        // zero store: V_0 slots and the constant halo (version 0) of bands starting at 1
+        VCS_CUDA(cudaMemsetAsync(sp->band_ver.p, 0, (total + 4) * sizeof(double), s));
+        VCS_CUDA(cudaMemsetAsync(delta, 0, (sp->H + 3) * sizeof(double), s));
+        const uint64_t rH = sp->layer_off[sp->H], nH = sp->S - rH;
+        VCS_CUDA(cudaMemsetAsync(sp->v[0].p + rH, 0, nH * sizeof(double), s));
+        VCS_CUDA(cudaMemsetAsync(sp->actions_dev.p + rH, 0xff, nH * sizeof(int32_t), s));
+        return VCS_OK;
+    });
+}
+
+int vcs_wave_shard_band(const vcs_space* sp, int32_t t, int32_t* lo, int32_t* hi) {
+    return guarded([&] {
+        if (sp->band_lo.empty()) raise(VCS_EINVAL, "vcs_wave_shard_begin was not called");
+        if (t < 0 || t > sp->H) raise(VCS_EINVAL, "layer out of range");
+        *lo = sp->band_lo[t];
+        *hi = sp->band_hi[t];
+        return VCS_OK;
+    });
+}
+
+int vcs_wave_shard_layer(vcs_space* sp, int32_t t, void* stream) {
+    return guarded([&] {
+        if (sp->band_lo.empty()) raise(VCS_EINVAL, "vcs_wave_shard_begin was not called");
+        if (t < 0 || t >= sp->H) raise(VCS_EINVAL, "layer out of range");
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
+        const bool disc = vcs::is_discounted(sp->wave_discount);
+        vcs::WaveArgs a{};
+        a.row_ptr = sp->row_ptr.p;
+        a.succ = sp->succ.p;
+        a.reward = sp->reward.p;
+        a.action = sp->action.p;
+        a.ver = sp->band_ver.p;
+        a.delta = sp->wave_delta;
+        a.values_out = sp->v[0].p;
+        a.act_out = sp->actions_dev.p;
+        a.eps = sp->wave_eps;
+        a.discount = sp->wave_discount;
+        a.H = sp->H;
+        a.row0 = sp->layer_off[t];
+        a.n = sp->layer_off[t + 1] - sp->layer_off[t];
+        a.next_row0 = sp->layer_off[t + 1];
+        a.voff = sp->band_off[t];
+        a.voff_next = sp->band_off[t + 1];
+        a.m = sp->H - t;
+        a.band_lo = sp->band_lo[t];
+        a.band_hi = sp->band_hi[t];
+        a.next_lo = sp->band_lo[t + 1];
+        a.base = sp->band_base[t];
+        a.base_next = sp->band_base[t + 1];
+        a.stride = sp->band_stride[t];
+        a.stride_next = sp->band_stride[t + 1];
+        vcs::launch_layer(sp, a, disc, s);
+        return VCS_OK;
+    });
+}
+
+int vcs_wave_shard_pack(vcs_space* sp, int32_t t, int32_t version, double* dst, void* stream) {
+    return guarded([&] {
+        if (sp->band_lo.empty()) raise(VCS_EINVAL, "vcs_wave_shard_begin was not called");
+        if (t < 0 || t > sp->H || version < sp->band_base[t] || version >= sp->band_hi[t])
+            raise(VCS_EINVAL, "version not held by this rank");
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
+        const uint64_t n = sp->layer_off[t + 1] - sp->layer_off[t];
+        if (!n) return VCS_OK;
+        vcs::k_band_pack<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+            sp->band_ver.p + sp->band_off[t], n, static_cast<uint32_t>(sp->band_stride[t]),
+            static_cast<uint32_t>(version - sp->band_base[t]), dst);
+        VCS_LAUNCHED();
+        return VCS_OK;
+    });
+}
+
+int vcs_wave_shard_unpack(vcs_space* sp, int32_t t, const double* src, void* stream) {
+    return guarded([&] {
+        if (sp->band_lo.empty()) raise(VCS_EINVAL, "vcs_wave_shard_begin was not called");
+        if (t < 0 || t > sp->H) raise(VCS_EINVAL, "layer out of range");
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
+        const uint64_t n = sp->layer_off[t + 1] - sp->layer_off[t];
+        if (!n) return VCS_OK;
+        const int lo = sp->band_lo[t];
+        const int has_low = sp->band_hi[t] > lo ? 1 : 0; // residual of version lo needs the halo
+        vcs::k_band_unpack<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+            sp->band_ver.p + sp->band_off[t], n, static_cast<uint32_t>(sp->band_stride[t]),
+            static_cast<uint32_t>(lo - 1 - sp->band_base[t]), src, has_low,
+            sp->wave_delta + lo);
+        VCS_LAUNCHED();
+        return VCS_OK;
+    });
+}
+
+int vcs_wave_shard_finish(vcs_space* sp, int32_t K, double* values_out, int32_t* actions_out,
+                          void* stream) {
+    return guarded([&] {
+        if (sp->band_lo.empty()) raise(VCS_EINVAL, "vcs_wave_shard_begin was not called");
+        if (K < 1) raise(VCS_EINVAL, "sweep count must be >= 1");
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
+        const int H = sp->H;
+        const bool disc = vcs::is_discounted(sp->wave_discount);
+        auto owns = [&](int t, int k) { return sp->band_lo[t] <= k && k < sp->band_hi[t]; };
+        // early-stop fix-up of layers t < H - K: values by the owner of version K of layer t,
+        // actions by the owner of version K of layer t+1 (the argmax reads V_K of successors)
+        for (int t = 0; t < H - K; ++t) {
+            const bool val = owns(t, K), act = owns(t + 1, K);
+            if (!val && !act) continue;
+            const uint64_t n = sp->layer_off[t + 1] - sp->layer_off[t];
+            if (!n) continue;
+            const unsigned grid = static_cast<unsigned>((n + 255) / 256);
+            auto launch = [&](auto kern) {
+                kern<<<grid, 256, 0, s>>>(
+                    sp->row_ptr.p, sp->succ.p, sp->reward.p, sp->action.p,
+                    val ? sp->band_ver.p + sp->band_off[t] : nullptr,
+                    static_cast<uint32_t>(sp->band_stride[t]),
+                    static_cast<uint32_t>(val ? K - sp->band_base[t] : 0),
+                    act ? sp->band_ver.p + sp->band_off[t + 1] : nullptr,
+                    static_cast<uint32_t>(sp->band_stride[t + 1]),
+                    static_cast<uint32_t>(act ? K - sp->band_base[t + 1] : 0), sp->layer_off[t], n,
+                    sp->layer_off[t + 1], sp->wave_discount, sp->v[0].p, sp->actions_dev.p);
+            };
+            if (disc) launch(vcs::k_band_fixup<true>);
+            else launch(vcs::k_band_fixup<false>);
+            VCS_LAUNCHED();
+        }
+        // every row's value and action reach the host from exactly one rank each: exact rows
+        // (t >= H-K, and the terminal layer) from the rank holding version m_t (the last rank),
+        // fix-up rows from the owners above
+        auto copy = [&](bool values, uint64_t r0, uint64_t r1) {
+            if (r1 <= r0) return;
+            if (values && values_out)
+                VCS_CUDA(cudaMemcpyAsync(values_out + r0, sp->v[0].p + r0, (r1 - r0) * sizeof(double),
+                                         cudaMemcpyDeviceToHost, s));
+            if (!values && actions_out)
+                VCS_CUDA(cudaMemcpyAsync(actions_out + r0, sp->actions_dev.p + r0,
+                                         (r1 - r0) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        };
+        const int first_exact = std::max(0, H - K);
+        const bool exact_owner = sp->wave_rank == sp->wave_world - 1;
+        for (int t = 0; t <= H; ++t) {
+            const uint64_t r0 = sp->layer_off[t], r1 = sp->layer_off[t + 1];
+            if (t >= first_exact) {
+                if (exact_owner) {
+                    copy(true, r0, r1);
+                    copy(false, r0, r1);
+                }
+            } else {
+                if (owns(t, K)) copy(true, r0, r1);
+                if (owns(t + 1, K)) copy(false, r0, r1);
+            }
+        }
+        VCS_CUDA(cudaStreamSynchronize(s));
         return VCS_OK;
     });
 }

@@ -590,6 +590,7 @@ vcs_space::~vcs_space() {
     ctrl.release();
     actions_dev.release();
     ver.release();
+    band_ver.release();
     ver_off.release();
     layer_off_dev.release();
     loc_table.release();

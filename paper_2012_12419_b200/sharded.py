@@ -189,3 +189,165 @@ def _cpu_group(group):
     if key not in _CPU_GROUPS:
         _CPU_GROUPS[key] = dist.new_group(backend="gloo")
     return _CPU_GROUPS[key]
+
+
+# ==============================================================================================
+# Version-band sharding of the layer wavefront (vcs_wave_shard_*).
+# Rank r owns versions [1 + r*m_t//N, 1 + (r+1)*m_t//N) of every layer t; per layer the only
+# exchange is one column (version lo-1) per rank, sent by the rank that computed it.
+# ==============================================================================================
+
+def band(m: int, r: int, world: int) -> tuple:
+    """Versions [lo, hi) of a layer with m versions owned by rank r (mirrors band_plan)."""
+    return 1 + r * m // world, 1 + (r + 1) * m // world
+
+
+def halo_schedule(H: int, world: int, t: int) -> list:
+    """(src, dst, version) transfers after layer t: every rank whose band starts above 1
+    receives the column just below it from the rank that owns that version."""
+    m = H - t
+    out = []
+    for r in range(world):
+        lo, _ = band(m, r, world)
+        c = lo - 1
+        if c < 1:
+            continue  # version 0 is the constant initial iterate
+        owner = next(q for q in range(world) if band(m, q, world)[0] <= c < band(m, q, world)[1])
+        out.append((owner, r, c))
+    return out
+
+
+class WaveBandCuda:
+    """Device backend of one rank: vcs_wave_shard_* on a dedicated torch stream."""
+
+    def __init__(self, space, device: torch.device, stream: "torch.cuda.Stream | None" = None):
+        self.space = space
+        self.device = device
+        self.torch_stream = stream or torch.cuda.Stream(device)
+        self.H = space.task_count()
+        self.delta = torch.zeros(self.H + 3, dtype=torch.float64, device=device)
+
+    def _s(self):
+        return C.c_void_p(self.torch_stream.cuda_stream)
+
+    def begin(self, world: int, rank: int, opts):
+        with torch.cuda.stream(self.torch_stream):
+            self.delta.zero_()
+        N.check(N.lib().vcs_wave_shard_begin(self.space.handle, world, rank, C.byref(opts),
+                                             C.c_void_p(self.delta.data_ptr()), self._s()))
+
+    def layer(self, t: int):
+        N.check(N.lib().vcs_wave_shard_layer(self.space.handle, t, self._s()))
+
+    def pack(self, t: int, version: int, dst: torch.Tensor):
+        N.check(N.lib().vcs_wave_shard_pack(self.space.handle, t, version,
+                                            C.c_void_p(dst.data_ptr()), self._s()))
+
+    def unpack(self, t: int, src: torch.Tensor):
+        N.check(N.lib().vcs_wave_shard_unpack(self.space.handle, t, C.c_void_p(src.data_ptr()),
+                                              self._s()))
+
+    def new_buffer(self, n: int) -> torch.Tensor:
+        return torch.empty(max(n, 1), dtype=torch.float64, device=self.device)
+
+    def finish(self, K: int, values: np.ndarray | None, actions: np.ndarray | None):
+        N.check(N.lib().vcs_wave_shard_finish(
+            self.space.handle, K, N.ptr(values, C.c_double) if values is not None else None,
+            N.ptr(actions, C.c_int32) if actions is not None else None, self._s()))
+
+
+def _first_converged(delta: np.ndarray, eps: float, M: int) -> int:
+    for k in range(1, M + 1):
+        if delta[k] < eps:
+            return k
+    return M
+
+
+def run_wave_sharded(backend, layer_offset: np.ndarray, opts, group=None, gather: bool = True):
+    """One rank of the band-sharded wavefront over torch.distributed (NCCL on B200s, gloo for
+    CPU backends).  Returns (values, actions, sweeps); the arrays are full (gathered on every
+    rank) when ``gather``, else None."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    H = len(layer_offset) - 2
+    S = int(layer_offset[-1])
+    n_layer = np.diff(np.asarray(layer_offset, dtype=np.int64))
+    M = H + 1 if opts.max_sweeps <= 0 else min(H + 1, opts.max_sweeps)
+    ctx = torch.cuda.stream(backend.torch_stream) if hasattr(backend, "torch_stream") else None
+    if ctx is not None:
+        ctx.__enter__()
+    try:
+        backend.begin(world, rank, opts)
+        send = backend.new_buffer(int(n_layer.max()))
+        recv = backend.new_buffer(int(n_layer.max()))
+        for t in range(H - 1, -1, -1):
+            backend.layer(t)
+            if world == 1:
+                continue
+            n = int(n_layer[t])
+            ops, got = [], False
+            sends = [(src, dst, v) for src, dst, v in halo_schedule(H, world, t) if src == rank]
+            sbufs = []
+            for i, (src, dst, v) in enumerate(sends):  # one staging buffer per destination
+                buf = send[:n] if i == 0 else backend.new_buffer(n)[:n]
+                backend.pack(t, v, buf)
+                sbufs.append(buf)
+                ops.append(dist.P2POp(dist.isend, buf, dst, group))
+            for src, dst, v in halo_schedule(H, world, t):
+                if dst == rank:
+                    ops.append(dist.P2POp(dist.irecv, recv[:n], src, group))
+                    got = True
+            if ops:
+                for req in dist.batch_isend_irecv(ops):
+                    req.wait()
+            if got:
+                backend.unpack(t, recv[:n])
+        dist.all_reduce(backend.delta, op=dist.ReduceOp.MAX, group=group)
+        delta = backend.delta.cpu().numpy() if hasattr(backend.delta, "cpu") else backend.delta
+    finally:
+        if ctx is not None:
+            ctx.__exit__(None, None, None)
+    K = _first_converged(np.asarray(delta), opts.epsilon, M)
+    values = np.zeros(S, np.float64) if gather else None
+    actions = np.zeros(S, np.int32) if gather else None
+    backend.finish(K, values, actions)
+    if gather and world > 1:
+        vt = torch.from_numpy(values.view(np.int64))
+        at = torch.from_numpy(actions)
+        dist.all_reduce(vt, op=dist.ReduceOp.SUM, group=_cpu_group(group))
+        dist.all_reduce(at, op=dist.ReduceOp.SUM, group=_cpu_group(group))
+        values, actions = vt.numpy().view(np.float64), at.numpy()
+    return values, actions, K
+
+
+def run_wave_emulated(backends: list, layer_offset: np.ndarray, opts):
+    """All `world` ranks of the band-sharded wavefront in ONE process (one backend per rank, on
+    one stream): the column exchange is a device copy and the all-reduce a host max.  No kernel
+    ever waits on another rank's kernel, so this is safe on a single GPU (test seam)."""
+    world = len(backends)
+    H = len(layer_offset) - 2
+    S = int(layer_offset[-1])
+    n_layer = np.diff(np.asarray(layer_offset, dtype=np.int64))
+    M = H + 1 if opts.max_sweeps <= 0 else min(H + 1, opts.max_sweeps)
+    for r, be in enumerate(backends):
+        be.begin(world, r, opts)
+    tmp = backends[0].new_buffer(int(n_layer.max()))
+    for t in range(H - 1, -1, -1):
+        for be in backends:
+            be.layer(t)
+        n = int(n_layer[t])
+        for src, dst, v in halo_schedule(H, world, t):
+            backends[src].pack(t, v, tmp[:n])
+            backends[dst].unpack(t, tmp[:n])
+    delta = np.max(np.stack([np.asarray(be.delta.cpu() if hasattr(be.delta, "cpu") else be.delta)
+                             for be in backends]), axis=0)
+    K = _first_converged(delta, opts.epsilon, M)
+    values = np.zeros(S, np.float64)
+    actions = np.zeros(S, np.int32)
+    for be in backends:  # every row is written by exactly one rank
+        v = np.zeros(S, np.float64)
+        a = np.zeros(S, np.int32)
+        be.finish(K, v, a)
+        values = (values.view(np.int64) + v.view(np.int64)).view(np.float64)
+        actions = actions + a
+    return values, actions, K

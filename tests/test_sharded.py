@@ -122,3 +122,140 @@ def test_sharded_driver_bit_identical(oracle, world, case, eps, skip):
     assert int(got["sweeps"]) == sw
     assert np.array_equal(got["values"].view(np.uint64), v.view(np.uint64))
     assert np.array_equal(got["actions"], a)
+
+
+# ---- the version-band sharded wavefront driver over gloo ----------------------------------
+
+class NumpyBandBackend:
+    """CPU restatement of the vcs_wave_shard_* semantics (test infrastructure): each rank keeps
+    full-size version arrays but only ever fills its band (NaN elsewhere), so a missing or
+    misrouted halo column would surface as NaN in the results."""
+
+    def __init__(self, csr, H):
+        self.lo_off, self.rp, self.su, self.rw, self.ac = csr
+        self.H = H
+        self.S = int(self.lo_off[-1])
+
+    def _rows(self, t):
+        return int(self.lo_off[t]), int(self.lo_off[t + 1])
+
+    def begin(self, world, rank, opts):
+        from paper_2012_12419_b200.sharded import band
+        self.world, self.rank, self.eps = world, rank, opts.epsilon
+        self.bands = [band(self.H - t, rank, world) for t in range(self.H + 1)]
+        self.ver = []
+        for t in range(self.H + 1):
+            a, b = self._rows(t)
+            arr = np.full((b - a, self.H - t + 1), np.nan)
+            arr[:, 0] = 0.0  # V_0
+            self.ver.append(arr)
+        self.values = np.full(self.S, np.nan)
+        self.actions = np.full(self.S, -7, np.int32)
+        a, b = self._rows(self.H)
+        self.values[a:b] = 0.0
+        self.actions[a:b] = -1
+        self.delta = torch.zeros(self.H + 3, dtype=torch.float64)
+
+    def _q(self, t, k):
+        """q_e = r_e + V_{k-1}(succ_e) for every edge of layer t, plus row segment starts."""
+        a, b = self._rows(t)
+        e0, e1 = int(self.rp[a]), int(self.rp[b])
+        nxt = self.ver[t + 1]
+        sl = self.su[e0:e1].astype(np.int64) - int(self.lo_off[t + 1])
+        v = nxt[sl, k - 1]
+        assert not np.isnan(v).any(), ("missing successor version", t, k)
+        q = self.rw[e0:e1] + v
+        starts = (self.rp[a:b] - e0).astype(np.int64)
+        return q, starts, e0
+
+    @staticmethod
+    def _first_argmax(q, starts):
+        mx = np.maximum.reduceat(q, starts)
+        seg = np.repeat(np.arange(len(starts)), np.diff(np.append(starts, len(q))))
+        idx = np.where(q == mx[seg], np.arange(len(q)), len(q))
+        return mx, np.minimum.reduceat(idx, starts)
+
+    def layer(self, t):
+        lo, hi = self.bands[t]
+        m = self.H - t
+        a, b = self._rows(t)
+        for k in range(lo, hi):
+            q, starts, e0 = self._q(t, k)
+            mx, first = self._first_argmax(q, starts)
+            self.ver[t][:, k] = mx
+            if k == m:
+                self.values[a:b] = mx
+                self.actions[a:b] = self.ac[e0 + first]
+            if k > lo or lo == 1:
+                d = float(np.max(np.abs(mx - self.ver[t][:, k - 1])))
+                self.delta[k] = max(float(self.delta[k]), d)
+
+    def pack(self, t, version, dst):
+        col = self.ver[t][:, version]
+        assert not np.isnan(col).any(), ("packing a version this rank does not hold", t, version)
+        dst.copy_(torch.from_numpy(col.copy()))
+
+    def unpack(self, t, src):
+        lo, hi = self.bands[t]
+        self.ver[t][:, lo - 1] = src.numpy()
+        if hi > lo:
+            d = float(np.max(np.abs(self.ver[t][:, lo] - self.ver[t][:, lo - 1])))
+            self.delta[lo] = max(float(self.delta[lo]), d)
+
+    def new_buffer(self, n):
+        return torch.empty(max(n, 1), dtype=torch.float64)
+
+    def finish(self, K, values_out, actions_out):
+        H = self.H
+        last = self.rank == self.world - 1
+        for t in range(H + 1):
+            a, b = self._rows(t)
+            if t >= max(0, H - K):
+                if last:
+                    values_out[a:b] = self.values[a:b]
+                    actions_out[a:b] = self.actions[a:b]
+                continue
+            if self.bands[t][0] <= K < self.bands[t][1]:
+                values_out[a:b] = self.ver[t][:, K]
+            if self.bands[t + 1][0] <= K < self.bands[t + 1][1]:
+                q, starts, e0 = self._q(t, K + 1)  # argmax against V_K of the successors
+                _, first = self._first_argmax(q, starts)
+                actions_out[a:b] = self.ac[e0 + first]
+
+
+def _wave_worker(rank, world, port, case, eps, out_path):
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    sys.path[:0] = [str(root), str(root / "tests")]
+    from oracle_bind import Oracle
+    from paper_2012_12419_b200.sharded import run_wave_sharded
+    from test_sharded import NumpyBandBackend, _instance
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ni = _instance(case)
+        sp = Oracle().build(ni.ref, 10**9)
+        csr = sp.csr()
+        opts = N.vcs_solve_opts(eps, 1, 0, 1.0, N.VCS_METHOD_WAVEFRONT)
+        values, actions, K = run_wave_sharded(NumpyBandBackend(csr, sp.H), csr[0], opts)
+        if rank == 0:
+            np.savez(out_path, values=values, actions=actions, sweeps=K)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case,eps", [((47, 3), 1e-6), ((47, 3), 0.7), ((3003, 0), 1e-6),
+                                      ((3003, 2), 0.4)])
+def test_wave_band_driver_bit_identical(oracle, world, case, eps):
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "r.npz")
+        mp.spawn(_wave_worker, args=(world, _free_port(), case, eps, out), nprocs=world,
+                 join=True)
+        got = np.load(out)
+    ni = _instance(case)
+    v, a, sw, _, _ = oracle.build(ni.ref, 10**9).vi(eps=eps)
+    assert int(got["sweeps"]) == sw
+    assert np.array_equal(got["values"].view(np.uint64), v.view(np.uint64))
+    assert np.array_equal(got["actions"], a)
