@@ -211,6 +211,61 @@ def run_reference(args):
     return 0
 
 
+PARALLELISM = {
+    "wave": lambda n: f"version-band sharded wavefront x{n}: one column per layer over NCCL "
+                      "send/recv + one MAX all-reduce per solve",
+    "halo": lambda n: f"row-block sharded Jacobi x{n}: forward halo over NCCL + MAX all-reduce "
+                      "per sweep",
+    "allgather": lambda n: f"row-block sharded Jacobi x{n}: all-gather of V + MAX all-reduce per "
+                           "sweep",
+}
+
+
+def e2e_sharded(args, ni, local, dev, stream, opts, sharding, S, rank):
+    """N>1 end to end: every rank builds the space from the host instance, runs its shard of
+    the solve and downloads the rows it owns (values + actions) into pinned host memory.
+    Wall time per step is the max over ranks (barrier before each step)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2012_12419_b200 as V
+    from paper_2012_12419_b200 import _native as N
+    from paper_2012_12419_b200 import sharded as SH
+    vals = torch.zeros(S, dtype=torch.float64, pin_memory=True)
+    acts = torch.zeros(S, dtype=torch.int32, pin_memory=True)
+    vn, an = vals.numpy(), acts.numpy()
+    s = ni.struct
+    inst_bytes = s.n_clouds * (3 * 4 + 2 * 8) + s.n_tasks * (2 * 4 + 2 * 8)
+    times, d2h = [], 0
+    for i in range(args.e2e_steps + 2):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sp = V.StateSpace.build_native(ni, 10**9, local)
+        lo = sp.layer_offsets()
+        if sharding == "wave":
+            be = SH.WaveBandCuda(sp, dev, stream)
+            _, _, K = SH.run_wave_sharded(be, lo, opts, local_out=(vn, an))
+        else:
+            be = SH.CudaBackend(sp, dev, stream)
+            _, _, K = SH.run_sharded(be, lo, sp.layer_edges(), opts, mode=sharding,
+                                     local_out=(vn, an))
+        torch.cuda.synchronize()
+        t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        del be, sp
+        if i >= 2:
+            times.append(float(t.item()))
+    # bytes this rank moved host->device (the instance) and device->host (its owned rows),
+    # summed over ranks
+    d2h = S * (8 + 4)
+    e2e_t = statistics.median(times)
+    return {"value": S * K / e2e_t, "unit": "backups/s",
+            "h2d_bytes_per_step": inst_bytes * dist.get_world_size(),
+            "d2h_bytes_per_step": d2h, "ms_per_step": e2e_t * 1e3,
+            "path": f"per rank: vcs_space_build(host instance) + sharded solve ({sharding}) + "
+                    "D2H of the rank's own rows", "steps": len(times)}
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -224,8 +279,15 @@ def run_b200(args):
         log(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # the sharded drivers run for N>1, or at N=1 when --sharding names one (a 1-rank group)
+    sharded_path = world > 1 or args.sharding != "auto"
+    if sharded_path:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=dev)
+    sharding = args.sharding
     gen, desc = WORKLOADS[args.workload]
     ni = V.generate_instance(*gen, as_objects=False)
     t0 = time.time()
@@ -243,7 +305,7 @@ def run_b200(args):
     sampler.start()
     launches0 = None
 
-    if world == 1:
+    if not sharded_path:
         h_stream = C.c_void_p(stream.cuda_stream)
         rep = N.vcs_solve_report()
         for _ in range(args.warmup):
@@ -273,11 +335,24 @@ def run_b200(args):
         method = rep.method
         model_bytes = rep.model_bytes
     else:
-        from paper_2012_12419_b200.sharded import CudaBackend, run_sharded
-        backend = CudaBackend(space, dev, stream)
+        from paper_2012_12419_b200 import sharded as SH
         lo, le = space.layer_offsets(), space.layer_edges()
+        if sharding == "auto":
+            sharding = "halo" if method == N.VCS_METHOD_JACOBI else "wave"
+        if sharding == "wave":
+            opts.method = N.VCS_METHOD_WAVEFRONT
+            backend = SH.WaveBandCuda(space, dev, stream)
+
+            def step():
+                return SH.run_wave_sharded(backend, lo, opts, gather=False)[2]
+        else:
+            opts.method = N.VCS_METHOD_JACOBI
+            backend = SH.CudaBackend(space, dev, stream)
+
+            def step():
+                return SH.run_sharded(backend, lo, le, opts, gather=False, mode=sharding)[2]
         for _ in range(args.warmup):
-            _, _, sweeps = run_sharded(backend, lo, le, opts, gather=False)
+            sweeps = step()
         dist.barrier()
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -285,7 +360,7 @@ def run_b200(args):
         tw0 = time.time()
         ev0.record(stream)
         for _ in range(args.steps):
-            _, _, sweeps = run_sharded(backend, lo, le, opts, gather=False)
+            sweeps = step()
         ev1.record(stream)
         torch.cuda.synchronize()
         dist.barrier()
@@ -295,12 +370,19 @@ def run_b200(args):
         dist.all_reduce(local_ms, op=dist.ReduceOp.MAX)
         total_ms = float(local_ms.item())
         sampler.mark(tw0, tw1)
-        rep = None
-        from paper_2012_12419_b200.sharded import sweep_row_end
-        backups_done = sum(sweep_row_end(lo, k, not args.no_skip) for k in range(1, sweeps + 1))
         dbar = E / S
-        alg_bytes_done = (24 + 12 * dbar) * backups_done
-        method, model_bytes = N.VCS_METHOD_JACOBI, (20 + 12 * dbar) * backups_done
+        n_layer = np.diff(lo.astype(np.int64))
+        if sharding == "wave":
+            # every (state, version) backup of the wavefront, summed over all ranks' bands
+            backups_done = int(sum(int(n_layer[t]) * (H - t) for t in range(H)))
+            method = N.VCS_METHOD_WAVEFRONT
+            model_bytes = 20 * S + 12 * E + 16 * backups_done
+            alg_bytes_done = model_bytes
+        else:
+            backups_done = sum(SH.sweep_row_end(lo, k, not args.no_skip)
+                               for k in range(1, sweeps + 1))
+            alg_bytes_done = (24 + 12 * dbar) * backups_done
+            method, model_bytes = N.VCS_METHOD_JACOBI, (20 + 12 * dbar) * backups_done
         sweep_ms, extract_ms = [total_ms / args.steps], [0.0]
 
     sampler.stop()
@@ -311,7 +393,7 @@ def run_b200(args):
 
     # ---- e2e through the C ABI with host buffers (rank 0 / N=1 path) --------------------------
     e2e = None
-    if world == 1 and args.e2e_steps > 0:
+    if not sharded_path and args.e2e_steps > 0:
         vals = torch.empty(S, dtype=torch.float64, pin_memory=True)
         acts = torch.empty(S, dtype=torch.int32, pin_memory=True)
         inst_bytes = 0
@@ -344,12 +426,14 @@ def run_b200(args):
                "solve_and_d2h_ms": statistics.median(p[1] for p in parts) * 1e3,
                "path": "vcs_space_build(host instance) + vcs_solve(pinned host values/actions)",
                "steps": len(e2e_times)}
+    elif args.e2e_steps > 0:
+        e2e = e2e_sharded(args, ni, local, dev, stream, opts, sharding, S, rank)
 
     # ---- roofline of the dominant kernel ----------------------------------------------------
     peak, peak_src = measured_peaks()
-    sweep_s = statistics.mean(sweep_ms) * 1e-3 if world == 1 else None
+    sweep_s = statistics.mean(sweep_ms) * 1e-3 if not sharded_path else None
     roofline = None
-    if world == 1 and sweep_s:
+    if sweep_s:
         tr = ncu_traffic(method)
         survey_equiv = b_ref * S * sweeps / sweep_s / 1e9  # SURVEY 8d bytes of the Jacobi sweeps
         if method == N.VCS_METHOD_WAVEFRONT:
@@ -385,8 +469,8 @@ def run_b200(args):
                    "sweeps": sweeps, "epsilon": args.eps, "layer_skip": not args.no_skip,
                    "method": {1: "jacobi", 2: "layer-wavefront"}.get(method, str(method)),
                    "backups_performed_per_step": backups_done,
-                   "parallelism": "single GPU" if world == 1 else
-                   f"row-block sharded x{world}, forward halo over NCCL + MAX all-reduce",
+                   "parallelism": "single GPU" if not sharded_path else
+                   PARALLELISM[sharding](world),
                    "l2": "no flush: CSR 1.7 GB and V buffers 2x155 MB exceed the 126 MB L2",
                    "build_ms": space.info.build_ms, "build_wall_ms": build_wall_ms},
         "time_to_convergence_ms": ms_per_step,
@@ -404,7 +488,7 @@ def run_b200(args):
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     if rank == 0:
         print(json.dumps(line))
-    if world > 1:
+    if sharded_path:
         dist.destroy_process_group()
     return 0
 
@@ -422,6 +506,9 @@ def main():
     ap.add_argument("--method", choices=["auto", "jacobi", "wavefront"], default="auto",
                     help="single-GPU solver (auto = layer wavefront when it fits in HBM)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharding", choices=["auto", "wave", "halo", "allgather"], default="auto",
+                    help="N>1: version-band wavefront (auto unless --method jacobi), or Jacobi "
+                         "row blocks with a forward halo / a full all-gather of V per sweep")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         log("note: the timing rules ask for >= 3 warm-up steps")

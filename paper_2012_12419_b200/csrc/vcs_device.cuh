@@ -92,16 +92,17 @@ struct GraphKey {
     int skip;
     int max_sweeps;
     int method;
+    int stream_out; // wavefront: record an event per layer (vcs_solve's overlapped download)
     bool operator<(const GraphKey& o) const {
-        return std::tie(eps, discount, skip, max_sweeps, method) <
-               std::tie(o.eps, o.discount, o.skip, o.max_sweeps, o.method);
+        return std::tie(eps, discount, skip, max_sweeps, method, stream_out) <
+               std::tie(o.eps, o.discount, o.skip, o.max_sweeps, o.method, o.stream_out);
     }
 };
 
 struct CachedGraph {
     cudaGraphExec_t exec = nullptr;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
-    std::vector<cudaEvent_t> layer_ev; // wavefront: after layer t's kernel (timing disabled)
+    std::vector<cudaEvent_t> layer_ev; // wavefront + stream_out: after layer t's kernel
     int n_sweeps = 0; // sweep kernels in the graph
     int launches = 0;
     int method = kMethodJacobi;

@@ -329,21 +329,29 @@ struct WaveArgs {
 //   phase 3: residuals |V_k - V_{k-1}| (a thread's k's are fixed: register running maxima).
 //            For k = a the predecessor V_{a-1} is V_0 = 0 when a = 1; otherwise it is the
 //            halo column another rank computes, and k_band_low_delta folds it in later.
-template <bool DISC, int U, int MINB>
+struct alignas(16) EdgeRec {
+    double reward;
+    uint32_t succ; // successor index within layer t+1
+    int32_t action;
+};
+
+// BAND = false: the single-GPU form (lo = 1, storage from V_0), with the shifts compile-time 0.
+template <bool DISC, int U, int MINB, bool BAND>
 __global__ void __launch_bounds__(kWaveWarps * 32, MINB) k_wave_layer(WaveArgs a) {
     constexpr int P = 2; // versions per thread (one aligned double2 gather per edge)
     // U: edges whose gathers are issued together; MINB: resident blocks per SM (register cap)
     extern __shared__ unsigned long long smem_u64[];
-    const int lo = a.band_lo;                    // first version computed (odd)
+    const int lo = BAND ? a.band_lo : 1;         // first version computed (odd)
     const int nb = a.band_hi - a.band_lo;        // versions computed per state
     const int T = a.tile;
     const int w1 = nb + 1;                       // shared slots per state: V_{lo-1} .. V_{hi-1}
-    unsigned long long* sdelta = smem_u64;                           // [nb]
-    double* sout = reinterpret_cast<double*>(smem_u64 + nb);         // [T*(nb+1)]
-    double* srew = sout + static_cast<size_t>(T) * w1;               // [T*max_deg]
-    uint32_t* ssucc = reinterpret_cast<uint32_t*>(srew + static_cast<size_t>(T) * a.max_deg);
-    int32_t* sact = reinterpret_cast<int32_t*>(ssucc + static_cast<size_t>(T) * a.max_deg);
-    uint32_t* srp = reinterpret_cast<uint32_t*>(sact + static_cast<size_t>(T) * a.max_deg); // [T+1]
+    // the tile's edges first, one 16-byte record each, so every per-edge shared access in the
+    // gather loop is an immediate offset from the edge index (no per-edge address arithmetic)
+    EdgeRec* sedge = reinterpret_cast<EdgeRec*>(smem_u64);           // [T*max_deg]
+    double* sout = reinterpret_cast<double*>(sedge + static_cast<size_t>(T) * a.max_deg); // [T*(nb+1)]
+    unsigned long long* sdelta =
+        reinterpret_cast<unsigned long long*>(sout + static_cast<size_t>(T) * w1); // [nb]
+    uint32_t* srp = reinterpret_cast<uint32_t*>(sdelta + nb);        // [T+1]
     const int tid = threadIdx.x;
     const int nthr = blockDim.x;
     for (int j = tid; j < nb; j += nthr) sdelta[j] = 0ull;
@@ -356,8 +364,8 @@ __global__ void __launch_bounds__(kWaveWarps * 32, MINB) k_wave_layer(WaveArgs a
     const uint32_t sn = static_cast<uint32_t>(a.stride_next); // stored stride of layer t+1
     const uint64_t st = static_cast<uint64_t>(a.stride);       // stored stride of layer t
     // successor slot of version (k-1) is k-1-base_next; for k = lo + gP it is even (aligned)
-    const uint32_t nshift = static_cast<uint32_t>(lo - 1 - a.base_next);
-    const int oshift = lo - a.base; // own storage slot of version lo + j is j + oshift
+    const uint32_t nshift = BAND ? static_cast<uint32_t>(lo - 1 - a.base_next) : 0u;
+    const int oshift = BAND ? lo - a.base : 1; // own storage slot of version lo + j is j + oshift
     const double* vn = a.ver + a.voff_next;
     const uint32_t nbase = static_cast<uint32_t>(a.next_row0);
     const uint64_t n_tiles = (a.n + T - 1) / T;
@@ -390,9 +398,11 @@ __global__ void __launch_bounds__(kWaveWarps * 32, MINB) k_wave_layer(WaveArgs a
         const uint32_t e0 = srp[0];
         const int ne = static_cast<int>(srp[nt] - e0);
         for (int j = tid; j < ne; j += nthr) {
-            ssucc[j] = __ldcs(a.succ + e0 + j) - nbase;
-            srew[j] = __ldcs(a.reward + e0 + j);
-            sact[j] = __ldcs(a.action + e0 + j); // the winner's action, without a dependent load
+            EdgeRec rec;
+            rec.reward = __ldcs(a.reward + e0 + j);
+            rec.succ = __ldcs(a.succ + e0 + j) - nbase;
+            rec.action = __ldcs(a.action + e0 + j); // the winner's action, without a dependent load
+            sedge[j] = rec;
         }
         __syncthreads();
         double* out = a.ver + a.voff + s0 * st;
@@ -414,11 +424,11 @@ __global__ void __launch_bounds__(kWaveWarps * 32, MINB) k_wave_layer(WaveArgs a
                         for (int u = 0; u < U; ++u)
                             if (eo + u < ee)
                                 x[u] = __ldg(reinterpret_cast<const double2*>(
-                                    vn + (ssucc[eo + u] * sn + nslot)));
+                                    vn + (sedge[eo + u].succ * sn + nslot)));
 #pragma unroll
                         for (int u = 0; u < U; ++u)
                             if (eo + u < ee) {
-                                const double r = srew[eo + u];
+                                const double r = sedge[eo + u].reward;
                                 const double v[P] = {x[u].x, x[u].y}; // V_{k-1} of both versions
 #pragma unroll
                                 for (int p = 0; p < P; ++p) {
@@ -446,7 +456,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32, MINB) k_wave_layer(WaveArgs a
                             if (lo + j == a.m) { // exact value: V_{K*}(s) and the policy
                                 const uint64_t s = a.row0 + s0 + sl;
                                 a.values_out[s] = best[p];
-                                a.act_out[s] = best_e[p] >= 0 ? sact[best_e[p]] : -1;
+                                a.act_out[s] = best_e[p] >= 0 ? sedge[best_e[p]].action : -1;
                             }
                         }
                     }
@@ -650,6 +660,20 @@ void record_event(cudaEvent_t ev, cudaStream_t s, bool capturing) {
 }
 
 // Enqueue one wavefront solve on `s` (directly, or into a stream capture).
+// Raise a kernel's dynamic shared-memory limit on `device` to at least `smem` — only ever
+// upwards, and once per (kernel, device, size) (the attribute is per device context).
+void raise_smem_limit(const void* fn, int device, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> set;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& cur = set[{fn, device}];
+    if (smem <= cur) return;
+    const size_t want = std::max<size_t>(smem, 48 * 1024);
+    VCS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(want)));
+    cur = want;
+}
+
 // Launch k_wave_layer for the band [a.band_lo, a.band_hi) of one layer (a.row0 / n / m /
 // strides / bases set by the caller): tile size, shared memory, grid.
 void launch_layer(vcs_space* sp, WaveArgs& a, bool disc, cudaStream_t s) {
@@ -659,12 +683,17 @@ void launch_layer(vcs_space* sp, WaveArgs& a, bool disc, cudaStream_t s) {
         return e ? std::atoi(e) : 1;
     }();
     using LayerFn = void (*)(WaveArgs);
-    static const LayerFn fns[2][4] = {
-        {k_wave_layer<false, 8, 3>, k_wave_layer<false, 4, 4>, k_wave_layer<false, 4, 5>,
-         k_wave_layer<false, 2, 6>},
-        {k_wave_layer<true, 8, 3>, k_wave_layer<true, 4, 4>, k_wave_layer<true, 4, 5>,
-         k_wave_layer<true, 2, 6>}};
-    const LayerFn layer_fn = fns[disc ? 1 : 0][std::min(3, std::max(0, variant))];
+    static const LayerFn fns[2][2][4] = {
+        {{k_wave_layer<false, 8, 3, false>, k_wave_layer<false, 4, 4, false>,
+          k_wave_layer<false, 4, 5, false>, k_wave_layer<false, 2, 6, false>},
+         {k_wave_layer<true, 8, 3, false>, k_wave_layer<true, 4, 4, false>,
+          k_wave_layer<true, 4, 5, false>, k_wave_layer<true, 2, 6, false>}},
+        {{k_wave_layer<false, 8, 3, true>, k_wave_layer<false, 4, 4, true>,
+          k_wave_layer<false, 4, 5, true>, k_wave_layer<false, 2, 6, true>},
+         {k_wave_layer<true, 8, 3, true>, k_wave_layer<true, 4, 4, true>,
+          k_wave_layer<true, 4, 5, true>, k_wave_layer<true, 2, 6, true>}}};
+    const bool band = a.band_lo != 1 || a.base != 0 || a.base_next != 0;
+    const LayerFn layer_fn = fns[band ? 1 : 0][disc ? 1 : 0][std::min(3, std::max(0, variant))];
     const void* fn = reinterpret_cast<const void*>(layer_fn);
     const int nb = a.band_hi - a.band_lo;
     if (nb <= 0 || a.n == 0) return;
@@ -677,9 +706,7 @@ void launch_layer(vcs_space* sp, WaveArgs& a, bool disc, cudaStream_t s) {
     const size_t smem = static_cast<size_t>(nb) * 8 + static_cast<size_t>(a.tile) * (nb + 1) * 8 +
                         static_cast<size_t>(a.tile) * qcap * 16 + static_cast<size_t>(a.tile + 1) * 4;
     if (smem > 200 * 1024) raise(VCS_EINVAL, "horizon/out-degree too large for the wavefront tile");
-    // (per device context, so set on every launch rather than cached per process)
-    VCS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(std::max<size_t>(smem, 48 * 1024))));
+    raise_smem_limit(fn, sp->device, smem);
     int per_sm = 0;
     VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kWaveWarps * 32, smem));
     const uint64_t tiles = (a.n + a.tile - 1) / a.tile;
@@ -746,7 +773,7 @@ void record_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
         ++launches;
         // layer t's values/actions are final here (unless an early stop needs the fix-up):
         // lets vcs_solve stream them to the host while the remaining layers compute
-        record_event(g.layer_ev[static_cast<size_t>(t)], s, capturing);
+        if (!g.layer_ev.empty()) record_event(g.layer_ev[static_cast<size_t>(t)], s, capturing);
     }
     record_event(g.ev[1], s, capturing);
     int per_sm_ext = 0;
@@ -807,8 +834,11 @@ CachedGraph& enqueue_solve(vcs_space* sp, const GraphKey& key, cudaStream_t s) {
         g.method = key.method;
         g.n_sweeps = key.max_sweeps;
         for (auto& e : g.ev) VCS_CUDA(cudaEventCreate(&e));
-        g.layer_ev.assign(static_cast<size_t>(std::max(0, sp->H)), nullptr);
-        for (auto& e : g.layer_ev) VCS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        if (key.stream_out && key.method == kMethodWavefront) {
+            g.layer_ev.assign(static_cast<size_t>(std::max(0, sp->H)), nullptr);
+            for (auto& e : g.layer_ev)
+                VCS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
         it = sp->graphs.emplace(key, g).first;
     }
     CachedGraph& g = it->second;
@@ -947,7 +977,8 @@ using vcs::raise;
 
 extern "C" {
 
-int vcs_solve_enqueue(vcs_space* sp, const vcs_solve_opts* opts, void* stream) {
+namespace {
+int enqueue_impl(vcs_space* sp, const vcs_solve_opts* opts, void* stream, int stream_out) {
     return guarded([&] {
         vcs_solve_opts o{1e-6, 1, 0, 1.0, VCS_METHOD_AUTO};
         if (opts) o = *opts;
@@ -966,13 +997,18 @@ int vcs_solve_enqueue(vcs_space* sp, const vcs_solve_opts* opts, void* stream) {
             vcs::ensure_wave_buffers(sp);
         const vcs::GraphKey key{o.epsilon, o.discount,
                                 method == VCS_METHOD_JACOBI && o.skip_converged ? 1 : 0, M,
-                                method};
+                                method, method == VCS_METHOD_WAVEFRONT ? stream_out : 0};
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
         auto& g = vcs::enqueue_solve(sp, key, s);
         sp->last_graph = &g;
         sp->last_key_skip = key.skip;
         return VCS_OK;
     });
+}
+} // namespace
+
+int vcs_solve_enqueue(vcs_space* sp, const vcs_solve_opts* opts, void* stream) {
+    return enqueue_impl(sp, opts, stream, 0);
 }
 
 namespace {
@@ -989,12 +1025,12 @@ bool is_pinned(const void* p) {
 
 int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int32_t* actions_out,
               vcs_solve_report* report) {
-    const int rc = vcs_solve_enqueue(sp, opts, nullptr);
+    const bool pinned_out =
+        (values_out || actions_out) && is_pinned(values_out) && is_pinned(actions_out);
+    const int rc = enqueue_impl(sp, opts, nullptr, pinned_out ? 1 : 0);
     if (rc != VCS_OK) return rc;
     const vcs::CachedGraph& g = *sp->last_graph;
-    const bool overlap = g.method == vcs::kMethodWavefront && !g.layer_ev.empty() &&
-                         (values_out || actions_out) && is_pinned(values_out) &&
-                         is_pinned(actions_out);
+    const bool overlap = g.method == vcs::kMethodWavefront && !g.layer_ev.empty() && pinned_out;
     if (!overlap) return vcs_solve_collect(sp, values_out, actions_out, report, nullptr);
     // Stream each layer's values/actions to the (pinned) host buffers as soon as its layer
     // kernel finished — the 12 B/state download overlaps the rest of the layer pass.

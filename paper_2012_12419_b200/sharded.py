@@ -123,9 +123,17 @@ def halo_transfers(plans: list, rows_done: int) -> list:
 
 
 def run_sharded(backend, layer_offset: np.ndarray, layer_edges: np.ndarray, opts,
-                group=None, gather: bool = True):
+                group=None, gather: bool = True, mode: str = "halo",
+                local_out: tuple | None = None):
     """Sharded Jacobi VI.  Returns (values, actions, sweeps) on every rank when ``gather``
-    (full arrays), else (None, None, sweeps) with only this rank's block extracted."""
+    (full arrays), else (None, None, sweeps) with only this rank's block extracted.
+
+    ``mode`` is the per-sweep exchange: "halo" (forward halo, <= one layer per rank) or
+    "allgather" (the north-star form of SURVEY 8e: every rank receives all of V each sweep,
+    as padded equal blocks through all_gather_into_tensor).  ``local_out=(values, actions)``
+    receives only this rank's rows, with no gather collective."""
+    if mode not in ("halo", "allgather"):
+        raise ValueError(f"unknown exchange mode {mode!r}")
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     plans = shard_plans(layer_offset, layer_edges, world, skip_weighted=False)
@@ -140,10 +148,13 @@ def run_sharded(backend, layer_offset: np.ndarray, layer_edges: np.ndarray, opts
     if ctx is not None:
         ctx.__enter__()
     try:
-        sweeps = _sweeps(backend, plans, rank, world, layer_offset, opts, group, M, skip)
+        sweeps = _sweeps(backend, plans, rank, world, layer_offset, opts, group, M, skip, mode)
     finally:
         if ctx is not None:
             ctx.__exit__(None, None, None)
+    if local_out is not None:
+        sweeps = backend.finish(M, me.row_begin, me.row_end, opts, *local_out)
+        return local_out[0], local_out[1], sweeps
     values = np.zeros(S, np.float64) if gather else None
     actions = np.zeros(S, np.int32) if gather else None
     sweeps = backend.finish(M, me.row_begin, me.row_end, opts, values, actions)
@@ -158,12 +169,26 @@ def run_sharded(backend, layer_offset: np.ndarray, layer_edges: np.ndarray, opts
     return values, actions, sweeps
 
 
-def _sweeps(backend, plans, rank, world, layer_offset, opts, group, M, skip):
+def _sweeps(backend, plans, rank, world, layer_offset, opts, group, M, skip, mode="halo"):
     me = plans[rank]
     backend.begin(opts)
+    if mode == "allgather" and world > 1:
+        width = max(p.row_end - p.row_begin for p in plans)
+        stage = torch.zeros(world * width, dtype=torch.float64, device=backend.v0.device)
     for k in range(1, M + 1):
         backend.sweep(k, me.row_begin, me.row_end, opts)
         dist.all_reduce(backend.delta[k:k + 1], op=dist.ReduceOp.MAX, group=group)
+        if mode == "allgather" and world > 1 and k < M:
+            buf = backend.buffer(k)
+            n = me.row_end - me.row_begin
+            mine = stage[rank * width:rank * width + width]
+            mine[:n].copy_(buf[me.row_begin:me.row_end])
+            dist.all_gather_into_tensor(stage, mine, group=group)
+            for r, p in enumerate(plans):
+                if r != rank and p.row_end > p.row_begin:
+                    buf[p.row_begin:p.row_end].copy_(
+                        stage[r * width:r * width + p.row_end - p.row_begin])
+            continue
         if world > 1 and k < M:
             buf = backend.buffer(k)
             ops = []
@@ -263,10 +288,12 @@ def _first_converged(delta: np.ndarray, eps: float, M: int) -> int:
     return M
 
 
-def run_wave_sharded(backend, layer_offset: np.ndarray, opts, group=None, gather: bool = True):
+def run_wave_sharded(backend, layer_offset: np.ndarray, opts, group=None, gather: bool = True,
+                     local_out: tuple | None = None):
     """One rank of the band-sharded wavefront over torch.distributed (NCCL on B200s, gloo for
     CPU backends).  Returns (values, actions, sweeps); the arrays are full (gathered on every
-    rank) when ``gather``, else None."""
+    rank) when ``gather``, else None.  ``local_out=(values, actions)`` (host arrays of S
+    entries) receives only the rows this rank owns, with no gather collective."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     H = len(layer_offset) - 2
@@ -308,6 +335,9 @@ def run_wave_sharded(backend, layer_offset: np.ndarray, opts, group=None, gather
         if ctx is not None:
             ctx.__exit__(None, None, None)
     K = _first_converged(np.asarray(delta), opts.epsilon, M)
+    if local_out is not None:
+        backend.finish(K, local_out[0], local_out[1])
+        return local_out[0], local_out[1], K
     values = np.zeros(S, np.float64) if gather else None
     actions = np.zeros(S, np.int32) if gather else None
     backend.finish(K, values, actions)

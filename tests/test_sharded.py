@@ -76,7 +76,7 @@ def _instance(case):
     return V.generate_instance(N.VCS_GEN_RANDOM, seed, trial, 4, 6, 25, 3, as_objects=False)
 
 
-def _worker(rank, world, port, case, eps, skip, out_path):
+def _worker(rank, world, port, case, eps, skip, out_path, mode="halo"):
     import sys
     from pathlib import Path
     root = Path(__file__).resolve().parents[1]
@@ -92,7 +92,7 @@ def _worker(rank, world, port, case, eps, skip, out_path):
         le = np.array([rp[lo[t + 1]] - rp[lo[t]] for t in range(sp.H + 1)], np.uint64)
         opts = N.vcs_solve_opts(eps, 1 if skip else 0, 0, 1.0)
         backend = OracleRowBackend(orc, sp, lo)
-        values, actions, sweeps = run_sharded(backend, lo, le, opts)
+        values, actions, sweeps = run_sharded(backend, lo, le, opts, mode=mode)
         if rank == 0:
             np.savez(out_path, values=values, actions=actions, sweeps=sweeps)
     finally:
@@ -119,6 +119,22 @@ def test_sharded_driver_bit_identical(oracle, world, case, eps, skip):
     ni = _instance(case)  # keep the SoA arrays alive across the C call
     sp = oracle.build(ni.ref, 10**9)
     v, a, sw, _, _ = sp.vi(eps=eps)
+    assert int(got["sweeps"]) == sw
+    assert np.array_equal(got["values"].view(np.uint64), v.view(np.uint64))
+    assert np.array_equal(got["actions"], a)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case,eps,skip", [("canonical", 1e-6, True), ((47, 5), 0.7, False)])
+def test_sharded_allgather_bit_identical(oracle, world, case, eps, skip):
+    """The north-star exchange (full all-gather of V every sweep) gives the same bits."""
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "r.npz")
+        mp.spawn(_worker, args=(world, _free_port(), case, eps, skip, out, "allgather"),
+                 nprocs=world, join=True)
+        got = np.load(out)
+    ni = _instance(case)
+    v, a, sw, _, _ = oracle.build(ni.ref, 10**9).vi(eps=eps)
     assert int(got["sweeps"]) == sw
     assert np.array_equal(got["values"].view(np.uint64), v.view(np.uint64))
     assert np.array_equal(got["actions"], a)
