@@ -167,6 +167,8 @@ struct vcs_space {
 };
 
 namespace vcs {
+bool trace_enabled(); // VCS_TRACE set: host-side phase timings on stderr
+double host_ms();
 void bind_device(int device);
 int sm_count(int device);
 }

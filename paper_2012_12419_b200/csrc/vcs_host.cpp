@@ -320,6 +320,15 @@ LayerPlan make_layer_plan(const vcs_instance* in) {
         // the full reward expression with nothing retired (same two rounded operations)
         L.r_cloud_kept = L.r_cloud - L.gamma * 0.0;
         L.r_paid_kept = L.r_paid - L.gamma * 0.0;
+        // mixed-radix weights of layer t+1's fields (dense successor index)
+        std::vector<uint32_t> wq;
+        uint64_t W = 1;
+        for (int c : pl.active[t + 1]) {
+            wq.push_back(static_cast<uint32_t>(W));
+            W *= static_cast<uint64_t>(std::max(0, in->cloud_vm_free[c])) + 1;
+            if (W > kDenseMax) break;
+        }
+        L.dense_size = W <= kDenseMax ? static_cast<uint32_t>(W) : 0u;
         int kept = 0;
         for (std::size_t p = 0; p < act.size(); ++p) {
             const int c = act[p];
@@ -327,9 +336,11 @@ LayerPlan make_layer_plan(const vcs_instance* in) {
             L.attr[p] = attr[c][t];
             L.width[p] = static_cast<uint8_t>(pl.width_of_cloud[c]);
             L.bit_off[p] = pl.bit_off[t][p];
+            L.radix[p] = static_cast<uint32_t>(std::max(0, in->cloud_vm_free[c]) + 1);
             if (pl.last_use[c] >= t + 1) {
                 L.keep_idx[p] = static_cast<int8_t>(kept);
                 L.next_bit_off[p] = pl.bit_off[t + 1][kept];
+                if (L.dense_size) L.wnext[p] = wq[static_cast<std::size_t>(kept)];
                 ++kept;
             } else {
                 L.keep_idx[p] = -1;

@@ -73,7 +73,17 @@ struct LayerParam {
     uint16_t bit_off[kMaxActive];      // bit offset of field p in the layer-t packed key
     uint16_t next_bit_off[kMaxActive]; // bit offset of field keep_idx[p] in the next packed key
     uint8_t width[kMaxActive];   // bit width of field p
+    // Dense successor index (when the layer-(t+1) key space is small): a layer-(t+1) key is a
+    // vector of free-VM counts f_q in [0, free_q], so idx = sum_q f_q * W_q with mixed-radix
+    // weights W_q = prod_{q' < q} (free_q' + 1) numbers the key space 0 .. dense_size-1.
+    uint32_t dense_size;         // prod (free_q + 1) over layer t+1's fields; 0 = too large
+    int32_t pad1;
+    uint32_t wnext[kMaxActive];  // W of field keep_idx[p] in layer t+1 (0 if p retires)
+    uint32_t radix[kMaxActive];  // free_{cloud[p]} + 1
 };
+
+// Dense successor indices are used up to this key-space size (a 4-byte first-edge table).
+constexpr uint64_t kDenseMax = 1ull << 26;
 
 struct LayerPlan {
     int horizon = 0;

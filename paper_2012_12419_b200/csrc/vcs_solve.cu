@@ -643,7 +643,13 @@ bool wavefront_fits(const vcs_space* sp) {
 void ensure_wave_buffers(vcs_space* sp) {
     std::vector<uint64_t> off;
     const uint64_t nv = wave_versions(sp, &off);
+    const double t0 = trace_enabled() ? host_ms() : 0.0;
     sp->ver.exact(std::max<uint64_t>(nv, 1), sp->stream);
+    if (trace_enabled()) {
+        cudaStreamSynchronize(sp->stream);
+        std::fprintf(stderr, "[vcs solve] version store %.1f MB alloc %.3f ms\n", nv * 8e-6,
+                     host_ms() - t0);
+    }
     sp->ver_off.exact(off.size(), sp->stream);
     sp->layer_off_dev.exact(sp->layer_off.size(), sp->stream);
     VCS_CUDA(cudaMemcpy(sp->ver_off.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
@@ -846,6 +852,7 @@ CachedGraph& enqueue_solve(vcs_space* sp, const GraphKey& key, cudaStream_t s) {
     // enqueueing it directly, whose host work between short layer kernels idles the GPU, so
     // even a one-shot solve goes through the graph.)
     if (!g.exec) {
+        const double t0 = trace_enabled() ? host_ms() : 0.0;
         cudaStream_t cs = sp->stream;
         if (cs != s) VCS_CUDA(cudaStreamSynchronize(s)); // no cross-stream work pending
         VCS_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
@@ -864,6 +871,8 @@ CachedGraph& enqueue_solve(vcs_space* sp, const GraphKey& key, cudaStream_t s) {
         cudaGraphDestroy(graph);
         if (ierr != cudaSuccess)
             raise(VCS_ECUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ierr));
+        if (trace_enabled())
+            std::fprintf(stderr, "[vcs solve] capture+instantiate %.3f ms\n", host_ms() - t0);
     }
     VCS_CUDA(cudaGraphLaunch(g.exec, s));
     note_launch(static_cast<uint64_t>(g.launches));
@@ -872,12 +881,14 @@ CachedGraph& enqueue_solve(vcs_space* sp, const GraphKey& key, cudaStream_t s) {
 }
 
 void ensure_solve_buffers(vcs_space* sp, int max_sweeps) {
+    const double t0 = trace_enabled() ? host_ms() : 0.0;
     sp->v[0].exact(sp->S, sp->stream);
     sp->v[1].exact(sp->S, sp->stream);
     sp->delta.exact(static_cast<size_t>(max_sweeps) + 2, sp->stream);
     sp->ctrl.exact(1, sp->stream);
     sp->actions_dev.exact(sp->S, sp->stream);
     VCS_CUDA(cudaStreamSynchronize(sp->stream)); // pool allocations ready for any stream
+    if (trace_enabled()) std::fprintf(stderr, "[vcs solve] solve buffers %.3f ms\n", host_ms() - t0);
 }
 
 // ---- version-band sharding of the wavefront (multi-GPU) ---------------------------------------
@@ -989,12 +1000,15 @@ int enqueue_impl(vcs_space* sp, const vcs_solve_opts* opts, void* stream, int st
         vcs::bind_device(sp->device);
         int M = sp->H + 1; // delta_{H+1} == 0 on the layered DAG, so this is never binding
         if (o.max_sweeps > 0) M = std::min(M, o.max_sweeps);
+        const double t0 = vcs::trace_enabled() ? vcs::host_ms() : 0.0;
         vcs::ensure_solve_buffers(sp, sp->H + 1); // fixed size: cached graphs keep addresses
         int method = o.method;
         if (method == VCS_METHOD_AUTO)
             method = vcs::wavefront_fits(sp) ? VCS_METHOD_WAVEFRONT : VCS_METHOD_JACOBI;
         if (method == VCS_METHOD_WAVEFRONT && sp->ver_off_host.empty())
             vcs::ensure_wave_buffers(sp);
+        if (vcs::trace_enabled())
+            std::fprintf(stderr, "[vcs solve] buffers %.3f ms\n", vcs::host_ms() - t0);
         const vcs::GraphKey key{o.epsilon, o.discount,
                                 method == VCS_METHOD_JACOBI && o.skip_converged ? 1 : 0, M,
                                 method, method == VCS_METHOD_WAVEFRONT ? stream_out : 0};
@@ -1025,6 +1039,14 @@ bool is_pinned(const void* p) {
 
 int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int32_t* actions_out,
               vcs_solve_report* report) {
+    const double t_start = vcs::trace_enabled() ? vcs::host_ms() : 0.0;
+    struct TraceEnd {
+        double t0;
+        ~TraceEnd() {
+            if (vcs::trace_enabled())
+                std::fprintf(stderr, "[vcs solve] vcs_solve total %.3f ms\n", vcs::host_ms() - t0);
+        }
+    } trace_end{t_start};
     const bool pinned_out =
         (values_out || actions_out) && is_pinned(values_out) && is_pinned(actions_out);
     const int rc = enqueue_impl(sp, opts, nullptr, pinned_out ? 1 : 0);

@@ -2,21 +2,26 @@
 // the device key index behind locate (mdp.cpp:227-234), and the space handle.
 //
 // Layered frontier expansion, one layer (decision epoch) at a time:
-//   1. k_count     out-degree of every frontier state (feasible active clouds + paid)
-//   2. scan        exclusive sum -> CSR row offsets (edge order of the reference: clouds
-//                  ascending, paid last, mdp.cpp:169-204)
-//   3. k_emit      per edge: packed successor key, fp64 reward (separate mul/sub, no FMA,
-//                  = mdp.cpp:191/202 bits), action
-//   4. k_insert    hash every successor key; each slot keeps the MINIMUM edge index carrying
-//                  that key (atomicMin) = its first occurrence in the reference's BFS
-//   5. k_mark/scan a successor's layer-local index is the rank of its first edge among all
-//                  first edges -> exactly the reference's first-insertion order (mdp.cpp:157-165)
-//   6. k_finalize  successor indices + next-frontier keys
+//   1. scan        out-degree of every frontier state (feasible active clouds + paid, computed
+//                  inside the scan's input iterator) -> CSR row offsets (edge order of the
+//                  reference: clouds ascending, paid last, mdp.cpp:169-204)
+//   2. k_emit      per edge: successor, fp64 reward (separate mul/sub, no FMA, = mdp.cpp:191/202
+//                  bits), action.  Each successor gets a table slot that keeps the MINIMUM edge
+//                  index carrying it (atomicMin) = its first occurrence in the reference's BFS:
+//                  dense path (small key space): slot = the successor's mixed-radix index,
+//                  written by k_emit itself into an L2-resident table;
+//                  hash path: k_emit writes packed successor keys, k_insert hashes them.
+//   3. scan        a successor's layer-local index is the rank of its first edge among all
+//                  first edges (flags computed inside the scan's input iterator) -> exactly the
+//                  reference's first-insertion order (mdp.cpp:157-165)
+//   4. k_finalize  successor indices + next-frontier keys
 // Keys are the reference's reduced keys (free counts of still-eligible clouds, mdp.hpp:70-79)
 // packed into 64-bit words, ceil(log2(vm_free+1)) bits per cloud.
 #include "vcs_device.cuh"
 
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include <algorithm>
 #include <chrono>
@@ -81,22 +86,37 @@ __device__ __forceinline__ void put_field(uint64_t (&k)[WM], int off, uint64_t v
         if (i == w) k[i] |= v << (off & 63);
 }
 
+// Out-degree of frontier state i (the paid edge always exists), 0 past the frontier: the input
+// of the row-offset scan.
+// (The layer's parameters are read through a pointer: a functor holding the ~1.3 KB struct by
+// value would be copied to local memory inside the scan kernel.)
 template <int WM>
-__global__ void k_count(uint32_t n, const uint64_t* __restrict__ keys, const LayerParam L,
-                        uint32_t* __restrict__ deg) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i > n) return;
-    if (i == n) {
-        deg[n] = 0;
-        return;
+struct DegreeOp {
+    const uint64_t* keys;
+    uint32_t n;
+    const LayerParam* L;
+    __device__ uint32_t operator()(uint32_t i) const {
+        if (i >= n) return 0u;
+        const int words = L->words, n_active = L->n_active, demand = L->demand;
+        uint64_t k[WM];
+        load_key<WM>(keys + static_cast<uint64_t>(i) * words, words, k);
+        uint32_t d = 1;
+        for (int p = 0; p < n_active; ++p)
+            if (L->attr[p] && get_field<WM>(k, L->bit_off[p], L->width[p]) >= demand) ++d;
+        return d;
     }
-    uint64_t k[WM];
-    load_key<WM>(keys + static_cast<uint64_t>(i) * L.words, L.words, k);
-    uint32_t d = 1; // the paid edge always exists
-    for (int p = 0; p < L.n_active; ++p)
-        if (L.attr[p] && get_field<WM>(k, L.bit_off[p], L.width[p]) >= L.demand) ++d;
-    deg[i] = d;
-}
+};
+
+// flag(j) = 1 iff edge j is the first occurrence of its successor (the table slot holds the
+// minimum edge index); 0 past E_t, so a scan over the launch bound gives rank[E_t] = n_{t+1}.
+struct FirstEdgeOp {
+    const uint32_t* n_edges_dev;
+    const uint32_t* table;
+    const uint32_t* slot_of;
+    __device__ uint32_t operator()(uint32_t j) const {
+        return j < *n_edges_dev && table[slot_of[j]] == j ? 1u : 0u;
+    }
+};
 
 // One edge: successor key in the layer-(t+1) packing, reward, action.  `p` = key position of
 // the chosen cloud, or -1 for the paid cloud.
@@ -124,6 +144,58 @@ __device__ __forceinline__ void emit_edge(const uint64_t (&k)[WM], int p, const 
     const double base = p < 0 ? L.r_paid : L.r_cloud;
     *rw = __dsub_rn(base, __dmul_rn(L.gamma, retired));
     *act = p < 0 ? -1 : L.cloud[p];
+}
+
+// Reward of one edge when clouds retire at this transition (mdp.cpp:179-185 / :196-197):
+// beta*n - gamma*retired, retired summed in key-position order.  p = -1: the paid cloud.
+template <int WM>
+__device__ __forceinline__ double retiring_reward(const uint64_t (&k)[WM], int p,
+                                                  const LayerParam& L) {
+    double retired = 0.0;
+    for (int q = 0; q < L.n_active; ++q) {
+        if (L.keep_idx[q] >= 0) continue;
+        int v = get_field<WM>(k, L.bit_off[q], L.width[q]);
+        if (q == p) v -= L.demand;
+        retired = __dadd_rn(retired, static_cast<double>(v));
+    }
+    const double base = p < 0 ? L.r_paid : L.r_cloud;
+    return __dsub_rn(base, __dmul_rn(L.gamma, retired));
+}
+
+// Dense path: the successor of an edge is identified by its mixed-radix index; the first-edge
+// table (dense_size entries, L2-resident) is updated right here.  idx(paid successor) =
+// sum over kept fields of f_p * W_p; a cloud action subtracts demand * W_p when p is kept.
+template <int WM>
+__global__ void k_emit_dense(uint32_t n, const uint64_t* __restrict__ keys,
+                             const uint32_t* __restrict__ off, const LayerParam L,
+                             uint32_t edge_base, uint32_t* __restrict__ row_ptr_layer,
+                             uint32_t* __restrict__ eidx, double* __restrict__ reward,
+                             int32_t* __restrict__ action, uint32_t* __restrict__ first_edge) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint64_t k[WM];
+    load_key<WM>(keys + static_cast<uint64_t>(i) * L.words, L.words, k);
+    uint32_t j = off[i];
+    row_ptr_layer[i] = edge_base + j;
+    uint32_t base = 0;
+    for (int p = 0; p < L.n_active; ++p)
+        if (L.keep_idx[p] >= 0)
+            base += static_cast<uint32_t>(get_field<WM>(k, L.bit_off[p], L.width[p])) * L.wnext[p];
+    const bool retires = L.n_keep != L.n_active;
+    auto put = [&](uint32_t idx, double r, int32_t a) {
+        eidx[j] = idx;
+        reward[edge_base + j] = r;
+        action[edge_base + j] = a;
+        if (first_edge[idx] > j) atomicMin(&first_edge[idx], j);
+        ++j;
+    };
+    for (int p = 0; p < L.n_active; ++p) {
+        if (!L.attr[p] || get_field<WM>(k, L.bit_off[p], L.width[p]) < L.demand) continue;
+        const uint32_t idx =
+            L.keep_idx[p] >= 0 ? base - static_cast<uint32_t>(L.demand) * L.wnext[p] : base;
+        put(idx, retires ? retiring_reward<WM>(k, p, L) : L.r_cloud_kept, L.cloud[p]);
+    }
+    put(base, retires ? retiring_reward<WM>(k, -1, L) : L.r_paid_kept, -1);
 }
 
 template <int WM>
@@ -225,17 +297,6 @@ __global__ void k_insert_kv(const uint32_t* __restrict__ n_edges_dev,
     slot_of[j] = h;
 }
 
-// flag[j] = 1 iff edge j is the first occurrence of its successor; zeros past E_t up to the
-// launch bound so the scan over the bound yields rank[E_t] = n_{t+1}
-__global__ void k_mark(const uint32_t* __restrict__ n_edges_dev, uint32_t bound,
-                       const uint32_t* __restrict__ table, const uint32_t* __restrict__ slot_of,
-                       uint32_t* __restrict__ flag) {
-    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j > bound) return;
-    const uint32_t n_edges = *n_edges_dev;
-    flag[j] = j < n_edges ? (table[slot_of[j]] == j ? 1u : 0u) : 0u;
-}
-
 __global__ void k_finalize(const uint32_t* __restrict__ n_edges_dev, const uint32_t* __restrict__ table,
                            const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ rank,
                            const uint64_t* __restrict__ ekeys, int words, uint32_t next_base,
@@ -249,6 +310,32 @@ __global__ void k_finalize(const uint32_t* __restrict__ n_edges_dev, const uint3
         uint64_t* dst = next_keys + static_cast<uint64_t>(rank[j]) * words;
         for (int w = 0; w < words; ++w) dst[w] = src[w];
     }
+}
+
+// Dense path: successor indices; a first edge also writes its successor's packed key, decoded
+// from the mixed-radix index.
+template <int WM>
+__global__ void k_finalize_dense(const uint32_t* __restrict__ n_edges_dev,
+                                 const uint32_t* __restrict__ first_edge,
+                                 const uint32_t* __restrict__ eidx, const uint32_t* __restrict__ rank,
+                                 const LayerParam L, uint32_t next_base,
+                                 uint32_t* __restrict__ succ, uint64_t* __restrict__ next_keys) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= *n_edges_dev) return;
+    const uint32_t idx = eidx[j];
+    const uint32_t first = first_edge[idx];
+    succ[j] = next_base + rank[first];
+    if (first != j) return;
+    uint64_t nk[WM];
+#pragma unroll
+    for (int w = 0; w < WM; ++w) nk[w] = 0ull;
+    for (int p = 0; p < L.n_active; ++p)
+        if (L.keep_idx[p] >= 0)
+            put_field<WM>(nk, L.next_bit_off[p], (idx / L.wnext[p]) % L.radix[p]);
+    uint64_t* dst = next_keys + static_cast<uint64_t>(rank[j]) * L.next_words;
+#pragma unroll
+    for (int w = 0; w < WM; ++w)
+        if (w < L.next_words) dst[w] = nk[w];
 }
 
 __global__ void k_fill_u32(uint32_t* __restrict__ p, uint64_t n, uint32_t v) {
@@ -314,17 +401,6 @@ __global__ void k_loc_lookup(int64_t n, const LocQuery* __restrict__ q,
     }
 }
 
-bool trace_enabled() {
-    static const bool on = std::getenv("VCS_TRACE") != nullptr;
-    return on;
-}
-
-double host_ms() {
-    return std::chrono::duration<double, std::milli>(
-               std::chrono::steady_clock::now().time_since_epoch())
-        .count();
-}
-
 uint32_t blocks_for(uint64_t n, uint32_t threads) {
     return static_cast<uint32_t>((n + threads - 1) / threads);
 }
@@ -350,8 +426,9 @@ __global__ void k_counters(const uint32_t* __restrict__ off_end, const uint32_t*
 }
 
 struct Scratch {
-    DevBuf<uint32_t> deg, off, slot, flag, rank, table;
+    DevBuf<uint32_t> off, slot, rank, table, eidx;
     DevBuf<uint64_t> ekeys, tkey;
+    DevBuf<LayerParam> params; // every layer's LayerParam (read by the degree scan)
     DevBuf<uint8_t> cub_tmp;
     LayerCounters* counters = nullptr;     // mapped pinned host memory
     LayerCounters* counters_dev = nullptr; // its device alias
@@ -360,7 +437,8 @@ struct Scratch {
     }
 };
 
-void exclusive_scan(Scratch& sc, const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t s) {
+template <class InputIt>
+void exclusive_scan(Scratch& sc, InputIt in, uint32_t* out, uint64_t n, cudaStream_t s) {
     size_t bytes = 0;
     VCS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, static_cast<int64_t>(n), s));
     sc.cub_tmp.exact(bytes, s);
@@ -380,6 +458,11 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
     VCS_CUDA(cudaHostAlloc(&sc.counters, sizeof(LayerCounters), cudaHostAllocMapped));
     VCS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&sc.counters_dev), sc.counters, 0));
 
+    if (H > 0) {
+        sc.params.exact(static_cast<size_t>(H), s);
+        VCS_CUDA(cudaMemcpyAsync(sc.params.p, pl.layers.data(), H * sizeof(LayerParam),
+                                 cudaMemcpyHostToDevice, s));
+    }
     sp->layer_off.assign(static_cast<size_t>(H) + 2, 0);
     sp->layer_edges.assign(static_cast<size_t>(H) + 1, 0);
     sp->key_off.assign(static_cast<size_t>(H) + 2, 0);
@@ -406,12 +489,13 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
         if (E + e_ub >= 0xffffffffull)
             raise(VCS_EINVAL, "more than 2^32-1 transitions are not supported");
 
-        sc.deg.exact(n_t + 1, s);
         sc.off.exact(n_t + 1, s);
-        k_count<WM><<<blocks_for(n_t + 1, T), T, 0, s>>>(static_cast<uint32_t>(n_t),
-                                                         sp->keys.p + key_t, L, sc.deg.p);
-        VCS_LAUNCHED();
-        exclusive_scan(sc, sc.deg.p, sc.off.p, n_t + 1, s);
+        exclusive_scan(sc,
+                       thrust::make_transform_iterator(
+                           thrust::counting_iterator<uint32_t>(0),
+                           DegreeOp<WM>{sp->keys.p + key_t, static_cast<uint32_t>(n_t),
+                                        sc.params.p + t}),
+                       sc.off.p, n_t + 1, s);
         const uint32_t* e_dev = sc.off.p + n_t; // exact E_t on the device
 
         const uint64_t row0 = sp->layer_off[static_cast<size_t>(t)];
@@ -419,40 +503,65 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
         sp->succ.reserve(E + e_ub, E, s);
         sp->reward.reserve(E + e_ub, E, s);
         sp->action.reserve(E + e_ub, E, s);
-        sc.ekeys.exact(e_ub * static_cast<uint64_t>(L.next_words), s);
-        k_emit<WM><<<blocks_for(n_t, T), T, 0, s>>>(
-            static_cast<uint32_t>(n_t), sp->keys.p + key_t, sc.off.p, L, static_cast<uint32_t>(E),
-            sp->row_ptr.p + row0, sc.ekeys.p, sp->reward.p, sp->action.p);
-        VCS_LAUNCHED();
-
-        const uint64_t cap = pow2_at_least(2 * e_ub);
-        sc.table.exact(cap, s);
-        sc.slot.exact(e_ub, s);
-        sc.flag.exact(e_ub + 1, s);
-        sc.rank.exact(e_ub + 1, s);
-        VCS_CUDA(cudaMemsetAsync(sc.table.p, 0xff, cap * sizeof(uint32_t), s));
-        if (L.next_words == 1 && pl.key_bits[static_cast<size_t>(t) + 1] < 64) {
-            sc.tkey.exact(cap, s);
-            VCS_CUDA(cudaMemsetAsync(sc.tkey.p, 0xff, cap * sizeof(uint64_t), s));
-            k_insert_kv<<<blocks_for(e_ub, T), T, 0, s>>>(
-                e_dev, sc.ekeys.p, reinterpret_cast<unsigned long long*>(sc.tkey.p), sc.table.p,
-                static_cast<uint32_t>(cap - 1), sc.slot.p);
-        } else {
-            k_insert<WM><<<blocks_for(e_ub, T), T, 0, s>>>(e_dev, sc.ekeys.p, L.next_words,
-                                                           sc.table.p, static_cast<uint32_t>(cap - 1),
-                                                           sc.slot.p);
-        }
-        VCS_LAUNCHED();
-        k_mark<<<blocks_for(e_ub + 1, T), T, 0, s>>>(e_dev, static_cast<uint32_t>(e_ub), sc.table.p,
-                                                     sc.slot.p, sc.flag.p);
-        VCS_LAUNCHED();
-        exclusive_scan(sc, sc.flag.p, sc.rank.p, e_ub + 1, s); // zeros past E_t: rank[E_t] = n_{t+1}
         const uint64_t key_next = sp->key_off[static_cast<size_t>(t) + 1];
         sp->keys.reserve(key_next + e_ub * static_cast<uint64_t>(L.next_words), key_next, s);
-        k_finalize<<<blocks_for(e_ub, T), T, 0, s>>>(
-            e_dev, sc.table.p, sc.slot.p, sc.rank.p, sc.ekeys.p, L.next_words,
-            static_cast<uint32_t>(S), sp->succ.p + E, sp->keys.p + key_next);
-        VCS_LAUNCHED();
+        sc.rank.exact(e_ub + 1, s);
+        const uint64_t cap = pow2_at_least(2 * e_ub);
+        // dense successor indices when the next key space is small: a first-edge table of
+        // dense_size words instead of a hash table of 2*E_t slots
+        const bool dense = L.dense_size != 0 &&
+                           static_cast<uint64_t>(L.dense_size) * 4 <=
+                               std::max<uint64_t>(16ull << 20, cap * 12);
+        if (dense) {
+            sc.table.exact(L.dense_size, s);
+            sc.eidx.exact(e_ub, s);
+            VCS_CUDA(cudaMemsetAsync(sc.table.p, 0xff, L.dense_size * sizeof(uint32_t), s));
+            k_emit_dense<WM><<<blocks_for(n_t, T), T, 0, s>>>(
+                static_cast<uint32_t>(n_t), sp->keys.p + key_t, sc.off.p, L,
+                static_cast<uint32_t>(E), sp->row_ptr.p + row0, sc.eidx.p, sp->reward.p,
+                sp->action.p, sc.table.p);
+            VCS_LAUNCHED();
+            exclusive_scan(sc,
+                           thrust::make_transform_iterator(
+                               thrust::counting_iterator<uint32_t>(0),
+                               FirstEdgeOp{e_dev, sc.table.p, sc.eidx.p}),
+                           sc.rank.p, e_ub + 1, s); // rank[E_t] = n_{t+1}
+            k_finalize_dense<WM><<<blocks_for(e_ub, T), T, 0, s>>>(
+                e_dev, sc.table.p, sc.eidx.p, sc.rank.p, L, static_cast<uint32_t>(S),
+                sp->succ.p + E, sp->keys.p + key_next);
+            VCS_LAUNCHED();
+        } else {
+            sc.ekeys.exact(e_ub * static_cast<uint64_t>(L.next_words), s);
+            k_emit<WM><<<blocks_for(n_t, T), T, 0, s>>>(
+                static_cast<uint32_t>(n_t), sp->keys.p + key_t, sc.off.p, L,
+                static_cast<uint32_t>(E), sp->row_ptr.p + row0, sc.ekeys.p, sp->reward.p,
+                sp->action.p);
+            VCS_LAUNCHED();
+            sc.table.exact(cap, s);
+            sc.slot.exact(e_ub, s);
+            VCS_CUDA(cudaMemsetAsync(sc.table.p, 0xff, cap * sizeof(uint32_t), s));
+            if (L.next_words == 1 && pl.key_bits[static_cast<size_t>(t) + 1] < 64) {
+                sc.tkey.exact(cap, s);
+                VCS_CUDA(cudaMemsetAsync(sc.tkey.p, 0xff, cap * sizeof(uint64_t), s));
+                k_insert_kv<<<blocks_for(e_ub, T), T, 0, s>>>(
+                    e_dev, sc.ekeys.p, reinterpret_cast<unsigned long long*>(sc.tkey.p),
+                    sc.table.p, static_cast<uint32_t>(cap - 1), sc.slot.p);
+            } else {
+                k_insert<WM><<<blocks_for(e_ub, T), T, 0, s>>>(
+                    e_dev, sc.ekeys.p, L.next_words, sc.table.p, static_cast<uint32_t>(cap - 1),
+                    sc.slot.p);
+            }
+            VCS_LAUNCHED();
+            exclusive_scan(sc,
+                           thrust::make_transform_iterator(
+                               thrust::counting_iterator<uint32_t>(0),
+                               FirstEdgeOp{e_dev, sc.table.p, sc.slot.p}),
+                           sc.rank.p, e_ub + 1, s); // rank[E_t] = n_{t+1}
+            k_finalize<<<blocks_for(e_ub, T), T, 0, s>>>(
+                e_dev, sc.table.p, sc.slot.p, sc.rank.p, sc.ekeys.p, L.next_words,
+                static_cast<uint32_t>(S), sp->succ.p + E, sp->keys.p + key_next);
+            VCS_LAUNCHED();
+        }
         k_counters<<<1, 1, 0, s>>>(e_dev, sc.rank.p, sc.counters_dev);
         VCS_LAUNCHED();
         VCS_CUDA(cudaStreamSynchronize(s)); // the layer's single host round trip
@@ -538,6 +647,17 @@ void ensure_locate_index(vcs_space* sp) {
 }
 
 } // namespace
+
+bool trace_enabled() {
+    static const bool on = std::getenv("VCS_TRACE") != nullptr;
+    return on;
+}
+
+double host_ms() {
+    return std::chrono::duration<double, std::milli>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
 
 void bind_device(int device) {
     int n = 0;
