@@ -34,8 +34,19 @@ constexpr uint32_t kEmpty32 = 0xffffffffu;
 // (building and freeing spaces repeatedly then costs no cudaMalloc / implicit device sync).
 void init_pool(int device);
 
-// RAII device buffer on the stream-ordered allocator (cudaMallocAsync / cudaFreeAsync on the
-// owner's stream), growable with copy.
+// Device allocation on the stream-ordered pool.  Requests of kBigBlock bytes or more are first
+// served from a per-device cache of IDLE large blocks (best fit, never split) that freed spaces
+// leave behind: a build + solve of the same instance then re-uses exactly the blocks of the
+// previous one instead of depending on the pool's (fragmenting) free lists.  `*got` = bytes.
+constexpr size_t kBigBlock = size_t(16) << 20;
+void* dev_alloc(size_t bytes, cudaStream_t s, size_t* got);
+size_t device_bytes(int device); // total device memory (cached per device)
+// Give back a block no pending work uses (its stream was synchronised): big blocks go to the
+// cache (bounded; the oldest are freed past the bound), others to the pool on stream `s`.
+void dev_release_idle(void* p, size_t bytes, cudaStream_t s);
+
+// RAII device buffer on the stream-ordered allocator (cudaFreeAsync on the owner's stream),
+// growable with copy.
 template <class T>
 struct DevBuf {
     T* p = nullptr;
@@ -50,28 +61,36 @@ struct DevBuf {
         p = nullptr;
         n = 0;
     }
+    // The owner's stream is synchronised: hand the block to the big-block cache.
+    void release_idle() {
+        if (p) dev_release_idle(p, n * sizeof(T), st);
+        p = nullptr;
+        n = 0;
+    }
     // Ensure capacity >= want; keeps the first `keep` elements when it must reallocate.
     void reserve(size_t want, size_t keep, cudaStream_t s, double growth = 2.0) {
         if (want <= n) return;
         size_t cap = n ? static_cast<size_t>(static_cast<double>(n) * growth) : want;
         if (cap < want) cap = want;
-        T* np = nullptr;
-        VCS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&np), cap * sizeof(T), s));
+        size_t got = 0;
+        T* np = static_cast<T*>(dev_alloc(cap * sizeof(T), s, &got));
         if (p && keep)
             VCS_CUDA(cudaMemcpyAsync(np, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, s));
         if (p) VCS_CUDA(cudaFreeAsync(p, s));
         p = np;
-        n = cap;
+        n = got / sizeof(T);
         st = s;
     }
     // Discard contents; capacity >= `want` (grows geometrically to amortise re-allocation).
     void exact(size_t want, cudaStream_t s) {
         if (want <= n) return;
+        const size_t cap = std::max<size_t>(want ? want : 1, n + n / 2);
         if (p) VCS_CUDA(cudaFreeAsync(p, s));
         p = nullptr;
-        const size_t cap = std::max<size_t>(want ? want : 1, n + n / 2);
-        VCS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), cap * sizeof(T), s));
-        n = cap;
+        n = 0; // stays empty if the allocation below throws
+        size_t got = 0;
+        p = static_cast<T*>(dev_alloc(cap * sizeof(T), s, &got));
+        n = got / sizeof(T);
         st = s;
     }
 };
@@ -163,8 +182,35 @@ struct vcs_space {
     uint64_t loc_cap = 0;
 
     int num_sms = 148;
+    // caller streams that have run work on this space: the destructor waits for their last
+    // recorded use before the space's blocks can be reused
+    std::map<cudaStream_t, cudaEvent_t> use_ev;
     ~vcs_space();
 };
+
+namespace vcs {
+// The stream an entry point enqueues on (the caller's, or the space's own when null).  On scope
+// exit it records the caller stream's progress so vcs_space_free can wait for it.
+struct StreamUse {
+    vcs_space* sp;
+    cudaStream_t s;
+    StreamUse(vcs_space* space, void* stream)
+        : sp(space), s(stream ? static_cast<cudaStream_t>(stream) : space->stream) {}
+    StreamUse(const StreamUse&) = delete;
+    StreamUse& operator=(const StreamUse&) = delete;
+    ~StreamUse() {
+        if (s == sp->stream) return;
+        cudaEvent_t& ev = sp->use_ev[s];
+        if (!ev && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+            ev = nullptr;
+            cudaStreamSynchronize(s); // cannot track it: finish it now
+            return;
+        }
+        cudaEventRecord(ev, s);
+    }
+    operator cudaStream_t() const { return s; }
+};
+} // namespace vcs
 
 namespace vcs {
 bool trace_enabled(); // VCS_TRACE set: host-side phase timings on stderr

@@ -633,11 +633,11 @@ uint64_t wave_backups(const vcs_space* sp) {
     return tot;
 }
 
+// (cudaMemGetInfo is avoided: it can stall for milliseconds; an allocation that still fails
+// makes VCS_METHOD_AUTO fall back to Jacobi.)
 bool wavefront_fits(const vcs_space* sp) {
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return false;
     const uint64_t need = wave_versions(sp) * sizeof(double) + (sp->H + 2) * 16;
-    return sp->ver.n >= wave_versions(sp) || need < free_b / 2;
+    return sp->ver.n >= wave_versions(sp) || need < device_bytes(sp->device) / 2;
 }
 
 void ensure_wave_buffers(vcs_space* sp) {
@@ -650,12 +650,20 @@ void ensure_wave_buffers(vcs_space* sp) {
         std::fprintf(stderr, "[vcs solve] version store %.1f MB alloc %.3f ms\n", nv * 8e-6,
                      host_ms() - t0);
     }
+    const double t1 = trace_enabled() ? host_ms() : 0.0;
     sp->ver_off.exact(off.size(), sp->stream);
     sp->layer_off_dev.exact(sp->layer_off.size(), sp->stream);
-    VCS_CUDA(cudaMemcpy(sp->ver_off.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
-    VCS_CUDA(cudaMemcpy(sp->layer_off_dev.p, sp->layer_off.data(), sp->layer_off.size() * 8,
-                        cudaMemcpyHostToDevice));
-    sp->ver_off_host = off;
+    const double t2 = trace_enabled() ? host_ms() : 0.0;
+    sp->ver_off_host = std::move(off); // lives with the space: the async copies read it
+    VCS_CUDA(cudaMemcpyAsync(sp->ver_off.p, sp->ver_off_host.data(), sp->ver_off_host.size() * 8,
+                             cudaMemcpyHostToDevice, sp->stream));
+    VCS_CUDA(cudaMemcpyAsync(sp->layer_off_dev.p, sp->layer_off.data(), sp->layer_off.size() * 8,
+                             cudaMemcpyHostToDevice, sp->stream));
+    const double t3 = trace_enabled() ? host_ms() : 0.0;
+    VCS_CUDA(cudaStreamSynchronize(sp->stream)); // solves may run on a caller's stream
+    if (trace_enabled())
+        std::fprintf(stderr, "[vcs solve] offsets alloc %.3f copy %.3f sync %.3f ms\n", t2 - t1,
+                     t3 - t2, host_ms() - t3);
 }
 
 void record_event(cudaEvent_t ev, cudaStream_t s, bool capturing) {
@@ -1005,14 +1013,21 @@ int enqueue_impl(vcs_space* sp, const vcs_solve_opts* opts, void* stream, int st
         int method = o.method;
         if (method == VCS_METHOD_AUTO)
             method = vcs::wavefront_fits(sp) ? VCS_METHOD_WAVEFRONT : VCS_METHOD_JACOBI;
-        if (method == VCS_METHOD_WAVEFRONT && sp->ver_off_host.empty())
-            vcs::ensure_wave_buffers(sp);
+        if (method == VCS_METHOD_WAVEFRONT && sp->ver_off_host.empty()) {
+            try {
+                vcs::ensure_wave_buffers(sp);
+            } catch (const vcs::Error&) {
+                if (o.method != VCS_METHOD_AUTO) throw;
+                cudaGetLastError();
+                method = VCS_METHOD_JACOBI; // the version store does not fit right now
+            }
+        }
         if (vcs::trace_enabled())
             std::fprintf(stderr, "[vcs solve] buffers %.3f ms\n", vcs::host_ms() - t0);
         const vcs::GraphKey key{o.epsilon, o.discount,
                                 method == VCS_METHOD_JACOBI && o.skip_converged ? 1 : 0, M,
                                 method, method == VCS_METHOD_WAVEFRONT ? stream_out : 0};
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
+        const vcs::StreamUse s(sp, stream);
         auto& g = vcs::enqueue_solve(sp, key, s);
         sp->last_graph = &g;
         sp->last_key_skip = key.skip;
@@ -1099,7 +1114,7 @@ int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
         vcs::bind_device(sp->device);
         auto& g = *sp->last_graph;
         const bool wave = g.method == vcs::kMethodWavefront;
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
+        const vcs::StreamUse s(sp, stream);
         vcs::SolveCtrl ctrl{};
         VCS_CUDA(cudaMemcpyAsync(&ctrl, sp->ctrl.p, sizeof ctrl, cudaMemcpyDeviceToHost, s));
         VCS_CUDA(cudaStreamSynchronize(s));
@@ -1146,7 +1161,7 @@ int vcs_shard_begin(vcs_space* sp, double* v0, double* v1, double* delta, int32_
                     void* stream) {
     return guarded([&] {
         vcs::bind_device(sp->device);
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
+        const vcs::StreamUse s(sp, stream);
         sp->ctrl.exact(1, sp->stream);
         sp->actions_dev.exact(sp->S, sp->stream);
         VCS_CUDA(cudaStreamSynchronize(sp->stream));
@@ -1168,7 +1183,7 @@ int vcs_shard_sweep(vcs_space* sp, int32_t k, uint64_t row_begin, uint64_t row_e
         if (k < 1 || k + 1 > sp->shard_n_delta) raise(VCS_EINVAL, "sweep index out of range");
         vcs_solve_opts o{1e-6, 1, 0, 1.0, VCS_METHOD_JACOBI};
         if (opts) o = *opts;
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
+        const vcs::StreamUse s(sp, stream);
         const bool disc = vcs::is_discounted(o.discount);
         const vcs::LaunchShape sh = vcs::shape_for(sp, disc, false);
         vcs::SweepArgs a =
@@ -1189,7 +1204,7 @@ int vcs_shard_finish(vcs_space* sp, int32_t n_sweeps, uint64_t row_begin, uint64
         if (!sp->shard_v0) raise(VCS_EINVAL, "vcs_shard_begin was not called");
         vcs_solve_opts o{1e-6, 1, 0, 1.0, VCS_METHOD_JACOBI};
         if (opts) o = *opts;
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
+        const vcs::StreamUse s(sp, stream);
         const bool disc = vcs::is_discounted(o.discount);
         const vcs::LaunchShape sh = vcs::shape_for(sp, disc, true);
         vcs::SweepArgs a =
@@ -1227,7 +1242,7 @@ int vcs_wave_shard_begin(vcs_space* sp, int32_t world, int32_t rank, const vcs_s
         if (!(o.epsilon > 0.0))
             raise(VCS_EINVAL, "epsilon must be > 0 (value iteration would never terminate)");
         vcs::bind_device(sp->device);
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
+        const vcs::StreamUse s(sp, stream);
         sp->wave_world = world;
         sp->wave_rank = rank;
         sp->wave_eps = o.epsilon;
@@ -1264,7 +1279,7 @@ int vcs_wave_shard_layer(vcs_space* sp, int32_t t, void* stream) {
     return guarded([&] {
         if (sp->band_lo.empty()) raise(VCS_EINVAL, "vcs_wave_shard_begin was not called");
         if (t < 0 || t >= sp->H) raise(VCS_EINVAL, "layer out of range");
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
+        const vcs::StreamUse s(sp, stream);
         const bool disc = vcs::is_discounted(sp->wave_discount);
         vcs::WaveArgs a{};
         a.row_ptr = sp->row_ptr.p;
@@ -1301,7 +1316,7 @@ int vcs_wave_shard_pack(vcs_space* sp, int32_t t, int32_t version, double* dst, 
         if (sp->band_lo.empty()) raise(VCS_EINVAL, "vcs_wave_shard_begin was not called");
         if (t < 0 || t > sp->H || version < sp->band_base[t] || version >= sp->band_hi[t])
             raise(VCS_EINVAL, "version not held by this rank");
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
+        const vcs::StreamUse s(sp, stream);
         const uint64_t n = sp->layer_off[t + 1] - sp->layer_off[t];
         if (!n) return VCS_OK;
         vcs::k_band_pack<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
@@ -1316,7 +1331,7 @@ int vcs_wave_shard_unpack(vcs_space* sp, int32_t t, const double* src, void* str
     return guarded([&] {
         if (sp->band_lo.empty()) raise(VCS_EINVAL, "vcs_wave_shard_begin was not called");
         if (t < 0 || t > sp->H) raise(VCS_EINVAL, "layer out of range");
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
+        const vcs::StreamUse s(sp, stream);
         const uint64_t n = sp->layer_off[t + 1] - sp->layer_off[t];
         if (!n) return VCS_OK;
         const int lo = sp->band_lo[t];
@@ -1335,7 +1350,7 @@ int vcs_wave_shard_finish(vcs_space* sp, int32_t K, double* values_out, int32_t*
     return guarded([&] {
         if (sp->band_lo.empty()) raise(VCS_EINVAL, "vcs_wave_shard_begin was not called");
         if (K < 1) raise(VCS_EINVAL, "sweep count must be >= 1");
-        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : sp->stream;
+        const vcs::StreamUse s(sp, stream);
         const int H = sp->H;
         const bool disc = vcs::is_discounted(sp->wave_discount);
         auto owns = [&](int t, int k) { return sp->band_lo[t] <= k && k < sp->band_hi[t]; };

@@ -165,6 +165,8 @@ __device__ __forceinline__ double retiring_reward(const uint64_t (&k)[WM], int p
 // Dense path: the successor of an edge is identified by its mixed-radix index; the first-edge
 // table (dense_size entries, L2-resident) is updated right here.  idx(paid successor) =
 // sum over kept fields of f_p * W_p; a cloud action subtracts demand * W_p when p is kept.
+// (Staging the block's edges in shared memory for coalesced stores measured slower: the
+// strided stores merge in L2.)
 template <int WM>
 __global__ void k_emit_dense(uint32_t n, const uint64_t* __restrict__ keys,
                              const uint32_t* __restrict__ off, const LayerParam L,
@@ -425,6 +427,11 @@ __global__ void k_counters(const uint32_t* __restrict__ off_end, const uint32_t*
     out->n_next = rank[e];
 }
 
+// Mapped pinned counter blocks are recycled across builds (a cudaHostAlloc costs far more than
+// a whole small layer).
+std::mutex g_counters_mu;
+std::vector<LayerCounters*> g_counters_free;
+
 struct Scratch {
     DevBuf<uint32_t> off, slot, rank, table, eidx;
     DevBuf<uint64_t> ekeys, tkey;
@@ -432,8 +439,22 @@ struct Scratch {
     DevBuf<uint8_t> cub_tmp;
     LayerCounters* counters = nullptr;     // mapped pinned host memory
     LayerCounters* counters_dev = nullptr; // its device alias
+    Scratch() {
+        {
+            std::lock_guard<std::mutex> lock(g_counters_mu);
+            if (!g_counters_free.empty()) {
+                counters = g_counters_free.back();
+                g_counters_free.pop_back();
+            }
+        }
+        if (!counters)
+            VCS_CUDA(cudaHostAlloc(&counters, sizeof(LayerCounters),
+                                   cudaHostAllocMapped | cudaHostAllocPortable));
+        VCS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&counters_dev), counters, 0));
+    }
     ~Scratch() {
-        if (counters) cudaFreeHost(counters);
+        std::lock_guard<std::mutex> lock(g_counters_mu);
+        g_counters_free.push_back(counters);
     }
 };
 
@@ -451,12 +472,11 @@ void exclusive_scan(Scratch& sc, InputIt in, uint32_t* out, uint64_t n, cudaStre
 // the exact E_t from device memory), and ONE stream synchronisation at the end of the layer.
 template <int WM>
 void build_layers(vcs_space* sp, uint64_t state_cap) {
+    const double t_setup = trace_enabled() ? host_ms() : 0.0;
     const LayerPlan& pl = sp->plan;
     const int H = pl.horizon;
     cudaStream_t s = sp->stream;
     Scratch sc;
-    VCS_CUDA(cudaHostAlloc(&sc.counters, sizeof(LayerCounters), cudaHostAllocMapped));
-    VCS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&sc.counters_dev), sc.counters, 0));
 
     if (H > 0) {
         sc.params.exact(static_cast<size_t>(H), s);
@@ -466,18 +486,41 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
     sp->layer_off.assign(static_cast<size_t>(H) + 2, 0);
     sp->layer_edges.assign(static_cast<size_t>(H) + 1, 0);
     sp->key_off.assign(static_cast<size_t>(H) + 2, 0);
-    sp->keys.reserve(1u << 20, 0, s);
+    // Upper bounds of the space: n_{t+1} <= min(dense key-space size, n_t * maxdeg_t, cap).
+    // When they are affordable the CSR arrays are allocated once at the bound (the same few
+    // pool requests on every build, no growth copies); otherwise they grow geometrically.
+    uint64_t s_bound = 1, e_bound = 0, k_bound = static_cast<uint64_t>(pl.words[0]);
+    {
+        uint64_t nb = 1;
+        for (int t = 0; t < H && e_bound < (1ull << 40); ++t) {
+            const LayerParam& L = pl.layers[static_cast<size_t>(t)];
+            int maxdeg = 1;
+            for (int p = 0; p < L.n_active; ++p) maxdeg += L.attr[p] ? 1 : 0;
+            e_bound += nb * static_cast<uint64_t>(maxdeg);
+            nb = std::min<uint64_t>(nb * static_cast<uint64_t>(maxdeg), state_cap);
+            if (L.dense_size) nb = std::min<uint64_t>(nb, L.dense_size);
+            s_bound += nb;
+            k_bound += nb * static_cast<uint64_t>(L.next_words);
+        }
+    }
+    const bool presize = e_bound < 0xffffffffull && s_bound < 0xffffffffull &&
+                         e_bound * 16 + s_bound * 4 + k_bound * 8 <= device_bytes(sp->device) / 8;
+    sp->keys.reserve(presize ? k_bound : 1u << 20, 0, s);
     VCS_CUDA(cudaMemcpyAsync(sp->keys.p, pl.init_key.data(), pl.words[0] * sizeof(uint64_t),
                              cudaMemcpyHostToDevice, s));
-    sp->row_ptr.reserve(1u << 20, 0, s);
-    sp->succ.reserve(1u << 20, 0, s);
-    sp->reward.reserve(1u << 20, 0, s);
-    sp->action.reserve(1u << 20, 0, s);
+    sp->row_ptr.reserve(presize ? s_bound + 1 : 1u << 20, 0, s);
+    sp->succ.reserve(presize ? e_bound : 1u << 20, 0, s);
+    sp->reward.reserve(presize ? e_bound : 1u << 20, 0, s);
+    sp->action.reserve(presize ? e_bound : 1u << 20, 0, s);
 
     uint64_t S = 1, E = 0, n_t = 1;
     sp->max_layer = 1;
     constexpr uint32_t T = 256;
     double t_last = host_ms();
+    if (trace_enabled())
+        std::fprintf(stderr, "[vcs build] setup %.3f ms (presize %d: S<=%llu E<=%llu)\n",
+                     t_last - t_setup, presize ? 1 : 0, static_cast<unsigned long long>(s_bound),
+                     static_cast<unsigned long long>(e_bound));
     for (int t = 0; t < H; ++t) {
         const LayerParam& L = pl.layers[static_cast<size_t>(t)];
         sp->layer_off[static_cast<size_t>(t) + 1] = S;
@@ -505,7 +548,6 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
         sp->action.reserve(E + e_ub, E, s);
         const uint64_t key_next = sp->key_off[static_cast<size_t>(t) + 1];
         sp->keys.reserve(key_next + e_ub * static_cast<uint64_t>(L.next_words), key_next, s);
-        sc.rank.exact(e_ub + 1, s);
         const uint64_t cap = pow2_at_least(2 * e_ub);
         // dense successor indices when the next key space is small: a first-edge table of
         // dense_size words instead of a hash table of 2*E_t slots
@@ -521,6 +563,7 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
                 static_cast<uint32_t>(E), sp->row_ptr.p + row0, sc.eidx.p, sp->reward.p,
                 sp->action.p, sc.table.p);
             VCS_LAUNCHED();
+            sc.rank.exact(e_ub + 1, s);
             exclusive_scan(sc,
                            thrust::make_transform_iterator(
                                thrust::counting_iterator<uint32_t>(0),
@@ -552,6 +595,7 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
                     sc.slot.p);
             }
             VCS_LAUNCHED();
+            sc.rank.exact(e_ub + 1, s);
             exclusive_scan(sc,
                            thrust::make_transform_iterator(
                                thrust::counting_iterator<uint32_t>(0),
@@ -598,6 +642,7 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
     VCS_CUDA(cudaStreamSynchronize(s));
     sp->S = S;
     sp->E = E;
+    if (trace_enabled()) std::fprintf(stderr, "[vcs build] final %.3f ms\n", host_ms() - t_last);
 }
 
 int words_template(int w) {
@@ -679,6 +724,105 @@ void init_pool(int device) {
     });
 }
 
+namespace {
+struct BigBlock {
+    void* p;
+    size_t bytes;
+    uint64_t stamp;
+};
+struct BigCache {
+    std::mutex mu;
+    std::vector<BigBlock> blocks[64];
+    size_t bytes[64] = {};
+    uint64_t clock = 0;
+};
+BigCache& big_cache() {
+    static BigCache* c = new BigCache; // never destroyed: blocks die with the context
+    return *c;
+}
+} // namespace
+
+size_t device_bytes(int device) {
+    static std::mutex mu;
+    static size_t total[64] = {};
+    if (device < 0 || device >= 64) return 0;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!total[device]) {
+        cudaDeviceProp prop{};
+        if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) total[device] = prop.totalGlobalMem;
+    }
+    return total[device];
+}
+
+namespace {
+int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+} // namespace
+
+void* dev_alloc(size_t bytes, cudaStream_t s, size_t* got) {
+    if (bytes == 0) bytes = 1;
+    const int dev = current_device();
+    if (bytes >= kBigBlock && dev >= 0 && dev < 64) {
+        BigCache& c = big_cache();
+        std::lock_guard<std::mutex> lock(c.mu);
+        auto& v = c.blocks[dev];
+        size_t best = v.size();
+        for (size_t i = 0; i < v.size(); ++i)
+            if (v[i].bytes >= bytes && v[i].bytes <= bytes + bytes / 4 &&
+                (best == v.size() || v[i].bytes < v[best].bytes))
+                best = i;
+        if (best != v.size()) {
+            void* p = v[best].p;
+            *got = v[best].bytes;
+            c.bytes[dev] -= v[best].bytes;
+            v.erase(v.begin() + static_cast<std::ptrdiff_t>(best));
+            return p;
+        }
+    }
+    void* p = nullptr;
+    cudaError_t err = cudaMallocAsync(&p, bytes, s);
+    if (err == cudaErrorMemoryAllocation && dev >= 0 && dev < 64) {
+        cudaGetLastError();
+        BigCache& c = big_cache(); // out of memory: drop the cache and retry once
+        {
+            std::lock_guard<std::mutex> lock(c.mu);
+            for (auto& b : c.blocks[dev]) cudaFreeAsync(b.p, s);
+            c.blocks[dev].clear();
+            c.bytes[dev] = 0;
+        }
+        err = cudaMallocAsync(&p, bytes, s);
+    }
+    if (err != cudaSuccess)
+        raise(VCS_ECUDA, std::string("cudaMallocAsync: ") + cudaGetErrorString(err));
+    *got = bytes;
+    return p;
+}
+
+void dev_release_idle(void* p, size_t bytes, cudaStream_t s) {
+    const int dev = current_device();
+    if (bytes < kBigBlock || dev < 0 || dev >= 64) {
+        cudaFreeAsync(p, s);
+        return;
+    }
+    const size_t limit = device_bytes(dev) / 4; // at most a quarter of the device stays cached
+    BigCache& c = big_cache();
+    std::lock_guard<std::mutex> lock(c.mu);
+    auto& v = c.blocks[dev];
+    v.push_back({p, bytes, ++c.clock});
+    c.bytes[dev] += bytes;
+    while (c.bytes[dev] > limit && !v.empty()) {
+        size_t oldest = 0;
+        for (size_t i = 1; i < v.size(); ++i)
+            if (v[i].stamp < v[oldest].stamp) oldest = i;
+        cudaFreeAsync(v[oldest].p, s);
+        c.bytes[dev] -= v[oldest].bytes;
+        v.erase(v.begin() + static_cast<std::ptrdiff_t>(oldest));
+    }
+}
+
 int sm_count(int device) {
     int v = 0;
     VCS_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
@@ -689,6 +833,11 @@ int sm_count(int device) {
 
 vcs_space::~vcs_space() {
     cudaSetDevice(device);
+    for (auto& [st, ev] : use_ev) {
+        if (!ev) continue;
+        cudaEventSynchronize(ev);
+        cudaEventDestroy(ev);
+    }
     if (stream) cudaStreamSynchronize(stream);
     for (auto& [k, g] : graphs) {
         if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -698,22 +847,23 @@ vcs_space::~vcs_space() {
             if (e) cudaEventDestroy(e);
     }
     if (d2h_stream) cudaStreamDestroy(d2h_stream);
-    // stream-ordered frees must be issued while the stream is alive
-    row_ptr.release();
-    succ.release();
-    reward.release();
-    action.release();
-    keys.release();
-    v[0].release();
-    v[1].release();
-    delta.release();
-    ctrl.release();
-    actions_dev.release();
-    ver.release();
-    band_ver.release();
-    ver_off.release();
-    layer_off_dev.release();
-    loc_table.release();
+    // the stream is idle: big blocks go to the per-device cache for the next space, the rest
+    // back to the pool (stream-ordered frees are issued while the stream is alive)
+    row_ptr.release_idle();
+    succ.release_idle();
+    reward.release_idle();
+    action.release_idle();
+    keys.release_idle();
+    v[0].release_idle();
+    v[1].release_idle();
+    delta.release_idle();
+    ctrl.release_idle();
+    actions_dev.release_idle();
+    ver.release_idle();
+    band_ver.release_idle();
+    ver_off.release_idle();
+    layer_off_dev.release_idle();
+    loc_table.release_idle();
     if (stream) {
         cudaStreamSynchronize(stream);
         cudaStreamDestroy(stream);
@@ -748,8 +898,11 @@ int vcs_space_build(const vcs_instance* inst, uint64_t state_cap, int device, vc
         for (int j = 0; j < inst->n_tasks; ++j)
             if (inst->task_demand[j] < 0)
                 raise(VCS_EINVAL, "negative vm_demand is not supported by the device builder");
+        const double tp = vcs::trace_enabled() ? vcs::host_ms() : 0.0;
         vcs::LayerPlan plan = vcs::make_layer_plan(inst); // throws the 65535 error first
         auto sp = new_space(device);
+        if (vcs::trace_enabled())
+            std::fprintf(stderr, "[vcs build] plan + space %.3f ms\n", vcs::host_ms() - tp);
         sp->plan = std::move(plan);
         sp->has_plan = true;
         sp->H = sp->plan.horizon;
