@@ -294,6 +294,8 @@ struct WaveArgs {
     const double* __restrict__ reward;
     const int32_t* __restrict__ action;
     double* ver;               // all version vectors
+    const double* __restrict__ ver_next; // = ver + voff_next (layer t+1's store), set by the host
+    double* ver_cur;                     // = ver + voff (layer t's store)
     const uint64_t* ver_off;   // per layer (H+2)
     const uint64_t* layer_off; // per layer (H+2), flat state index
     double* delta;             // delta[k], k = 1..H+1
@@ -366,7 +368,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32, MINB) k_wave_layer(WaveArgs a
     // successor slot of version (k-1) is k-1-base_next; for k = lo + gP it is even (aligned)
     const uint32_t nshift = BAND ? static_cast<uint32_t>(lo - 1 - a.base_next) : 0u;
     const int oshift = BAND ? lo - a.base : 1; // own storage slot of version lo + j is j + oshift
-    const double* vn = a.ver + a.voff_next;
+    const double* vn = a.ver_next; // one 64-bit base: a gather address is one IMAD.WIDE
     const uint32_t nbase = static_cast<uint32_t>(a.next_row0);
     const uint64_t n_tiles = (a.n + T - 1) / T;
     double dmax[P] = {0.0, 0.0}; // narrow case: the thread's k's never change
@@ -405,7 +407,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32, MINB) k_wave_layer(WaveArgs a
             sedge[j] = rec;
         }
         __syncthreads();
-        double* out = a.ver + a.voff + s0 * st;
+        double* out = a.ver_cur + s0 * st;
         if (active) {
             for (int sl = my_s; sl < nt; sl += spp) {
                 const int eb = static_cast<int>(srp[sl] - e0), ee = static_cast<int>(srp[sl + 1] - e0);
@@ -418,28 +420,41 @@ __global__ void __launch_bounds__(kWaveWarps * 32, MINB) k_wave_layer(WaveArgs a
                         best_e[p] = -1;
                     }
                     const uint32_t nslot = nshift + static_cast<uint32_t>(g * P);
-                    for (int eo = eb; eo < ee; eo += U) {
-                        double2 x[U]; // all of the round's gathers in flight together
+                    // one edge's contribution to both versions: q = r + V_{k-1}(succ), strict
+                    // first maximum with its edge (mdp.cpp:254-260)
+                    auto relax = [&](int e, const double2& x) {
+                        const double r = sedge[e].reward;
+                        const double v[P] = {x.x, x.y}; // V_{k-1} of both versions
+#pragma unroll
+                        for (int p = 0; p < P; ++p) {
+                            const double q = DISC ? __dadd_rn(r, __dmul_rn(a.discount, v[p]))
+                                                  : __dadd_rn(r, v[p]);
+                            if (q > best[p]) { // strict: the first maximal edge wins
+                                best[p] = q;
+                                best_e[p] = e;
+                            }
+                        }
+                    };
+                    int eo = eb;
+                    for (; eo + U <= ee; eo += U) { // full rounds: U gathers in flight, no guards
+                        double2 x[U];
 #pragma unroll
                         for (int u = 0; u < U; ++u)
+                            x[u] = __ldg(reinterpret_cast<const double2*>(
+                                vn + (sedge[eo + u].succ * sn + nslot)));
+#pragma unroll
+                        for (int u = 0; u < U; ++u) relax(eo + u, x[u]);
+                    }
+                    if (eo < ee) { // the last < U edges
+                        double2 x[U];
+#pragma unroll
+                        for (int u = 0; u < U - 1; ++u)
                             if (eo + u < ee)
                                 x[u] = __ldg(reinterpret_cast<const double2*>(
                                     vn + (sedge[eo + u].succ * sn + nslot)));
 #pragma unroll
-                        for (int u = 0; u < U; ++u)
-                            if (eo + u < ee) {
-                                const double r = sedge[eo + u].reward;
-                                const double v[P] = {x[u].x, x[u].y}; // V_{k-1} of both versions
-#pragma unroll
-                                for (int p = 0; p < P; ++p) {
-                                    const double q = DISC ? __dadd_rn(r, __dmul_rn(a.discount, v[p]))
-                                                          : __dadd_rn(r, v[p]);
-                                    if (q > best[p]) { // strict: the first maximal edge wins
-                                        best[p] = q;
-                                        best_e[p] = eo + u;
-                                    }
-                                }
-                            }
+                        for (int u = 0; u < U - 1; ++u)
+                            if (eo + u < ee) relax(eo + u, x[u]);
                     }
                     double* o = out + sl * st;
                     double* so = sout + sl * w1;
@@ -697,32 +712,44 @@ void launch_layer(vcs_space* sp, WaveArgs& a, bool disc, cudaStream_t s) {
         return e ? std::atoi(e) : 1;
     }();
     using LayerFn = void (*)(WaveArgs);
+#define VCS_WAVE_VARIANTS(D, B)                                                                 \
+    {k_wave_layer<D, 8, 3, B>, k_wave_layer<D, 4, 4, B>, k_wave_layer<D, 4, 5, B>,              \
+     k_wave_layer<D, 2, 6, B>}
     static const LayerFn fns[2][2][4] = {
-        {{k_wave_layer<false, 8, 3, false>, k_wave_layer<false, 4, 4, false>,
-          k_wave_layer<false, 4, 5, false>, k_wave_layer<false, 2, 6, false>},
-         {k_wave_layer<true, 8, 3, false>, k_wave_layer<true, 4, 4, false>,
-          k_wave_layer<true, 4, 5, false>, k_wave_layer<true, 2, 6, false>}},
-        {{k_wave_layer<false, 8, 3, true>, k_wave_layer<false, 4, 4, true>,
-          k_wave_layer<false, 4, 5, true>, k_wave_layer<false, 2, 6, true>},
-         {k_wave_layer<true, 8, 3, true>, k_wave_layer<true, 4, 4, true>,
-          k_wave_layer<true, 4, 5, true>, k_wave_layer<true, 2, 6, true>}}};
+        {VCS_WAVE_VARIANTS(false, false), VCS_WAVE_VARIANTS(true, false)},
+        {VCS_WAVE_VARIANTS(false, true), VCS_WAVE_VARIANTS(true, true)}};
+#undef VCS_WAVE_VARIANTS
     const bool band = a.band_lo != 1 || a.base != 0 || a.base_next != 0;
     const LayerFn layer_fn = fns[band ? 1 : 0][disc ? 1 : 0][std::min(3, std::max(0, variant))];
     const void* fn = reinterpret_cast<const void*>(layer_fn);
     const int nb = a.band_hi - a.band_lo;
     if (nb <= 0 || a.n == 0) return;
+    a.ver_next = a.ver + a.voff_next;
+    a.ver_cur = a.ver + a.voff;
     const int qcap = std::max(1, sp->max_degree);
-    // tile: whole passes of (states x 2-version groups) threads, ~8 passes per tile
+    // tile: whole passes of (states x 2-version groups) threads, up to 8 passes per tile (the
+    // staging of a tile's CSR is amortised over its passes); a small layer gets fewer passes
+    // per tile so that its tiles still cover every SM (its passes run in parallel instead)
     const int G = (nb + 1) / 2;
     const int spp = G > kWaveWarps * 32 ? 1 : (kWaveWarps * 32) / G;
-    a.tile = G > kWaveWarps * 32 ? 2 : std::min(512, spp * 8);
     a.max_deg = qcap;
-    const size_t smem = static_cast<size_t>(nb) * 8 + static_cast<size_t>(a.tile) * (nb + 1) * 8 +
-                        static_cast<size_t>(a.tile) * qcap * 16 + static_cast<size_t>(a.tile + 1) * 4;
+    auto smem_for = [&](int tile) {
+        return static_cast<size_t>(nb) * 8 + static_cast<size_t>(tile) * (nb + 1) * 8 +
+               static_cast<size_t>(tile) * qcap * 16 + static_cast<size_t>(tile + 1) * 4;
+    };
+    a.tile = G > kWaveWarps * 32 ? 2 : std::min(512, spp * 8);
+    size_t smem = smem_for(a.tile);
     if (smem > 200 * 1024) raise(VCS_EINVAL, "horizon/out-degree too large for the wavefront tile");
     raise_smem_limit(fn, sp->device, smem);
     int per_sm = 0;
     VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kWaveWarps * 32, smem));
+    const uint64_t slots = static_cast<uint64_t>(std::max(1, per_sm)) * sp->num_sms;
+    if (G <= kWaveWarps * 32 && (a.n + a.tile - 1) / a.tile < slots) {
+        const uint64_t per_tile = std::max<uint64_t>(1, (a.n + slots - 1) / slots); // states
+        const uint64_t passes = std::min<uint64_t>(8, (per_tile + spp - 1) / spp);
+        a.tile = static_cast<int>(std::min<uint64_t>(512, spp * passes));
+        smem = smem_for(a.tile);
+    }
     const uint64_t tiles = (a.n + a.tile - 1) / a.tile;
     const uint64_t blocks = std::max<uint64_t>(
         1, std::min<uint64_t>(tiles, static_cast<uint64_t>(std::max(1, per_sm)) * sp->num_sms));

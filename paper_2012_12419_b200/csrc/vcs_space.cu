@@ -24,6 +24,7 @@
 #include <thrust/iterator/transform_iterator.h>
 
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -949,6 +950,7 @@ int vcs_space_from_csr(uint64_t n_states, uint64_t n_edges, int32_t horizon,
             sp->max_layer = std::max(sp->max_layer, sp->layer_off[t + 1] - sp->layer_off[t]);
         }
         sp->max_degree = maxdeg;
+
         cudaStream_t s = sp->stream;
         sp->row_ptr.exact(n_states + 1, sp->stream);
         sp->succ.exact(n_edges, sp->stream);
