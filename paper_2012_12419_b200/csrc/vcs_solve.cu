@@ -727,9 +727,9 @@ void launch_layer(vcs_space* sp, WaveArgs& a, bool disc, cudaStream_t s) {
     a.ver_next = a.ver + a.voff_next;
     a.ver_cur = a.ver + a.voff;
     const int qcap = std::max(1, sp->max_degree);
-    // tile: whole passes of (states x 2-version groups) threads, up to 8 passes per tile (the
-    // staging of a tile's CSR is amortised over its passes); a small layer gets fewer passes
-    // per tile so that its tiles still cover every SM (its passes run in parallel instead)
+    // tile: whole passes of (states x 2-version groups) threads (the staging of a tile's CSR is
+    // amortised over its passes); a small layer gets fewer passes per tile so that its tiles
+    // still cover every SM (its passes run in parallel instead)
     const int G = (nb + 1) / 2;
     const int spp = G > kWaveWarps * 32 ? 1 : (kWaveWarps * 32) / G;
     a.max_deg = qcap;
@@ -737,7 +737,13 @@ void launch_layer(vcs_space* sp, WaveArgs& a, bool disc, cudaStream_t s) {
         return static_cast<size_t>(nb) * 8 + static_cast<size_t>(tile) * (nb + 1) * 8 +
                static_cast<size_t>(tile) * qcap * 16 + static_cast<size_t>(tile + 1) * 4;
     };
-    a.tile = G > kWaveWarps * 32 ? 2 : std::min(512, spp * 8);
+    // 4 passes per tile measured best on C4 (3.96 ms vs 4.49 with 8: the smaller tile's shared
+    // memory lets 4 blocks per SM be resident, the register limit); VCS_WAVE_PASSES overrides
+    static const int max_passes = [] {
+        const char* e = std::getenv("VCS_WAVE_PASSES");
+        return e ? std::max(1, std::atoi(e)) : 4;
+    }();
+    a.tile = G > kWaveWarps * 32 ? 2 : std::min(512, spp * max_passes);
     size_t smem = smem_for(a.tile);
     if (smem > 200 * 1024) raise(VCS_EINVAL, "horizon/out-degree too large for the wavefront tile");
     raise_smem_limit(fn, sp->device, smem);
@@ -746,7 +752,7 @@ void launch_layer(vcs_space* sp, WaveArgs& a, bool disc, cudaStream_t s) {
     const uint64_t slots = static_cast<uint64_t>(std::max(1, per_sm)) * sp->num_sms;
     if (G <= kWaveWarps * 32 && (a.n + a.tile - 1) / a.tile < slots) {
         const uint64_t per_tile = std::max<uint64_t>(1, (a.n + slots - 1) / slots); // states
-        const uint64_t passes = std::min<uint64_t>(8, (per_tile + spp - 1) / spp);
+        const uint64_t passes = std::min<uint64_t>(max_passes, (per_tile + spp - 1) / spp);
         a.tile = static_cast<int>(std::min<uint64_t>(512, spp * passes));
         smem = smem_for(a.tile);
     }
