@@ -157,14 +157,19 @@ typedef struct vcs_solve_opts {
                                other value is the labelled EXTENSION q = r + discount*V(s')
                                (BASELINE.json configs[0] "gamma=0.9"); it has no reference
                                counterpart and is checked against the C oracle only. */
-    int32_t method;         /* VCS_METHOD_AUTO (layer wavefront when its version store fits in
-                               half of the free HBM, else Jacobi), VCS_METHOD_JACOBI (one kernel
-                               per sweep) or VCS_METHOD_WAVEFRONT.  All give identical bits. */
+    int32_t method;         /* VCS_METHOD_AUTO (= VCS_METHOD_CERTIFIED when the wavefront's version
+                               store fits in half of the HBM, else Jacobi), VCS_METHOD_JACOBI (one
+                               kernel per sweep), VCS_METHOD_WAVEFRONT (all truncation horizons,
+                               one pass) or VCS_METHOD_CERTIFIED (one backward pass with the two
+                               top versions of every state; when it proves that no sweep k <= H
+                               reaches delta < epsilon the result is final, otherwise the
+                               wavefront runs).  All give identical bits. */
 } vcs_solve_opts;
 
 #define VCS_METHOD_AUTO 0
 #define VCS_METHOD_JACOBI 1
 #define VCS_METHOD_WAVEFRONT 2
+#define VCS_METHOD_CERTIFIED 3
 
 typedef struct vcs_solve_report {
     int32_t sweeps;            /* ValueTable::sweeps() */
@@ -175,7 +180,8 @@ typedef struct vcs_solve_report {
     double extract_ms;         /* policy extraction, CUDA events */
     double alg_bytes;          /* SURVEY §8(d) algorithmic bytes of the sweeps: (24+12 d) per backup_ref */
     double alg_bytes_done;     /* same formula over the performed backups */
-    int32_t method;            /* the method that ran (VCS_METHOD_JACOBI / _WAVEFRONT) */
+    int32_t method;            /* the method that ran: VCS_METHOD_JACOBI, _WAVEFRONT, or _CERTIFIED
+                                  (the certificate held: one backward pass was the whole solve) */
     int32_t pad;
     double model_bytes;        /* minimum HBM bytes of the method that ran: Jacobi = alg_bytes_done
                                   with the u32 row_ptr layout; wavefront = CSR once + every

@@ -16,7 +16,7 @@ import numpy as np
 VCS_OK, VCS_EINVAL, VCS_ECAP, VCS_EIO, VCS_ECUDA, VCS_ERANGE = 0, 2, 3, 4, 5, 6
 VCS_PAID_CLOUD = -1
 VCS_GEN_RANDOM, VCS_GEN_HOMOG, VCS_GEN_GREEDY = 0, 1, 2
-VCS_METHOD_AUTO, VCS_METHOD_JACOBI, VCS_METHOD_WAVEFRONT = 0, 1, 2
+VCS_METHOD_AUTO, VCS_METHOD_JACOBI, VCS_METHOD_WAVEFRONT, VCS_METHOD_CERTIFIED = 0, 1, 2, 3
 
 LIB_PATH = Path(__file__).resolve().parent / "libvcs_gpu.so"
 

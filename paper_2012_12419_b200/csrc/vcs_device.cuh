@@ -97,13 +97,16 @@ struct DevBuf {
 
 // Device-side control block of one solve.
 struct SolveCtrl {
-    int32_t stop;   // sticky: set by the first sweep that sees delta[k-1] < eps
-    int32_t sweeps; // K*: the converged sweep count
+    int32_t stop;      // sticky: set by the first sweep that sees delta[k-1] < eps
+    int32_t sweeps;    // K*: the converged sweep count
+    int32_t certified; // certified pass: K* = H+1 proven, the wavefront fallback was skipped
+    int32_t pad;
 };
 
 constexpr int kMethodAuto = 0;
 constexpr int kMethodJacobi = 1;
 constexpr int kMethodWavefront = 2;
+constexpr int kMethodCertified = 3;
 
 struct GraphKey {
     double eps;
@@ -162,6 +165,10 @@ struct vcs_space {
     vcs::DevBuf<uint64_t> ver_off;
     vcs::DevBuf<uint64_t> layer_off_dev;
     std::vector<uint64_t> ver_off_host;
+    // certified pass: (V_{m-1}, V_m) of every state, lower bounds lb[k] of the residuals
+    vcs::DevBuf<double2> cert_xd;
+    vcs::DevBuf<double> cert_lb;
+    cudaStream_t aux_stream = nullptr; // captures the fallback body of the certified graph
     std::map<vcs::GraphKey, vcs::CachedGraph> graphs;
     vcs::CachedGraph* last_graph = nullptr; // graph of the last vcs_solve_enqueue
     int last_key_skip = 1;

@@ -628,6 +628,136 @@ __global__ void __launch_bounds__(kWaveWarps * 32) k_wave_extract(WaveArgs a, in
     }
 }
 
+// ---- certified pass (VCS_METHOD_CERTIFIED) -----------------------------------------------------
+// The reference's observable result is V_{K*}, the argmax against V_{K*} and K* (mdp.hpp:136-175).
+// When K* = H+1 (no sweep k <= H has delta_k < eps) every state's output is its EXACT value
+// V_{m_t} and the argmax against its successors' exact values: one backward pass.  The same pass
+// also carries V_{m_t - 1}(s) (same recursion one version lower, V_0 = 0 for layer H-1), which
+// gives for every k the lower bound lb_k = max over layer H-k of |V_k - V_{k-1}| <= delta_k.
+// lb_k >= eps for all k <= H proves K* = H+1 (delta_{H+1} = 0 ends the reference's loop): the
+// pass is then the whole solve, bit for bit.  Otherwise the full wavefront runs (graph IF node).
+
+struct CertArgs {
+    const uint32_t* __restrict__ row_ptr;
+    const uint32_t* __restrict__ succ;
+    const double* __restrict__ reward;
+    const int32_t* __restrict__ action;
+    const double2* __restrict__ xd_next; // layer t+1: (V_{m-2}, V_{m-1}) relative to layer t
+    double2* xd_cur;                     // layer t:   (V_{m-1}, V_m)
+    double* values_out;
+    int32_t* act_out;
+    double* lb;                          // lb[k], k = m_t
+    uint64_t row0, n, next_row0;
+    int m;
+    int qcap;                            // staged edge slots per row
+    double discount;
+};
+
+// Warp-cooperative like the Jacobi sweep: 32 consecutive rows per warp; the rows' edge range is
+// streamed with coalesced loads, the successors' (V_{m-2}, V_{m-1}) pairs gathered with one
+// 16-byte load per edge (8 edges per lane in flight), q pairs staged in shared memory, then each
+// lane scans its row: strict first maximum of V_m with its edge, strict maximum of V_{m-1}.
+template <bool DISC>
+__global__ void __launch_bounds__(256) k_cert_layer(CertArgs a) {
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int U = 8;
+    extern __shared__ double2 s_q[];
+    __shared__ unsigned long long s_lb;
+    double2* qw = s_q + (threadIdx.x >> 5) * 32 * a.qcap;
+    if (threadIdx.x == 0) s_lb = 0ull;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    double dmax = 0.0;
+    for (uint64_t r0 = warp * 32; r0 < a.n; r0 += n_warps * 32) {
+        const uint64_t r = r0 + lane;
+        const bool valid = r < a.n;
+        const uint64_t rr = a.row0 + (valid ? r : a.n);
+        const uint32_t eb = __ldg(a.row_ptr + rr);
+        uint32_t ee = __shfl_down_sync(FULL, eb, 1);
+        if (lane == 31) ee = valid ? __ldg(a.row_ptr + rr + 1) : eb;
+        const uint32_t w0 = __shfl_sync(FULL, eb, 0);
+        const uint32_t w1 = __shfl_sync(FULL, ee, 31);
+        for (uint32_t base = w0; base < w1; base += 32 * U) {
+            uint32_t sidx[U];
+            double rw[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t e = base + u * 32 + lane;
+                if (e < w1) {
+                    sidx[u] = __ldcs(a.succ + e) - static_cast<uint32_t>(a.next_row0);
+                    rw[u] = __ldcs(a.reward + e);
+                }
+            }
+            double2 x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (base + u * 32 + lane < w1) x[u] = __ldg(a.xd_next + sidx[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t e = base + u * 32 + lane;
+                if (e < w1) {
+                    double2 q;
+                    q.x = DISC ? __dadd_rn(rw[u], __dmul_rn(a.discount, x[u].x)) : __dadd_rn(rw[u], x[u].x);
+                    q.y = DISC ? __dadd_rn(rw[u], __dmul_rn(a.discount, x[u].y)) : __dadd_rn(rw[u], x[u].y);
+                    qw[e - w0] = q;
+                }
+            }
+        }
+        __syncwarp();
+        if (valid) {
+            double hi = -INFINITY, lo = -INFINITY;
+            uint32_t best_e = 0xffffffffu;
+            for (uint32_t e = eb; e < ee; ++e) {
+                const double2 q = qw[e - w0];
+                if (q.y > hi) { // strict: the first maximal edge wins (mdp.cpp:254-260)
+                    hi = q.y;
+                    best_e = e;
+                }
+                if (q.x > lo) lo = q.x;
+            }
+            if (a.m == 1) lo = 0.0; // V_0
+            a.xd_cur[r] = make_double2(lo, hi);
+            a.values_out[a.row0 + r] = hi;
+            a.act_out[a.row0 + r] = best_e != 0xffffffffu ? __ldg(a.action + best_e) : -1;
+            const double d = fabs(hi - lo); // parallel_vi.cpp: |v_new - v_old|
+            dmax = dmax < d ? d : dmax;
+        }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double other = __shfl_xor_sync(FULL, dmax, o);
+        dmax = dmax < other ? other : dmax;
+    }
+    if (lane == 0 && dmax > 0.0)
+        atomicMax(&s_lb, static_cast<unsigned long long>(__double_as_longlong(dmax)));
+    __syncthreads();
+    if (threadIdx.x == 0 && s_lb)
+        atomicMax(reinterpret_cast<unsigned long long*>(a.lb + a.m), s_lb);
+}
+
+// K* = H+1 is proven iff lb_k >= eps for k = 1..H (and no sweep cap below H+1).  Sets the graph
+// conditional to run the wavefront fallback otherwise.
+__global__ void k_cert_check(const double* __restrict__ lb, int H, double eps, int max_sweeps,
+                             SolveCtrl* ctrl, cudaGraphConditionalHandle fallback) {
+    __shared__ int bad;
+    if (threadIdx.x == 0) bad = max_sweeps < H + 1 ? 1 : 0;
+    __syncthreads();
+    for (int k = 1 + threadIdx.x; k <= H; k += blockDim.x)
+        if (!(lb[k] >= eps)) bad = 1; // (NaN-safe: anything but a proven lb_k >= eps)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (!bad) {
+            ctrl->sweeps = H + 1;
+            ctrl->stop = 1;
+            ctrl->certified = 1;
+        }
+        cudaGraphSetConditional(fallback, bad ? 1u : 0u);
+    }
+}
+
 // Stored doubles of the version store (V_0..V_{m_t} per state, stride wave_stride(m_t)).
 uint64_t wave_versions(const vcs_space* sp, std::vector<uint64_t>* off = nullptr) {
     uint64_t tot = 0;
@@ -763,8 +893,9 @@ void launch_layer(vcs_space* sp, WaveArgs& a, bool disc, cudaStream_t s) {
     VCS_LAUNCHED();
 }
 
+// `events` = false: no event nodes (the fallback body of a certified graph may not hold any).
 void record_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaStream_t s,
-                      bool capturing) {
+                      bool capturing, bool events = true) {
     const bool disc = is_discounted(key.discount);
     WaveArgs a{};
     a.row_ptr = sp->row_ptr.p;
@@ -792,7 +923,7 @@ void record_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
                                   static_cast<int>(std::max<size_t>(smem_ext, 1024))));
     VCS_CUDA(cudaMemsetAsync(sp->delta.p, 0, (sp->H + 3) * sizeof(double), s));
     VCS_CUDA(cudaMemsetAsync(sp->ctrl.p, 0, sizeof(SolveCtrl), s));
-    record_event(g.ev[0], s, capturing);
+    if (events) record_event(g.ev[0], s, capturing);
     // terminal layer: V = 0.0 (+0), action = kPaidCloud (mdp.cpp:248-251); its stored V_0 = 0
     {
         const uint64_t rH = sp->layer_off[sp->H], nH = sp->S - rH;
@@ -820,9 +951,10 @@ void record_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
         ++launches;
         // layer t's values/actions are final here (unless an early stop needs the fix-up):
         // lets vcs_solve stream them to the host while the remaining layers compute
-        if (!g.layer_ev.empty()) record_event(g.layer_ev[static_cast<size_t>(t)], s, capturing);
+        if (events && !g.layer_ev.empty())
+            record_event(g.layer_ev[static_cast<size_t>(t)], s, capturing);
     }
-    record_event(g.ev[1], s, capturing);
+    if (events) record_event(g.ev[1], s, capturing);
     int per_sm_ext = 0;
     VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_ext, fn_ext, kWaveWarps * 32,
                                                            smem_ext));
@@ -834,8 +966,112 @@ void record_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
     else
         k_wave_extract<false><<<static_cast<unsigned>(eblocks), kWaveWarps * 32, smem_ext, s>>>(a, qcap);
     VCS_LAUNCHED();
-    record_event(g.ev[2], s, capturing);
+    if (events) record_event(g.ev[2], s, capturing);
     g.launches = launches + 1;
+}
+
+// Enqueue one certified solve: the two-version backward pass, the proof, and the full
+// wavefront as the body of a graph IF node that runs only when the proof fails.
+void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaStream_t s,
+                      bool capturing) {
+    if (!capturing) raise(VCS_EINVAL, "the certified solve is only recorded into a CUDA graph");
+    const bool disc = is_discounted(key.discount);
+    const int H = sp->H;
+    // (cert_xd / cert_lb are allocated before capture: an allocation inside a capture would
+    // become a graph allocation node, and such a graph cannot be relaunched)
+    if (sp->cert_xd.n < sp->S || sp->cert_lb.n < static_cast<size_t>(H) + 2)
+        raise(VCS_EINVAL, "certified solve buffers were not allocated");
+    VCS_CUDA(cudaMemsetAsync(sp->ctrl.p, 0, sizeof(SolveCtrl), s));
+    VCS_CUDA(cudaMemsetAsync(sp->cert_lb.p, 0, (H + 2) * sizeof(double), s));
+    record_event(g.ev[0], s, capturing);
+    {
+        const uint64_t rH = sp->layer_off[H], nH = sp->S - rH;
+        VCS_CUDA(cudaMemsetAsync(sp->v[0].p + rH, 0, nH * sizeof(double), s));
+        VCS_CUDA(cudaMemsetAsync(sp->actions_dev.p + rH, 0xff, nH * sizeof(int32_t), s));
+        VCS_CUDA(cudaMemsetAsync(sp->cert_xd.p + rH, 0, nH * sizeof(double2), s)); // V_0 = 0
+    }
+    const int qcap = std::max(1, sp->max_degree);
+    // warps per block: 32 rows x qcap staged q pairs (16 B) per warp within 96 KB
+    const int wpb = static_cast<int>(std::max<size_t>(
+        1, std::min<size_t>(8, (96u << 10) / (static_cast<size_t>(32) * qcap * sizeof(double2)))));
+    const size_t smem = static_cast<size_t>(wpb) * 32 * qcap * sizeof(double2);
+    const void* fn = disc ? reinterpret_cast<const void*>(k_cert_layer<true>)
+                          : reinterpret_cast<const void*>(k_cert_layer<false>);
+    raise_smem_limit(fn, sp->device, smem);
+    int per_sm = 0;
+    VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, wpb * 32, smem));
+    CertArgs a{};
+    a.row_ptr = sp->row_ptr.p;
+    a.succ = sp->succ.p;
+    a.reward = sp->reward.p;
+    a.action = sp->action.p;
+    a.values_out = sp->v[0].p;
+    a.act_out = sp->actions_dev.p;
+    a.lb = sp->cert_lb.p;
+    a.qcap = qcap;
+    a.discount = key.discount;
+    int launches = 0;
+    for (int t = H - 1; t >= 0; --t) {
+        a.row0 = sp->layer_off[t];
+        a.n = sp->layer_off[t + 1] - sp->layer_off[t];
+        a.next_row0 = sp->layer_off[t + 1];
+        a.m = H - t;
+        a.xd_next = sp->cert_xd.p + a.next_row0;
+        a.xd_cur = sp->cert_xd.p + a.row0;
+        if (a.n) {
+            const uint64_t warps = (a.n + 31) / 32;
+            const uint64_t blocks = std::max<uint64_t>(
+                1, std::min<uint64_t>((warps + wpb - 1) / wpb,
+                                      static_cast<uint64_t>(std::max(1, per_sm)) * sp->num_sms));
+            if (disc)
+                k_cert_layer<true><<<static_cast<unsigned>(blocks), wpb * 32, smem, s>>>(a);
+            else
+                k_cert_layer<false><<<static_cast<unsigned>(blocks), wpb * 32, smem, s>>>(a);
+            VCS_LAUNCHED();
+            ++launches;
+        }
+        if (!g.layer_ev.empty()) record_event(g.layer_ev[static_cast<size_t>(t)], s, capturing);
+    }
+    // the proof, then IF (not proven) { the full wavefront } as a conditional graph node
+    cudaStreamCaptureStatus cst;
+    cudaGraph_t cg = nullptr;
+    VCS_CUDA(cudaStreamGetCaptureInfo(s, &cst, nullptr, &cg, nullptr, nullptr));
+    if (cst != cudaStreamCaptureStatusActive || !cg) raise(VCS_ECUDA, "stream is not capturing");
+    cudaGraphConditionalHandle fallback;
+    VCS_CUDA(cudaGraphConditionalHandleCreate(&fallback, cg, 1, cudaGraphCondAssignDefault));
+    k_cert_check<<<1, 64, 0, s>>>(sp->cert_lb.p, H, key.eps, key.max_sweeps, sp->ctrl.p, fallback);
+    VCS_LAUNCHED();
+    ++launches;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t n_deps = 0;
+    VCS_CUDA(cudaStreamGetCaptureInfo(s, &cst, nullptr, &cg, &deps, &n_deps));
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = fallback;
+    cp.conditional.type = cudaGraphCondTypeIf;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cond = nullptr;
+    VCS_CUDA(cudaGraphAddNode(&cond, cg, deps, n_deps, &cp));
+    VCS_CUDA(cudaStreamUpdateCaptureDependencies(s, &cond, 1, cudaStreamSetCaptureDependencies));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    if (!sp->aux_stream)
+        VCS_CUDA(cudaStreamCreateWithFlags(&sp->aux_stream, cudaStreamNonBlocking));
+    VCS_CUDA(cudaStreamBeginCaptureToGraph(sp->aux_stream, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal));
+    const int certified_launches = launches;
+    try {
+        record_wavefront(sp, key, g, sp->aux_stream, true, /*events=*/false);
+    } catch (...) {
+        cudaGraph_t dummy = nullptr;
+        cudaStreamEndCapture(sp->aux_stream, &dummy);
+        throw;
+    }
+    cudaGraph_t body_out = nullptr;
+    VCS_CUDA(cudaStreamEndCapture(sp->aux_stream, &body_out));
+    unnote_launch(static_cast<uint64_t>(g.launches)); // the body's kernels were only recorded
+    record_event(g.ev[1], s, capturing);
+    record_event(g.ev[2], s, capturing);
+    g.launches = certified_launches;
 }
 
 // Enqueue one Jacobi solve on `s`: zeroing, up to max_sweeps sweep kernels, extraction.
@@ -868,6 +1104,8 @@ void record_solve(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaStream
                   bool capturing) {
     if (key.method == kMethodWavefront)
         record_wavefront(sp, key, g, s, capturing);
+    else if (key.method == kMethodCertified)
+        record_certified(sp, key, g, s, capturing);
     else
         record_jacobi(sp, key, g, s, capturing);
 }
@@ -881,7 +1119,7 @@ CachedGraph& enqueue_solve(vcs_space* sp, const GraphKey& key, cudaStream_t s) {
         g.method = key.method;
         g.n_sweeps = key.max_sweeps;
         for (auto& e : g.ev) VCS_CUDA(cudaEventCreate(&e));
-        if (key.stream_out && key.method == kMethodWavefront) {
+        if (key.stream_out && (key.method == kMethodWavefront || key.method == kMethodCertified)) {
             g.layer_ev.assign(static_cast<size_t>(std::max(0, sp->H)), nullptr);
             for (auto& e : g.layer_ev)
                 VCS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1036,7 +1274,7 @@ int enqueue_impl(vcs_space* sp, const vcs_solve_opts* opts, void* stream, int st
         if (opts) o = *opts;
         if (!(o.epsilon > 0.0))
             raise(VCS_EINVAL, "epsilon must be > 0 (value iteration would never terminate)");
-        if (o.method < VCS_METHOD_AUTO || o.method > VCS_METHOD_WAVEFRONT)
+        if (o.method < VCS_METHOD_AUTO || o.method > VCS_METHOD_CERTIFIED)
             raise(VCS_EINVAL, "unknown solve method");
         vcs::bind_device(sp->device);
         int M = sp->H + 1; // delta_{H+1} == 0 on the layered DAG, so this is never binding
@@ -1045,8 +1283,10 @@ int enqueue_impl(vcs_space* sp, const vcs_solve_opts* opts, void* stream, int st
         vcs::ensure_solve_buffers(sp, sp->H + 1); // fixed size: cached graphs keep addresses
         int method = o.method;
         if (method == VCS_METHOD_AUTO)
-            method = vcs::wavefront_fits(sp) ? VCS_METHOD_WAVEFRONT : VCS_METHOD_JACOBI;
-        if (method == VCS_METHOD_WAVEFRONT && sp->ver_off_host.empty()) {
+            method = vcs::wavefront_fits(sp) ? VCS_METHOD_CERTIFIED : VCS_METHOD_JACOBI;
+        // (the certified solve keeps the wavefront as its fallback: same buffers)
+        if ((method == VCS_METHOD_WAVEFRONT || method == VCS_METHOD_CERTIFIED) &&
+            sp->ver_off_host.empty()) {
             try {
                 vcs::ensure_wave_buffers(sp);
             } catch (const vcs::Error&) {
@@ -1055,11 +1295,16 @@ int enqueue_impl(vcs_space* sp, const vcs_solve_opts* opts, void* stream, int st
                 method = VCS_METHOD_JACOBI; // the version store does not fit right now
             }
         }
+        if (method == VCS_METHOD_CERTIFIED && sp->cert_xd.n < sp->S) {
+            sp->cert_xd.exact(sp->S, sp->stream);
+            sp->cert_lb.exact(static_cast<size_t>(sp->H) + 2, sp->stream);
+            VCS_CUDA(cudaStreamSynchronize(sp->stream));
+        }
         if (vcs::trace_enabled())
             std::fprintf(stderr, "[vcs solve] buffers %.3f ms\n", vcs::host_ms() - t0);
         const vcs::GraphKey key{o.epsilon, o.discount,
                                 method == VCS_METHOD_JACOBI && o.skip_converged ? 1 : 0, M,
-                                method, method == VCS_METHOD_WAVEFRONT ? stream_out : 0};
+                                method, method != VCS_METHOD_JACOBI ? stream_out : 0};
         const vcs::StreamUse s(sp, stream);
         auto& g = vcs::enqueue_solve(sp, key, s);
         sp->last_graph = &g;
@@ -1100,7 +1345,7 @@ int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int
     const int rc = enqueue_impl(sp, opts, nullptr, pinned_out ? 1 : 0);
     if (rc != VCS_OK) return rc;
     const vcs::CachedGraph& g = *sp->last_graph;
-    const bool overlap = g.method == vcs::kMethodWavefront && !g.layer_ev.empty() && pinned_out;
+    const bool overlap = g.method != vcs::kMethodJacobi && !g.layer_ev.empty() && pinned_out;
     if (!overlap) return vcs_solve_collect(sp, values_out, actions_out, report, nullptr);
     // Stream each layer's values/actions to the (pinned) host buffers as soon as its layer
     // kernel finished — the 12 B/state download overlaps the rest of the layer pass.
@@ -1146,7 +1391,7 @@ int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
         if (!sp->last_graph) raise(VCS_EINVAL, "no solve was enqueued on this space");
         vcs::bind_device(sp->device);
         auto& g = *sp->last_graph;
-        const bool wave = g.method == vcs::kMethodWavefront;
+        const bool wave = g.method != vcs::kMethodJacobi; // wavefront or certified: V in v[0]
         const vcs::StreamUse s(sp, stream);
         vcs::SolveCtrl ctrl{};
         VCS_CUDA(cudaMemcpyAsync(&ctrl, sp->ctrl.p, sizeof ctrl, cudaMemcpyDeviceToHost, s));
@@ -1170,7 +1415,15 @@ int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
             report->backups_ref = sp->S * static_cast<uint64_t>(K);
             const double dbar = sp->S ? static_cast<double>(sp->E) / static_cast<double>(sp->S) : 0.0;
             uint64_t done = 0;
-            if (wave) {
+            const bool certified = g.method == vcs::kMethodCertified && ctrl.certified;
+            if (certified) {
+                // two versions of every non-terminal state, once; per state: row_ptr 4 +
+                // value 8 + action 4 + winning action 4 + its (V_{m-1}, V_m) pair written 16 and
+                // read back 16; per edge: succ 4 + reward 8
+                const uint64_t nt = sp->layer_off[sp->H];
+                done = 2 * nt;
+                report->model_bytes = 20.0 * sp->S + 32.0 * nt + 12.0 * sp->E;
+            } else if (wave) {
                 done = vcs::wave_backups(sp); // every version of every state, once
                 // per state: row_ptr 4 + value out 8 + action out 4 + winning action 4; per
                 // edge: succ 4 + reward 8; per version: written once + read back once (8 + 8)
@@ -1182,7 +1435,9 @@ int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
             report->backups_done = done;
             report->sweep_ms = ms_sweep;
             report->extract_ms = ms_ext;
-            report->method = g.method;
+            report->method = g.method == vcs::kMethodCertified && !ctrl.certified
+                                 ? vcs::kMethodWavefront // the proof failed: the wavefront ran
+                                 : g.method;
             report->alg_bytes = (24.0 + 12.0 * dbar) * static_cast<double>(report->backups_ref);
             report->alg_bytes_done = (24.0 + 12.0 * dbar) * static_cast<double>(done);
         }

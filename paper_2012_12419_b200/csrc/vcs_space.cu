@@ -848,6 +848,7 @@ vcs_space::~vcs_space() {
             if (e) cudaEventDestroy(e);
     }
     if (d2h_stream) cudaStreamDestroy(d2h_stream);
+    if (aux_stream) cudaStreamDestroy(aux_stream);
     // the stream is idle: big blocks go to the per-device cache for the next space, the rest
     // back to the pool (stream-ordered frees are issued while the stream is alive)
     row_ptr.release_idle();
@@ -861,6 +862,8 @@ vcs_space::~vcs_space() {
     ctrl.release_idle();
     actions_dev.release_idle();
     ver.release_idle();
+    cert_xd.release_idle();
+    cert_lb.release_idle();
     band_ver.release_idle();
     ver_off.release_idle();
     layer_off_dev.release_idle();

@@ -362,7 +362,7 @@ class ViOptions:
     skip_converged: bool = True
     discount: float = 1.0
     device: int = 0
-    method: int = 0  # 0 auto (wavefront if it fits), 1 Jacobi sweeps, 2 layer wavefront
+    method: int = 0  # 0 auto (= 3 if the version store fits), 1 Jacobi, 2 wavefront, 3 certified
 
 
 class StateSpace:

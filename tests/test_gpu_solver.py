@@ -28,7 +28,14 @@ def _csr_equal(sp, osp):
 
 # (method, skip): every solver path must give the same bits
 METHODS = [(N.VCS_METHOD_JACOBI, True), (N.VCS_METHOD_JACOBI, False),
-           (N.VCS_METHOD_WAVEFRONT, True)]
+           (N.VCS_METHOD_WAVEFRONT, True), (N.VCS_METHOD_CERTIFIED, True)]
+
+
+def _ran(method):
+    """Methods a report may name for a requested method (a failed proof runs the wavefront)."""
+    if method == N.VCS_METHOD_CERTIFIED:
+        return (N.VCS_METHOD_CERTIFIED, N.VCS_METHOD_WAVEFRONT)
+    return (method,)
 
 
 def _solve(sp, eps=1e-6, skip=True, discount=1.0, method=N.VCS_METHOD_AUTO):
@@ -49,7 +56,7 @@ def test_named_cases_bitwise(gpu, oracle, golden, name):
         g = rec[f"eps={eps:g}"]
         for method, skip in METHODS:
             r = _solve(sp, eps, skip, method=method)
-            assert r.values.report.method == method
+            assert r.values.report.method in _ran(method)
             assert r.values.sweeps() == g["sweeps"]
             assert sha(r.values.raw_values()) == g["values_sha"]
             assert sha(r.policy.raw_actions()) == g["actions_sha"]
@@ -387,3 +394,54 @@ def test_shard_kernels_emulated_ranks(gpu, oracle):
             assert set(sweeps) == {sw_ref}
             assert np.array_equal(bits(values), bits(v_ref))
             assert np.array_equal(actions, a_ref)
+
+
+def test_certified_proof_and_fallback(gpu, golden):
+    """VCS_METHOD_CERTIFIED: the two-version backward pass is the whole solve exactly when its
+    residual lower bounds prove K* = H+1; early stops and sweep caps must take the wavefront
+    fallback (graph IF node).  Bits equal the reference's digests either way."""
+    import ctypes as C
+    p = V.load_instance(str(GOLDEN / "canonical_instance.txt"))
+    ni = V.NativeInstance(p.vcc, bots=p.bots)
+    sp = V.StateSpace.build_native(ni)
+    H = sp.task_count()
+
+    def run(eps, cap=0):
+        opts = N.vcs_solve_opts(eps, 1, cap, 1.0, N.VCS_METHOD_CERTIFIED)
+        vals = np.empty(sp.size())
+        acts = np.empty(sp.size(), np.int32)
+        rep = N.vcs_solve_report()
+        N.check(N.lib().vcs_solve(sp.handle, C.byref(opts), N.ptr(vals, C.c_double),
+                                  N.ptr(acts, C.c_int32), C.byref(rep)))
+        return vals, acts, rep
+
+    for eps in (1e-6, 5.0, 0.5):
+        g = golden["cases"]["canonical"][f"eps={eps:g}"]
+        vals, acts, rep = run(eps)
+        assert rep.sweeps == g["sweeps"]
+        assert sha(vals) == g["values_sha"] and sha(acts) == g["actions_sha"]
+        if g["sweeps"] == H + 1:
+            assert rep.method == N.VCS_METHOD_CERTIFIED, eps  # the proof holds
+        else:
+            assert rep.method == N.VCS_METHOD_WAVEFRONT, eps  # early stop: the fallback ran
+    # a sweep cap below H+1 can never be certified
+    vals, acts, rep = run(1e-6, cap=H)
+    assert rep.sweeps == H and rep.method == N.VCS_METHOD_WAVEFRONT
+    # the same graph alternates between both outcomes when re-run with other options
+    vals, acts, rep = run(1e-6)
+    assert rep.method == N.VCS_METHOD_CERTIFIED
+    assert sha(vals) == golden["cases"]["canonical"]["eps=1e-06"]["values_sha"]
+
+
+def test_certified_full_size(gpu, golden):
+    """C3 and C4: the proof holds and the single pass reproduces the reference digests."""
+    for gen, name in (((N.VCS_GEN_HOMOG, 2012, 0, 5, 8, 40, 3), "C3"),
+                      ((N.VCS_GEN_HOMOG, 2012, 0, 6, 8, 48, 3), "C4")):
+        ni = V.generate_instance(*gen, as_objects=False)
+        sp = V.StateSpace.build_native(ni, 10**9)
+        r = _solve(sp, method=N.VCS_METHOD_CERTIFIED)
+        g = golden["cases"][name]["eps=1e-06"]
+        assert r.values.report.method == N.VCS_METHOD_CERTIFIED
+        assert r.values.sweeps() == g["sweeps"] == sp.task_count() + 1
+        assert sha(r.values.raw_values()) == g["values_sha"]
+        assert sha(r.policy.raw_actions()) == g["actions_sha"]
