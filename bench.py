@@ -121,7 +121,8 @@ def ncu_traffic(method):
     """DRAM bytes per launch of the profiled launch of the dominant kernel (from the committed
     ncu capture summary under profiles/), or None."""
     from paper_2012_12419_b200 import _native as N
-    name = "ncu_wave.json" if method == N.VCS_METHOD_WAVEFRONT else "ncu_sweep.json"
+    name = {N.VCS_METHOD_WAVEFRONT: "ncu_wave.json",
+            N.VCS_METHOD_CERTIFIED: "ncu_cert.json"}.get(method, "ncu_sweep.json")
     p = ROOT / "profiles" / name
     if not p.exists():
         return None
@@ -296,7 +297,7 @@ def run_b200(args):
     S, E, H = space.size(), space.edges(), space.task_count()
     log(f"[rank {rank}] built {desc}: S={S} E={E} H={H} in {space.info.build_ms:.1f} ms")
     method = {"auto": N.VCS_METHOD_AUTO, "jacobi": N.VCS_METHOD_JACOBI,
-              "wavefront": N.VCS_METHOD_WAVEFRONT}[args.method]
+              "wavefront": N.VCS_METHOD_WAVEFRONT, "certified": N.VCS_METHOD_CERTIFIED}[args.method]
     opts = N.vcs_solve_opts(args.eps, 0 if args.no_skip else 1, 0, 1.0, method)
     # A dedicated (non-default) stream: the library, torch's events and NCCL all order on it.
     stream = torch.cuda.Stream(dev)
@@ -436,7 +437,14 @@ def run_b200(args):
     if sweep_s:
         tr = ncu_traffic(method)
         survey_equiv = b_ref * S * sweeps / sweep_s / 1e9  # SURVEY 8d bytes of the Jacobi sweeps
-        if method == N.VCS_METHOD_WAVEFRONT:
+        if method == N.VCS_METHOD_CERTIFIED:
+            # k_cert_layer (all H launches of one solve; the proof held, no fallback ran): per
+            # state row_ptr 4 + value 8 + action 4 + winner's action 4 + (V_{m-1}, V_m) pair
+            # written 16 and read back 16, per edge succ 4 + reward 8
+            alg = model_bytes
+            formula = "20*S + 32*S_nonterminal + 12*E per solve (DESIGN.md 3.5)"
+            kernel = "k_cert_layer<false,4,4> (all H layer launches of one solve)"
+        elif method == N.VCS_METHOD_WAVEFRONT:
             # k_wave_layer (all H launches of one solve, extraction fused): per state row_ptr 4
             # + value 8 + action 4 + winner's action 4, per edge succ 4 + reward 8, per
             # performed backup (state, version) 16 (written once, read once by layer t-1)
@@ -467,7 +475,7 @@ def run_b200(args):
         "data": "synthetic",
         "config": {"workload": desc, "states": S, "transitions": E, "horizon": H,
                    "sweeps": sweeps, "epsilon": args.eps, "layer_skip": not args.no_skip,
-                   "method": {1: "jacobi", 2: "layer-wavefront"}.get(method, str(method)),
+                   "method": {1: "jacobi", 2: "layer-wavefront", 3: "certified backward pass"}.get(method, str(method)),
                    "backups_performed_per_step": backups_done,
                    "parallelism": "single GPU" if not sharded_path else
                    PARALLELISM[sharding](world),
@@ -503,8 +511,10 @@ def main():
     ap.add_argument("--eps", type=float, default=1e-6)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-skip", action="store_true", help="disable the converged-layer skip")
-    ap.add_argument("--method", choices=["auto", "jacobi", "wavefront"], default="auto",
-                    help="single-GPU solver (auto = layer wavefront when it fits in HBM)")
+    ap.add_argument("--method", choices=["auto", "jacobi", "wavefront", "certified"],
+                    default="auto",
+                    help="single-GPU solver (auto = certified pass with the wavefront as fallback "
+                         "when the version store fits in HBM, else Jacobi)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharding", choices=["auto", "wave", "halo", "allgather"], default="auto",
                     help="N>1: version-band wavefront (auto unless --method jacobi), or Jacobi "

@@ -1,10 +1,11 @@
-"""Summarise an ncu --set full capture of k_wave_layer (C4, tools/prof_sweep.py) into
-profiles/ncu_wave.json: per captured launch, DRAM traffic vs the algorithmic bytes of that layer.
+"""Summarise an ncu --set full capture of k_wave_layer or k_cert_layer (C4,
+tools/prof_sweep.py) into profiles/ncu_{wave,cert}.json: per captured launch, DRAM traffic vs
+the algorithmic bytes of that layer.
 
-    python tools/ncu_summary.py gpurun_out/prof_wave.ncu-rep <first_skip> [out.json]
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep <first_skip> [out.json] [wave|cert]
 
-`first_skip` is the -s value used for the capture: k_wave_layer launches are numbered over
-two solves of H=48 layer launches each, layers descending (t = H-1 .. 0)."""
+`first_skip` is the -s value used for the capture: layer launches are numbered over two solves
+of H=48 layer launches each, layers descending (t = H-1 .. 0)."""
 import csv
 import io
 import json
@@ -15,7 +16,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 
 
-def main(rep, skip, out=None):
+def main(rep, skip, out=None, kind="wave"):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -34,6 +35,11 @@ def main(rep, skip, out=None):
         # reward 8 per edge, versions written (8 per backup) and the successor versions read
         # once (8 * n_{t+1} * (m-1))
         alg = 20 * n + 12 * e + 8 * n * m + 8 * n_next * (m - 1)
+        if kind == "cert":
+            # certified pass: per state row_ptr 4 + value 8 + action 4 + winner's action 4 +
+            # its (V_{m-1}, V_m) pair written 16; per edge succ 4 + reward 8; the successors'
+            # pairs read once (16 * n_{t+1})
+            alg = 20 * n + 16 * n + 12 * e + 16 * n_next
         g = lambda k: float(r[hdr.index(k)]) * scale.get(units[hdr.index(k)], 1)
         dram = g("dram__bytes_read.sum") + g("dram__bytes_write.sum")
         tt = float(r[hdr.index("gpu__time_duration.sum")]) * (1e-6 if units[hdr.index("gpu__time_duration.sum")] == "us" else 1e-9)
@@ -43,13 +49,15 @@ def main(rep, skip, out=None):
                          "l2_hit_pct": float(r[hdr.index("lts__t_sector_hit_rate.pct")]),
                          "warps_active_pct": float(r[hdr.index("sm__warps_active.avg.pct_of_peak_sustained_active")]),
                          "issue_active_pct": float(r[hdr.index("smsp__issue_active.avg.pct_of_peak_sustained_active")])})
-    summary = {"kernel": "k_wave_layer<false>", "capture": f"ncu --set full, C4, launches {skip}..{skip + len(launches) - 1} of tools/prof_sweep.py",
+    summary = {"kernel": "k_cert_layer<false,4,4>" if kind == "cert" else "k_wave_layer<false>",
+               "capture": f"ncu --set full, C4, launches {skip}..{skip + len(launches) - 1} of tools/prof_sweep.py",
                "dram_bytes_per_launch": launches[0]["dram_bytes"],
                "alg_bytes_per_launch": launches[0]["alg_bytes"], "launches": launches,
                "note": "dram/alg = %.2f on layer %d" % (launches[0]["dram_over_alg"], launches[0]["layer"])}
-    Path(out or ROOT / "profiles" / "ncu_wave.json").write_text(json.dumps(summary, indent=1))
+    Path(out or ROOT / "profiles" / f"ncu_{kind}.json").write_text(json.dumps(summary, indent=1))
     print(json.dumps(summary, indent=1)[:1500])
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]), sys.argv[3] if len(sys.argv) > 3 else None)
+    main(sys.argv[1], int(sys.argv[2]), sys.argv[3] if len(sys.argv) > 3 else None,
+         sys.argv[4] if len(sys.argv) > 4 else "wave")
