@@ -213,6 +213,9 @@ def run_reference(args):
 
 
 PARALLELISM = {
+    "single": lambda n: "single GPU",
+    "instances": lambda n: f"{n} independent instances, one per GPU (weak scaling; no data-path "
+                           "collective, barrier + max-over-ranks timing)",
     "wave": lambda n: f"version-band sharded wavefront x{n}: one column per layer over NCCL "
                       "send/recv + one MAX all-reduce per solve",
     "halo": lambda n: f"row-block sharded Jacobi x{n}: forward halo over NCCL + MAX all-reduce "
@@ -280,16 +283,23 @@ def run_b200(args):
         log(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    # the sharded drivers run for N>1, or at N=1 when --sharding names one (a 1-rank group)
-    sharded_path = world > 1 or args.sharding != "auto"
-    if sharded_path:
+    # N>1 default: independent instances, one per GPU (weak scaling, no data-path collective);
+    # --sharding wave/halo/allgather shards ONE instance (also at N=1, through a 1-rank group)
+    sharding = args.sharding
+    if sharding == "auto":
+        sharding = "instances" if world > 1 else "single"
+    sharded_path = sharding in ("wave", "halo", "allgather")
+    use_dist = world > 1 or sharding != "single"
+    if use_dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
         os.environ.setdefault("RANK", str(rank))
         os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=dev)
-    sharding = args.sharding
     gen, desc = WORKLOADS[args.workload]
+    if sharding == "instances":  # rank r solves trial r of the same generator family
+        gen = gen[:2] + (rank,) + gen[3:]
+        desc = f"{desc}; rank r solves trial r of the family"
     ni = V.generate_instance(*gen, as_objects=False)
     t0 = time.time()
     space = V.StateSpace.build_native(ni, 10**9, local)
@@ -314,6 +324,8 @@ def run_b200(args):
         N.check(N.lib().vcs_solve_collect(space.handle, None, None, C.byref(rep), h_stream))
         sweeps = rep.sweeps
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         launches0 = N.kernel_launches()
         sweep_ms, extract_ms = [], []
@@ -323,11 +335,17 @@ def run_b200(args):
             N.check(N.lib().vcs_solve_enqueue(space.handle, C.byref(opts), h_stream))
         ev1.record(stream)
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         tw1 = time.time()
         launches = N.kernel_launches() - launches0
         # the library's in-graph events of the last step split sweeps vs extraction
         N.check(N.lib().vcs_solve_collect(space.handle, None, None, C.byref(rep), h_stream))
         total_ms = ev0.elapsed_time(ev1)
+        if world > 1:  # max over ranks
+            t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            total_ms = float(t.item())
         sweep_ms.append(rep.sweep_ms)
         extract_ms.append(rep.extract_ms)
         sampler.mark(tw0, tw1)
@@ -338,8 +356,6 @@ def run_b200(args):
     else:
         from paper_2012_12419_b200 import sharded as SH
         lo, le = space.layer_offsets(), space.layer_edges()
-        if sharding == "auto":
-            sharding = "halo" if method == N.VCS_METHOD_JACOBI else "wave"
         if sharding == "wave":
             opts.method = N.VCS_METHOD_WAVEFRONT
             backend = SH.WaveBandCuda(space, dev, stream)
@@ -388,13 +404,20 @@ def run_b200(args):
 
     sampler.stop()
     ms_per_step = total_ms / args.steps
-    value = S * sweeps * args.steps / (total_ms * 1e-3)
+    backups_step = S * sweeps  # reference-equivalent backups of one step, all ranks
+    if sharding == "instances":
+        t = torch.tensor([float(S * sweeps)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        backups_step = float(t.item())
+    value = backups_step * args.steps / (total_ms * 1e-3)
     dbar = E / S
     b_ref = 24 + 12 * dbar
 
     # ---- e2e through the C ABI with host buffers (rank 0 / N=1 path) --------------------------
     e2e = None
     if not sharded_path and args.e2e_steps > 0:
+        if world > 1:
+            dist.barrier()
         vals = torch.empty(S, dtype=torch.float64, pin_memory=True)
         acts = torch.empty(S, dtype=torch.int32, pin_memory=True)
         inst_bytes = 0
@@ -420,8 +443,17 @@ def run_b200(args):
                 e2e_times.append(t1 - t0)
                 parts.append((tb - t0, t1 - tb))
         e2e_t = statistics.median(e2e_times)
-        e2e = {"value": S * rep2.sweeps / e2e_t, "unit": "backups/s",
-               "h2d_bytes_per_step": inst_bytes, "d2h_bytes_per_step": S * (8 + 4),
+        e2e_backups = S * rep2.sweeps
+        if world > 1:  # all ranks' instances, slowest rank's median step
+            t = torch.tensor([e2e_t, float(e2e_backups)], dtype=torch.float64, device=dev)
+            tm = t.clone()
+            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            e2e_t, e2e_backups = float(tm[0].item()), float(t[1].item())
+            inst_bytes *= world
+        e2e = {"value": e2e_backups / e2e_t, "unit": "backups/s",
+               "h2d_bytes_per_step": inst_bytes,
+               "d2h_bytes_per_step": S * (8 + 4) * (world if world > 1 else 1),
                "ms_per_step": e2e_t * 1e3,
                "build_ms": statistics.median(p[0] for p in parts) * 1e3,
                "solve_and_d2h_ms": statistics.median(p[1] for p in parts) * 1e3,
@@ -471,14 +503,14 @@ def run_b200(args):
     line = {
         "metric": METRIC, "value": value, "unit": "backups/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak" if sharding == "instances" else "strong",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": desc, "states": S, "transitions": E, "horizon": H,
                    "sweeps": sweeps, "epsilon": args.eps, "layer_skip": not args.no_skip,
                    "method": {1: "jacobi", 2: "layer-wavefront", 3: "certified backward pass"}.get(method, str(method)),
                    "backups_performed_per_step": backups_done,
-                   "parallelism": "single GPU" if not sharded_path else
-                   PARALLELISM[sharding](world),
+                   "parallelism": PARALLELISM[sharding](world),
                    "l2": "no flush: CSR 1.7 GB and V buffers 2x155 MB exceed the 126 MB L2",
                    "build_ms": space.info.build_ms, "build_wall_ms": build_wall_ms},
         "time_to_convergence_ms": ms_per_step,
@@ -496,7 +528,7 @@ def run_b200(args):
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     if rank == 0:
         print(json.dumps(line))
-    if sharded_path:
+    if use_dist:
         dist.destroy_process_group()
     return 0
 
@@ -516,9 +548,11 @@ def main():
                     help="single-GPU solver (auto = certified pass with the wavefront as fallback "
                          "when the version store fits in HBM, else Jacobi)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--sharding", choices=["auto", "wave", "halo", "allgather"], default="auto",
-                    help="N>1: version-band wavefront (auto unless --method jacobi), or Jacobi "
-                         "row blocks with a forward halo / a full all-gather of V per sweep")
+    ap.add_argument("--sharding", choices=["auto", "instances", "wave", "halo", "allgather"],
+                    default="auto",
+                    help="auto: single GPU at N=1, independent instances (one per GPU) at N>1; "
+                         "wave / halo / allgather shard ONE instance: version-band wavefront, "
+                         "Jacobi row blocks with a forward halo / a full all-gather of V")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         log("note: the timing rules ask for >= 3 warm-up steps")
