@@ -19,6 +19,7 @@
 // packed into 64-bit words, ceil(log2(vm_free+1)) bits per cloud.
 #include "vcs_device.cuh"
 
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
@@ -466,6 +467,456 @@ void exclusive_scan(Scratch& sc, InputIt in, uint32_t* out, uint64_t n, cudaStre
     sc.cub_tmp.exact(bytes, s);
     VCS_CUDA(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.p, bytes, in, out, static_cast<int64_t>(n), s));
     note_launch();
+}
+
+// ---- persistent dense builder ----------------------------------------------------------------
+// When every layer's successor key space is dense (mixed-radix index, see LayerParam) and the
+// CSR fits at its a-priori bound, the whole build is ONE cooperative kernel: per layer
+//   phase 1  degrees of the block's state chunk -> block sums                      | grid sync
+//   phase 2  each block scans the block sums itself; emit edges (reward bits as k_emit_dense),
+//            row offsets, atomicMin of the edge into the first-edge table        | grid sync
+//   phase 3  first-occurrence flags of the block's edge chunk -> block sums          | grid sync
+//   phase 4  ranks of first edges = successor indices in BFS order; first edges write the next
+//            frontier's keys and rank_of[idx]; the state cap is checked           | grid sync
+//   phase 5  (with the next layer's phase 1) successor ids of every edge; clear the table
+// No host round trip per layer (the multi-kernel path needs one to size the next layer).
+namespace cg = cooperative_groups;
+
+struct DenseBuild {
+    const LayerParam* __restrict__ params; // H
+    uint64_t* keys;
+    uint32_t* row_ptr;
+    uint32_t* succ;
+    double* reward;
+    int32_t* action;
+    uint32_t* table0;    // first-edge tables, alternating per layer (dense_max entries each)
+    uint32_t* table1;
+    uint32_t* rank_of;   // successor index -> its layer-local state index
+    uint32_t* bsum;      // per (round, block)
+    uint64_t* info;      // n_t for t = 0..H at [t], E_t for t = 0..H-1 at [H+1+t]
+    int32_t* status;     // 0 ok, 1 state cap exceeded, 2 more than 2^32-1 states
+    uint64_t state_cap;
+    uint32_t dense_max;
+    int max_rounds;      // bsum holds max_rounds x gridDim.x entries
+    int H;
+};
+
+constexpr int kDenseThreads = 256;
+constexpr int kDenseSlots = 8; // edge slots of a state: clouds 0..6 by key position, 7 = paid
+
+// A state's edges in static slots (registers only): slot p < 7 is the edge choosing the cloud at
+// key position p (valid if eligible with enough free VMs), slot 7 the paid edge (always valid).
+// off[e] = the edge's index within the state's row (the reference's order: clouds ascending,
+// paid last); idx[e] = the successor's mixed-radix index.
+template <int WM>
+struct StateEdges {
+    uint32_t idx[kDenseSlots];
+    uint32_t off[kDenseSlots];
+    bool valid[kDenseSlots];
+    uint32_t deg;
+    __device__ __forceinline__ StateEdges(const uint64_t (&k)[WM], const LayerParam& L) {
+        uint32_t f[kDenseSlots - 1];
+        uint32_t basei = 0;
+#pragma unroll
+        for (int p = 0; p < kDenseSlots - 1; ++p) {
+            f[p] = p < L.n_active ? static_cast<uint32_t>(get_field<WM>(k, L.bit_off[p], L.width[p])) : 0u;
+            if (p < L.n_active && L.keep_idx[p] >= 0) basei += f[p] * L.wnext[p];
+        }
+        uint32_t o = 0;
+#pragma unroll
+        for (int p = 0; p < kDenseSlots - 1; ++p) {
+            valid[p] = p < L.n_active && L.attr[p] && f[p] >= static_cast<uint32_t>(L.demand);
+            off[p] = o;
+            idx[p] = (p < L.n_active && L.keep_idx[p] >= 0)
+                         ? basei - static_cast<uint32_t>(L.demand) * L.wnext[p]
+                         : basei;
+            o += valid[p] ? 1u : 0u;
+        }
+        valid[kDenseSlots - 1] = true;
+        off[kDenseSlots - 1] = o;
+        idx[kDenseSlots - 1] = basei;
+        deg = o + 1;
+    }
+};
+
+// Successor key of the edge choosing key position p (-1 = paid), in layer t+1's packing.
+template <int WM>
+__device__ __forceinline__ void next_key(const uint64_t (&k)[WM], int p, const LayerParam& L,
+                                         uint64_t (&nk)[WM]) {
+#pragma unroll
+    for (int w = 0; w < WM; ++w) nk[w] = 0ull;
+    if (L.n_keep == L.n_active) { // same layout: subtract the demand from the chosen field
+#pragma unroll
+        for (int w = 0; w < WM; ++w) nk[w] = k[w];
+        if (p >= 0) {
+            const int off = L.bit_off[p];
+#pragma unroll
+            for (int w = 0; w < WM; ++w)
+                if (w == (off >> 6)) nk[w] -= static_cast<uint64_t>(L.demand) << (off & 63);
+        }
+        return;
+    }
+    for (int q = 0; q < L.n_active; ++q) {
+        if (L.keep_idx[q] < 0) continue;
+        int v = get_field<WM>(k, L.bit_off[q], L.width[q]);
+        if (q == p) v -= L.demand;
+        put_field<WM>(nk, L.next_bit_off[q], static_cast<uint64_t>(v));
+    }
+}
+
+// Prefixes of (round r, block b) for every round r over the per-(round, block) sums in
+// round-major order (one blocked scan of the R x G values, a few thousand), into s_before[r];
+// returns the grand total.
+__device__ __forceinline__ uint32_t round_prefixes(const uint32_t* __restrict__ bsum, int R, int G,
+                                                   int b, uint32_t* s_before) {
+    using Scan = cub::BlockScan<uint32_t, kDenseThreads>;
+    __shared__ typename Scan::TempStorage scan;
+    const int N = R * G;
+    const int per = (N + kDenseThreads - 1) / kDenseThreads;
+    const int i0 = threadIdx.x * per, i1 = min(N, i0 + per);
+    uint32_t loc = 0;
+    for (int i = i0; i < i1; ++i) loc += __ldcg(bsum + i);
+    uint32_t off, total;
+    Scan(scan).ExclusiveSum(loc, off, total);
+    for (int r = 0; r < R; ++r) {
+        const int pos = r * G + b;
+        if (pos >= i0 && pos < i1) {
+            uint32_t v = off;
+            for (int i = i0; i < pos; ++i) v += __ldcg(bsum + i);
+            s_before[r] = v;
+        }
+    }
+    __syncthreads();
+    return total;
+}
+
+// Per-round block sums without a block barrier per round: warp sums, shared atomics.
+__device__ __forceinline__ void round_add(uint32_t* s_round, int r, uint32_t v) {
+    const uint32_t w = __reduce_add_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0 && w) atomicAdd(s_round + r, w);
+}
+
+template <int WM, int MINB>
+__global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild A) {
+    using Scan = cub::BlockScan<uint32_t, kDenseThreads>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ LayerParam sL;
+    __shared__ uint32_t s_round[8];  // per-round block sums
+    __shared__ uint32_t s_before[8]; // per-round prefixes of this block
+    cg::grid_group grid = cg::this_grid();
+    const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+    const uint32_t T = static_cast<uint32_t>(G) * blockDim.x; // states per round
+    const uint32_t q = static_cast<uint32_t>(b) * blockDim.x + tid;
+    uint64_t S_t = 0;   // first state of layer t
+    uint64_t E = 0;     // edges of layers < t
+    uint64_t key_t = 0; // first key word of layer t
+    uint32_t n_t = 1;
+    if (b == 0 && tid == 0) A.info[0] = 1;
+    auto publish_rounds = [&](int R) { // s_round -> bsum[r * G + b]
+        __syncthreads();
+        if (tid < R) A.bsum[tid * G + b] = s_round[tid];
+    };
+    for (int t = 0; t < A.H; ++t) {
+        __syncthreads();
+        for (int i = tid; i < static_cast<int>(sizeof(LayerParam) / 4); i += blockDim.x)
+            reinterpret_cast<uint32_t*>(&sL)[i] = reinterpret_cast<const uint32_t*>(A.params + t)[i];
+        if (tid < 8) s_round[tid] = 0;
+        __syncthreads();
+        const LayerParam& L = sL;
+        uint32_t* table = (t & 1) ? A.table1 : A.table0;
+        const uint64_t S_next = S_t + n_t;
+        const uint64_t key_next = key_t + static_cast<uint64_t>(n_t) * L.words;
+        const int R = static_cast<int>((n_t + T - 1) / T); // rounds: state r*T + q
+        const bool retires = L.n_keep != L.n_active;
+        auto key_of = [&](uint32_t i, uint64_t (&k)[WM]) {
+            load_key<WM>(A.keys + key_t + static_cast<uint64_t>(i) * L.words, L.words, k);
+        };
+        // phase 1: degrees per (round, block)
+        for (int r = 0; r < R; ++r) {
+            const uint32_t i = static_cast<uint32_t>(r) * T + q;
+            uint32_t d = 0;
+            if (i < n_t) {
+                uint64_t k[WM];
+                key_of(i, k);
+                d = StateEdges<WM>(k, L).deg;
+            }
+            round_add(s_round, r, d);
+        }
+        publish_rounds(R);
+        grid.sync();
+        // phase 2: row offsets, rewards, actions, first-edge atomicMin
+        const uint32_t E_t = round_prefixes(A.bsum, R, G, b, s_before);
+        uint32_t jfirst[8]; // my state's first edge (layer-local) per round
+        for (int r = 0; r < R; ++r) {
+            const uint32_t i = static_cast<uint32_t>(r) * T + q;
+            uint64_t k[WM] = {};
+            if (i < n_t) key_of(i, k);
+            const StateEdges<WM> se(k, L);
+            const uint32_t deg = i < n_t ? se.deg : 0u;
+            uint32_t excl;
+            Scan(scan_tmp).ExclusiveSum(deg, excl);
+            __syncthreads();
+            const uint32_t j = s_before[r] + excl;
+#pragma unroll
+            for (int rr = 0; rr < 8; ++rr)
+                if (rr == r) jfirst[rr] = j;
+            if (i < n_t) {
+                A.row_ptr[S_t + i] = static_cast<uint32_t>(E + j);
+                uint32_t cur[kDenseSlots];
+#pragma unroll
+                for (int e = 0; e < kDenseSlots; ++e)
+                    if (se.valid[e]) cur[e] = table[se.idx[e]]; // the state's checks in flight
+#pragma unroll
+                for (int e = 0; e < kDenseSlots; ++e) {
+                    if (!se.valid[e]) continue;
+                    const int pe = e == kDenseSlots - 1 ? -1 : e;
+                    const uint32_t je = j + se.off[e];
+                    A.reward[E + je] = retires ? retiring_reward<WM>(k, pe, L)
+                                               : (pe < 0 ? L.r_paid_kept : L.r_cloud_kept);
+                    A.action[E + je] = pe < 0 ? -1 : L.cloud[pe];
+                    if (cur[e] > je) atomicMin(&table[se.idx[e]], je); // first edge wins
+                }
+            }
+        }
+        if (tid < 8) s_round[tid] = 0;
+        grid.sync();
+        // phase 3: first-occurrence flags per (round, block)
+        for (int r = 0; r < R; ++r) {
+            const uint32_t i = static_cast<uint32_t>(r) * T + q;
+            uint32_t f = 0;
+            if (i < n_t) {
+                uint64_t k[WM];
+                key_of(i, k);
+                const StateEdges<WM> se(k, L);
+                uint32_t j = 0;
+#pragma unroll
+                for (int rr = 0; rr < 8; ++rr)
+                    if (rr == r) j = jfirst[rr];
+                uint32_t cur[kDenseSlots];
+#pragma unroll
+                for (int e = 0; e < kDenseSlots; ++e)
+                    if (se.valid[e]) cur[e] = __ldcg(table + se.idx[e]);
+#pragma unroll
+                for (int e = 0; e < kDenseSlots; ++e)
+                    if (se.valid[e]) f += cur[e] == j + se.off[e] ? 1u : 0u;
+            }
+            round_add(s_round, r, f);
+        }
+        publish_rounds(R);
+        grid.sync();
+        // phase 4: ranks of first edges = successor indices; next frontier keys; cap check
+        const uint32_t n_next = round_prefixes(A.bsum, R, G, b, s_before);
+        if (S_next + n_next > A.state_cap || S_next + n_next >= 0xffffffffull) {
+            if (b == 0 && tid == 0) {
+                *A.status = S_next + n_next > A.state_cap ? 1 : 2;
+                A.info[t + 1] = n_next;
+            }
+            return; // every block takes the same decision
+        }
+        for (int r = 0; r < R; ++r) {
+            const uint32_t i = static_cast<uint32_t>(r) * T + q;
+            uint64_t k[WM] = {};
+            uint32_t f = 0;
+            uint32_t cur[kDenseSlots];
+            uint32_t j = 0;
+#pragma unroll
+            for (int rr = 0; rr < 8; ++rr)
+                if (rr == r) j = jfirst[rr];
+            if (i < n_t) key_of(i, k);
+            const StateEdges<WM> se(k, L);
+            if (i < n_t) {
+#pragma unroll
+                for (int e = 0; e < kDenseSlots; ++e)
+                    if (se.valid[e]) cur[e] = __ldcg(table + se.idx[e]);
+#pragma unroll
+                for (int e = 0; e < kDenseSlots; ++e)
+                    if (se.valid[e]) f += cur[e] == j + se.off[e] ? 1u : 0u;
+            }
+            uint32_t rank;
+            Scan(scan_tmp).ExclusiveSum(f, rank);
+            __syncthreads();
+            rank += s_before[r];
+            if (f) {
+#pragma unroll
+                for (int e = 0; e < kDenseSlots; ++e) {
+                    if (!se.valid[e] || cur[e] != j + se.off[e]) continue;
+                    A.rank_of[se.idx[e]] = rank;
+                    uint64_t nk[WM];
+                    next_key<WM>(k, e == kDenseSlots - 1 ? -1 : e, L, nk);
+                    uint64_t* dst = A.keys + key_next + static_cast<uint64_t>(rank) * L.next_words;
+#pragma unroll
+                    for (int w = 0; w < WM; ++w)
+                        if (w < L.next_words) dst[w] = nk[w];
+                    ++rank;
+                }
+            }
+        }
+        if (b == 0 && tid == 0) {
+            A.info[t + 1] = n_next;
+            A.info[A.H + 1 + t] = E_t;
+        }
+        grid.sync();
+        // phase 5: successor ids; clear this layer's table for layer t+2 (layer t+1 uses the
+        // other one; rank_of is rewritten by the next layer's phase 4, two grid syncs later)
+        for (int r = 0; r < R; ++r) {
+            const uint32_t i = static_cast<uint32_t>(r) * T + q;
+            if (i >= n_t) continue;
+            uint64_t k[WM];
+            key_of(i, k);
+            const StateEdges<WM> se(k, L);
+            uint32_t j = 0;
+#pragma unroll
+            for (int rr = 0; rr < 8; ++rr)
+                if (rr == r) j = jfirst[rr];
+            uint32_t rk[kDenseSlots];
+#pragma unroll
+            for (int e = 0; e < kDenseSlots; ++e)
+                if (se.valid[e]) rk[e] = __ldcg(A.rank_of + se.idx[e]);
+#pragma unroll
+            for (int e = 0; e < kDenseSlots; ++e)
+                if (se.valid[e]) A.succ[E + j + se.off[e]] = static_cast<uint32_t>(S_next) + rk[e];
+        }
+        for (uint32_t i = q; i < A.dense_max; i += T) table[i] = kEmpty32;
+        S_t = S_next;
+        E += E_t;
+        key_t = key_next;
+        n_t = n_next;
+    }
+    // the terminal layer's rows have no edges (mdp.cpp:207-209)
+    for (uint32_t i = q; i <= n_t; i += T) A.row_ptr[S_t + i] = static_cast<uint32_t>(E);
+}
+
+// Host side of the persistent dense builder.  Returns false (nothing done) when it does not
+// apply: some layer's key space is not dense, the a-priori CSR bound is not affordable, or the
+// device cannot launch cooperative kernels.  VCS_BUILD_LAYERED forces the multi-kernel path.
+template <int WM>
+bool build_dense(vcs_space* sp, uint64_t state_cap) {
+    const bool layered = std::getenv("VCS_BUILD_LAYERED") != nullptr; // (read per build: tests)
+    const LayerPlan& pl = sp->plan;
+    const int H = pl.horizon;
+    if (layered || H < 1) return false;
+    uint64_t s_bound = 1, e_bound = 0, k_bound = static_cast<uint64_t>(pl.words[0]);
+    uint64_t e_layer_max = 1, dense_max = 1, nb = 1;
+    for (int t = 0; t < H; ++t) {
+        const LayerParam& L = pl.layers[static_cast<size_t>(t)];
+        if (!L.dense_size || L.n_active > kDenseSlots - 1) return false;
+        int maxdeg = 1;
+        for (int p = 0; p < L.n_active; ++p) maxdeg += L.attr[p] ? 1 : 0;
+        const uint64_t e_ub = nb * static_cast<uint64_t>(maxdeg);
+        e_bound += e_ub;
+        e_layer_max = std::max(e_layer_max, e_ub);
+        dense_max = std::max<uint64_t>(dense_max, L.dense_size);
+        nb = std::min<uint64_t>({nb * static_cast<uint64_t>(maxdeg), state_cap, L.dense_size});
+        s_bound += nb;
+        k_bound += nb * static_cast<uint64_t>(L.next_words);
+        if (e_bound >= 0xffffffffull || s_bound >= 0xffffffffull) return false;
+    }
+    const uint64_t bytes = e_bound * 16 + s_bound * 4 + k_bound * 8 + e_layer_max * 4 + dense_max * 12;
+    if (bytes > device_bytes(sp->device) / 8) return false;
+    int coop = 0;
+    VCS_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, sp->device));
+    if (!coop) return false;
+    // (2 blocks per SM at ~125 registers: forcing 3 or 4 spills and measured slower)
+    const void* fn = reinterpret_cast<const void*>(k_build_dense<WM, 2>);
+    int per_sm = 0;
+    VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kDenseThreads, 0));
+    if (per_sm < 1) return false;
+    const int G = per_sm * sp->num_sms;
+    // rounds of G*256 states per layer (the kernel keeps <= 8 per-round offsets in registers)
+    uint64_t n_max = 1;
+    {
+        uint64_t nb2 = 1;
+        for (int t = 0; t < H; ++t) {
+            const LayerParam& L = pl.layers[static_cast<size_t>(t)];
+            int maxdeg = 1;
+            for (int p = 0; p < L.n_active; ++p) maxdeg += L.attr[p] ? 1 : 0;
+            nb2 = std::min<uint64_t>({nb2 * static_cast<uint64_t>(maxdeg), state_cap, L.dense_size});
+            n_max = std::max(n_max, nb2);
+        }
+    }
+    const uint64_t T = static_cast<uint64_t>(G) * kDenseThreads;
+    const int max_rounds = static_cast<int>((n_max + T - 1) / T);
+    if (max_rounds > 8) return false;
+
+    const double t_setup = trace_enabled() ? host_ms() : 0.0;
+    cudaStream_t s = sp->stream;
+    sp->keys.reserve(k_bound, 0, s);
+    sp->row_ptr.reserve(s_bound + 1, 0, s);
+    sp->succ.reserve(e_bound, 0, s);
+    sp->reward.reserve(e_bound, 0, s);
+    sp->action.reserve(e_bound, 0, s);
+    DevBuf<uint32_t> tables, rank_of, bsum;
+    DevBuf<uint64_t> info;
+    DevBuf<int32_t> status;
+    DevBuf<LayerParam> params;
+    tables.exact(2 * dense_max, s);
+    rank_of.exact(dense_max, s);
+    bsum.exact(static_cast<size_t>(G) * max_rounds, s);
+    info.exact(2 * static_cast<size_t>(H) + 2, s);
+    status.exact(1, s);
+    params.exact(static_cast<size_t>(H), s);
+    VCS_CUDA(cudaMemcpyAsync(params.p, pl.layers.data(), H * sizeof(LayerParam),
+                             cudaMemcpyHostToDevice, s));
+    VCS_CUDA(cudaMemcpyAsync(sp->keys.p, pl.init_key.data(), pl.words[0] * sizeof(uint64_t),
+                             cudaMemcpyHostToDevice, s));
+    VCS_CUDA(cudaMemsetAsync(tables.p, 0xff, 2 * dense_max * sizeof(uint32_t), s));
+    VCS_CUDA(cudaMemsetAsync(status.p, 0, sizeof(int32_t), s));
+    VCS_CUDA(cudaMemsetAsync(info.p, 0, (2 * static_cast<size_t>(H) + 2) * sizeof(uint64_t), s));
+    DenseBuild A{};
+    A.params = params.p;
+    A.keys = sp->keys.p;
+    A.row_ptr = sp->row_ptr.p;
+    A.succ = sp->succ.p;
+    A.reward = sp->reward.p;
+    A.action = sp->action.p;
+    A.table0 = tables.p;
+    A.table1 = tables.p + dense_max;
+    A.rank_of = rank_of.p;
+    A.bsum = bsum.p;
+    A.info = info.p;
+    A.status = status.p;
+    A.state_cap = state_cap;
+    A.dense_max = static_cast<uint32_t>(dense_max);
+    A.max_rounds = max_rounds;
+    A.H = H;
+    void* args[] = {&A};
+    const double t_launch = trace_enabled() ? host_ms() : 0.0;
+    VCS_CUDA(cudaLaunchCooperativeKernel(fn, G, kDenseThreads, args, 0, s));
+    VCS_LAUNCHED();
+    std::vector<uint64_t> hinfo(2 * static_cast<size_t>(H) + 2);
+    int32_t hstatus = 0;
+    VCS_CUDA(cudaMemcpyAsync(hinfo.data(), info.p, hinfo.size() * sizeof(uint64_t),
+                             cudaMemcpyDeviceToHost, s));
+    VCS_CUDA(cudaMemcpyAsync(&hstatus, status.p, sizeof hstatus, cudaMemcpyDeviceToHost, s));
+    VCS_CUDA(cudaStreamSynchronize(s));
+    if (trace_enabled())
+        std::fprintf(stderr, "[vcs build] persistent dense builder: %d blocks, setup %.3f ms, "
+                             "kernel %.3f ms\n", G, t_launch - t_setup, host_ms() - t_launch);
+    if (hstatus == 1)
+        raise(VCS_ECAP, "reachable state space exceeds cap of " + std::to_string(state_cap) +
+                            " states");
+    if (hstatus == 2) raise(VCS_EINVAL, "more than 2^32-1 states are not supported");
+    sp->layer_off.assign(static_cast<size_t>(H) + 2, 0);
+    sp->layer_edges.assign(static_cast<size_t>(H) + 1, 0);
+    sp->key_off.assign(static_cast<size_t>(H) + 2, 0);
+    sp->max_layer = 0;
+    uint64_t S = 0, E = 0;
+    for (int t = 0; t <= H; ++t) {
+        const uint64_t n = hinfo[static_cast<size_t>(t)];
+        sp->layer_off[static_cast<size_t>(t)] = S;
+        sp->key_off[static_cast<size_t>(t) + 1] =
+            sp->key_off[static_cast<size_t>(t)] + n * static_cast<uint64_t>(pl.words[static_cast<size_t>(t)]);
+        S += n;
+        sp->max_layer = std::max(sp->max_layer, n);
+        if (t < H) {
+            sp->layer_edges[static_cast<size_t>(t)] = hinfo[static_cast<size_t>(H) + 1 + t];
+            E += sp->layer_edges[static_cast<size_t>(t)];
+        }
+    }
+    sp->layer_off[static_cast<size_t>(H) + 1] = S;
+    sp->S = S;
+    sp->E = E;
+    return true;
 }
 
 // Per layer: count -> scan -> emit -> insert -> mark -> scan -> finalize -> counters, with the
@@ -919,7 +1370,9 @@ int vcs_space_build(const vcs_instance* inst, uint64_t state_cap, int device, vc
         sp->max_degree = maxdeg;
         const auto t0 = std::chrono::steady_clock::now();
         vcs::dispatch_words(vcs::max_words(sp.get()), [&](auto wm) {
-            vcs::build_layers<decltype(wm)::value>(sp.get(), state_cap);
+            constexpr int WM = decltype(wm)::value;
+            if (!vcs::build_dense<WM>(sp.get(), state_cap))
+                vcs::build_layers<WM>(sp.get(), state_cap);
         });
         const auto t1 = std::chrono::steady_clock::now();
         sp->build_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();

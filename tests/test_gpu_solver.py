@@ -445,3 +445,27 @@ def test_certified_full_size(gpu, golden):
         assert r.values.sweeps() == g["sweeps"] == sp.task_count() + 1
         assert sha(r.values.raw_values()) == g["values_sha"]
         assert sha(r.policy.raw_actions()) == g["actions_sha"]
+
+
+def test_builder_paths_agree(gpu, oracle, monkeypatch):
+    """The persistent one-kernel builder (dense key spaces) and the layered multi-kernel builder
+    produce identical CSR; a wide-capacity instance (key space far beyond the dense limit) takes
+    the hash path and still matches the oracle bit for bit."""
+    from cases import cloud
+    ni = V.generate_instance(N.VCS_GEN_HOMOG, 2012, 0, 5, 8, 40, 3, as_objects=False)
+    a = V.StateSpace.build_native(ni, 10**9)
+    monkeypatch.setenv("VCS_BUILD_LAYERED", "1")
+    b = V.StateSpace.build_native(ni, 10**9)
+    monkeypatch.delenv("VCS_BUILD_LAYERED")
+    assert np.array_equal(a.layer_offsets(), b.layer_offsets())
+    for x, y in zip(a.csr(), b.csr()):
+        assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
+    # 8 clouds x 300 VMs: 301^8 keys -> hash path
+    vcc = V.VccModel([cloud(i + 1, 300, 100.0 + i, 5.0 + i) for i in range(8)], 1.0, 1.2, 0.5)
+    tasks = [V.Task(j + 1, 1 + (j * 7) % 3, 60.0, 90.0) for j in range(7)]
+    wide = V.NativeInstance(vcc, bots=[V.BagOfTasks(1, tasks)])
+    sp = V.StateSpace.build_native(wide, 10**9)
+    _csr_equal(sp, oracle.build(wide.ref, 10**9))
+    # the state cap is enforced with the reference's message on the persistent path too
+    with pytest.raises(N.StateCapacityError, match="exceeds cap of 1000 states"):
+        V.StateSpace.build_native(ni, 1000)
