@@ -737,6 +737,67 @@ __global__ void __launch_bounds__(256, MINB) k_cert_layer(CertArgs a) {
         atomicMax(reinterpret_cast<unsigned long long*>(a.lb + a.m), s_lb);
 }
 
+// Thread-per-row form of the certified layer: each thread streams its own row's contiguous
+// edge range (through L1: a warp's 32 rows are one contiguous span) and keeps U gathers in
+// flight; no shared-memory staging.
+template <bool DISC, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_cert_rows(CertArgs a) {
+    constexpr unsigned FULL = 0xffffffffu;
+    __shared__ unsigned long long s_lb;
+    if (threadIdx.x == 0) s_lb = 0ull;
+    __syncthreads();
+    double dmax = 0.0;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < a.n;
+         r += stride) {
+        const uint32_t eb = __ldg(a.row_ptr + a.row0 + r);
+        const uint32_t ee = __ldg(a.row_ptr + a.row0 + r + 1);
+        double hi = -INFINITY, lo = -INFINITY;
+        uint32_t best_e = 0xffffffffu;
+        for (uint32_t e0 = eb; e0 < ee; e0 += U) {
+            uint32_t sidx[U];
+            double rw[U];
+            double2 x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (e0 + u < ee) {
+                    sidx[u] = __ldcs(a.succ + e0 + u) - static_cast<uint32_t>(a.next_row0);
+                    rw[u] = __ldcs(a.reward + e0 + u);
+                }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (e0 + u < ee) x[u] = __ldg(a.xd_next + sidx[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (e0 + u < ee) {
+                    const double qx = DISC ? __dadd_rn(rw[u], __dmul_rn(a.discount, x[u].x)) : __dadd_rn(rw[u], x[u].x);
+                    const double qy = DISC ? __dadd_rn(rw[u], __dmul_rn(a.discount, x[u].y)) : __dadd_rn(rw[u], x[u].y);
+                    if (qy > hi) { // strict: the first maximal edge wins (mdp.cpp:254-260)
+                        hi = qy;
+                        best_e = e0 + u;
+                    }
+                    if (qx > lo) lo = qx;
+                }
+        }
+        if (a.m == 1) lo = 0.0; // V_0
+        a.xd_cur[r] = make_double2(lo, hi);
+        a.values_out[a.row0 + r] = hi;
+        a.act_out[a.row0 + r] = best_e != 0xffffffffu ? __ldg(a.action + best_e) : -1;
+        const double d = fabs(hi - lo);
+        dmax = dmax < d ? d : dmax;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double other = __shfl_xor_sync(FULL, dmax, o);
+        dmax = dmax < other ? other : dmax;
+    }
+    if ((threadIdx.x & 31) == 0 && dmax > 0.0)
+        atomicMax(&s_lb, static_cast<unsigned long long>(__double_as_longlong(dmax)));
+    __syncthreads();
+    if (threadIdx.x == 0 && s_lb)
+        atomicMax(reinterpret_cast<unsigned long long*>(a.lb + a.m), s_lb);
+}
+
 // K* = H+1 is proven iff lb_k >= eps for k = 1..H (and no sweep cap below H+1).  Sets the graph
 // conditional to run the wavefront fallback otherwise.
 __global__ void k_cert_check(const double* __restrict__ lb, int H, double eps, int max_sweeps,
@@ -994,6 +1055,9 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
     const int wpb = static_cast<int>(std::max<size_t>(
         1, std::min<size_t>(8, (96u << 10) / (static_cast<size_t>(32) * qcap * sizeof(double2)))));
     const size_t smem = static_cast<size_t>(wpb) * 32 * qcap * sizeof(double2);
+    // variants (VCS_CERT_VARIANT): 0-3 warp-cooperative k_cert_layer, 4-8 thread-per-row
+    // k_cert_rows; default 4 = rows, 4 edges in flight, 4 blocks/SM (C4: 0.77 ms per solve vs
+    // 0.83 for the best warp-cooperative form; more resident warps thrash L1)
     using CertFn = void (*)(CertArgs);
     static const CertFn fns[2][4] = {
         {k_cert_layer<false, 8, 2>, k_cert_layer<false, 4, 4>, k_cert_layer<false, 8, 3>,
@@ -1002,13 +1066,20 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
          k_cert_layer<true, 4, 6>}};
     static const int variant = [] {
         const char* e = std::getenv("VCS_CERT_VARIANT");
-        return e ? std::min(3, std::max(0, std::atoi(e))) : 1;
+        return e ? std::min(8, std::max(0, std::atoi(e))) : 4;
     }();
-    const CertFn layer_fn = fns[disc ? 1 : 0][variant];
+    const CertFn row_fns[2][5] = {
+        {k_cert_rows<false, 4, 4>, k_cert_rows<false, 3, 4>, k_cert_rows<false, 3, 5>,
+         k_cert_rows<false, 4, 5>, k_cert_rows<false, 2, 6>},
+        {k_cert_rows<true, 4, 4>, k_cert_rows<true, 3, 4>, k_cert_rows<true, 3, 5>,
+         k_cert_rows<true, 4, 5>, k_cert_rows<true, 2, 6>}};
+    const bool rows = variant >= 4;
+    const CertFn layer_fn = rows ? row_fns[disc ? 1 : 0][variant - 4] : fns[disc ? 1 : 0][variant];
     const void* fn = reinterpret_cast<const void*>(layer_fn);
-    raise_smem_limit(fn, sp->device, smem);
+    if (!rows) raise_smem_limit(fn, sp->device, smem);
     int per_sm = 0;
-    VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, wpb * 32, smem));
+    VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, rows ? 256 : wpb * 32,
+                                                           rows ? 0 : smem));
     CertArgs a{};
     a.row_ptr = sp->row_ptr.p;
     a.succ = sp->succ.p;
@@ -1029,10 +1100,11 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
         a.xd_cur = sp->cert_xd.p + a.row0;
         if (a.n) {
             const uint64_t warps = (a.n + 31) / 32;
+            const int threads = rows ? 256 : wpb * 32;
             const uint64_t blocks = std::max<uint64_t>(
-                1, std::min<uint64_t>((warps + wpb - 1) / wpb,
+                1, std::min<uint64_t>((warps * 32 + threads - 1) / threads,
                                       static_cast<uint64_t>(std::max(1, per_sm)) * sp->num_sms));
-            layer_fn<<<static_cast<unsigned>(blocks), wpb * 32, smem, s>>>(a);
+            layer_fn<<<static_cast<unsigned>(blocks), threads, rows ? 0 : smem, s>>>(a);
             VCS_LAUNCHED();
             ++launches;
         }
