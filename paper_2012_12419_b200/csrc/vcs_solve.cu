@@ -748,10 +748,19 @@ __global__ void __launch_bounds__(256, MINB) k_cert_rows(CertArgs a) {
     __syncthreads();
     double dmax = 0.0;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < a.n;
-         r += stride) {
-        const uint32_t eb = __ldg(a.row_ptr + a.row0 + r);
-        const uint32_t ee = __ldg(a.row_ptr + a.row0 + r + 1);
+    uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    // the next row's bounds are loaded while the current row computes (one round trip less)
+    uint32_t nb = 0, ne = 0;
+    if (r < a.n) {
+        nb = __ldg(a.row_ptr + a.row0 + r);
+        ne = __ldg(a.row_ptr + a.row0 + r + 1);
+    }
+    for (; r < a.n; r += stride) {
+        const uint32_t eb = nb, ee = ne;
+        if (r + stride < a.n) {
+            nb = __ldg(a.row_ptr + a.row0 + r + stride);
+            ne = __ldg(a.row_ptr + a.row0 + r + stride + 1);
+        }
         double hi = -INFINITY, lo = -INFINITY;
         uint32_t best_e = 0xffffffffu;
         for (uint32_t e0 = eb; e0 < ee; e0 += U) {
