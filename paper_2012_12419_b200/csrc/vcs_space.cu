@@ -493,6 +493,9 @@ struct DenseBuild {
     uint32_t* table1;
     uint32_t* rank_of;   // successor index -> its layer-local state index
     uint32_t* bsum;      // per (round, block)
+    uint64_t* desc;      // per state of the current layer: Slots::pack()
+    uint32_t* jfirst;    // per state of the current layer: its first edge (layer-local)
+    uint64_t* stamps;    // VCS_TRACE: globaltimer at each phase boundary, 6 per layer (or null)
     uint64_t* info;      // n_t for t = 0..H at [t], E_t for t = 0..H-1 at [H+1+t]
     int32_t* status;     // 0 ok, 1 state cap exceeded, 2 more than 2^32-1 states
     uint64_t state_cap;
@@ -504,38 +507,40 @@ struct DenseBuild {
 constexpr int kDenseThreads = 256;
 constexpr int kDenseSlots = 8; // edge slots of a state: clouds 0..6 by key position, 7 = paid
 
-// A state's edges in static slots (registers only): slot p < 7 is the edge choosing the cloud at
-// key position p (valid if eligible with enough free VMs), slot 7 the paid edge (always valid).
-// off[e] = the edge's index within the state's row (the reference's order: clouds ascending,
-// paid last); idx[e] = the successor's mixed-radix index.
-template <int WM>
-struct StateEdges {
-    uint32_t idx[kDenseSlots];
-    uint32_t off[kDenseSlots];
-    bool valid[kDenseSlots];
-    uint32_t deg;
-    __device__ __forceinline__ StateEdges(const uint64_t (&k)[WM], const LayerParam& L) {
-        uint32_t f[kDenseSlots - 1];
-        uint32_t basei = 0;
+// A state's edges as 8 static slots: slot p < 7 is the edge choosing the cloud at key position p
+// (valid if eligible with enough free VMs), slot 7 the paid edge (always valid).  The state is
+// described by two words — the paid successor's mixed-radix index and the valid-cloud mask —
+// from which every slot's row offset (the reference's order: clouds ascending, paid last) and
+// successor index follow with a few integer operations (slot indices are compile-time).
+struct Slots {
+    uint32_t base; // successor index of the paid edge (nothing subtracted)
+    uint32_t mask; // bit p: the cloud at key position p is a valid action
+    __device__ __forceinline__ Slots(uint64_t desc)
+        : base(static_cast<uint32_t>(desc)), mask(static_cast<uint32_t>(desc >> 32)) {}
+    template <int WM>
+    __device__ __forceinline__ Slots(const uint64_t (&k)[WM], const LayerParam& L) : base(0), mask(0) {
 #pragma unroll
         for (int p = 0; p < kDenseSlots - 1; ++p) {
-            f[p] = p < L.n_active ? static_cast<uint32_t>(get_field<WM>(k, L.bit_off[p], L.width[p])) : 0u;
-            if (p < L.n_active && L.keep_idx[p] >= 0) basei += f[p] * L.wnext[p];
+            if (p >= L.n_active) continue;
+            const uint32_t f = static_cast<uint32_t>(get_field<WM>(k, L.bit_off[p], L.width[p]));
+            if (L.keep_idx[p] >= 0) base += f * L.wnext[p];
+            if (L.attr[p] && f >= static_cast<uint32_t>(L.demand)) mask |= 1u << p;
         }
-        uint32_t o = 0;
-#pragma unroll
-        for (int p = 0; p < kDenseSlots - 1; ++p) {
-            valid[p] = p < L.n_active && L.attr[p] && f[p] >= static_cast<uint32_t>(L.demand);
-            off[p] = o;
-            idx[p] = (p < L.n_active && L.keep_idx[p] >= 0)
-                         ? basei - static_cast<uint32_t>(L.demand) * L.wnext[p]
-                         : basei;
-            o += valid[p] ? 1u : 0u;
-        }
-        valid[kDenseSlots - 1] = true;
-        off[kDenseSlots - 1] = o;
-        idx[kDenseSlots - 1] = basei;
-        deg = o + 1;
+    }
+    __device__ __forceinline__ uint64_t pack() const {
+        return static_cast<uint64_t>(base) | (static_cast<uint64_t>(mask) << 32);
+    }
+    __device__ __forceinline__ bool valid(int e) const {
+        return e == kDenseSlots - 1 || ((mask >> e) & 1u);
+    }
+    __device__ __forceinline__ uint32_t off(int e) const {
+        return static_cast<uint32_t>(__popc(mask & ((1u << e) - 1u)));
+    }
+    __device__ __forceinline__ uint32_t deg() const { return static_cast<uint32_t>(__popc(mask)) + 1u; }
+    __device__ __forceinline__ uint32_t idx(int e, const LayerParam& L) const {
+        return (e < kDenseSlots - 1 && e < L.n_active && L.keep_idx[e] >= 0)
+                   ? base - static_cast<uint32_t>(L.demand) * L.wnext[e]
+                   : base;
     }
 };
 
@@ -565,35 +570,51 @@ __device__ __forceinline__ void next_key(const uint64_t (&k)[WM], int p, const L
 }
 
 // Prefixes of (round r, block b) for every round r over the per-(round, block) sums in
-// round-major order (one blocked scan of the R x G values, a few thousand), into s_before[r];
-// returns the grand total.
+// round-major order, into s_before[r]; returns the grand total.  Warp r sums round r (coalesced,
+// all loads in flight), then one thread combines the <= 8 rounds.
 __device__ __forceinline__ uint32_t round_prefixes(const uint32_t* __restrict__ bsum, int R, int G,
                                                    int b, uint32_t* s_before) {
-    using Scan = cub::BlockScan<uint32_t, kDenseThreads>;
-    __shared__ typename Scan::TempStorage scan;
-    const int N = R * G;
-    const int per = (N + kDenseThreads - 1) / kDenseThreads;
-    const int i0 = threadIdx.x * per, i1 = min(N, i0 + per);
-    uint32_t loc = 0;
-    for (int i = i0; i < i1; ++i) loc += __ldcg(bsum + i);
-    uint32_t off, total;
-    Scan(scan).ExclusiveSum(loc, off, total);
-    for (int r = 0; r < R; ++r) {
-        const int pos = r * G + b;
-        if (pos >= i0 && pos < i1) {
-            uint32_t v = off;
-            for (int i = i0; i < pos; ++i) v += __ldcg(bsum + i);
-            s_before[r] = v;
+    __shared__ uint32_t s_part[8], s_tot[8], s_total;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (w < R) {
+        uint32_t part = 0, tot = 0;
+        for (int i = lane; i < G; i += 32) {
+            const uint32_t v = __ldcg(bsum + w * G + i);
+            tot += v;
+            if (i < b) part += v;
+        }
+        part = __reduce_add_sync(0xffffffffu, part);
+        tot = __reduce_add_sync(0xffffffffu, tot);
+        if (lane == 0) {
+            s_part[w] = part;
+            s_tot[w] = tot;
         }
     }
     __syncthreads();
-    return total;
+    if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (int r = 0; r < R; ++r) {
+            s_before[r] = acc + s_part[r];
+            acc += s_tot[r];
+        }
+        s_total = acc;
+    }
+    __syncthreads();
+    return s_total;
 }
 
 // Per-round block sums without a block barrier per round: warp sums, shared atomics.
 __device__ __forceinline__ void round_add(uint32_t* s_round, int r, uint32_t v) {
     const uint32_t w = __reduce_add_sync(0xffffffffu, v);
     if ((threadIdx.x & 31) == 0 && w) atomicAdd(s_round + r, w);
+}
+
+__device__ __forceinline__ void stamp(uint64_t* stamps, int slot) {
+    if (stamps && blockIdx.x == 0 && threadIdx.x == 0) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        stamps[slot] = t;
+    }
 }
 
 template <int WM, int MINB>
@@ -603,6 +624,9 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
     __shared__ LayerParam sL;
     __shared__ uint32_t s_round[8];  // per-round block sums
     __shared__ uint32_t s_before[8]; // per-round prefixes of this block
+    // a round's edges of this block are one contiguous range: staged here, written coalesced
+    __shared__ double s_rew[kDenseThreads * kDenseSlots];
+    __shared__ int32_t s_act[kDenseThreads * kDenseSlots];
     cg::grid_group grid = cg::this_grid();
     const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
     const uint32_t T = static_cast<uint32_t>(G) * blockDim.x; // states per round
@@ -616,6 +640,7 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
         __syncthreads();
         if (tid < R) A.bsum[tid * G + b] = s_round[tid];
     };
+    constexpr int SL = kDenseSlots;
     for (int t = 0; t < A.H; ++t) {
         __syncthreads();
         for (int i = tid; i < static_cast<int>(sizeof(LayerParam) / 4); i += blockDim.x)
@@ -631,79 +656,84 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
         auto key_of = [&](uint32_t i, uint64_t (&k)[WM]) {
             load_key<WM>(A.keys + key_t + static_cast<uint64_t>(i) * L.words, L.words, k);
         };
-        // phase 1: degrees per (round, block)
+        stamp(A.stamps, 6 * t + 0);
+        // phase 1: degrees per (round, block); each state's slot descriptor
         for (int r = 0; r < R; ++r) {
             const uint32_t i = static_cast<uint32_t>(r) * T + q;
             uint32_t d = 0;
             if (i < n_t) {
                 uint64_t k[WM];
                 key_of(i, k);
-                d = StateEdges<WM>(k, L).deg;
+                const Slots sl(k, L);
+                d = sl.deg();
+                A.desc[i] = sl.pack();
             }
             round_add(s_round, r, d);
         }
         publish_rounds(R);
         grid.sync();
+        stamp(A.stamps, 6 * t + 1);
         // phase 2: row offsets, rewards, actions, first-edge atomicMin
         const uint32_t E_t = round_prefixes(A.bsum, R, G, b, s_before);
-        uint32_t jfirst[8]; // my state's first edge (layer-local) per round
         for (int r = 0; r < R; ++r) {
             const uint32_t i = static_cast<uint32_t>(r) * T + q;
-            uint64_t k[WM] = {};
-            if (i < n_t) key_of(i, k);
-            const StateEdges<WM> se(k, L);
-            const uint32_t deg = i < n_t ? se.deg : 0u;
-            uint32_t excl;
-            Scan(scan_tmp).ExclusiveSum(deg, excl);
+            const Slots sl(i < n_t ? __ldcg(A.desc + i) : 0ull);
+            const uint32_t deg = i < n_t ? sl.deg() : 0u;
+            uint32_t excl, cnt;
+            Scan(scan_tmp).ExclusiveSum(deg, excl, cnt);
             __syncthreads();
-            const uint32_t j = s_before[r] + excl;
-#pragma unroll
-            for (int rr = 0; rr < 8; ++rr)
-                if (rr == r) jfirst[rr] = j;
+            const uint32_t j0 = s_before[r]; // the block's first edge in this round
             if (i < n_t) {
+                const uint32_t j = j0 + excl;
+                A.jfirst[i] = j;
                 A.row_ptr[S_t + i] = static_cast<uint32_t>(E + j);
-                uint32_t cur[kDenseSlots];
+                uint32_t cur[SL];
 #pragma unroll
-                for (int e = 0; e < kDenseSlots; ++e)
-                    if (se.valid[e]) cur[e] = table[se.idx[e]]; // the state's checks in flight
+                for (int e = 0; e < SL; ++e)
+                    if (sl.valid(e)) cur[e] = table[sl.idx(e, L)]; // the state's checks in flight
+                uint64_t k[WM];
+                if (retires) key_of(i, k);
 #pragma unroll
-                for (int e = 0; e < kDenseSlots; ++e) {
-                    if (!se.valid[e]) continue;
-                    const int pe = e == kDenseSlots - 1 ? -1 : e;
-                    const uint32_t je = j + se.off[e];
-                    A.reward[E + je] = retires ? retiring_reward<WM>(k, pe, L)
-                                               : (pe < 0 ? L.r_paid_kept : L.r_cloud_kept);
-                    A.action[E + je] = pe < 0 ? -1 : L.cloud[pe];
-                    if (cur[e] > je) atomicMin(&table[se.idx[e]], je); // first edge wins
+                for (int e = 0; e < SL; ++e) {
+                    if (!sl.valid(e)) continue;
+                    const int pe = e == SL - 1 ? -1 : e;
+                    const uint32_t o = excl + (e == SL - 1 ? sl.deg() - 1u : sl.off(e));
+                    s_rew[o] = retires ? retiring_reward<WM>(k, pe, L)
+                                       : (pe < 0 ? L.r_paid_kept : L.r_cloud_kept);
+                    s_act[o] = pe < 0 ? -1 : L.cloud[pe];
+                    if (cur[e] > j0 + o) atomicMin(&table[sl.idx(e, L)], j0 + o); // first edge wins
                 }
+            }
+            __syncthreads();
+            for (uint32_t o = tid; o < cnt; o += blockDim.x) {
+                A.reward[E + j0 + o] = s_rew[o];
+                A.action[E + j0 + o] = s_act[o];
             }
         }
         if (tid < 8) s_round[tid] = 0;
         grid.sync();
+        stamp(A.stamps, 6 * t + 2);
         // phase 3: first-occurrence flags per (round, block)
         for (int r = 0; r < R; ++r) {
             const uint32_t i = static_cast<uint32_t>(r) * T + q;
             uint32_t f = 0;
             if (i < n_t) {
-                uint64_t k[WM];
-                key_of(i, k);
-                const StateEdges<WM> se(k, L);
-                uint32_t j = 0;
+                const Slots sl(__ldcg(A.desc + i));
+                const uint32_t j = __ldcg(A.jfirst + i);
+                uint32_t cur[SL];
 #pragma unroll
-                for (int rr = 0; rr < 8; ++rr)
-                    if (rr == r) j = jfirst[rr];
-                uint32_t cur[kDenseSlots];
+                for (int e = 0; e < SL; ++e)
+                    if (sl.valid(e)) cur[e] = __ldcg(table + sl.idx(e, L));
 #pragma unroll
-                for (int e = 0; e < kDenseSlots; ++e)
-                    if (se.valid[e]) cur[e] = __ldcg(table + se.idx[e]);
-#pragma unroll
-                for (int e = 0; e < kDenseSlots; ++e)
-                    if (se.valid[e]) f += cur[e] == j + se.off[e] ? 1u : 0u;
+                for (int e = 0; e < SL; ++e)
+                    if (sl.valid(e))
+                        f += cur[e] == j + (e == SL - 1 ? sl.deg() - 1u : sl.off(e)) ? 1u : 0u;
             }
             round_add(s_round, r, f);
         }
         publish_rounds(R);
         grid.sync();
+        stamp(A.stamps, 6 * t + 3);
         // phase 4: ranks of first edges = successor indices; next frontier keys; cap check
         const uint32_t n_next = round_prefixes(A.bsum, R, G, b, s_before);
         if (S_next + n_next > A.state_cap || S_next + n_next >= 0xffffffffull) {
@@ -715,34 +745,32 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
         }
         for (int r = 0; r < R; ++r) {
             const uint32_t i = static_cast<uint32_t>(r) * T + q;
-            uint64_t k[WM] = {};
-            uint32_t f = 0;
-            uint32_t cur[kDenseSlots];
-            uint32_t j = 0;
-#pragma unroll
-            for (int rr = 0; rr < 8; ++rr)
-                if (rr == r) j = jfirst[rr];
-            if (i < n_t) key_of(i, k);
-            const StateEdges<WM> se(k, L);
+            const Slots sl(i < n_t ? __ldcg(A.desc + i) : 0ull);
+            const uint32_t j = i < n_t ? __ldcg(A.jfirst + i) : 0u;
+            uint32_t first = 0; // bit e: slot e is its successor's first edge
             if (i < n_t) {
+                uint32_t cur[SL];
 #pragma unroll
-                for (int e = 0; e < kDenseSlots; ++e)
-                    if (se.valid[e]) cur[e] = __ldcg(table + se.idx[e]);
+                for (int e = 0; e < SL; ++e)
+                    if (sl.valid(e)) cur[e] = __ldcg(table + sl.idx(e, L));
 #pragma unroll
-                for (int e = 0; e < kDenseSlots; ++e)
-                    if (se.valid[e]) f += cur[e] == j + se.off[e] ? 1u : 0u;
+                for (int e = 0; e < SL; ++e)
+                    if (sl.valid(e) && cur[e] == j + (e == SL - 1 ? sl.deg() - 1u : sl.off(e)))
+                        first |= 1u << e;
             }
             uint32_t rank;
-            Scan(scan_tmp).ExclusiveSum(f, rank);
+            Scan(scan_tmp).ExclusiveSum(static_cast<uint32_t>(__popc(first)), rank);
             __syncthreads();
             rank += s_before[r];
-            if (f) {
+            if (first) {
+                uint64_t k[WM];
+                key_of(i, k); // the parent key: next keys are derived from it
 #pragma unroll
-                for (int e = 0; e < kDenseSlots; ++e) {
-                    if (!se.valid[e] || cur[e] != j + se.off[e]) continue;
-                    A.rank_of[se.idx[e]] = rank;
+                for (int e = 0; e < SL; ++e) {
+                    if (!((first >> e) & 1u)) continue;
+                    A.rank_of[sl.idx(e, L)] = rank;
                     uint64_t nk[WM];
-                    next_key<WM>(k, e == kDenseSlots - 1 ? -1 : e, L, nk);
+                    next_key<WM>(k, e == SL - 1 ? -1 : e, L, nk);
                     uint64_t* dst = A.keys + key_next + static_cast<uint64_t>(rank) * L.next_words;
 #pragma unroll
                     for (int w = 0; w < WM; ++w)
@@ -756,25 +784,41 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
             A.info[A.H + 1 + t] = E_t;
         }
         grid.sync();
+        stamp(A.stamps, 6 * t + 4);
         // phase 5: successor ids; clear this layer's table for layer t+2 (layer t+1 uses the
         // other one; rank_of is rewritten by the next layer's phase 4, two grid syncs later)
+        uint32_t* s_succ = reinterpret_cast<uint32_t*>(s_act); // (phase 2 is done with it)
+        __shared__ uint32_t s_j0, s_j1;
         for (int r = 0; r < R; ++r) {
             const uint32_t i = static_cast<uint32_t>(r) * T + q;
-            if (i >= n_t) continue;
-            uint64_t k[WM];
-            key_of(i, k);
-            const StateEdges<WM> se(k, L);
-            uint32_t j = 0;
+            const uint32_t blk0 = static_cast<uint32_t>(r) * T + static_cast<uint32_t>(b) * blockDim.x;
+            __syncthreads();
+            if (tid == 0) { // this block's edge range in round r: first and last valid state
+                const uint32_t last = min(n_t, blk0 + blockDim.x);
+                if (blk0 < n_t) {
+                    s_j0 = __ldcg(A.jfirst + blk0);
+                    s_j1 = __ldcg(A.jfirst + last - 1) + Slots(__ldcg(A.desc + last - 1)).deg();
+                } else {
+                    s_j0 = s_j1 = 0;
+                }
+            }
+            __syncthreads();
+            const uint32_t j0 = s_j0, cnt = s_j1 - s_j0;
+            if (i < n_t) {
+                const Slots sl(__ldcg(A.desc + i));
+                const uint32_t o0 = __ldcg(A.jfirst + i) - j0;
+                uint32_t rk[SL];
 #pragma unroll
-            for (int rr = 0; rr < 8; ++rr)
-                if (rr == r) j = jfirst[rr];
-            uint32_t rk[kDenseSlots];
+                for (int e = 0; e < SL; ++e)
+                    if (sl.valid(e)) rk[e] = __ldcg(A.rank_of + sl.idx(e, L));
 #pragma unroll
-            for (int e = 0; e < kDenseSlots; ++e)
-                if (se.valid[e]) rk[e] = __ldcg(A.rank_of + se.idx[e]);
-#pragma unroll
-            for (int e = 0; e < kDenseSlots; ++e)
-                if (se.valid[e]) A.succ[E + j + se.off[e]] = static_cast<uint32_t>(S_next) + rk[e];
+                for (int e = 0; e < SL; ++e)
+                    if (sl.valid(e))
+                        s_succ[o0 + (e == SL - 1 ? sl.deg() - 1u : sl.off(e))] =
+                            static_cast<uint32_t>(S_next) + rk[e];
+            }
+            __syncthreads();
+            for (uint32_t o = tid; o < cnt; o += blockDim.x) A.succ[E + j0 + o] = s_succ[o];
         }
         for (uint32_t i = q; i < A.dense_max; i += T) table[i] = kEmpty32;
         S_t = S_next;
@@ -816,7 +860,7 @@ bool build_dense(vcs_space* sp, uint64_t state_cap) {
     int coop = 0;
     VCS_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, sp->device));
     if (!coop) return false;
-    // (2 blocks per SM at ~125 registers: forcing 3 or 4 spills and measured slower)
+    // (2 blocks per SM; forcing 3 or 4 by register caps measured slower)
     const void* fn = reinterpret_cast<const void*>(k_build_dense<WM, 2>);
     int per_sm = 0;
     VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kDenseThreads, 0));
@@ -846,12 +890,17 @@ bool build_dense(vcs_space* sp, uint64_t state_cap) {
     sp->reward.reserve(e_bound, 0, s);
     sp->action.reserve(e_bound, 0, s);
     DevBuf<uint32_t> tables, rank_of, bsum;
+    DevBuf<uint64_t> desc;
+    DevBuf<uint32_t> jfirst;
+    DevBuf<uint64_t> stamps;
     DevBuf<uint64_t> info;
     DevBuf<int32_t> status;
     DevBuf<LayerParam> params;
     tables.exact(2 * dense_max, s);
     rank_of.exact(dense_max, s);
     bsum.exact(static_cast<size_t>(G) * max_rounds, s);
+    desc.exact(n_max, s);
+    jfirst.exact(n_max, s);
     info.exact(2 * static_cast<size_t>(H) + 2, s);
     status.exact(1, s);
     params.exact(static_cast<size_t>(H), s);
@@ -873,6 +922,12 @@ bool build_dense(vcs_space* sp, uint64_t state_cap) {
     A.table1 = tables.p + dense_max;
     A.rank_of = rank_of.p;
     A.bsum = bsum.p;
+    A.desc = desc.p;
+    A.jfirst = jfirst.p;
+    if (trace_enabled()) {
+        stamps.exact(6 * static_cast<size_t>(H) + 6, s);
+        A.stamps = stamps.p;
+    }
     A.info = info.p;
     A.status = status.p;
     A.state_cap = state_cap;
@@ -892,6 +947,20 @@ bool build_dense(vcs_space* sp, uint64_t state_cap) {
     if (trace_enabled())
         std::fprintf(stderr, "[vcs build] persistent dense builder: %d blocks, setup %.3f ms, "
                              "kernel %.3f ms\n", G, t_launch - t_setup, host_ms() - t_launch);
+    if (trace_enabled() && stamps.p) {
+        std::vector<uint64_t> st(6 * static_cast<size_t>(H));
+        VCS_CUDA(cudaMemcpy(st.data(), stamps.p, st.size() * 8, cudaMemcpyDeviceToHost));
+        double ph[5] = {};
+        for (int t = 0; t < H; ++t) {
+            const uint64_t end = t + 1 < H ? st[6 * (t + 1)] : st[6 * t + 4];
+            for (int k = 0; k < 5; ++k) {
+                const uint64_t a = st[6 * t + k], b = k < 4 ? st[6 * t + k + 1] : end;
+                if (b > a) ph[k] += (b - a) * 1e-6;
+            }
+        }
+        std::fprintf(stderr, "[vcs build] phase ms: degrees %.3f emit %.3f flags %.3f ranks %.3f "
+                             "succ+next-layer-start %.3f\n", ph[0], ph[1], ph[2], ph[3], ph[4]);
+    }
     if (hstatus == 1)
         raise(VCS_ECAP, "reachable state space exceeds cap of " + std::to_string(state_cap) +
                             " states");
