@@ -1460,11 +1460,17 @@ int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int
                 VCS_CUDA(cudaMemcpyAsync(actions_out + r0, sp->actions_dev.p + r0,
                                          (r1 - r0) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
         };
-        VCS_CUDA(cudaStreamWaitEvent(d, g.ev[0], 0)); // terminal layer: set at the solve's start
-        copy_rows(sp->layer_off[sp->H], sp->S, d);
+        // Rows are final layer by layer, from the back: copy them in chunks of >= 16 MB (fewer,
+        // larger DMA transfers), each after the event of its last (lowest) layer.  The terminal
+        // layer's rows go with the first chunk: its memsets precede layer H-1's kernel.
+        const uint64_t row_bytes = (values_out ? 8 : 0) + (actions_out ? 4 : 0);
+        uint64_t chunk_end = sp->S;
         for (int t = sp->H - 1; t >= 0; --t) {
+            const uint64_t r0 = sp->layer_off[t];
+            if ((chunk_end - r0) * row_bytes < (16ull << 20) && t > 0) continue;
             VCS_CUDA(cudaStreamWaitEvent(d, g.layer_ev[static_cast<size_t>(t)], 0));
-            copy_rows(sp->layer_off[t], sp->layer_off[t + 1], d);
+            copy_rows(r0, chunk_end, d);
+            chunk_end = r0;
         }
         vcs_solve_report local{};
         vcs_solve_report* rep = report ? report : &local;
