@@ -140,6 +140,19 @@ int vcs_space_csr(const vcs_space* sp, uint64_t* row_ptr, uint32_t* succ, double
  * std::out_of_range "state not reachable in enumerated space"). */
 int vcs_space_locate(vcs_space* sp, int64_t n, const int32_t* free_vms, const int32_t* task_index,
                      const uint8_t* terminal, int64_t* idx_out);
+/* Batched policy queries: ValueTable::value_of and Policy::action_for
+ * (mdp.cpp:227-282) for n full states at once, served from the device-resident results of the
+ * last collected solve on this space (vcs_solve, or vcs_solve_enqueue + vcs_solve_collect).
+ * Keys are packed, located and the hidden penalty applied on the device.  value_out[i] =
+ * V(locate(s)) - hidden_penalty(s), NaN when s is unreachable (the reference throws
+ * std::out_of_range); action_out[i] = the cloud index or VCS_PAID_CLOUD, VCS_NO_ACTION for
+ * unreachable or terminal states (action_for throws); idx_out[i] = the flat index or -1.  Every
+ * array may live in host or device memory (device arrays are used in place); any output may be
+ * NULL.  Returns after the outputs are complete when any of them is in host memory. */
+#define VCS_NO_ACTION (-2)
+int vcs_policy_query(vcs_space* sp, int64_t n, const int32_t* free_vms, const int32_t* task_index,
+                     const uint8_t* terminal, double* value_out, int32_t* action_out,
+                     int64_t* idx_out, void* stream);
 /* Replaces mdp.cpp:236-243 StateSpace::hidden_penalty for a batch of full states. */
 int vcs_space_hidden_penalty(const vcs_space* sp, int64_t n, const int32_t* free_vms,
                              const int32_t* task_index, const uint8_t* terminal, double* out);

@@ -15,6 +15,7 @@ import numpy as np
 
 VCS_OK, VCS_EINVAL, VCS_ECAP, VCS_EIO, VCS_ECUDA, VCS_ERANGE = 0, 2, 3, 4, 5, 6
 VCS_PAID_CLOUD = -1
+VCS_NO_ACTION = -2
 VCS_GEN_RANDOM, VCS_GEN_HOMOG, VCS_GEN_GREEDY = 0, 1, 2
 VCS_METHOD_AUTO, VCS_METHOD_JACOBI, VCS_METHOD_WAVEFRONT, VCS_METHOD_CERTIFIED = 0, 1, 2, 3
 
@@ -26,7 +27,7 @@ EXPORTS = (
     "vcs_instance_free", "vcs_instance_generate",
     "vcs_space_build", "vcs_space_from_csr", "vcs_space_info_get", "vcs_space_layer_offsets",
     "vcs_space_layer_edges", "vcs_space_csr", "vcs_space_locate", "vcs_space_hidden_penalty",
-    "vcs_space_free",
+    "vcs_policy_query", "vcs_space_free",
     "vcs_solve", "vcs_solve_enqueue", "vcs_solve_collect", "vcs_shard_plan", "vcs_shard_begin", "vcs_shard_sweep", "vcs_shard_finish",
     "vcs_wave_shard_begin", "vcs_wave_shard_band", "vcs_wave_shard_layer", "vcs_wave_shard_pack",
     "vcs_wave_shard_unpack", "vcs_wave_shard_finish",
@@ -154,6 +155,7 @@ _SIGS = {
     "vcs_space_csr": (C.c_int, [_P, _U64P, _U32P, _F64P, _I32P]),
     "vcs_space_locate": (C.c_int, [_P, C.c_int64, _I32P, _I32P, _U8P, _I64P]),
     "vcs_space_hidden_penalty": (C.c_int, [_P, C.c_int64, _I32P, _I32P, _U8P, _F64P]),
+    "vcs_policy_query": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, _P, _P]),
     "vcs_space_free": (None, [_P]),
     "vcs_solve": (C.c_int, [_P, C.POINTER(vcs_solve_opts), _F64P, _I32P,
                             C.POINTER(vcs_solve_report)]),

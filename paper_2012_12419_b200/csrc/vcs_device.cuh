@@ -186,6 +186,10 @@ struct vcs_space {
 
     // lazily built device index for locate (hash over (layer, key) -> state)
     vcs::DevBuf<uint32_t> loc_table;
+    // results of the last collected solve (device-resident): vcs_policy_query reads them
+    const double* result_values = nullptr;
+    const int32_t* result_actions = nullptr;
+    vcs::DevBuf<unsigned char> query_meta; // per layer: key layout for device-side packing
     uint64_t loc_cap = 0;
 
     int num_sms = 148;

@@ -1506,6 +1506,8 @@ int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
             raise(VCS_EINVAL, "VCS_PROFILE_NO_FALLBACK: the proof failed, results are invalid");
         // Jacobi leaves V_{K*} in ping-pong buffer K*&1; the wavefront extraction writes it to v[0]
         const double* vsrc = wave ? sp->v[0].p : sp->v[K & 1].p;
+        sp->result_values = vsrc;
+        sp->result_actions = sp->actions_dev.p;
         if (values_out)
             VCS_CUDA(cudaMemcpyAsync(values_out, vsrc, sp->S * sizeof(double),
                                      cudaMemcpyDeviceToHost, s));

@@ -20,6 +20,7 @@
 #include "vcs_device.cuh"
 
 #include <cooperative_groups.h>
+#include <math_constants.h>
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
@@ -30,6 +31,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 namespace vcs {
 
@@ -403,6 +405,88 @@ __global__ void k_loc_lookup(int64_t n, const LocQuery* __restrict__ q,
         }
         h = (h + 1) & mask;
     }
+}
+
+// ---- batched policy queries: value_of / action_for over many full states ----
+// Per layer t = 0..H: the packed-key layout (active clouds, bit offsets, widths), so keys are
+// packed on the device from the callers' free-VM vectors.
+struct QueryLayer {
+    int32_t n_active;
+    int32_t words;
+    uint8_t cloud[kMaxActive];
+    uint16_t bit_off[kMaxActive];
+    uint8_t width[kMaxActive];
+};
+
+struct QueryArgs {
+    const QueryLayer* layers; // H+1
+    const int32_t* last_use;  // per cloud (hidden penalty, mdp.cpp:236-243)
+    const uint64_t* layer_off;
+    const uint64_t* key_off;
+    const uint64_t* keys;
+    const uint32_t* table;
+    uint32_t mask;
+    const double* values;     // V_{K*} of the last solve
+    const int32_t* actions;
+    const int32_t* free_vms;  // n x n_clouds
+    const int32_t* task_index;
+    const uint8_t* terminal;
+    double* value_out;
+    int32_t* action_out;
+    int64_t* idx_out;
+    int64_t n;
+    int32_t n_clouds;
+    int32_t H;
+    double gamma;
+};
+
+template <int WM>
+__global__ void k_policy_query(QueryArgs a) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= a.n) return;
+    const int32_t* fv = a.free_vms + i * a.n_clouds;
+    const bool term = a.terminal[i] != 0;
+    const int t = term ? a.H : a.task_index[i];
+    int64_t idx = -1;
+    double penalty = 0.0;
+    if (t >= 0 && t <= a.H) {
+        const QueryLayer& Q = a.layers[t];
+        uint64_t k[WM];
+#pragma unroll
+        for (int w = 0; w < WM; ++w) k[w] = 0ull;
+        bool ok = true;
+        for (int p = 0; p < Q.n_active; ++p) { // pack_key (vcs_host.cpp)
+            const int v = fv[Q.cloud[p]];
+            if (v < 0 || v > 0xffff || (Q.width[p] < 31 && v >= (1 << Q.width[p]))) ok = false;
+            put_field<WM>(k, Q.bit_off[p], static_cast<uint64_t>(v < 0 ? 0 : v));
+        }
+        if (ok) {
+            uint32_t h = static_cast<uint32_t>(hash_key<WM>(k, Q.words, static_cast<uint64_t>(t) + 1)) &
+                         a.mask;
+            const uint64_t lo = a.layer_off[t], hi = a.layer_off[t + 1];
+            for (;;) {
+                const uint32_t cur = a.table[h];
+                if (cur == kEmpty32) break;
+                if (cur >= lo && cur < hi &&
+                    key_equal<WM>(a.keys + a.key_off[t] + (cur - lo) * static_cast<uint64_t>(Q.words),
+                                  Q.words, k)) {
+                    idx = cur;
+                    break;
+                }
+                h = (h + 1) & a.mask;
+            }
+        }
+        if (a.H > 0) { // (the host's exact operations: no contraction into an FMA)
+            double retired = 0.0;
+            for (int c = 0; c < a.n_clouds; ++c)
+                if (a.last_use[c] < t) retired = __dadd_rn(retired, static_cast<double>(fv[c]));
+            penalty = __dmul_rn(a.gamma, retired);
+        }
+    }
+    if (a.idx_out) a.idx_out[i] = idx;
+    if (a.value_out) a.value_out[i] = idx >= 0 ? __dsub_rn(a.values[idx], penalty) : CUDART_NAN;
+    if (a.action_out)
+        a.action_out[i] = (idx >= 0 && !term && t < a.H) ? a.actions[idx] : VCS_NO_ACTION;
 }
 
 uint32_t blocks_for(uint64_t n, uint32_t threads) {
@@ -1388,6 +1472,7 @@ vcs_space::~vcs_space() {
     ver_off.release_idle();
     layer_off_dev.release_idle();
     loc_table.release_idle();
+    query_meta.release_idle();
     if (stream) {
         cudaStreamSynchronize(stream);
         cudaStreamDestroy(stream);
@@ -1602,6 +1687,115 @@ int vcs_space_hidden_penalty(const vcs_space* sp, int64_t n, const int32_t* free
                 if (sp->plan.last_use[c] < t) retired += free_vms[i * K + c];
             out[i] = sp->plan.layers.empty() ? 0.0 : sp->plan.layers[0].gamma * retired;
         }
+        return VCS_OK;
+    });
+}
+
+namespace {
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+} // namespace
+
+int vcs_policy_query(vcs_space* sp, int64_t n, const int32_t* free_vms, const int32_t* task_index,
+                     const uint8_t* terminal, double* value_out, int32_t* action_out,
+                     int64_t* idx_out, void* stream) {
+    return guarded([&] {
+        if (!sp->has_plan) raise(VCS_EINVAL, "space was not built from an instance");
+        if (!sp->result_values)
+            raise(VCS_EINVAL, "no solve results on this space (vcs_solve / vcs_solve_collect first)");
+        if (n <= 0) return VCS_OK;
+        if (!free_vms || !task_index || !terminal) raise(VCS_EINVAL, "null argument");
+        vcs::bind_device(sp->device);
+        const vcs::StreamUse s(sp, stream);
+        vcs::ensure_locate_index(sp);
+        const int K = sp->plan.n_clouds, H = sp->H;
+        const size_t ql = sizeof(vcs::QueryLayer) * (static_cast<size_t>(H) + 1);
+        const size_t lu = ((sizeof(int32_t) * std::max(K, 1) + 7) / 8) * 8;
+        const size_t lo = sizeof(uint64_t) * (static_cast<size_t>(H) + 2);
+        if (!sp->query_meta.p) { // key layouts, last_use, layer and key offsets: once per space
+            std::vector<unsigned char> blob(ql + lu + 2 * lo, 0);
+            auto* layers = reinterpret_cast<vcs::QueryLayer*>(blob.data());
+            for (int t = 0; t <= H; ++t) {
+                auto& Q = layers[t];
+                Q.n_active = static_cast<int32_t>(sp->plan.active[t].size());
+                Q.words = sp->plan.words[t];
+                for (int p = 0; p < Q.n_active; ++p) {
+                    const int c = sp->plan.active[t][p];
+                    Q.cloud[p] = static_cast<uint8_t>(c);
+                    Q.bit_off[p] = sp->plan.bit_off[t][p];
+                    Q.width[p] = static_cast<uint8_t>(sp->plan.width_of_cloud[c]);
+                }
+            }
+            std::memcpy(blob.data() + ql, sp->plan.last_use.data(), sizeof(int32_t) * K);
+            std::memcpy(blob.data() + ql + lu, sp->layer_off.data(), lo);
+            std::memcpy(blob.data() + ql + lu + lo, sp->key_off.data(), lo);
+            sp->query_meta.exact(blob.size(), sp->stream);
+            VCS_CUDA(cudaMemcpyAsync(sp->query_meta.p, blob.data(), blob.size(),
+                                     cudaMemcpyHostToDevice, sp->stream));
+            VCS_CUDA(cudaStreamSynchronize(sp->stream));
+        }
+        // host or device buffers: device ones are used in place, host ones staged
+        vcs::DevBuf<int32_t> dfv, dti, dact;
+        vcs::DevBuf<uint8_t> dte;
+        vcs::DevBuf<double> dval;
+        vcs::DevBuf<int64_t> didx;
+        auto stage_in = [&](const auto* src, auto& buf, size_t count) {
+            using T = std::remove_cv_t<std::remove_pointer_t<decltype(src)>>;
+            if (is_device_ptr(src)) return src;
+            buf.exact(count, s);
+            VCS_CUDA(cudaMemcpyAsync(buf.p, src, count * sizeof(T), cudaMemcpyHostToDevice, s));
+            return static_cast<const T*>(buf.p);
+        };
+        auto stage_out = [&](auto* dst, auto& buf, size_t count) {
+            if (!dst || is_device_ptr(dst)) return dst;
+            buf.exact(count, s);
+            return buf.p;
+        };
+        const size_t nn = static_cast<size_t>(n);
+        vcs::QueryArgs a{};
+        a.layers = reinterpret_cast<const vcs::QueryLayer*>(sp->query_meta.p);
+        a.last_use = reinterpret_cast<const int32_t*>(sp->query_meta.p + ql);
+        a.layer_off = reinterpret_cast<const uint64_t*>(sp->query_meta.p + ql + lu);
+        a.key_off = reinterpret_cast<const uint64_t*>(sp->query_meta.p + ql + lu + lo);
+        a.keys = sp->keys.p;
+        a.table = sp->loc_table.p;
+        a.mask = static_cast<uint32_t>(sp->loc_cap - 1);
+        a.values = sp->result_values;
+        a.actions = sp->result_actions;
+        a.free_vms = stage_in(free_vms, dfv, nn * static_cast<size_t>(K));
+        a.task_index = stage_in(task_index, dti, nn);
+        a.terminal = stage_in(terminal, dte, nn);
+        a.value_out = stage_out(value_out, dval, nn);
+        a.action_out = stage_out(action_out, dact, nn);
+        a.idx_out = stage_out(idx_out, didx, nn);
+        a.n = n;
+        a.n_clouds = K;
+        a.H = H;
+        a.gamma = sp->plan.layers.empty() ? 0.0 : sp->plan.layers[0].gamma;
+        vcs::dispatch_words(vcs::max_words(sp), [&](auto wm) {
+            constexpr int WM = decltype(wm)::value;
+            vcs::k_policy_query<WM><<<vcs::blocks_for(static_cast<uint64_t>(n), 256), 256, 0, s>>>(a);
+            VCS_LAUNCHED();
+        });
+        bool host_out = false;
+        auto copy_out = [&](auto* dst, auto* staged, size_t count) {
+            if (dst && staged != dst) {
+                VCS_CUDA(cudaMemcpyAsync(dst, staged, count * sizeof(*dst), cudaMemcpyDeviceToHost, s));
+                host_out = true;
+            }
+        };
+        copy_out(value_out, a.value_out, nn);
+        copy_out(action_out, a.action_out, nn);
+        copy_out(idx_out, a.idx_out, nn);
+        // staged buffers are freed in stream order; host outputs are complete on return
+        if (host_out || dfv.p || dti.p || dte.p) VCS_CUDA(cudaStreamSynchronize(s));
         return VCS_OK;
     });
 }

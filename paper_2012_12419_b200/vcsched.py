@@ -487,6 +487,18 @@ class StateSpace:
             raise OutOfRange("state not reachable in enumerated space")
         return idx
 
+    def policy_query(self, states: Sequence[MdpState]):
+        """vcs_policy_query: (values, actions, flat indices) for a batch of full states."""
+        fv, ti, te = self._state_arrays(states)
+        n = len(states)
+        vals = np.zeros(n, dtype=np.float64)
+        acts = np.zeros(n, dtype=np.int32)
+        idx = np.zeros(n, dtype=np.int64)
+        vp = lambda a: C.c_void_p(a.ctypes.data)  # noqa: E731
+        N.check(N.lib().vcs_policy_query(self._h, n, vp(fv), vp(ti), vp(te), vp(vals), vp(acts),
+                                         vp(idx), None))
+        return vals, acts, idx
+
     def hidden_penalty(self, s: MdpState) -> float:
         fv, ti, te = self._state_arrays([s])
         out = np.zeros(1, dtype=np.float64)
@@ -512,6 +524,11 @@ class ValueTable:
 
     def initial_value(self) -> float:
         return self.value_of(initial_state(self._space.instance()))
+
+    def value_of_many(self, states: Sequence[MdpState]) -> np.ndarray:
+        """Batched value_of on the device (vcs_policy_query): NaN where a state is unreachable
+        (value_of raises OutOfRange there).  Answers from the space's last collected solve."""
+        return self._space.policy_query(states)[0]
 
     def sweeps(self) -> int:
         return self._sweeps
@@ -540,6 +557,11 @@ class Policy:
         if s.terminal or s.next_task_index >= self._space.task_count():
             raise OutOfRange("terminal states carry no action")
         return MdpAction(int(self._actions[self._space.locate(s)]))
+
+    def action_for_many(self, states: Sequence[MdpState]) -> np.ndarray:
+        """Batched action_for on the device: cloud index, -1 = paid cloud, VCS_NO_ACTION (-2)
+        where action_for raises (terminal or unreachable)."""
+        return self._space.policy_query(states)[1]
 
     def raw_actions(self) -> np.ndarray:
         return self._actions

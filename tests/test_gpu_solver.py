@@ -469,3 +469,55 @@ def test_builder_paths_agree(gpu, oracle, monkeypatch):
     # the state cap is enforced with the reference's message on the persistent path too
     with pytest.raises(N.StateCapacityError, match="exceeds cap of 1000 states"):
         V.StateSpace.build_native(ni, 1000)
+
+
+def test_batched_policy_query(gpu):
+    """vcs_policy_query: value_of / action_for for many full states at once on the
+    device, bit-identical to the per-state path; unreachable -> NaN / VCS_NO_ACTION (the
+    reference raises), terminal -> VCS_NO_ACTION; host and device buffers both accepted."""
+    import torch
+    rng = np.random.default_rng(7)
+    for trial in range(4):
+        p = V.generate_instance(N.VCS_GEN_RANDOM, 61, trial, 3, 6, 10, 3)
+        inst = V.MdpInstance.from_workload(p.vcc, p.bots)
+        vi = V.value_iteration(inst)
+        states = []
+        for walk in range(6):
+            s = V.initial_state(inst)
+            while True:
+                states.append(s)
+                if s.terminal:
+                    break
+                acts = V.legal_actions(inst, s)
+                s = V.transition(s, acts[rng.integers(len(acts))], inst)
+        # unreachable: more free VMs than the cloud has
+        s0 = V.initial_state(inst)
+        bad = V.MdpState([v + 1 for v in s0.free_vms], s0.next_task_index, False)
+        states.append(bad)
+        vals = vi.values.value_of_many(states)
+        acts = vi.policy.action_for_many(states)
+        for s, v, a in zip(states, vals, acts):
+            try:
+                ref_v = vi.values.value_of(s)
+            except N.OutOfRange:
+                assert np.isnan(v) and a == N.VCS_NO_ACTION
+                continue
+            assert np.float64(v).view(np.uint64) == np.float64(ref_v).view(np.uint64)
+            if s.terminal or s.next_task_index >= vi.values.space().task_count():
+                assert a == N.VCS_NO_ACTION
+            else:
+                assert a == vi.policy.action_for(s).target
+        # device-resident inputs and outputs are used in place
+        space = vi.values.space()
+        fv, ti, te = space._state_arrays(states)
+        dev = torch.device("cuda", 0)
+        dfv, dti, dte = (torch.from_numpy(x).to(dev) for x in (fv, ti, te))
+        dval = torch.empty(len(states), dtype=torch.float64, device=dev)
+        dact = torch.empty(len(states), dtype=torch.int32, device=dev)
+        torch.cuda.synchronize()
+        ptr = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+        N.check(N.lib().vcs_policy_query(space.handle, len(states), ptr(dfv), ptr(dti), ptr(dte),
+                                         ptr(dval), ptr(dact), None, None))
+        torch.cuda.synchronize()
+        assert np.array_equal(dval.cpu().numpy().view(np.uint64), vals.view(np.uint64))
+        assert np.array_equal(dact.cpu().numpy(), acts)
