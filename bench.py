@@ -270,6 +270,33 @@ def e2e_sharded(args, ni, local, dev, stream, opts, sharding, S, rank):
                     "D2H of the rank's own rows", "steps": len(times)}
 
 
+def greedy_c2(V, N):
+    """BASELINE configs[1] beside the headline: greedy first-fit placement of 10^5 tasks over
+    10^3 clouds through the C ABI from host SoA arrays to host placements
+    (tests/test_gpu_greedy.py checks the placements bit-exact against the reference)."""
+    ni = V.generate_instance(N.VCS_GEN_GREEDY, 12345, 0, 1000, 100, 1000, 3, as_objects=False)
+    tgt = np.empty(100000, np.int32)
+    paid, unused = C.c_int64(), C.c_int64()
+    ts = []
+    for _ in range(7):
+        t0 = time.perf_counter()
+        N.check(N.lib().vcs_greedy(ni.ref, 0, N.ptr(tgt, C.c_int32), None, C.byref(paid),
+                                   C.byref(unused)))
+        ts.append((time.perf_counter() - t0) * 1e3)
+    e2e = statistics.median(ts[2:])
+    import hashlib
+    golden = json.loads((ROOT / "tests" / "golden" / "golden.json").read_text())["cases"]["C2"]
+    exact = hashlib.sha256(np.ascontiguousarray(tgt).tobytes()).hexdigest() == \
+        golden["greedy"]["targets_sha"]
+    return {"workload": "C2: 1000 clouds x 100 VMs, 10^5 tasks demand U[1,3] (seed 12345)",
+            "placements_equal_reference": exact,
+            "e2e_ms": e2e, "tasks_per_s": 1e5 / (e2e * 1e-3), "paid": paid.value,
+            "unused_vms": unused.value,
+            "reference_ms_container": 306.7,
+            "note": "reference_ms_container: the unmodified reference's greedy_schedule on the "
+                    "build container's cores (tests/golden/golden.json C2.ref_ms)"}
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -521,6 +548,8 @@ def run_b200(args):
         "clocks": sampler.summary(),
         "gpu_launches": int(launches),
     }
+    if rank == 0 and not args.no_greedy:
+        line["greedy"] = greedy_c2(V, N)
     if world == 1 and not args.no_cpu_baseline and rank == 0:
         try:
             line["cpu_baseline"] = cpu_baseline(space, args.eps)
@@ -548,6 +577,7 @@ def main():
                     help="single-GPU solver (auto = certified pass with the wavefront as fallback "
                          "when the version store fits in HBM, else Jacobi)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-greedy", action="store_true", help="skip the C2 greedy side number")
     ap.add_argument("--sharding", choices=["auto", "instances", "wave", "halo", "allgather"],
                     default="auto",
                     help="auto: single GPU at N=1, independent instances (one per GPU) at N>1; "
