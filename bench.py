@@ -502,7 +502,7 @@ def run_b200(args):
             # written 16 and read back 16, per edge succ 4 + reward 8
             alg = model_bytes
             formula = "20*S + 32*S_nonterminal + 12*E per solve (DESIGN.md 3.4)"
-            kernel = "k_cert_layer<false,4,4> (all H layer launches of one solve)"
+            kernel = "k_cert_rows<false,4,4> (all H layer launches of one solve)"
         elif method == N.VCS_METHOD_WAVEFRONT:
             # k_wave_layer (all H launches of one solve, extraction fused): per state row_ptr 4
             # + value 8 + action 4 + winner's action 4, per edge succ 4 + reward 8, per

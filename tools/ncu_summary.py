@@ -49,7 +49,7 @@ def main(rep, skip, out=None, kind="wave"):
                          "l2_hit_pct": float(r[hdr.index("lts__t_sector_hit_rate.pct")]),
                          "warps_active_pct": float(r[hdr.index("sm__warps_active.avg.pct_of_peak_sustained_active")]),
                          "issue_active_pct": float(r[hdr.index("smsp__issue_active.avg.pct_of_peak_sustained_active")])})
-    summary = {"kernel": "k_cert_layer<false,4,4>" if kind == "cert" else "k_wave_layer<false>",
+    summary = {"kernel": "k_cert_rows<false,4,4>" if kind == "cert" else "k_wave_layer<false>",
                "capture": f"ncu --set full, C4, launches {skip}..{skip + len(launches) - 1} of tools/prof_sweep.py",
                "dram_bytes_per_launch": launches[0]["dram_bytes"],
                "alg_bytes_per_launch": launches[0]["alg_bytes"], "launches": launches,
