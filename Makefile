@@ -16,7 +16,7 @@ JSON_INC  ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_fron
 CU_SRCS   := $(SRC)/vcs_space.cu $(SRC)/vcs_solve.cu $(SRC)/vcs_greedy.cu
 CU_OBJS   := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU_SRCS))
 HOST_OBJS := $(OBJ)/vcs_host.o
-HDRS      := include/vcs_gpu.h $(SRC)/vcs_internal.h $(SRC)/vcs_device.cuh
+HDRS      := include/vcs_gpu.h $(SRC)/vcs_internal.h $(SRC)/vcs_device.cuh $(SRC)/vcs_keys.cuh
 
 LIB       := $(PKG)/libvcs_gpu.so
 SHIM      := $(PKG)/libvcsched_b200.so

@@ -24,11 +24,17 @@
         if (err_ != cudaSuccess)                                                               \
             ::vcs::raise(VCS_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(err_)); \
         ::vcs::note_launch();                                                                  \
+        ::vcs::debug_sync_check(__FILE__, __LINE__);                                           \
     } while (0)
 
 namespace vcs {
 
 constexpr uint32_t kEmpty32 = 0xffffffffu;
+
+// VCS_SYNC_CHECK (debugging): synchronise after every launch that is not being captured and
+// report the launch site of an asynchronous fault.
+void debug_sync_check(const char* file, int line);
+extern thread_local bool g_capturing; // set while a solve graph is being captured
 
 // Configure the device's default memory pool once so freed blocks stay cached for reuse
 // (building and freeing spaces repeatedly then costs no cudaMalloc / implicit device sync).
@@ -129,6 +135,7 @@ struct CachedGraph {
     int launches = 0;
     int method = kMethodJacobi;
     int uses = 0; // solves enqueued so far (the first runs without a graph)
+    bool implicit = false; // certified pass on the implicit-CSR form: fallback runs at collect
 };
 
 } // namespace vcs
@@ -154,6 +161,15 @@ struct vcs_space {
     vcs::DevBuf<double> reward;
     vcs::DevBuf<int32_t> action;
     vcs::DevBuf<uint64_t> keys;
+    // implicit-CSR form of a dense space (the persistent builder without EXPLICIT): the edges of
+    // a state follow from its key and the layer's LayerParam; successor indices from the rank
+    // tables.  The explicit CSR above is materialised on first use (vcs::ensure_csr).
+    bool implicit = false;
+    bool csr_ready = true;
+    uint64_t state_cap = 0;
+    vcs::DevBuf<uint32_t> rank_tables;  // per transition t at rank_off[t]
+    std::vector<uint64_t> rank_off;     // H+1
+    vcs::DevBuf<vcs::LayerParam> params_dev; // plan.layers on the device
 
     // value iteration state
     vcs::DevBuf<double> v[2];
@@ -171,6 +187,7 @@ struct vcs_space {
     cudaStream_t aux_stream = nullptr; // captures the fallback body of the certified graph
     std::map<vcs::GraphKey, vcs::CachedGraph> graphs;
     vcs::CachedGraph* last_graph = nullptr; // graph of the last vcs_solve_enqueue
+    vcs_solve_opts last_opts{};             // its options (the implicit-certified fallback)
     int last_key_skip = 1;
     // version-band sharded wavefront (vcs_wave_shard_*): this rank's band per layer
     int wave_world = 0, wave_rank = 0;
@@ -225,6 +242,7 @@ struct StreamUse {
 
 namespace vcs {
 bool trace_enabled(); // VCS_TRACE set: host-side phase timings on stderr
+void ensure_csr(vcs_space* sp); // materialise the explicit CSR of an implicit space
 double host_ms();
 void bind_device(int device);
 int sm_count(int device);

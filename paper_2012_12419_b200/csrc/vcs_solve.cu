@@ -18,6 +18,7 @@
 // residual.  Sweep k therefore only visits layers 0..min(H, H-k+1) (the +1 keeps both ping-pong
 // buffers exact).  Values, actions and the sweep count are bit-identical with and without it.
 #include "vcs_device.cuh"
+#include "vcs_keys.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -807,6 +808,87 @@ __global__ void __launch_bounds__(256, MINB) k_cert_rows(CertArgs a) {
         atomicMax(reinterpret_cast<unsigned long long*>(a.lb + a.m), s_lb);
 }
 
+// Certified layer on the implicit-CSR form of a dense space: a state's edges are
+// its valid slots (clouds in key order, paid last = the reference's edge order), the successor
+// of slot e is rank_t[idx_e], the reward is the layer's kept constant or the retirement formula
+// with the builder's rounded operations, the action the slot's cloud.  Per state: an 8-byte key
+// in, the (V_{m-1}, V_m) pair, value and action out; no CSR is read.
+struct CertImplArgs {
+    const uint64_t* __restrict__ keys;   // layer t's packed keys
+    const LayerParam* __restrict__ L;    // layer t's parameters (device)
+    const uint32_t* __restrict__ rank;   // transition t's rank table
+    const double2* __restrict__ xd_next; // layer t+1: (V_{m-2}, V_{m-1})
+    double2* xd_cur;                     // layer t:   (V_{m-1}, V_m)
+    double* values_out;
+    int32_t* act_out;
+    double* lb;
+    uint64_t row0, n;
+    int m;
+    double discount;
+};
+
+template <int WM, bool DISC>
+__global__ void __launch_bounds__(256, 4) k_cert_implicit(CertImplArgs a) {
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int SL = kDenseSlots;
+    __shared__ LayerParam sL;
+    __shared__ unsigned long long s_lb;
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(LayerParam) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t*>(&sL)[i] = __ldg(reinterpret_cast<const uint32_t*>(a.L) + i);
+    if (threadIdx.x == 0) s_lb = 0ull;
+    __syncthreads();
+    const LayerParam& L = sL;
+    const bool retires = L.n_keep != L.n_active;
+    double dmax = 0.0;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < a.n;
+         i += stride) {
+        uint64_t k[WM];
+        load_key<WM>(a.keys + i * static_cast<uint64_t>(L.words), L.words, k);
+        const Slots sl(k, L);
+        uint32_t rk[SL];
+#pragma unroll
+        for (int e = 0; e < SL; ++e)
+            if (sl.valid(e)) rk[e] = __ldg(a.rank + sl.idx(e, L));
+        double2 x[SL];
+#pragma unroll
+        for (int e = 0; e < SL; ++e)
+            if (sl.valid(e)) x[e] = __ldg(a.xd_next + rk[e]);
+        double hi = -INFINITY, lo = -INFINITY;
+        int best = -1;
+#pragma unroll
+        for (int e = 0; e < SL; ++e) {
+            if (!sl.valid(e)) continue;
+            const int pe = e == SL - 1 ? -1 : e;
+            const double r = retires ? retiring_reward<WM>(k, pe, L)
+                                     : (pe < 0 ? L.r_paid_kept : L.r_cloud_kept);
+            const double qx = DISC ? __dadd_rn(r, __dmul_rn(a.discount, x[e].x)) : __dadd_rn(r, x[e].x);
+            const double qy = DISC ? __dadd_rn(r, __dmul_rn(a.discount, x[e].y)) : __dadd_rn(r, x[e].y);
+            if (qy > hi) { // strict: the first maximal edge wins (mdp.cpp:254-260)
+                hi = qy;
+                best = pe;
+            }
+            if (qx > lo) lo = qx;
+        }
+        if (a.m == 1) lo = 0.0; // V_0
+        a.xd_cur[i] = make_double2(lo, hi);
+        a.values_out[a.row0 + i] = hi;
+        a.act_out[a.row0 + i] = best < 0 ? -1 : L.cloud[best];
+        const double d = fabs(hi - lo);
+        dmax = dmax < d ? d : dmax;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double other = __shfl_xor_sync(FULL, dmax, o);
+        dmax = dmax < other ? other : dmax;
+    }
+    if ((threadIdx.x & 31) == 0 && dmax > 0.0)
+        atomicMax(&s_lb, static_cast<unsigned long long>(__double_as_longlong(dmax)));
+    __syncthreads();
+    if (threadIdx.x == 0 && s_lb)
+        atomicMax(reinterpret_cast<unsigned long long*>(a.lb + a.m), s_lb);
+}
+
 // K* = H+1 is proven iff lb_k >= eps for k = 1..H (and no sweep cap below H+1).  Sets the graph
 // conditional to run the wavefront fallback otherwise.
 __global__ void k_cert_check(const double* __restrict__ lb, int H, double eps, int max_sweeps,
@@ -878,6 +960,20 @@ void ensure_wave_buffers(vcs_space* sp) {
     if (trace_enabled())
         std::fprintf(stderr, "[vcs solve] offsets alloc %.3f copy %.3f sync %.3f ms\n", t2 - t1,
                      t3 - t2, host_ms() - t3);
+}
+
+int max_key_words(const vcs_space* sp) {
+    int wm = 1;
+    for (int w : sp->plan.words) wm = std::max(wm, w);
+    return wm;
+}
+
+template <class F>
+void dispatch_words_solve(int wm, F&& f) {
+    if (wm <= 1) f(std::integral_constant<int, 1>{});
+    else if (wm <= 2) f(std::integral_constant<int, 2>{});
+    else if (wm <= 4) f(std::integral_constant<int, 4>{});
+    else f(std::integral_constant<int, 8>{});
 }
 
 void record_event(cudaEvent_t ev, cudaStream_t s, bool capturing) {
@@ -1043,7 +1139,6 @@ void record_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
 // wavefront as the body of a graph IF node that runs only when the proof fails.
 void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaStream_t s,
                       bool capturing) {
-    if (!capturing) raise(VCS_EINVAL, "the certified solve is only recorded into a CUDA graph");
     const bool disc = is_discounted(key.discount);
     const int H = sp->H;
     // (cert_xd / cert_lb are allocated before capture: an allocation inside a capture would
@@ -1089,6 +1184,51 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
     int per_sm = 0;
     VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, rows ? 256 : wpb * 32,
                                                            rows ? 0 : smem));
+    if (sp->implicit) { // implicit-CSR form: keys + rank tables; the fallback runs at collect
+        CertImplArgs c{};
+        c.values_out = sp->v[0].p;
+        c.act_out = sp->actions_dev.p;
+        c.lb = sp->cert_lb.p;
+        c.discount = key.discount;
+        int launches = 0;
+        for (int t = H - 1; t >= 0; --t) {
+            c.row0 = sp->layer_off[t];
+            c.n = sp->layer_off[t + 1] - sp->layer_off[t];
+            c.m = H - t;
+            c.keys = sp->keys.p + sp->key_off[t];
+            c.L = sp->params_dev.p + t;
+            c.rank = sp->rank_tables.p + sp->rank_off[t];
+            c.xd_next = sp->cert_xd.p + sp->layer_off[t + 1];
+            c.xd_cur = sp->cert_xd.p + c.row0;
+            if (c.n) {
+                dispatch_words_solve(max_key_words(sp), [&](auto wm) {
+                    constexpr int WM = decltype(wm)::value;
+                    const void* fn = disc ? reinterpret_cast<const void*>(k_cert_implicit<WM, true>)
+                                          : reinterpret_cast<const void*>(k_cert_implicit<WM, false>);
+                    int per_sm = 0;
+                    VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
+                    const uint64_t blocks = std::max<uint64_t>(
+                        1, std::min<uint64_t>((c.n + 255) / 256,
+                                              static_cast<uint64_t>(std::max(1, per_sm)) * sp->num_sms));
+                    if (disc)
+                        k_cert_implicit<WM, true><<<static_cast<unsigned>(blocks), 256, 0, s>>>(c);
+                    else
+                        k_cert_implicit<WM, false><<<static_cast<unsigned>(blocks), 256, 0, s>>>(c);
+                    VCS_LAUNCHED();
+                });
+                ++launches;
+            }
+            if (!g.layer_ev.empty()) record_event(g.layer_ev[static_cast<size_t>(t)], s, capturing);
+        }
+        k_cert_check<<<1, 64, 0, s>>>(sp->cert_lb.p, H, key.eps, key.max_sweeps, sp->ctrl.p, 0);
+        VCS_LAUNCHED();
+        record_event(g.ev[1], s, capturing);
+        record_event(g.ev[2], s, capturing);
+        g.launches = launches + 1;
+        g.implicit = true;
+        return;
+    }
+    if (!capturing) raise(VCS_EINVAL, "the certified solve is only recorded into a CUDA graph");
     CertArgs a{};
     a.row_ptr = sp->row_ptr.p;
     a.succ = sp->succ.p;
@@ -1225,6 +1365,10 @@ CachedGraph& enqueue_solve(vcs_space* sp, const GraphKey& key, cudaStream_t s) {
         it = sp->graphs.emplace(key, g).first;
     }
     CachedGraph& g = it->second;
+    if (std::getenv("VCS_NO_GRAPH") && sp->implicit && key.method == kMethodCertified) {
+        record_solve(sp, key, g, s, false); // debugging: direct launches (VCS_SYNC_CHECK works)
+        return g;
+    }
     // (Measured on C4: capture + instantiate + replay of the 49-node solve costs less than
     // enqueueing it directly, whose host work between short layer kernels idles the GPU, so
     // even a one-shot solve goes through the graph.)
@@ -1233,10 +1377,13 @@ CachedGraph& enqueue_solve(vcs_space* sp, const GraphKey& key, cudaStream_t s) {
         cudaStream_t cs = sp->stream;
         if (cs != s) VCS_CUDA(cudaStreamSynchronize(s)); // no cross-stream work pending
         VCS_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        g_capturing = true;
         try {
             record_solve(sp, key, g, cs, true);
             unnote_launch(static_cast<uint64_t>(g.launches)); // captured, not launched
+            g_capturing = false;
         } catch (...) {
+            g_capturing = false;
             cudaGraph_t dummy = nullptr;
             cudaStreamEndCapture(cs, &dummy);
             if (dummy) cudaGraphDestroy(dummy);
@@ -1380,10 +1527,13 @@ int enqueue_impl(vcs_space* sp, const vcs_solve_opts* opts, void* stream, int st
         const double t0 = vcs::trace_enabled() ? vcs::host_ms() : 0.0;
         vcs::ensure_solve_buffers(sp, sp->H + 1); // fixed size: cached graphs keep addresses
         int method = o.method;
-        if (method == VCS_METHOD_AUTO)
-            method = vcs::wavefront_fits(sp) ? VCS_METHOD_CERTIFIED : VCS_METHOD_JACOBI;
-        // (the certified solve keeps the wavefront as its fallback: same buffers)
-        if ((method == VCS_METHOD_WAVEFRONT || method == VCS_METHOD_CERTIFIED) &&
+        if (method == VCS_METHOD_AUTO) // implicit spaces: the fallback's buffers come at collect
+            method = sp->implicit || vcs::wavefront_fits(sp) ? VCS_METHOD_CERTIFIED
+                                                             : VCS_METHOD_JACOBI;
+        // Jacobi and the wavefront read the explicit CSR
+        if (method == VCS_METHOD_JACOBI || method == VCS_METHOD_WAVEFRONT) vcs::ensure_csr(sp);
+        // (the explicit certified solve keeps the wavefront as its in-graph fallback)
+        if ((method == VCS_METHOD_WAVEFRONT || (method == VCS_METHOD_CERTIFIED && !sp->implicit)) &&
             sp->ver_off_host.empty()) {
             try {
                 vcs::ensure_wave_buffers(sp);
@@ -1407,6 +1557,7 @@ int enqueue_impl(vcs_space* sp, const vcs_solve_opts* opts, void* stream, int st
         auto& g = vcs::enqueue_solve(sp, key, s);
         sp->last_graph = &g;
         sp->last_key_skip = key.skip;
+        sp->last_opts = o;
         return VCS_OK;
     });
 }
@@ -1494,16 +1645,29 @@ int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
     return guarded([&] {
         if (!sp->last_graph) raise(VCS_EINVAL, "no solve was enqueued on this space");
         vcs::bind_device(sp->device);
-        auto& g = *sp->last_graph;
-        const bool wave = g.method != vcs::kMethodJacobi; // wavefront or certified: V in v[0]
         const vcs::StreamUse s(sp, stream);
         vcs::SolveCtrl ctrl{};
         VCS_CUDA(cudaMemcpyAsync(&ctrl, sp->ctrl.p, sizeof ctrl, cudaMemcpyDeviceToHost, s));
         VCS_CUDA(cudaStreamSynchronize(s));
+        if (sp->last_graph->implicit && !ctrl.certified) {
+            // the proof failed (an early stop is possible): the layer wavefront on the explicit
+            // CSR, materialised now, gives the reference's result
+            if (std::getenv("VCS_PROFILE_NO_FALLBACK"))
+                raise(VCS_EINVAL, "VCS_PROFILE_NO_FALLBACK: the proof failed, results are invalid");
+            vcs_solve_opts fo = sp->last_opts;
+            fo.method = VCS_METHOD_WAVEFRONT;
+            const int rc = enqueue_impl(sp, &fo, stream, 0);
+            if (rc != VCS_OK) vcs::raise(rc, vcs_last_error());
+            VCS_CUDA(cudaMemcpyAsync(&ctrl, sp->ctrl.p, sizeof ctrl, cudaMemcpyDeviceToHost, s));
+            VCS_CUDA(cudaStreamSynchronize(s));
+        }
+        auto& g = *sp->last_graph;
+        const bool wave = g.method != vcs::kMethodJacobi; // wavefront or certified: V in v[0]
         const int K = ctrl.sweeps;
         if (g.method == vcs::kMethodCertified && !ctrl.certified &&
             std::getenv("VCS_PROFILE_NO_FALLBACK"))
             raise(VCS_EINVAL, "VCS_PROFILE_NO_FALLBACK: the proof failed, results are invalid");
+        (void)0;
         // Jacobi leaves V_{K*} in ping-pong buffer K*&1; the wavefront extraction writes it to v[0]
         const double* vsrc = wave ? sp->v[0].p : sp->v[K & 1].p;
         sp->result_values = vsrc;
@@ -1525,7 +1689,15 @@ int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
             const double dbar = sp->S ? static_cast<double>(sp->E) / static_cast<double>(sp->S) : 0.0;
             uint64_t done = 0;
             const bool certified = g.method == vcs::kMethodCertified && ctrl.certified;
-            if (certified) {
+            if (certified && g.implicit) {
+                // implicit-CSR form: per non-terminal state its key 8 + (V_{m-1}, V_m) pair
+                // written 16 and read back 16; per state value 8 + action 4; the rank tables
+                // read once (4 B per entry)
+                const uint64_t nt = sp->layer_off[sp->H];
+                done = 2 * nt;
+                report->model_bytes = 40.0 * nt + 12.0 * sp->S +
+                                      4.0 * static_cast<double>(sp->rank_off.empty() ? 0 : sp->rank_off.back());
+            } else if (certified) {
                 // two versions of every non-terminal state, once; per state: row_ptr 4 +
                 // value 8 + action 4 + winning action 4 + its (V_{m-1}, V_m) pair written 16 and
                 // read back 16; per edge: succ 4 + reward 8
@@ -1558,6 +1730,7 @@ int vcs_shard_begin(vcs_space* sp, double* v0, double* v1, double* delta, int32_
                     void* stream) {
     return guarded([&] {
         vcs::bind_device(sp->device);
+        vcs::ensure_csr(sp); // the sharded solvers read the explicit CSR
         const vcs::StreamUse s(sp, stream);
         sp->ctrl.exact(1, sp->stream);
         sp->actions_dev.exact(sp->S, sp->stream);
@@ -1639,6 +1812,7 @@ int vcs_wave_shard_begin(vcs_space* sp, int32_t world, int32_t rank, const vcs_s
         if (!(o.epsilon > 0.0))
             raise(VCS_EINVAL, "epsilon must be > 0 (value iteration would never terminate)");
         vcs::bind_device(sp->device);
+        vcs::ensure_csr(sp); // the sharded solvers read the explicit CSR
         const vcs::StreamUse s(sp, stream);
         sp->wave_world = world;
         sp->wave_rank = rank;

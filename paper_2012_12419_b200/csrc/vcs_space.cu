@@ -18,6 +18,7 @@
 // Keys are the reference's reduced keys (free counts of still-eligible clouds, mdp.hpp:70-79)
 // packed into 64-bit words, ceil(log2(vm_free+1)) bits per cloud.
 #include "vcs_device.cuh"
+#include "vcs_keys.cuh"
 
 #include <cooperative_groups.h>
 #include <math_constants.h>
@@ -36,59 +37,6 @@
 namespace vcs {
 
 namespace {
-
-__device__ __forceinline__ uint64_t mix64(uint64_t x) {
-    x ^= x >> 30;
-    x *= 0xbf58476d1ce4e5b9ull;
-    x ^= x >> 27;
-    x *= 0x94d049bb133111ebull;
-    x ^= x >> 31;
-    return x;
-}
-
-template <int WM>
-__device__ __forceinline__ uint64_t hash_key(const uint64_t (&k)[WM], int words, uint64_t salt) {
-    uint64_t h = mix64(salt * 0x9e3779b97f4a7c15ull + 0x632be59bd9b4e019ull);
-#pragma unroll
-    for (int i = 0; i < WM; ++i)
-        if (i < words) h = mix64(h ^ k[i]);
-    return h;
-}
-
-template <int WM>
-__device__ __forceinline__ void load_key(const uint64_t* __restrict__ p, int words,
-                                         uint64_t (&k)[WM]) {
-#pragma unroll
-    for (int i = 0; i < WM; ++i) k[i] = i < words ? p[i] : 0ull;
-}
-
-template <int WM>
-__device__ __forceinline__ bool key_equal(const uint64_t* __restrict__ p, int words,
-                                          const uint64_t (&k)[WM]) {
-    bool eq = true;
-#pragma unroll
-    for (int i = 0; i < WM; ++i)
-        if (i < words) eq &= (p[i] == k[i]);
-    return eq;
-}
-
-template <int WM>
-__device__ __forceinline__ int get_field(const uint64_t (&k)[WM], int off, int width) {
-    const int w = off >> 6;
-    uint64_t word = k[0];
-#pragma unroll
-    for (int i = 1; i < WM; ++i)
-        if (i == w) word = k[i];
-    return static_cast<int>((word >> (off & 63)) & ((1ull << width) - 1ull));
-}
-
-template <int WM>
-__device__ __forceinline__ void put_field(uint64_t (&k)[WM], int off, uint64_t v) {
-    const int w = off >> 6;
-#pragma unroll
-    for (int i = 0; i < WM; ++i)
-        if (i == w) k[i] |= v << (off & 63);
-}
 
 // Out-degree of frontier state i (the paid edge always exists), 0 past the frontier: the input
 // of the row-offset scan.
@@ -148,22 +96,6 @@ __device__ __forceinline__ void emit_edge(const uint64_t (&k)[WM], int p, const 
     const double base = p < 0 ? L.r_paid : L.r_cloud;
     *rw = __dsub_rn(base, __dmul_rn(L.gamma, retired));
     *act = p < 0 ? -1 : L.cloud[p];
-}
-
-// Reward of one edge when clouds retire at this transition (mdp.cpp:179-185 / :196-197):
-// beta*n - gamma*retired, retired summed in key-position order.  p = -1: the paid cloud.
-template <int WM>
-__device__ __forceinline__ double retiring_reward(const uint64_t (&k)[WM], int p,
-                                                  const LayerParam& L) {
-    double retired = 0.0;
-    for (int q = 0; q < L.n_active; ++q) {
-        if (L.keep_idx[q] >= 0) continue;
-        int v = get_field<WM>(k, L.bit_off[q], L.width[q]);
-        if (q == p) v -= L.demand;
-        retired = __dadd_rn(retired, static_cast<double>(v));
-    }
-    const double base = p < 0 ? L.r_paid : L.r_cloud;
-    return __dsub_rn(base, __dmul_rn(L.gamma, retired));
 }
 
 // Dense path: the successor of an edge is identified by its mixed-radix index; the first-edge
@@ -575,7 +507,9 @@ struct DenseBuild {
     int32_t* action;
     uint32_t* table0;    // first-edge tables, alternating per layer (dense_max entries each)
     uint32_t* table1;
-    uint32_t* rank_of;   // successor index -> its layer-local state index
+    uint32_t* rank_tables; // per transition t (at sum of dense_size of t' < t): successor
+                           // mixed-radix index -> its layer-local state index (kept: the
+                           // implicit-CSR solver reads them)
     uint32_t* bsum;      // per (round, block)
     uint64_t* desc;      // per state of the current layer: Slots::pack()
     uint32_t* jfirst;    // per state of the current layer: its first edge (layer-local)
@@ -589,44 +523,6 @@ struct DenseBuild {
 };
 
 constexpr int kDenseThreads = 256;
-constexpr int kDenseSlots = 8; // edge slots of a state: clouds 0..6 by key position, 7 = paid
-
-// A state's edges as 8 static slots: slot p < 7 is the edge choosing the cloud at key position p
-// (valid if eligible with enough free VMs), slot 7 the paid edge (always valid).  The state is
-// described by two words — the paid successor's mixed-radix index and the valid-cloud mask —
-// from which every slot's row offset (the reference's order: clouds ascending, paid last) and
-// successor index follow with a few integer operations (slot indices are compile-time).
-struct Slots {
-    uint32_t base; // successor index of the paid edge (nothing subtracted)
-    uint32_t mask; // bit p: the cloud at key position p is a valid action
-    __device__ __forceinline__ Slots(uint64_t desc)
-        : base(static_cast<uint32_t>(desc)), mask(static_cast<uint32_t>(desc >> 32)) {}
-    template <int WM>
-    __device__ __forceinline__ Slots(const uint64_t (&k)[WM], const LayerParam& L) : base(0), mask(0) {
-#pragma unroll
-        for (int p = 0; p < kDenseSlots - 1; ++p) {
-            if (p >= L.n_active) continue;
-            const uint32_t f = static_cast<uint32_t>(get_field<WM>(k, L.bit_off[p], L.width[p]));
-            if (L.keep_idx[p] >= 0) base += f * L.wnext[p];
-            if (L.attr[p] && f >= static_cast<uint32_t>(L.demand)) mask |= 1u << p;
-        }
-    }
-    __device__ __forceinline__ uint64_t pack() const {
-        return static_cast<uint64_t>(base) | (static_cast<uint64_t>(mask) << 32);
-    }
-    __device__ __forceinline__ bool valid(int e) const {
-        return e == kDenseSlots - 1 || ((mask >> e) & 1u);
-    }
-    __device__ __forceinline__ uint32_t off(int e) const {
-        return static_cast<uint32_t>(__popc(mask & ((1u << e) - 1u)));
-    }
-    __device__ __forceinline__ uint32_t deg() const { return static_cast<uint32_t>(__popc(mask)) + 1u; }
-    __device__ __forceinline__ uint32_t idx(int e, const LayerParam& L) const {
-        return (e < kDenseSlots - 1 && e < L.n_active && L.keep_idx[e] >= 0)
-                   ? base - static_cast<uint32_t>(L.demand) * L.wnext[e]
-                   : base;
-    }
-};
 
 // Successor key of the edge choosing key position p (-1 = paid), in layer t+1's packing.
 template <int WM>
@@ -701,7 +597,9 @@ __device__ __forceinline__ void stamp(uint64_t* stamps, int slot) {
     }
 }
 
-template <int WM, int MINB>
+// EXPLICIT: also write the CSR (row_ptr, succ, reward, action).  Without it the build keeps
+// only keys, layer sizes and the rank tables: the implicit-CSR form.
+template <int WM, int MINB, bool EXPLICIT>
 __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild A) {
     using Scan = cub::BlockScan<uint32_t, kDenseThreads>;
     __shared__ typename Scan::TempStorage scan_tmp;
@@ -718,6 +616,7 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
     uint64_t S_t = 0;   // first state of layer t
     uint64_t E = 0;     // edges of layers < t
     uint64_t key_t = 0; // first key word of layer t
+    uint64_t rank_t = 0; // first entry of transition t's rank table
     uint32_t n_t = 1;
     if (b == 0 && tid == 0) A.info[0] = 1;
     auto publish_rounds = [&](int R) { // s_round -> bsum[r * G + b]
@@ -770,28 +669,32 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
             if (i < n_t) {
                 const uint32_t j = j0 + excl;
                 A.jfirst[i] = j;
-                A.row_ptr[S_t + i] = static_cast<uint32_t>(E + j);
+                if (EXPLICIT) A.row_ptr[S_t + i] = static_cast<uint32_t>(E + j);
                 uint32_t cur[SL];
 #pragma unroll
                 for (int e = 0; e < SL; ++e)
                     if (sl.valid(e)) cur[e] = table[sl.idx(e, L)]; // the state's checks in flight
                 uint64_t k[WM];
-                if (retires) key_of(i, k);
+                if (EXPLICIT && retires) key_of(i, k);
 #pragma unroll
                 for (int e = 0; e < SL; ++e) {
                     if (!sl.valid(e)) continue;
                     const int pe = e == SL - 1 ? -1 : e;
                     const uint32_t o = excl + (e == SL - 1 ? sl.deg() - 1u : sl.off(e));
-                    s_rew[o] = retires ? retiring_reward<WM>(k, pe, L)
-                                       : (pe < 0 ? L.r_paid_kept : L.r_cloud_kept);
-                    s_act[o] = pe < 0 ? -1 : L.cloud[pe];
+                    if (EXPLICIT) {
+                        s_rew[o] = retires ? retiring_reward<WM>(k, pe, L)
+                                           : (pe < 0 ? L.r_paid_kept : L.r_cloud_kept);
+                        s_act[o] = pe < 0 ? -1 : L.cloud[pe];
+                    }
                     if (cur[e] > j0 + o) atomicMin(&table[sl.idx(e, L)], j0 + o); // first edge wins
                 }
             }
-            __syncthreads();
-            for (uint32_t o = tid; o < cnt; o += blockDim.x) {
-                A.reward[E + j0 + o] = s_rew[o];
-                A.action[E + j0 + o] = s_act[o];
+            if (EXPLICIT) {
+                __syncthreads();
+                for (uint32_t o = tid; o < cnt; o += blockDim.x) {
+                    A.reward[E + j0 + o] = s_rew[o];
+                    A.action[E + j0 + o] = s_act[o];
+                }
             }
         }
         if (tid < 8) s_round[tid] = 0;
@@ -852,7 +755,7 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
 #pragma unroll
                 for (int e = 0; e < SL; ++e) {
                     if (!((first >> e) & 1u)) continue;
-                    A.rank_of[sl.idx(e, L)] = rank;
+                    A.rank_tables[rank_t + sl.idx(e, L)] = rank;
                     uint64_t nk[WM];
                     next_key<WM>(k, e == SL - 1 ? -1 : e, L, nk);
                     uint64_t* dst = A.keys + key_next + static_cast<uint64_t>(rank) * L.next_words;
@@ -869,11 +772,11 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
         }
         grid.sync();
         stamp(A.stamps, 6 * t + 4);
-        // phase 5: successor ids; clear this layer's table for layer t+2 (layer t+1 uses the
-        // other one; rank_of is rewritten by the next layer's phase 4, two grid syncs later)
+        // phase 5: successor ids (explicit form); clear this layer's first-edge table for layer
+        // t+2 (layer t+1 uses the other one)
         uint32_t* s_succ = reinterpret_cast<uint32_t*>(s_act); // (phase 2 is done with it)
         __shared__ uint32_t s_j0, s_j1;
-        for (int r = 0; r < R; ++r) {
+        for (int r = 0; EXPLICIT && r < R; ++r) {
             const uint32_t i = static_cast<uint32_t>(r) * T + q;
             const uint32_t blk0 = static_cast<uint32_t>(r) * T + static_cast<uint32_t>(b) * blockDim.x;
             __syncthreads();
@@ -894,7 +797,7 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
                 uint32_t rk[SL];
 #pragma unroll
                 for (int e = 0; e < SL; ++e)
-                    if (sl.valid(e)) rk[e] = __ldcg(A.rank_of + sl.idx(e, L));
+                    if (sl.valid(e)) rk[e] = __ldcg(A.rank_tables + rank_t + sl.idx(e, L));
 #pragma unroll
                 for (int e = 0; e < SL; ++e)
                     if (sl.valid(e))
@@ -908,16 +811,18 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
         S_t = S_next;
         E += E_t;
         key_t = key_next;
+        rank_t += L.dense_size;
         n_t = n_next;
     }
     // the terminal layer's rows have no edges (mdp.cpp:207-209)
-    for (uint32_t i = q; i <= n_t; i += T) A.row_ptr[S_t + i] = static_cast<uint32_t>(E);
+    if (EXPLICIT)
+        for (uint32_t i = q; i <= n_t; i += T) A.row_ptr[S_t + i] = static_cast<uint32_t>(E);
 }
 
 // Host side of the persistent dense builder.  Returns false (nothing done) when it does not
 // apply: some layer's key space is not dense, the a-priori CSR bound is not affordable, or the
 // device cannot launch cooperative kernels.  VCS_BUILD_LAYERED forces the multi-kernel path.
-template <int WM>
+template <int WM, bool EXPLICIT>
 bool build_dense(vcs_space* sp, uint64_t state_cap) {
     const bool layered = std::getenv("VCS_BUILD_LAYERED") != nullptr; // (read per build: tests)
     const LayerPlan& pl = sp->plan;
@@ -939,13 +844,16 @@ bool build_dense(vcs_space* sp, uint64_t state_cap) {
         k_bound += nb * static_cast<uint64_t>(L.next_words);
         if (e_bound >= 0xffffffffull || s_bound >= 0xffffffffull) return false;
     }
-    const uint64_t bytes = e_bound * 16 + s_bound * 4 + k_bound * 8 + e_layer_max * 4 + dense_max * 12;
+    uint64_t rank_total = 0;
+    for (int t = 0; t < H; ++t) rank_total += pl.layers[static_cast<size_t>(t)].dense_size;
+    const uint64_t bytes = (EXPLICIT ? e_bound * 16 + s_bound * 4 : 0) + k_bound * 8 +
+                           e_layer_max * 4 + dense_max * 8 + rank_total * 4;
     if (bytes > device_bytes(sp->device) / 8) return false;
     int coop = 0;
     VCS_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, sp->device));
     if (!coop) return false;
     // (2 blocks per SM; forcing 3 or 4 by register caps measured slower)
-    const void* fn = reinterpret_cast<const void*>(k_build_dense<WM, 2>);
+    const void* fn = reinterpret_cast<const void*>(k_build_dense<WM, 2, EXPLICIT>);
     int per_sm = 0;
     VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kDenseThreads, 0));
     if (per_sm < 1) return false;
@@ -969,26 +877,27 @@ bool build_dense(vcs_space* sp, uint64_t state_cap) {
     const double t_setup = trace_enabled() ? host_ms() : 0.0;
     cudaStream_t s = sp->stream;
     sp->keys.reserve(k_bound, 0, s);
-    sp->row_ptr.reserve(s_bound + 1, 0, s);
-    sp->succ.reserve(e_bound, 0, s);
-    sp->reward.reserve(e_bound, 0, s);
-    sp->action.reserve(e_bound, 0, s);
-    DevBuf<uint32_t> tables, rank_of, bsum;
+    if (EXPLICIT) {
+        sp->row_ptr.reserve(s_bound + 1, 0, s);
+        sp->succ.reserve(e_bound, 0, s);
+        sp->reward.reserve(e_bound, 0, s);
+        sp->action.reserve(e_bound, 0, s);
+    }
+    sp->rank_tables.exact(rank_total, s);
+    DevBuf<uint32_t> tables, bsum;
     DevBuf<uint64_t> desc;
     DevBuf<uint32_t> jfirst;
     DevBuf<uint64_t> stamps;
     DevBuf<uint64_t> info;
     DevBuf<int32_t> status;
-    DevBuf<LayerParam> params;
     tables.exact(2 * dense_max, s);
-    rank_of.exact(dense_max, s);
     bsum.exact(static_cast<size_t>(G) * max_rounds, s);
     desc.exact(n_max, s);
     jfirst.exact(n_max, s);
     info.exact(2 * static_cast<size_t>(H) + 2, s);
     status.exact(1, s);
-    params.exact(static_cast<size_t>(H), s);
-    VCS_CUDA(cudaMemcpyAsync(params.p, pl.layers.data(), H * sizeof(LayerParam),
+    sp->params_dev.exact(static_cast<size_t>(H), s); // kept: the implicit-CSR solver reads it
+    VCS_CUDA(cudaMemcpyAsync(sp->params_dev.p, pl.layers.data(), H * sizeof(LayerParam),
                              cudaMemcpyHostToDevice, s));
     VCS_CUDA(cudaMemcpyAsync(sp->keys.p, pl.init_key.data(), pl.words[0] * sizeof(uint64_t),
                              cudaMemcpyHostToDevice, s));
@@ -996,7 +905,7 @@ bool build_dense(vcs_space* sp, uint64_t state_cap) {
     VCS_CUDA(cudaMemsetAsync(status.p, 0, sizeof(int32_t), s));
     VCS_CUDA(cudaMemsetAsync(info.p, 0, (2 * static_cast<size_t>(H) + 2) * sizeof(uint64_t), s));
     DenseBuild A{};
-    A.params = params.p;
+    A.params = sp->params_dev.p;
     A.keys = sp->keys.p;
     A.row_ptr = sp->row_ptr.p;
     A.succ = sp->succ.p;
@@ -1004,7 +913,7 @@ bool build_dense(vcs_space* sp, uint64_t state_cap) {
     A.action = sp->action.p;
     A.table0 = tables.p;
     A.table1 = tables.p + dense_max;
-    A.rank_of = rank_of.p;
+    A.rank_tables = sp->rank_tables.p;
     A.bsum = bsum.p;
     A.desc = desc.p;
     A.jfirst = jfirst.p;
@@ -1069,6 +978,12 @@ bool build_dense(vcs_space* sp, uint64_t state_cap) {
     sp->layer_off[static_cast<size_t>(H) + 1] = S;
     sp->S = S;
     sp->E = E;
+    sp->rank_off.assign(static_cast<size_t>(H) + 1, 0);
+    for (int t = 0; t < H; ++t)
+        sp->rank_off[static_cast<size_t>(t) + 1] =
+            sp->rank_off[static_cast<size_t>(t)] + pl.layers[static_cast<size_t>(t)].dense_size;
+    sp->implicit = true;     // keys + rank tables + params_dev
+    sp->csr_ready = EXPLICIT; // (ensure_csr re-runs the build with EXPLICIT to materialise)
     return true;
 }
 
@@ -1298,6 +1213,21 @@ void ensure_locate_index(vcs_space* sp) {
 
 } // namespace
 
+thread_local bool g_capturing = false;
+
+void debug_sync_check(const char* file, int line) {
+    static const bool on = std::getenv("VCS_SYNC_CHECK") != nullptr;
+    if (!on || g_capturing) return; // inside a stream capture nothing has run yet
+    const cudaError_t e = cudaDeviceSynchronize();
+    if (std::getenv("VCS_SYNC_CHECK_VERBOSE"))
+        std::fprintf(stderr, "[vcs sync-check] %s:%d %s\n", file, line, cudaGetErrorString(e));
+    if (e != cudaSuccess) {
+        std::fprintf(stderr, "[vcs sync-check] fault after the launch at %s:%d: %s\n", file, line,
+                     cudaGetErrorString(e));
+        raise(VCS_ECUDA, std::string("fault after launch at ") + file + ":" + std::to_string(line));
+    }
+}
+
 bool trace_enabled() {
     static const bool on = std::getenv("VCS_TRACE") != nullptr;
     return on;
@@ -1307,6 +1237,22 @@ double host_ms() {
     return std::chrono::duration<double, std::milli>(
                std::chrono::steady_clock::now().time_since_epoch())
         .count();
+}
+
+// Materialise the explicit CSR of a space built in the implicit form: the dense builder runs
+// again with EXPLICIT (same keys and layer order, bit for bit); the layered builder if the CSR
+// bound is not affordable.
+void ensure_csr(vcs_space* sp) {
+    if (sp->csr_ready) return;
+    bind_device(sp->device);
+    const double t0 = trace_enabled() ? host_ms() : 0.0;
+    dispatch_words(max_words(sp), [&](auto wm) {
+        constexpr int WM = decltype(wm)::value;
+        if (!build_dense<WM, true>(sp, sp->state_cap)) build_layers<WM>(sp, sp->state_cap);
+    });
+    sp->csr_ready = true;
+    if (trace_enabled()) std::fprintf(stderr, "[vcs build] explicit CSR materialised in %.3f ms\n",
+                                      host_ms() - t0);
 }
 
 void bind_device(int device) {
@@ -1473,6 +1419,10 @@ vcs_space::~vcs_space() {
     layer_off_dev.release_idle();
     loc_table.release_idle();
     query_meta.release_idle();
+    rank_tables.release_idle();
+    params_dev.release_idle();
+    // (every DevBuf member must be released above: their destructors would free on the
+    // destroyed stream below)
     if (stream) {
         cudaStreamSynchronize(stream);
         cudaStreamDestroy(stream);
@@ -1523,10 +1473,15 @@ int vcs_space_build(const vcs_instance* inst, uint64_t state_cap, int device, vc
         }
         sp->max_degree = maxdeg;
         const auto t0 = std::chrono::steady_clock::now();
+        sp->state_cap = state_cap;
+        // dense spaces: the implicit-CSR form (keys + rank tables), the explicit CSR is
+        // materialised on first use (vcs::ensure_csr); VCS_BUILD_EXPLICIT builds it right away
+        const bool explicit_now = std::getenv("VCS_BUILD_EXPLICIT") != nullptr;
         vcs::dispatch_words(vcs::max_words(sp.get()), [&](auto wm) {
             constexpr int WM = decltype(wm)::value;
-            if (!vcs::build_dense<WM>(sp.get(), state_cap))
-                vcs::build_layers<WM>(sp.get(), state_cap);
+            const bool dense = explicit_now ? vcs::build_dense<WM, true>(sp.get(), state_cap)
+                                            : vcs::build_dense<WM, false>(sp.get(), state_cap);
+            if (!dense) vcs::build_layers<WM>(sp.get(), state_cap);
         });
         const auto t1 = std::chrono::steady_clock::now();
         sp->build_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
@@ -1612,6 +1567,7 @@ int vcs_space_layer_edges(const vcs_space* sp, uint64_t* layer_edges) {
 int vcs_space_csr(const vcs_space* sp, uint64_t* row_ptr, uint32_t* succ, double* reward,
                   int32_t* action) {
     return guarded([&] {
+        vcs::ensure_csr(const_cast<vcs_space*>(sp));
         vcs::bind_device(sp->device);
         cudaStream_t s = sp->stream;
         if (row_ptr) {
