@@ -117,5 +117,48 @@ struct Slots {
     }
 };
 
+// The slot constants of one layer held in registers (a thread decodes many states per layer):
+// per cloud slot p the key word, shift, field mask (0 = slot unused), the successor weight
+// W_p (0 when the cloud retires: its successor index does not move), and the eligibility mask.
+template <int WM>
+struct SlotDecoder {
+    uint32_t sw[kDenseSlots - 1]; // bits 0-5 shift, 8-15 width, 16 eligible, 17 used, 24+ key word
+    uint32_t wn[kDenseSlots - 1];
+    uint32_t demand;
+    __device__ __forceinline__ explicit SlotDecoder(const LayerParam& L) {
+        demand = static_cast<uint32_t>(L.demand);
+#pragma unroll
+        for (int p = 0; p < kDenseSlots - 1; ++p) {
+            const bool on = p < L.n_active;
+            const uint32_t off = on ? L.bit_off[p] : 0u;
+            sw[p] = (off & 63u) | ((on ? static_cast<uint32_t>(L.width[p]) : 0u) << 8) |
+                    ((on && L.attr[p]) ? 1u << 16 : 0u) | (on ? 1u << 17 : 0u) | ((off >> 6) << 24);
+            wn[p] = (on && L.keep_idx[p] >= 0) ? L.wnext[p] : 0u;
+        }
+    }
+    __device__ __forceinline__ uint32_t field(const uint64_t (&k)[WM], int p) const {
+        uint64_t w = k[0];
+#pragma unroll
+        for (int i = 1; i < WM; ++i)
+            if (static_cast<uint32_t>(i) == (sw[p] >> 24)) w = k[i];
+        const uint32_t width = (sw[p] >> 8) & 0xffu;
+        return static_cast<uint32_t>(w >> (sw[p] & 63u)) & ((1u << width) - 1u);
+    }
+    // the state's Slots (same result as Slots(k, L))
+    __device__ __forceinline__ Slots decode(const uint64_t (&k)[WM]) const {
+        uint32_t base = 0, mask = 0;
+#pragma unroll
+        for (int p = 0; p < kDenseSlots - 1; ++p) {
+            const uint32_t f = field(k, p);
+            base += f * wn[p];
+            if (((sw[p] >> 16) & 1u) && f >= demand) mask |= 1u << p;
+        }
+        return Slots(static_cast<uint64_t>(base) | (static_cast<uint64_t>(mask) << 32));
+    }
+    __device__ __forceinline__ uint32_t idx(const Slots& sl, int e) const {
+        return e < kDenseSlots - 1 ? sl.base - demand * wn[e] : sl.base;
+    }
+};
+
 } // namespace
 } // namespace vcs
