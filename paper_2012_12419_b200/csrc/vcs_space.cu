@@ -631,6 +631,7 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
         if (tid < 8) s_round[tid] = 0;
         __syncthreads();
         const LayerParam& L = sL;
+        const SlotDecoder<WM> dec(L); // the layer's slot constants, in registers
         uint32_t* table = (t & 1) ? A.table1 : A.table0;
         const uint64_t S_next = S_t + n_t;
         const uint64_t key_next = key_t + static_cast<uint64_t>(n_t) * L.words;
@@ -640,6 +641,110 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
             load_key<WM>(A.keys + key_t + static_cast<uint64_t>(i) * L.words, L.words, k);
         };
         stamp(A.stamps, 6 * t + 0);
+        if (!EXPLICIT) {
+            // Implicit form: no edge offsets are needed.  Edges are ordered by (state, slot), so
+            // the first edge into a successor is the minimum of (i << 3 | slot) over its edges.
+            // phase 1: descriptors, degree sum (E_t), first-edge atomicMin
+            stamp(A.stamps, 6 * t + 1);
+            uint32_t dsum = 0;
+            for (int r = 0; r < R; ++r) {
+                const uint32_t i = static_cast<uint32_t>(r) * T + q;
+                if (i >= n_t) continue;
+                uint64_t k[WM];
+                key_of(i, k);
+                const Slots sl = dec.decode(k);
+                A.desc[i] = sl.pack();
+                dsum += sl.deg();
+                uint32_t cur[SL];
+#pragma unroll
+                for (int e = 0; e < SL; ++e)
+                    if (sl.valid(e)) cur[e] = table[dec.idx(sl, e)];
+#pragma unroll
+                for (int e = 0; e < SL; ++e) {
+                    const uint32_t key = (i << 3) | static_cast<uint32_t>(e);
+                    if (sl.valid(e) && cur[e] > key) atomicMin(&table[dec.idx(sl, e)], key);
+                }
+            }
+            dsum = __reduce_add_sync(0xffffffffu, dsum);
+            if ((tid & 31) == 0 && dsum)
+                atomicAdd(reinterpret_cast<unsigned long long*>(A.info + A.H + 1 + t),
+                          static_cast<unsigned long long>(dsum));
+            grid.sync();
+            stamp(A.stamps, 6 * t + 2);
+            // phase 2: first-occurrence counts per (round, block)
+            for (int r = 0; r < R; ++r) {
+                const uint32_t i = static_cast<uint32_t>(r) * T + q;
+                uint32_t f = 0;
+                if (i < n_t) {
+                    const Slots sl(__ldcg(A.desc + i));
+                    uint32_t cur[SL];
+#pragma unroll
+                    for (int e = 0; e < SL; ++e)
+                        if (sl.valid(e)) cur[e] = __ldcg(table + dec.idx(sl, e));
+#pragma unroll
+                    for (int e = 0; e < SL; ++e)
+                        if (sl.valid(e) && cur[e] == ((i << 3) | static_cast<uint32_t>(e))) ++f;
+                }
+                round_add(s_round, r, f);
+            }
+            publish_rounds(R);
+            grid.sync();
+            stamp(A.stamps, 6 * t + 3);
+            // phase 3: ranks, next keys, cap check
+            const uint32_t n_next = round_prefixes(A.bsum, R, G, b, s_before);
+            if (S_next + n_next > A.state_cap || S_next + n_next >= 0xffffffffull) {
+                if (b == 0 && tid == 0) {
+                    *A.status = S_next + n_next > A.state_cap ? 1 : 2;
+                    A.info[t + 1] = n_next;
+                }
+                return; // every block takes the same decision
+            }
+            for (int r = 0; r < R; ++r) {
+                const uint32_t i = static_cast<uint32_t>(r) * T + q;
+                const Slots sl(i < n_t ? __ldcg(A.desc + i) : 0ull);
+                uint32_t first = 0;
+                if (i < n_t) {
+                    uint32_t cur[SL];
+#pragma unroll
+                    for (int e = 0; e < SL; ++e)
+                        if (sl.valid(e)) cur[e] = __ldcg(table + dec.idx(sl, e));
+#pragma unroll
+                    for (int e = 0; e < SL; ++e)
+                        if (sl.valid(e) && cur[e] == ((i << 3) | static_cast<uint32_t>(e)))
+                            first |= 1u << e;
+                }
+                uint32_t rank;
+                Scan(scan_tmp).ExclusiveSum(static_cast<uint32_t>(__popc(first)), rank);
+                __syncthreads();
+                rank += s_before[r];
+                if (first) {
+                    uint64_t k[WM];
+                    key_of(i, k);
+#pragma unroll
+                    for (int e = 0; e < SL; ++e) {
+                        if (!((first >> e) & 1u)) continue;
+                        A.rank_tables[rank_t + dec.idx(sl, e)] = rank;
+                        uint64_t nk[WM];
+                        next_key<WM>(k, e == SL - 1 ? -1 : e, L, nk);
+                        uint64_t* dst = A.keys + key_next + static_cast<uint64_t>(rank) * L.next_words;
+#pragma unroll
+                        for (int w = 0; w < WM; ++w)
+                            if (w < L.next_words) dst[w] = nk[w];
+                        ++rank;
+                    }
+                }
+            }
+            if (b == 0 && tid == 0) A.info[t + 1] = n_next;
+            if (tid < 8) s_round[tid] = 0;
+            grid.sync();
+            stamp(A.stamps, 6 * t + 4);
+            for (uint32_t i = q; i < A.dense_max; i += T) table[i] = kEmpty32;
+            S_t = S_next;
+            key_t = key_next;
+            rank_t += L.dense_size;
+            n_t = n_next;
+            continue;
+        }
         // phase 1: degrees per (round, block); each state's slot descriptor
         for (int r = 0; r < R; ++r) {
             const uint32_t i = static_cast<uint32_t>(r) * T + q;
@@ -647,7 +752,7 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
             if (i < n_t) {
                 uint64_t k[WM];
                 key_of(i, k);
-                const Slots sl(k, L);
+                const Slots sl = dec.decode(k);
                 d = sl.deg();
                 A.desc[i] = sl.pack();
             }
@@ -673,7 +778,7 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
                 uint32_t cur[SL];
 #pragma unroll
                 for (int e = 0; e < SL; ++e)
-                    if (sl.valid(e)) cur[e] = table[sl.idx(e, L)]; // the state's checks in flight
+                    if (sl.valid(e)) cur[e] = table[dec.idx(sl, e)]; // the state's checks in flight
                 uint64_t k[WM];
                 if (EXPLICIT && retires) key_of(i, k);
 #pragma unroll
@@ -686,7 +791,7 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
                                            : (pe < 0 ? L.r_paid_kept : L.r_cloud_kept);
                         s_act[o] = pe < 0 ? -1 : L.cloud[pe];
                     }
-                    if (cur[e] > j0 + o) atomicMin(&table[sl.idx(e, L)], j0 + o); // first edge wins
+                    if (cur[e] > j0 + o) atomicMin(&table[dec.idx(sl, e)], j0 + o); // first edge wins
                 }
             }
             if (EXPLICIT) {
@@ -710,7 +815,7 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
                 uint32_t cur[SL];
 #pragma unroll
                 for (int e = 0; e < SL; ++e)
-                    if (sl.valid(e)) cur[e] = __ldcg(table + sl.idx(e, L));
+                    if (sl.valid(e)) cur[e] = __ldcg(table + dec.idx(sl, e));
 #pragma unroll
                 for (int e = 0; e < SL; ++e)
                     if (sl.valid(e))
@@ -739,7 +844,7 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
                 uint32_t cur[SL];
 #pragma unroll
                 for (int e = 0; e < SL; ++e)
-                    if (sl.valid(e)) cur[e] = __ldcg(table + sl.idx(e, L));
+                    if (sl.valid(e)) cur[e] = __ldcg(table + dec.idx(sl, e));
 #pragma unroll
                 for (int e = 0; e < SL; ++e)
                     if (sl.valid(e) && cur[e] == j + (e == SL - 1 ? sl.deg() - 1u : sl.off(e)))
@@ -755,7 +860,7 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
 #pragma unroll
                 for (int e = 0; e < SL; ++e) {
                     if (!((first >> e) & 1u)) continue;
-                    A.rank_tables[rank_t + sl.idx(e, L)] = rank;
+                    A.rank_tables[rank_t + dec.idx(sl, e)] = rank;
                     uint64_t nk[WM];
                     next_key<WM>(k, e == SL - 1 ? -1 : e, L, nk);
                     uint64_t* dst = A.keys + key_next + static_cast<uint64_t>(rank) * L.next_words;
@@ -797,7 +902,7 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
                 uint32_t rk[SL];
 #pragma unroll
                 for (int e = 0; e < SL; ++e)
-                    if (sl.valid(e)) rk[e] = __ldcg(A.rank_tables + rank_t + sl.idx(e, L));
+                    if (sl.valid(e)) rk[e] = __ldcg(A.rank_tables + rank_t + dec.idx(sl, e));
 #pragma unroll
                 for (int e = 0; e < SL; ++e)
                     if (sl.valid(e))
