@@ -521,3 +521,25 @@ def test_batched_policy_query(gpu):
         torch.cuda.synchronize()
         assert np.array_equal(dval.cpu().numpy().view(np.uint64), vals.view(np.uint64))
         assert np.array_equal(dact.cpu().numpy(), acts)
+
+
+def test_pinned_download_large(gpu, golden):
+    """C3 (1.8 M states) into pinned buffers: the chunked download behind the layer events of the
+    certified pass is exact, on a fresh and on a re-used graph."""
+    import torch
+    ni = V.generate_instance(N.VCS_GEN_HOMOG, 2012, 0, 5, 8, 40, 3, as_objects=False)
+    sp = V.StateSpace.build_native(ni, 10**9)
+    S = sp.size()
+    vals = torch.full((S,), float("nan"), dtype=torch.float64, pin_memory=True)
+    acts = torch.full((S,), 12345, dtype=torch.int32, pin_memory=True)
+    g = golden["cases"]["C3"]["eps=1e-06"]
+    for _ in range(2):
+        opts = N.vcs_solve_opts(1e-6, 1, 0, 1.0, N.VCS_METHOD_AUTO)
+        rep = N.vcs_solve_report()
+        N.check(N.lib().vcs_solve(sp.handle, C.byref(opts),
+                                  C.cast(C.c_void_p(vals.data_ptr()), C.POINTER(C.c_double)),
+                                  C.cast(C.c_void_p(acts.data_ptr()), C.POINTER(C.c_int32)),
+                                  C.byref(rep)))
+        assert rep.sweeps == g["sweeps"]
+        assert sha(vals.numpy()) == g["values_sha"]
+        assert sha(acts.numpy()) == g["actions_sha"]
