@@ -497,12 +497,13 @@ def run_b200(args):
         tr = ncu_traffic(method)
         survey_equiv = b_ref * S * sweeps / sweep_s / 1e9  # SURVEY 8d bytes of the Jacobi sweeps
         if method == N.VCS_METHOD_CERTIFIED:
-            # k_cert_layer (all H launches of one solve; the proof held, no fallback ran): per
-            # state row_ptr 4 + value 8 + action 4 + winner's action 4 + (V_{m-1}, V_m) pair
-            # written 16 and read back 16, per edge succ 4 + reward 8
+            # k_cert_implicit (all H launches of one solve; the proof held, no fallback ran):
+            # implicit-CSR form, per non-terminal state key 8 + (V_{m-1}, V_m) pair written 16
+            # and read back 16, per state value 8 + action 4, the rank tables read once
             alg = model_bytes
-            formula = "20*S + 32*S_nonterminal + 12*E per solve (DESIGN.md 3.4)"
-            kernel = "k_cert_rows<false,4,4> (all H layer launches of one solve)"
+            formula = ("40*S_nonterminal + 12*S + 4*sum(rank-table entries) per solve "
+                       "(DESIGN.md 3.4)")
+            kernel = "k_cert_implicit<1,false,3> (all H layer launches of one solve)"
         elif method == N.VCS_METHOD_WAVEFRONT:
             # k_wave_layer (all H launches of one solve, extraction fused): per state row_ptr 4
             # + value 8 + action 4 + winner's action 4, per edge succ 4 + reward 8, per

@@ -36,10 +36,10 @@ def main(rep, skip, out=None, kind="wave"):
         # once (8 * n_{t+1} * (m-1))
         alg = 20 * n + 12 * e + 8 * n * m + 8 * n_next * (m - 1)
         if kind == "cert":
-            # certified pass: per state row_ptr 4 + value 8 + action 4 + winner's action 4 +
-            # its (V_{m-1}, V_m) pair written 16; per edge succ 4 + reward 8; the successors'
-            # pairs read once (16 * n_{t+1})
-            alg = 20 * n + 16 * n + 12 * e + 16 * n_next
+            # certified pass on the implicit-CSR form: per state its key 8 + value 8 + action 4
+            # + its (V_{m-1}, V_m) pair written 16; the successors' pairs read once
+            # (16 * n_{t+1}); the layer's rank table read once (4 per entry, C4: 9^6 entries)
+            alg = 36 * n + 16 * n_next + 4 * 531441
         g = lambda k: float(r[hdr.index(k)]) * scale.get(units[hdr.index(k)], 1)
         dram = g("dram__bytes_read.sum") + g("dram__bytes_write.sum")
         tt = float(r[hdr.index("gpu__time_duration.sum")]) * (1e-6 if units[hdr.index("gpu__time_duration.sum")] == "us" else 1e-9)
@@ -49,7 +49,7 @@ def main(rep, skip, out=None, kind="wave"):
                          "l2_hit_pct": float(r[hdr.index("lts__t_sector_hit_rate.pct")]),
                          "warps_active_pct": float(r[hdr.index("sm__warps_active.avg.pct_of_peak_sustained_active")]),
                          "issue_active_pct": float(r[hdr.index("smsp__issue_active.avg.pct_of_peak_sustained_active")])})
-    summary = {"kernel": "k_cert_rows<false,4,4>" if kind == "cert" else "k_wave_layer<false>",
+    summary = {"kernel": "k_cert_implicit<1,false,3>" if kind == "cert" else "k_wave_layer<false>",
                "capture": f"ncu --set full, C4, launches {skip}..{skip + len(launches) - 1} of tools/prof_sweep.py",
                "dram_bytes_per_launch": launches[0]["dram_bytes"],
                "alg_bytes_per_launch": launches[0]["alg_bytes"], "launches": launches,
