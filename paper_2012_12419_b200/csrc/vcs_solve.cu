@@ -844,10 +844,14 @@ __global__ void __launch_bounds__(256, MINB) k_cert_implicit(CertImplArgs a) {
     const double r_cloud = L.r_cloud_kept, r_paid = L.r_paid_kept;
     double dmax = 0.0;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < a.n;
-         i += stride) {
+    uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    uint64_t kn[WM] = {}; // the next state's key, loaded while the current state computes
+    if (i < a.n) load_key<WM>(a.keys + i * static_cast<uint64_t>(words), words, kn);
+    for (; i < a.n; i += stride) {
         uint64_t k[WM];
-        load_key<WM>(a.keys + i * static_cast<uint64_t>(words), words, k);
+#pragma unroll
+        for (int w = 0; w < WM; ++w) k[w] = kn[w];
+        if (i + stride < a.n) load_key<WM>(a.keys + (i + stride) * static_cast<uint64_t>(words), words, kn);
         const Slots sl = dec.decode(k);
         uint32_t rk[SL];
 #pragma unroll
