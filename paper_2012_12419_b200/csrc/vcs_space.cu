@@ -655,14 +655,25 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
                 const Slots sl = dec.decode(k);
                 A.desc[i] = sl.pack();
                 dsum += sl.deg();
-                uint32_t cur[SL];
+                if (L.dense_size > 4096) {
+                    // a large successor space spreads the edges: plain reductions, no result
+                    // and no check load (nothing on the thread's latency chain)
 #pragma unroll
-                for (int e = 0; e < SL; ++e)
-                    if (sl.valid(e)) cur[e] = table[dec.idx(sl, e)];
+                    for (int e = 0; e < SL; ++e)
+                        if (sl.valid(e))
+                            atomicMin(&table[dec.idx(sl, e)], (i << 3) | static_cast<uint32_t>(e));
+                } else {
+                    // few successors (e.g. the single terminal state): read first, so that
+                    // heavily shared entries are not serialised by atomics
+                    uint32_t cur[SL];
 #pragma unroll
-                for (int e = 0; e < SL; ++e) {
-                    const uint32_t key = (i << 3) | static_cast<uint32_t>(e);
-                    if (sl.valid(e) && cur[e] > key) atomicMin(&table[dec.idx(sl, e)], key);
+                    for (int e = 0; e < SL; ++e)
+                        if (sl.valid(e)) cur[e] = table[dec.idx(sl, e)];
+#pragma unroll
+                    for (int e = 0; e < SL; ++e) {
+                        const uint32_t key = (i << 3) | static_cast<uint32_t>(e);
+                        if (sl.valid(e) && cur[e] > key) atomicMin(&table[dec.idx(sl, e)], key);
+                    }
                 }
             }
             dsum = __reduce_add_sync(0xffffffffu, dsum);
