@@ -641,6 +641,130 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
             load_key<WM>(A.keys + key_t + static_cast<uint64_t>(i) * L.words, L.words, k);
         };
         stamp(A.stamps, 6 * t + 0);
+        if (!EXPLICIT && WM == 1) {
+            // Implicit form, single-word keys, all of a thread's rounds at once: keys,
+            // descriptors and first-edge masks stay in registers across the grid syncs, the
+            // table loads of four rounds are in flight together, and ranks come from warp scans
+            // with one block barrier (instead of a block scan per round).
+            constexpr int RB = 8; // rounds (the host guarantees R <= 8)
+            uint64_t kr[RB], dr[RB];
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+                const uint32_t i = static_cast<uint32_t>(r) * T + q;
+                kr[r] = (r < R && i < n_t) ? A.keys[key_t + i] : 0ull;
+            }
+            stamp(A.stamps, 6 * t + 1);
+            uint32_t dsum = 0;
+            const bool red = L.dense_size > 4096;
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+                const uint32_t i = static_cast<uint32_t>(r) * T + q;
+                dr[r] = 0ull;
+                if (r >= R || i >= n_t) continue;
+                const uint64_t k1[1] = {kr[r]};
+                const Slots sl = reinterpret_cast<const SlotDecoder<1>&>(dec).decode(k1);
+                dr[r] = sl.pack();
+                dsum += sl.deg();
+#pragma unroll
+                for (int e = 0; e < SL; ++e) {
+                    if (!sl.valid(e)) continue;
+                    const uint32_t key = (i << 3) | static_cast<uint32_t>(e);
+                    uint32_t* slot = &table[dec.idx(sl, e)];
+                    if (red || *slot > key) atomicMin(slot, key);
+                }
+            }
+            dsum = __reduce_add_sync(0xffffffffu, dsum);
+            if ((tid & 31) == 0 && dsum)
+                atomicAdd(reinterpret_cast<unsigned long long*>(A.info + A.H + 1 + t),
+                          static_cast<unsigned long long>(dsum));
+            grid.sync();
+            stamp(A.stamps, 6 * t + 2);
+            // first-occurrence masks (kept for the rank phase), counts per (round, block)
+            uint32_t fm[RB];
+#pragma unroll
+            for (int h = 0; h < RB; h += 4) {
+                uint32_t cur[4][SL];
+#pragma unroll
+                for (int rr = 0; rr < 4; ++rr) {
+                    const int r = h + rr;
+                    // (a live state may have descriptor 0: only the paid edge, to index 0)
+                    const bool live = r < R && static_cast<uint32_t>(r) * T + q < n_t;
+                    const Slots sl(dr[r]);
+#pragma unroll
+                    for (int e = 0; e < SL; ++e)
+                        if (live && sl.valid(e)) cur[rr][e] = __ldcg(table + dec.idx(sl, e));
+                }
+#pragma unroll
+                for (int rr = 0; rr < 4; ++rr) {
+                    const int r = h + rr;
+                    const uint32_t i = static_cast<uint32_t>(r) * T + q;
+                    const bool live = r < R && i < n_t;
+                    const Slots sl(dr[r]);
+                    uint32_t f = 0;
+#pragma unroll
+                    for (int e = 0; e < SL; ++e)
+                        if (live && sl.valid(e) && cur[rr][e] == ((i << 3) | static_cast<uint32_t>(e)))
+                            f |= 1u << e;
+                    fm[r] = f;
+                    if (r < R) round_add(s_round, r, static_cast<uint32_t>(__popc(f)));
+                }
+            }
+            publish_rounds(R);
+            grid.sync();
+            stamp(A.stamps, 6 * t + 3);
+            const uint32_t n_next = round_prefixes(A.bsum, R, G, b, s_before);
+            if (S_next + n_next > A.state_cap || S_next + n_next >= 0xffffffffull) {
+                if (b == 0 && tid == 0) {
+                    *A.status = S_next + n_next > A.state_cap ? 1 : 2;
+                    A.info[t + 1] = n_next;
+                }
+                return; // every block takes the same decision
+            }
+            // ranks: warp exclusive scans of every round, one barrier for the warps' offsets
+            __shared__ uint32_t s_wsum[RB][kDenseThreads / 32];
+            const int lane = tid & 31, warp = tid >> 5;
+            uint32_t wex[RB];
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+                const uint32_t f = static_cast<uint32_t>(__popc(fm[r]));
+                uint32_t incl = f;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                wex[r] = incl - f;
+                if (lane == 31) s_wsum[r][warp] = incl;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+                if (!fm[r]) continue;
+                uint32_t rank = s_before[r] + wex[r];
+                for (int w = 0; w < warp; ++w) rank += s_wsum[r][w];
+                const uint64_t k1[1] = {kr[r]};
+                const Slots sl(dr[r]);
+#pragma unroll
+                for (int e = 0; e < SL; ++e) {
+                    if (!((fm[r] >> e) & 1u)) continue;
+                    A.rank_tables[rank_t + dec.idx(sl, e)] = rank;
+                    uint64_t nk[1];
+                    next_key<1>(k1, e == SL - 1 ? -1 : e, L, nk);
+                    A.keys[key_next + rank] = nk[0];
+                    ++rank;
+                }
+            }
+            if (b == 0 && tid == 0) A.info[t + 1] = n_next;
+            if (tid < 8) s_round[tid] = 0;
+            grid.sync();
+            stamp(A.stamps, 6 * t + 4);
+            for (uint32_t i = q; i < A.dense_max; i += T) table[i] = kEmpty32;
+            S_t = S_next;
+            key_t = key_next;
+            rank_t += L.dense_size;
+            n_t = n_next;
+            continue;
+        }
         if (!EXPLICIT) {
             // Implicit form: no edge offsets are needed.  Edges are ordered by (state, slot), so
             // the first edge into a successor is the minimum of (i << 3 | slot) over its edges.
