@@ -650,93 +650,8 @@ struct CertArgs {
     double* lb;                          // lb[k], k = m_t
     uint64_t row0, n, next_row0;
     int m;
-    int qcap;                            // staged edge slots per row
     double discount;
 };
-
-// Warp-cooperative like the Jacobi sweep: 32 consecutive rows per warp; the rows' edge range is
-// streamed with coalesced loads, the successors' (V_{m-2}, V_{m-1}) pairs gathered with one
-// 16-byte load per edge (8 edges per lane in flight), q pairs staged in shared memory, then each
-// lane scans its row: strict first maximum of V_m with its edge, strict maximum of V_{m-1}.
-template <bool DISC, int U, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_cert_layer(CertArgs a) {
-    constexpr unsigned FULL = 0xffffffffu;
-    extern __shared__ double2 s_q[];
-    __shared__ unsigned long long s_lb;
-    double2* qw = s_q + (threadIdx.x >> 5) * 32 * a.qcap;
-    if (threadIdx.x == 0) s_lb = 0ull;
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-    double dmax = 0.0;
-    for (uint64_t r0 = warp * 32; r0 < a.n; r0 += n_warps * 32) {
-        const uint64_t r = r0 + lane;
-        const bool valid = r < a.n;
-        const uint64_t rr = a.row0 + (valid ? r : a.n);
-        const uint32_t eb = __ldg(a.row_ptr + rr);
-        uint32_t ee = __shfl_down_sync(FULL, eb, 1);
-        if (lane == 31) ee = valid ? __ldg(a.row_ptr + rr + 1) : eb;
-        const uint32_t w0 = __shfl_sync(FULL, eb, 0);
-        const uint32_t w1 = __shfl_sync(FULL, ee, 31);
-        for (uint32_t base = w0; base < w1; base += 32 * U) {
-            uint32_t sidx[U];
-            double rw[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t e = base + u * 32 + lane;
-                if (e < w1) {
-                    sidx[u] = __ldcs(a.succ + e) - static_cast<uint32_t>(a.next_row0);
-                    rw[u] = __ldcs(a.reward + e);
-                }
-            }
-            double2 x[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (base + u * 32 + lane < w1) x[u] = __ldg(a.xd_next + sidx[u]);
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t e = base + u * 32 + lane;
-                if (e < w1) {
-                    double2 q;
-                    q.x = DISC ? __dadd_rn(rw[u], __dmul_rn(a.discount, x[u].x)) : __dadd_rn(rw[u], x[u].x);
-                    q.y = DISC ? __dadd_rn(rw[u], __dmul_rn(a.discount, x[u].y)) : __dadd_rn(rw[u], x[u].y);
-                    qw[e - w0] = q;
-                }
-            }
-        }
-        __syncwarp();
-        if (valid) {
-            double hi = -INFINITY, lo = -INFINITY;
-            uint32_t best_e = 0xffffffffu;
-            for (uint32_t e = eb; e < ee; ++e) {
-                const double2 q = qw[e - w0];
-                if (q.y > hi) { // strict: the first maximal edge wins (mdp.cpp:254-260)
-                    hi = q.y;
-                    best_e = e;
-                }
-                if (q.x > lo) lo = q.x;
-            }
-            if (a.m == 1) lo = 0.0; // V_0
-            a.xd_cur[r] = make_double2(lo, hi);
-            a.values_out[a.row0 + r] = hi;
-            a.act_out[a.row0 + r] = best_e != 0xffffffffu ? __ldg(a.action + best_e) : -1;
-            const double d = fabs(hi - lo); // parallel_vi.cpp: |v_new - v_old|
-            dmax = dmax < d ? d : dmax;
-        }
-        __syncwarp();
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const double other = __shfl_xor_sync(FULL, dmax, o);
-        dmax = dmax < other ? other : dmax;
-    }
-    if (lane == 0 && dmax > 0.0)
-        atomicMax(&s_lb, static_cast<unsigned long long>(__double_as_longlong(dmax)));
-    __syncthreads();
-    if (threadIdx.x == 0 && s_lb)
-        atomicMax(reinterpret_cast<unsigned long long*>(a.lb + a.m), s_lb);
-}
 
 // Thread-per-row form of the certified layer: each thread streams its own row's contiguous
 // edge range (through L1: a warp's 32 rows are one contiguous span) and keeps U gathers in
@@ -1007,21 +922,12 @@ void raise_smem_limit(const void* fn, int device, size_t smem) {
 // Launch k_wave_layer for the band [a.band_lo, a.band_hi) of one layer (a.row0 / n / m /
 // strides / bases set by the caller): tile size, shared memory, grid.
 void launch_layer(vcs_space* sp, WaveArgs& a, bool disc, cudaStream_t s) {
-    // kernel variant (gathers in flight per thread vs occupancy); VCS_WAVE_VARIANT overrides
-    static const int variant = [] {
-        const char* e = std::getenv("VCS_WAVE_VARIANT");
-        return e ? std::atoi(e) : 1;
-    }();
+    // 4 gathers in flight per thread, 4 blocks per SM (64 registers): measured best of
+    // (U, blocks) in {(8,3), (4,4), (4,5), (2,6)} on C4
     using LayerFn = void (*)(WaveArgs);
-#define VCS_WAVE_VARIANTS(D, B)                                                                 \
-    {k_wave_layer<D, 8, 3, B>, k_wave_layer<D, 4, 4, B>, k_wave_layer<D, 4, 5, B>,              \
-     k_wave_layer<D, 2, 6, B>}
-    static const LayerFn fns[2][2][4] = {
-        {VCS_WAVE_VARIANTS(false, false), VCS_WAVE_VARIANTS(true, false)},
-        {VCS_WAVE_VARIANTS(false, true), VCS_WAVE_VARIANTS(true, true)}};
-#undef VCS_WAVE_VARIANTS
     const bool band = a.band_lo != 1 || a.base != 0 || a.base_next != 0;
-    const LayerFn layer_fn = fns[band ? 1 : 0][disc ? 1 : 0][std::min(3, std::max(0, variant))];
+    const LayerFn layer_fn = band ? (disc ? k_wave_layer<true, 4, 4, true> : k_wave_layer<false, 4, 4, true>)
+                                  : (disc ? k_wave_layer<true, 4, 4, false> : k_wave_layer<false, 4, 4, false>);
     const void* fn = reinterpret_cast<const void*>(layer_fn);
     const int nb = a.band_hi - a.band_lo;
     if (nb <= 0 || a.n == 0) return;
@@ -1160,36 +1066,6 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
         VCS_CUDA(cudaMemsetAsync(sp->actions_dev.p + rH, 0xff, nH * sizeof(int32_t), s));
         VCS_CUDA(cudaMemsetAsync(sp->cert_xd.p + rH, 0, nH * sizeof(double2), s)); // V_0 = 0
     }
-    const int qcap = std::max(1, sp->max_degree);
-    // warps per block: 32 rows x qcap staged q pairs (16 B) per warp within 96 KB
-    const int wpb = static_cast<int>(std::max<size_t>(
-        1, std::min<size_t>(8, (96u << 10) / (static_cast<size_t>(32) * qcap * sizeof(double2)))));
-    const size_t smem = static_cast<size_t>(wpb) * 32 * qcap * sizeof(double2);
-    // variants (VCS_CERT_VARIANT): 0-3 warp-cooperative k_cert_layer, 4-8 thread-per-row
-    // k_cert_rows; default 4 = rows, 4 edges in flight, 4 blocks/SM (C4: 0.77 ms per solve vs
-    // 0.83 for the best warp-cooperative form; more resident warps thrash L1)
-    using CertFn = void (*)(CertArgs);
-    static const CertFn fns[2][4] = {
-        {k_cert_layer<false, 8, 2>, k_cert_layer<false, 4, 4>, k_cert_layer<false, 8, 3>,
-         k_cert_layer<false, 4, 6>},
-        {k_cert_layer<true, 8, 2>, k_cert_layer<true, 4, 4>, k_cert_layer<true, 8, 3>,
-         k_cert_layer<true, 4, 6>}};
-    static const int variant = [] {
-        const char* e = std::getenv("VCS_CERT_VARIANT");
-        return e ? std::min(8, std::max(0, std::atoi(e))) : 4;
-    }();
-    const CertFn row_fns[2][5] = {
-        {k_cert_rows<false, 4, 4>, k_cert_rows<false, 3, 4>, k_cert_rows<false, 3, 5>,
-         k_cert_rows<false, 4, 5>, k_cert_rows<false, 2, 6>},
-        {k_cert_rows<true, 4, 4>, k_cert_rows<true, 3, 4>, k_cert_rows<true, 3, 5>,
-         k_cert_rows<true, 4, 5>, k_cert_rows<true, 2, 6>}};
-    const bool rows = variant >= 4;
-    const CertFn layer_fn = rows ? row_fns[disc ? 1 : 0][variant - 4] : fns[disc ? 1 : 0][variant];
-    const void* fn = reinterpret_cast<const void*>(layer_fn);
-    if (!rows) raise_smem_limit(fn, sp->device, smem);
-    int per_sm = 0;
-    VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, rows ? 256 : wpb * 32,
-                                                           rows ? 0 : smem));
     if (sp->implicit) { // implicit-CSR form: keys + rank tables; the fallback runs at collect
         CertImplArgs c{};
         c.values_out = sp->v[0].p;
@@ -1236,6 +1112,13 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
         return;
     }
     if (!capturing) raise(VCS_EINVAL, "the certified solve is only recorded into a CUDA graph");
+    // explicit CSR: k_cert_rows, a thread per row, 4 edges in flight, 4 blocks per SM (C4:
+    // 0.75 ms; a warp-cooperative form that staged q pairs in shared memory measured 0.83 ms,
+    // more resident warps thrash L1)
+    const void* fn = disc ? reinterpret_cast<const void*>(k_cert_rows<true, 4, 4>)
+                          : reinterpret_cast<const void*>(k_cert_rows<false, 4, 4>);
+    int per_sm = 0;
+    VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
     CertArgs a{};
     a.row_ptr = sp->row_ptr.p;
     a.succ = sp->succ.p;
@@ -1244,7 +1127,6 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
     a.values_out = sp->v[0].p;
     a.act_out = sp->actions_dev.p;
     a.lb = sp->cert_lb.p;
-    a.qcap = qcap;
     a.discount = key.discount;
     int launches = 0;
     for (int t = H - 1; t >= 0; --t) {
@@ -1255,12 +1137,13 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
         a.xd_next = sp->cert_xd.p + a.next_row0;
         a.xd_cur = sp->cert_xd.p + a.row0;
         if (a.n) {
-            const uint64_t warps = (a.n + 31) / 32;
-            const int threads = rows ? 256 : wpb * 32;
             const uint64_t blocks = std::max<uint64_t>(
-                1, std::min<uint64_t>((warps * 32 + threads - 1) / threads,
+                1, std::min<uint64_t>((a.n + 255) / 256,
                                       static_cast<uint64_t>(std::max(1, per_sm)) * sp->num_sms));
-            layer_fn<<<static_cast<unsigned>(blocks), threads, rows ? 0 : smem, s>>>(a);
+            if (disc)
+                k_cert_rows<true, 4, 4><<<static_cast<unsigned>(blocks), 256, 0, s>>>(a);
+            else
+                k_cert_rows<false, 4, 4><<<static_cast<unsigned>(blocks), 256, 0, s>>>(a);
             VCS_LAUNCHED();
             ++launches;
         }

@@ -396,14 +396,19 @@ def test_shard_kernels_emulated_ranks(gpu, oracle):
             assert np.array_equal(actions, a_ref)
 
 
-def test_certified_proof_and_fallback(gpu, golden):
+@pytest.mark.parametrize("form", ["implicit", "explicit"])
+def test_certified_proof_and_fallback(gpu, golden, form, monkeypatch):
     """VCS_METHOD_CERTIFIED: the two-version backward pass is the whole solve exactly when its
     residual lower bounds prove K* = H+1; early stops and sweep caps must take the wavefront
-    fallback (graph IF node).  Bits equal the reference's digests either way."""
+    fallback (implicit form: at collect, after materialising the CSR; explicit form: the graph
+    IF node).  Bits equal the reference's digests either way."""
     import ctypes as C
     p = V.load_instance(str(GOLDEN / "canonical_instance.txt"))
     ni = V.NativeInstance(p.vcc, bots=p.bots)
+    if form == "explicit":
+        monkeypatch.setenv("VCS_BUILD_EXPLICIT", "1")
     sp = V.StateSpace.build_native(ni)
+    monkeypatch.delenv("VCS_BUILD_EXPLICIT", raising=False)
     H = sp.task_count()
 
     def run(eps, cap=0):
