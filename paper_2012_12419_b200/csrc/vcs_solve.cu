@@ -20,6 +20,7 @@
 #include "vcs_device.cuh"
 #include "vcs_keys.cuh"
 
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -742,24 +743,20 @@ struct CertImplArgs {
     double discount;
 };
 
-template <int WM, bool DISC, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_cert_implicit(CertImplArgs a) {
+// One layer of the implicit certified pass over states first_i, first_i + stride, ... (the
+// block has loaded the layer's LayerParam into sL and zeroed s_lb).
+template <int WM, bool DISC>
+__device__ __forceinline__ void cert_implicit_layer(const CertImplArgs& a, const LayerParam& L,
+                                                    unsigned long long& s_lb, uint64_t first_i,
+                                                    uint64_t stride) {
     constexpr unsigned FULL = 0xffffffffu;
     constexpr int SL = kDenseSlots;
-    __shared__ LayerParam sL;
-    __shared__ unsigned long long s_lb;
-    for (int i = threadIdx.x; i < static_cast<int>(sizeof(LayerParam) / 4); i += blockDim.x)
-        reinterpret_cast<uint32_t*>(&sL)[i] = __ldg(reinterpret_cast<const uint32_t*>(a.L) + i);
-    if (threadIdx.x == 0) s_lb = 0ull;
-    __syncthreads();
-    const LayerParam& L = sL;
     const bool retires = L.n_keep != L.n_active;
     const SlotDecoder<WM> dec(L); // the layer's slot constants, in registers
     const int words = L.words;
     const double r_cloud = L.r_cloud_kept, r_paid = L.r_paid_kept;
     double dmax = 0.0;
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    uint64_t i = first_i;
     uint64_t kn[WM] = {}; // the next state's key, loaded while the current state computes
     if (i < a.n) load_key<WM>(a.keys + i * static_cast<uint64_t>(words), words, kn);
     for (; i < a.n; i += stride) {
@@ -808,6 +805,27 @@ __global__ void __launch_bounds__(256, MINB) k_cert_implicit(CertImplArgs a) {
     __syncthreads();
     if (threadIdx.x == 0 && s_lb)
         atomicMax(reinterpret_cast<unsigned long long*>(a.lb + a.m), s_lb);
+}
+
+__device__ __forceinline__ void load_layer_param(LayerParam& sL, const LayerParam* src,
+                                                 unsigned long long& s_lb) {
+    __syncthreads(); // the previous layer's readers of sL are done
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(LayerParam) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t*>(&sL)[i] = __ldg(reinterpret_cast<const uint32_t*>(src) + i);
+    if (threadIdx.x == 0) s_lb = 0ull;
+    __syncthreads();
+}
+
+// One launch per layer.  (A single cooperative launch over all layers with a grid sync between
+// them measured slower, 0.86 vs 0.66 ms on C4: every sync waits for the slowest block.)
+template <int WM, bool DISC, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_cert_implicit(CertImplArgs a) {
+    __shared__ LayerParam sL;
+    __shared__ unsigned long long s_lb;
+    load_layer_param(sL, a.L, s_lb);
+    cert_implicit_layer<WM, DISC>(a, sL, s_lb,
+                                  static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x,
+                                  static_cast<uint64_t>(gridDim.x) * blockDim.x);
 }
 
 // K* = H+1 is proven iff lb_k >= eps for k = 1..H (and no sweep cap below H+1).  Sets the graph
