@@ -270,6 +270,35 @@ def e2e_sharded(args, ni, local, dev, stream, opts, sharding, S, rank):
                     "D2H of the rank's own rows", "steps": len(times)}
 
 
+def full_work_methods(space, args, stream):
+    """The same solve by the methods that compute every Jacobi iterate (no certificate): the
+    layer wavefront (all truncation horizons) and layer-skipping Jacobi sweeps — device time per
+    solve, same bits (tests/test_gpu_solver.py)."""
+    from paper_2012_12419_b200 import _native as N
+    import torch
+    out = {}
+    h = C.c_void_p(stream.cuda_stream)
+    for name, m in (("layer_wavefront", N.VCS_METHOD_WAVEFRONT), ("jacobi_layer_skip", N.VCS_METHOD_JACOBI)):
+        opts = N.vcs_solve_opts(args.eps, 1, 0, 1.0, m)
+        for _ in range(2):
+            N.check(N.lib().vcs_solve_enqueue(space.handle, C.byref(opts), h))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        steps = 5
+        e0.record(stream)
+        for _ in range(steps):
+            N.check(N.lib().vcs_solve_enqueue(space.handle, C.byref(opts), h))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        rep = N.vcs_solve_report()
+        N.check(N.lib().vcs_solve_collect(space.handle, None, None, C.byref(rep), h))
+        ms = e0.elapsed_time(e1) / steps
+        out[name] = {"ms_per_solve": ms, "sweeps": rep.sweeps,
+                     "backups_per_s": space.size() * rep.sweeps / (ms * 1e-3),
+                     "backups_performed": rep.backups_done}
+    return out
+
+
 def greedy_c2(V, N):
     """BASELINE configs[1] beside the headline: greedy first-fit placement of 10^5 tasks over
     10^3 clouds through the C ABI from host SoA arrays to host placements
@@ -549,6 +578,8 @@ def run_b200(args):
         "clocks": sampler.summary(),
         "gpu_launches": int(launches),
     }
+    if not sharded_path and not args.no_alt and method == N.VCS_METHOD_CERTIFIED:
+        line["full_work_methods"] = full_work_methods(space, args, stream)
     if rank == 0 and not args.no_greedy:
         line["greedy"] = greedy_c2(V, N)
     if world == 1 and not args.no_cpu_baseline and rank == 0:
@@ -579,6 +610,8 @@ def main():
                          "when the version store fits in HBM, else Jacobi)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-greedy", action="store_true", help="skip the C2 greedy side number")
+    ap.add_argument("--no-alt", action="store_true",
+                    help="skip the full-work (wavefront / Jacobi) side numbers")
     ap.add_argument("--sharding", choices=["auto", "instances", "wave", "halo", "allgather"],
                     default="auto",
                     help="auto: single GPU at N=1, independent instances (one per GPU) at N>1; "
