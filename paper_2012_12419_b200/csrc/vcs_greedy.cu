@@ -160,6 +160,8 @@ __global__ void __launch_bounds__(32) k_first_fit(const GreedyDesc* __restrict__
 // registers (lane j%32 keeps task j's) and stored 32 at a time, coalesced.
 constexpr int kFastLevels = 8;
 
+// NL >= every instance's distinct-demand count (the level loops are unrolled to NL)
+template <int NL>
 __global__ void __launch_bounds__(32) k_first_fit_fast(const GreedyDesc* __restrict__ descs) {
     extern __shared__ int32_t sm[];
     const GreedyDesc D = descs[blockIdx.x];
@@ -167,10 +169,10 @@ __global__ void __launch_bounds__(32) k_first_fit_fast(const GreedyDesc* __restr
     int32_t* fr = sm; // free counts, word-major: cloud c at fr[c]
     for (int c = lane; c < D.K; c += 32) fr[c] = D.free_vms[c];
     __syncwarp();
-    int lvl[kFastLevels];
-    uint32_t capw[kFastLevels];
+    int lvl[NL];
+    uint32_t capw[NL];
 #pragma unroll
-    for (int L = 0; L < kFastLevels; ++L) {
+    for (int L = 0; L < NL; ++L) {
         lvl[L] = L < D.n_levels ? D.levels[L] : 0x7fffffff;
         uint32_t bits = 0;
         if (L < D.n_levels)
@@ -181,7 +183,7 @@ __global__ void __launch_bounds__(32) k_first_fit_fast(const GreedyDesc* __restr
         capw[L] = bits;
     }
     long long paid = 0;
-    int my_target = -1;
+    __shared__ int32_t s_tgt[32];
     uint32_t cur[kPrefetch], nxt[kPrefetch];
     int2 tcur[kPrefetch], tnxt[kPrefetch];
 #pragma unroll
@@ -203,10 +205,11 @@ __global__ void __launch_bounds__(32) k_first_fit_fast(const GreedyDesc* __restr
                 const int level = tcur[u].x, d = tcur[u].y;
                 uint32_t c = 0;
 #pragma unroll
-                for (int L = 0; L < kFastLevels; ++L) c = L == level ? capw[L] : c;
+                for (int L = 0; L < NL; ++L) c = L == level ? capw[L] : c;
                 const uint32_t m = cur[u] & c;
                 const uint32_t any = __ballot_sync(0xffffffffu, m != 0);
-                int winner = -1;
+                // the winner is recorded by the owning lane in shared memory (no shuffle on the
+                // task chain); the group of 32 targets is written out coalesced
                 if (any) {
                     const int src = __ffs(any) - 1;
                     if (lane == src) { // the owning lane updates its free count and bits
@@ -216,16 +219,19 @@ __global__ void __launch_bounds__(32) k_first_fit_fast(const GreedyDesc* __restr
                         fr[cloud] = f;
                         const uint32_t bit = 1u << b;
 #pragma unroll
-                        for (int L = 0; L < kFastLevels; ++L)
+                        for (int L = 0; L < NL; ++L)
                             capw[L] = f >= lvl[L] ? (capw[L] | bit) : (capw[L] & ~bit);
-                        winner = cloud;
+                        s_tgt[j & 31] = cloud;
                     }
-                    winner = __shfl_sync(0xffffffffu, winner, src);
                 } else {
                     paid += d;
+                    if (lane == 0) s_tgt[j & 31] = -1;
                 }
-                if (lane == (j & 31)) my_target = winner;
-                if ((j & 31) == 31) D.target[j - 31 + lane] = my_target;
+                if ((j & 31) == 31) {
+                    __syncwarp();
+                    D.target[j - 31 + lane] = s_tgt[lane];
+                    __syncwarp();
+                }
             }
         }
 #pragma unroll
@@ -235,7 +241,8 @@ __global__ void __launch_bounds__(32) k_first_fit_fast(const GreedyDesc* __restr
         }
     }
     const int tail = D.T & 31; // the last partial group of 32 targets
-    if (tail && lane < tail) D.target[D.T - tail + lane] = my_target;
+    __syncwarp();
+    if (tail && lane < tail) D.target[D.T - tail + lane] = s_tgt[lane];
     __syncwarp();
     for (int c = lane; c < D.K; c += 32) D.free_vms[c] = fr[c];
     if (lane == 0) *D.paid = paid;
@@ -328,12 +335,19 @@ bool fast_path(const HostGreedy& h) {
 }
 
 void launch_first_fit(const GreedyDesc* d_descs, int n, size_t smem, bool fast, size_t max_k,
-                      cudaStream_t s) {
+                      int max_levels, cudaStream_t s) {
     if (fast) {
         const size_t fs = std::max<size_t>(max_k * 4, 4);
-        VCS_CUDA(cudaFuncSetAttribute(k_first_fit_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(fs)));
-        k_first_fit_fast<<<n, 32, fs, s>>>(d_descs);
+        auto go = [&](auto kern) {
+            VCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(fs)));
+            kern<<<n, 32, fs, s>>>(d_descs);
+        };
+        if (max_levels <= 1) go(k_first_fit_fast<1>);
+        else if (max_levels <= 2) go(k_first_fit_fast<2>);
+        else if (max_levels <= 3) go(k_first_fit_fast<3>);
+        else if (max_levels <= 4) go(k_first_fit_fast<4>);
+        else go(k_first_fit_fast<kFastLevels>);
     } else {
         VCS_CUDA(cudaFuncSetAttribute(k_first_fit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(std::max<size_t>(smem, 1))));
@@ -368,7 +382,8 @@ int vcs_greedy(const vcs_instance* in, int device, int32_t* target_per_task,
         dd.exact(1, s);
         const vcs::GreedyDesc desc = vcs::desc_of(h, g);
         VCS_CUDA(cudaMemcpyAsync(dd.p, &desc, sizeof desc, cudaMemcpyHostToDevice, s));
-        vcs::launch_first_fit(dd.p, 1, h.smem, vcs::fast_path(h), static_cast<size_t>(h.K), s);
+        vcs::launch_first_fit(dd.p, 1, h.smem, vcs::fast_path(h), static_cast<size_t>(h.K),
+                              h.n_levels, s);
         std::vector<int32_t> free_out(static_cast<size_t>(h.K));
         long long p = 0;
         if (h.T)
@@ -408,6 +423,7 @@ int vcs_greedy_batch(int32_t n, const vcs_instance* insts, int device, int32_t**
         std::vector<vcs::GreedyDesc> descs;
         size_t smem = 4, max_k = 1;
         bool fast = true;
+        int max_levels = 1;
         const int sms = vcs::sm_count(device);
         for (int i = 0; i < n; ++i) {
             hs.push_back(vcs::plan_greedy(&insts[i]));
@@ -418,12 +434,13 @@ int vcs_greedy_batch(int32_t n, const vcs_instance* insts, int device, int32_t**
             smem = std::max(smem, hs.back().smem);
             max_k = std::max(max_k, static_cast<size_t>(hs.back().K));
             fast = fast && vcs::fast_path(hs.back());
+            max_levels = std::max(max_levels, hs.back().n_levels);
         }
         vcs::DevBuf<vcs::GreedyDesc> dd;
         dd.exact(static_cast<size_t>(n), s);
         VCS_CUDA(cudaMemcpyAsync(dd.p, descs.data(), descs.size() * sizeof(vcs::GreedyDesc),
                                  cudaMemcpyHostToDevice, s));
-        vcs::launch_first_fit(dd.p, n, smem, fast, max_k, s);
+        vcs::launch_first_fit(dd.p, n, smem, fast, max_k, max_levels, s);
         std::vector<std::vector<int32_t>> frees(static_cast<size_t>(n));
         std::vector<long long> ps(static_cast<size_t>(n), 0);
         for (int i = 0; i < n; ++i) {
