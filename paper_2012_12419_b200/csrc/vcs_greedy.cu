@@ -248,6 +248,185 @@ __global__ void __launch_bounds__(32) k_first_fit_fast(const GreedyDesc* __restr
     if (lane == 0) *D.paid = paid;
 }
 
+// Speculative chunked form of the fast path (the default): 32 tasks per step instead of one.
+// Every task of the chunk [j0, j0+32) takes its candidate = first feasible cloud under the
+// capacity state S0 at the chunk start (32 independent AND -> ballot -> ffs, pipelined).  Free
+// counts only decrease, so under the sequential state S_u of task u the feasible set is a subset
+// of S0's: the true answer is >= the candidate and EQUALS it iff the candidate still fits,
+// i.e. S0[c] >= inclusive prefix of demands of the chunk's tasks with the same candidate (a
+// task without a candidate stays without one: paid).  The chunk commits tasks up to the first
+// that fails this test and the next chunk starts there.  A failure leaves its candidate cloud
+// with free < that task's demand, clearing a capacity bit for good, so there are at most
+// K x n_levels failures: at most T/32 + K*n_levels steps for any input.  Same placements as the
+// one-task-per-step scan (greedy.cpp:5-30 order), bit for bit.
+// mbarrier + 1-D bulk copy (TMA) helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile("{\n\t.reg .pred p;\n"
+                 "WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+                 "r"(parity)
+                 : "memory");
+}
+
+constexpr int kRingBlocks = 4; // 32-row blocks of attribute rows staged in shared memory
+
+// Speculative first-fit, one warp per instance (see the comment above k_first_fit_fast for the
+// layout).  The attribute rows and task descriptors (padded to whole 32-row blocks) stream
+// into a 4-block shared-memory ring by 1-D bulk copies, two blocks ahead of the chunk.
+template <int NL>
+__global__ void __launch_bounds__(32) k_first_fit_spec(const GreedyDesc* __restrict__ descs) {
+    extern __shared__ int32_t sm[];
+    constexpr int kRing = kRingBlocks * 32;
+    __shared__ __align__(128) uint32_t s_rows[kRing * 32]; // row j at (j % kRing) * W
+    __shared__ __align__(16) int2 s_task[kRing];
+    __shared__ __align__(8) uint64_t s_bar[kRingBlocks];
+    __shared__ uint32_t s_cap[NL][32]; // word w of level L: bit b = (free[32w+b] >= lvl[L])
+    __shared__ __align__(16) uint32_t s_any[32]; // ballot of each task of the chunk
+    const GreedyDesc D = descs[blockIdx.x];
+    const int lane = threadIdx.x;
+    constexpr uint32_t kAll = 0xffffffffu;
+    if (D.T == 0) {
+        if (lane == 0) *D.paid = 0;
+        return;
+    }
+    const int W = D.W;
+    const int n_blocks = (D.T + 31) >> 5;
+    if (lane == 0) {
+        for (int k = 0; k < kRingBlocks; ++k) bar_init(&s_bar[k], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    int32_t* fr = sm; // free counts, cloud c at fr[c]
+    for (int c = lane; c < D.K; c += 32) fr[c] = D.free_vms[c];
+    // a chunk near the end reads ring rows past the last block: their (stale) levels must still
+    // index s_cap, their ballots belong to tasks past T and are never used
+    for (int r = lane; r < kRing; r += 32) s_task[r] = make_int2(0, 0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    int lvl[NL];
+#pragma unroll
+    for (int L = 0; L < NL; ++L) {
+        lvl[L] = L < D.n_levels ? D.levels[L] : 0x7fffffff;
+        uint32_t bits = 0;
+        if (L < D.n_levels)
+            for (int b = 0; b < 32; ++b) {
+                const int c = lane * 32 + b;
+                if (c < D.K && fr[c] >= lvl[L]) bits |= 1u << b;
+            }
+        s_cap[L][lane] = bits;
+    }
+    const uint32_t le = (2u << lane) - 1u; // lanes <= this one
+    const uint32_t wmask = lane < W ? kAll : 0u;
+    int issued = 0, ready = 0;
+    auto issue = [&]() { // block `issued` into its ring slot (lane 0)
+        const int slot = issued & (kRingBlocks - 1);
+        const uint32_t row_bytes = 32u * static_cast<uint32_t>(W) * 4u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); // earlier reads of the slot
+        bar_expect_tx(&s_bar[slot], row_bytes + 32u * 8u);
+        bulk_g2s(&s_rows[slot * 32 * W], D.mask + static_cast<size_t>(issued) * 32 * W, row_bytes, &s_bar[slot]);
+        bulk_g2s(&s_task[slot * 32], D.task + static_cast<size_t>(issued) * 32, 32u * 8u, &s_bar[slot]);
+        ++issued;
+    };
+    long long paid = 0;
+    for (int j0 = 0; j0 < D.T;) {
+        const int n = min(32, D.T - j0);
+        const int b0 = j0 >> 5;
+        // the ring holds blocks b0..b0+3; the chunk needs b0 and b0+1
+        if (lane == 0)
+            while (issued < b0 + kRingBlocks && issued < n_blocks) issue();
+        const int need = min(b0 + 1, n_blocks - 1);
+        while (ready <= need) {
+            bar_wait(&s_bar[ready & (kRingBlocks - 1)], (ready / kRingBlocks) & 1);
+            ++ready;
+        }
+        __syncwarp();
+        uint32_t any[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) { // 32 independent evaluations against the chunk-start state
+            const int r = (j0 + u) & (kRing - 1);
+            const uint32_t cw = s_cap[s_task[r].x][lane]; // padding rows: level 0, zero words
+            // branch-free and store-free (a branch region or a shared store per task would
+            // serialise the unrolled chains): lanes past W read inside the ring, masked off
+            const uint32_t m = s_rows[r * W + lane] & cw & wmask;
+            any[u] = __ballot_sync(kAll, m != 0);
+        }
+        if (lane == 0) {
+            uint4* dst = reinterpret_cast<uint4*>(s_any);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                dst[q] = make_uint4(any[4 * q], any[4 * q + 1], any[4 * q + 2], any[4 * q + 3]);
+        }
+        __syncwarp();
+        // lane u resolves task j0+u: the lowest lane with a feasible cloud, its lowest bit
+        const int rme = (j0 + lane) & (kRing - 1);
+        const int2 tk = s_task[rme];
+        const int lvme = lane < n ? tk.x : NL;
+        int my_c = -1;
+        {
+            const uint32_t any = s_any[lane];
+            if (lane < n && any) {
+                const int src = __ffs(any) - 1;
+                const uint32_t m = s_rows[rme * W + src] & s_cap[lvme][src];
+                my_c = src * 32 + __ffs(m) - 1;
+            }
+        }
+        const bool placed = my_c >= 0;
+        // same-candidate groups and the inclusive prefix of their demands (levels: popcounts)
+        const uint32_t peers = __match_any_sync(kAll, placed ? my_c : -1 - lane);
+        int pre = 0;
+#pragma unroll
+        for (int L = 0; L < NL; ++L)
+            if (L < D.n_levels) pre += lvl[L] * __popc(peers & le & __ballot_sync(kAll, lvme == L));
+        const int f0 = placed ? fr[my_c] : 0;
+        const uint32_t fails = __ballot_sync(kAll, placed && f0 < pre);
+        const int ncommit = fails ? __ffs(fails) - 1 : n; // >= 1: the first task fits S0
+        const uint32_t cmask = ncommit >= 32 ? kAll : ((1u << ncommit) - 1u);
+        const bool commit = lane < ncommit;
+        __syncwarp(); // every lane has read the chunk-start capacity words
+        // the last committed member of each group writes its cloud's new free count and clears
+        // the capacity bits the cloud lost
+        if (placed && commit && !(peers & cmask & ~le)) {
+            const int f1 = f0 - pre;
+            fr[my_c] = f1;
+            const uint32_t keep = ~(1u << (my_c & 31));
+#pragma unroll
+            for (int L = 0; L < NL; ++L)
+                if (f1 < lvl[L]) atomicAnd(&s_cap[L][my_c >> 5], keep);
+        }
+        if (commit) {
+            D.target[j0 + lane] = my_c;
+            if (!placed) paid += tk.y;
+        }
+        __syncwarp();
+        j0 += ncommit;
+    }
+    while (ready < issued) { // drain the bulk copies still in flight
+        bar_wait(&s_bar[ready & (kRingBlocks - 1)], (ready / kRingBlocks) & 1);
+        ++ready;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) paid += __shfl_xor_sync(kAll, paid, o);
+    __syncwarp();
+    for (int c = lane; c < D.K; c += 32) D.free_vms[c] = fr[c];
+    if (lane == 0) *D.paid = paid;
+}
+
 struct HostGreedy {
     int K, T, W, n_levels;
     std::vector<int2> task;
@@ -295,8 +474,13 @@ void stage(const vcs_instance* in, const HostGreedy& h, GreedyDev& g, cudaStream
     g.c_thr.exact(K, s);
     g.t_delay.exact(T, s);
     g.t_thr.exact(T, s);
-    g.mask.exact(T * static_cast<size_t>(h.W), s);
-    g.task.exact(T, s);
+    const size_t T_pad = (T + 31) / 32 * 32; // whole 32-row blocks (the bulk copies of k_first_fit_spec)
+    g.mask.exact(std::max<size_t>(T_pad, 1) * static_cast<size_t>(h.W), s);
+    g.task.exact(std::max<size_t>(T_pad, 1), s);
+    if (T_pad > T) {
+        VCS_CUDA(cudaMemsetAsync(g.mask.p + T * h.W, 0, (T_pad - T) * h.W * 4, s));
+        VCS_CUDA(cudaMemsetAsync(g.task.p + T, 0, (T_pad - T) * sizeof(int2), s));
+    }
     g.levels.exact(std::max<size_t>(1, h.levels.size()), s);
     g.free_vms.exact(K, s);
     g.target.exact(T, s);
@@ -343,11 +527,20 @@ void launch_first_fit(const GreedyDesc* d_descs, int n, size_t smem, bool fast, 
                                           static_cast<int>(fs)));
             kern<<<n, 32, fs, s>>>(d_descs);
         };
-        if (max_levels <= 1) go(k_first_fit_fast<1>);
-        else if (max_levels <= 2) go(k_first_fit_fast<2>);
-        else if (max_levels <= 3) go(k_first_fit_fast<3>);
-        else if (max_levels <= 4) go(k_first_fit_fast<4>);
-        else go(k_first_fit_fast<kFastLevels>);
+        static const bool serial = std::getenv("VCS_GREEDY_SERIAL") != nullptr;
+        if (serial) {
+            if (max_levels <= 1) go(k_first_fit_fast<1>);
+            else if (max_levels <= 2) go(k_first_fit_fast<2>);
+            else if (max_levels <= 3) go(k_first_fit_fast<3>);
+            else if (max_levels <= 4) go(k_first_fit_fast<4>);
+            else go(k_first_fit_fast<kFastLevels>);
+        } else {
+            if (max_levels <= 1) go(k_first_fit_spec<1>);
+            else if (max_levels <= 2) go(k_first_fit_spec<2>);
+            else if (max_levels <= 3) go(k_first_fit_spec<3>);
+            else if (max_levels <= 4) go(k_first_fit_spec<4>);
+            else go(k_first_fit_spec<kFastLevels>);
+        }
     } else {
         VCS_CUDA(cudaFuncSetAttribute(k_first_fit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(std::max<size_t>(smem, 1))));
