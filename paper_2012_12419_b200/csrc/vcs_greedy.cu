@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(32) k_first_fit_spec(const GreedyDesc* __restr
     auto issue = [&]() { // block `issued` into its ring slot (lane 0)
         const int slot = issued & (kRingBlocks - 1);
         const uint32_t row_bytes = 32u * static_cast<uint32_t>(W) * 4u;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); // earlier reads of the slot
+        // (the slot's earlier shared reads were consumed before this point: no proxy fence)
         bar_expect_tx(&s_bar[slot], row_bytes + 32u * 8u);
         bulk_g2s(&s_rows[slot * 32 * W], D.mask + static_cast<size_t>(issued) * 32 * W, row_bytes, &s_bar[slot]);
         bulk_g2s(&s_task[slot * 32], D.task + static_cast<size_t>(issued) * 32, 32u * 8u, &s_bar[slot]);
@@ -387,28 +387,45 @@ __global__ void __launch_bounds__(32) k_first_fit_spec(const GreedyDesc* __restr
             }
         }
         const bool placed = my_c >= 0;
-        // same-candidate groups and the inclusive prefix of their demands (levels: popcounts)
-        const uint32_t peers = __match_any_sync(kAll, placed ? my_c : -1 - lane);
-        int pre = 0;
+        int ncommit = n;
+        // common case first: take every placed demand off its candidate's free count.  The totals
+        // do not depend on the order, and every inclusive prefix fits iff no count went negative.
+        if (placed) atomicAdd(&fr[my_c], -tk.y);
+        __syncwarp();
+        const int fend = placed ? fr[my_c] : 0;
+        if (!__any_sync(kAll, fend < 0)) {
+            if (placed) { // clear the capacity bits the cloud lost (idempotent across its group)
+                const uint32_t keep = ~(1u << (my_c & 31));
 #pragma unroll
-        for (int L = 0; L < NL; ++L)
-            if (L < D.n_levels) pre += lvl[L] * __popc(peers & le & __ballot_sync(kAll, lvme == L));
-        const int f0 = placed ? fr[my_c] : 0;
-        const uint32_t fails = __ballot_sync(kAll, placed && f0 < pre);
-        const int ncommit = fails ? __ffs(fails) - 1 : n; // >= 1: the first task fits S0
-        const uint32_t cmask = ncommit >= 32 ? kAll : ((1u << ncommit) - 1u);
-        const bool commit = lane < ncommit;
-        __syncwarp(); // every lane has read the chunk-start capacity words
-        // the last committed member of each group writes its cloud's new free count and clears
-        // the capacity bits the cloud lost
-        if (placed && commit && !(peers & cmask & ~le)) {
-            const int f1 = f0 - pre;
-            fr[my_c] = f1;
-            const uint32_t keep = ~(1u << (my_c & 31));
+                for (int L = 0; L < NL; ++L)
+                    if (fend < lvl[L]) atomicAnd(&s_cap[L][my_c >> 5], keep);
+            }
+        } else {
+            if (placed) atomicAdd(&fr[my_c], tk.y); // undo; commit the exact prefix instead
+            __syncwarp();
+            // same-candidate groups and the inclusive prefix of their demands (levels: popcounts)
+            const uint32_t peers = __match_any_sync(kAll, placed ? my_c : -1 - lane);
+            int pre = 0;
 #pragma unroll
             for (int L = 0; L < NL; ++L)
-                if (f1 < lvl[L]) atomicAnd(&s_cap[L][my_c >> 5], keep);
+                if (L < D.n_levels) pre += lvl[L] * __popc(peers & le & __ballot_sync(kAll, lvme == L));
+            const int f0 = placed ? fr[my_c] : 0;
+            const uint32_t fails = __ballot_sync(kAll, placed && f0 < pre);
+            ncommit = __ffs(fails) - 1; // >= 1: the first task fits S0
+            const uint32_t cmask = (1u << ncommit) - 1u;
+            __syncwarp();
+            // the last committed member of each group writes its cloud's new free count and
+            // clears the capacity bits the cloud lost
+            if (placed && lane < ncommit && !(peers & cmask & ~le)) {
+                const int f1 = f0 - pre;
+                fr[my_c] = f1;
+                const uint32_t keep = ~(1u << (my_c & 31));
+#pragma unroll
+                for (int L = 0; L < NL; ++L)
+                    if (f1 < lvl[L]) atomicAnd(&s_cap[L][my_c >> 5], keep);
+            }
         }
+        const bool commit = lane < ncommit;
         if (commit) {
             D.target[j0 + lane] = my_c;
             if (!placed) paid += tk.y;
