@@ -14,7 +14,7 @@
 #include "vcs_device.cuh"
 
 #include <algorithm>
-#include <set>
+#include <cstdio>
 
 namespace vcs {
 
@@ -33,9 +33,13 @@ struct GreedyDesc {
     long long* paid;           // 1
 };
 
+// Also writes each task's descriptor {level index, demand} (levels: the n_levels distinct
+// demands, ascending; n_levels == 0: level 0).
 __global__ void k_attr_mask(int32_t K, int32_t T, int32_t W, const double* __restrict__ c_delay,
                             const double* __restrict__ c_thr, const double* __restrict__ t_delay,
-                            const double* __restrict__ t_thr, uint32_t* __restrict__ mask) {
+                            const double* __restrict__ t_thr, uint32_t* __restrict__ mask,
+                            const int32_t* __restrict__ demand, const int32_t* __restrict__ levels,
+                            int32_t n_levels, int2* __restrict__ task) {
     const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -48,6 +52,12 @@ __global__ void k_attr_mask(int32_t K, int32_t T, int32_t W, const double* __res
         if (c < K) ok = c_delay[c] <= t_delay[j] && c_thr[c] >= t_thr[j];
         const uint32_t bits = __ballot_sync(0xffffffffu, ok);
         if (lane == 0) mask[item] = bits;
+        if (w == 0 && lane == 1) {
+            const int32_t d = demand[j];
+            int level = 0;
+            while (level < n_levels && levels[level] != d) ++level;
+            task[j] = make_int2(n_levels ? level : 0, d);
+        }
     }
 }
 
@@ -446,7 +456,6 @@ __global__ void __launch_bounds__(32) k_first_fit_spec(const GreedyDesc* __restr
 
 struct HostGreedy {
     int K, T, W, n_levels;
-    std::vector<int2> task;
     std::vector<int32_t> levels;
     size_t smem;
 };
@@ -456,19 +465,36 @@ HostGreedy plan_greedy(const vcs_instance* in) {
     h.K = in->n_clouds;
     h.T = in->n_tasks;
     h.W = std::max(1, (h.K + 31) / 32);
-    std::set<int32_t> distinct(in->task_demand, in->task_demand + h.T);
-    if (static_cast<int>(distinct.size()) <= kMaxLevels) {
-        h.levels.assign(distinct.begin(), distinct.end());
-        h.n_levels = static_cast<int>(h.levels.size());
+    // distinct demands (at most kMaxLevels, else the generic capacity test).  Branch-free
+    // passes: min/max, then a 64-bit presence bitmap when the range allows it (random demands
+    // would mispredict a compare-per-task scan); otherwise a short table scan.
+    const int32_t* dem = in->task_demand;
+    std::vector<int32_t> lv;
+    bool small = true;
+    if (h.T) {
+        int32_t lo = dem[0], hi = dem[0];
+        for (int j = 1; j < h.T; ++j) {
+            lo = std::min(lo, dem[j]);
+            hi = std::max(hi, dem[j]);
+        }
+        if (static_cast<int64_t>(hi) - lo < 64) {
+            uint64_t bits = 0;
+            for (int j = 0; j < h.T; ++j) bits |= uint64_t(1) << (dem[j] - lo);
+            for (int b = 0; b < 64; ++b)
+                if (bits >> b & 1) lv.push_back(lo + b);
+            small = static_cast<int>(lv.size()) <= kMaxLevels;
+        } else {
+            for (int j = 0; j < h.T && small; ++j)
+                if (std::find(lv.begin(), lv.end(), dem[j]) == lv.end()) {
+                    lv.push_back(dem[j]);
+                    small = static_cast<int>(lv.size()) <= kMaxLevels;
+                }
+            std::sort(lv.begin(), lv.end());
+        }
     }
-    h.task.resize(static_cast<size_t>(h.T));
-    for (int j = 0; j < h.T; ++j) {
-        int level = 0;
-        if (h.n_levels)
-            level = static_cast<int>(std::lower_bound(h.levels.begin(), h.levels.end(),
-                                                      in->task_demand[j]) -
-                                     h.levels.begin());
-        h.task[static_cast<size_t>(j)] = make_int2(level, in->task_demand[j]);
+    if (small) {
+        h.levels = lv;
+        h.n_levels = static_cast<int>(lv.size());
     }
     h.smem = static_cast<size_t>(h.K) * 4 + static_cast<size_t>(h.n_levels) * h.W * 4;
     if (h.smem > 200 * 1024)
@@ -481,7 +507,7 @@ struct GreedyDev {
     DevBuf<double> c_delay, c_thr, t_delay, t_thr;
     DevBuf<uint32_t> mask;
     DevBuf<int2> task;
-    DevBuf<int32_t> levels, free_vms, target;
+    DevBuf<int32_t> demand, levels, free_vms, target;
     DevBuf<long long> paid;
 };
 
@@ -498,6 +524,7 @@ void stage(const vcs_instance* in, const HostGreedy& h, GreedyDev& g, cudaStream
         VCS_CUDA(cudaMemsetAsync(g.mask.p + T * h.W, 0, (T_pad - T) * h.W * 4, s));
         VCS_CUDA(cudaMemsetAsync(g.task.p + T, 0, (T_pad - T) * sizeof(int2), s));
     }
+    g.demand.exact(std::max<size_t>(T, 1), s);
     g.levels.exact(std::max<size_t>(1, h.levels.size()), s);
     g.free_vms.exact(K, s);
     g.target.exact(T, s);
@@ -510,7 +537,7 @@ void stage(const vcs_instance* in, const HostGreedy& h, GreedyDev& g, cudaStream
     if (T) {
         VCS_CUDA(cudaMemcpyAsync(g.t_delay.p, in->task_max_delay_ms, T * 8, cudaMemcpyHostToDevice, s));
         VCS_CUDA(cudaMemcpyAsync(g.t_thr.p, in->task_min_thr_kbps, T * 8, cudaMemcpyHostToDevice, s));
-        VCS_CUDA(cudaMemcpyAsync(g.task.p, h.task.data(), T * sizeof(int2), cudaMemcpyHostToDevice, s));
+        VCS_CUDA(cudaMemcpyAsync(g.demand.p, in->task_demand, T * 4, cudaMemcpyHostToDevice, s));
     }
     if (!h.levels.empty())
         VCS_CUDA(cudaMemcpyAsync(g.levels.p, h.levels.data(), h.levels.size() * 4,
@@ -522,7 +549,8 @@ void launch_mask(const HostGreedy& h, GreedyDev& g, int sms, cudaStream_t s) {
     const uint64_t items = static_cast<uint64_t>(h.T) * static_cast<uint64_t>(h.W);
     const uint64_t blocks = std::min<uint64_t>((items + 7) / 8, static_cast<uint64_t>(sms) * 16);
     k_attr_mask<<<static_cast<unsigned>(std::max<uint64_t>(1, blocks)), 256, 0, s>>>(
-        h.K, h.T, h.W, g.c_delay.p, g.c_thr.p, g.t_delay.p, g.t_thr.p, g.mask.p);
+        h.K, h.T, h.W, g.c_delay.p, g.c_thr.p, g.t_delay.p, g.t_thr.p, g.mask.p, g.demand.p,
+        g.levels.p, h.n_levels, g.task.p);
     VCS_LAUNCHED();
 }
 
@@ -578,7 +606,10 @@ int vcs_greedy(const vcs_instance* in, int device, int32_t* target_per_task,
                int64_t* per_cloud_used, int64_t* paid, int64_t* unused) {
     return guarded([&] {
         vcs::bind_device(device);
+        const bool tr = vcs::trace_enabled();
+        const double t0 = tr ? vcs::host_ms() : 0.0;
         const vcs::HostGreedy h = vcs::plan_greedy(in);
+        const double t1 = tr ? vcs::host_ms() : 0.0;
         cudaStream_t s = nullptr;
         VCS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
         struct StreamGuard {
@@ -594,6 +625,7 @@ int vcs_greedy(const vcs_instance* in, int device, int32_t* target_per_task,
         VCS_CUDA(cudaMemcpyAsync(dd.p, &desc, sizeof desc, cudaMemcpyHostToDevice, s));
         vcs::launch_first_fit(dd.p, 1, h.smem, vcs::fast_path(h), static_cast<size_t>(h.K),
                               h.n_levels, s);
+        const double t2 = tr ? vcs::host_ms() : 0.0;
         std::vector<int32_t> free_out(static_cast<size_t>(h.K));
         long long p = 0;
         if (h.T)
@@ -603,7 +635,12 @@ int vcs_greedy(const vcs_instance* in, int device, int32_t* target_per_task,
             VCS_CUDA(cudaMemcpyAsync(free_out.data(), g.free_vms.p, static_cast<size_t>(h.K) * 4,
                                      cudaMemcpyDeviceToHost, s));
         VCS_CUDA(cudaMemcpyAsync(&p, g.paid.p, sizeof p, cudaMemcpyDeviceToHost, s));
+        const double t3 = tr ? vcs::host_ms() : 0.0;
         VCS_CUDA(cudaStreamSynchronize(s));
+        const double t4 = tr ? vcs::host_ms() : 0.0;
+        if (tr)
+            std::fprintf(stderr, "[vcs] greedy T=%d K=%d: plan %.3f ms, stage+enqueue %.3f, d2h enqueue %.3f, sync %.3f\n",
+                         h.T, h.K, t1 - t0, t2 - t1, t3 - t2, t4 - t3);
         int64_t placed = 0, capacity = 0;
         for (int c = 0; c < h.K; ++c) {
             const int64_t used = static_cast<int64_t>(in->cloud_vm_free[c]) - free_out[c];
