@@ -40,19 +40,26 @@ __global__ void k_attr_mask(int32_t K, int32_t T, int32_t W, const double* __res
                             const double* __restrict__ t_thr, uint32_t* __restrict__ mask,
                             const int32_t* __restrict__ demand, const int32_t* __restrict__ levels,
                             int32_t n_levels, int2* __restrict__ task) {
-    const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    // one warp per task: a ballot per 32 clouds; lane w keeps word w of its group of 32 words
+    // and the group is stored coalesced
+    const int warp = static_cast<int>((static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+    const int n_warps = static_cast<int>((static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5);
     const int lane = threadIdx.x & 31;
-    const uint64_t total = static_cast<uint64_t>(T) * static_cast<uint64_t>(W);
-    for (uint64_t item = warp; item < total; item += n_warps) {
-        const uint64_t j = item / static_cast<uint64_t>(W);
-        const int w = static_cast<int>(item - j * static_cast<uint64_t>(W));
-        const int c = w * 32 + lane;
-        bool ok = false;
-        if (c < K) ok = c_delay[c] <= t_delay[j] && c_thr[c] >= t_thr[j];
-        const uint32_t bits = __ballot_sync(0xffffffffu, ok);
-        if (lane == 0) mask[item] = bits;
-        if (w == 0 && lane == 1) {
+    for (int j = warp; j < T; j += n_warps) {
+        const double td = __ldg(t_delay + j), tt = __ldg(t_thr + j);
+        uint32_t* row = mask + static_cast<size_t>(j) * W;
+        for (int w0 = 0; w0 < W; w0 += 32) {
+            uint32_t mine = 0;
+            const int nw = min(32, W - w0);
+            for (int w = 0; w < nw; ++w) {
+                const int c = (w0 + w) * 32 + lane;
+                const bool ok = c < K && __ldg(c_delay + c) <= td && __ldg(c_thr + c) >= tt;
+                const uint32_t bits = __ballot_sync(0xffffffffu, ok);
+                if (lane == w) mine = bits;
+            }
+            if (lane < nw) row[w0 + lane] = mine;
+        }
+        if (lane == 0) {
             const int32_t d = demand[j];
             int level = 0;
             while (level < n_levels && levels[level] != d) ++level;
@@ -546,8 +553,8 @@ void stage(const vcs_instance* in, const HostGreedy& h, GreedyDev& g, cudaStream
 
 void launch_mask(const HostGreedy& h, GreedyDev& g, int sms, cudaStream_t s) {
     if (!h.T) return;
-    const uint64_t items = static_cast<uint64_t>(h.T) * static_cast<uint64_t>(h.W);
-    const uint64_t blocks = std::min<uint64_t>((items + 7) / 8, static_cast<uint64_t>(sms) * 16);
+    const uint64_t blocks = std::min<uint64_t>((static_cast<uint64_t>(h.T) + 7) / 8,
+                                               static_cast<uint64_t>(sms) * 16);
     k_attr_mask<<<static_cast<unsigned>(std::max<uint64_t>(1, blocks)), 256, 0, s>>>(
         h.K, h.T, h.W, g.c_delay.p, g.c_thr.p, g.t_delay.p, g.t_thr.p, g.mask.p, g.demand.p,
         g.levels.p, h.n_levels, g.task.p);
