@@ -302,17 +302,22 @@ __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
                  : "memory");
 }
 
-constexpr int kRingBlocks = 4; // 32-row blocks of attribute rows staged in shared memory
+constexpr int kRingBlocks = 4;   // blocks of attribute rows staged in shared memory
+constexpr int kBlockRows = 128;  // rows per bulk copy (task arrays are padded to whole blocks)
+constexpr int kRingRows = kRingBlocks * kBlockRows;
+// dynamic shared memory of k_first_fit_spec: free counts, then the row ring, then the task ring
+__host__ __device__ constexpr size_t spec_free_bytes(size_t K) { return (K * 4 + 127) / 128 * 128; }
+__host__ __device__ constexpr size_t spec_smem_bytes(size_t K, size_t W) {
+    return spec_free_bytes(K) + kRingRows * W * 4 + kRingRows * 8;
+}
 
 // Speculative first-fit, one warp per instance (see the comment above k_first_fit_fast for the
 // layout).  The attribute rows and task descriptors (padded to whole 32-row blocks) stream
 // into a 4-block shared-memory ring by 1-D bulk copies, two blocks ahead of the chunk.
 template <int NL>
 __global__ void __launch_bounds__(32) k_first_fit_spec(const GreedyDesc* __restrict__ descs) {
-    extern __shared__ int32_t sm[];
-    constexpr int kRing = kRingBlocks * 32;
-    __shared__ __align__(128) uint32_t s_rows[kRing * 32]; // row j at (j % kRing) * W
-    __shared__ __align__(16) int2 s_task[kRing];
+    extern __shared__ __align__(128) int32_t sm[];
+    constexpr int kRing = kRingRows;
     __shared__ __align__(8) uint64_t s_bar[kRingBlocks];
     __shared__ uint32_t s_cap[NL][32]; // word w of level L: bit b = (free[32w+b] >= lvl[L])
     __shared__ __align__(16) uint32_t s_any[32]; // ballot of each task of the chunk
@@ -324,7 +329,9 @@ __global__ void __launch_bounds__(32) k_first_fit_spec(const GreedyDesc* __restr
         return;
     }
     const int W = D.W;
-    const int n_blocks = (D.T + 31) >> 5;
+    const int n_blocks = (D.T + kBlockRows - 1) / kBlockRows;
+    uint32_t* s_rows = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(sm) + spec_free_bytes(D.K)); // row j at (j % kRing) * W
+    int2* s_task = reinterpret_cast<int2*>(s_rows + static_cast<size_t>(kRing) * W);
     if (lane == 0) {
         for (int k = 0; k < kRingBlocks; ++k) bar_init(&s_bar[k], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -353,21 +360,23 @@ __global__ void __launch_bounds__(32) k_first_fit_spec(const GreedyDesc* __restr
     int issued = 0, ready = 0;
     auto issue = [&]() { // block `issued` into its ring slot (lane 0)
         const int slot = issued & (kRingBlocks - 1);
-        const uint32_t row_bytes = 32u * static_cast<uint32_t>(W) * 4u;
+        const uint32_t row_bytes = kBlockRows * static_cast<uint32_t>(W) * 4u;
         // (the slot's earlier shared reads were consumed before this point: no proxy fence)
-        bar_expect_tx(&s_bar[slot], row_bytes + 32u * 8u);
-        bulk_g2s(&s_rows[slot * 32 * W], D.mask + static_cast<size_t>(issued) * 32 * W, row_bytes, &s_bar[slot]);
-        bulk_g2s(&s_task[slot * 32], D.task + static_cast<size_t>(issued) * 32, 32u * 8u, &s_bar[slot]);
+        bar_expect_tx(&s_bar[slot], row_bytes + kBlockRows * 8u);
+        bulk_g2s(&s_rows[static_cast<size_t>(slot) * kBlockRows * W],
+                 D.mask + static_cast<size_t>(issued) * kBlockRows * W, row_bytes, &s_bar[slot]);
+        bulk_g2s(&s_task[slot * kBlockRows], D.task + static_cast<size_t>(issued) * kBlockRows,
+                 kBlockRows * 8u, &s_bar[slot]);
         ++issued;
     };
     long long paid = 0;
     for (int j0 = 0; j0 < D.T;) {
         const int n = min(32, D.T - j0);
-        const int b0 = j0 >> 5;
-        // the ring holds blocks b0..b0+3; the chunk needs b0 and b0+1
+        const int b0 = j0 / kBlockRows;
+        // the ring holds blocks b0..b0+3; the chunk needs the blocks of rows j0..j0+31
         if (lane == 0)
             while (issued < b0 + kRingBlocks && issued < n_blocks) issue();
-        const int need = min(b0 + 1, n_blocks - 1);
+        const int need = min((j0 + 31) / kBlockRows, n_blocks - 1);
         while (ready <= need) {
             bar_wait(&s_bar[ready & (kRingBlocks - 1)], (ready / kRingBlocks) & 1);
             ++ready;
@@ -524,7 +533,7 @@ void stage(const vcs_instance* in, const HostGreedy& h, GreedyDev& g, cudaStream
     g.c_thr.exact(K, s);
     g.t_delay.exact(T, s);
     g.t_thr.exact(T, s);
-    const size_t T_pad = (T + 31) / 32 * 32; // whole 32-row blocks (the bulk copies of k_first_fit_spec)
+    const size_t T_pad = (T + kBlockRows - 1) / kBlockRows * kBlockRows; // whole bulk-copy blocks
     g.mask.exact(std::max<size_t>(T_pad, 1) * static_cast<size_t>(h.W), s);
     g.task.exact(std::max<size_t>(T_pad, 1), s);
     if (T_pad > T) {
@@ -573,13 +582,13 @@ bool fast_path(const HostGreedy& h) {
 void launch_first_fit(const GreedyDesc* d_descs, int n, size_t smem, bool fast, size_t max_k,
                       int max_levels, cudaStream_t s) {
     if (fast) {
-        const size_t fs = std::max<size_t>(max_k * 4, 4);
+        static const bool serial = std::getenv("VCS_GREEDY_SERIAL") != nullptr;
+        const size_t fs = serial ? std::max<size_t>(max_k * 4, 4) : spec_smem_bytes(max_k, 32);
         auto go = [&](auto kern) {
             VCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(fs)));
             kern<<<n, 32, fs, s>>>(d_descs);
         };
-        static const bool serial = std::getenv("VCS_GREEDY_SERIAL") != nullptr;
         if (serial) {
             if (max_levels <= 1) go(k_first_fit_fast<1>);
             else if (max_levels <= 2) go(k_first_fit_fast<2>);
