@@ -305,10 +305,12 @@ __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
 constexpr int kRingBlocks = 4;   // blocks of attribute rows staged in shared memory
 constexpr int kBlockRows = 128;  // rows per bulk copy (task arrays are padded to whole blocks)
 constexpr int kRingRows = kRingBlocks * kBlockRows;
-// dynamic shared memory of k_first_fit_spec: free counts, then the row ring, then the task ring
+constexpr int kShadowRows = 32;  // ring rows 0..31 repeated past the end: a chunk never wraps
+// dynamic shared memory of k_first_fit_spec: free counts, then the row ring (32 words per row:
+// the fast path stores attribute rows at stride 32), then the task ring
 __host__ __device__ constexpr size_t spec_free_bytes(size_t K) { return (K * 4 + 127) / 128 * 128; }
-__host__ __device__ constexpr size_t spec_smem_bytes(size_t K, size_t W) {
-    return spec_free_bytes(K) + kRingRows * W * 4 + kRingRows * 8;
+__host__ __device__ constexpr size_t spec_smem_bytes(size_t K) {
+    return spec_free_bytes(K) + (kRingRows + kShadowRows) * (32 * 4 + 8);
 }
 
 // Speculative first-fit, one warp per instance (see the comment above k_first_fit_fast for the
@@ -328,10 +330,10 @@ __global__ void __launch_bounds__(32) k_first_fit_spec(const GreedyDesc* __restr
         if (lane == 0) *D.paid = 0;
         return;
     }
-    const int W = D.W;
+    constexpr int W = 32; // row stride of the fast path (words past ceil(K/32) are zero)
     const int n_blocks = (D.T + kBlockRows - 1) / kBlockRows;
     uint32_t* s_rows = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(sm) + spec_free_bytes(D.K)); // row j at (j % kRing) * W
-    int2* s_task = reinterpret_cast<int2*>(s_rows + static_cast<size_t>(kRing) * W);
+    int2* s_task = reinterpret_cast<int2*>(s_rows + static_cast<size_t>(kRing + kShadowRows) * W);
     if (lane == 0) {
         for (int k = 0; k < kRingBlocks; ++k) bar_init(&s_bar[k], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -340,7 +342,7 @@ __global__ void __launch_bounds__(32) k_first_fit_spec(const GreedyDesc* __restr
     for (int c = lane; c < D.K; c += 32) fr[c] = D.free_vms[c];
     // a chunk near the end reads ring rows past the last block: their (stale) levels must still
     // index s_cap, their ballots belong to tasks past T and are never used
-    for (int r = lane; r < kRing; r += 32) s_task[r] = make_int2(0, 0);
+    for (int r = lane; r < kRing + kShadowRows; r += 32) s_task[r] = make_int2(0, 0);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     int lvl[NL];
@@ -356,17 +358,21 @@ __global__ void __launch_bounds__(32) k_first_fit_spec(const GreedyDesc* __restr
         s_cap[L][lane] = bits;
     }
     const uint32_t le = (2u << lane) - 1u; // lanes <= this one
-    const uint32_t wmask = lane < W ? kAll : 0u;
     int issued = 0, ready = 0;
     auto issue = [&]() { // block `issued` into its ring slot (lane 0)
         const int slot = issued & (kRingBlocks - 1);
         const uint32_t row_bytes = kBlockRows * static_cast<uint32_t>(W) * 4u;
         // (the slot's earlier shared reads were consumed before this point: no proxy fence)
-        bar_expect_tx(&s_bar[slot], row_bytes + kBlockRows * 8u);
-        bulk_g2s(&s_rows[static_cast<size_t>(slot) * kBlockRows * W],
-                 D.mask + static_cast<size_t>(issued) * kBlockRows * W, row_bytes, &s_bar[slot]);
-        bulk_g2s(&s_task[slot * kBlockRows], D.task + static_cast<size_t>(issued) * kBlockRows,
-                 kBlockRows * 8u, &s_bar[slot]);
+        const uint32_t shadow = slot == 0 ? kShadowRows * (W * 4u + 8u) : 0u;
+        bar_expect_tx(&s_bar[slot], row_bytes + kBlockRows * 8u + shadow);
+        const uint32_t* src_rows = D.mask + static_cast<size_t>(issued) * kBlockRows * W;
+        const int2* src_task = D.task + static_cast<size_t>(issued) * kBlockRows;
+        bulk_g2s(&s_rows[static_cast<size_t>(slot) * kBlockRows * W], src_rows, row_bytes, &s_bar[slot]);
+        bulk_g2s(&s_task[slot * kBlockRows], src_task, kBlockRows * 8u, &s_bar[slot]);
+        if (slot == 0) { // the shadow copy of ring rows 0..31
+            bulk_g2s(&s_rows[static_cast<size_t>(kRing) * W], src_rows, kShadowRows * W * 4u, &s_bar[slot]);
+            bulk_g2s(&s_task[kRing], src_task, kShadowRows * 8u, &s_bar[slot]);
+        }
         ++issued;
     };
     long long paid = 0;
@@ -383,13 +389,14 @@ __global__ void __launch_bounds__(32) k_first_fit_spec(const GreedyDesc* __restr
         }
         __syncwarp();
         uint32_t any[32];
+        const int r0 = j0 & (kRing - 1); // rows r0..r0+31 are contiguous (shadow rows)
+        const uint32_t* rowp = s_rows + r0 * W + lane;
+        const int2* taskp = s_task + r0;
 #pragma unroll
         for (int u = 0; u < 32; ++u) { // 32 independent evaluations against the chunk-start state
-            const int r = (j0 + u) & (kRing - 1);
-            const uint32_t cw = s_cap[s_task[r].x][lane]; // padding rows: level 0, zero words
-            // branch-free and store-free (a branch region or a shared store per task would
-            // serialise the unrolled chains): lanes past W read inside the ring, masked off
-            const uint32_t m = s_rows[r * W + lane] & cw & wmask;
+            // branch-free and store-free: a branch region or a shared store per task would
+            // serialise the unrolled chains (padding rows: level 0, zero words)
+            const uint32_t m = rowp[u * W] & s_cap[taskp[u].x][lane];
             any[u] = __ballot_sync(kAll, m != 0);
         }
         if (lane == 0) {
@@ -512,6 +519,8 @@ HostGreedy plan_greedy(const vcs_instance* in) {
         h.levels = lv;
         h.n_levels = static_cast<int>(lv.size());
     }
+    if (h.W <= 32 && h.n_levels > 0 && h.n_levels <= kFastLevels)
+        h.W = 32; // fast path: attribute rows at stride 32 (zero words past ceil(K/32))
     h.smem = static_cast<size_t>(h.K) * 4 + static_cast<size_t>(h.n_levels) * h.W * 4;
     if (h.smem > 200 * 1024)
         raise(VCS_EINVAL, "too many clouds for the device first-fit (shared-memory bound)");
@@ -583,7 +592,7 @@ void launch_first_fit(const GreedyDesc* d_descs, int n, size_t smem, bool fast, 
                       int max_levels, cudaStream_t s) {
     if (fast) {
         static const bool serial = std::getenv("VCS_GREEDY_SERIAL") != nullptr;
-        const size_t fs = serial ? std::max<size_t>(max_k * 4, 4) : spec_smem_bytes(max_k, 32);
+        const size_t fs = serial ? std::max<size_t>(max_k * 4, 4) : spec_smem_bytes(max_k);
         auto go = [&](auto kern) {
             VCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(fs)));
