@@ -122,3 +122,25 @@ def test_batch_matches_single(gpu):
         r = V.greedy_schedule(None, None, native=ni)
         assert np.array_equal(outs[i][:ni.struct.n_tasks], r.target_index)
         assert (paid[i], unused[i]) == (r.paid_vms, r.unused_vms)
+
+
+@pytest.mark.parametrize("n_tasks,n_clouds,n_levels,cap_hi", [
+    (1, 1, 1, 2), (31, 7, 2, 3), (33, 33, 3, 4), (127, 64, 5, 6), (129, 1000, 3, 3),
+    (545, 1024, 8, 9), (1000, 5, 2, 40), (5000, 300, 3, 5), (5000, 1024, 8, 12), (4096, 96, 1, 2)])
+def test_speculative_chunks_against_oracle(gpu, oracle, n_tasks, n_clouds, n_levels, cap_hi):
+    """The chunked first-fit (k_first_fit_spec): task counts across the 32-task chunk, 128-row
+    block and 512-row ring (+shadow rows) boundaries, 1..1024 clouds, 1..8 demand levels (every
+    template width) and tight capacities (many overflowing chunks, many paid tasks)."""
+    rng = np.random.default_rng(n_tasks * 7919 + n_clouds)
+    vm = rng.integers(1, cap_hi + 1, n_clouds)
+    clouds = [V.VehicularCloud(i + 1, int(c), int(c), float(t), float(d)) for i, (c, t, d) in
+              enumerate(zip(vm, rng.integers(60, 161, n_clouds), rng.integers(5, 51, n_clouds)))]
+    tasks = [V.Task(j + 1, int(rng.integers(1, n_levels + 1)), float(rng.integers(5, 61)),
+                    float(rng.integers(50, 171))) for j in range(n_tasks)]
+    vcc = V.VccModel(clouds)
+    bots = [V.BagOfTasks(1, tasks)]
+    ni = V.NativeInstance(vcc, bots=bots)
+    r = V.greedy_schedule(vcc, bots, native=ni)
+    tgt, used, paid, unused, _ = oracle.greedy(ni.ref, n_tasks, n_clouds)
+    assert np.array_equal(r.target_index, tgt)
+    assert (r.paid_vms, r.unused_vms) == (paid, unused)
