@@ -1,15 +1,16 @@
 // vcs_greedy.cu — Alg. 2 first-fit placement on the device (replaces greedy_schedule,
 // greedy.cpp:5-30, with feasible() of workload.cpp:22-26).
 //
-// The scan is inherently sequential through vm_free, so the work is split in two:
+// The scan is sequential through vm_free; the work is split in two:
 //   1. k_attr_mask (all SMs): the batched feasibility scoring.  For every (task, cloud) pair the
-//      link test `delay <= max_delay && thr >= min_thr` becomes one bit; a warp covers 32 clouds
-//      and emits one 32-bit word with a ballot.  T x ceil(K/32) words.
-//   2. k_first_fit (one warp per instance): per task, lane l ANDs its attribute word(s) with the
-//      capacity word "free >= demand" (kept incrementally per distinct demand value in shared
-//      memory), a ballot finds the lowest word with a candidate and ffs the lowest cloud —
-//      exactly the first cloud in list order that feasible() accepts.  The next tasks'
-//      attribute words are prefetched into registers while the current batch is scanned.
+//      link test `delay <= max_delay && thr >= min_thr` becomes one bit; a warp covers a task,
+//      one ballot per 32 clouds, and also writes the task's {demand level, demand} descriptor.
+//   2. first fit, one warp per instance:
+//      k_first_fit_spec (default, <= 1024 clouds and <= 8 distinct demands): 32 tasks per step,
+//        each evaluated against the capacity state at the step start, committed up to the first
+//        task whose candidate no longer fits (see the comment at the kernel);
+//      k_first_fit_fast (VCS_GREEDY_SERIAL=1): one task per step, AND -> ballot -> ffs;
+//      k_first_fit (generic): more clouds or demands, capacity bits from the free counts.
 // Placements are bit-exact against the reference (same first feasible cloud, same paid set).
 #include "vcs_device.cuh"
 
