@@ -266,17 +266,6 @@ __global__ void __launch_bounds__(32) k_first_fit_fast(const GreedyDesc* __restr
     if (lane == 0) *D.paid = paid;
 }
 
-// Speculative chunked form of the fast path (the default): 32 tasks per step instead of one.
-// Every task of the chunk [j0, j0+32) takes its candidate = first feasible cloud under the
-// capacity state S0 at the chunk start (32 independent AND -> ballot -> ffs, pipelined).  Free
-// counts only decrease, so under the sequential state S_u of task u the feasible set is a subset
-// of S0's: the true answer is >= the candidate and EQUALS it iff the candidate still fits,
-// i.e. S0[c] >= inclusive prefix of demands of the chunk's tasks with the same candidate (a
-// task without a candidate stays without one: paid).  The chunk commits tasks up to the first
-// that fails this test and the next chunk starts there.  A failure leaves its candidate cloud
-// with free < that task's demand, clearing a capacity bit for good, so there are at most
-// K x n_levels failures: at most T/32 + K*n_levels steps for any input.  Same placements as the
-// one-task-per-step scan (greedy.cpp:5-30 order), bit for bit.
 // mbarrier + 1-D bulk copy (TMA) helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -314,9 +303,24 @@ __host__ __device__ constexpr size_t spec_smem_bytes(size_t K) {
     return spec_free_bytes(K) + (kRingRows + kShadowRows) * (32 * 4 + 8);
 }
 
-// Speculative first-fit, one warp per instance (see the comment above k_first_fit_fast for the
-// layout).  The attribute rows and task descriptors (padded to whole 32-row blocks) stream
-// into a 4-block shared-memory ring by 1-D bulk copies, two blocks ahead of the chunk.
+// Speculative chunked form of the fast path (the default): 32 tasks per step instead of one.
+// Every task of the chunk [j0, j0+32) takes its candidate = first feasible cloud under the
+// capacity state S0 at the chunk start (32 independent AND -> ballot -> ffs, pipelined).  Free
+// counts only decrease, so under the sequential state S_u of task u the feasible set is a subset
+// of S0's: the true answer is >= the candidate and EQUALS it iff the candidate still fits,
+// i.e. S0[c] >= inclusive prefix of demands of the chunk's tasks with the same candidate (a
+// task without a candidate stays without one: paid).  The chunk commits tasks up to the first
+// that fails this test and the next chunk starts there.  A failure leaves its candidate cloud
+// with free < that task's demand, clearing a capacity bit for good, so there are at most
+// K x n_levels failures: at most T/32 + K*n_levels steps for any input.  Same placements as the
+// one-task-per-step scan (greedy.cpp:5-30 order), bit for bit.
+// The common case is checked order-free: every placed demand is subtracted atomically from its
+// candidate's free count; no count below zero means every prefix fits.  Only an overflowing
+// chunk computes the prefixes (match.any groups + popcounts per level).
+// Layout: lane l owns capacity word l (clouds 32l..32l+31), in shared memory per level.  The
+// attribute rows (stride 32 words) and task descriptors, padded to whole 128-row blocks,
+// stream into a 4-block shared-memory ring by 1-D bulk copies (+ 32 shadow rows so a chunk
+// never wraps), up to three blocks ahead of the chunk.
 template <int NL>
 __global__ void __launch_bounds__(32) k_first_fit_spec(const GreedyDesc* __restrict__ descs) {
     extern __shared__ __align__(128) int32_t sm[];
