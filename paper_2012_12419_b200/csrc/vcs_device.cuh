@@ -176,6 +176,8 @@ struct vcs_space {
     vcs::DevBuf<double> delta;   // residual per sweep (index k = sweep k)
     vcs::DevBuf<vcs::SolveCtrl> ctrl;
     vcs::DevBuf<int32_t> actions_dev;
+    vcs::DevBuf<int8_t> act8_dev;          // int8 action column for the narrowed download
+    std::vector<cudaEvent_t> piece_ev;     // events of the narrowed download pieces
     // layer-wavefront solver: version vectors of every layer + offsets
     vcs::DevBuf<double> ver;
     vcs::DevBuf<uint64_t> ver_off;

@@ -22,8 +22,13 @@
 
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <condition_variable>
 #include <cstdlib>
+#include <functional>
+#include <mutex>
+#include <thread>
 
 namespace vcs {
 
@@ -1476,6 +1481,130 @@ int vcs_solve_enqueue(vcs_space* sp, const vcs_solve_opts* opts, void* stream) {
 }
 
 namespace {
+// int32 actions -> int8 (every action of a space with <= 127 clouds fits): the download of the
+// action column shrinks 4x and the host widens it back while later chunks are in flight.
+__global__ void k_narrow_actions(const int32_t* __restrict__ a, int8_t* __restrict__ b, uint64_t n) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        b[i] = static_cast<int8_t>(a[i]);
+}
+
+// Pinned host staging blocks, recycled across spaces (a cudaHostAlloc costs milliseconds).
+struct PinnedFreeList {
+    std::mutex m;
+    std::vector<std::pair<void*, size_t>> blocks;
+};
+PinnedFreeList& pinned_free_list() {
+    static PinnedFreeList* f = new PinnedFreeList; // never destroyed: used until process exit
+    return *f;
+}
+void* pinned_acquire(size_t bytes, size_t* got) {
+    auto& f = pinned_free_list();
+    {
+        std::lock_guard<std::mutex> lk(f.m);
+        size_t best = f.blocks.size();
+        for (size_t i = 0; i < f.blocks.size(); ++i)
+            if (f.blocks[i].second >= bytes &&
+                (best == f.blocks.size() || f.blocks[i].second < f.blocks[best].second))
+                best = i;
+        if (best < f.blocks.size()) {
+            auto b = f.blocks[best];
+            f.blocks.erase(f.blocks.begin() + static_cast<long>(best));
+            *got = b.second;
+            return b.first;
+        }
+    }
+    const size_t want = bytes + bytes / 4; // headroom for the next, slightly larger space
+    void* p = nullptr;
+    VCS_CUDA(cudaHostAlloc(&p, want, cudaHostAllocPortable));
+    *got = want;
+    return p;
+}
+void pinned_release(void* p, size_t bytes) {
+    auto& f = pinned_free_list();
+    std::lock_guard<std::mutex> lk(f.m);
+    f.blocks.emplace_back(p, bytes);
+    while (f.blocks.size() > 4) { // bounded: free the smallest
+        auto it = std::min_element(f.blocks.begin(), f.blocks.end(),
+                                   [](const auto& x, const auto& y) { return x.second < y.second; });
+        cudaFreeHost(it->first);
+        f.blocks.erase(it);
+    }
+}
+
+// Persistent host workers for the widening (the calling thread works too).
+class HostWorkers {
+public:
+    static HostWorkers& get() {
+        static HostWorkers* w = new HostWorkers; // never destroyed: no join at process exit
+        return *w;
+    }
+    // fn(begin, end) over [0, n) in pieces of `grain`; returns when every piece is done
+    void parallel_for(size_t n, size_t grain, const std::function<void(size_t, size_t)>& fn) {
+        if (n == 0) return;
+        if (th_.empty() || n <= grain) {
+            fn(0, n);
+            return;
+        }
+        std::unique_lock<std::mutex> lk(m_);
+        job_ = &fn;
+        n_ = n;
+        grain_ = grain;
+        next_.store(0);
+        busy_ = static_cast<int>(th_.size());
+        ++gen_;
+        cv_.notify_all();
+        lk.unlock();
+        work();
+        lk.lock();
+        done_cv_.wait(lk, [&] { return busy_ == 0; });
+        job_ = nullptr;
+    }
+
+private:
+    HostWorkers() {
+        const unsigned hw = std::thread::hardware_concurrency();
+        unsigned cap = 7u; // 7..11 measured equal on the 16-core box; fewer lose, more lose
+        if (const char* e = std::getenv("VCS_HOST_WORKERS")) cap = static_cast<unsigned>(std::atoi(e));
+        const unsigned n = hw > 2 ? std::min(cap, hw - 1) : 0u;
+        for (unsigned i = 0; i < n; ++i) th_.emplace_back([this] { loop(); });
+        for (auto& t : th_) t.detach();
+    }
+    void work() {
+        for (;;) {
+            const size_t b = next_.fetch_add(grain_);
+            if (b >= n_) return;
+            (*job_)(b, std::min(n_, b + grain_));
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            std::unique_lock<std::mutex> lk(m_);
+            cv_.wait(lk, [&] { return gen_ != seen; });
+            seen = gen_;
+            lk.unlock();
+            work();
+            lk.lock();
+            if (--busy_ == 0) done_cv_.notify_all();
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(size_t, size_t)>* job_ = nullptr;
+    size_t n_ = 0, grain_ = 1;
+    std::atomic<size_t> next_{0};
+    int busy_ = 0;
+    uint64_t gen_ = 0;
+};
+
+// int8 -> int32 widening of the action column on the host (plain stores: non-temporal stores
+// measured slower, they compete with the DMA writing the value column into host memory)
+void widen(const int8_t* src, int32_t* dst, size_t n) {
+    for (size_t i = 0; i < n; ++i) dst[i] = src[i];
+}
+
 bool is_pinned(const void* p) {
     if (!p) return true;
     cudaPointerAttributes attr{};
@@ -1499,6 +1628,19 @@ int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int
     } trace_end{t_start};
     const bool pinned_out =
         (values_out || actions_out) && is_pinned(values_out) && is_pinned(actions_out);
+    // int8 action column on the wire when every action fits (<= 127 clouds); its device buffer
+    // is allocated before the solve is enqueued so the download stream, which waits on the
+    // solve's layer events, is ordered after the allocation
+    const bool narrow = pinned_out && actions_out && sp->has_plan && sp->plan.n_clouds <= 127 &&
+                        !std::getenv("VCS_NO_NARROW");
+    if (narrow) {
+        const int rca = guarded([&] {
+            vcs::bind_device(sp->device);
+            sp->act8_dev.exact(sp->S, sp->stream);
+            return VCS_OK;
+        });
+        if (rca != VCS_OK) return rca;
+    }
     const int rc = enqueue_impl(sp, opts, nullptr, pinned_out ? 1 : 0);
     if (rc != VCS_OK) return rc;
     const vcs::CachedGraph& g = *sp->last_graph;
@@ -1510,6 +1652,21 @@ int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int
         if (!sp->d2h_stream)
             VCS_CUDA(cudaStreamCreateWithFlags(&sp->d2h_stream, cudaStreamNonBlocking));
         cudaStream_t d = sp->d2h_stream;
+        int8_t* staging = nullptr;
+        size_t staging_bytes = 0;
+        struct StagingGuard {
+            int8_t*& p;
+            size_t& n;
+            ~StagingGuard() {
+                if (p) pinned_release(p, n);
+            }
+        } staging_guard{staging, staging_bytes};
+        if (narrow) staging = static_cast<int8_t*>(pinned_acquire(sp->S, &staging_bytes));
+        struct Piece {
+            uint64_t r0, r1;
+            cudaEvent_t ev;
+        };
+        std::vector<Piece> pieces;
         auto copy_rows = [&](uint64_t r0, uint64_t r1, cudaStream_t st) {
             if (r1 <= r0) return;
             if (values_out)
@@ -1522,19 +1679,58 @@ int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int
         // Rows are final layer by layer, from the back: copy them in chunks of >= 16 MB (fewer,
         // larger DMA transfers), each after the event of its last (lowest) layer.  The terminal
         // layer's rows go with the first chunk: its memsets precede layer H-1's kernel.
-        const uint64_t row_bytes = (values_out ? 8 : 0) + (actions_out ? 4 : 0);
+        const uint64_t row_bytes = (values_out ? 8 : 0) + (actions_out ? (narrow ? 1 : 4) : 0);
         uint64_t chunk_end = sp->S;
         for (int t = sp->H - 1; t >= 0; --t) {
             const uint64_t r0 = sp->layer_off[t];
             if ((chunk_end - r0) * row_bytes < (16ull << 20) && t > 0) continue;
             VCS_CUDA(cudaStreamWaitEvent(d, g.layer_ev[static_cast<size_t>(t)], 0));
-            copy_rows(r0, chunk_end, d);
+            if (!narrow) {
+                copy_rows(r0, chunk_end, d);
+            } else {
+                const uint64_t n = chunk_end - r0;
+                if (values_out)
+                    VCS_CUDA(cudaMemcpyAsync(values_out + r0, sp->v[0].p + r0, n * sizeof(double),
+                                             cudaMemcpyDeviceToHost, d));
+                const unsigned blocks = static_cast<unsigned>(
+                    std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(sp->num_sms) * 8));
+                k_narrow_actions<<<std::max(1u, blocks), 256, 0, d>>>(sp->actions_dev.p + r0,
+                                                                      sp->act8_dev.p + r0, n);
+                VCS_LAUNCHED();
+                VCS_CUDA(cudaMemcpyAsync(staging + r0, sp->act8_dev.p + r0, n, cudaMemcpyDeviceToHost, d));
+                const size_t k = pieces.size();
+                if (sp->piece_ev.size() <= k) {
+                    cudaEvent_t e = nullptr;
+                    VCS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                    sp->piece_ev.push_back(e);
+                }
+                VCS_CUDA(cudaEventRecord(sp->piece_ev[k], d));
+                pieces.push_back(Piece{r0, chunk_end, sp->piece_ev[k]});
+            }
             chunk_end = r0;
         }
         vcs_solve_report local{};
         vcs_solve_report* rep = report ? report : &local;
         const int rc3 = vcs_solve_collect(sp, nullptr, nullptr, rep, nullptr);
         if (rc3 != VCS_OK) vcs::raise(rc3, vcs_last_error());
+        // widen each int8 piece into the caller's int32 column as soon as it landed (the later
+        // pieces are still on the wire)
+        const bool tr = vcs::trace_enabled();
+        const double tw0 = tr ? vcs::host_ms() : 0.0;
+        for (const Piece& pc : pieces) {
+            const double ta = tr ? vcs::host_ms() : 0.0;
+            VCS_CUDA(cudaEventSynchronize(pc.ev));
+            const double tb = tr ? vcs::host_ms() : 0.0;
+            const int8_t* src = staging + pc.r0;
+            int32_t* dst = actions_out + pc.r0;
+            HostWorkers::get().parallel_for(pc.r1 - pc.r0, size_t(1) << 17, [&](size_t b, size_t e) {
+                widen(src + b, dst + b, e - b);
+            });
+            if (tr)
+                std::fprintf(stderr, "[vcs solve] piece %llu rows: waited %.3f ms, widened %.3f ms (t=%.3f)\n",
+                             static_cast<unsigned long long>(pc.r1 - pc.r0), tb - ta, vcs::host_ms() - tb,
+                             vcs::host_ms() - tw0);
+        }
         // an early stop (K* < H) rewrote the prefix of layers t < H - K* after their events
         const int K = rep->sweeps;
         if (sp->H - K > 0) {

@@ -1637,6 +1637,9 @@ vcs_space::~vcs_space() {
         for (auto& e : g.layer_ev)
             if (e) cudaEventDestroy(e);
     }
+    for (auto e : piece_ev)
+        if (e) cudaEventDestroy(e);
+    if (d2h_stream) cudaStreamSynchronize(d2h_stream);
     if (d2h_stream) cudaStreamDestroy(d2h_stream);
     if (aux_stream) cudaStreamDestroy(aux_stream);
     // the stream is idle: big blocks go to the per-device cache for the next space, the rest
@@ -1651,6 +1654,7 @@ vcs_space::~vcs_space() {
     delta.release_idle();
     ctrl.release_idle();
     actions_dev.release_idle();
+    act8_dev.release_idle();
     ver.release_idle();
     cert_xd.release_idle();
     cert_lb.release_idle();

@@ -177,10 +177,16 @@ def test_capped_sweeps_match_oracle(gpu, oracle):
             assert np.array_equal(acts, a)
 
 
-def test_pinned_outputs_overlapped_download(gpu, golden):
-    """vcs_solve into PINNED host buffers streams each layer's results while the wavefront
-    runs; an early stop (eps = 5, 0.5) rewrites a prefix afterwards — both must be exact."""
+@pytest.mark.parametrize("method", ["WAVEFRONT", "AUTO"])
+@pytest.mark.parametrize("narrow", [True, False])
+def test_pinned_outputs_overlapped_download(gpu, golden, monkeypatch, method, narrow):
+    """vcs_solve into PINNED host buffers streams each layer's results while the layer pass
+    runs (int8 action column widened on the host, or int32 with VCS_NO_NARROW); an early stop
+    (eps = 5, 0.5) rewrites a prefix afterwards (AUTO: after the certified pass's fallback) —
+    all must be exact."""
     import torch
+    if not narrow:
+        monkeypatch.setenv("VCS_NO_NARROW", "1")
     p = V.load_instance(str(GOLDEN / "canonical_instance.txt"))
     ni = V.NativeInstance(p.vcc, bots=p.bots)
     sp = V.StateSpace.build_native(ni)
@@ -194,7 +200,7 @@ def test_pinned_outputs_overlapped_download(gpu, golden):
         for _ in range(2):  # first solve captures the graph, the second replays it
             vals.fill_(float("nan"))
             acts.fill_(-7)
-            opts = N.vcs_solve_opts(eps, 1, 0, 1.0, N.VCS_METHOD_WAVEFRONT)
+            opts = N.vcs_solve_opts(eps, 1, 0, 1.0, getattr(N, f"VCS_METHOD_{method}"))
             rep = N.vcs_solve_report()
             N.check(N.lib().vcs_solve(sp.handle, C.byref(opts), vp, ap, C.byref(rep)))
             assert rep.sweeps == g["sweeps"]
