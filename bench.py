@@ -514,13 +514,18 @@ def run_b200(args):
             dist.all_reduce(t, op=dist.ReduceOp.SUM)
             e2e_t, e2e_backups = float(tm[0].item()), float(t[1].item())
             inst_bytes *= world
+        # on the wire: f64 values + the action column as int8 when every action fits (<= 127
+        # clouds; widened into the caller's int32 buffer on the host), else int32
+        act_wire = 1 if (s.n_clouds <= 127 and not os.environ.get("VCS_NO_NARROW")) else 4
         e2e = {"value": e2e_backups / e2e_t, "unit": "backups/s",
                "h2d_bytes_per_step": inst_bytes,
-               "d2h_bytes_per_step": S * (8 + 4) * (world if world > 1 else 1),
+               "d2h_bytes_per_step": S * (8 + act_wire) * (world if world > 1 else 1),
+               "d2h_result_bytes_per_step": S * (8 + 4) * (world if world > 1 else 1),
                "ms_per_step": e2e_t * 1e3,
                "build_ms": statistics.median(p[0] for p in parts) * 1e3,
                "solve_and_d2h_ms": statistics.median(p[1] for p in parts) * 1e3,
-               "path": "vcs_space_build(host instance) + vcs_solve(pinned host values/actions)",
+               "path": "vcs_space_build(host instance) + vcs_solve(pinned host values/actions; "
+                       "the int8 action column is widened to int32 on host threads)",
                "steps": len(e2e_times)}
     elif args.e2e_steps > 0:
         e2e = e2e_sharded(args, ni, local, dev, stream, opts, sharding, S, rank)
