@@ -204,7 +204,11 @@ typedef struct vcs_solve_report {
 /* Replaces parallel_vi.cpp:48-116 detail::run_value_iteration (the sweep loop, the sup-norm
  * residual `delta < epsilon`, buffer parity, and the argmax extraction of
  * parallel_vi.cpp:109-111).  values_out (n_states f64) and actions_out (n_states i32) may be
- * NULL.  Bit-identical to the reference for every epsilon (same sweep count). */
+ * NULL.  Bit-identical to the reference for every epsilon (same sweep count).
+ * With PINNED (cudaHostAlloc) outputs the results stream to the host while the layer pass runs;
+ * for spaces of <= 127 clouds the action column crosses PCIe as int8 and is widened into
+ * actions_out by library-owned host threads (VCS_HOST_WORKERS, default 7; VCS_NO_NARROW=1
+ * disables it).  The call returns after every output byte is written. */
 int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int32_t* actions_out,
               vcs_solve_report* report);
 /* The same solve split in two for callers that overlap or time it on their own stream
