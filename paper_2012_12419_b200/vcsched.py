@@ -44,7 +44,7 @@ __all__ = [
     "MdpInstance", "MdpAction", "MdpState", "initial_state", "legal_actions", "transition",
     "step_reward", "StateCapacityError", "StateSpace", "ViOptions", "ValueTable", "Policy",
     "ViResult", "value_iteration", "bellman_backup", "rollout", "run_value_iteration",
-    "BlockPartition", "SweepBarrier", "parallel_value_iteration", "SpeedupRow", "measure_speedup",
+    "BlockPartition", "SweepBarrier", "parallel_value_iteration", "SpeedupRow", "measure_speedup", "speedup_csv",
     "ScheduleResult", "greedy_schedule", "greedy_reward", "ParsedInstance", "parse_instance",
     "load_instance", "generate_instance", "ConfigError", "IoError", "InvalidArgument",
     "OutOfRange", "CudaError", "VcsError", "NativeInstance",
@@ -723,6 +723,14 @@ class SpeedupRow:
     workers: int = 1
     wall_ms: float = 0.0
     speedup_vs_one: float = 1.0
+
+
+def speedup_csv(rows) -> str:
+    """io.cpp:351-357: `workers,wall_ms,speedup_vs_one` with doubles printed as %.17g."""
+    out = ["workers,wall_ms,speedup_vs_one\n"]
+    for r in rows:
+        out.append(f"{r.workers},{'%.17g' % r.wall_ms},{'%.17g' % r.speedup_vs_one}\n")
+    return "".join(out)
 
 
 def measure_speedup(instance: MdpInstance, worker_counts: Iterable[int],

@@ -251,3 +251,11 @@ def test_full_state_helpers():
     assert V.step_reward(s0, V.MdpAction(0), s1, inst) == pytest.approx(5.0)
     s2 = V.transition(s1, V.MdpAction(V.kPaidCloud), inst)
     assert V.step_reward(s1, V.MdpAction(V.kPaidCloud), s2, inst) == pytest.approx(-12.0)
+
+
+def test_speedup_csv_format():
+    """io.cpp:351-357: header, then workers,wall_ms,speedup_vs_one with %.17g doubles."""
+    rows = [V.SpeedupRow(1, 12.5, 1.0), V.SpeedupRow(8, 0.1, 125.0), V.SpeedupRow(2, 1 / 3, 37.5)]
+    assert V.speedup_csv(rows) == ("workers,wall_ms,speedup_vs_one\n1,12.5,1\n8,0.10000000000000001,125\n"
+                                   "2,0.33333333333333331,37.5\n")
+    assert V.speedup_csv([]) == "workers,wall_ms,speedup_vs_one\n"
