@@ -744,10 +744,12 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
                 for (int w = 0; w < warp; ++w) rank += s_wsum[r][w];
                 const uint64_t k1[1] = {kr[r]};
                 const Slots sl(dr[r]);
-#pragma unroll
-                for (int e = 0; e < SL; ++e) {
-                    if (!((fm[r] >> e) & 1u)) continue;
-                    A.rank_tables[rank_t + dec.idx(sl, e)] = rank;
+                // over the set bits, not unrolled: 8 x 8 inlined next_key bodies made the kernel
+                // large enough to miss in the instruction cache (shared-memory slot constants)
+#pragma unroll 1
+                for (uint32_t m = fm[r]; m; m &= m - 1) {
+                    const int e = __ffs(m) - 1;
+                    A.rank_tables[rank_t + sl.idx(e, L)] = rank;
                     uint64_t nk[1];
                     next_key<1>(k1, e == SL - 1 ? -1 : e, L, nk);
                     A.keys[key_next + rank] = nk[0];
