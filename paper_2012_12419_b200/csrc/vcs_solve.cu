@@ -727,6 +727,7 @@ __global__ void __launch_bounds__(256, MINB) k_cert_rows(CertArgs a) {
     __syncthreads();
     if (threadIdx.x == 0 && s_lb)
         atomicMax(reinterpret_cast<unsigned long long*>(a.lb + a.m), s_lb);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); // the next layer may launch
 }
 
 // Certified layer on the implicit-CSR form of a dense space: a state's edges are
@@ -764,6 +765,9 @@ __device__ __forceinline__ void cert_implicit_layer(const CertImplArgs& a, const
     uint64_t i = first_i;
     uint64_t kn[WM] = {}; // the next state's key, loaded while the current state computes
     if (i < a.n) load_key<WM>(a.keys + i * static_cast<uint64_t>(words), words, kn);
+    // programmatic dependent launch: everything above reads only build outputs; the previous
+    // layer's pairs (and this layer's outputs) are touched after the wait
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (; i < a.n; i += stride) {
         uint64_t k[WM];
 #pragma unroll
@@ -810,6 +814,7 @@ __device__ __forceinline__ void cert_implicit_layer(const CertImplArgs& a, const
     __syncthreads();
     if (threadIdx.x == 0 && s_lb)
         atomicMax(reinterpret_cast<unsigned long long*>(a.lb + a.m), s_lb);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); // the next layer may launch
 }
 
 __device__ __forceinline__ void load_layer_param(LayerParam& sL, const LayerParam* src,
@@ -1096,6 +1101,7 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
         c.lb = sp->cert_lb.p;
         c.discount = key.discount;
         int launches = 0;
+        const bool pdl = g.layer_ev.empty() && !std::getenv("VCS_NO_PDL");
         for (int t = H - 1; t >= 0; --t) {
             c.row0 = sp->layer_off[t];
             c.n = sp->layer_off[t + 1] - sp->layer_off[t];
@@ -1116,10 +1122,22 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
                     const uint64_t blocks = std::max<uint64_t>(
                         1, std::min<uint64_t>((c.n + 255) / 256,
                                               static_cast<uint64_t>(std::max(1, per_sm)) * sp->num_sms));
+                    // layers after the first launch programmatically (PDL): their blocks load the
+                    // layer constants and first keys while the previous layer drains.  Not with
+                    // per-layer events in between (vcs_solve's streamed download).
+                    cudaLaunchConfig_t cfg{};
+                    cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+                    cfg.blockDim = dim3(256);
+                    cfg.stream = s;
+                    cudaLaunchAttribute attr[1];
+                    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                    attr[0].val.programmaticStreamSerializationAllowed = 1;
+                    cfg.attrs = attr;
+                    cfg.numAttrs = (pdl && t < H - 1) ? 1 : 0;
                     if (disc)
-                        k_cert_implicit<WM, true, 3><<<static_cast<unsigned>(blocks), 256, 0, s>>>(c);
+                        VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, true, 3>, c));
                     else
-                        k_cert_implicit<WM, false, 3><<<static_cast<unsigned>(blocks), 256, 0, s>>>(c);
+                        VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, false, 3>, c));
                     VCS_LAUNCHED();
                 });
                 ++launches;
