@@ -30,6 +30,8 @@
 #include <mutex>
 #include <thread>
 
+#include <unistd.h>
+
 namespace vcs {
 
 namespace {
@@ -1560,7 +1562,8 @@ public:
     // fn(begin, end) over [0, n) in pieces of `grain`; returns when every piece is done
     void parallel_for(size_t n, size_t grain, const std::function<void(size_t, size_t)>& fn) {
         if (n == 0) return;
-        if (th_.empty() || n <= grain) {
+        // a forked child inherits this object but not the threads: work inline there
+        if (th_.empty() || n <= grain || getpid() != pid_) {
             fn(0, n);
             return;
         }
@@ -1580,7 +1583,7 @@ public:
     }
 
 private:
-    HostWorkers() {
+    HostWorkers() : pid_(getpid()) {
         const unsigned hw = std::thread::hardware_concurrency();
         unsigned cap = 7u; // 7..11 measured equal on the 16-core box; fewer lose, more lose
         if (const char* e = std::getenv("VCS_HOST_WORKERS")) cap = static_cast<unsigned>(std::atoi(e));
@@ -1607,6 +1610,7 @@ private:
             if (--busy_ == 0) done_cv_.notify_all();
         }
     }
+    const pid_t pid_;
     std::vector<std::thread> th_;
     std::mutex m_;
     std::condition_variable cv_, done_cv_;
