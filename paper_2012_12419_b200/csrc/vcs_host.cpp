@@ -329,6 +329,14 @@ LayerPlan make_layer_plan(const vcs_instance* in) {
             if (W > kDenseMax) break;
         }
         L.dense_size = W <= kDenseMax ? static_cast<uint32_t>(W) : 0u;
+        {   // layer t's own key space, numbered like transition t-1 numbers its successors
+            uint64_t Ws = 1;
+            for (std::size_t p = 0; p < act.size() && Ws <= kDenseMax; ++p) {
+                L.wself[p] = static_cast<uint32_t>(Ws);
+                Ws *= static_cast<uint64_t>(std::max(0, in->cloud_vm_free[act[p]])) + 1;
+            }
+            L.self_size = Ws <= kDenseMax ? static_cast<uint32_t>(Ws) : 0u;
+        }
         int kept = 0;
         for (std::size_t p = 0; p < act.size(); ++p) {
             const int c = act[p];

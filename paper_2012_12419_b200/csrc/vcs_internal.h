@@ -80,6 +80,11 @@ struct LayerParam {
     int32_t pad1;
     uint32_t wnext[kMaxActive];  // W of field keep_idx[p] in layer t+1 (0 if p retires)
     uint32_t radix[kMaxActive];  // free_{cloud[p]} + 1
+    // the same numbering of layer t's OWN key space (= the successor index of transition t-1):
+    // idx = sum_p f_p * wself[p]; self_size = prod radix (0 = too large)
+    uint32_t wself[kMaxActive];
+    uint32_t self_size;
+    int32_t pad2;
 };
 
 // Dense successor indices are used up to this key-space size (a 4-byte first-edge table).

@@ -749,11 +749,17 @@ struct CertImplArgs {
     uint64_t row0, n;
     int m;
     double discount;
+    // key-space layout of the pairs (DXD): layer t+1's pairs at their successor index, layer t's
+    // at its own key-space index (write_own: someone reads them)
+    const uint32_t* __restrict__ rank_self; // transition t-1's table: layer t's BFS rank by index
+    uint64_t dense_n;                       // layer t's key-space size
+    int write_own;
 };
 
 // One layer of the implicit certified pass over states first_i, first_i + stride, ... (the
-// block has loaded the layer's LayerParam into sL and zeroed s_lb).
-template <int WM, bool DISC>
+// block has loaded the layer's LayerParam into sL and zeroed s_lb).  DXD: the pairs are stored
+// by key-space index (one gather per edge, no rank-table hop); otherwise by BFS index.
+template <int WM, bool DISC, bool DXD>
 __device__ __forceinline__ void cert_implicit_layer(const CertImplArgs& a, const LayerParam& L,
                                                     unsigned long long& s_lb, uint64_t first_i,
                                                     uint64_t stride) {
@@ -776,14 +782,20 @@ __device__ __forceinline__ void cert_implicit_layer(const CertImplArgs& a, const
         for (int w = 0; w < WM; ++w) k[w] = kn[w];
         if (i + stride < a.n) load_key<WM>(a.keys + (i + stride) * static_cast<uint64_t>(words), words, kn);
         const Slots sl = dec.decode(k);
-        uint32_t rk[SL];
-#pragma unroll
-        for (int e = 0; e < SL; ++e)
-            if (sl.valid(e)) rk[e] = __ldg(a.rank + dec.idx(sl, e));
         double2 x[SL];
+        if (DXD) {
 #pragma unroll
-        for (int e = 0; e < SL; ++e)
-            if (sl.valid(e)) x[e] = __ldg(a.xd_next + rk[e]);
+            for (int e = 0; e < SL; ++e)
+                if (sl.valid(e)) x[e] = __ldg(a.xd_next + dec.idx(sl, e));
+        } else {
+            uint32_t rk[SL];
+#pragma unroll
+            for (int e = 0; e < SL; ++e)
+                if (sl.valid(e)) rk[e] = __ldg(a.rank + dec.idx(sl, e));
+#pragma unroll
+            for (int e = 0; e < SL; ++e)
+                if (sl.valid(e)) x[e] = __ldg(a.xd_next + rk[e]);
+        }
         double hi = -INFINITY, lo = -INFINITY;
         int best = -1;
 #pragma unroll
@@ -800,7 +812,14 @@ __device__ __forceinline__ void cert_implicit_layer(const CertImplArgs& a, const
             if (qx > lo) lo = qx;
         }
         if (a.m == 1) lo = 0.0; // V_0
-        a.xd_cur[i] = make_double2(lo, hi);
+        if (!DXD) {
+            a.xd_cur[i] = make_double2(lo, hi);
+        } else if (a.write_own) {
+            uint32_t own = 0;
+            for (int p = 0; p < L.n_active; ++p)
+                own += static_cast<uint32_t>(get_field<WM>(k, L.bit_off[p], L.width[p])) * L.wself[p];
+            a.xd_cur[own] = make_double2(lo, hi);
+        }
         a.values_out[a.row0 + i] = hi;
         a.act_out[a.row0 + i] = best < 0 ? -1 : L.cloud[best];
         const double d = fabs(hi - lo);
@@ -819,6 +838,115 @@ __device__ __forceinline__ void cert_implicit_layer(const CertImplArgs& a, const
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); // the next layer may launch
 }
 
+// One layer in KEY-SPACE order: index d of layer t's key space (d = sum_p f_p * wself[p]) is a
+// state iff transition t-1's rank table holds its BFS rank.  The key is decoded from d, the
+// successors' pairs are gathered by their key-space index (one hop), the own pair is written at
+// d (coalesced) and the value/action at the BFS rank.
+template <int WM, bool DISC>
+__device__ __forceinline__ void cert_dense_layer(const CertImplArgs& a, const LayerParam& L,
+                                                 unsigned long long& s_lb, uint64_t first,
+                                                 uint64_t stride) {
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int SL = kDenseSlots;
+    const bool retires = L.n_keep != L.n_active;
+    const SlotDecoder<WM> dec(L);
+    const double r_cloud = L.r_cloud_kept, r_paid = L.r_paid_kept;
+    constexpr int NF = kDenseSlots - 1; // key-space layers have <= 7 fields
+    const int na = L.n_active;
+    double dmax = 0.0;
+    uint64_t d = first;
+    uint32_t rn = d < a.dense_n ? __ldg(a.rank_self + d) : kEmpty32; // next index's rank
+    // mixed-radix digits of d and of the stride, divided out once; the loop steps an odometer
+    uint32_t g[NF], sd[NF], rad[NF];
+    {
+        uint32_t rem = static_cast<uint32_t>(d < a.dense_n ? d : 0);
+        uint32_t srem = static_cast<uint32_t>(stride < a.dense_n ? stride : 0);
+#pragma unroll
+        for (int p = 0; p < NF; ++p) {
+            rad[p] = p < na ? L.radix[p] : 1u;
+            g[p] = rem % rad[p];
+            rem /= rad[p];
+            sd[p] = srem % rad[p];
+            srem /= rad[p];
+        }
+    }
+    // clouds retiring at this transition (their free counts are charged by the reward)
+    uint32_t retmask = 0;
+#pragma unroll
+    for (int p = 0; p < NF; ++p)
+        if (p < na && L.keep_idx[p] < 0) retmask |= 1u << p;
+    const double r_cl = L.r_cloud, r_pd = L.r_paid, gam = L.gamma;
+    const int dem = L.demand;
+    asm volatile("griddepcontrol.wait;" ::: "memory"); // (PDL) the previous layer's pairs
+    for (; d < a.dense_n; d += stride) {
+        const uint32_t r = rn;
+        if (d + stride < a.dense_n) rn = __ldg(a.rank_self + d + stride);
+        // the state's slots straight from its digits (= dec.decode of its packed key), and the
+        // retired free VMs (an integer: the reference's fp64 running sum of integers is exact)
+        uint32_t base = 0, mask = 0;
+        int ret_all = 0;
+#pragma unroll
+        for (int p = 0; p < NF; ++p) {
+            base += g[p] * dec.wn[p];
+            if (((dec.sw[p] >> 16) & 1u) && g[p] >= dec.demand) mask |= 1u << p;
+            if ((retmask >> p) & 1u) ret_all += static_cast<int>(g[p]);
+        }
+        { // advance the digits by the stride (the carry out of the top digit ends the loop)
+            uint32_t carry = 0;
+#pragma unroll
+            for (int p = 0; p < NF; ++p) {
+                const uint32_t v = g[p] + sd[p] + carry;
+                carry = v >= rad[p] ? 1u : 0u;
+                g[p] = carry ? v - rad[p] : v;
+            }
+        }
+        if (r == kEmpty32) continue;
+        const Slots sl(static_cast<uint64_t>(base) | (static_cast<uint64_t>(mask) << 32));
+        double2 x[SL];
+#pragma unroll
+        for (int e = 0; e < SL; ++e)
+            if (sl.valid(e)) x[e] = __ldg(a.xd_next + dec.idx(sl, e));
+        double hi = -INFINITY, lo = -INFINITY;
+        int best = -1;
+#pragma unroll
+        for (int e = 0; e < SL; ++e) {
+            if (!sl.valid(e)) continue;
+            const int pe = e == SL - 1 ? -1 : e;
+            double rw;
+            if (retires) { // retiring_reward: beta*n - gamma*retired, two rounded operations
+                const int ret = ret_all - ((pe >= 0 && ((retmask >> pe) & 1u)) ? dem : 0);
+                rw = __dsub_rn(pe < 0 ? r_pd : r_cl, __dmul_rn(gam, static_cast<double>(ret)));
+            } else {
+                rw = pe < 0 ? r_paid : r_cloud;
+            }
+            const double qx = DISC ? __dadd_rn(rw, __dmul_rn(a.discount, x[e].x)) : __dadd_rn(rw, x[e].x);
+            const double qy = DISC ? __dadd_rn(rw, __dmul_rn(a.discount, x[e].y)) : __dadd_rn(rw, x[e].y);
+            if (qy > hi) { // strict: the first maximal edge wins (mdp.cpp:254-260)
+                hi = qy;
+                best = pe;
+            }
+            if (qx > lo) lo = qx;
+        }
+        if (a.m == 1) lo = 0.0; // V_0
+        a.xd_cur[d] = make_double2(lo, hi);
+        a.values_out[a.row0 + r] = hi;
+        a.act_out[a.row0 + r] = best < 0 ? -1 : L.cloud[best];
+        const double dd = fabs(hi - lo);
+        dmax = dmax < dd ? dd : dmax;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double other = __shfl_xor_sync(FULL, dmax, o);
+        dmax = dmax < other ? other : dmax;
+    }
+    if ((threadIdx.x & 31) == 0 && dmax > 0.0)
+        atomicMax(&s_lb, static_cast<unsigned long long>(__double_as_longlong(dmax)));
+    __syncthreads();
+    if (threadIdx.x == 0 && s_lb)
+        atomicMax(reinterpret_cast<unsigned long long*>(a.lb + a.m), s_lb);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void load_layer_param(LayerParam& sL, const LayerParam* src,
                                                  unsigned long long& s_lb) {
     __syncthreads(); // the previous layer's readers of sL are done
@@ -830,14 +958,24 @@ __device__ __forceinline__ void load_layer_param(LayerParam& sL, const LayerPara
 
 // One launch per layer.  (A single cooperative launch over all layers with a grid sync between
 // them measured slower, 0.86 vs 0.66 ms on C4: every sync waits for the slowest block.)
-template <int WM, bool DISC, int MINB>
+template <int WM, bool DISC, int MINB, bool DXD>
 __global__ void __launch_bounds__(256, MINB) k_cert_implicit(CertImplArgs a) {
     __shared__ LayerParam sL;
     __shared__ unsigned long long s_lb;
     load_layer_param(sL, a.L, s_lb);
-    cert_implicit_layer<WM, DISC>(a, sL, s_lb,
-                                  static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x,
-                                  static_cast<uint64_t>(gridDim.x) * blockDim.x);
+    cert_implicit_layer<WM, DISC, DXD>(a, sL, s_lb,
+                                       static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x,
+                                       static_cast<uint64_t>(gridDim.x) * blockDim.x);
+}
+
+template <int WM, bool DISC, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_cert_dense(CertImplArgs a) {
+    __shared__ LayerParam sL;
+    __shared__ unsigned long long s_lb;
+    load_layer_param(sL, a.L, s_lb);
+    cert_dense_layer<WM, DISC>(a, sL, s_lb,
+                               static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x,
+                               static_cast<uint64_t>(gridDim.x) * blockDim.x);
 }
 
 // K* = H+1 is proven iff lb_k >= eps for k = 1..H (and no sweep cap below H+1).  Sets the graph
@@ -1079,13 +1217,31 @@ void record_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
 
 // Enqueue one certified solve: the two-version backward pass, the proof, and the full
 // wavefront as the body of a graph IF node that runs only when the proof fails.
+//
+// Implicit spaces keep the (V_{m-1}, V_m) pairs by key-space index in two halves of the largest
+// layer key space (layer t in half t & 1); otherwise (and with VCS_CERT_BFS=1) by BFS index.
+bool cert_keyspace(const vcs_space* sp) {
+    return sp->implicit && sp->has_plan && !std::getenv("VCS_CERT_BFS");
+}
+uint64_t cert_half(const vcs_space* sp) {
+    uint64_t h = 1;
+    for (int t = 1; t <= sp->H; ++t)
+        h = std::max<uint64_t>(h, sp->plan.layers[static_cast<size_t>(t - 1)].dense_size);
+    return h;
+}
+uint64_t cert_pairs_needed(const vcs_space* sp) {
+    return cert_keyspace(sp) ? 2 * cert_half(sp) : sp->S;
+}
+
 void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaStream_t s,
                       bool capturing) {
     const bool disc = is_discounted(key.discount);
     const int H = sp->H;
     // (cert_xd / cert_lb are allocated before capture: an allocation inside a capture would
     // become a graph allocation node, and such a graph cannot be relaunched)
-    if (sp->cert_xd.n < sp->S || sp->cert_lb.n < static_cast<size_t>(H) + 2)
+    const bool ks = cert_keyspace(sp);
+    const uint64_t half = ks ? cert_half(sp) : 0;
+    if (sp->cert_xd.n < cert_pairs_needed(sp) || sp->cert_lb.n < static_cast<size_t>(H) + 2)
         raise(VCS_EINVAL, "certified solve buffers were not allocated");
     VCS_CUDA(cudaMemsetAsync(sp->ctrl.p, 0, sizeof(SolveCtrl), s));
     VCS_CUDA(cudaMemsetAsync(sp->cert_lb.p, 0, (H + 2) * sizeof(double), s));
@@ -1094,7 +1250,10 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
         const uint64_t rH = sp->layer_off[H], nH = sp->S - rH;
         VCS_CUDA(cudaMemsetAsync(sp->v[0].p + rH, 0, nH * sizeof(double), s));
         VCS_CUDA(cudaMemsetAsync(sp->actions_dev.p + rH, 0xff, nH * sizeof(int32_t), s));
-        VCS_CUDA(cudaMemsetAsync(sp->cert_xd.p + rH, 0, nH * sizeof(double2), s)); // V_0 = 0
+        if (ks) // the terminal layer's single state, key-space index 0
+            VCS_CUDA(cudaMemsetAsync(sp->cert_xd.p + (H & 1) * half, 0, sizeof(double2), s));
+        else
+            VCS_CUDA(cudaMemsetAsync(sp->cert_xd.p + rH, 0, nH * sizeof(double2), s)); // V_0 = 0
     }
     if (sp->implicit) { // implicit-CSR form: keys + rank tables; the fallback runs at collect
         CertImplArgs c{};
@@ -1111,18 +1270,34 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
             c.keys = sp->keys.p + sp->key_off[t];
             c.L = sp->params_dev.p + t;
             c.rank = sp->rank_tables.p + sp->rank_off[t];
-            c.xd_next = sp->cert_xd.p + sp->layer_off[t + 1];
-            c.xd_cur = sp->cert_xd.p + c.row0;
+            bool dense_order = false;
+            if (ks) {
+                c.xd_next = sp->cert_xd.p + ((t + 1) & 1) * half;
+                c.xd_cur = sp->cert_xd.p + (t & 1) * half;
+                c.dense_n = t >= 1 ? sp->plan.layers[static_cast<size_t>(t - 1)].dense_size : 0;
+                c.rank_self = t >= 1 ? sp->rank_tables.p + sp->rank_off[static_cast<size_t>(t - 1)] : nullptr;
+                c.write_own = t >= 1 ? 1 : 0;
+                // walk the key space when at least half of it is reached (coalesced pair
+                // writes, no key loads); sparse layers walk their states
+                dense_order = t >= 1 && c.n * 2 >= c.dense_n;
+            } else {
+                c.xd_next = sp->cert_xd.p + sp->layer_off[t + 1];
+                c.xd_cur = sp->cert_xd.p + c.row0;
+            }
             if (c.n) {
                 dispatch_words_solve(max_key_words(sp), [&](auto wm) {
                     constexpr int WM = decltype(wm)::value;
                     // 3 blocks per SM (80 registers, no spills): C4 0.68 ms vs 0.72 at 4, 0.74 at 2
-                    const void* fn = disc ? reinterpret_cast<const void*>(k_cert_implicit<WM, true, 3>)
-                                          : reinterpret_cast<const void*>(k_cert_implicit<WM, false, 3>);
+                    const void* fn =
+                        dense_order ? (disc ? reinterpret_cast<const void*>(k_cert_dense<WM, true, 3>)
+                                            : reinterpret_cast<const void*>(k_cert_dense<WM, false, 3>))
+                                    : (disc ? reinterpret_cast<const void*>(k_cert_implicit<WM, true, 3, false>)
+                                            : reinterpret_cast<const void*>(k_cert_implicit<WM, false, 3, false>));
                     int per_sm = 0;
                     VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
+                    const uint64_t items = dense_order ? c.dense_n : c.n;
                     const uint64_t blocks = std::max<uint64_t>(
-                        1, std::min<uint64_t>((c.n + 255) / 256,
+                        1, std::min<uint64_t>((items + 255) / 256,
                                               static_cast<uint64_t>(std::max(1, per_sm)) * sp->num_sms));
                     // layers after the first launch programmatically (PDL): their blocks load the
                     // layer constants and first keys while the previous layer drains.  Not with
@@ -1136,10 +1311,16 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
                     attr[0].val.programmaticStreamSerializationAllowed = 1;
                     cfg.attrs = attr;
                     cfg.numAttrs = (pdl && t < H - 1) ? 1 : 0;
-                    if (disc)
-                        VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, true, 3>, c));
-                    else
-                        VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, false, 3>, c));
+                    if (dense_order) {
+                        if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense<WM, true, 3>, c));
+                        else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense<WM, false, 3>, c));
+                    } else if (ks) {
+                        if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, true, 3, true>, c));
+                        else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, false, 3, true>, c));
+                    } else {
+                        if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, true, 3, false>, c));
+                        else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, false, 3, false>, c));
+                    }
                     VCS_LAUNCHED();
                 });
                 ++launches;
@@ -1476,8 +1657,8 @@ int enqueue_impl(vcs_space* sp, const vcs_solve_opts* opts, void* stream, int st
                 method = VCS_METHOD_JACOBI; // the version store does not fit right now
             }
         }
-        if (method == VCS_METHOD_CERTIFIED && sp->cert_xd.n < sp->S) {
-            sp->cert_xd.exact(sp->S, sp->stream);
+        if (method == VCS_METHOD_CERTIFIED && sp->cert_xd.n < vcs::cert_pairs_needed(sp)) {
+            sp->cert_xd.exact(vcs::cert_pairs_needed(sp), sp->stream);
             sp->cert_lb.exact(static_cast<size_t>(sp->H) + 2, sp->stream);
             VCS_CUDA(cudaStreamSynchronize(sp->stream));
         }

@@ -1126,6 +1126,9 @@ bool build_dense(vcs_space* sp, uint64_t state_cap) {
         sp->action.reserve(e_bound, 0, s);
     }
     sp->rank_tables.exact(rank_total, s);
+    // unreached successor indices read as kEmpty32 (the certified pass walks layers in key-space
+    // order and skips them)
+    if (rank_total) VCS_CUDA(cudaMemsetAsync(sp->rank_tables.p, 0xff, rank_total * sizeof(uint32_t), s));
     DevBuf<uint32_t> tables, bsum;
     DevBuf<uint64_t> desc;
     DevBuf<uint32_t> jfirst;
