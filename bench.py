@@ -538,13 +538,14 @@ def run_b200(args):
         tr = ncu_traffic(method)
         survey_equiv = b_ref * S * sweeps / sweep_s / 1e9  # SURVEY 8d bytes of the Jacobi sweeps
         if method == N.VCS_METHOD_CERTIFIED:
-            # k_cert_implicit (all H launches of one solve; the proof held, no fallback ran):
-            # implicit-CSR form, per non-terminal state key 8 + (V_{m-1}, V_m) pair written 16
-            # and read back 16, per state value 8 + action 4, the rank tables read once
+            # k_cert_dense on the full layers + k_cert_implicit on the sparse ones (all H
+            # launches of one solve; the proof held, no fallback ran): pairs by key-space index
             alg = model_bytes
-            formula = ("40*S_nonterminal + 12*S + 4*sum(rank-table entries) per solve "
-                       "(DESIGN.md 3.4)")
-            kernel = "k_cert_implicit<1,false,3> (all H layer launches of one solve)"
+            formula = ("per layer: full layers 4*key-space size (rank entries), sparse layers "
+                       "8*states (keys); + 28*states (value, action, pair written) + 16*states "
+                       "of layer t+1 (successor pairs read once) (DESIGN.md 3.4)")
+            kernel = ("k_cert_dense<1,false,3> on the full layers + k_cert_implicit<1,false,3,true> "
+                      "on the sparse ones (all H launches of one solve)")
         elif method == N.VCS_METHOD_WAVEFRONT:
             # k_wave_layer (all H launches of one solve, extraction fused): per state row_ptr 4
             # + value 8 + action 4 + winner's action 4, per edge succ 4 + reward 8, per

@@ -2002,8 +2002,26 @@ int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
                 // read once (4 B per entry)
                 const uint64_t nt = sp->layer_off[sp->H];
                 done = 2 * nt;
-                report->model_bytes = 40.0 * nt + 12.0 * sp->S +
-                                      4.0 * static_cast<double>(sp->rank_off.empty() ? 0 : sp->rank_off.back());
+                if (vcs::cert_keyspace(sp)) {
+                    // pairs by key-space index: per layer its own index (full layers: the rank
+                    // table entry of every key-space index, 4; sparse layers: the key, 8 per
+                    // word), per state value 8 + action 4 + pair written 16, and the
+                    // successors' pairs read once (16 per state of layer t+1)
+                    double b = 12.0 * static_cast<double>(sp->S - nt); // terminal value/action
+                    for (int t = 0; t < sp->H; ++t) {
+                        const uint64_t n = sp->layer_off[t + 1] - sp->layer_off[t];
+                        const uint64_t n1 = sp->layer_off[t + 2] - sp->layer_off[t + 1];
+                        const uint64_t dn = t >= 1 ? sp->plan.layers[static_cast<size_t>(t - 1)].dense_size : 0;
+                        const bool dense_order = t >= 1 && n * 2 >= dn;
+                        b += dense_order ? 4.0 * static_cast<double>(dn)
+                                         : 8.0 * static_cast<double>(n) * sp->plan.words[static_cast<size_t>(t)];
+                        b += 28.0 * static_cast<double>(n) + 16.0 * static_cast<double>(n1);
+                    }
+                    report->model_bytes = b;
+                } else {
+                    report->model_bytes = 40.0 * nt + 12.0 * sp->S +
+                                          4.0 * static_cast<double>(sp->rank_off.empty() ? 0 : sp->rank_off.back());
+                }
             } else if (certified) {
                 // two versions of every non-terminal state, once; per state: row_ptr 4 +
                 // value 8 + action 4 + winning action 4 + its (V_{m-1}, V_m) pair written 16 and

@@ -1,11 +1,11 @@
-"""Summarise an ncu --set full capture of k_wave_layer or k_cert_layer (C4,
+"""Summarise an ncu --set full capture of k_wave_layer or k_cert_dense (C4,
 tools/prof_sweep.py) into profiles/ncu_{wave,cert}.json: per captured launch, DRAM traffic vs
 the algorithmic bytes of that layer.
 
     python tools/ncu_summary.py gpurun_out/prof.ncu-rep <first_skip> [out.json] [wave|cert]
 
-`first_skip` is the -s value used for the capture: layer launches are numbered over two solves
-of H=48 layer launches each, layers descending (t = H-1 .. 0)."""
+`first_skip` is the -s value used for the capture: layer launches are numbered over solves of
+H=48 layer launches each (cert: the full layers only), layers descending (t = H-1 .. 0)."""
 import csv
 import io
 import json
@@ -25,9 +25,11 @@ def main(rep, skip, out=None, kind="wave"):
     H = lay["H"]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     launches = []
+    full = 531441  # C4 layer key space (9^6)
+    # cert: k_cert_dense runs the full layers (at least half of the key space reached)
+    order = [t for t in range(H - 1, -1, -1) if kind != "cert" or (t >= 1 and 2 * lay["layers"][t]["n"] >= full)]
     for j, r in enumerate(rows[2:]):
-        idx = (skip + j) % H
-        t = H - 1 - idx
+        t = order[(skip + j) % len(order)]
         n, e = lay["layers"][t]["n"], lay["layers"][t]["edges"]
         n_next = lay["layers"][t + 1]["n"]
         m = H - t
@@ -36,10 +38,10 @@ def main(rep, skip, out=None, kind="wave"):
         # once (8 * n_{t+1} * (m-1))
         alg = 20 * n + 12 * e + 8 * n * m + 8 * n_next * (m - 1)
         if kind == "cert":
-            # certified pass on the implicit-CSR form: per state its key 8 + value 8 + action 4
-            # + its (V_{m-1}, V_m) pair written 16; the successors' pairs read once
-            # (16 * n_{t+1}); the layer's rank table read once (4 per entry, C4: 9^6 entries)
-            alg = 36 * n + 16 * n_next + 4 * 531441
+            # k_cert_dense (pairs by key-space index, a thread per key-space index): the rank
+            # entry of every index 4, per state value 8 + action 4 + pair written 16, the
+            # successors' pairs read once (16 * n_{t+1})
+            alg = 4 * full + 28 * n + 16 * n_next
         g = lambda k: float(r[hdr.index(k)]) * scale.get(units[hdr.index(k)], 1)
         dram = g("dram__bytes_read.sum") + g("dram__bytes_write.sum")
         tt = float(r[hdr.index("gpu__time_duration.sum")]) * (1e-6 if units[hdr.index("gpu__time_duration.sum")] == "us" else 1e-9)
@@ -49,7 +51,7 @@ def main(rep, skip, out=None, kind="wave"):
                          "l2_hit_pct": float(r[hdr.index("lts__t_sector_hit_rate.pct")]),
                          "warps_active_pct": float(r[hdr.index("sm__warps_active.avg.pct_of_peak_sustained_active")]),
                          "issue_active_pct": float(r[hdr.index("smsp__issue_active.avg.pct_of_peak_sustained_active")])})
-    summary = {"kernel": "k_cert_implicit<1,false,3>" if kind == "cert" else "k_wave_layer<false>",
+    summary = {"kernel": "k_cert_dense<1,false,3>" if kind == "cert" else "k_wave_layer<false>",
                "capture": f"ncu --set full, C4, launches {skip}..{skip + len(launches) - 1} of tools/prof_sweep.py",
                "dram_bytes_per_launch": launches[0]["dram_bytes"],
                "alg_bytes_per_launch": launches[0]["alg_bytes"], "launches": launches,
