@@ -902,15 +902,18 @@ __device__ __forceinline__ void cert_dense_layer(const CertImplArgs& a, const La
         }
         if (r == kEmpty32) continue;
         const Slots sl(static_cast<uint64_t>(base) | (static_cast<uint64_t>(mask) << 32));
+        // branch-free over the 8 slots: an invalid slot's pair is -inf, which never wins the
+        // strict first maximum (and never raises lo)
         double2 x[SL];
 #pragma unroll
-        for (int e = 0; e < SL; ++e)
+        for (int e = 0; e < SL; ++e) {
+            x[e] = make_double2(-INFINITY, -INFINITY);
             if (sl.valid(e)) x[e] = __ldg(a.xd_next + dec.idx(sl, e));
+        }
         double hi = -INFINITY, lo = -INFINITY;
         int best = -1;
 #pragma unroll
         for (int e = 0; e < SL; ++e) {
-            if (!sl.valid(e)) continue;
             const int pe = e == SL - 1 ? -1 : e;
             double rw;
             if (retires) { // retiring_reward: beta*n - gamma*retired, two rounded operations
