@@ -1768,7 +1768,12 @@ public:
 
 private:
     HostWorkers() : pid_(getpid()) {
-        const unsigned hw = std::thread::hardware_concurrency();
+        unsigned hw = std::thread::hardware_concurrency();
+        // one process per GPU (torchrun): each takes its share of the host's cores
+        if (const char* lw = std::getenv("LOCAL_WORLD_SIZE")) {
+            const int n = std::atoi(lw);
+            if (n > 1) hw /= static_cast<unsigned>(n);
+        }
         unsigned cap = 7u; // 7..11 measured equal on the 16-core box; fewer lose, more lose
         if (const char* e = std::getenv("VCS_HOST_WORKERS")) cap = static_cast<unsigned>(std::atoi(e));
         const unsigned n = hw > 2 ? std::min(cap, hw - 1) : 0u;
