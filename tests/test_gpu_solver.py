@@ -458,6 +458,34 @@ def test_certified_full_size(gpu, golden):
         assert sha(r.policy.raw_actions()) == g["actions_sha"]
 
 
+@pytest.mark.parametrize("layout", ["keyspace", "bfs"])
+def test_certified_pair_layouts(gpu, golden, monkeypatch, layout):
+    """Both pair layouts of the implicit certified pass reproduce the reference digests. The
+    default layout stores pairs by key-space index: C4's full layers run k_cert_dense and its
+    sparse layers the BFS-order kernel. VCS_CERT_BFS=1 keeps pairs by BFS index with a
+    rank-table hop. The canonical instance covers the early stop (eps = 5): the proof fails
+    and the fallback runs at collect."""
+    if layout == "bfs":
+        monkeypatch.setenv("VCS_CERT_BFS", "1")
+    for gen, name in (((N.VCS_GEN_HOMOG, 2012, 0, 5, 8, 40, 3), "C3"),
+                      ((N.VCS_GEN_HOMOG, 2012, 0, 6, 8, 48, 3), "C4")):
+        ni = V.generate_instance(*gen, as_objects=False)
+        sp = V.StateSpace.build_native(ni, 10**9)  # a fresh space: a fresh graph
+        r = _solve(sp, method=N.VCS_METHOD_CERTIFIED)
+        g = golden["cases"][name]["eps=1e-06"]
+        assert r.values.report.method == N.VCS_METHOD_CERTIFIED
+        assert sha(r.values.raw_values()) == g["values_sha"]
+        assert sha(r.policy.raw_actions()) == g["actions_sha"]
+    p = V.load_instance(str(GOLDEN / "canonical_instance.txt"))
+    sp = V.StateSpace.build_native(V.NativeInstance(p.vcc, bots=p.bots))
+    for eps in (1e-6, 5.0):
+        r = _solve(sp, eps=eps, method=N.VCS_METHOD_AUTO)
+        g = golden["cases"]["canonical"][f"eps={eps:g}"]
+        assert r.values.sweeps() == g["sweeps"]
+        assert sha(r.values.raw_values()) == g["values_sha"]
+        assert sha(r.policy.raw_actions()) == g["actions_sha"]
+
+
 def test_builder_paths_agree(gpu, oracle, monkeypatch):
     """The persistent one-kernel builder (dense key spaces) and the layered multi-kernel builder
     produce identical CSR; a wide-capacity instance (key space far beyond the dense limit) takes
