@@ -156,6 +156,33 @@ def test_discounted_extension_matches_oracle(gpu, oracle, discount):
         assert np.array_equal(r.policy.raw_actions(), a)
 
 
+@pytest.mark.parametrize("discount", [1.0, 0.9, 0.5])
+def test_keyspace_certified_against_oracle(gpu, oracle, discount):
+    """A dense instance (implicit-CSR build, certified pass by key-space index: k_cert_dense on
+    the full layers, DISC and non-DISC kernels) against the oracle, bit for bit, every method."""
+    ni = V.generate_instance(N.VCS_GEN_HOMOG, 2012, 0, 4, 6, 20, 3, as_objects=False)
+    sp = V.StateSpace.build_native(ni, 10**9)
+    osp = oracle.build(ni.ref, 10**9)
+    v, a, sw, _, _ = osp.vi(discount=discount)
+    for method, skip in METHODS:
+        r = _solve(sp, discount=discount, skip=skip, method=method)
+        if method == N.VCS_METHOD_CERTIFIED:  # the key-space pass itself, not the fallback
+            assert r.values.report.method == N.VCS_METHOD_CERTIFIED
+        assert r.values.sweeps() == sw
+        assert np.array_equal(bits(r.values.raw_values()), bits(v))
+        assert np.array_equal(r.policy.raw_actions(), a)
+    # retiring clouds (random attributes): the retired-VM reward from the digits
+    for trial in range(3):
+        ni = V.generate_instance(N.VCS_GEN_RANDOM, 41, trial, 5, 6, 18, 3, as_objects=False)
+        sp = V.StateSpace.build_native(ni, 10**9)
+        osp = oracle.build(ni.ref, 10**9)
+        v, a, sw, _, _ = osp.vi(discount=discount)
+        r = _solve(sp, discount=discount, method=N.VCS_METHOD_CERTIFIED)
+        assert r.values.sweeps() == sw
+        assert np.array_equal(bits(r.values.raw_values()), bits(v))
+        assert np.array_equal(r.policy.raw_actions(), a)
+
+
 def test_capped_sweeps_match_oracle(gpu, oracle):
     """max_sweeps caps (bench sampling): both methods return V_M of the capped Jacobi run."""
     p = V.load_instance(str(GOLDEN / "canonical_instance.txt"))
