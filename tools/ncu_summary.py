@@ -28,8 +28,27 @@ def main(rep, skip, out=None, kind="wave"):
     full = 531441  # C4 layer key space (9^6)
     # cert: k_cert_dense runs the full layers (at least half of the key space reached)
     order = [t for t in range(H - 1, -1, -1) if kind != "cert" or (t >= 1 and 2 * lay["layers"][t]["n"] >= full)]
+    if kind == "sweep":  # Jacobi with the layer skip: sweep k = 1..H+1 covers layers 0..H-k+1
+        order = list(range(1, H + 2))
     for j, r in enumerate(rows[2:]):
         t = order[(skip + j) % len(order)]
+        if kind == "sweep":
+            k = t
+            last = min(H, H - k + 1)
+            rows_k = sum(x["n"] for x in lay["layers"][:last + 1])
+            edges_k = sum(x["edges"] for x in lay["layers"][:last + 1])
+            g = lambda name: float(r[hdr.index(name)]) * scale.get(units[hdr.index(name)], 1)
+            dram = g("dram__bytes_read.sum") + g("dram__bytes_write.sum")
+            tu = units[hdr.index("gpu__time_duration.sum")]
+            tt = float(r[hdr.index("gpu__time_duration.sum")]) * (1e-6 if tu == "us" else 1e-3 if tu == "ms" else 1e-9)
+            alg = 24 * rows_k + 12 * edges_k  # 24 + 12*E/S bytes per backup
+            launches.append({"sweep": k, "rows": rows_k, "edges": edges_k, "alg_bytes": alg,
+                             "dram_bytes": dram, "dram_over_alg": dram / alg,
+                             "ncu_time_us": tt * 1e6, "dram_GBps": dram / tt / 1e9,
+                             "l2_hit_pct": float(r[hdr.index("lts__t_sector_hit_rate.pct")]),
+                             "warps_active_pct": float(r[hdr.index("sm__warps_active.avg.pct_of_peak_sustained_active")]),
+                             "issue_active_pct": float(r[hdr.index("smsp__issue_active.avg.pct_of_peak_sustained_active")])})
+            continue
         n, e = lay["layers"][t]["n"], lay["layers"][t]["edges"]
         n_next = lay["layers"][t + 1]["n"]
         m = H - t
@@ -51,11 +70,12 @@ def main(rep, skip, out=None, kind="wave"):
                          "l2_hit_pct": float(r[hdr.index("lts__t_sector_hit_rate.pct")]),
                          "warps_active_pct": float(r[hdr.index("sm__warps_active.avg.pct_of_peak_sustained_active")]),
                          "issue_active_pct": float(r[hdr.index("smsp__issue_active.avg.pct_of_peak_sustained_active")])})
-    summary = {"kernel": "k_cert_dense<1,false,3>" if kind == "cert" else "k_wave_layer<false>",
+    summary = {"kernel": {"cert": "k_cert_dense<1,false,3>", "sweep": "k_sweep<false>"}.get(kind, "k_wave_layer<false>"),
                "capture": f"ncu --set full, C4, launches {skip}..{skip + len(launches) - 1} of tools/prof_sweep.py",
                "dram_bytes_per_launch": launches[0]["dram_bytes"],
                "alg_bytes_per_launch": launches[0]["alg_bytes"], "launches": launches,
-               "note": "dram/alg = %.2f on layer %d" % (launches[0]["dram_over_alg"], launches[0]["layer"])}
+               "note": "dram/alg = %.2f on %s %d" % (launches[0]["dram_over_alg"], "sweep" if kind == "sweep" else "layer",
+                                                     launches[0]["sweep" if kind == "sweep" else "layer"])}
     Path(out or ROOT / "profiles" / f"ncu_{kind}.json").write_text(json.dumps(summary, indent=1))
     print(json.dumps(summary, indent=1)[:1500])
 
