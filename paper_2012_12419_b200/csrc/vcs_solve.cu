@@ -1749,8 +1749,10 @@ public:
     // fn(begin, end) over [0, n) in pieces of `grain`; returns when every piece is done
     void parallel_for(size_t n, size_t grain, const std::function<void(size_t, size_t)>& fn) {
         if (n == 0) return;
-        // a forked child inherits this object but not the threads: work inline there
-        if (th_.empty() || n <= grain || getpid() != pid_) {
+        // a forked child inherits this object but not the threads: work inline there; so does a
+        // caller that finds the pool busy with another thread's job (one job at a time)
+        std::unique_lock<std::mutex> job(job_m_, std::try_to_lock);
+        if (th_.empty() || n <= grain || getpid() != pid_ || !job.owns_lock()) {
             fn(0, n);
             return;
         }
@@ -1804,6 +1806,7 @@ private:
     }
     const pid_t pid_;
     std::vector<std::thread> th_;
+    std::mutex job_m_; // held by the caller whose job the workers run
     std::mutex m_;
     std::condition_variable cv_, done_cv_;
     const std::function<void(size_t, size_t)>* job_ = nullptr;

@@ -609,3 +609,42 @@ def test_pinned_download_large(gpu, golden):
         assert rep.sweeps == g["sweeps"]
         assert sha(vals.numpy()) == g["values_sha"]
         assert sha(acts.numpy()) == g["actions_sha"]
+
+
+def test_concurrent_pinned_solves(gpu, golden):
+    """Two host threads, each with its own space, solve into pinned buffers at the same time:
+    the narrowed download's host workers serve one job at a time (the other caller widens
+    inline), and both results equal the reference digests (C ABI re-entrancy)."""
+    import threading
+    import torch
+    gen = (N.VCS_GEN_HOMOG, 2012, 0, 5, 8, 40, 3)  # C3
+    g = golden["cases"]["C3"]["eps=1e-06"]
+    out, errs = {}, []
+
+    def run(tag):
+        try:
+            ni = V.generate_instance(*gen, as_objects=False)
+            sp = V.StateSpace.build_native(ni, 10**9)
+            S = sp.size()
+            vals = torch.empty(S, dtype=torch.float64, pin_memory=True)
+            acts = torch.empty(S, dtype=torch.int32, pin_memory=True)
+            for _ in range(3):
+                opts = N.vcs_solve_opts(1e-6, 1, 0, 1.0, N.VCS_METHOD_AUTO)
+                rep = N.vcs_solve_report()
+                N.check(N.lib().vcs_solve(sp.handle, C.byref(opts),
+                                          C.cast(C.c_void_p(vals.data_ptr()), C.POINTER(C.c_double)),
+                                          C.cast(C.c_void_p(acts.data_ptr()), C.POINTER(C.c_int32)),
+                                          C.byref(rep)))
+                out.setdefault(tag, []).append((sha(vals.numpy()), sha(acts.numpy())))
+        except Exception as e:  # noqa: BLE001
+            errs.append(repr(e))
+
+    ts = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for tag in range(2):
+        for vs, as_ in out[tag]:
+            assert (vs, as_) == (g["values_sha"], g["actions_sha"])
