@@ -482,6 +482,173 @@ __global__ void __launch_bounds__(32) k_first_fit_spec(const GreedyDesc* __restr
     if (lane == 0) *D.paid = paid;
 }
 
+// The same first-fit with the 32 candidate evaluations of a chunk split over 4 warps (8 tasks
+// each); warp 0 resolves, validates and commits the chunk between two block barriers.
+template <int NL>
+__global__ void __launch_bounds__(128) k_first_fit_spec4(const GreedyDesc* __restrict__ descs) {
+    extern __shared__ __align__(128) int32_t sm[];
+    constexpr int kRing = kRingRows;
+    __shared__ __align__(8) uint64_t s_bar[kRingBlocks];
+    __shared__ uint32_t s_cap[NL][32]; // word w of level L: bit b = (free[32w+b] >= lvl[L])
+    __shared__ __align__(16) uint32_t s_any[32]; // ballot of each task of the chunk
+    __shared__ int s_j0;
+    const GreedyDesc D = descs[blockIdx.x];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr uint32_t kAll = 0xffffffffu;
+    if (D.T == 0) {
+        if (tid == 0) *D.paid = 0;
+        return;
+    }
+    constexpr int W = 32; // row stride of the fast path (words past ceil(K/32) are zero)
+    const int n_blocks = (D.T + kBlockRows - 1) / kBlockRows;
+    uint32_t* s_rows = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(sm) + spec_free_bytes(D.K));
+    int2* s_task = reinterpret_cast<int2*>(s_rows + static_cast<size_t>(kRing + kShadowRows) * W);
+    if (tid == 0) {
+        for (int k = 0; k < kRingBlocks; ++k) bar_init(&s_bar[k], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    int32_t* fr = sm; // free counts, cloud c at fr[c]
+    for (int c = tid; c < D.K; c += blockDim.x) fr[c] = D.free_vms[c];
+    for (int r = tid; r < kRing + kShadowRows; r += blockDim.x) s_task[r] = make_int2(0, 0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    int lvl[NL];
+#pragma unroll
+    for (int L = 0; L < NL; ++L) {
+        lvl[L] = L < D.n_levels ? D.levels[L] : 0x7fffffff;
+        if (warp == 0) {
+            uint32_t bits = 0;
+            if (L < D.n_levels)
+                for (int b = 0; b < 32; ++b) {
+                    const int c = lane * 32 + b;
+                    if (c < D.K && fr[c] >= lvl[L]) bits |= 1u << b;
+                }
+            s_cap[L][lane] = bits;
+        }
+    }
+    __syncthreads();
+    const uint32_t le = (2u << lane) - 1u; // lanes <= this one
+    int issued = 0, ready = 0;
+    auto issue = [&]() { // block `issued` into its ring slot (thread 0)
+        const int slot = issued & (kRingBlocks - 1);
+        const uint32_t row_bytes = kBlockRows * static_cast<uint32_t>(W) * 4u;
+        const uint32_t shadow = slot == 0 ? kShadowRows * (W * 4u + 8u) : 0u;
+        bar_expect_tx(&s_bar[slot], row_bytes + kBlockRows * 8u + shadow);
+        const uint32_t* src_rows = D.mask + static_cast<size_t>(issued) * kBlockRows * W;
+        const int2* src_task = D.task + static_cast<size_t>(issued) * kBlockRows;
+        bulk_g2s(&s_rows[static_cast<size_t>(slot) * kBlockRows * W], src_rows, row_bytes, &s_bar[slot]);
+        bulk_g2s(&s_task[slot * kBlockRows], src_task, kBlockRows * 8u, &s_bar[slot]);
+        if (slot == 0) {
+            bulk_g2s(&s_rows[static_cast<size_t>(kRing) * W], src_rows, kShadowRows * W * 4u, &s_bar[slot]);
+            bulk_g2s(&s_task[kRing], src_task, kShadowRows * 8u, &s_bar[slot]);
+        }
+        ++issued;
+    };
+    long long paid = 0;
+    for (int j0 = 0; j0 < D.T;) {
+        const int n = min(32, D.T - j0);
+        const int b0 = j0 / kBlockRows;
+        if (tid == 0)
+            while (issued < b0 + kRingBlocks && issued < n_blocks) issue();
+        const int need = min((j0 + 31) / kBlockRows, n_blocks - 1);
+        while (ready <= need) { // every thread waits for the blocks it reads
+            bar_wait(&s_bar[ready & (kRingBlocks - 1)], (ready / kRingBlocks) & 1);
+            ++ready;
+        }
+        {   // warp w evaluates tasks 8w .. 8w+7 of the chunk
+            const int r0 = j0 & (kRing - 1);
+            const uint32_t* rowp = s_rows + (r0 + warp * 8) * W + lane;
+            const int2* taskp = s_task + r0 + warp * 8;
+            uint32_t any[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t m = rowp[u * W] & s_cap[taskp[u].x][lane];
+                any[u] = __ballot_sync(kAll, m != 0);
+            }
+            if (lane == 0) {
+                uint4* dst = reinterpret_cast<uint4*>(s_any + warp * 8);
+                dst[0] = make_uint4(any[0], any[1], any[2], any[3]);
+                dst[1] = make_uint4(any[4], any[5], any[6], any[7]);
+            }
+        }
+        __syncthreads(); // the chunk's ballots are in; every read of s_cap is done
+        if (warp == 0) {
+            // lane u resolves task j0+u: the lowest lane with a feasible cloud, its lowest bit
+            const int rme = (j0 + lane) & (kRing - 1);
+            const int2 tk = s_task[rme];
+            const int lvme = lane < n ? tk.x : NL;
+            int my_c = -1;
+            {
+                const uint32_t any = s_any[lane];
+                if (lane < n && any) {
+                    const int src = __ffs(any) - 1;
+                    const uint32_t m = s_rows[rme * W + src] & s_cap[lvme][src];
+                    my_c = src * 32 + __ffs(m) - 1;
+                }
+            }
+            const bool placed = my_c >= 0;
+            int ncommit = n;
+            // common case first: take every placed demand off its candidate's free count.  The totals
+            // do not depend on the order, and every inclusive prefix fits iff no count went negative.
+            if (placed) atomicAdd(&fr[my_c], -tk.y);
+            __syncwarp();
+            const int fend = placed ? fr[my_c] : 0;
+            if (!__any_sync(kAll, fend < 0)) {
+                if (placed) { // clear the capacity bits the cloud lost (idempotent across its group)
+                    const uint32_t keep = ~(1u << (my_c & 31));
+#pragma unroll
+                    for (int L = 0; L < NL; ++L)
+                        if (fend < lvl[L]) atomicAnd(&s_cap[L][my_c >> 5], keep);
+                }
+            } else {
+                if (placed) atomicAdd(&fr[my_c], tk.y); // undo; commit the exact prefix instead
+                __syncwarp();
+                // same-candidate groups and the inclusive prefix of their demands (levels: popcounts)
+                const uint32_t peers = __match_any_sync(kAll, placed ? my_c : -1 - lane);
+                int pre = 0;
+#pragma unroll
+                for (int L = 0; L < NL; ++L)
+                    if (L < D.n_levels) pre += lvl[L] * __popc(peers & le & __ballot_sync(kAll, lvme == L));
+                const int f0 = placed ? fr[my_c] : 0;
+                const uint32_t fails = __ballot_sync(kAll, placed && f0 < pre);
+                ncommit = __ffs(fails) - 1; // >= 1: the first task fits S0
+                const uint32_t cmask = (1u << ncommit) - 1u;
+                __syncwarp();
+                // the last committed member of each group writes its cloud's new free count and
+                // clears the capacity bits the cloud lost
+                if (placed && lane < ncommit && !(peers & cmask & ~le)) {
+                    const int f1 = f0 - pre;
+                    fr[my_c] = f1;
+                    const uint32_t keep = ~(1u << (my_c & 31));
+#pragma unroll
+                    for (int L = 0; L < NL; ++L)
+                        if (f1 < lvl[L]) atomicAnd(&s_cap[L][my_c >> 5], keep);
+                }
+            }
+            const bool commit = lane < ncommit;
+            if (commit) {
+                D.target[j0 + lane] = my_c;
+                if (!placed) paid += tk.y;
+            }
+            __syncwarp();
+            if (lane == 0) s_j0 = j0 + ncommit;
+        }
+        __syncthreads(); // the commit and the next start are visible
+        j0 = s_j0;
+    }
+    while (ready < issued) { // drain the bulk copies still in flight (thread 0)
+        bar_wait(&s_bar[ready & (kRingBlocks - 1)], (ready / kRingBlocks) & 1);
+        ++ready;
+    }
+    if (warp == 0) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) paid += __shfl_xor_sync(kAll, paid, o);
+        __syncwarp();
+        for (int c = lane; c < D.K; c += 32) D.free_vms[c] = fr[c];
+        if (lane == 0) *D.paid = paid;
+    }
+}
+
 struct HostGreedy {
     int K, T, W, n_levels;
     std::vector<int32_t> levels;
@@ -603,18 +770,29 @@ void launch_first_fit(const GreedyDesc* d_descs, int n, size_t smem, bool fast, 
                                           static_cast<int>(fs)));
             kern<<<n, 32, fs, s>>>(d_descs);
         };
+        auto go4 = [&](auto kern) {
+            VCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(fs)));
+            kern<<<n, 128, fs, s>>>(d_descs);
+        };
         if (serial) {
             if (max_levels <= 1) go(k_first_fit_fast<1>);
             else if (max_levels <= 2) go(k_first_fit_fast<2>);
             else if (max_levels <= 3) go(k_first_fit_fast<3>);
             else if (max_levels <= 4) go(k_first_fit_fast<4>);
             else go(k_first_fit_fast<kFastLevels>);
-        } else {
+        } else if (std::getenv("VCS_GREEDY_1WARP")) {
             if (max_levels <= 1) go(k_first_fit_spec<1>);
             else if (max_levels <= 2) go(k_first_fit_spec<2>);
             else if (max_levels <= 3) go(k_first_fit_spec<3>);
             else if (max_levels <= 4) go(k_first_fit_spec<4>);
             else go(k_first_fit_spec<kFastLevels>);
+        } else {
+            if (max_levels <= 1) go4(k_first_fit_spec4<1>);
+            else if (max_levels <= 2) go4(k_first_fit_spec4<2>);
+            else if (max_levels <= 3) go4(k_first_fit_spec4<3>);
+            else if (max_levels <= 4) go4(k_first_fit_spec4<4>);
+            else go4(k_first_fit_spec4<kFastLevels>);
         }
     } else {
         VCS_CUDA(cudaFuncSetAttribute(k_first_fit, cudaFuncAttributeMaxDynamicSharedMemorySize,
