@@ -293,6 +293,8 @@ __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 constexpr int kRingBlocks = 4;   // blocks of attribute rows staged in shared memory
+// warps of k_first_fit_spec4 (32 / kSpecWarps tasks each): C2 1.83 ms at 8, 1.94 ms at 4
+constexpr int kSpecWarps = 8;
 constexpr int kBlockRows = 128;  // rows per bulk copy (task arrays are padded to whole blocks)
 constexpr int kRingRows = kRingBlocks * kBlockRows;
 constexpr int kShadowRows = 32;  // ring rows 0..31 repeated past the end: a chunk never wraps
@@ -482,10 +484,11 @@ __global__ void __launch_bounds__(32) k_first_fit_spec(const GreedyDesc* __restr
     if (lane == 0) *D.paid = paid;
 }
 
-// The same first-fit with the 32 candidate evaluations of a chunk split over 4 warps (8 tasks
-// each); warp 0 resolves, validates and commits the chunk between two block barriers.
-template <int NL>
-__global__ void __launch_bounds__(128) k_first_fit_spec4(const GreedyDesc* __restrict__ descs) {
+// The same first-fit with the 32 candidate evaluations of a chunk split over NW warps (32/NW
+// tasks each); warp 0 resolves, validates and commits the chunk between two block barriers.
+template <int NL, int NW>
+__global__ void __launch_bounds__(NW * 32) k_first_fit_spec4(const GreedyDesc* __restrict__ descs) {
+    constexpr int TPW = 32 / NW; // tasks per warp
     extern __shared__ __align__(128) int32_t sm[];
     constexpr int kRing = kRingRows;
     __shared__ __align__(8) uint64_t s_bar[kRingBlocks];
@@ -555,20 +558,21 @@ __global__ void __launch_bounds__(128) k_first_fit_spec4(const GreedyDesc* __res
             bar_wait(&s_bar[ready & (kRingBlocks - 1)], (ready / kRingBlocks) & 1);
             ++ready;
         }
-        {   // warp w evaluates tasks 8w .. 8w+7 of the chunk
+        {   // warp w evaluates tasks TPW*w .. TPW*w + TPW-1 of the chunk
             const int r0 = j0 & (kRing - 1);
-            const uint32_t* rowp = s_rows + (r0 + warp * 8) * W + lane;
-            const int2* taskp = s_task + r0 + warp * 8;
-            uint32_t any[8];
+            const uint32_t* rowp = s_rows + (r0 + warp * TPW) * W + lane;
+            const int2* taskp = s_task + r0 + warp * TPW;
+            uint32_t any[TPW];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < TPW; ++u) {
                 const uint32_t m = rowp[u * W] & s_cap[taskp[u].x][lane];
                 any[u] = __ballot_sync(kAll, m != 0);
             }
             if (lane == 0) {
-                uint4* dst = reinterpret_cast<uint4*>(s_any + warp * 8);
-                dst[0] = make_uint4(any[0], any[1], any[2], any[3]);
-                dst[1] = make_uint4(any[4], any[5], any[6], any[7]);
+                uint4* dst = reinterpret_cast<uint4*>(s_any + warp * TPW);
+#pragma unroll
+                for (int q = 0; q < TPW / 4; ++q)
+                    dst[q] = make_uint4(any[4 * q], any[4 * q + 1], any[4 * q + 2], any[4 * q + 3]);
             }
         }
         __syncthreads(); // the chunk's ballots are in; every read of s_cap is done
@@ -773,7 +777,7 @@ void launch_first_fit(const GreedyDesc* d_descs, int n, size_t smem, bool fast, 
         auto go4 = [&](auto kern) {
             VCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(fs)));
-            kern<<<n, 128, fs, s>>>(d_descs);
+            kern<<<n, kSpecWarps * 32, fs, s>>>(d_descs);
         };
         if (serial) {
             if (max_levels <= 1) go(k_first_fit_fast<1>);
@@ -788,11 +792,11 @@ void launch_first_fit(const GreedyDesc* d_descs, int n, size_t smem, bool fast, 
             else if (max_levels <= 4) go(k_first_fit_spec<4>);
             else go(k_first_fit_spec<kFastLevels>);
         } else {
-            if (max_levels <= 1) go4(k_first_fit_spec4<1>);
-            else if (max_levels <= 2) go4(k_first_fit_spec4<2>);
-            else if (max_levels <= 3) go4(k_first_fit_spec4<3>);
-            else if (max_levels <= 4) go4(k_first_fit_spec4<4>);
-            else go4(k_first_fit_spec4<kFastLevels>);
+            if (max_levels <= 1) go4(k_first_fit_spec4<1, kSpecWarps>);
+            else if (max_levels <= 2) go4(k_first_fit_spec4<2, kSpecWarps>);
+            else if (max_levels <= 3) go4(k_first_fit_spec4<3, kSpecWarps>);
+            else if (max_levels <= 4) go4(k_first_fit_spec4<4, kSpecWarps>);
+            else go4(k_first_fit_spec4<kFastLevels, kSpecWarps>);
         }
     } else {
         VCS_CUDA(cudaFuncSetAttribute(k_first_fit, cudaFuncAttributeMaxDynamicSharedMemorySize,
