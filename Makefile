@@ -11,6 +11,7 @@ ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
 CXXFLAGS  := -O2 -std=c++17 -fPIC -Wall -Wextra -ffp-contract=off -I$(CUDA)/include
 REF       ?= /root/reference/proj
+REF_CXX   := $(shell test -x /usr/bin/g++ && echo /usr/bin/g++ || echo $(CXX))
 JSON_INC  ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
 
 CU_SRCS   := $(SRC)/vcs_space.cu $(SRC)/vcs_solve.cu $(SRC)/vcs_greedy.cu
@@ -47,13 +48,15 @@ $(ORACLE): oracle/vcs_oracle.c include/vcs_gpu.h
 
 # The unmodified reference, compiled from its own sources where they lie (never copied), with
 # the reference's Release flags (-O3 -DNDEBUG, no -march), plus the C shim of oracle/ref_capi.cpp.
+# Linked against the system's shared libstdc++ (the one numpy/torch load): a toolchain wrapper that
+# links libstdc++ statically made the reference's iostream parser crash inside such a process.
 ref:
 	@if [ -d $(REF)/core/src ]; then $(MAKE) --no-print-directory $(REFLIB) $(REF_SUITES); \
 	 else echo "reference sources absent: using the prebuilt $(REFLIB) if present"; fi
 
 $(REFLIB): oracle/ref_capi.cpp include/vcs_gpu.h
 	@mkdir -p oracle/_ref
-	$(CXX) -std=c++20 -O3 -DNDEBUG -fPIC -shared -pthread -I$(REF)/core/include -I$(REF)/tests -I$(JSON_INC) \
+	$(REF_CXX) -std=c++20 -O3 -DNDEBUG -fPIC -shared -pthread -I$(REF)/core/include -I$(REF)/tests -I$(JSON_INC) \
 	    -o $@ $(REF)/core/src/*.cpp oracle/ref_capi.cpp
 
 # The reference's OWN solver test suites (doctest files compiled where they lie, unchanged),

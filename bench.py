@@ -1,18 +1,23 @@
 #!/usr/bin/env python
 """Benchmark of the B200 solver path: fp64 value iteration on the ~10^7-state VC MDP.
 
-Metric (BASELINE.json): Bellman state-action backups/sec and time-to-convergence.
-  step   = one complete solve (all Jacobi sweeps until `delta < eps` + policy extraction,
-           the reference's time-to-convergence convention, parallel_vi.cpp:126-147) on the
-           device-resident prebuilt space of SURVEY §8(d) C4 (19,333,781 states).
-  value  = reference-equivalent backups/s = n_states * sweeps * steps / device time (whole job).
-  e2e    = the same metric through the C ABI with HOST buffers: per step vcs_space_build from
-           the host instance (H2D) + vcs_solve into pinned host values/actions (D2H).
+Metric (BASELINE.json): time-to-convergence and Bellman state-action backups/sec.
+  step   = one complete solve (value iteration until `delta < eps` + policy extraction, the
+           reference's time-to-convergence convention, parallel_vi.cpp:126-147) on the
+           device-resident prebuilt space of SURVEY 8(d) C4 (19,333,781 states).
+  value  = time-to-convergence in ms per solve (device time / steps; lower is better).  The
+           backups/s beside it are reported twice: performed (what the kernels computed) and
+           reference-equivalent (n_states * sweeps, the work a per-sweep solver does).
+  e2e    = the same metric through the C ABI with HOST buffers: per step vcs_instance_parse of
+           the instance text + vcs_space_build (H2D) + vcs_solve into pinned host
+           values/actions (D2H).
   --impl reference : the unmodified reference CPU solver (oracle/_ref/libvcsref.so,
-           detail::run_value_iteration with all host threads) on the same config.
+           detail::run_value_iteration with all host threads) on the same instance file, read
+           by the reference's own parser; this arm never loads the product library.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...   (row-block sharded, NCCL halo exchange)
+                    [--workload c4|c3|c1|c5]
+    torchrun --nproc-per-node N bench.py --gpus N ...
 """
 from __future__ import annotations
 
@@ -32,14 +37,11 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-WORKLOADS = {
-    # name: (generator args, description)
-    "c4": ((1, 2012, 0, 6, 8, 48, 3),
-           "C4: 6 clouds x 8 VMs, 48 tasks demand U[1,3] (mt19937_64 seed 2012), 6 bags"),
-    "c3": ((1, 2012, 0, 5, 8, 40, 3),
-           "C3: 5 clouds x 8 VMs, 40 tasks demand U[1,3] (mt19937_64 seed 2012), 5 bags"),
-}
-METRIC = "Bellman state-action backups/sec (fp64 value iteration to eps=1e-6, time-to-convergence)"
+import bench_workloads as W  # noqa: E402  (pure Python: no product / oracle import)
+
+METRIC = ("time-to-convergence (fp64 value iteration to eps=1e-6 + policy extraction on the "
+          "prebuilt state space; Bellman backups/s beside it)")
+UNIT = "ms"
 
 
 def log(*a):
@@ -132,81 +134,105 @@ def ncu_traffic(method):
         return None
 
 
-def cpu_baseline(space, opts_eps):
-    """The C oracle's Jacobi port on the SAME CSR (downloaded from HBM), all host threads,
-    full solves repeated for ~10 s.  Test infrastructure: only this leg runs oracle/."""
+def common_config(workload, S, H, sweeps, eps):
+    """The `config` dict both arms print (identical keys and values)."""
+    return {"workload": W.DESCRIPTIONS.get(workload, workload), "states": int(S),
+            "horizon": int(H), "sweeps": int(sweeps), "epsilon": eps,
+            "instance": str(W.FILES[workload].relative_to(ROOT)) if workload in W.FILES else None}
+
+
+def _reference():
     sys.path.insert(0, str(ROOT / "tests"))
-    from oracle_bind import Oracle
-    orc = Oracle()
-    rp, su, rw, ac = space.csr()
-    lo = space.layer_offsets()
-    osp = orc.wrap(lo, rp, su, rw, ac)
-    threads = os.cpu_count() or 1
-    rates, t_total, runs = [], 0.0, 0
-    while runs < 1 or (t_total < 10.0 and runs < 20):
-        v, a, sw, t_sw, t_ex = osp.vi(eps=opts_eps, workers=threads)
-        t = (t_sw + t_ex) * 1e-3
-        rates.append(osp.S * sw / t)
-        t_total += t
-        runs += 1
-    return {"value": max(rates), "unit": "backups/s", "cores": threads, "kind": "port",
-            "sample": f"{runs} full solve(s) ({sw} sweeps + extraction each, {t_total:.1f} s) of "
-                      f"oracle/vcs_oracle.c orc_vi on the device-built C4 CSR, {threads} threads",
-            "time_to_convergence_ms": t_total / runs * 1e3}
+    from oracle_bind import Reference
+    return Reference(standalone=True)
+
+
+def cpu_solve_timing(ref, inst, eps, workers, budget_s, min_runs=1, max_runs=20):
+    """The unmodified reference (detail::run_value_iteration on a prebuilt StateSpace, the
+    reference's own timing convention) repeated for about `budget_s` seconds."""
+    sp = inst.build(10**9)
+    times, sweeps = [], 0
+    while len(times) < min_runs or (sum(times) < budget_s and len(times) < max_runs):
+        r = sp.vi(eps=eps, workers=workers)
+        times.append(r.ms)
+        sweeps = r.sweeps
+        del r
+    return sp, times, sweeps
+
+
+def cpu_baseline(workload, eps):
+    """bench's cpu_baseline leg: the unmodified reference (oracle/_ref, kind "reference") on the
+    same instance file, all host threads, full solves for ~10-20 s (test infrastructure: only this
+    leg and --impl reference run oracle/)."""
+    ref = _reference()
+    inst = ref.load(W.FILES[workload])
+    threads = ref.threads()
+    sp, times, sweeps = cpu_solve_timing(ref, inst, eps, threads, 15.0)
+    ms = statistics.median(times)
+    return {"value": ms, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{len(times)} full solve(s) ({sweeps} sweeps + extraction each, "
+                      f"{sum(times) / 1e3:.1f} s) of the unmodified reference "
+                      f"detail::run_value_iteration on {W.FILES[workload].name}, {threads} threads",
+            "time_to_convergence_ms": ms, "build_ms": sp.build_ms,
+            "backups_per_s": sp.S * sweeps / (ms * 1e-3)}
+
+
+def reference_greedy(ref, repeats=3):
+    """greedy_schedule of the unmodified reference on C2, timed on this box (single-threaded by
+    design, greedy.cpp:5-30)."""
+    inst = ref.generate(*W.C2_GEN)
+    runs = [inst.greedy() for _ in range(repeats)]
+    return runs[0], statistics.median(r["ms"] for r in runs)
 
 
 def run_reference(args):
-    """--impl reference: the unmodified reference solver on the host cores (rank 0 only)."""
+    """--impl reference: the unmodified reference solver on the host cores (rank 0 only), the
+    same instance file read by the reference's own parser; never loads the product library."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    sys.path.insert(0, str(ROOT / "tests"))
-    import paper_2012_12419_b200 as V
     try:
-        from oracle_bind import Reference
-        ref = Reference()
+        ref = _reference()
     except Exception as e:  # noqa: BLE001
         print(json.dumps({"impl": "reference", "unavailable": f"reference library: {e}"}))
         return 0
-    gen, desc = WORKLOADS[args.workload]
-    ni = V.generate_instance(*gen, as_objects=False)
-    log(f"[reference] building the state space with StateSpace::build ({desc}) ...")
-    sp = ref.build(ni.ref, 10**9)
+    workload = args.workload if args.workload in W.FILES else "c4"
+    inst = ref.load(W.FILES[workload])
+    log(f"[reference] StateSpace::build of {W.FILES[workload].name} ...")
+    sp = inst.build(10**9)
     workers = ref.threads()
-    budget_s = float(os.environ.get("VCS_REF_BUDGET_S", "150"))
     times, sweeps = [], 0
-    t_start = time.time()
-    for i in range(max(0, min(args.warmup, 1))):
+    for _ in range(args.warmup):
         r = sp.vi(eps=args.eps, workers=workers)
         sweeps = r.sweeps
         del r
-    steps = 0
-    while steps < args.steps:
+    for _ in range(args.steps):
         r = sp.vi(eps=args.eps, workers=workers)
-        times.append(r.ms * 1e-3)
+        times.append(r.ms)
         sweeps = r.sweeps
         del r
-        steps += 1
-        if time.time() - t_start > budget_s:
-            break
-    total = sum(times)
-    value = sp.S * sweeps * steps / total
+    total_ms = sum(times)
+    ms = total_ms / len(times)
+    greedy, greedy_ms = reference_greedy(ref)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "backups/s",
-        "n_gpus": args.gpus, "steps": steps, "warmup": min(args.warmup, 1),
-        "ms_per_step": total / steps * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": desc, "states": sp.S, "sweeps": sweeps, "epsilon": args.eps,
-                   "build_ms_excluded": sp.build_ms,
-                   "timing": "detail::run_value_iteration on a prebuilt StateSpace "
-                             "(reference convention, parallel_vi.cpp:126-147), steady_clock"},
-        "time_to_convergence_ms": total / steps * 1e3,
-        "cpu_baseline": {"value": value, "unit": "backups/s", "cores": workers,
-                         "kind": "reference",
-                         "sample": f"{steps} full solve(s) of the unmodified reference "
-                                   f"(oracle/_ref/libvcsref.so), {workers} worker threads"},
-        "e2e": {"value": value, "unit": "backups/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": ms, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": common_config(workload, sp.S, sp.H, sweeps, args.eps),
+        "time_to_convergence_ms": ms,
+        "backups_per_s": {"performed": sp.S * sweeps / (ms * 1e-3),
+                          "reference_equivalent": sp.S * sweeps / (ms * 1e-3)},
+        "timing": "detail::run_value_iteration on a prebuilt StateSpace (reference convention, "
+                  "parallel_vi.cpp:126-147), steady_clock; StateSpace::build excluded",
+        "build_ms_excluded": sp.build_ms,
+        "cpu_baseline": {"value": ms, "unit": UNIT, "cores": workers, "kind": "reference",
+                         "sample": f"{len(times)} full solve(s) after {args.warmup} warm-up of the "
+                                   f"unmodified reference (oracle/_ref/libvcsref.so), "
+                                   f"{workers} worker threads"},
+        "e2e": {"value": ms, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "greedy": {"workload": W.DESCRIPTIONS["c2"], "reference_ms": greedy_ms,
+                   "paid": greedy["paid"], "unused_vms": greedy["unused"]},
     }
     print(json.dumps(line))
     return 0
@@ -263,7 +289,7 @@ def e2e_sharded(args, ni, local, dev, stream, opts, sharding, S, rank):
     # summed over ranks
     d2h = S * (8 + 4)
     e2e_t = statistics.median(times)
-    return {"value": S * K / e2e_t, "unit": "backups/s",
+    return {"value": e2e_t * 1e3, "unit": UNIT, "sweeps": K,
             "h2d_bytes_per_step": inst_bytes * dist.get_world_size(),
             "d2h_bytes_per_step": d2h, "ms_per_step": e2e_t * 1e3,
             "path": f"per rank: vcs_space_build(host instance) + sharded solve ({sharding}) + "
@@ -301,9 +327,10 @@ def full_work_methods(space, args, stream):
 
 def greedy_c2(V, N):
     """BASELINE configs[1] beside the headline: greedy first-fit placement of 10^5 tasks over
-    10^3 clouds through the C ABI from host SoA arrays to host placements
-    (tests/test_gpu_greedy.py checks the placements bit-exact against the reference)."""
-    ni = V.generate_instance(N.VCS_GEN_GREEDY, 12345, 0, 1000, 100, 1000, 3, as_objects=False)
+    10^3 clouds through the C ABI from host SoA arrays to host placements, next to
+    the unmodified reference's greedy_schedule timed on this box in the same run (its
+    placements are compared element by element)."""
+    ni = V.generate_instance(*W.C2_GEN[:2], 0, *W.C2_GEN[2:], as_objects=False)
     tgt = np.empty(100000, np.int32)
     paid, unused = C.c_int64(), C.c_int64()
     ts = []
@@ -313,17 +340,157 @@ def greedy_c2(V, N):
                                    C.byref(unused)))
         ts.append((time.perf_counter() - t0) * 1e3)
     e2e = statistics.median(ts[2:])
-    import hashlib
-    golden = json.loads((ROOT / "tests" / "golden" / "golden.json").read_text())["cases"]["C2"]
-    exact = hashlib.sha256(np.ascontiguousarray(tgt).tobytes()).hexdigest() == \
-        golden["greedy"]["targets_sha"]
-    return {"workload": "C2: 1000 clouds x 100 VMs, 10^5 tasks demand U[1,3] (seed 12345)",
-            "placements_equal_reference": exact,
-            "e2e_ms": e2e, "tasks_per_s": 1e5 / (e2e * 1e-3), "paid": paid.value,
-            "unused_vms": unused.value,
-            "reference_ms_container": 306.7,
-            "note": "reference_ms_container: the unmodified reference's greedy_schedule on the "
-                    "build container's cores (tests/golden/golden.json C2.ref_ms)"}
+    out = {"workload": W.DESCRIPTIONS["c2"], "e2e_ms": e2e, "tasks_per_s": 1e5 / (e2e * 1e-3),
+           "paid": paid.value, "unused_vms": unused.value}
+    try:
+        ref = _reference()
+        g, ref_ms = reference_greedy(ref)
+        ids = np.asarray(ni.arrays()["cloud_id"])
+        ours = np.where(tgt >= 0, ids[np.clip(tgt, 0, None)], tgt)
+        out.update({"reference_ms": ref_ms, "speedup_vs_reference": ref_ms / e2e,
+                    "placements_equal_reference": bool(np.array_equal(ours, g["target_ids"])),
+                    "reference_cores": 1})
+    except Exception as e:  # noqa: BLE001
+        out["reference_error"] = str(e)
+    return out
+
+
+def solve_timing(N, space, opts, stream, warmup, steps):
+    """Device time of `steps` back-to-back solves on `stream` after `warmup` (CUDA events on the
+    launching stream, synchronize on both sides).  Returns (total_ms, report, launches)."""
+    import torch
+    h_stream = C.c_void_p(stream.cuda_stream)
+    rep = N.vcs_solve_report()
+    for _ in range(max(1, warmup)):
+        N.check(N.lib().vcs_solve_enqueue(space.handle, C.byref(opts), h_stream))
+    N.check(N.lib().vcs_solve_collect(space.handle, None, None, C.byref(rep), h_stream))
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = N.kernel_launches()
+    ev0.record(stream)
+    for _ in range(steps):
+        N.check(N.lib().vcs_solve_enqueue(space.handle, C.byref(opts), h_stream))
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    launches = N.kernel_launches() - launches0
+    N.check(N.lib().vcs_solve_collect(space.handle, None, None, C.byref(rep), h_stream))
+    return ev0.elapsed_time(ev1), rep, launches
+
+
+def e2e_c_abi(N, text, opts, device, steps, S):
+    """End to end through the C ABI with host buffers, per step: vcs_instance_parse of the
+    instance text, vcs_space_build (the instance crosses H2D), vcs_solve into pinned host
+    values/actions (the 12 B/state result crosses D2H), vcs_space_free.  Wall clock per step
+    (every call returns only when its outputs are complete)."""
+    import torch
+    vals = torch.empty(S, dtype=torch.float64, pin_memory=True)
+    acts = torch.empty(S, dtype=torch.int32, pin_memory=True)
+    vp = C.cast(C.c_void_p(vals.data_ptr()), C.POINTER(C.c_double))
+    ap = C.cast(C.c_void_p(acts.data_ptr()), C.POINTER(C.c_int32))
+    times, parts, inst_bytes, rep = [], [], 0, None
+    warm = 2  # the stream-ordered pool reaches its steady size after two builds
+    for i in range(steps + warm):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ih = C.c_void_p()
+        N.check(N.lib().vcs_instance_parse(text.encode(), C.byref(ih)))
+        inst = N.lib().vcs_instance_view(ih)
+        h = C.c_void_p()
+        N.check(N.lib().vcs_space_build(inst, 10**9, device, C.byref(h)))
+        tb = time.perf_counter()
+        rep = N.vcs_solve_report()
+        N.check(N.lib().vcs_solve(h, C.byref(opts), vp, ap, C.byref(rep)))
+        t1 = time.perf_counter()
+        s = inst.contents
+        inst_bytes = s.n_clouds * (3 * 4 + 2 * 8) + s.n_tasks * (2 * 4 + 2 * 8)
+        n_clouds = s.n_clouds
+        N.lib().vcs_space_free(h)
+        N.lib().vcs_instance_free(ih)
+        if i >= warm:
+            times.append(t1 - t0)
+            parts.append((tb - t0, t1 - tb))
+    act_wire = 1 if (n_clouds <= 127 and not os.environ.get("VCS_NO_NARROW")) else 4
+    t = statistics.median(times)
+    return {"value": t * 1e3, "unit": UNIT, "h2d_bytes_per_step": inst_bytes,
+            "d2h_bytes_per_step": S * (8 + act_wire),
+            "d2h_result_bytes_per_step": S * (8 + 4), "ms_per_step": t * 1e3,
+            "parse_and_build_ms": statistics.median(p[0] for p in parts) * 1e3,
+            "solve_and_d2h_ms": statistics.median(p[1] for p in parts) * 1e3,
+            "sweeps": rep.sweeps,
+            "path": "vcs_instance_parse(text) + vcs_space_build + vcs_solve(pinned host "
+                    "values/actions; the int8 action column is widened to int32 on host "
+                    "threads) + vcs_space_free",
+            "steps": len(times)}
+
+
+def roofline_for(N, method, model_bytes, alg_bytes_done, solve_ms, S, sweeps, dbar):
+    peak, peak_src = measured_peaks()
+    tr = ncu_traffic(method)
+    b_ref = 24 + 12 * dbar
+    survey_equiv = b_ref * S * sweeps / (solve_ms * 1e-3) / 1e9
+    if method == N.VCS_METHOD_CERTIFIED:
+        alg = model_bytes
+        formula = ("per layer: full layers 4*key-space size (rank entries), sparse layers "
+                   "8*states (keys); + 28*states (value, action, pair written) + 16*states "
+                   "of layer t+1 (successor pairs read once) (DESIGN.md 3.4)")
+        kernel = ("k_cert_dense on the full layers + k_cert_implicit on the sparse ones (all "
+                  "layer launches of one solve)")
+    elif method == N.VCS_METHOD_WAVEFRONT:
+        alg = model_bytes
+        formula = "20*S + 12*E + 16*backups_performed per solve (DESIGN.md 3.3)"
+        kernel = "k_wave_layer<false> (all H layer launches of one solve)"
+    else:
+        alg = alg_bytes_done
+        formula = "24 + 12*E/S per performed backup (SURVEY 8d)"
+        kernel = "k_sweep<false> (all sweep launches of one solve)"
+    achieved = alg / (solve_ms * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak,
+            "traffic": tr.get("dram_bytes_per_launch") if tr else None,
+            "traffic_alg_bytes_per_launch": tr.get("alg_bytes_per_launch") if tr else None,
+            "kernel": kernel, "alg_bytes_per_solve": alg, "alg_bytes_formula": formula,
+            "survey_B_equivalent_GBps": survey_equiv,
+            "survey_B_note": "SURVEY 8d Jacobi bytes (24+12*E/S per backup x S x sweeps) over the "
+                             "same time: the traffic a per-sweep solver would need to stream "
+                             "for this result",
+            "peak_source": peak_src, "traffic_note": (tr or {}).get("note")}
+
+
+def side_workload(V, N, name, eps, stream, local, steps=20):
+    """A smaller configuration beside the headline (C1 canonical, C3): device
+    time-to-convergence, e2e through the C ABI and the unmodified reference on the same file."""
+    text = W.instance_text(name)
+    p = V.parse_instance(text)
+    ni = V.MdpInstance.from_workload(p.vcc, p.bots).native()
+    space = V.StateSpace.build_native(ni, 10**9, local)
+    opts = N.vcs_solve_opts(eps, 1, 0, 1.0, N.VCS_METHOD_AUTO)
+    total_ms, rep, launches = solve_timing(N, space, opts, stream, 3, steps)
+    ms = total_ms / steps
+    S = space.size()
+    out = {"workload": W.DESCRIPTIONS[name], "states": S, "transitions": space.edges(),
+           "sweeps": rep.sweeps, "time_to_convergence_ms": ms,
+           "method": METHODS.get(rep.method, str(rep.method)),
+           "backups_performed_per_s": rep.backups_done / (ms * 1e-3),
+           "backups_reference_equivalent_per_s": S * rep.sweeps / (ms * 1e-3),
+           "launches_per_solve": launches / steps,
+           "build_ms": space.info.build_ms}
+    del space
+    out["e2e"] = e2e_c_abi(N, text, opts, local, 5, S)
+    try:
+        ref = _reference()
+        inst = ref.load(W.FILES[name])
+        sp, times, sweeps = cpu_solve_timing(ref, inst, eps, ref.threads(), 3.0)
+        ref_ms = statistics.median(times)
+        out["reference"] = {"time_to_convergence_ms": ref_ms, "cores": ref.threads(),
+                            "build_ms": sp.build_ms, "sweeps": sweeps,
+                            "speedup_device": ref_ms / ms,
+                            "speedup_e2e": ref_ms / out["e2e"]["ms_per_step"]}
+    except Exception as e:  # noqa: BLE001
+        out["reference"] = {"error": str(e)}
+    return out
+
+
+METHODS = {1: "jacobi", 2: "layer-wavefront", 3: "certified backward pass"}
 
 
 def run_b200(args):
@@ -339,8 +506,6 @@ def run_b200(args):
         log(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    # N>1 default: independent instances, one per GPU (weak scaling, no data-path collective);
-    # --sharding wave/halo/allgather shards ONE instance (also at N=1, through a 1-rank group)
     sharding = args.sharding
     if sharding == "auto":
         sharding = "instances" if world > 1 else "single"
@@ -352,16 +517,16 @@ def run_b200(args):
         os.environ.setdefault("RANK", str(rank))
         os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=dev)
-    gen, desc = WORKLOADS[args.workload]
-    if sharding == "instances":  # rank r solves trial r of the same generator family
-        gen = gen[:2] + (rank,) + gen[3:]
-        desc = f"{desc}; rank r solves trial r of the family"
-    ni = V.generate_instance(*gen, as_objects=False)
+    workload = args.workload
+    text = W.instance_text(workload)
+    p = V.parse_instance(text)  # the product's parser (io.cpp:51-95 grammar)
+    ni = V.MdpInstance.from_workload(p.vcc, p.bots).native()
     t0 = time.time()
     space = V.StateSpace.build_native(ni, 10**9, local)
     build_wall_ms = (time.time() - t0) * 1e3
     S, E, H = space.size(), space.edges(), space.task_count()
-    log(f"[rank {rank}] built {desc}: S={S} E={E} H={H} in {space.info.build_ms:.1f} ms")
+    log(f"[rank {rank}] built {W.DESCRIPTIONS[workload]}: S={S} E={E} H={H} in "
+        f"{space.info.build_ms:.1f} ms")
     method = {"auto": N.VCS_METHOD_AUTO, "jacobi": N.VCS_METHOD_JACOBI,
               "wavefront": N.VCS_METHOD_WAVEFRONT, "certified": N.VCS_METHOD_CERTIFIED}[args.method]
     opts = N.vcs_solve_opts(args.eps, 0 if args.no_skip else 1, 0, 1.0, method)
@@ -370,52 +535,26 @@ def run_b200(args):
     torch.cuda.set_stream(stream)
     sampler = ClockSampler(local)
     sampler.start()
-    launches0 = None
 
     if not sharded_path:
-        h_stream = C.c_void_p(stream.cuda_stream)
-        rep = N.vcs_solve_report()
-        for _ in range(args.warmup):
-            N.check(N.lib().vcs_solve_enqueue(space.handle, C.byref(opts), h_stream))
-        N.check(N.lib().vcs_solve_collect(space.handle, None, None, C.byref(rep), h_stream))
-        sweeps = rep.sweeps
-        if rep.method != opts.method and opts.method != N.VCS_METHOD_JACOBI:
-            # the certificate did not hold (or AUTO chose Jacobi): time the method that produced
-            # the result, not the certified pass alone
-            log(f"note: the solve ran method {rep.method}; timing that method")
-            opts.method = rep.method
-            for _ in range(args.warmup):
-                N.check(N.lib().vcs_solve_enqueue(space.handle, C.byref(opts), h_stream))
-        torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        launches0 = N.kernel_launches()
-        sweep_ms, extract_ms = [], []
         tw0 = time.time()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            N.check(N.lib().vcs_solve_enqueue(space.handle, C.byref(opts), h_stream))
-        ev1.record(stream)
-        torch.cuda.synchronize()
+        total_ms, rep, launches = solve_timing(N, space, opts, stream, args.warmup, args.steps)
+        if rep.method != opts.method and opts.method != N.VCS_METHOD_AUTO:
+            log(f"note: the solve ran method {rep.method}")
         if world > 1:
             dist.barrier()
         tw1 = time.time()
-        launches = N.kernel_launches() - launches0
-        # the library's in-graph events of the last step split sweeps vs extraction
-        N.check(N.lib().vcs_solve_collect(space.handle, None, None, C.byref(rep), h_stream))
-        total_ms = ev0.elapsed_time(ev1)
         if world > 1:  # max over ranks
             t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             total_ms = float(t.item())
-        sweep_ms.append(rep.sweep_ms)
-        extract_ms.append(rep.extract_ms)
         sampler.mark(tw0, tw1)
+        sweeps = rep.sweeps
+        sweep_ms, extract_ms = rep.sweep_ms, rep.extract_ms
+        backups_done, method, model_bytes = rep.backups_done, rep.method, rep.model_bytes
         alg_bytes_done = rep.alg_bytes_done
-        backups_done = rep.backups_done
-        method = rep.method
-        model_bytes = rep.model_bytes
     else:
         from paper_2012_12419_b200 import sharded as SH
         lo, le = space.layer_offsets(), space.layer_edges()
@@ -450,141 +589,60 @@ def run_b200(args):
         dist.all_reduce(local_ms, op=dist.ReduceOp.MAX)
         total_ms = float(local_ms.item())
         sampler.mark(tw0, tw1)
-        dbar = E / S
         n_layer = np.diff(lo.astype(np.int64))
         if sharding == "wave":
-            # every (state, version) backup of the wavefront, summed over all ranks' bands
             backups_done = int(sum(int(n_layer[t]) * (H - t) for t in range(H)))
             method = N.VCS_METHOD_WAVEFRONT
-            model_bytes = 20 * S + 12 * E + 16 * backups_done
-            alg_bytes_done = model_bytes
+            model_bytes = alg_bytes_done = 20 * S + 12 * E + 16 * backups_done
         else:
             backups_done = sum(SH.sweep_row_end(lo, k, not args.no_skip)
                                for k in range(1, sweeps + 1))
-            alg_bytes_done = (24 + 12 * dbar) * backups_done
-            method, model_bytes = N.VCS_METHOD_JACOBI, (20 + 12 * dbar) * backups_done
-        sweep_ms, extract_ms = [total_ms / args.steps], [0.0]
+            alg_bytes_done = (24 + 12 * E / S) * backups_done
+            method, model_bytes = N.VCS_METHOD_JACOBI, (20 + 12 * E / S) * backups_done
+        sweep_ms, extract_ms = total_ms / args.steps, 0.0
 
     sampler.stop()
     ms_per_step = total_ms / args.steps
-    backups_step = S * sweeps  # reference-equivalent backups of one step, all ranks
-    if sharding == "instances":
-        t = torch.tensor([float(S * sweeps)], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        backups_step = float(t.item())
-    value = backups_step * args.steps / (total_ms * 1e-3)
-    dbar = E / S
-    b_ref = 24 + 12 * dbar
-
-    # ---- e2e through the C ABI with host buffers (rank 0 / N=1 path) --------------------------
+    n_instances = world if sharding == "instances" else 1
+    value = ms_per_step
     e2e = None
-    if not sharded_path and args.e2e_steps > 0:
+    if args.e2e_steps > 0 and not sharded_path:
         if world > 1:
             dist.barrier()
-        vals = torch.empty(S, dtype=torch.float64, pin_memory=True)
-        acts = torch.empty(S, dtype=torch.int32, pin_memory=True)
-        inst_bytes = 0
-        s = ni.struct
-        inst_bytes = s.n_clouds * (3 * 4 + 2 * 8) + s.n_tasks * (2 * 4 + 2 * 8)
-        e2e_times = []
-        vp = C.cast(C.c_void_p(vals.data_ptr()), C.POINTER(C.c_double))
-        ap = C.cast(C.c_void_p(acts.data_ptr()), C.POINTER(C.c_int32))
-        parts = []
-        e2e_warm = 2  # the stream-ordered pool reaches its steady size after two builds
-        for i in range(args.e2e_steps + e2e_warm):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            h = C.c_void_p()
-            N.check(N.lib().vcs_space_build(ni.ref, 10**9, local, C.byref(h)))
-            tb = time.perf_counter()
-            rep2 = N.vcs_solve_report()
-            N.check(N.lib().vcs_solve(h, C.byref(opts), vp, ap, C.byref(rep2)))
-            t1 = time.perf_counter()
-            N.lib().vcs_space_free(h)
-            log(f"[e2e {i}] build {1e3 * (tb - t0):.1f} ms, solve+D2H {1e3 * (t1 - tb):.1f} ms")
-            if i >= e2e_warm:
-                e2e_times.append(t1 - t0)
-                parts.append((tb - t0, t1 - tb))
-        e2e_t = statistics.median(e2e_times)
-        e2e_backups = S * rep2.sweeps
-        if world > 1:  # all ranks' instances, slowest rank's median step
-            t = torch.tensor([e2e_t, float(e2e_backups)], dtype=torch.float64, device=dev)
-            tm = t.clone()
-            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-            dist.all_reduce(t, op=dist.ReduceOp.SUM)
-            e2e_t, e2e_backups = float(tm[0].item()), float(t[1].item())
-            inst_bytes *= world
-        # on the wire: f64 values + the action column as int8 when every action fits (<= 127
-        # clouds; widened into the caller's int32 buffer on the host), else int32
-        act_wire = 1 if (s.n_clouds <= 127 and not os.environ.get("VCS_NO_NARROW")) else 4
-        e2e = {"value": e2e_backups / e2e_t, "unit": "backups/s",
-               "h2d_bytes_per_step": inst_bytes,
-               "d2h_bytes_per_step": S * (8 + act_wire) * (world if world > 1 else 1),
-               "d2h_result_bytes_per_step": S * (8 + 4) * (world if world > 1 else 1),
-               "ms_per_step": e2e_t * 1e3,
-               "build_ms": statistics.median(p[0] for p in parts) * 1e3,
-               "solve_and_d2h_ms": statistics.median(p[1] for p in parts) * 1e3,
-               "path": "vcs_space_build(host instance) + vcs_solve(pinned host values/actions; "
-                       "the int8 action column is widened to int32 on host threads)",
-               "steps": len(e2e_times)}
+        e2e = e2e_c_abi(N, text, opts, local, args.e2e_steps, S)
+        if world > 1:  # slowest rank
+            t = torch.tensor([e2e["ms_per_step"]], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e["value"] = e2e["ms_per_step"] = float(t.item())
+            e2e["h2d_bytes_per_step"] *= world
+            e2e["d2h_bytes_per_step"] *= world
     elif args.e2e_steps > 0:
         e2e = e2e_sharded(args, ni, local, dev, stream, opts, sharding, S, rank)
 
-    # ---- roofline of the dominant kernel ----------------------------------------------------
-    peak, peak_src = measured_peaks()
-    sweep_s = statistics.mean(sweep_ms) * 1e-3 if not sharded_path else None
     roofline = None
-    if sweep_s:
-        tr = ncu_traffic(method)
-        survey_equiv = b_ref * S * sweeps / sweep_s / 1e9  # SURVEY 8d bytes of the Jacobi sweeps
-        if method == N.VCS_METHOD_CERTIFIED:
-            # k_cert_dense on the full layers + k_cert_implicit on the sparse ones (all H
-            # launches of one solve; the proof held, no fallback ran): pairs by key-space index
-            alg = model_bytes
-            formula = ("per layer: full layers 4*key-space size (rank entries), sparse layers "
-                       "8*states (keys); + 28*states (value, action, pair written) + 16*states "
-                       "of layer t+1 (successor pairs read once) (DESIGN.md 3.4)")
-            kernel = ("k_cert_dense<1,false,3> on the full layers + k_cert_implicit<1,false,3,true> "
-                      "on the sparse ones (all H launches of one solve)")
-        elif method == N.VCS_METHOD_WAVEFRONT:
-            # k_wave_layer (all H launches of one solve, extraction fused): per state row_ptr 4
-            # + value 8 + action 4 + winner's action 4, per edge succ 4 + reward 8, per
-            # performed backup (state, version) 16 (written once, read once by layer t-1)
-            alg = model_bytes
-            formula = "20*S + 12*E + 16*backups_performed per solve (DESIGN.md 3.3)"
-            kernel = "k_wave_layer<false> (all H layer launches of one solve)"
-        else:
-            alg = alg_bytes_done
-            formula = "24 + 12*E/S per performed backup (SURVEY 8d)"
-            kernel = "k_sweep<false> (all sweep launches of one solve)"
-        achieved = alg / sweep_s / 1e9
-        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak,
-                    "traffic": tr.get("dram_bytes_per_launch") if tr else None,
-                    "traffic_alg_bytes_per_launch": tr.get("alg_bytes_per_launch") if tr else None,
-                    "kernel": kernel, "alg_bytes_per_solve": alg, "alg_bytes_formula": formula,
-                    "survey_B_equivalent_GBps": survey_equiv,
-                    "survey_B_note": "SURVEY 8d Jacobi bytes (24+12*E/S per backup x S x sweeps) "
-                                     "over the same time: the traffic a per-sweep solver would "
-                                     "need to stream for this result",
-                    "peak_source": peak_src,
-                    "traffic_note": (tr or {}).get("note")}
+    if not sharded_path:
+        roofline = roofline_for(N, method, model_bytes, alg_bytes_done, sweep_ms, S, sweeps, E / S)
 
     line = {
-        "metric": METRIC, "value": value, "unit": "backups/s", "n_gpus": world,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak" if sharding == "instances" else "strong",
-        "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": desc, "states": S, "transitions": E, "horizon": H,
-                   "sweeps": sweeps, "epsilon": args.eps, "layer_skip": not args.no_skip,
-                   "method": {1: "jacobi", 2: "layer-wavefront", 3: "certified backward pass"}.get(method, str(method)),
-                   "backups_performed_per_step": backups_done,
-                   "parallelism": PARALLELISM[sharding](world),
-                   "l2": "no flush: CSR 1.7 GB and V buffers 2x155 MB exceed the 126 MB L2",
-                   "build_ms": space.info.build_ms, "build_wall_ms": build_wall_ms},
+        "higher_is_better": False, "scaling": "weak" if sharding == "instances" else "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": common_config(workload, S, H, sweeps, args.eps),
         "time_to_convergence_ms": ms_per_step,
-        "sweep_ms": statistics.mean(sweep_ms), "extract_ms": statistics.mean(extract_ms),
+        "backups_per_s": {
+            "performed": n_instances * backups_done / (ms_per_step * 1e-3),
+            "reference_equivalent": n_instances * S * sweeps / (ms_per_step * 1e-3),
+            "note": "performed = backups the kernels computed (certified pass: about 2 per "
+                    "state); reference_equivalent = n_states * sweeps, the backups a per-sweep "
+                    "solver (the reference) performs for the same result"},
+        "solve": {"transitions": E, "method": METHODS.get(method, str(method)),
+                  "backups_performed_per_step": backups_done, "layer_skip": not args.no_skip,
+                  "parallelism": PARALLELISM[sharding](world), "instances": n_instances,
+                  "l2": "no flush between steps: the certified pass reads the 100 MB rank tables "
+                        "+ 155 MB keys and writes 232 MB of results per solve (> 126 MB L2)",
+                  "build_ms": space.info.build_ms, "build_wall_ms": build_wall_ms,
+                  "sweep_ms": sweep_ms, "extract_ms": extract_ms},
         "roofline": roofline,
         "cpu_baseline": None,
         "e2e": e2e,
@@ -595,9 +653,12 @@ def run_b200(args):
         line["full_work_methods"] = full_work_methods(space, args, stream)
     if rank == 0 and not args.no_greedy:
         line["greedy"] = greedy_c2(V, N)
+    if rank == 0 and world == 1 and not args.no_side:
+        line["side_workloads"] = {n: side_workload(V, N, n, args.eps, stream, local)
+                                  for n in ("c1", "c3") if n != workload}
     if world == 1 and not args.no_cpu_baseline and rank == 0:
         try:
-            line["cpu_baseline"] = cpu_baseline(space, args.eps)
+            line["cpu_baseline"] = cpu_baseline(workload, args.eps)
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     if rank == 0:
@@ -613,7 +674,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
+    ap.add_argument("--workload", choices=["c1", "c3", "c4"], default="c4")
     ap.add_argument("--eps", type=float, default=1e-6)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-skip", action="store_true", help="disable the converged-layer skip")
@@ -623,6 +684,7 @@ def main():
                          "when the version store fits in HBM, else Jacobi)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-greedy", action="store_true", help="skip the C2 greedy side number")
+    ap.add_argument("--no-side", action="store_true", help="skip the C1 / C3 side workloads")
     ap.add_argument("--no-alt", action="store_true",
                     help="skip the full-work (wavefront / Jacobi) side numbers")
     ap.add_argument("--sharding", choices=["auto", "instances", "wave", "halo", "allgather"],

@@ -11,6 +11,8 @@
 // Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline / --impl reference) load it.
 #include "vcsched/greedy.hpp"
 #include "vcsched/io.hpp"
+#include "vcsched/metrics.hpp"
+#include "vcsched/sim.hpp"
 #include "vcsched/mdp.hpp"
 #include "vcsched/parallel_vi.hpp"
 
@@ -19,6 +21,8 @@
 #include <chrono>
 #include <cstring>
 #include <memory>
+#include <random>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -252,6 +256,156 @@ int ref_greedy(const vcs_instance* in, int32_t* target_ids, int32_t* vms_used, i
         *unused = r.unused_vms;
         *placed = r.vc_placed_vms();
         *reward = greedy_reward(r, c.vcc);
+        return VCS_OK;
+    });
+}
+
+// ---- instance handles for bench.py's reference arm ------------------------------------------
+// The reference arm must not load the product library, so it reads (or generates) its instance
+// here, through the reference's own io.cpp parser, and builds/solves/places from the handle.
+struct RefInstance {
+    ParsedInstance p;
+};
+
+int ref_instance_load(const char* path, void** out) {
+    return guarded([&] {
+        auto h = std::make_unique<RefInstance>();
+        h->p = load_instance(path); // io.cpp:97-101
+        *out = h.release();
+        return VCS_OK;
+    });
+}
+
+int ref_instance_parse(const char* text, void** out) {
+    return guarded([&] {
+        auto h = std::make_unique<RefInstance>();
+        std::istringstream in(text);
+        h->p = parse_instance(in); // io.cpp:51-95
+        *out = h.release();
+        return VCS_OK;
+    });
+}
+
+// The bench's seeded families, restated here for the reference arm (the product's generator is
+// paper_2012_12419_b200/csrc/vcs_host.cpp gen_homog / gen_greedy; tests/test_host.py checks that
+// both produce the same instance text).  kind 1 = HOMOG, 2 = GREEDY (C2).
+int ref_instance_generate(int kind, uint64_t seed, int32_t a, int32_t b, int32_t c, int32_t d,
+                          void** out) {
+    return guarded([&] {
+        auto h = std::make_unique<RefInstance>();
+        std::mt19937_64 rng(seed);
+        auto draw = [&](int lo, int hi) { return std::uniform_int_distribution<int>(lo, hi)(rng); };
+        auto& vcc = h->p.vcc;
+        if (kind == VCS_GEN_HOMOG) {
+            for (int i = 0; i < a; ++i) {
+                VehicularCloud cl;
+                cl.id = i + 1;
+                cl.vm_total = cl.vm_free = b;
+                cl.vm_throughput_kbps = 100.0;
+                cl.v2i_delay_ms = 10.0;
+                vcc.clouds.push_back(cl);
+            }
+            const int n_bots = std::max(1, a);
+            h->p.bots.resize(static_cast<std::size_t>(n_bots));
+            for (int bi = 0; bi < n_bots; ++bi) h->p.bots[static_cast<std::size_t>(bi)].id = bi + 1;
+            for (int t = 0; t < c; ++t) {
+                Task task;
+                task.id = t + 1;
+                task.vm_demand = draw(1, d);
+                task.max_delay_ms = 100.0;
+                task.min_vm_throughput_kbps = 50.0;
+                h->p.bots[static_cast<std::size_t>(t % n_bots)].tasks.push_back(task);
+            }
+        } else if (kind == VCS_GEN_GREEDY) {
+            for (int i = 0; i < a; ++i) {
+                VehicularCloud cl;
+                cl.id = i + 1;
+                cl.vm_total = cl.vm_free = draw(50, 150);
+                cl.vm_throughput_kbps = draw(60, 160);
+                cl.v2i_delay_ms = draw(5, 50);
+                vcc.clouds.push_back(cl);
+            }
+            int id = 0;
+            for (int bi = 0; bi < b; ++bi) {
+                BagOfTasks bot;
+                bot.id = bi + 1;
+                for (int k = 0; k < c; ++k) {
+                    Task task;
+                    task.vm_demand = draw(1, d);
+                    task.max_delay_ms = draw(5, 60);
+                    task.min_vm_throughput_kbps = draw(50, 170);
+                    task.id = ++id;
+                    bot.tasks.push_back(task);
+                }
+                h->p.bots.push_back(std::move(bot));
+            }
+        } else {
+            throw std::invalid_argument("unknown generator kind");
+        }
+        *out = h.release();
+        return VCS_OK;
+    });
+}
+
+void ref_instance_free(void* h) { delete static_cast<RefInstance*>(h); }
+
+void ref_instance_counts(void* h, int32_t* n_clouds, int32_t* n_tasks) {
+    const auto& p = static_cast<RefInstance*>(h)->p;
+    *n_clouds = static_cast<int32_t>(p.vcc.clouds.size());
+    *n_tasks = static_cast<int32_t>(flatten_tasks(p.bots).size());
+}
+
+// io.cpp:103-118 instance_text; returns the length, copies at most cap bytes.
+uint64_t ref_instance_text(void* h, char* buf, uint64_t cap) {
+    const std::string s = instance_text(static_cast<RefInstance*>(h)->p);
+    if (buf) std::memcpy(buf, s.data(), std::min<std::size_t>(cap, s.size()));
+    return s.size();
+}
+
+int ref_space_build_inst(void* inst, uint64_t cap, void** out, double* build_ms) {
+    return guarded([&] {
+        const auto& p = static_cast<RefInstance*>(inst)->p;
+        auto h = std::make_unique<RefSpace>();
+        h->inst = MdpInstance::from_workload(p.vcc, p.bots);
+        const auto t0 = std::chrono::steady_clock::now();
+        h->space = StateSpace::build(h->inst, static_cast<std::size_t>(cap));
+        const auto t1 = std::chrono::steady_clock::now();
+        if (build_ms) *build_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        *out = h.release();
+        return VCS_OK;
+    });
+}
+
+// greedy_schedule (greedy.cpp:5-30) timed with steady_clock; targets as cloud IDS.
+int ref_greedy_inst(void* inst, int32_t* target_ids, int64_t* paid, int64_t* unused,
+                    double* ms) {
+    return guarded([&] {
+        const auto& p = static_cast<RefInstance*>(inst)->p;
+        const auto t0 = std::chrono::steady_clock::now();
+        const auto r = greedy_schedule(p.vcc, p.bots);
+        const auto t1 = std::chrono::steady_clock::now();
+        if (ms) *ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        for (std::size_t i = 0; i < r.placements.size(); ++i) target_ids[i] = r.placements[i].target;
+        *paid = r.paid_vms;
+        *unused = r.unused_vms;
+        return VCS_OK;
+    });
+}
+
+// The reference's DSRC simulator (sim.cpp run_simulation + vc_throughput, metrics.cpp:8-11
+// per_vehicle_throughput): the per-vehicle service-channel share at a coverage density, used
+// once by tools/c5_channel_table.py to tabulate tests/golden/c5_channel.json (the C5 sweep's
+// channel-availability variants).  scheme 0 = static1609, 1 = aaa.
+int ref_per_vehicle_kbps(int32_t n_vehicles, int32_t scheme, uint64_t seed, int64_t duration_ms,
+                         double* out) {
+    return guarded([&] {
+        VanetScenario sc;
+        sc.n_vehicles = n_vehicles;
+        sc.scheme = scheme ? Scheme::kAaa : Scheme::kStatic1609;
+        sc.rng_seed = seed;
+        sc.sim_duration_ms = duration_ms;
+        const SimTrace tr = run_simulation(sc);
+        *out = per_vehicle_throughput(vc_throughput(tr), n_vehicles);
         return VCS_OK;
     });
 }

@@ -46,7 +46,7 @@ __all__ = [
     "ViResult", "value_iteration", "bellman_backup", "rollout", "run_value_iteration",
     "BlockPartition", "SweepBarrier", "parallel_value_iteration", "SpeedupRow", "measure_speedup", "speedup_csv",
     "ScheduleResult", "greedy_schedule", "greedy_reward", "ParsedInstance", "parse_instance",
-    "load_instance", "generate_instance", "ConfigError", "IoError", "InvalidArgument",
+    "load_instance", "generate_instance", "instance_text", "ConfigError", "IoError", "InvalidArgument",
     "OutOfRange", "CudaError", "VcsError", "NativeInstance",
 ]
 
@@ -269,6 +269,26 @@ def load_instance(path: str) -> ParsedInstance:
     h = C.c_void_p()
     N.check(N.lib().vcs_instance_load(str(path).encode(), C.byref(h)))
     return _parsed_from_native(NativeInstance.owned(h))
+
+
+def _fmt(v: float) -> str:
+    """io.cpp:16-20 fmt: printf %.17g."""
+    return "%.17g" % float(v)
+
+
+def instance_text(instance: ParsedInstance) -> str:
+    """io.cpp:103-118 instance_text: the instance file a parse_instance round trip reproduces."""
+    vcc = instance.vcc
+    out = [f"beta_vc {_fmt(vcc.reward_per_vc_vm)}", f"beta_tc {_fmt(vcc.cost_per_tcc_vm)}",
+           f"gamma_vc {_fmt(vcc.penalty_per_idle_vm)}"]
+    for c in vcc.clouds:
+        out.append(f"cloud {c.id} {c.vm_total} {_fmt(c.vm_throughput_kbps)} {_fmt(c.v2i_delay_ms)}")
+    for bot in instance.bots:
+        out.append(f"bot {bot.id}")
+        for t in bot.tasks:
+            out.append(f"task {t.id} {t.vm_demand} {_fmt(t.max_delay_ms)} "
+                       f"{_fmt(t.min_vm_throughput_kbps)}")
+    return "\n".join(out) + "\n"
 
 
 def generate_instance(kind: int, seed: int, trial: int = 0, a: int = 0, b: int = 0, c: int = 0,

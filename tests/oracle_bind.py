@@ -132,14 +132,29 @@ class OracleSpace:
 class Reference:
     """The unmodified reference solver (oracle/_ref/libvcsref.so)."""
 
-    def __init__(self, path: Path = REF_SO):
+    def __init__(self, path: Path = REF_SO, standalone: bool = False):
         if not path.exists():
             raise FileNotFoundError(f"{path} missing: build it with `make ref` where "
                                     "/root/reference exists")
         L = C.CDLL(str(path))
-        from paper_2012_12419_b200._native import vcs_instance
-        INST = C.POINTER(vcs_instance)
+        if standalone:
+            # bench.py's reference arm: no product import at all (the vcs_instance-typed entry
+            # points are left unchecked; the arm only uses the instance handles below)
+            INST = None
+        else:
+            from paper_2012_12419_b200._native import vcs_instance
+            INST = C.POINTER(vcs_instance)
         sig = {
+            "ref_instance_load": (C.c_int, [C.c_char_p, C.POINTER(_P)]),
+            "ref_instance_parse": (C.c_int, [C.c_char_p, C.POINTER(_P)]),
+            "ref_instance_generate": (C.c_int, [C.c_int, C.c_uint64, C.c_int32, C.c_int32,
+                                                C.c_int32, C.c_int32, C.POINTER(_P)]),
+            "ref_instance_free": (None, [_P]),
+            "ref_instance_counts": (None, [_P, _I32P, _I32P]),
+            "ref_instance_text": (C.c_uint64, [_P, C.c_char_p, C.c_uint64]),
+            "ref_space_build_inst": (C.c_int, [_P, C.c_uint64, C.POINTER(_P), _F64P]),
+            "ref_greedy_inst": (C.c_int, [_P, _I32P, _I64P, _I64P, _F64P]),
+            "ref_per_vehicle_kbps": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, C.c_int64, _F64P]),
             "ref_last_error": (C.c_char_p, []),
             "ref_hardware_threads": (C.c_int, []),
             "ref_space_build": (C.c_int, [INST, C.c_uint64, C.POINTER(_P), _F64P]),
@@ -160,11 +175,25 @@ class Reference:
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
-            f.restype, f.argtypes = res, args
+            f.restype = res
+            if args is None or None in args:
+                f.argtypes = None
+            else:
+                f.argtypes = args
         self.L = L
 
     def err(self):
         return self.L.ref_last_error().decode()
+
+    # ---- instance handles (the reference's own parser / the restated bench generators) -----
+    def load(self, path):
+        return RefInstance(self, "ref_instance_load", str(path).encode())
+
+    def parse(self, text: str):
+        return RefInstance(self, "ref_instance_parse", text.encode())
+
+    def generate(self, kind, seed, a, b, c, d):
+        return RefInstance(self, "ref_instance_generate", kind, seed, a, b, c, d)
 
     def threads(self):
         return int(self.L.ref_hardware_threads())
@@ -188,6 +217,49 @@ class Reference:
             raise OracleError(rc, self.err())
         return dict(target_ids=ids[:n_tasks], vms_used=used[:n_tasks], paid=paid.value,
                     unused=unused.value, placed=placed.value, reward=reward.value, ms=ms.value)
+
+
+class RefInstance:
+    """A reference-owned ParsedInstance (oracle/ref_capi.cpp RefInstance)."""
+
+    def __init__(self, ref: Reference, fn: str, *args):
+        self.ref, self.h = ref, _P()
+        rc = getattr(ref.L, fn)(*args, C.byref(self.h))
+        if rc != 0:
+            self.h = None
+            raise OracleError(rc, ref.err())
+        nc, nt = C.c_int32(), C.c_int32()
+        ref.L.ref_instance_counts(self.h, C.byref(nc), C.byref(nt))
+        self.n_clouds, self.n_tasks = nc.value, nt.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.ref.L.ref_instance_free(self.h)
+            self.h = None
+
+    def text(self) -> str:
+        n = self.ref.L.ref_instance_text(self.h, None, 0)
+        buf = C.create_string_buffer(int(n) + 1)
+        self.ref.L.ref_instance_text(self.h, buf, n)
+        return buf.raw[:n].decode()
+
+    def build(self, cap=5_000_000):
+        h = _P()
+        ms = C.c_double()
+        rc = self.ref.L.ref_space_build_inst(self.h, cap, C.byref(h), C.byref(ms))
+        if rc != 0:
+            raise OracleError(rc, self.ref.err())
+        return RefSpace(self.ref, h, ms.value)
+
+    def greedy(self):
+        ids = np.empty(max(self.n_tasks, 1), np.int32)
+        paid, unused, ms = C.c_int64(), C.c_int64(), C.c_double()
+        rc = self.ref.L.ref_greedy_inst(self.h, _p(ids, C.c_int32), C.byref(paid), C.byref(unused),
+                                        C.byref(ms))
+        if rc != 0:
+            raise OracleError(rc, self.ref.err())
+        return dict(target_ids=ids[:self.n_tasks], paid=paid.value, unused=unused.value,
+                    ms=ms.value)
 
 
 class RefSpace:

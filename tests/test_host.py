@@ -112,6 +112,57 @@ def test_homog_and_greedy_generators_shape():
     assert int(c2["cloud_vm_total"].sum()) == 98991  # = placed + unused of the golden run
 
 
+# ---- bench workloads: both arms read the same instance ------------------------------------
+
+@pytest.mark.parametrize("name,args", [("c3", (5, 8, 40, 3)), ("c4", (6, 8, 48, 3))])
+def test_committed_instance_files_match_generators(reference, name, args):
+    """tests/golden/instances/cN.txt = the product generator's instance, and the reference's own
+    parser reads it back to the same text the reference's restated generator writes."""
+    import bench_workloads as W
+    prod = V.generate_instance(N.VCS_GEN_HOMOG, 2012, 0, *args)
+    body = W.instance_text(name).split("\n", 2)[2]  # drop the two comment lines
+    assert V.instance_text(prod) == body
+    via_ref_parser = reference.load(W.FILES[name]).text()
+    via_ref_gen = reference.generate(N.VCS_GEN_HOMOG, 2012, *args).text()
+    assert via_ref_parser == via_ref_gen == body
+    assert V.instance_text(V.load_instance(str(W.FILES[name]))) == body
+
+
+def test_c2_generator_restatement_matches_product(reference):
+    import bench_workloads as W
+    kind, seed, a, b, c, d = W.C2_GEN
+    prod = V.generate_instance(kind, seed, 0, a, b, c, d)
+    assert V.instance_text(prod) == reference.generate(kind, seed, a, b, c, d).text()
+
+
+def test_c5_points_parse_identically(reference):
+    """Every C5 point parses to the same instance in both arms' parsers; the channel variants
+    really differ (the scheme changes at least one cloud's throughput on most points)."""
+    import bench_workloads as W
+    table = W.channel_table()
+    differ = 0
+    for K, c, scheme in W.c5_points():
+        txt = W.c5_text(K, c, scheme, table)
+        ours = V.instance_text(V.parse_instance(txt))
+        assert ours == reference.parse(txt).text(), (K, c, scheme)
+        if scheme == "aaa":
+            differ += W.c5_text(K, c, "static1609", table).split("bot", 1)[0] != txt.split("bot", 1)[0]
+    assert differ >= 30
+
+
+def test_c5_channel_table_is_the_reference_simulator(reference):
+    import bench_workloads as W
+    table = W.channel_table()
+    for n in (5, 15, 20, 28, 35, 84):
+        for scheme, k in (("static1609", 0), ("aaa", 1)):
+            out = C.c_double()
+            assert reference.L.ref_per_vehicle_kbps(n, k, 42, 10_000, C.byref(out)) == 0
+            assert out.value == table[scheme][n - 1]
+    # SURVEY 8(d): static 120/96/72/57.6 kbps at 10/15/20/25 vehicles, AAA 120/120/96.6/69.12
+    assert [round(table["static1609"][n - 1], 2) for n in (10, 15, 20, 25)] == [120, 96, 72, 57.6]
+    assert [round(table["aaa"][n - 1], 2) for n in (10, 15, 20, 25)] == [120, 120, 96.6, 69.12]
+
+
 def test_generator_rejects_bad_kind():
     with pytest.raises(V.InvalidArgument):
         V.generate_instance(7, 1)
