@@ -49,11 +49,16 @@ def log(*a):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled in the background."""
+    """SM clocks + throttle reasons sampled DURING the timed region: an NVML polling thread
+    (every ~2 ms: the timed regions here are tens of ms, shorter than nvidia-smi's 50 ms
+    period), with nvidia-smi -lms 50 as the fallback when NVML is unavailable."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits (nvml.h nvmlClocksEventReason*)
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, device: int):
         self.device = device
@@ -61,8 +66,21 @@ class ClockSampler:
         self.proc = None
         self.thread = None
         self.window = None
+        self.nvml = None
+        self.stop_flag = threading.Event()
 
     def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:  # noqa: BLE001
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
@@ -74,6 +92,21 @@ class ClockSampler:
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
 
+    def _poll(self):
+        nv = self.nvml
+        while not self.stop_flag.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM)
+                try:
+                    bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+                except AttributeError:
+                    bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.handle)
+                names = [n for b, n in self.REASONS.items() if bits & b]
+                self.samples.append((time.time(), ("nvml", sm, self.max_mhz, names)))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
+
     def _read(self):
         for line in self.proc.stdout:
             self.samples.append((time.time(), [x.strip() for x in line.split(",")]))
@@ -82,22 +115,31 @@ class ClockSampler:
         self.window = (t0, t1)
 
     def stop(self):
+        self.stop_flag.set()
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        if self.thread and self.nvml:
+            self.thread.join(timeout=1)
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"],
                     "samples": 0}
         rows = self.samples
+        inside = rows
         if self.window:
-            inside = [s for s in rows if self.window[0] - 0.05 <= s[0] <= self.window[1] + 0.05]
-            if inside:
-                rows = inside
+            inside = [s for s in rows if self.window[0] - 0.002 <= s[0] <= self.window[1] + 0.002]
+            rows = inside or rows
+        if rows[0][1][0] == "nvml":
+            sm = [r[1][1] for r in rows]
+            reasons = sorted({n for r in rows for n in r[1][3]})
+            return {"sm_mhz": statistics.median(sm), "sm_max_mhz": rows[0][1][2],
+                    "reasons": reasons, "samples": len(rows), "source": "nvml, 2 ms poll",
+                    "in_timed_window": bool(self.window and inside)}
         sm = [float(r[1][0]) for r in rows if r[1][0].replace(".", "").isdigit()]
         mx = [float(r[1][1]) for r in rows if r[1][1].replace(".", "").isdigit()]
         reasons = set()
@@ -108,7 +150,8 @@ class ClockSampler:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(rows), "in_timed_window": self.window is not None}
+                "samples": len(rows), "source": "nvidia-smi -lms 50",
+                "in_timed_window": bool(self.window and inside)}
 
 
 def measured_peaks():
