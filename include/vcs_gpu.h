@@ -219,6 +219,40 @@ int vcs_solve_enqueue(vcs_space* sp, const vcs_solve_opts* opts, void* stream);
 int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
                       vcs_solve_report* report, void* stream);
 
+/* Multi-GPU certified solve: ONE state space sharded across n_ranks GPUs of this
+ * process — the B200 replacement of the block-parallel driver (parallel_vi.cpp:68-107,
+ * BlockPartition::even :11-24, SweepBarrier :34-44): GPUs instead of std::threads, contiguous
+ * shares of every large layer's pair index space (key space, or BFS rows of an explicit CSR)
+ * instead of row blocks of the whole space, and per-layer peer copies over NVLink instead of the
+ * shared-memory flush + barriers.  devices[r] is rank r's CUDA device (NULL = space device,
+ * then the next ones); a device may repeat (several ranks on one GPU: the emulated-rank test
+ * mode).  exchange: VCS_EXCHANGE_HALO pulls only the successor window a rank reads (forward halo
+ * on non-retiring transitions of the key space), VCS_EXCHANGE_ALLGATHER every layer in full (the
+ * north-star all-gather, kept for comparison).  Values, actions and sweeps are bit-identical to
+ * vcs_solve for every n_ranks; the results land in the space's device (the primary), and
+ * vcs_solve_collect downloads them (and runs the single-GPU fallback when the certificate does
+ * not hold).  n_ranks == 1 on the space's device is vcs_solve_enqueue.  Methods AUTO/CERTIFIED
+ * only (VCS_EINVAL otherwise). */
+#define VCS_EXCHANGE_HALO 0
+#define VCS_EXCHANGE_ALLGATHER 1
+int vcs_solve_multi_enqueue(vcs_space* sp, const vcs_solve_opts* opts, int32_t n_ranks,
+                            const int32_t* devices, int32_t exchange, void* stream);
+/* = vcs_solve_multi_enqueue + vcs_solve_collect (values_out / actions_out host or NULL). */
+int vcs_solve_multi(vcs_space* sp, const vcs_solve_opts* opts, int32_t n_ranks,
+                    const int32_t* devices, int32_t exchange, double* values_out,
+                    int32_t* actions_out, vcs_solve_report* report);
+typedef struct vcs_multi_report {
+    int32_t n_ranks;
+    int32_t split_layers;      /* layers divided between the ranks */
+    int32_t replicated_layers; /* small / sparse layers every rank computes whole */
+    int32_t exchange;
+    double halo_bytes;         /* pair bytes copied between ranks per solve */
+    double max_share;          /* largest rank share of the divided work (1/n_ranks = balanced) */
+    int32_t graph;             /* 1: the pass is one CUDA graph; 0: direct launches */
+    int32_t pad;
+} vcs_multi_report;
+int vcs_multi_info(const vcs_space* sp, vcs_multi_report* out);
+
 /* Sharded (multi-GPU) building blocks.  One process per GPU; the host runtime owns the value
  * buffers and the collectives (torch.distributed / NCCL over NVLink), these calls only enqueue
  * device work on `stream` (a cudaStream_t; NULL = the space's own stream) and never synchronise

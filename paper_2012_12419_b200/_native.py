@@ -18,6 +18,7 @@ VCS_PAID_CLOUD = -1
 VCS_NO_ACTION = -2
 VCS_GEN_RANDOM, VCS_GEN_HOMOG, VCS_GEN_GREEDY = 0, 1, 2
 VCS_METHOD_AUTO, VCS_METHOD_JACOBI, VCS_METHOD_WAVEFRONT, VCS_METHOD_CERTIFIED = 0, 1, 2, 3
+VCS_EXCHANGE_HALO, VCS_EXCHANGE_ALLGATHER = 0, 1
 
 LIB_PATH = Path(__file__).resolve().parent / "libvcs_gpu.so"
 
@@ -28,7 +29,8 @@ EXPORTS = (
     "vcs_space_build", "vcs_space_from_csr", "vcs_space_info_get", "vcs_space_layer_offsets",
     "vcs_space_layer_edges", "vcs_space_csr", "vcs_space_locate", "vcs_space_hidden_penalty",
     "vcs_policy_query", "vcs_space_free",
-    "vcs_solve", "vcs_solve_enqueue", "vcs_solve_collect", "vcs_shard_plan", "vcs_shard_begin", "vcs_shard_sweep", "vcs_shard_finish",
+    "vcs_solve", "vcs_solve_enqueue", "vcs_solve_collect",
+    "vcs_solve_multi_enqueue", "vcs_solve_multi", "vcs_multi_info", "vcs_shard_plan", "vcs_shard_begin", "vcs_shard_sweep", "vcs_shard_finish",
     "vcs_wave_shard_begin", "vcs_wave_shard_band", "vcs_wave_shard_layer", "vcs_wave_shard_pack",
     "vcs_wave_shard_unpack", "vcs_wave_shard_finish",
     "vcs_greedy", "vcs_greedy_batch", "vcs_greedy_reward",
@@ -129,6 +131,19 @@ class vcs_solve_report(C.Structure):
     ]
 
 
+class vcs_multi_report(C.Structure):
+    _fields_ = [
+        ("n_ranks", C.c_int32),
+        ("split_layers", C.c_int32),
+        ("replicated_layers", C.c_int32),
+        ("exchange", C.c_int32),
+        ("halo_bytes", C.c_double),
+        ("max_share", C.c_double),
+        ("graph", C.c_int32),
+        ("pad", C.c_int32),
+    ]
+
+
 _P = C.c_void_p
 _I32P = C.POINTER(C.c_int32)
 _I64P = C.POINTER(C.c_int64)
@@ -161,6 +176,11 @@ _SIGS = {
                             C.POINTER(vcs_solve_report)]),
     "vcs_solve_enqueue": (C.c_int, [_P, C.POINTER(vcs_solve_opts), _P]),
     "vcs_solve_collect": (C.c_int, [_P, _F64P, _I32P, C.POINTER(vcs_solve_report), _P]),
+    "vcs_solve_multi_enqueue": (C.c_int, [_P, C.POINTER(vcs_solve_opts), C.c_int32, _I32P,
+                                          C.c_int32, _P]),
+    "vcs_solve_multi": (C.c_int, [_P, C.POINTER(vcs_solve_opts), C.c_int32, _I32P, C.c_int32,
+                                  _F64P, _I32P, C.POINTER(vcs_solve_report)]),
+    "vcs_multi_info": (C.c_int, [_P, C.POINTER(vcs_multi_report)]),
     "vcs_shard_plan": (C.c_int, [_U64P, _U64P, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                  _U64P, _U64P, _U64P, _U64P]),
     "vcs_shard_begin": (C.c_int, [_P, _P, _P, _P, C.c_int32, _P]),
@@ -236,3 +256,4 @@ def kernel_launches() -> int:
 
 def device_count() -> int:
     return int(lib().vcs_device_count())
+

@@ -136,7 +136,12 @@ struct CachedGraph {
     int method = kMethodJacobi;
     int uses = 0; // solves enqueued so far (the first runs without a graph)
     bool implicit = false; // certified pass on the implicit-CSR form: fallback runs at collect
+    bool fallback_at_collect = false; // the proof's fallback is not in the graph (implicit / multi-GPU)
+    int n_ranks = 1;       // GPUs (ranks) the solve ran on
 };
+
+struct MultiState;               // multi-GPU certified pass (vcs_solve.cu)
+void destroy_multi(MultiState*); // waits for and frees everything it owns
 
 } // namespace vcs
 
@@ -212,6 +217,7 @@ struct vcs_space {
     uint64_t loc_cap = 0;
 
     int num_sms = 148;
+    vcs::MultiState* multi = nullptr; // the multi-GPU solve's per-rank state (vcs_solve_multi)
     // caller streams that have run work on this space: the destructor waits for their last
     // recorded use before the space's blocks can be reused
     std::map<cudaStream_t, cudaEvent_t> use_ev;

@@ -662,6 +662,7 @@ struct CertArgs {
     uint64_t row0, n, next_row0;
     int m;
     double discount;
+    int write_out; // 0: values/actions are written by another rank
 };
 
 // Thread-per-row form of the certified layer: each thread streams its own row's contiguous
@@ -717,8 +718,10 @@ __global__ void __launch_bounds__(256, MINB) k_cert_rows(CertArgs a) {
         }
         if (a.m == 1) lo = 0.0; // V_0
         a.xd_cur[r] = make_double2(lo, hi);
-        a.values_out[a.row0 + r] = hi;
-        a.act_out[a.row0 + r] = best_e != 0xffffffffu ? __ldg(a.action + best_e) : -1;
+        if (a.write_out) {
+            a.values_out[a.row0 + r] = hi;
+            a.act_out[a.row0 + r] = best_e != 0xffffffffu ? __ldg(a.action + best_e) : -1;
+        }
         const double d = fabs(hi - lo);
         dmax = dmax < d ? d : dmax;
     }
@@ -757,6 +760,10 @@ struct CertImplArgs {
     const uint32_t* __restrict__ rank_self; // transition t-1's table: layer t's BFS rank by index
     uint64_t dense_n;                       // layer t's key-space size
     int write_own;
+    int write_out;                          // 0: values/actions are written by another rank
+    // key-space order: the indices [d_lo, d_hi) of this launch (the whole key space on one GPU,
+    // a rank's contiguous share when the layer is sharded across GPUs)
+    uint64_t d_lo, d_hi;
 };
 
 // One layer of the implicit certified pass over states first_i, first_i + stride, ... (the
@@ -823,8 +830,10 @@ __device__ __forceinline__ void cert_implicit_layer(const CertImplArgs& a, const
                 own += static_cast<uint32_t>(get_field<WM>(k, L.bit_off[p], L.width[p])) * L.wself[p];
             a.xd_cur[own] = make_double2(lo, hi);
         }
-        a.values_out[a.row0 + i] = hi;
-        a.act_out[a.row0 + i] = best < 0 ? -1 : L.cloud[best];
+        if (a.write_out) {
+            a.values_out[a.row0 + i] = hi;
+            a.act_out[a.row0 + i] = best < 0 ? -1 : L.cloud[best];
+        }
         const double d = fabs(hi - lo);
         dmax = dmax < d ? d : dmax;
     }
@@ -857,12 +866,13 @@ __device__ __forceinline__ void cert_dense_layer(const CertImplArgs& a, const La
     constexpr int NF = kDenseSlots - 1; // key-space layers have <= 7 fields
     const int na = L.n_active;
     double dmax = 0.0;
-    uint64_t d = first;
-    uint32_t rn = d < a.dense_n ? __ldg(a.rank_self + d) : kEmpty32; // next index's rank
+    uint64_t d = a.d_lo + first;
+    const uint64_t d_hi = a.d_hi;
+    uint32_t rn = d < d_hi ? __ldg(a.rank_self + d) : kEmpty32; // next index's rank
     // mixed-radix digits of d and of the stride, divided out once; the loop steps an odometer
     uint32_t g[NF], sd[NF], rad[NF];
     {
-        uint32_t rem = static_cast<uint32_t>(d < a.dense_n ? d : 0);
+        uint32_t rem = static_cast<uint32_t>(d < d_hi ? d : 0);
         uint32_t srem = static_cast<uint32_t>(stride < a.dense_n ? stride : 0);
 #pragma unroll
         for (int p = 0; p < NF; ++p) {
@@ -881,9 +891,9 @@ __device__ __forceinline__ void cert_dense_layer(const CertImplArgs& a, const La
     const double r_cl = L.r_cloud, r_pd = L.r_paid, gam = L.gamma;
     const int dem = L.demand;
     asm volatile("griddepcontrol.wait;" ::: "memory"); // (PDL) the previous layer's pairs
-    for (; d < a.dense_n; d += stride) {
+    for (; d < d_hi; d += stride) {
         const uint32_t r = rn;
-        if (d + stride < a.dense_n) rn = __ldg(a.rank_self + d + stride);
+        if (d + stride < d_hi) rn = __ldg(a.rank_self + d + stride);
         // the state's slots straight from its digits (= dec.decode of its packed key), and the
         // retired free VMs (an integer: the reference's fp64 running sum of integers is exact)
         uint32_t base = 0, mask = 0;
@@ -935,7 +945,7 @@ __device__ __forceinline__ void cert_dense_layer(const CertImplArgs& a, const La
         }
         if (a.m == 1) lo = 0.0; // V_0
         a.xd_cur[d] = make_double2(lo, hi);
-        a.values_out[a.row0 + r] = hi;
+        a.values_out[a.row0 + r] = hi; // (on another GPU: a peer store into the primary's arrays)
         a.act_out[a.row0 + r] = best < 0 ? -1 : L.cloud[best];
         const double dd = fabs(hi - lo);
         dmax = dmax < dd ? dd : dmax;
@@ -1239,6 +1249,119 @@ uint64_t cert_pairs_needed(const vcs_space* sp) {
     return cert_keyspace(sp) ? 2 * cert_half(sp) : sp->S;
 }
 
+// Device pointers of the implicit form a certified layer reads (the space's own, or a replica
+// of them on another GPU for the multi-GPU pass).
+struct CertData {
+    const uint64_t* keys;
+    const uint32_t* rank_tables;
+    const LayerParam* params;
+};
+CertData cert_data_of(const vcs_space* sp) {
+    return CertData{sp->keys.p, sp->rank_tables.p, sp->params_dev.p};
+}
+
+// Layer t of the certified pass on the implicit form: which kernel walks it and where its pairs
+// live.  Key-space layout (ks): layer t's pairs in half t&1 of `xd` at their key-space index.
+struct CertLayer {
+    int t = 0;
+    uint64_t row0 = 0, n = 0;  // the layer's states (BFS rows)
+    uint64_t dense_n = 0;      // the layer's key-space size (0 for the root)
+    bool dense_order = false;  // a thread per key-space index (k_cert_dense)
+    double2* xd_next = nullptr;
+    double2* xd_cur = nullptr;
+    uint64_t d_lo = 0, d_hi = 0; // k_cert_dense: the indices of this launch
+};
+CertLayer cert_layer(const vcs_space* sp, int t, double2* xd, uint64_t half, bool ks) {
+    CertLayer L;
+    L.t = t;
+    L.row0 = sp->layer_off[t];
+    L.n = sp->layer_off[t + 1] - sp->layer_off[t];
+    if (ks) {
+        L.xd_next = xd + ((t + 1) & 1) * half;
+        L.xd_cur = xd + (t & 1) * half;
+        L.dense_n = t >= 1 ? sp->plan.layers[static_cast<size_t>(t - 1)].dense_size : 0;
+        // walk the key space when at least half of it is reached (coalesced pair writes, no
+        // key loads); sparse layers walk their states
+        L.dense_order = t >= 1 && L.n * 2 >= L.dense_n;
+    } else {
+        L.xd_next = xd + sp->layer_off[t + 1];
+        L.xd_cur = xd + L.row0;
+    }
+    return L;
+}
+
+// Launch one certified layer on the implicit form (on the current device's stream `s`).
+void launch_cert_layer(const vcs_space* sp, const CertData& data, const CertLayer& L,
+                       double* values_out, int32_t* act_out, double* lb, double discount,
+                       int write_out, bool pdl, cudaStream_t s) {
+    const bool disc = is_discounted(discount);
+    const int t = L.t;
+    const bool ks = cert_keyspace(sp);
+    CertImplArgs c{};
+    c.values_out = values_out;
+    c.act_out = act_out;
+    c.lb = lb;
+    c.discount = discount;
+    c.row0 = L.row0;
+    c.n = L.n;
+    c.m = sp->H - t;
+    c.keys = data.keys + sp->key_off[t];
+    c.L = data.params + t;
+    c.rank = data.rank_tables + sp->rank_off[t];
+    c.xd_next = L.xd_next;
+    c.xd_cur = L.xd_cur;
+    c.write_out = write_out;
+    if (ks) {
+        c.dense_n = L.dense_n;
+        c.rank_self = t >= 1 ? data.rank_tables + sp->rank_off[static_cast<size_t>(t - 1)] : nullptr;
+        c.write_own = t >= 1 ? 1 : 0;
+        c.d_lo = L.d_lo;
+        c.d_hi = L.d_hi;
+    }
+    const bool dense_order = L.dense_order;
+    dispatch_words_solve(max_key_words(sp), [&](auto wm) {
+        constexpr int WM = decltype(wm)::value;
+        // 3 blocks per SM (80 registers, no spills): C4 0.68 ms vs 0.72 at 4, 0.74 at 2
+        const void* fn =
+            dense_order ? (disc ? reinterpret_cast<const void*>(k_cert_dense<WM, true, 3>)
+                                : reinterpret_cast<const void*>(k_cert_dense<WM, false, 3>))
+                        : (disc ? reinterpret_cast<const void*>(k_cert_implicit<WM, true, 3, false>)
+                                : reinterpret_cast<const void*>(k_cert_implicit<WM, false, 3, false>));
+        static thread_local std::map<std::pair<const void*, int>, int> occ;
+        int dev = 0;
+        VCS_CUDA(cudaGetDevice(&dev));
+        int& per_sm = occ[{fn, dev}];
+        if (!per_sm) VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
+        const uint64_t items = dense_order ? (L.d_hi > L.d_lo ? L.d_hi - L.d_lo : 0) : L.n;
+        const uint64_t blocks = std::max<uint64_t>(
+            1, std::min<uint64_t>((items + 255) / 256,
+                                  static_cast<uint64_t>(std::max(1, per_sm)) * sp->num_sms));
+        // layers after the first launch programmatically (PDL): their blocks load the layer
+        // constants and first keys while the previous layer drains.  Not with per-layer events
+        // in between (vcs_solve's streamed download) nor across streams.
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+        cfg.blockDim = dim3(256);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl ? 1 : 0;
+        if (dense_order) {
+            if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense<WM, true, 3>, c));
+            else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense<WM, false, 3>, c));
+        } else if (ks) {
+            if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, true, 3, true>, c));
+            else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, false, 3, true>, c));
+        } else {
+            if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, true, 3, false>, c));
+            else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, false, 3, false>, c));
+        }
+        VCS_LAUNCHED();
+    });
+}
+
 void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaStream_t s,
                       bool capturing) {
     const bool disc = is_discounted(key.discount);
@@ -1262,73 +1385,15 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
             VCS_CUDA(cudaMemsetAsync(sp->cert_xd.p + rH, 0, nH * sizeof(double2), s)); // V_0 = 0
     }
     if (sp->implicit) { // implicit-CSR form: keys + rank tables; the fallback runs at collect
-        CertImplArgs c{};
-        c.values_out = sp->v[0].p;
-        c.act_out = sp->actions_dev.p;
-        c.lb = sp->cert_lb.p;
-        c.discount = key.discount;
+        const CertData data = cert_data_of(sp);
         int launches = 0;
         const bool pdl = g.layer_ev.empty() && !std::getenv("VCS_NO_PDL");
         for (int t = H - 1; t >= 0; --t) {
-            c.row0 = sp->layer_off[t];
-            c.n = sp->layer_off[t + 1] - sp->layer_off[t];
-            c.m = H - t;
-            c.keys = sp->keys.p + sp->key_off[t];
-            c.L = sp->params_dev.p + t;
-            c.rank = sp->rank_tables.p + sp->rank_off[t];
-            bool dense_order = false;
-            if (ks) {
-                c.xd_next = sp->cert_xd.p + ((t + 1) & 1) * half;
-                c.xd_cur = sp->cert_xd.p + (t & 1) * half;
-                c.dense_n = t >= 1 ? sp->plan.layers[static_cast<size_t>(t - 1)].dense_size : 0;
-                c.rank_self = t >= 1 ? sp->rank_tables.p + sp->rank_off[static_cast<size_t>(t - 1)] : nullptr;
-                c.write_own = t >= 1 ? 1 : 0;
-                // walk the key space when at least half of it is reached (coalesced pair
-                // writes, no key loads); sparse layers walk their states
-                dense_order = t >= 1 && c.n * 2 >= c.dense_n;
-            } else {
-                c.xd_next = sp->cert_xd.p + sp->layer_off[t + 1];
-                c.xd_cur = sp->cert_xd.p + c.row0;
-            }
-            if (c.n) {
-                dispatch_words_solve(max_key_words(sp), [&](auto wm) {
-                    constexpr int WM = decltype(wm)::value;
-                    // 3 blocks per SM (80 registers, no spills): C4 0.68 ms vs 0.72 at 4, 0.74 at 2
-                    const void* fn =
-                        dense_order ? (disc ? reinterpret_cast<const void*>(k_cert_dense<WM, true, 3>)
-                                            : reinterpret_cast<const void*>(k_cert_dense<WM, false, 3>))
-                                    : (disc ? reinterpret_cast<const void*>(k_cert_implicit<WM, true, 3, false>)
-                                            : reinterpret_cast<const void*>(k_cert_implicit<WM, false, 3, false>));
-                    int per_sm = 0;
-                    VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
-                    const uint64_t items = dense_order ? c.dense_n : c.n;
-                    const uint64_t blocks = std::max<uint64_t>(
-                        1, std::min<uint64_t>((items + 255) / 256,
-                                              static_cast<uint64_t>(std::max(1, per_sm)) * sp->num_sms));
-                    // layers after the first launch programmatically (PDL): their blocks load the
-                    // layer constants and first keys while the previous layer drains.  Not with
-                    // per-layer events in between (vcs_solve's streamed download).
-                    cudaLaunchConfig_t cfg{};
-                    cfg.gridDim = dim3(static_cast<unsigned>(blocks));
-                    cfg.blockDim = dim3(256);
-                    cfg.stream = s;
-                    cudaLaunchAttribute attr[1];
-                    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-                    attr[0].val.programmaticStreamSerializationAllowed = 1;
-                    cfg.attrs = attr;
-                    cfg.numAttrs = (pdl && t < H - 1) ? 1 : 0;
-                    if (dense_order) {
-                        if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense<WM, true, 3>, c));
-                        else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense<WM, false, 3>, c));
-                    } else if (ks) {
-                        if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, true, 3, true>, c));
-                        else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, false, 3, true>, c));
-                    } else {
-                        if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, true, 3, false>, c));
-                        else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, false, 3, false>, c));
-                    }
-                    VCS_LAUNCHED();
-                });
+            CertLayer L = cert_layer(sp, t, sp->cert_xd.p, half, ks);
+            L.d_hi = L.dense_order ? L.dense_n : 0;
+            if (L.n) {
+                launch_cert_layer(sp, data, L, sp->v[0].p, sp->actions_dev.p, sp->cert_lb.p,
+                                  key.discount, 1, pdl && t < H - 1, s);
                 ++launches;
             }
             if (!g.layer_ev.empty()) record_event(g.layer_ev[static_cast<size_t>(t)], s, capturing);
@@ -1339,6 +1404,7 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
         record_event(g.ev[2], s, capturing);
         g.launches = launches + 1;
         g.implicit = true;
+        g.fallback_at_collect = true;
         return;
     }
     if (!capturing) raise(VCS_EINVAL, "the certified solve is only recorded into a CUDA graph");
@@ -1358,6 +1424,7 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
     a.act_out = sp->actions_dev.p;
     a.lb = sp->cert_lb.p;
     a.discount = key.discount;
+    a.write_out = 1;
     int launches = 0;
     for (int t = H - 1; t >= 0; --t) {
         a.row0 = sp->layer_off[t];
@@ -1625,6 +1692,483 @@ void band_plan(vcs_space* sp, int world, int rank) {
 }
 
 } // namespace
+
+// ---- multi-GPU certified pass (replaces the block-parallel driver of
+// parallel_vi.cpp:68-107 for n GPUs of this process) ----------------------------------------------
+//
+// ONE state space, n ranks (GPUs; a device may repeat, which runs several ranks on one GPU —
+// the emulated-rank test mode).  Layer t of the backward pass is split into contiguous ranges of
+// its pair index space: the key space (implicit form, dense-order layers) or the BFS rows
+// (explicit CSR).  Small and sparse layers are computed whole by every rank (replicated: no
+// exchange).  After a split layer t, rank h pulls from each owner q the part of q's range that
+// h's layer t-1 reads:
+//   * key space, non-retiring transition: a successor index is d - demand*W_p <= d, so rank h
+//     with layer-(t-1) range [lo, hi) reads [lo - demand*max_p W_p, hi): a forward halo from
+//     the ranks below it;
+//   * anything else (retiring transition, explicit CSR, replicated consumer): the whole layer
+//     (an all-gather).
+// The pulls are peer copies (cudaMemcpyPeerAsync over NVLink) on the puller's stream after the
+// owner's layer event; a rank rewrites a pair half two layers later only after every puller's
+// copy event (write-after-read).  Values and actions are stored by every rank's kernel straight
+// into the primary GPU's result arrays (peer stores).  Each rank's residual lower bounds are
+// gathered to the primary, max-reduced and checked there (k_cert_check_multi).  No kernel waits
+// on another: all ordering is by stream events, so the same code runs with every rank on one GPU.
+// The whole pass is captured into one CUDA graph (one launch per solve).
+
+struct MultiRank {
+    int device = 0;
+    bool shared = false; // on the primary GPU: reads the space's own buffers
+    cudaStream_t stream = nullptr;
+    // replicas of the space's read-only data on this rank's GPU (unused when `shared`)
+    uint64_t* keys = nullptr;
+    uint32_t* rank_tables = nullptr;
+    LayerParam* params = nullptr;
+    uint32_t* row_ptr = nullptr;
+    uint32_t* succ = nullptr;
+    double* reward = nullptr;
+    int32_t* action = nullptr;
+    double2* xd = nullptr; // this rank's pair buffer (key space: two halves; explicit: S pairs)
+    double* lb = nullptr;  // H+2 residual lower bounds
+    std::vector<cudaEvent_t> ev_layer, ev_copy; // per layer t
+    cudaEvent_t ev_done = nullptr;
+    std::vector<std::pair<int, void*>> owned; // (device, pointer) allocations
+};
+
+struct MultiState {
+    std::vector<int> devices;
+    int exchange = 0;
+    int primary = 0;
+    bool keyspace = false;
+    uint64_t half = 0;
+    std::vector<MultiRank> ranks;
+    // plan per layer t (0..H-1): split or replicated, the ranks' ranges and needed windows
+    std::vector<char> split;
+    std::vector<std::vector<uint64_t>> lo, hi, need_lo, need_hi;
+    double* lb_stage = nullptr;
+    cudaEvent_t ev_fork = nullptr;
+    std::map<GraphKey, CachedGraph> graphs;
+    bool no_graph = false;
+    double halo_bytes = 0.0;   // pair bytes pulled between ranks per solve
+    int split_layers = 0, replicated_layers = 0;
+    double max_share = 0.0;    // largest rank share of the split work (1/n = balanced)
+};
+
+namespace {
+
+void* multi_alloc(MultiRank& r, size_t bytes) {
+    VCS_CUDA(cudaSetDevice(r.device));
+    void* p = nullptr;
+    VCS_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+    r.owned.emplace_back(r.device, p);
+    return p;
+}
+
+template <class T>
+T* replica(MultiRank& r, const DevBuf<T>& src, size_t n, int src_dev) {
+    if (!src.p || n == 0) return nullptr;
+    T* p = static_cast<T*>(multi_alloc(r, n * sizeof(T)));
+    VCS_CUDA(cudaMemcpyPeer(p, r.device, src.p, src_dev, n * sizeof(T)));
+    return p;
+}
+
+// The largest successor weight of an eligible cloud of transition t-1 -> t when nothing retires
+// and the successor numbering equals the state numbering (then succ = d - demand*W_p); 0 = no
+// such bound (the consumer reads the whole layer).
+int64_t halo_shift(const vcs_space* sp, int t_consumer) {
+    const LayerParam& P = sp->plan.layers[static_cast<size_t>(t_consumer)];
+    if (P.n_keep != P.n_active || P.dense_size == 0 || P.self_size != P.dense_size) return -1;
+    uint64_t wmax = 0;
+    for (int p = 0; p < P.n_active; ++p) {
+        if (P.keep_idx[p] != p || P.wnext[p] != P.wself[p]) return -1;
+        if (P.attr[p]) wmax = std::max<uint64_t>(wmax, P.wnext[p]);
+    }
+    return static_cast<int64_t>(static_cast<uint64_t>(P.demand) * wmax);
+}
+
+void multi_plan(const vcs_space* sp, MultiState& ms) {
+    const int H = sp->H, n = static_cast<int>(ms.ranks.size());
+    uint64_t min_split = 65536;
+    if (const char* e = std::getenv("VCS_MULTI_MIN_SPLIT")) min_split = std::strtoull(e, nullptr, 10);
+    ms.split.assign(static_cast<size_t>(H), 0);
+    ms.lo.assign(static_cast<size_t>(H), std::vector<uint64_t>(static_cast<size_t>(n), 0));
+    ms.hi = ms.need_lo = ms.need_hi = ms.lo;
+    std::vector<uint64_t> size(static_cast<size_t>(H), 0);
+    ms.split_layers = ms.replicated_layers = 0;
+    double split_work = 0.0, max_rank_work = 0.0;
+    std::vector<double> rank_work(static_cast<size_t>(n), 0.0);
+    for (int t = 0; t < H; ++t) {
+        const CertLayer L = cert_layer(sp, t, nullptr, ms.half, ms.keyspace);
+        bool split = false;
+        uint64_t sz = 0;
+        if (ms.keyspace) {
+            sz = L.dense_order ? L.dense_n : L.n;
+            split = L.dense_order && sz >= min_split && n > 1;
+        } else {
+            sz = L.n;
+            split = sz >= min_split && n > 1;
+        }
+        size[static_cast<size_t>(t)] = sz;
+        ms.split[static_cast<size_t>(t)] = split ? 1 : 0;
+        for (int r = 0; r < n; ++r) {
+            ms.lo[t][r] = split ? sz * static_cast<uint64_t>(r) / static_cast<uint64_t>(n) : 0;
+            ms.hi[t][r] = split ? sz * static_cast<uint64_t>(r + 1) / static_cast<uint64_t>(n) : sz;
+            if (split) rank_work[static_cast<size_t>(r)] += static_cast<double>(ms.hi[t][r] - ms.lo[t][r]);
+        }
+        if (split) {
+            ++ms.split_layers;
+            split_work += static_cast<double>(sz);
+        } else {
+            ++ms.replicated_layers;
+        }
+    }
+    for (double w : rank_work) max_rank_work = std::max(max_rank_work, w);
+    ms.max_share = split_work > 0 ? max_rank_work / split_work : 1.0;
+    // the window of layer t's pairs each rank's layer t-1 reads
+    ms.halo_bytes = 0.0;
+    for (int t = 1; t < H; ++t) {
+        if (!ms.split[static_cast<size_t>(t)]) continue;
+        const uint64_t D = size[static_cast<size_t>(t)];
+        const bool consumer_split = ms.split[static_cast<size_t>(t - 1)] != 0;
+        const int64_t shift = (ms.keyspace && consumer_split && ms.exchange == VCS_EXCHANGE_HALO)
+                                  ? halo_shift(sp, t - 1) : -1;
+        for (int h = 0; h < n; ++h) {
+            uint64_t a = 0, b = D;
+            if (shift >= 0) {
+                const uint64_t clo = ms.lo[t - 1][h], chi = ms.hi[t - 1][h];
+                a = clo > static_cast<uint64_t>(shift) ? clo - static_cast<uint64_t>(shift) : 0;
+                b = std::min(D, chi);
+                if (chi <= clo) a = b = 0; // no layer t-1 work: nothing needed
+            }
+            ms.need_lo[t][h] = a;
+            ms.need_hi[t][h] = b;
+            for (int q = 0; q < n; ++q) {
+                if (q == h) continue;
+                const uint64_t x = std::max(a, ms.lo[t][q]), y = std::min(b, ms.hi[t][q]);
+                if (x < y) ms.halo_bytes += 16.0 * static_cast<double>(y - x);
+            }
+        }
+    }
+}
+
+void destroy_rank(MultiRank& r) {
+    cudaSetDevice(r.device);
+    if (r.stream) cudaStreamSynchronize(r.stream);
+    for (auto e : r.ev_layer)
+        if (e) cudaEventDestroy(e);
+    for (auto e : r.ev_copy)
+        if (e) cudaEventDestroy(e);
+    if (r.ev_done) cudaEventDestroy(r.ev_done);
+    for (auto& [dev, p] : r.owned) {
+        cudaSetDevice(dev);
+        cudaFree(p);
+    }
+    r.owned.clear();
+    if (r.stream) {
+        cudaSetDevice(r.device);
+        cudaStreamDestroy(r.stream);
+    }
+    r.stream = nullptr;
+}
+
+// Set up (or reuse) the per-rank state for `devices`.
+MultiState& multi_state(vcs_space* sp, const std::vector<int>& devices, int exchange) {
+    if (sp->multi && (sp->multi->devices != devices || sp->multi->exchange != exchange)) {
+        destroy_multi(sp->multi);
+        sp->multi = nullptr;
+    }
+    if (sp->multi) return *sp->multi;
+    auto ms = std::make_unique<MultiState>();
+    ms->devices = devices;
+    ms->exchange = exchange;
+    ms->primary = sp->device;
+    ms->keyspace = cert_keyspace(sp);
+    if (sp->implicit && !ms->keyspace)
+        raise(VCS_EINVAL, "the multi-GPU certified pass needs key-space pairs (unset VCS_CERT_BFS)");
+    if (!sp->implicit) ensure_csr(sp);
+    ms->half = ms->keyspace ? cert_half(sp) : 0;
+    const int H = sp->H;
+    const size_t xd_n = ms->keyspace ? 2 * ms->half : sp->S;
+    ms->ranks.resize(devices.size());
+    try {
+        for (size_t i = 0; i < devices.size(); ++i) {
+            MultiRank& r = ms->ranks[i];
+            r.device = devices[i];
+            r.shared = r.device == sp->device;
+            VCS_CUDA(cudaSetDevice(r.device));
+            VCS_CUDA(cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking));
+            if (!r.shared) {
+                if (sp->implicit) {
+                    r.keys = replica(r, sp->keys, sp->key_off.back(), sp->device);
+                    r.rank_tables = replica(r, sp->rank_tables, sp->rank_off.back(), sp->device);
+                    r.params = replica(r, sp->params_dev, static_cast<size_t>(H), sp->device);
+                } else {
+                    r.row_ptr = replica(r, sp->row_ptr, sp->S + 1, sp->device);
+                    r.succ = replica(r, sp->succ, sp->E, sp->device);
+                    r.reward = replica(r, sp->reward, sp->E, sp->device);
+                    r.action = replica(r, sp->action, sp->E, sp->device);
+                }
+            }
+            r.xd = static_cast<double2*>(multi_alloc(r, xd_n * sizeof(double2)));
+            r.lb = static_cast<double*>(multi_alloc(r, (static_cast<size_t>(H) + 2) * sizeof(double)));
+            VCS_CUDA(cudaSetDevice(r.device));
+            r.ev_layer.assign(static_cast<size_t>(std::max(H, 1)), nullptr);
+            r.ev_copy.assign(static_cast<size_t>(std::max(H, 1)), nullptr);
+            for (auto& e : r.ev_layer) VCS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            for (auto& e : r.ev_copy) VCS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            VCS_CUDA(cudaEventCreateWithFlags(&r.ev_done, cudaEventDisableTiming));
+        }
+        // NVLink peer access between every pair of distinct GPUs (peer stores into the
+        // primary's results, halo copies between ranks)
+        {
+            std::vector<int> uniq(devices.begin(), devices.end());
+            uniq.push_back(sp->device);
+            std::sort(uniq.begin(), uniq.end());
+            uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+            for (int a : uniq)
+                for (int b : uniq) {
+                    if (a == b) continue;
+                    int can = 0;
+                    VCS_CUDA(cudaDeviceCanAccessPeer(&can, a, b));
+                    if (!can)
+                        raise(VCS_ECUDA, "GPU " + std::to_string(a) + " cannot access GPU " +
+                                             std::to_string(b) + " (no peer path)");
+                    VCS_CUDA(cudaSetDevice(a));
+                    const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+                    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                        raise(VCS_ECUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+                    cudaGetLastError();
+                }
+        }
+        { // the ranks' lower bounds, gathered on the primary
+            VCS_CUDA(cudaSetDevice(sp->device));
+            void* p = nullptr;
+            VCS_CUDA(cudaMalloc(&p, devices.size() * (static_cast<size_t>(H) + 2) * sizeof(double)));
+            ms->ranks[0].owned.emplace_back(sp->device, p);
+            ms->lb_stage = static_cast<double*>(p);
+        }
+        VCS_CUDA(cudaEventCreateWithFlags(&ms->ev_fork, cudaEventDisableTiming));
+        multi_plan(sp, *ms);
+    } catch (...) {
+        destroy_multi(ms.release());
+        VCS_CUDA(cudaSetDevice(sp->device));
+        throw;
+    }
+    sp->multi = ms.release();
+    return *sp->multi;
+}
+
+// lb[k] = max over ranks, then the certificate test of k_cert_check.
+__global__ void k_cert_check_multi(const double* __restrict__ lb_stage, int n_ranks, int H,
+                                   double eps, int max_sweeps, double* lb_out, SolveCtrl* ctrl) {
+    __shared__ int bad;
+    if (threadIdx.x == 0) bad = max_sweeps < H + 1 ? 1 : 0;
+    __syncthreads();
+    for (int k = 1 + threadIdx.x; k <= H; k += blockDim.x) {
+        double m = 0.0;
+        for (int r = 0; r < n_ranks; ++r) m = fmax(m, lb_stage[static_cast<size_t>(r) * (H + 2) + k]);
+        lb_out[k] = m;
+        if (!(m >= eps)) bad = 1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && !bad) {
+        ctrl->sweeps = H + 1;
+        ctrl->stop = 1;
+        ctrl->certified = 1;
+    }
+}
+
+// Enqueue (or record into a capture on `s`) one multi-GPU certified solve.
+void record_multi(vcs_space* sp, MultiState& ms, const GraphKey& key, CachedGraph& g,
+                  cudaStream_t s, bool capturing) {
+    const int H = sp->H, n = static_cast<int>(ms.ranks.size());
+    const bool ks = ms.keyspace;
+    int launches = 0;
+    VCS_CUDA(cudaSetDevice(sp->device));
+    VCS_CUDA(cudaMemsetAsync(sp->ctrl.p, 0, sizeof(SolveCtrl), s));
+    const uint64_t rH = sp->layer_off[H], nH = sp->S - rH;
+    VCS_CUDA(cudaMemsetAsync(sp->v[0].p + rH, 0, nH * sizeof(double), s));
+    VCS_CUDA(cudaMemsetAsync(sp->actions_dev.p + rH, 0xff, nH * sizeof(int32_t), s));
+    record_event(g.ev[0], s, capturing);
+    VCS_CUDA(cudaEventRecord(ms.ev_fork, s));
+    for (auto& r : ms.ranks) {
+        VCS_CUDA(cudaSetDevice(r.device));
+        VCS_CUDA(cudaStreamWaitEvent(r.stream, ms.ev_fork, 0));
+        VCS_CUDA(cudaMemsetAsync(r.lb, 0, (H + 2) * sizeof(double), r.stream));
+        if (ks)
+            VCS_CUDA(cudaMemsetAsync(r.xd + (H & 1) * ms.half, 0, sizeof(double2), r.stream));
+        else
+            VCS_CUDA(cudaMemsetAsync(r.xd + rH, 0, nH * sizeof(double2), r.stream));
+    }
+    // readers[t][q]: ranks that pulled from rank q's layer-t pairs (write-after-read)
+    std::vector<std::vector<std::vector<int>>> readers(
+        static_cast<size_t>(H) + 2, std::vector<std::vector<int>>(static_cast<size_t>(n)));
+    for (int t = H - 1; t >= 0; --t) {
+        const bool split = ms.split[static_cast<size_t>(t)] != 0;
+        for (int ri = 0; ri < n; ++ri) {
+            MultiRank& r = ms.ranks[static_cast<size_t>(ri)];
+            VCS_CUDA(cudaSetDevice(r.device));
+            // this layer rewrites the pair half of layer t+2: wait for its pullers' copies
+            if (t + 2 <= H - 1)
+                for (int h : readers[static_cast<size_t>(t + 2)][static_cast<size_t>(ri)])
+                    VCS_CUDA(cudaStreamWaitEvent(r.stream, ms.ranks[static_cast<size_t>(h)].ev_copy[static_cast<size_t>(t + 2)], 0));
+            CertData data = r.shared ? cert_data_of(sp)
+                                     : CertData{r.keys, r.rank_tables, r.params};
+            const uint64_t lo = ms.lo[t][ri], hi = ms.hi[t][ri];
+            if (ks) {
+                CertLayer L = cert_layer(sp, t, r.xd, ms.half, true);
+                if (L.dense_order) {
+                    L.d_lo = lo;
+                    L.d_hi = hi;
+                }
+                if (L.n && (!L.dense_order || hi > lo)) {
+                    launch_cert_layer(sp, data, L, sp->v[0].p, sp->actions_dev.p, r.lb, key.discount,
+                                      (split || ri == 0) ? 1 : 0, false, r.stream);
+                    ++launches;
+                }
+            } else if (hi > lo) {
+                CertArgs a{};
+                a.row_ptr = r.shared ? sp->row_ptr.p : r.row_ptr;
+                a.succ = r.shared ? sp->succ.p : r.succ;
+                a.reward = r.shared ? sp->reward.p : r.reward;
+                a.action = r.shared ? sp->action.p : r.action;
+                a.values_out = sp->v[0].p;
+                a.act_out = sp->actions_dev.p;
+                a.write_out = (split || ri == 0) ? 1 : 0;
+                a.lb = r.lb;
+                a.discount = key.discount;
+                a.row0 = sp->layer_off[t] + lo;
+                a.n = hi - lo;
+                a.next_row0 = sp->layer_off[t + 1];
+                a.m = H - t;
+                a.xd_next = r.xd + a.next_row0;
+                a.xd_cur = r.xd + a.row0;
+                const bool disc = is_discounted(key.discount);
+                const unsigned blocks = static_cast<unsigned>(std::max<uint64_t>(
+                    1, std::min<uint64_t>((a.n + 255) / 256, static_cast<uint64_t>(4) * sp->num_sms)));
+                if (disc) k_cert_rows<true, 4, 4><<<blocks, 256, 0, r.stream>>>(a);
+                else k_cert_rows<false, 4, 4><<<blocks, 256, 0, r.stream>>>(a);
+                VCS_LAUNCHED();
+                ++launches;
+            }
+            VCS_CUDA(cudaEventRecord(r.ev_layer[static_cast<size_t>(t)], r.stream));
+        }
+        if (!split || t == 0) continue;
+        // pulls: rank h copies from owner q the part of q's range its layer t-1 reads
+        const uint64_t base = ks ? (t & 1) * ms.half : sp->layer_off[t];
+        for (int h = 0; h < n; ++h) {
+            MultiRank& dst = ms.ranks[static_cast<size_t>(h)];
+            VCS_CUDA(cudaSetDevice(dst.device));
+            for (int q = 0; q < n; ++q) {
+                if (q == h) continue;
+                const uint64_t x = std::max(ms.need_lo[t][h], ms.lo[t][q]);
+                const uint64_t y = std::min(ms.need_hi[t][h], ms.hi[t][q]);
+                if (x >= y) continue;
+                MultiRank& src = ms.ranks[static_cast<size_t>(q)];
+                VCS_CUDA(cudaStreamWaitEvent(dst.stream, src.ev_layer[static_cast<size_t>(t)], 0));
+                // (UVA copy: capturable, peer-to-peer over NVLink between the two GPUs)
+                VCS_CUDA(cudaMemcpyAsync(dst.xd + base + x, src.xd + base + x,
+                                         (y - x) * sizeof(double2), cudaMemcpyDefault, dst.stream));
+                readers[static_cast<size_t>(t)][static_cast<size_t>(q)].push_back(h);
+            }
+            VCS_CUDA(cudaEventRecord(dst.ev_copy[static_cast<size_t>(t)], dst.stream));
+        }
+    }
+    // every rank's lower bounds to the primary; join
+    for (int ri = 0; ri < n; ++ri) {
+        MultiRank& r = ms.ranks[static_cast<size_t>(ri)];
+        VCS_CUDA(cudaSetDevice(r.device));
+        VCS_CUDA(cudaMemcpyAsync(ms.lb_stage + static_cast<size_t>(ri) * (H + 2), r.lb,
+                                 (H + 2) * sizeof(double), cudaMemcpyDefault, r.stream));
+        VCS_CUDA(cudaEventRecord(r.ev_done, r.stream));
+    }
+    VCS_CUDA(cudaSetDevice(sp->device));
+    for (auto& r : ms.ranks) VCS_CUDA(cudaStreamWaitEvent(s, r.ev_done, 0));
+    k_cert_check_multi<<<1, 64, 0, s>>>(ms.lb_stage, n, H, key.eps, key.max_sweeps, sp->cert_lb.p,
+                                        sp->ctrl.p);
+    VCS_LAUNCHED();
+    record_event(g.ev[1], s, capturing);
+    record_event(g.ev[2], s, capturing);
+    g.launches = launches + 1;
+}
+
+} // namespace
+
+void destroy_multi(MultiState* ms) {
+    if (!ms) return;
+    for (auto& r : ms->ranks) destroy_rank(r);
+    for (auto& [k, g] : ms->graphs) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        for (auto& e : g.ev)
+            if (e) cudaEventDestroy(e);
+    }
+    if (ms->ev_fork) cudaEventDestroy(ms->ev_fork);
+    delete ms;
+}
+
+namespace {
+// Enqueue one multi-GPU certified solve on `s` (the primary's stream): captured into a graph on
+// first use, replayed afterwards.
+CachedGraph& enqueue_multi(vcs_space* sp, MultiState& ms, const GraphKey& key, cudaStream_t s) {
+    auto it = ms.graphs.find(key);
+    if (it == ms.graphs.end()) {
+        CachedGraph g;
+        g.method = kMethodCertified;
+        g.n_sweeps = key.max_sweeps;
+        for (auto& e : g.ev) VCS_CUDA(cudaEventCreate(&e));
+        it = ms.graphs.emplace(key, g).first;
+    }
+    CachedGraph& g = it->second;
+    g.implicit = sp->implicit;
+    g.fallback_at_collect = true;
+    g.n_ranks = static_cast<int>(ms.ranks.size());
+    if (!g.exec && !ms.no_graph && !std::getenv("VCS_NO_GRAPH")) {
+        cudaStream_t cs = sp->stream;
+        if (cs != s) VCS_CUDA(cudaStreamSynchronize(s));
+        VCS_CUDA(cudaSetDevice(sp->device));
+        VCS_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        g_capturing = true;
+        cudaGraph_t graph = nullptr;
+        try {
+            record_multi(sp, ms, key, g, cs, true);
+            unnote_launch(static_cast<uint64_t>(g.launches));
+            g_capturing = false;
+            VCS_CUDA(cudaSetDevice(sp->device));
+            VCS_CUDA(cudaStreamEndCapture(cs, &graph));
+        } catch (const Error& e) {
+            g_capturing = false;
+            cudaSetDevice(sp->device);
+            cudaGraph_t dummy = nullptr;
+            cudaStreamEndCapture(cs, &dummy);
+            if (dummy) cudaGraphDestroy(dummy);
+            cudaGetLastError();
+            if (std::getenv("VCS_TRACE")) std::fprintf(stderr, "[vcs multi] capture: %s\n", e.msg.c_str());
+            ms.no_graph = true; // this driver / topology cannot capture it: direct launches
+        }
+        if (graph) {
+            const cudaError_t ierr = cudaGraphInstantiate(&g.exec, graph, 0);
+            cudaGraphDestroy(graph);
+            if (ierr != cudaSuccess) {
+                if (std::getenv("VCS_TRACE"))
+                    std::fprintf(stderr, "[vcs multi] instantiate: %s\n", cudaGetErrorString(ierr));
+                cudaGetLastError();
+                g.exec = nullptr;
+                ms.no_graph = true;
+            }
+        }
+    }
+    VCS_CUDA(cudaSetDevice(sp->device));
+    if (g.exec) {
+        VCS_CUDA(cudaGraphLaunch(g.exec, s));
+        note_launch(static_cast<uint64_t>(g.launches));
+    } else {
+        record_multi(sp, ms, key, g, s, false);
+        VCS_CUDA(cudaSetDevice(sp->device));
+    }
+    ++g.uses;
+    return g;
+}
+} // namespace
+
 } // namespace vcs
 
 using vcs::guarded;
@@ -1685,6 +2229,73 @@ int enqueue_impl(vcs_space* sp, const vcs_solve_opts* opts, void* stream, int st
 
 int vcs_solve_enqueue(vcs_space* sp, const vcs_solve_opts* opts, void* stream) {
     return enqueue_impl(sp, opts, stream, 0);
+}
+
+int vcs_solve_multi_enqueue(vcs_space* sp, const vcs_solve_opts* opts, int32_t n_ranks,
+                            const int32_t* devices, int32_t exchange, void* stream) {
+    if (n_ranks == 1 && (!devices || devices[0] == sp->device))
+        return enqueue_impl(sp, opts, stream, 0);
+    return guarded([&] {
+        vcs_solve_opts o{1e-6, 1, 0, 1.0, VCS_METHOD_AUTO};
+        if (opts) o = *opts;
+        if (!(o.epsilon > 0.0))
+            raise(VCS_EINVAL, "epsilon must be > 0 (value iteration would never terminate)");
+        if (o.method != VCS_METHOD_AUTO && o.method != VCS_METHOD_CERTIFIED)
+            raise(VCS_EINVAL, "the multi-GPU solve runs the certified pass (method AUTO or CERTIFIED)");
+        if (n_ranks < 1) raise(VCS_EINVAL, "n_gpus must be >= 1");
+        if (exchange != VCS_EXCHANGE_HALO && exchange != VCS_EXCHANGE_ALLGATHER)
+            raise(VCS_EINVAL, "unknown exchange mode");
+        int n_dev = 0;
+        VCS_CUDA(cudaGetDeviceCount(&n_dev));
+        std::vector<int> devs(static_cast<size_t>(n_ranks));
+        for (int r = 0; r < n_ranks; ++r) {
+            devs[static_cast<size_t>(r)] = devices ? devices[r] : (sp->device + r) % n_dev;
+            if (devs[static_cast<size_t>(r)] < 0 || devs[static_cast<size_t>(r)] >= n_dev)
+                raise(VCS_EINVAL, "device index out of range");
+        }
+        vcs::bind_device(sp->device);
+        int M = sp->H + 1;
+        if (o.max_sweeps > 0) M = std::min(M, o.max_sweeps);
+        vcs::ensure_solve_buffers(sp, sp->H + 1);
+        if (sp->cert_lb.n < static_cast<size_t>(sp->H) + 2) {
+            sp->cert_lb.exact(static_cast<size_t>(sp->H) + 2, sp->stream);
+            VCS_CUDA(cudaStreamSynchronize(sp->stream));
+        }
+        vcs::MultiState& ms = vcs::multi_state(sp, devs, exchange);
+        const vcs::GraphKey key{o.epsilon, o.discount, 0, M, vcs::kMethodCertified, 0};
+        const vcs::StreamUse s(sp, stream);
+        auto& g = vcs::enqueue_multi(sp, ms, key, s);
+        vcs::bind_device(sp->device);
+        sp->last_graph = &g;
+        sp->last_key_skip = 0;
+        sp->last_opts = o;
+        sp->last_opts.method = VCS_METHOD_CERTIFIED;
+        return VCS_OK;
+    });
+}
+
+int vcs_solve_multi(vcs_space* sp, const vcs_solve_opts* opts, int32_t n_ranks,
+                    const int32_t* devices, int32_t exchange, double* values_out,
+                    int32_t* actions_out, vcs_solve_report* report) {
+    const int rc = vcs_solve_multi_enqueue(sp, opts, n_ranks, devices, exchange, nullptr);
+    if (rc != VCS_OK) return rc;
+    return vcs_solve_collect(sp, values_out, actions_out, report, nullptr);
+}
+
+int vcs_multi_info(const vcs_space* sp, vcs_multi_report* out) {
+    return guarded([&] {
+        if (!sp->multi) raise(VCS_EINVAL, "no multi-GPU solve ran on this space");
+        const vcs::MultiState& ms = *sp->multi;
+        *out = vcs_multi_report{};
+        out->n_ranks = static_cast<int32_t>(ms.ranks.size());
+        out->split_layers = ms.split_layers;
+        out->replicated_layers = ms.replicated_layers;
+        out->exchange = ms.exchange;
+        out->halo_bytes = ms.halo_bytes;
+        out->max_share = ms.max_share;
+        out->graph = ms.no_graph ? 0 : 1;
+        return VCS_OK;
+    });
 }
 
 namespace {
@@ -1970,7 +2581,7 @@ int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
         vcs::SolveCtrl ctrl{};
         VCS_CUDA(cudaMemcpyAsync(&ctrl, sp->ctrl.p, sizeof ctrl, cudaMemcpyDeviceToHost, s));
         VCS_CUDA(cudaStreamSynchronize(s));
-        if (sp->last_graph->implicit && !ctrl.certified) {
+        if (sp->last_graph->fallback_at_collect && !ctrl.certified) {
             // the proof failed (an early stop is possible): the layer wavefront on the explicit
             // CSR, materialised now, gives the reference's result
             if (std::getenv("VCS_PROFILE_NO_FALLBACK"))

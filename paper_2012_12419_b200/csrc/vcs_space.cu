@@ -1628,6 +1628,7 @@ int sm_count(int device) {
 } // namespace vcs
 
 vcs_space::~vcs_space() {
+    vcs::destroy_multi(multi);
     cudaSetDevice(device);
     for (auto& [st, ev] : use_ev) {
         if (!ev) continue;

@@ -597,11 +597,16 @@ class ViResult:
 
 
 def run_value_iteration(space: StateSpace, options: ViOptions | None = None,
-                        n_workers: int = 1) -> ViResult:
+                        n_workers: int = 1, devices: Sequence[int] | None = None,
+                        exchange: int = N.VCS_EXCHANGE_HALO) -> ViResult:
     """detail::run_value_iteration (parallel_vi.cpp:48-116) on the device.
 
-    ``n_workers`` is validated like the reference; the device solve is one kernel sequence whose
-    result is independent of any partition (multi-GPU sharding: ``sharded.py``)."""
+    ``n_workers`` is validated like the reference.  The reference's workers are threads over
+    row blocks; here they are GPUs: the solve runs sharded over min(n_workers, visible GPUs)
+    devices of this process (vcs_solve_multi, one state space split layer by layer), or over
+    ``devices`` when given (a device may repeat: several ranks on one GPU).  The result is
+    bit-identical for every partition, as the reference's contract requires
+    (tests/test_parallel.cpp:89-106)."""
     options = options or ViOptions()
     if n_workers < 1:
         raise InvalidArgument("n_workers must be >= 1")
@@ -611,8 +616,21 @@ def run_value_iteration(space: StateSpace, options: ViOptions | None = None,
     opts = N.vcs_solve_opts(options.epsilon, 1 if options.skip_converged else 0, 0,
                             options.discount, options.method)
     rep = N.vcs_solve_report()
-    N.check(N.lib().vcs_solve(space.handle, C.byref(opts), N.ptr(values, C.c_double),
-                              N.ptr(actions, C.c_int32), C.byref(rep)))
+    if devices is None:
+        n_dev = max(1, N.device_count())
+        devices = [(space.info.device + r) % n_dev for r in range(min(n_workers, n_dev))]
+    devices = [int(d) for d in devices]
+    if len(devices) == 1 and devices[0] == space.info.device:
+        N.check(N.lib().vcs_solve(space.handle, C.byref(opts), N.ptr(values, C.c_double),
+                                  N.ptr(actions, C.c_int32), C.byref(rep)))
+    else:
+        if options.method not in (N.VCS_METHOD_AUTO, N.VCS_METHOD_CERTIFIED):
+            raise InvalidArgument("the multi-GPU solve runs the certified pass "
+                                  "(method AUTO or CERTIFIED)")
+        dv = np.asarray(devices, dtype=np.int32)
+        N.check(N.lib().vcs_solve_multi(space.handle, C.byref(opts), len(dv), N.ptr(dv, C.c_int32),
+                                        exchange, N.ptr(values, C.c_double),
+                                        N.ptr(actions, C.c_int32), C.byref(rep)))
     return ViResult(ValueTable(space, values, rep.sweeps, options.epsilon, rep),
                     Policy(space, actions))
 
