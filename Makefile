@@ -63,7 +63,8 @@ $(REFLIB): oracle/ref_capi.cpp include/vcs_gpu.h
 # linked (a) against the reference library as the control and (b) against the B200 drop-in shim.
 REF_TESTS  := $(REF)/tests/test_workload.cpp $(REF)/tests/test_greedy.cpp \
               $(REF)/tests/test_mdp.cpp $(REF)/tests/test_parallel.cpp
-REF_SUITES := oracle/_ref/ref_suite_on_reference oracle/_ref/ref_suite_on_b200
+REF_SUITES := oracle/_ref/ref_suite_on_reference oracle/_ref/ref_suite_on_b200 \
+              oracle/_ref/acceptance_on_b200
 
 oracle/_ref/ref_suite_on_reference: tests/cpp/doctest.h tests/cpp/doctest_main.cpp
 	@mkdir -p oracle/_ref
@@ -81,3 +82,13 @@ clean:
 	rm -rf build $(LIB) $(SHIM) $(ORACLE) oracle/_ref
 
 .PHONY: all ref clean
+
+# The reference's acceptance suite (tests/acceptance.cpp, unchanged) against the drop-in shim.
+# Its criteria 6-9 exercise the reference's DSRC simulator / metrics (out of scope for the B200
+# path): those translation units are the reference's own sources, compiled where they lie.
+REF_SIM := $(REF)/core/src/metrics.cpp $(REF)/core/src/sim.cpp $(REF)/core/src/channel.cpp
+oracle/_ref/acceptance_on_b200: $(SHIM) $(SHIM_HDRS)
+	@mkdir -p oracle/_ref
+	$(CXX) -std=c++20 -O2 -pthread -I$(PKG)/include -I$(REF)/core/include -I$(REF)/tests \
+	    -DVCSCHED_DATA_DIR='"tests/golden"' -o $@ $(REF)/tests/acceptance.cpp $(REF_SIM) \
+	    -L$(PKG) -lvcsched_b200 -lvcs_gpu -Wl,-rpath,'$$ORIGIN/../../$(PKG)'

@@ -14,8 +14,10 @@
  * messages of the reference exceptions are reproduced verbatim (e.g. "reachable state space
  * exceeds cap of N states", mdp.hpp:58-68).
  *
- * Threading: every call is synchronous and re-entrant; one handle must not be used by two host
- * threads at once.  There is no global mutable state apart from the per-thread error message.
+ * Threading: every call is synchronous and re-entrant.  The solve, query and rollout entry points
+ * serialise on a per-space lock, so threads may share one handle (as the reference's
+ * shared_ptr<const StateSpace> allows); a vcs_solve_enqueue / vcs_solve_collect PAIR is two
+ * calls, and a caller interleaving pairs from several threads must order them itself.
  */
 #ifndef VCS_GPU_H
 #define VCS_GPU_H
@@ -153,6 +155,15 @@ int vcs_space_locate(vcs_space* sp, int64_t n, const int32_t* free_vms, const in
 int vcs_policy_query(vcs_space* sp, int64_t n, const int32_t* free_vms, const int32_t* task_index,
                      const uint8_t* terminal, double* value_out, int32_t* action_out,
                      int64_t* idx_out, void* stream);
+/* Replaces mdp.cpp:305-324 rollout's policy walk: applies the last collected solve's policy on
+ * this space from the initial state (inst = the instance the space was built from), on the
+ * device — one kernel walks the H decisions through the device key index.  target_per_task[t]
+ * receives the cloud index chosen for flattened task t, or VCS_PAID_CLOUD.  VCS_ERANGE when a
+ * visited state is not enumerated (the reference throws std::out_of_range). */
+int vcs_rollout(vcs_space* sp, const vcs_instance* inst, int32_t* target_per_task, void* stream);
+/* Incremented whenever a collected solve replaces the device-resident results that
+ * vcs_policy_query / vcs_rollout read (callers holding older host results compare it). */
+uint64_t vcs_space_result_generation(const vcs_space* sp);
 /* Replaces mdp.cpp:236-243 StateSpace::hidden_penalty for a batch of full states. */
 int vcs_space_hidden_penalty(const vcs_space* sp, int64_t n, const int32_t* free_vms,
                              const int32_t* task_index, const uint8_t* terminal, double* out);
@@ -324,6 +335,17 @@ int vcs_greedy_batch(int32_t n, const vcs_instance* insts, int device, int32_t**
                      int64_t* paid, int64_t* unused);
 /* greedy.cpp:32-36 greedy_reward. */
 double vcs_greedy_reward(const vcs_instance* inst, int64_t placed, int64_t paid, int64_t unused);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Host memory                                                                                 */
+/* ------------------------------------------------------------------------------------------ */
+
+/* Page-locked host memory from the library's recycled pool (cudaHostAlloc costs milliseconds per
+ * call; blocks are reused across calls).  Outputs of vcs_solve in such memory stream to the host
+ * while the layer pass runs.  NULL on failure.  The C++ drop-in keeps ValueTable / Policy
+ * storage here. */
+void* vcs_host_alloc(uint64_t bytes);
+void vcs_host_free(void* p);
 
 /* ------------------------------------------------------------------------------------------ */
 /* Diagnostics                                                                                 */

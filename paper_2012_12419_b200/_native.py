@@ -28,7 +28,8 @@ EXPORTS = (
     "vcs_instance_free", "vcs_instance_generate",
     "vcs_space_build", "vcs_space_from_csr", "vcs_space_info_get", "vcs_space_layer_offsets",
     "vcs_space_layer_edges", "vcs_space_csr", "vcs_space_locate", "vcs_space_hidden_penalty",
-    "vcs_policy_query", "vcs_space_free",
+    "vcs_policy_query", "vcs_rollout", "vcs_space_result_generation", "vcs_space_free",
+    "vcs_host_alloc", "vcs_host_free",
     "vcs_solve", "vcs_solve_enqueue", "vcs_solve_collect",
     "vcs_solve_multi_enqueue", "vcs_solve_multi", "vcs_multi_info", "vcs_shard_plan", "vcs_shard_begin", "vcs_shard_sweep", "vcs_shard_finish",
     "vcs_wave_shard_begin", "vcs_wave_shard_band", "vcs_wave_shard_layer", "vcs_wave_shard_pack",
@@ -172,6 +173,10 @@ _SIGS = {
     "vcs_space_hidden_penalty": (C.c_int, [_P, C.c_int64, _I32P, _I32P, _U8P, _F64P]),
     "vcs_policy_query": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, _P, _P]),
     "vcs_space_free": (None, [_P]),
+    "vcs_rollout": (C.c_int, [_P, _INSTP, _I32P, _P]),
+    "vcs_space_result_generation": (C.c_uint64, [_P]),
+    "vcs_host_alloc": (_P, [C.c_uint64]),
+    "vcs_host_free": (None, [_P]),
     "vcs_solve": (C.c_int, [_P, C.POINTER(vcs_solve_opts), _F64P, _I32P,
                             C.POINTER(vcs_solve_report)]),
     "vcs_solve_enqueue": (C.c_int, [_P, C.POINTER(vcs_solve_opts), _P]),

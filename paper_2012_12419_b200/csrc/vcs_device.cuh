@@ -218,6 +218,10 @@ struct vcs_space {
 
     int num_sms = 148;
     vcs::MultiState* multi = nullptr; // the multi-GPU solve's per-rank state (vcs_solve_multi)
+    uint64_t result_gen = 0;          // bumped whenever result_values / result_actions change
+    // one caller at a time per space (the reference's const StateSpace may be shared by threads:
+    // the solve, query and rollout entry points serialise on this)
+    std::recursive_mutex mu;
     // caller streams that have run work on this space: the destructor waits for their last
     // recorded use before the space's blocks can be reused
     std::map<cudaStream_t, cudaEvent_t> use_ev;

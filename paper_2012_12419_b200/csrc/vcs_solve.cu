@@ -2228,11 +2228,13 @@ int enqueue_impl(vcs_space* sp, const vcs_solve_opts* opts, void* stream, int st
 } // namespace
 
 int vcs_solve_enqueue(vcs_space* sp, const vcs_solve_opts* opts, void* stream) {
+    std::lock_guard<std::recursive_mutex> space_lock(sp->mu);
     return enqueue_impl(sp, opts, stream, 0);
 }
 
 int vcs_solve_multi_enqueue(vcs_space* sp, const vcs_solve_opts* opts, int32_t n_ranks,
                             const int32_t* devices, int32_t exchange, void* stream) {
+    std::lock_guard<std::recursive_mutex> space_lock(sp->mu);
     if (n_ranks == 1 && (!devices || devices[0] == sp->device))
         return enqueue_impl(sp, opts, stream, 0);
     return guarded([&] {
@@ -2277,6 +2279,7 @@ int vcs_solve_multi_enqueue(vcs_space* sp, const vcs_solve_opts* opts, int32_t n
 int vcs_solve_multi(vcs_space* sp, const vcs_solve_opts* opts, int32_t n_ranks,
                     const int32_t* devices, int32_t exchange, double* values_out,
                     int32_t* actions_out, vcs_solve_report* report) {
+    std::lock_guard<std::recursive_mutex> space_lock(sp->mu);
     const int rc = vcs_solve_multi_enqueue(sp, opts, n_ranks, devices, exchange, nullptr);
     if (rc != VCS_OK) return rc;
     return vcs_solve_collect(sp, values_out, actions_out, report, nullptr);
@@ -2444,8 +2447,59 @@ bool is_pinned(const void* p) {
 }
 } // namespace
 
+namespace {
+std::mutex& host_alloc_mu() {
+    static std::mutex* m = new std::mutex;
+    return *m;
+}
+std::map<void*, size_t>& host_alloc_sizes() {
+    static auto* m = new std::map<void*, size_t>;
+    return *m;
+}
+} // namespace
+
+// Blocks below 1 MB come from malloc (a small result gains nothing from page-locking and would
+// tie up a large recycled pinned block); size 0 in the map marks them.
+constexpr size_t kPinnedMin = size_t(1) << 20;
+
+void* vcs_host_alloc(uint64_t bytes) {
+    try {
+        size_t got = 0;
+        void* p = nullptr;
+        if (bytes < kPinnedMin) {
+            p = std::malloc(std::max<size_t>(static_cast<size_t>(bytes), 64));
+            if (!p) return nullptr;
+        } else {
+            p = pinned_acquire(static_cast<size_t>(bytes), &got);
+        }
+        std::lock_guard<std::mutex> lk(host_alloc_mu());
+        host_alloc_sizes()[p] = got;
+        return p;
+    } catch (...) {
+        cudaGetLastError();
+        return nullptr;
+    }
+}
+
+void vcs_host_free(void* p) {
+    if (!p) return;
+    size_t n = 0;
+    {
+        std::lock_guard<std::mutex> lk(host_alloc_mu());
+        auto it = host_alloc_sizes().find(p);
+        if (it == host_alloc_sizes().end()) return;
+        n = it->second;
+        host_alloc_sizes().erase(it);
+    }
+    if (n == 0) std::free(p);
+    else pinned_release(p, n);
+}
+
+uint64_t vcs_space_result_generation(const vcs_space* sp) { return sp->result_gen; }
+
 int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int32_t* actions_out,
               vcs_solve_report* report) {
+    std::lock_guard<std::recursive_mutex> space_lock(sp->mu);
     const double t_start = vcs::trace_enabled() ? vcs::host_ms() : 0.0;
     struct TraceEnd {
         double t0;
@@ -2574,6 +2628,7 @@ int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int
 
 int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
                       vcs_solve_report* report, void* stream) {
+    std::lock_guard<std::recursive_mutex> space_lock(sp->mu);
     return guarded([&] {
         if (!sp->last_graph) raise(VCS_EINVAL, "no solve was enqueued on this space");
         vcs::bind_device(sp->device);
@@ -2604,6 +2659,7 @@ int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
         const double* vsrc = wave ? sp->v[0].p : sp->v[K & 1].p;
         sp->result_values = vsrc;
         sp->result_actions = sp->actions_dev.p;
+        ++sp->result_gen;
         if (values_out)
             VCS_CUDA(cudaMemcpyAsync(values_out, vsrc, sp->S * sizeof(double),
                                      cudaMemcpyDeviceToHost, s));

@@ -421,6 +421,47 @@ __global__ void k_policy_query(QueryArgs a) {
         a.action_out[i] = (idx >= 0 && !term && t < a.H) ? a.actions[idx] : VCS_NO_ACTION;
 }
 
+// rollout (mdp.cpp:305-324) on the device: ONE thread applies the policy from the initial
+// state: pack the layer-t key of the current free counts, locate it in the device key index,
+// read the last solve's action, apply the transition (free[a] -= demand).  status: 0 ok, 1 a
+// visited state is not in the enumerated space (the reference throws std::out_of_range).
+template <int WM>
+__global__ void k_rollout(QueryArgs a, const int32_t* __restrict__ demand, int32_t* fv,
+                          int32_t* targets, int32_t* status) {
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    for (int c = 0; c < a.n_clouds; ++c) fv[c] = a.free_vms[c];
+    for (int t = 0; t < a.H; ++t) {
+        const QueryLayer& Q = a.layers[t];
+        uint64_t k[WM];
+#pragma unroll
+        for (int w = 0; w < WM; ++w) k[w] = 0ull;
+        for (int p = 0; p < Q.n_active; ++p)
+            put_field<WM>(k, Q.bit_off[p], static_cast<uint64_t>(fv[Q.cloud[p]]));
+        uint32_t h = static_cast<uint32_t>(hash_key<WM>(k, Q.words, static_cast<uint64_t>(t) + 1)) & a.mask;
+        const uint64_t lo = a.layer_off[t], hi = a.layer_off[t + 1];
+        int64_t idx = -1;
+        for (;;) {
+            const uint32_t cur = a.table[h];
+            if (cur == kEmpty32) break;
+            if (cur >= lo && cur < hi &&
+                key_equal<WM>(a.keys + a.key_off[t] + (cur - lo) * static_cast<uint64_t>(Q.words),
+                              Q.words, k)) {
+                idx = cur;
+                break;
+            }
+            h = (h + 1) & a.mask;
+        }
+        if (idx < 0) {
+            *status = 1;
+            return;
+        }
+        const int32_t act = a.actions[idx];
+        targets[t] = act;
+        if (act >= 0) fv[act] -= demand[t];
+    }
+    *status = 0;
+}
+
 uint32_t blocks_for(uint64_t n, uint32_t threads) {
     return static_cast<uint32_t>((n + threads - 1) / threads);
 }
@@ -1838,6 +1879,7 @@ int vcs_space_csr(const vcs_space* sp, uint64_t* row_ptr, uint32_t* succ, double
 
 int vcs_space_locate(vcs_space* sp, int64_t n, const int32_t* free_vms, const int32_t* task_index,
                      const uint8_t* terminal, int64_t* idx_out) {
+    std::lock_guard<std::recursive_mutex> space_lock(sp->mu);
     return guarded([&] {
         if (!sp->has_plan) raise(VCS_EINVAL, "space was not built from an instance");
         if (n <= 0) return VCS_OK;
@@ -1909,23 +1951,15 @@ bool is_device_ptr(const void* p) {
 }
 } // namespace
 
-int vcs_policy_query(vcs_space* sp, int64_t n, const int32_t* free_vms, const int32_t* task_index,
-                     const uint8_t* terminal, double* value_out, int32_t* action_out,
-                     int64_t* idx_out, void* stream) {
-    return guarded([&] {
-        if (!sp->has_plan) raise(VCS_EINVAL, "space was not built from an instance");
-        if (!sp->result_values)
-            raise(VCS_EINVAL, "no solve results on this space (vcs_solve / vcs_solve_collect first)");
-        if (n <= 0) return VCS_OK;
-        if (!free_vms || !task_index || !terminal) raise(VCS_EINVAL, "null argument");
-        vcs::bind_device(sp->device);
-        const vcs::StreamUse s(sp, stream);
-        vcs::ensure_locate_index(sp);
-        const int K = sp->plan.n_clouds, H = sp->H;
-        const size_t ql = sizeof(vcs::QueryLayer) * (static_cast<size_t>(H) + 1);
-        const size_t lu = ((sizeof(int32_t) * std::max(K, 1) + 7) / 8) * 8;
-        const size_t lo = sizeof(uint64_t) * (static_cast<size_t>(H) + 2);
-        if (!sp->query_meta.p) { // key layouts, last_use, layer and key offsets: once per space
+namespace {
+// Device key layouts, last_use, layer and key offsets for the query / rollout kernels (once per
+// space); returns the QueryArgs fields that point into them.
+void ensure_query_meta(vcs_space* sp, vcs::QueryArgs& a) {
+    const int K = sp->plan.n_clouds, H = sp->H;
+    const size_t ql = sizeof(vcs::QueryLayer) * (static_cast<size_t>(H) + 1);
+    const size_t lu = ((sizeof(int32_t) * std::max(K, 1) + 7) / 8) * 8;
+    const size_t lo = sizeof(uint64_t) * (static_cast<size_t>(H) + 2);
+    if (!sp->query_meta.p) {
             std::vector<unsigned char> blob(ql + lu + 2 * lo, 0);
             auto* layers = reinterpret_cast<vcs::QueryLayer*>(blob.data());
             for (int t = 0; t <= H; ++t) {
@@ -1946,7 +1980,38 @@ int vcs_policy_query(vcs_space* sp, int64_t n, const int32_t* free_vms, const in
             VCS_CUDA(cudaMemcpyAsync(sp->query_meta.p, blob.data(), blob.size(),
                                      cudaMemcpyHostToDevice, sp->stream));
             VCS_CUDA(cudaStreamSynchronize(sp->stream));
-        }
+    }
+    a.layers = reinterpret_cast<const vcs::QueryLayer*>(sp->query_meta.p);
+    a.last_use = reinterpret_cast<const int32_t*>(sp->query_meta.p + ql);
+    a.layer_off = reinterpret_cast<const uint64_t*>(sp->query_meta.p + ql + lu);
+    a.key_off = reinterpret_cast<const uint64_t*>(sp->query_meta.p + ql + lu + lo);
+    a.keys = sp->keys.p;
+    a.table = sp->loc_table.p;
+    a.mask = static_cast<uint32_t>(sp->loc_cap - 1);
+    a.values = sp->result_values;
+    a.actions = sp->result_actions;
+    a.n_clouds = K;
+    a.H = H;
+    a.gamma = sp->plan.layers.empty() ? 0.0 : sp->plan.layers[0].gamma;
+}
+} // namespace
+
+int vcs_policy_query(vcs_space* sp, int64_t n, const int32_t* free_vms, const int32_t* task_index,
+                     const uint8_t* terminal, double* value_out, int32_t* action_out,
+                     int64_t* idx_out, void* stream) {
+    std::lock_guard<std::recursive_mutex> space_lock(sp->mu);
+    return guarded([&] {
+        if (!sp->has_plan) raise(VCS_EINVAL, "space was not built from an instance");
+        if (!sp->result_values)
+            raise(VCS_EINVAL, "no solve results on this space (vcs_solve / vcs_solve_collect first)");
+        if (n <= 0) return VCS_OK;
+        if (!free_vms || !task_index || !terminal) raise(VCS_EINVAL, "null argument");
+        vcs::bind_device(sp->device);
+        const vcs::StreamUse s(sp, stream);
+        vcs::ensure_locate_index(sp);
+        const int K = sp->plan.n_clouds;
+        vcs::QueryArgs a{};
+        ensure_query_meta(sp, a);
         // host or device buffers: device ones are used in place, host ones staged
         vcs::DevBuf<int32_t> dfv, dti, dact;
         vcs::DevBuf<uint8_t> dte;
@@ -1965,16 +2030,6 @@ int vcs_policy_query(vcs_space* sp, int64_t n, const int32_t* free_vms, const in
             return buf.p;
         };
         const size_t nn = static_cast<size_t>(n);
-        vcs::QueryArgs a{};
-        a.layers = reinterpret_cast<const vcs::QueryLayer*>(sp->query_meta.p);
-        a.last_use = reinterpret_cast<const int32_t*>(sp->query_meta.p + ql);
-        a.layer_off = reinterpret_cast<const uint64_t*>(sp->query_meta.p + ql + lu);
-        a.key_off = reinterpret_cast<const uint64_t*>(sp->query_meta.p + ql + lu + lo);
-        a.keys = sp->keys.p;
-        a.table = sp->loc_table.p;
-        a.mask = static_cast<uint32_t>(sp->loc_cap - 1);
-        a.values = sp->result_values;
-        a.actions = sp->result_actions;
         a.free_vms = stage_in(free_vms, dfv, nn * static_cast<size_t>(K));
         a.task_index = stage_in(task_index, dti, nn);
         a.terminal = stage_in(terminal, dte, nn);
@@ -1982,9 +2037,6 @@ int vcs_policy_query(vcs_space* sp, int64_t n, const int32_t* free_vms, const in
         a.action_out = stage_out(action_out, dact, nn);
         a.idx_out = stage_out(idx_out, didx, nn);
         a.n = n;
-        a.n_clouds = K;
-        a.H = H;
-        a.gamma = sp->plan.layers.empty() ? 0.0 : sp->plan.layers[0].gamma;
         vcs::dispatch_words(vcs::max_words(sp), [&](auto wm) {
             constexpr int WM = decltype(wm)::value;
             vcs::k_policy_query<WM><<<vcs::blocks_for(static_cast<uint64_t>(n), 256), 256, 0, s>>>(a);
@@ -2002,6 +2054,50 @@ int vcs_policy_query(vcs_space* sp, int64_t n, const int32_t* free_vms, const in
         copy_out(idx_out, a.idx_out, nn);
         // staged buffers are freed in stream order; host outputs are complete on return
         if (host_out || dfv.p || dti.p || dte.p) VCS_CUDA(cudaStreamSynchronize(s));
+        return VCS_OK;
+    });
+}
+
+int vcs_rollout(vcs_space* sp, const vcs_instance* inst, int32_t* target_per_task, void* stream) {
+    std::lock_guard<std::recursive_mutex> space_lock(sp->mu);
+    return guarded([&] {
+        if (!sp->has_plan) raise(VCS_EINVAL, "space was not built from an instance");
+        if (!sp->result_actions)
+            raise(VCS_EINVAL, "no solve results on this space (vcs_solve / vcs_solve_collect first)");
+        if (!inst || !target_per_task) raise(VCS_EINVAL, "null argument");
+        const int K = sp->plan.n_clouds, H = sp->H;
+        if (inst->n_clouds != K || inst->n_tasks != H)
+            raise(VCS_EINVAL, "instance does not match the space");
+        if (H == 0) return VCS_OK;
+        vcs::bind_device(sp->device);
+        const vcs::StreamUse s(sp, stream);
+        vcs::ensure_locate_index(sp);
+        vcs::QueryArgs a{};
+        ensure_query_meta(sp, a);
+        // one staging block: initial free counts, demands, scratch free counts, targets, status
+        const size_t nk = static_cast<size_t>(std::max(K, 1)), nh = static_cast<size_t>(H);
+        std::vector<int32_t> host(2 * nk + 2 * nh + 1, 0);
+        std::memcpy(host.data(), inst->cloud_vm_free, sizeof(int32_t) * static_cast<size_t>(K));
+        std::memcpy(host.data() + nk, inst->task_demand, sizeof(int32_t) * nh);
+        vcs::DevBuf<int32_t> buf;
+        buf.exact(host.size(), s);
+        VCS_CUDA(cudaMemcpyAsync(buf.p, host.data(), sizeof(int32_t) * (nk + nh),
+                                 cudaMemcpyHostToDevice, s));
+        a.free_vms = buf.p;
+        int32_t* fv = buf.p + nk + nh;
+        int32_t* tg = fv + nk;
+        int32_t* st = tg + nh;
+        vcs::dispatch_words(vcs::max_words(sp), [&](auto wm) {
+            constexpr int WM = decltype(wm)::value;
+            vcs::k_rollout<WM><<<1, 32, 0, s>>>(a, buf.p + nk, fv, tg, st);
+            VCS_LAUNCHED();
+        });
+        VCS_CUDA(cudaMemcpyAsync(host.data() + 2 * nk + nh, tg, sizeof(int32_t) * (nh + 1),
+                                 cudaMemcpyDeviceToHost, s));
+        VCS_CUDA(cudaStreamSynchronize(s));
+        if (host[2 * nk + 2 * nh] != 0)
+            raise(VCS_ERANGE, "state not reachable in enumerated space");
+        std::memcpy(target_per_task, host.data() + 2 * nk + nh, sizeof(int32_t) * nh);
         return VCS_OK;
     });
 }

@@ -21,6 +21,8 @@
 
 namespace vcsched {
 
+using detail::PinnedVector;
+
 namespace {
 
 [[noreturn]] void rethrow(int rc, std::size_t cap = 0, bool io = false) {
@@ -338,17 +340,40 @@ MdpAction Policy::action_for(const MdpState& s) const {
     return MdpAction{actions_[space_->locate(s)]};
 }
 
+namespace {
+// The GPUs n_workers maps to: the reference's workers are threads over row blocks
+// (parallel_vi.cpp:68-107); here they are GPUs over one state space (vcs_solve_multi), as many as
+// are visible.  VCS_EMULATE_RANKS=1 runs n_workers ranks even on fewer GPUs (round robin; the
+// emulated-rank test mode of the multi-GPU path).
+std::vector<int32_t> worker_devices(int first, int n_workers) {
+    int n_dev = vcs_device_count();
+    if (n_dev < 1) n_dev = 1;
+    const bool emulate = std::getenv("VCS_EMULATE_RANKS") != nullptr;
+    const int n = emulate ? n_workers : std::min(n_workers, n_dev);
+    std::vector<int32_t> devs(static_cast<std::size_t>(n));
+    for (int r = 0; r < n; ++r) devs[static_cast<std::size_t>(r)] = (first + r) % n_dev;
+    return devs;
+}
+} // namespace
+
 namespace detail {
 ViResult run_value_iteration(std::shared_ptr<const StateSpace> space, const ViOptions& options,
                              int n_workers) {
     if (n_workers < 1) throw std::invalid_argument("n_workers must be >= 1");
-    std::vector<double> values(space->size());
-    std::vector<std::int32_t> actions(space->size());
-    vcs_solve_opts opts{options.epsilon, 1, 0, 1.0};
+    // page-locked results: the solve streams them to the host behind the layer pass
+    PinnedVector<double> values(space->size());
+    PinnedVector<std::int32_t> actions(space->size());
+    vcs_solve_opts opts{options.epsilon, 1, 0, 1.0, VCS_METHOD_AUTO};
     vcs_solve_report rep{};
-    check(vcs_solve(space->handle(), &opts, values.data(), actions.data(), &rep));
+    const auto devs = worker_devices(space->device(), n_workers);
+    if (devs.size() == 1)
+        check(vcs_solve(space->handle(), &opts, values.data(), actions.data(), &rep));
+    else
+        check(vcs_solve_multi(space->handle(), &opts, static_cast<int32_t>(devs.size()), devs.data(),
+                              VCS_EXCHANGE_HALO, values.data(), actions.data(), &rep));
+    const std::uint64_t gen = vcs_space_result_generation(space->handle());
     ValueTable table(space, std::move(values), rep.sweeps, options.epsilon);
-    Policy policy(std::move(space), std::move(actions));
+    Policy policy(std::move(space), std::move(actions), gen);
     return ViResult{std::move(table), std::move(policy)};
 }
 } // namespace detail
@@ -373,22 +398,40 @@ std::pair<double, MdpAction> bellman_backup(const MdpState& s, const ValueTable&
     return {best, best_action};
 }
 
+// rollout (mdp.cpp:305-324).  The policy walk runs on the device (vcs_rollout: one kernel
+// follows the H decisions through the device key index) when the space still holds this policy's
+// results; a policy whose space has solved again since walks with one device locate per step
+// against its own actions.  The ScheduleResult bookkeeping is the reference's.
 ScheduleResult rollout(const Policy& policy, const MdpInstance& instance) {
     ScheduleResult result;
     for (const auto& c : instance.vcc.clouds) result.per_vc_used[c.id] = 0;
-    MdpState s = initial_state(instance);
-    while (!s.terminal) {
-        const MdpAction a = policy.action_for(s);
-        const auto& task = instance.tasks[static_cast<std::size_t>(s.next_task_index)];
-        if (a.is_paid()) {
+    const StateSpace& space = policy.space();
+    const std::size_t H = instance.tasks.size();
+    std::vector<int32_t> targets;
+    if (policy.generation() == vcs_space_result_generation(space.handle())) {
+        targets.resize(std::max<std::size_t>(H, 1));
+        Soa soa(instance.vcc, instance.tasks, {});
+        check(vcs_rollout(space.handle(), &soa.v, targets.data(), nullptr));
+        targets.resize(H);
+    } else {
+        MdpState s = initial_state(instance);
+        while (!s.terminal) {
+            const MdpAction a = policy.action_for(s);
+            targets.push_back(a.target);
+            s = transition(s, a, instance);
+        }
+    }
+    for (std::size_t t = 0; t < H; ++t) {
+        const auto& task = instance.tasks[t];
+        const int a = targets[t];
+        if (a == kPaidCloud) {
             result.paid_vms += task.vm_demand;
             result.placements.push_back({task.id, kPaidCloud, task.vm_demand});
         } else {
-            const int id = instance.vcc.clouds[static_cast<std::size_t>(a.target)].id;
+            const int id = instance.vcc.clouds[static_cast<std::size_t>(a)].id;
             result.per_vc_used[id] += task.vm_demand;
             result.placements.push_back({task.id, id, task.vm_demand});
         }
-        s = transition(s, a, instance);
     }
     result.unused_vms = total_capacity(instance.vcc) - result.vc_placed_vms();
     return result;

@@ -572,6 +572,8 @@ class Policy:
     def __init__(self, space: StateSpace, actions: np.ndarray):
         self._space = space
         self._actions = actions
+        # the device-resident results these actions came from (vcs_rollout reads those)
+        self._gen = int(N.lib().vcs_space_result_generation(space.handle))
 
     def action_for(self, s: MdpState) -> MdpAction:
         if s.terminal or s.next_task_index >= self._space.task_count():
@@ -678,30 +680,44 @@ class ScheduleResult:
         return sum(self.per_vc_used.values())
 
 
-def rollout(policy: Policy, instance: MdpInstance) -> ScheduleResult:
-    """mdp.cpp:305-324: follow the policy from the initial state.
-
-    Walks the device CSR: the successor under the chosen action is the row's edge carrying
-    that action, so no per-step key lookup is needed after the first."""
-    res = ScheduleResult()
-    for c in instance.vcc.clouds:
-        res.per_vc_used[c.id] = 0
+def _policy_walk(policy: Policy, instance: MdpInstance) -> np.ndarray:
+    """The decisions of rollout on the device: one vcs_rollout kernel walks the H steps through
+    the device key index (when the space's device results are still this policy's), else one
+    device locate per step against the policy's own actions."""
+    space = policy.space()
+    H = len(instance.tasks)
+    if policy._gen == int(N.lib().vcs_space_result_generation(space.handle)):
+        targets = np.empty(max(H, 1), dtype=np.int32)
+        ni = instance.native()
+        N.check(N.lib().vcs_rollout(space.handle, ni.ref, N.ptr(targets, C.c_int32), None))
+        return targets[:H]
     s = initial_state(instance)
     targets = []
     while not s.terminal:
         a = policy.action_for(s)
-        task = instance.tasks[s.next_task_index]
-        if a.is_paid():
+        targets.append(a.target)
+        s = transition(s, a, instance)
+    return np.array(targets, dtype=np.int32)
+
+
+def rollout(policy: Policy, instance: MdpInstance) -> ScheduleResult:
+    """mdp.cpp:305-324: follow the policy from the initial state (the walk runs on the device,
+    ``_policy_walk``); the ScheduleResult bookkeeping is the reference's."""
+    res = ScheduleResult()
+    for c in instance.vcc.clouds:
+        res.per_vc_used[c.id] = 0
+    targets = _policy_walk(policy, instance)
+    for t, a in enumerate(targets):
+        task = instance.tasks[t]
+        if a == kPaidCloud:
             res.paid_vms += task.vm_demand
             res.placements.append(PlacementRecord(task.id, kPaidCloud, task.vm_demand))
         else:
-            cid = instance.vcc.clouds[a.target].id
+            cid = instance.vcc.clouds[int(a)].id
             res.per_vc_used[cid] = res.per_vc_used.get(cid, 0) + task.vm_demand
             res.placements.append(PlacementRecord(task.id, cid, task.vm_demand))
-        targets.append(a.target)
-        s = transition(s, a, instance)
     res.unused_vms = total_capacity(instance.vcc) - res.vc_placed_vms()
-    res.target_index = np.array(targets, dtype=np.int32)
+    res.target_index = np.asarray(targets, dtype=np.int32)
     return res
 
 
