@@ -283,8 +283,15 @@ def run_reference(args):
 
 PARALLELISM = {
     "single": lambda n: "single GPU",
+    "multi": lambda n: f"one state space split across {n} GPUs of rank 0's process "
+                       "(vcs_solve_multi: per-layer key-space ranges, forward-halo peer copies "
+                       "over NVLink, lower bounds max-reduced on the primary; the other ranks "
+                       "only join the barriers)",
     "instances": lambda n: f"{n} independent instances, one per GPU (weak scaling; no data-path "
                            "collective, barrier + max-over-ranks timing)",
+    "cert": lambda n: f"certified pass, one rank per process x{n} (sharded.run_cert_sharded: "
+                      "per-layer key-space ranges, halo windows over NCCL send/recv, one MAX "
+                      "all-reduce of the residual bounds per solve)",
     "wave": lambda n: f"version-band sharded wavefront x{n}: one column per layer over NCCL "
                       "send/recv + one MAX all-reduce per solve",
     "halo": lambda n: f"row-block sharded Jacobi x{n}: forward halo over NCCL + MAX all-reduce "
@@ -315,7 +322,11 @@ def e2e_sharded(args, ni, local, dev, stream, opts, sharding, S, rank):
         t0 = time.perf_counter()
         sp = V.StateSpace.build_native(ni, 10**9, local)
         lo = sp.layer_offsets()
-        if sharding == "wave":
+        if sharding == "cert":  # the gathered result lands on every rank, then rank-local D2H
+            be = SH.CertShardCuda(sp, dev, stream)
+            v, a, K = SH.run_cert_sharded(be, opts, gather=True)
+            vn[:], an[:] = v, a
+        elif sharding == "wave":
             be = SH.WaveBandCuda(sp, dev, stream)
             _, _, K = SH.run_wave_sharded(be, lo, opts, local_out=(vn, an))
         else:
@@ -398,21 +409,31 @@ def greedy_c2(V, N):
     return out
 
 
-def solve_timing(N, space, opts, stream, warmup, steps):
+def enqueue_fn(N, devices=None, exchange=0):
+    """vcs_solve_enqueue, or vcs_solve_multi_enqueue over `devices` (rank r on devices[r])."""
+    if not devices:
+        return lambda space, opts, h: N.lib().vcs_solve_enqueue(space.handle, C.byref(opts), h)
+    dv = np.asarray(devices, dtype=np.int32)
+    return lambda space, opts, h: N.lib().vcs_solve_multi_enqueue(
+        space.handle, C.byref(opts), len(dv), N.ptr(dv, C.c_int32), exchange, h)
+
+
+def solve_timing(N, space, opts, stream, warmup, steps, enqueue=None):
     """Device time of `steps` back-to-back solves on `stream` after `warmup` (CUDA events on the
     launching stream, synchronize on both sides).  Returns (total_ms, report, launches)."""
     import torch
+    enqueue = enqueue or enqueue_fn(N)
     h_stream = C.c_void_p(stream.cuda_stream)
     rep = N.vcs_solve_report()
     for _ in range(max(1, warmup)):
-        N.check(N.lib().vcs_solve_enqueue(space.handle, C.byref(opts), h_stream))
+        N.check(enqueue(space, opts, h_stream))
     N.check(N.lib().vcs_solve_collect(space.handle, None, None, C.byref(rep), h_stream))
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = N.kernel_launches()
     ev0.record(stream)
     for _ in range(steps):
-        N.check(N.lib().vcs_solve_enqueue(space.handle, C.byref(opts), h_stream))
+        N.check(enqueue(space, opts, h_stream))
     ev1.record(stream)
     torch.cuda.synchronize()
     launches = N.kernel_launches() - launches0
@@ -420,7 +441,7 @@ def solve_timing(N, space, opts, stream, warmup, steps):
     return ev0.elapsed_time(ev1), rep, launches
 
 
-def e2e_c_abi(N, text, opts, device, steps, S):
+def e2e_c_abi(N, text, opts, device, steps, S, devices=None, exchange=0):
     """End to end through the C ABI with host buffers, per step: vcs_instance_parse of the
     instance text, vcs_space_build (the instance crosses H2D), vcs_solve into pinned host
     values/actions (the 12 B/state result crosses D2H), vcs_space_free.  Wall clock per step
@@ -442,7 +463,12 @@ def e2e_c_abi(N, text, opts, device, steps, S):
         N.check(N.lib().vcs_space_build(inst, 10**9, device, C.byref(h)))
         tb = time.perf_counter()
         rep = N.vcs_solve_report()
-        N.check(N.lib().vcs_solve(h, C.byref(opts), vp, ap, C.byref(rep)))
+        if devices:
+            dv = np.asarray(devices, dtype=np.int32)
+            N.check(N.lib().vcs_solve_multi(h, C.byref(opts), len(dv), N.ptr(dv, C.c_int32),
+                                            exchange, vp, ap, C.byref(rep)))
+        else:
+            N.check(N.lib().vcs_solve(h, C.byref(opts), vp, ap, C.byref(rep)))
         t1 = time.perf_counter()
         s = inst.contents
         inst_bytes = s.n_clouds * (3 * 4 + 2 * 8) + s.n_tasks * (2 * 4 + 2 * 8)
@@ -551,9 +577,15 @@ def run_b200(args):
     dev = torch.device("cuda", local)
     sharding = args.sharding
     if sharding == "auto":
-        sharding = "instances" if world > 1 else "single"
-    sharded_path = sharding in ("wave", "halo", "allgather")
-    use_dist = world > 1 or sharding != "single"
+        sharding = "multi" if world > 1 or args.ranks > 1 else "single"
+    sharded_path = sharding in ("wave", "halo", "allgather", "cert")
+    multi = sharding == "multi"
+    # multi: rank 0 drives every GPU of the node through vcs_solve_multi (one process owns the
+    # whole state space); --ranks R > WORLD_SIZE puts several ranks on a GPU
+    n_ranks = max(args.ranks, world) if multi else 1
+    devices = [r % max(1, world) for r in range(n_ranks)] if multi else None
+    exchange = N.VCS_EXCHANGE_ALLGATHER if args.exchange == "allgather" else N.VCS_EXCHANGE_HALO
+    use_dist = world > 1 or sharded_path or sharding == "instances"
     if use_dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
@@ -583,7 +615,14 @@ def run_b200(args):
         if world > 1:
             dist.barrier()
         tw0 = time.time()
-        total_ms, rep, launches = solve_timing(N, space, opts, stream, args.warmup, args.steps)
+        if multi and rank != 0:  # the solve runs in rank 0's process on every GPU
+            total_ms, launches = 0.0, 0
+            rep = N.vcs_solve_report()
+            rep.sweeps, rep.method = H + 1, N.VCS_METHOD_CERTIFIED
+        else:
+            total_ms, rep, launches = solve_timing(
+                N, space, opts, stream, args.warmup, args.steps,
+                enqueue_fn(N, devices, exchange) if multi else None)
         if rep.method != opts.method and opts.method != N.VCS_METHOD_AUTO:
             log(f"note: the solve ran method {rep.method}")
         if world > 1:
@@ -607,6 +646,12 @@ def run_b200(args):
 
             def step():
                 return SH.run_wave_sharded(backend, lo, opts, gather=False)[2]
+        elif sharding == "cert":
+            opts.method = N.VCS_METHOD_CERTIFIED
+            backend = SH.CertShardCuda(space, dev, stream, exchange)
+
+            def step():
+                return SH.run_cert_sharded(backend, opts, gather=False)[2]
         else:
             opts.method = N.VCS_METHOD_JACOBI
             backend = SH.CudaBackend(space, dev, stream)
@@ -633,7 +678,11 @@ def run_b200(args):
         total_ms = float(local_ms.item())
         sampler.mark(tw0, tw1)
         n_layer = np.diff(lo.astype(np.int64))
-        if sharding == "wave":
+        if sharding == "cert":
+            backups_done = 2 * int(lo[H])
+            method = N.VCS_METHOD_CERTIFIED
+            model_bytes = alg_bytes_done = 0.0
+        elif sharding == "wave":
             backups_done = int(sum(int(n_layer[t]) * (H - t) for t in range(H)))
             method = N.VCS_METHOD_WAVEFRONT
             model_bytes = alg_bytes_done = 20 * S + 12 * E + 16 * backups_done
@@ -652,8 +701,15 @@ def run_b200(args):
     if args.e2e_steps > 0 and not sharded_path:
         if world > 1:
             dist.barrier()
-        e2e = e2e_c_abi(N, text, opts, local, args.e2e_steps, S)
-        if world > 1:  # slowest rank
+        if multi and rank != 0:
+            e2e = {"ms_per_step": 0.0, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+        else:
+            e2e = e2e_c_abi(N, text, opts, local, args.e2e_steps, S, devices, exchange)
+        if multi and world > 1:
+            t = torch.tensor([e2e["ms_per_step"]], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e["value"] = e2e["ms_per_step"] = float(t.item())
+        elif world > 1:  # slowest rank
             t = torch.tensor([e2e["ms_per_step"]], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e["value"] = e2e["ms_per_step"] = float(t.item())
@@ -666,6 +722,14 @@ def run_b200(args):
     if not sharded_path:
         roofline = roofline_for(N, method, model_bytes, alg_bytes_done, sweep_ms, S, sweeps, E / S)
 
+    multi_info = None
+    if multi and rank == 0:
+        mi = N.vcs_multi_report()
+        if N.lib().vcs_multi_info(space.handle, C.byref(mi)) == 0:
+            multi_info = {"ranks": mi.n_ranks, "devices": devices, "split_layers": mi.split_layers,
+                          "replicated_layers": mi.replicated_layers,
+                          "exchange": args.exchange, "halo_bytes_per_solve": mi.halo_bytes,
+                          "max_rank_share": mi.max_share, "cuda_graph": bool(mi.graph)}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -687,12 +751,13 @@ def run_b200(args):
                   "build_ms": space.info.build_ms, "build_wall_ms": build_wall_ms,
                   "sweep_ms": sweep_ms, "extract_ms": extract_ms},
         "roofline": roofline,
+        "multi_gpu": multi_info,
         "cpu_baseline": None,
         "e2e": e2e,
         "clocks": sampler.summary(),
         "gpu_launches": int(launches),
     }
-    if not sharded_path and not args.no_alt and method == N.VCS_METHOD_CERTIFIED:
+    if not sharded_path and not multi and not args.no_alt and method == N.VCS_METHOD_CERTIFIED:
         line["full_work_methods"] = full_work_methods(space, args, stream)
     if rank == 0 and not args.no_greedy:
         line["greedy"] = greedy_c2(V, N)
@@ -730,11 +795,20 @@ def main():
     ap.add_argument("--no-side", action="store_true", help="skip the C1 / C3 side workloads")
     ap.add_argument("--no-alt", action="store_true",
                     help="skip the full-work (wavefront / Jacobi) side numbers")
-    ap.add_argument("--sharding", choices=["auto", "instances", "wave", "halo", "allgather"],
+    ap.add_argument("--sharding", choices=["auto", "single", "multi", "instances", "cert", "wave",
+                                           "halo", "allgather"],
                     default="auto",
-                    help="auto: single GPU at N=1, independent instances (one per GPU) at N>1; "
-                         "wave / halo / allgather shard ONE instance: version-band wavefront, "
-                         "Jacobi row blocks with a forward halo / a full all-gather of V")
+                    help="auto: single GPU at N=1, multi at N>1 (ONE state space split across "
+                         "the N GPUs by rank 0's process, vcs_solve_multi); instances: one "
+                         "independent instance per GPU (weak scaling); cert / wave / halo / "
+                         "allgather: the one-process-per-GPU drivers of sharded.py (certified "
+                         "pass with NCCL windows, version-band wavefront, Jacobi row blocks with "
+                         "a forward halo / a full all-gather of V)")
+    ap.add_argument("--ranks", type=int, default=1,
+                    help="multi: ranks of the split solve (default WORLD_SIZE; more ranks than "
+                         "GPUs share GPUs round robin, the emulated-rank mode)")
+    ap.add_argument("--exchange", choices=["halo", "allgather"], default="halo",
+                    help="multi: pull only the successor window (halo) or whole layers")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         log("note: the timing rules ask for >= 3 warm-up steps")

@@ -264,6 +264,27 @@ typedef struct vcs_multi_report {
 } vcs_multi_report;
 int vcs_multi_info(const vcs_space* sp, vcs_multi_report* out);
 
+/* The same pass with one rank per PROCESS (torchrun, one GPU each; the caller moves the windows
+ * between processes, e.g. torch.distributed over NCCL — paper_2012_12419_b200/sharded.py
+ * run_cert_sharded).  Every rank holds the whole space:
+ *   begin(opts, world, rank, exchange)   zero this rank's pairs / bounds / outputs (enqueued)
+ *   for t = horizon-1 .. 0:
+ *       layer(t)                          this rank's range of layer t (or all of a replicated one)
+ *       if plan(t).split and t > 0:       rank q sends [max(need_lo_h, lo_q), min(need_hi_h, hi_q))
+ *                                         of pairs(t) (2 doubles per index) to every rank h
+ *   all-reduce(lb, MAX); finish(lb) -> certified
+ *   certified: SUM-all-reduce the int64 view of values and the actions (every element is written
+ *              by exactly one rank, the others hold 0) = vcs_solve's result, sweeps = horizon+1;
+ *   otherwise: run vcs_solve (the fallback) on any rank.
+ * plan(t, q) out[6] = {split, lo_q, hi_q, need_lo_q, need_hi_q, index-space size of layer t}. */
+int vcs_cert_shard_begin(vcs_space* sp, const vcs_solve_opts* opts, int32_t world, int32_t rank,
+                         int32_t exchange, void* stream);
+int vcs_cert_shard_plan(const vcs_space* sp, int32_t t, int32_t q, uint64_t* out);
+int vcs_cert_shard_layer(vcs_space* sp, int32_t t, void* stream);
+int vcs_cert_shard_pairs(const vcs_space* sp, int32_t t, double** pairs);
+int vcs_cert_shard_buffers(const vcs_space* sp, double** lb, double** values, int32_t** actions);
+int vcs_cert_shard_finish(const vcs_space* sp, const double* lb_max, int32_t* certified);
+
 /* Sharded (multi-GPU) building blocks.  One process per GPU; the host runtime owns the value
  * buffers and the collectives (torch.distributed / NCCL over NVLink), these calls only enqueue
  * device work on `stream` (a cudaStream_t; NULL = the space's own stream) and never synchronise

@@ -31,7 +31,9 @@ EXPORTS = (
     "vcs_policy_query", "vcs_rollout", "vcs_space_result_generation", "vcs_space_free",
     "vcs_host_alloc", "vcs_host_free",
     "vcs_solve", "vcs_solve_enqueue", "vcs_solve_collect",
-    "vcs_solve_multi_enqueue", "vcs_solve_multi", "vcs_multi_info", "vcs_shard_plan", "vcs_shard_begin", "vcs_shard_sweep", "vcs_shard_finish",
+    "vcs_solve_multi_enqueue", "vcs_solve_multi", "vcs_multi_info",
+    "vcs_cert_shard_begin", "vcs_cert_shard_plan", "vcs_cert_shard_layer", "vcs_cert_shard_pairs",
+    "vcs_cert_shard_buffers", "vcs_cert_shard_finish", "vcs_shard_plan", "vcs_shard_begin", "vcs_shard_sweep", "vcs_shard_finish",
     "vcs_wave_shard_begin", "vcs_wave_shard_band", "vcs_wave_shard_layer", "vcs_wave_shard_pack",
     "vcs_wave_shard_unpack", "vcs_wave_shard_finish",
     "vcs_greedy", "vcs_greedy_batch", "vcs_greedy_reward",
@@ -186,6 +188,13 @@ _SIGS = {
     "vcs_solve_multi": (C.c_int, [_P, C.POINTER(vcs_solve_opts), C.c_int32, _I32P, C.c_int32,
                                   _F64P, _I32P, C.POINTER(vcs_solve_report)]),
     "vcs_multi_info": (C.c_int, [_P, C.POINTER(vcs_multi_report)]),
+    "vcs_cert_shard_begin": (C.c_int, [_P, C.POINTER(vcs_solve_opts), C.c_int32, C.c_int32,
+                                       C.c_int32, _P]),
+    "vcs_cert_shard_plan": (C.c_int, [_P, C.c_int32, C.c_int32, _U64P]),
+    "vcs_cert_shard_layer": (C.c_int, [_P, C.c_int32, _P]),
+    "vcs_cert_shard_pairs": (C.c_int, [_P, C.c_int32, C.POINTER(_P)]),
+    "vcs_cert_shard_buffers": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]),
+    "vcs_cert_shard_finish": (C.c_int, [_P, _F64P, _I32P]),
     "vcs_shard_plan": (C.c_int, [_U64P, _U64P, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                  _U64P, _U64P, _U64P, _U64P]),
     "vcs_shard_begin": (C.c_int, [_P, _P, _P, _P, C.c_int32, _P]),

@@ -142,6 +142,8 @@ struct CachedGraph {
 
 struct MultiState;               // multi-GPU certified pass (vcs_solve.cu)
 void destroy_multi(MultiState*); // waits for and frees everything it owns
+struct CertShard;                // one rank of its multi-process form (vcs_cert_shard_*)
+void destroy_cert_shard(CertShard*);
 
 } // namespace vcs
 
@@ -218,6 +220,7 @@ struct vcs_space {
 
     int num_sms = 148;
     vcs::MultiState* multi = nullptr; // the multi-GPU solve's per-rank state (vcs_solve_multi)
+    vcs::CertShard* cert_shard = nullptr; // vcs_cert_shard_* state of this process's rank
     uint64_t result_gen = 0;          // bumped whenever result_values / result_actions change
     // one caller at a time per space (the reference's const StateSpace may be shared by threads:
     // the solve, query and rollout entry points serialise on this)

@@ -1753,6 +1753,23 @@ struct MultiState {
     double max_share = 0.0;    // largest rank share of the split work (1/n = balanced)
 };
 
+// One rank of the multi-PROCESS form of the same pass (vcs_cert_shard_*): this process owns one
+// rank's GPU; the caller moves the windows between processes (torch.distributed / NCCL).
+struct CertShard {
+    int world = 1, rank = 0, exchange = 0;
+    bool keyspace = false;
+    uint64_t half = 0;
+    double eps = 1e-6, discount = 1.0;
+    int max_sweeps = 0;
+    std::vector<char> split;
+    std::vector<std::vector<uint64_t>> lo, hi, need_lo, need_hi;
+    double halo_bytes = 0.0;
+    int split_layers = 0, replicated_layers = 0;
+    double max_share = 0.0;
+    DevBuf<double2> xd;
+    DevBuf<double> lb;
+};
+
 namespace {
 
 void* multi_alloc(MultiRank& r, size_t bytes) {
@@ -1785,8 +1802,11 @@ int64_t halo_shift(const vcs_space* sp, int t_consumer) {
     return static_cast<int64_t>(static_cast<uint64_t>(P.demand) * wmax);
 }
 
-void multi_plan(const vcs_space* sp, MultiState& ms) {
-    const int H = sp->H, n = static_cast<int>(ms.ranks.size());
+// The split of every layer between n ranks and the windows their next layers read (fills the
+// plan fields shared by MultiState and CertShard).
+template <class P>
+void multi_plan(const vcs_space* sp, int n, P& ms) {
+    const int H = sp->H;
     uint64_t min_split = 65536;
     if (const char* e = std::getenv("VCS_MULTI_MIN_SPLIT")) min_split = std::strtoull(e, nullptr, 10);
     ms.split.assign(static_cast<size_t>(H), 0);
@@ -1947,7 +1967,7 @@ MultiState& multi_state(vcs_space* sp, const std::vector<int>& devices, int exch
             ms->lb_stage = static_cast<double*>(p);
         }
         VCS_CUDA(cudaEventCreateWithFlags(&ms->ev_fork, cudaEventDisableTiming));
-        multi_plan(sp, *ms);
+        multi_plan(sp, static_cast<int>(ms->ranks.size()), *ms);
     } catch (...) {
         destroy_multi(ms.release());
         VCS_CUDA(cudaSetDevice(sp->device));
@@ -2092,6 +2112,13 @@ void record_multi(vcs_space* sp, MultiState& ms, const GraphKey& key, CachedGrap
 }
 
 } // namespace
+
+void destroy_cert_shard(CertShard* cs) {
+    if (!cs) return;
+    cs->xd.release();
+    cs->lb.release();
+    delete cs;
+}
 
 void destroy_multi(MultiState* ms) {
     if (!ms) return;
@@ -2283,6 +2310,156 @@ int vcs_solve_multi(vcs_space* sp, const vcs_solve_opts* opts, int32_t n_ranks,
     const int rc = vcs_solve_multi_enqueue(sp, opts, n_ranks, devices, exchange, nullptr);
     if (rc != VCS_OK) return rc;
     return vcs_solve_collect(sp, values_out, actions_out, report, nullptr);
+}
+
+// ---- multi-process form: one rank per process (vcs_cert_shard_*) -------------------------------
+
+int vcs_cert_shard_begin(vcs_space* sp, const vcs_solve_opts* opts, int32_t world, int32_t rank,
+                         int32_t exchange, void* stream) {
+    std::lock_guard<std::recursive_mutex> space_lock(sp->mu);
+    return guarded([&] {
+        vcs_solve_opts o{1e-6, 1, 0, 1.0, VCS_METHOD_AUTO};
+        if (opts) o = *opts;
+        if (!(o.epsilon > 0.0))
+            raise(VCS_EINVAL, "epsilon must be > 0 (value iteration would never terminate)");
+        if (world < 1 || rank < 0 || rank >= world) raise(VCS_EINVAL, "bad world/rank");
+        if (exchange != VCS_EXCHANGE_HALO && exchange != VCS_EXCHANGE_ALLGATHER)
+            raise(VCS_EINVAL, "unknown exchange mode");
+        vcs::bind_device(sp->device);
+        const bool ks = vcs::cert_keyspace(sp);
+        if (sp->implicit && !ks)
+            raise(VCS_EINVAL, "the sharded certified pass needs key-space pairs (unset VCS_CERT_BFS)");
+        if (!sp->implicit) vcs::ensure_csr(sp);
+        vcs::ensure_solve_buffers(sp, sp->H + 1);
+        if (!sp->cert_shard) sp->cert_shard = new vcs::CertShard;
+        vcs::CertShard& cs = *sp->cert_shard;
+        cs.world = world;
+        cs.rank = rank;
+        cs.exchange = exchange;
+        cs.keyspace = ks;
+        cs.half = ks ? vcs::cert_half(sp) : 0;
+        cs.eps = o.epsilon;
+        cs.discount = o.discount;
+        cs.max_sweeps = o.max_sweeps;
+        vcs::multi_plan(sp, world, cs);
+        const int H = sp->H;
+        cs.xd.exact(ks ? 2 * cs.half : sp->S, sp->stream);
+        cs.lb.exact(static_cast<size_t>(H) + 2, sp->stream);
+        VCS_CUDA(cudaStreamSynchronize(sp->stream)); // pool allocations ready for any stream
+        const vcs::StreamUse s(sp, stream);
+        // every output element is written by exactly one rank; the others hold zeros, so a
+        // SUM of the ranks' arrays (integer views) assembles the result bit for bit
+        VCS_CUDA(cudaMemsetAsync(sp->v[0].p, 0, sp->S * sizeof(double), s));
+        VCS_CUDA(cudaMemsetAsync(sp->actions_dev.p, 0, sp->S * sizeof(int32_t), s));
+        const uint64_t rH = sp->layer_off[H], nH = sp->S - rH;
+        if (rank == 0) VCS_CUDA(cudaMemsetAsync(sp->actions_dev.p + rH, 0xff, nH * sizeof(int32_t), s));
+        VCS_CUDA(cudaMemsetAsync(cs.lb.p, 0, (H + 2) * sizeof(double), s));
+        if (ks)
+            VCS_CUDA(cudaMemsetAsync(cs.xd.p + (H & 1) * cs.half, 0, sizeof(double2), s));
+        else
+            VCS_CUDA(cudaMemsetAsync(cs.xd.p + rH, 0, nH * sizeof(double2), s));
+        return VCS_OK;
+    });
+}
+
+int vcs_cert_shard_plan(const vcs_space* sp, int32_t t, int32_t q, uint64_t* out) {
+    return guarded([&] {
+        if (!sp->cert_shard) raise(VCS_EINVAL, "vcs_cert_shard_begin first");
+        const vcs::CertShard& cs = *sp->cert_shard;
+        if (t < 0 || t >= sp->H || q < 0 || q >= cs.world) raise(VCS_EINVAL, "layer/rank out of range");
+        const size_t tt = static_cast<size_t>(t), qq = static_cast<size_t>(q);
+        const vcs::CertLayer L = vcs::cert_layer(sp, t, nullptr, cs.half, cs.keyspace);
+        out[0] = cs.split[tt] ? 1 : 0;
+        out[1] = cs.lo[tt][qq];
+        out[2] = cs.hi[tt][qq];
+        out[3] = cs.need_lo[tt][qq];
+        out[4] = cs.need_hi[tt][qq];
+        out[5] = cs.keyspace ? (L.dense_order ? L.dense_n : L.n) : L.n;
+        return VCS_OK;
+    });
+}
+
+int vcs_cert_shard_layer(vcs_space* sp, int32_t t, void* stream) {
+    std::lock_guard<std::recursive_mutex> space_lock(sp->mu);
+    return guarded([&] {
+        if (!sp->cert_shard) raise(VCS_EINVAL, "vcs_cert_shard_begin first");
+        vcs::CertShard& cs = *sp->cert_shard;
+        if (t < 0 || t >= sp->H) raise(VCS_EINVAL, "layer out of range");
+        vcs::bind_device(sp->device);
+        const vcs::StreamUse s(sp, stream);
+        const size_t tt = static_cast<size_t>(t), rr = static_cast<size_t>(cs.rank);
+        const bool split = cs.split[tt] != 0;
+        const uint64_t lo = cs.lo[tt][rr], hi = cs.hi[tt][rr];
+        const int write_out = (split || cs.rank == 0) ? 1 : 0;
+        if (cs.keyspace) {
+            vcs::CertLayer L = vcs::cert_layer(sp, t, cs.xd.p, cs.half, true);
+            if (L.dense_order) {
+                L.d_lo = lo;
+                L.d_hi = hi;
+            }
+            if (L.n && (!L.dense_order || hi > lo))
+                vcs::launch_cert_layer(sp, vcs::cert_data_of(sp), L, sp->v[0].p, sp->actions_dev.p,
+                                       cs.lb.p, cs.discount, write_out, false, s);
+        } else if (hi > lo) {
+            vcs::CertArgs a{};
+            a.row_ptr = sp->row_ptr.p;
+            a.succ = sp->succ.p;
+            a.reward = sp->reward.p;
+            a.action = sp->action.p;
+            a.values_out = sp->v[0].p;
+            a.act_out = sp->actions_dev.p;
+            a.write_out = write_out;
+            a.lb = cs.lb.p;
+            a.discount = cs.discount;
+            a.row0 = sp->layer_off[tt] + lo;
+            a.n = hi - lo;
+            a.next_row0 = sp->layer_off[tt + 1];
+            a.m = sp->H - t;
+            a.xd_next = cs.xd.p + a.next_row0;
+            a.xd_cur = cs.xd.p + a.row0;
+            const unsigned blocks = static_cast<unsigned>(std::max<uint64_t>(
+                1, std::min<uint64_t>((a.n + 255) / 256, static_cast<uint64_t>(4) * sp->num_sms)));
+            if (vcs::is_discounted(cs.discount)) vcs::k_cert_rows<true, 4, 4><<<blocks, 256, 0, s>>>(a);
+            else vcs::k_cert_rows<false, 4, 4><<<blocks, 256, 0, s>>>(a);
+            VCS_LAUNCHED();
+        }
+        return VCS_OK;
+    });
+}
+
+int vcs_cert_shard_pairs(const vcs_space* sp, int32_t t, double** pairs) {
+    return guarded([&] {
+        if (!sp->cert_shard) raise(VCS_EINVAL, "vcs_cert_shard_begin first");
+        const vcs::CertShard& cs = *sp->cert_shard;
+        if (t < 0 || t > sp->H) raise(VCS_EINVAL, "layer out of range");
+        const uint64_t base = cs.keyspace ? (t & 1) * cs.half : sp->layer_off[static_cast<size_t>(t)];
+        *pairs = reinterpret_cast<double*>(cs.xd.p + base);
+        return VCS_OK;
+    });
+}
+
+int vcs_cert_shard_buffers(const vcs_space* sp, double** lb, double** values, int32_t** actions) {
+    return guarded([&] {
+        if (!sp->cert_shard) raise(VCS_EINVAL, "vcs_cert_shard_begin first");
+        if (lb) *lb = sp->cert_shard->lb.p;
+        if (values) *values = sp->v[0].p;
+        if (actions) *actions = sp->actions_dev.p;
+        return VCS_OK;
+    });
+}
+
+int vcs_cert_shard_finish(const vcs_space* sp, const double* lb_max, int32_t* certified) {
+    return guarded([&] {
+        if (!sp->cert_shard) raise(VCS_EINVAL, "vcs_cert_shard_begin first");
+        const vcs::CertShard& cs = *sp->cert_shard;
+        const int H = sp->H;
+        int M = H + 1;
+        if (cs.max_sweeps > 0) M = std::min(M, cs.max_sweeps);
+        bool ok = M >= H + 1;
+        for (int k = 1; k <= H && ok; ++k) ok = lb_max[k] >= cs.eps; // NaN-safe, as k_cert_check
+        *certified = ok ? 1 : 0;
+        return VCS_OK;
+    });
 }
 
 int vcs_multi_info(const vcs_space* sp, vcs_multi_report* out) {

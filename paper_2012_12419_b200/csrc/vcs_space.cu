@@ -1670,6 +1670,7 @@ int sm_count(int device) {
 
 vcs_space::~vcs_space() {
     vcs::destroy_multi(multi);
+    vcs::destroy_cert_shard(cert_shard);
     cudaSetDevice(device);
     for (auto& [st, ev] : use_ev) {
         if (!ev) continue;

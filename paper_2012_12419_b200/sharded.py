@@ -381,3 +381,137 @@ def run_wave_emulated(backends: list, layer_offset: np.ndarray, opts):
         values = (values.view(np.int64) + v.view(np.int64)).view(np.float64)
         actions = actions + a
     return values, actions, K
+
+
+# ==============================================================================================
+# Certified backward pass, one rank per process (vcs_cert_shard_*).
+# Layer t of the pass is split into contiguous ranges of its pair index space (key space or BFS
+# rows); after a split layer every rank receives from each owner the part of the owner's range
+# its own next layer reads (forward halo / whole layer), once per layer.  The residual lower
+# bounds are MAX-reduced once per solve; a failed certificate runs the single-GPU fallback.
+# ==============================================================================================
+
+class CertShardCuda:
+    """Device backend of one rank: vcs_cert_shard_* on a dedicated torch stream."""
+
+    def __init__(self, space, device: torch.device, stream: "torch.cuda.Stream | None" = None,
+                 exchange: int = N.VCS_EXCHANGE_HALO):
+        self.space = space
+        self.device = device
+        self.torch_stream = stream or torch.cuda.Stream(device)
+        self.H = space.task_count()
+        self.S = space.size()
+        self.exchange = exchange
+
+    def _s(self):
+        return C.c_void_p(self.torch_stream.cuda_stream)
+
+    def begin(self, world: int, rank: int, opts):
+        self.opts = opts
+        N.check(N.lib().vcs_cert_shard_begin(self.space.handle, C.byref(opts), world, rank,
+                                             self.exchange, self._s()))
+
+    def plan(self, t: int, q: int) -> tuple:
+        out = np.zeros(6, np.uint64)
+        N.check(N.lib().vcs_cert_shard_plan(self.space.handle, t, q, N.ptr(out, C.c_uint64)))
+        return tuple(int(x) for x in out)
+
+    def layer(self, t: int):
+        N.check(N.lib().vcs_cert_shard_layer(self.space.handle, t, self._s()))
+
+    def _view(self, ptr: int, n: int, dtype) -> torch.Tensor:
+        # a torch view of library-owned device memory (no copy): NCCL moves it in place
+        esz = torch.empty((), dtype=dtype).element_size()
+        return _device_view(ptr, n * esz, self.device).view(dtype)
+
+    def pairs(self, t: int, size: int) -> torch.Tensor:
+        p = C.c_void_p()
+        N.check(N.lib().vcs_cert_shard_pairs(self.space.handle, t, C.byref(p)))
+        return self._view(p.value, 2 * size, torch.float64)
+
+    def buffers(self):
+        lb, v, a = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        N.check(N.lib().vcs_cert_shard_buffers(self.space.handle, C.byref(lb), C.byref(v), C.byref(a)))
+        return (self._view(lb.value, self.H + 2, torch.float64),
+                self._view(v.value, self.S, torch.float64),
+                self._view(a.value, self.S, torch.int32))
+
+    def finish(self, lb: np.ndarray) -> bool:
+        ok = C.c_int32()
+        lb = np.ascontiguousarray(lb, dtype=np.float64)
+        N.check(N.lib().vcs_cert_shard_finish(self.space.handle, N.ptr(lb, C.c_double), C.byref(ok)))
+        return bool(ok.value)
+
+    def fallback(self, opts):
+        """The certificate failed: the single-GPU solve (its own fallback) on this rank."""
+        vals = np.empty(self.S, np.float64)
+        acts = np.empty(self.S, np.int32)
+        rep = N.vcs_solve_report()
+        o = N.vcs_solve_opts(opts.epsilon, opts.skip_converged, opts.max_sweeps, opts.discount,
+                             N.VCS_METHOD_AUTO)
+        N.check(N.lib().vcs_solve(self.space.handle, C.byref(o), N.ptr(vals, C.c_double),
+                                  N.ptr(acts, C.c_int32), C.byref(rep)))
+        return vals, acts, rep.sweeps
+
+
+def _device_view(ptr: int, nbytes: int, device: torch.device) -> torch.Tensor:
+    """A uint8 tensor over `nbytes` of device memory at `ptr` (owned by the library)."""
+    class _Holder:
+        pass
+
+    h = _Holder()
+    h.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                  "version": 3, "strides": None}
+    return torch.as_tensor(h, device=device)
+
+
+def run_cert_sharded(backend, opts, group=None, gather: bool = True):
+    """One rank of the sharded certified pass over torch.distributed (NCCL between GPUs, gloo for
+    CPU backends).  Returns (values, actions, sweeps): the full result on every rank when
+    ``gather``, else (None, None, sweeps).  Bit-identical to vcs_solve for every world size."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    H = backend.H
+    ctx = torch.cuda.stream(backend.torch_stream) if hasattr(backend, "torch_stream") else None
+    if ctx is not None:
+        ctx.__enter__()
+    try:
+        backend.begin(world, rank, opts)
+        for t in range(H - 1, -1, -1):
+            backend.layer(t)
+            if world == 1 or t == 0:
+                continue
+            mine = backend.plan(t, rank)
+            if not mine[0]:
+                continue  # replicated: every rank computed all of layer t
+            plans = [backend.plan(t, q) for q in range(world)]
+            pairs = backend.pairs(t, mine[5])
+            ops = []
+            for q in range(world):
+                if q == rank:
+                    continue
+                x, y = max(plans[q][3], mine[1]), min(plans[q][4], mine[2])  # q reads from me
+                if x < y:
+                    ops.append(dist.P2POp(dist.isend, pairs[2 * x:2 * y], q, group))
+                x, y = max(mine[3], plans[q][1]), min(mine[4], plans[q][2])  # I read from q
+                if x < y:
+                    ops.append(dist.P2POp(dist.irecv, pairs[2 * x:2 * y], q, group))
+            if ops:
+                for req in dist.batch_isend_irecv(ops):
+                    req.wait()
+        lb, values, actions = backend.buffers()
+        dist.all_reduce(lb, op=dist.ReduceOp.MAX, group=group)
+        certified = backend.finish(lb.cpu().numpy() if hasattr(lb, "cpu") else np.asarray(lb))
+        if certified:
+            if gather and world > 1:  # every element has one writer, zeros elsewhere
+                dist.all_reduce(values.view(torch.int64), op=dist.ReduceOp.SUM, group=group)
+                dist.all_reduce(actions, op=dist.ReduceOp.SUM, group=group)
+            K = H + 1
+            out_v = values.cpu().numpy().copy() if gather else None
+            out_a = actions.cpu().numpy().copy() if gather else None
+            return out_v, out_a, K
+    finally:
+        if ctx is not None:
+            ctx.__exit__(None, None, None)
+    vals, acts, K = backend.fallback(opts)
+    return (vals, acts, K) if gather else (None, None, K)
