@@ -562,6 +562,77 @@ def side_workload(V, N, name, eps, stream, local, steps=20):
 METHODS = {1: "jacobi", 2: "layer-wavefront", 3: "certified backward pass"}
 
 
+def run_c5(args):
+    """--workload c5 (BASELINE configs[4]): the density / channel-availability sweep, K clouds x
+    c vehicles per cloud x {static1609, aaa} (bench_workloads.c5_text).  Per point: S, E, sweeps,
+    device time-to-convergence (CUDA events, prebuilt space), build time, e2e through the C ABI
+    (parse + build + solve + D2H) and, for points up to --c5-ref-max states, the unmodified
+    reference (StateSpace::build + detail::run_value_iteration, all host threads) on the same
+    text.  Prints ONE JSON line whose `points` list is the curve."""
+    import torch
+    import paper_2012_12419_b200 as V
+    from paper_2012_12419_b200 import _native as N
+    torch.cuda.set_device(0)
+    stream = torch.cuda.Stream(torch.device("cuda", 0))
+    torch.cuda.set_stream(stream)
+    table = W.channel_table()
+    try:
+        ref = _reference()
+        ref_threads = ref.threads()
+    except Exception as e:  # noqa: BLE001
+        ref, ref_threads = None, 0
+        log(f"reference unavailable: {e}")
+    opts = N.vcs_solve_opts(args.eps, 1, 0, 1.0, N.VCS_METHOD_AUTO)
+    points = []
+    t_start = time.time()
+    for K, c, scheme in W.c5_points():
+        text = W.c5_text(K, c, scheme, table)
+        p = V.parse_instance(text)
+        inst = V.MdpInstance.from_workload(p.vcc, p.bots)
+        space = V.StateSpace.build_native(inst.native(), 10**9, 0, inst)
+        S = space.size()
+        probe_ms, rep, _ = solve_timing(N, space, opts, stream, 2, 3)
+        steps = int(max(5, min(100, 200.0 / max(probe_ms / 3, 1e-3))))
+        total_ms, rep, launches = solve_timing(N, space, opts, stream, 2, steps)
+        ms = total_ms / steps
+        pt = {"K": K, "c": c, "scheme": scheme, "states": S, "transitions": space.edges(),
+              "horizon": space.task_count(), "sweeps": rep.sweeps,
+              "method": METHODS.get(rep.method, str(rep.method)),
+              "time_to_convergence_ms": ms, "steps": steps,
+              "launches_per_solve": launches / steps,
+              "backups_performed_per_s": rep.backups_done / (ms * 1e-3),
+              "backups_reference_equivalent_per_s": S * rep.sweeps / (ms * 1e-3),
+              "build_ms": space.info.build_ms}
+        del space
+        e = e2e_c_abi(N, text, opts, 0, 2, S)
+        pt["e2e_ms"] = e["ms_per_step"]
+        if ref is not None and S <= args.c5_ref_max:
+            ri = ref.parse(text)
+            rsp, times, sweeps = cpu_solve_timing(ref, ri, args.eps, ref_threads, 0.2, 1, 3)
+            assert rsp.S == S and sweeps == rep.sweeps, (K, c, scheme, rsp.S, S)
+            rms = statistics.median(times)
+            pt["reference"] = {"time_to_convergence_ms": rms, "build_ms": rsp.build_ms,
+                               "cores": ref_threads, "speedup_device": rms / ms,
+                               "speedup_e2e": (rms + rsp.build_ms) / e["ms_per_step"]}
+        points.append(pt)
+        log(f"[c5] K={K} c={c} {scheme:10s} S={S:>10} sweeps={rep.sweeps:>3} "
+            f"t={ms:.4f} ms e2e={e['ms_per_step']:.3f} ms"
+            + (f" ref={pt['reference']['time_to_convergence_ms']:.1f} ms" if "reference" in pt else ""))
+    big = max(points, key=lambda q: q["states"])
+    line = {"metric": METRIC, "value": big["time_to_convergence_ms"], "unit": UNIT, "n_gpus": 1,
+            "steps": big["steps"], "warmup": 2, "ms_per_step": big["time_to_convergence_ms"],
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "C5: density / channel-availability sweep (bench_workloads."
+                                   "c5_text), value = the largest point",
+                       "grid": {"K": list(W.C5_CLOUDS), "c": list(W.C5_VMS),
+                                "schemes": list(W.C5_SCHEMES)},
+                       "epsilon": args.eps, "reference_max_states": args.c5_ref_max},
+            "points": points, "wall_s": time.time() - t_start}
+    print(json.dumps(line))
+    return 0
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -764,7 +835,7 @@ def run_b200(args):
     if rank == 0 and world == 1 and not args.no_side:
         line["side_workloads"] = {n: side_workload(V, N, n, args.eps, stream, local)
                                   for n in ("c1", "c3") if n != workload}
-    if world == 1 and not args.no_cpu_baseline and rank == 0:
+    if world == 1 and not args.no_cpu_baseline and rank == 0 and workload != "c7":
         try:
             line["cpu_baseline"] = cpu_baseline(workload, args.eps)
         except Exception as e:  # noqa: BLE001
@@ -782,7 +853,12 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", choices=["c1", "c3", "c4"], default="c4")
+    ap.add_argument("--workload", choices=["c1", "c3", "c4", "c5", "c7"], default="c4",
+                    help="c4: the headline (configs[3]); c1 / c3: configs[0] / [2]; c5: the "
+                         "density / channel sweep (configs[4]); c7: 7 clouds x 8 VMs, the "
+                         "HBM-bound size (pair vectors > L2)")
+    ap.add_argument("--c5-ref-max", type=int, default=2_000_000,
+                    help="c5: time the reference on points up to this many states")
     ap.add_argument("--eps", type=float, default=1e-6)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-skip", action="store_true", help="disable the converged-layer skip")
@@ -814,6 +890,8 @@ def main():
         log("note: the timing rules ask for >= 3 warm-up steps")
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "c5":
+        return run_c5(args)
     return run_b200(args)
 
 

@@ -11,6 +11,8 @@ Pure Python, no product or oracle import (the reference arm must not load libvcs
   c3  5 clouds x 8 VMs, 40 tasks demand U[1,3], seed 2012: S = 1,788,700 (configs[2])
   c4  6 clouds x 8 VMs, 48 tasks demand U[1,3], seed 2012: S = 19,333,781 (configs[3])
   c5  density / channel-availability sweep (configs[4]), see c5_text()
+  c7  7 clouds x 8 VMs, 56 tasks demand U[1,3], seed 2012: the size where the certified pass is
+      bound by HBM rather than L2 (no reference timing: its hash-map build would take minutes)
 """
 from __future__ import annotations
 
@@ -24,12 +26,15 @@ FILES = {
     "c1": ROOT / "tests" / "golden" / "canonical_instance.txt",
     "c3": INSTANCES / "c3.txt",
     "c4": INSTANCES / "c4.txt",
+    "c7": INSTANCES / "c7.txt",
 }
 DESCRIPTIONS = {
     "c1": "C1: canonical instance (reference data/canonical_instance.txt), 11 clouds, 330 unit tasks",
     "c2": "C2: greedy first-fit, 1000 clouds x U[50,150] VMs, 10^5 tasks demand U[1,3] (seed 12345)",
     "c3": "C3: 5 clouds x 8 VMs, 40 tasks demand U[1,3] (mt19937_64 seed 2012), 5 bags",
     "c4": "C4: 6 clouds x 8 VMs, 48 tasks demand U[1,3] (mt19937_64 seed 2012), 6 bags",
+    "c7": "C7: 7 clouds x 8 VMs, 56 tasks demand U[1,3] (mt19937_64 seed 2012), 7 bags "
+          "(HBM-bound: a layer's pair vector is 76 MB, two exceed the 126 MB L2)",
 }
 # C2 through the seeded generator (kind 2 = VCS_GEN_GREEDY): seed, clouds, bags, tasks/bag, demand
 C2_GEN = (2, 12345, 1000, 100, 1000, 3)

@@ -75,6 +75,11 @@ def record(ref: Reference, ni, eps_list=(1e-6,), cap=10**9, with_brute=False):
     return rec
 
 
+# C5 points with reference digests (both channel schemes, small to ~0.8 M states)
+C5_SAMPLES = ((3, 6, "static1609"), (3, 6, "aaa"), (4, 10, "aaa"), (5, 9, "aaa"),
+              (6, 8, "static1609"), (7, 6, "aaa"))
+
+
 def main(argv):
     ref = Reference()
     out = {"generator": "tests/golden/make_golden.py", "reference": "oracle/_ref/libvcsref.so",
@@ -89,6 +94,18 @@ def main(argv):
             recs.append(record(ref, ni, with_brute=brute_ok))
         out["families"][fam] = recs
         print(fam, len(recs), flush=True)
+    if "--c5" in argv:  # add / refresh only the C5 sample points (bench_workloads.c5_text)
+        import bench_workloads as W
+        old = json.loads((HERE / "golden.json").read_text())
+        table = W.channel_table()
+        for K, c, scheme in C5_SAMPLES:
+            p = V.parse_instance(W.c5_text(K, c, scheme, table))
+            ni = V.MdpInstance.from_workload(p.vcc, p.bots).native()
+            old["cases"][f"C5_K{K}_c{c}_{scheme}"] = record(ref, ni)
+            print("C5", K, c, scheme, old["cases"][f"C5_K{K}_c{c}_{scheme}"]["S"], flush=True)
+        (HERE / "golden.json").write_text(json.dumps(old, indent=1, sort_keys=True))
+        print("wrote", HERE / "golden.json")
+        return
     if "--big" in argv:
         for name, args in (("C3", (2012, 0, 5, 8, 40, 3)), ("C4", (2012, 0, 6, 8, 48, 3))):
             ni = V.generate_instance(N.VCS_GEN_HOMOG, *args, as_objects=False)
