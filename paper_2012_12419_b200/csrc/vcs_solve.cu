@@ -994,6 +994,260 @@ __global__ void __launch_bounds__(256, MINB) k_cert_dense(CertImplArgs a) {
                                static_cast<uint64_t>(gridDim.x) * blockDim.x);
 }
 
+// ---- k_cert_dense_tma: the key-space walk with the successor windows staged by TMA -------------
+// On a NON-RETIRING transition (same clouds, same numbering in layers t and t+1) the successor
+// of index d through cloud slot p is d - demand*W_p and the paid successor is d itself, so for a
+// tile of T consecutive indices [d0, d0+T) the successors of every slot form ONE contiguous
+// window of layer t+1's pairs: [d0 - demand*W_p, d0 + T - demand*W_p).  A block owns tiles
+// d0 = d_lo + (blockIdx + k*gridDim)*T; its thread 0 streams the windows of the tile NST ahead
+// into a shared-memory ring with 1-D bulk copies (cp.async.bulk + mbarrier complete_tx), while
+// the 8 warps evaluate the current tile from shared memory.  Windows whose shifts lie within a
+// tile of each other are merged into one span (W = 1, 9, 81 overlap the paid window: C4/C7 move
+// about half the bytes of eight separate windows).  Arithmetic, slot order and the strict first
+// maximum are k_cert_dense's, so the bits are too.
+constexpr int kTmaT = 256;  // indices per tile (= consumer threads per block)
+constexpr int kTmaNst = 3;  // ring stages
+constexpr int kTmaSlots = kDenseSlots; // 7 cloud slots + paid
+constexpr int kTmaThreads = kTmaT + 32; // 8 consumer warps + 1 producer warp
+
+struct TmaSpans {
+    int n;                          // spans per tile
+    int start[kTmaSlots];           // span start relative to d0 (<= 0)
+    int len[kTmaSlots];             // span length in pairs (for a full tile)
+    int off[kTmaSlots];             // span offset in the stage buffer (pairs)
+    int base[kTmaSlots];            // slot e: stage offset of the pair of the tile's index 0
+    uint32_t valid_slots;           // bit e: slot e can be valid in this layer
+};
+
+struct TmaSmem {
+    double2 win[kTmaNst][kTmaSlots * kTmaT];
+    uint32_t rank[kTmaNst][kTmaT + 8]; // the tile's BFS ranks (bulk copies need 16-B alignment)
+    uint64_t full[kTmaNst];  // the stage's bulk copies landed (1 arrival + tx bytes)
+    uint64_t empty[kTmaNst]; // the 8 consumer warps are done with the stage
+    LayerParam L;
+    TmaSpans sp;
+    unsigned long long lb;
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile("{\n\t.reg .pred p;\n"
+                 "WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+                 "r"(parity)
+                 : "memory");
+}
+
+// Warp-specialised: warp 8 (one elected lane) produces — waits until a stage is free, posts the
+// expected bytes and issues the tile's span copies; warps 0-7 consume — each thread evaluates
+// one index of the tile from shared memory, then its warp releases the stage.
+template <bool DISC>
+__global__ void __launch_bounds__(kTmaThreads, 2) k_cert_dense_tma(CertImplArgs a, uint64_t d_next) {
+    extern __shared__ __align__(128) unsigned char tma_raw[];
+    TmaSmem& sm = *reinterpret_cast<TmaSmem*>(tma_raw);
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int NF = kDenseSlots - 1;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < static_cast<int>(sizeof(LayerParam) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t*>(&sm.L)[i] = __ldg(reinterpret_cast<const uint32_t*>(a.L) + i);
+    if (tid == 0) {
+        sm.lb = 0ull;
+        for (int k = 0; k < kTmaNst; ++k) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&sm.full[k])) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&sm.empty[k])),
+                         "r"(kTmaT / 32)
+                         : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const LayerParam& L = sm.L;
+    const int na = L.n_active;
+    const int dem = L.demand;
+    if (tid == kTmaT) { // the layer's windows, merged into spans (by shift, largest first)
+        int shift[kTmaSlots], order[kTmaSlots], ns = 0;
+        uint32_t vs = 1u << (kTmaSlots - 1);
+        for (int e = 0; e < NF; ++e)
+            if (e < na && L.attr[e]) vs |= 1u << e;
+        for (int e = 0; e < kTmaSlots; ++e) {
+            if (!((vs >> e) & 1u)) continue;
+            shift[e] = e == kTmaSlots - 1 ? 0 : dem * static_cast<int>(L.wnext[e]);
+            order[ns++] = e;
+        }
+        for (int i = 1; i < ns; ++i)
+            for (int j = i; j > 0 && shift[order[j]] > shift[order[j - 1]]; --j) {
+                const int x = order[j];
+                order[j] = order[j - 1];
+                order[j - 1] = x;
+            }
+        TmaSpans& P = sm.sp;
+        P.n = 0;
+        P.valid_slots = vs;
+        int off = 0;
+        for (int i = 0; i < ns; ++i) {
+            const int e = order[i];
+            const int st = -shift[e];
+            if (P.n > 0 && st <= P.start[P.n - 1] + P.len[P.n - 1]) { // overlaps the open span
+                const int end = st + kTmaT;
+                const int cur_end = P.start[P.n - 1] + P.len[P.n - 1];
+                if (end > cur_end) {
+                    P.len[P.n - 1] = end - P.start[P.n - 1];
+                    off += end - cur_end;
+                }
+            } else {
+                P.start[P.n] = st;
+                P.len[P.n] = kTmaT;
+                P.off[P.n] = off;
+                off += kTmaT;
+                ++P.n;
+            }
+            P.base[e] = P.off[P.n - 1] + (st - P.start[P.n - 1]);
+        }
+    }
+    __syncthreads();
+    const TmaSpans& P = sm.sp;
+    const uint64_t d_lo = a.d_lo, d_hi = a.d_hi;
+    const uint64_t n_tiles = d_hi > d_lo ? (d_hi - d_lo + kTmaT - 1) / kTmaT : 0;
+    const uint64_t G = gridDim.x;
+    if (tid >= kTmaT) { // ---- producer warp -------------------------------------------------
+        asm volatile("griddepcontrol.wait;" ::: "memory"); // (PDL) the previous layer's pairs
+        if (tid == kTmaT) {
+            int k = 0;
+            for (uint64_t j = blockIdx.x; j < n_tiles; j += G, ++k) {
+                const int st = k % kTmaNst;
+                if (k >= kTmaNst) mbar_wait(&sm.empty[st], static_cast<uint32_t>(k / kTmaNst - 1) & 1u);
+                const int64_t d0 = static_cast<int64_t>(d_lo + j * kTmaT);
+                const uint64_t left = d_hi - (d_lo + j * kTmaT);
+                const int64_t cut = kTmaT - static_cast<int64_t>(left < kTmaT ? left : kTmaT);
+                uint32_t bytes = 0;
+                for (int q = 0; q < P.n; ++q) {
+                    const int64_t s0 = d0 + P.start[q];
+                    const int64_t s1 = s0 + P.len[q] - cut;
+                    const int64_t lo = s0 < 0 ? 0 : s0;
+                    const int64_t hi = s1 > static_cast<int64_t>(d_next) ? static_cast<int64_t>(d_next) : s1;
+                    if (hi > lo) bytes += static_cast<uint32_t>(hi - lo) * 16u;
+                }
+                // the tile's ranks: from the 16-B aligned address at or below rank_self + d0
+                // (the tables of later transitions follow, so rounding up stays in bounds)
+                const uint32_t* rsrc = a.rank_self + d0;
+                const uint32_t pre = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(rsrc) & 15u) >> 2);
+                const uint32_t rcnt = (pre + static_cast<uint32_t>(kTmaT - cut) + 3u) & ~3u;
+                bytes += rcnt * 4u;
+                const uint32_t bar = smem_addr(&sm.full[st]);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                             : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_addr(&sm.rank[st][0])),
+                    "l"(rsrc - pre), "r"(rcnt * 4u), "r"(bar)
+                    : "memory");
+                for (int q = 0; q < P.n; ++q) {
+                    const int64_t s0 = d0 + P.start[q];
+                    const int64_t s1 = s0 + P.len[q] - cut;
+                    const int64_t lo = s0 < 0 ? 0 : s0;
+                    const int64_t hi = s1 > static_cast<int64_t>(d_next) ? static_cast<int64_t>(d_next) : s1;
+                    if (hi <= lo) continue;
+                    const double2* dst = &sm.win[st][P.off[q] + (lo - s0)];
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            smem_addr(dst)),
+                        "l"(a.xd_next + lo), "r"(static_cast<uint32_t>(hi - lo) * 16u), "r"(bar)
+                        : "memory");
+                }
+            }
+        }
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        return;
+    }
+    // ---- consumers: a per-thread odometer over d = d_lo + (blockIdx + k*G)*T + tid ------------
+    const uint64_t first = d_lo + static_cast<uint64_t>(blockIdx.x) * kTmaT + tid;
+    const uint64_t stride = G * kTmaT;
+    uint32_t g[NF], sd[NF], rad[NF];
+    {
+        uint32_t rem = static_cast<uint32_t>(first < d_hi ? first : 0);
+        uint32_t srem = static_cast<uint32_t>(stride);
+#pragma unroll
+        for (int p = 0; p < NF; ++p) {
+            rad[p] = p < na ? L.radix[p] : 1u;
+            g[p] = rem % rad[p];
+            rem /= rad[p];
+            sd[p] = srem % rad[p];
+            srem /= rad[p];
+        }
+    }
+    int base[kTmaSlots];
+#pragma unroll
+    for (int e = 0; e < kTmaSlots; ++e) base[e] = P.base[e] + tid;
+    const uint32_t vs = P.valid_slots;
+    const double r_cloud = L.r_cloud_kept, r_paid = L.r_paid_kept;
+    asm volatile("griddepcontrol.wait;" ::: "memory"); // (this layer's outputs after the wait)
+    double dmax = 0.0;
+    uint64_t d = first;
+    int k = 0;
+    for (uint64_t j = blockIdx.x; j < n_tiles; j += G, ++k, d += stride) {
+        const int st = k % kTmaNst;
+        const uint32_t pre = static_cast<uint32_t>(
+            (reinterpret_cast<uintptr_t>(a.rank_self + (d - tid)) & 15u) >> 2);
+        uint32_t mask = 0;
+#pragma unroll
+        for (int p = 0; p < NF; ++p)
+            if (((vs >> p) & 1u) && g[p] >= static_cast<uint32_t>(dem)) mask |= 1u << p;
+        { // advance the digits by the stride
+            uint32_t carry = 0;
+#pragma unroll
+            for (int p = 0; p < NF; ++p) {
+                const uint32_t v = g[p] + sd[p] + carry;
+                carry = v >= rad[p] ? 1u : 0u;
+                g[p] = carry ? v - rad[p] : v;
+            }
+        }
+        mbar_wait(&sm.full[st], static_cast<uint32_t>(k / kTmaNst) & 1u);
+        const uint32_t r = d < d_hi ? sm.rank[st][pre + tid] : kEmpty32;
+        if (r != kEmpty32) {
+            const double2* w = sm.win[st];
+            double hi = -INFINITY, lo = -INFINITY;
+            int best = -1;
+#pragma unroll
+            for (int e = 0; e < kTmaSlots; ++e) {
+                const bool valid = e == kTmaSlots - 1 || ((mask >> e) & 1u);
+                if (!valid) continue;
+                const double2 x = w[base[e]];
+                const double rw = e == kTmaSlots - 1 ? r_paid : r_cloud;
+                const double qx = DISC ? __dadd_rn(rw, __dmul_rn(a.discount, x.x)) : __dadd_rn(rw, x.x);
+                const double qy = DISC ? __dadd_rn(rw, __dmul_rn(a.discount, x.y)) : __dadd_rn(rw, x.y);
+                if (qy > hi) { // strict: the first maximal edge wins (mdp.cpp:254-260)
+                    hi = qy;
+                    best = e == kTmaSlots - 1 ? -1 : e;
+                }
+                if (qx > lo) lo = qx;
+            }
+            if (a.m == 1) lo = 0.0; // V_0
+            a.xd_cur[d] = make_double2(lo, hi);
+            if (a.write_out) {
+                a.values_out[a.row0 + r] = hi;
+                a.act_out[a.row0 + r] = best < 0 ? -1 : L.cloud[best];
+            }
+            const double dd = fabs(hi - lo);
+            dmax = dmax < dd ? dd : dmax;
+        }
+        __syncwarp();
+        if ((tid & 31) == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&sm.empty[st])) : "memory");
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double other = __shfl_xor_sync(FULL, dmax, o);
+        dmax = dmax < other ? other : dmax;
+    }
+    if ((tid & 31) == 0 && dmax > 0.0)
+        atomicMax(reinterpret_cast<unsigned long long*>(a.lb + a.m),
+                  static_cast<unsigned long long>(__double_as_longlong(dmax)));
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // K* = H+1 is proven iff lb_k >= eps for k = 1..H (and no sweep cap below H+1).  Sets the graph
 // conditional to run the wavefront fallback otherwise.
 __global__ void k_cert_check(const double* __restrict__ lb, int H, double eps, int max_sweeps,
@@ -1290,6 +1544,21 @@ CertLayer cert_layer(const vcs_space* sp, int t, double2* xd, uint64_t half, boo
     return L;
 }
 
+// Layer t's transition keeps every cloud with the same numbering (succ = d - demand*W_p): the
+// TMA-staged kernel applies.
+// (Opt-in, VCS_CERT_TMA=1: measured on the B200 it does not beat k_cert_dense — C4 0.63 vs
+// 0.52 ms, C7 5.6 vs 5.4 ms; its consumers wait on the bulk copies while the scattered
+// value/action stores, 27 % of the C7 time, stay.  DESIGN.md section 3.4.)
+bool cert_tma_ok(const vcs_space* sp, int t) {
+    static const bool on = std::getenv("VCS_CERT_TMA") != nullptr;
+    if (!on || t < 1 || t >= sp->H) return false;
+    const LayerParam& P = sp->plan.layers[static_cast<size_t>(t)];
+    if (P.n_keep != P.n_active || P.dense_size == 0 || P.self_size != P.dense_size) return false;
+    for (int p = 0; p < P.n_active; ++p)
+        if (P.keep_idx[p] != p || P.wnext[p] != P.wself[p]) return false;
+    return P.n_active <= kDenseSlots - 1;
+}
+
 // Launch one certified layer on the implicit form (on the current device's stream `s`).
 void launch_cert_layer(const vcs_space* sp, const CertData& data, const CertLayer& L,
                        double* values_out, int32_t* act_out, double* lb, double discount,
@@ -1319,6 +1588,37 @@ void launch_cert_layer(const vcs_space* sp, const CertData& data, const CertLaye
         c.d_hi = L.d_hi;
     }
     const bool dense_order = L.dense_order;
+    if (dense_order && ks && cert_tma_ok(sp, t)) {
+        // the successor windows staged in shared memory by bulk copies (k_cert_dense_tma)
+        const void* fn = disc ? reinterpret_cast<const void*>(k_cert_dense_tma<true>)
+                              : reinterpret_cast<const void*>(k_cert_dense_tma<false>);
+        int dev = 0;
+        VCS_CUDA(cudaGetDevice(&dev));
+        raise_smem_limit(fn, dev, sizeof(TmaSmem));
+        const uint64_t tiles = L.d_hi > L.d_lo ? (L.d_hi - L.d_lo + kTmaT - 1) / kTmaT : 0;
+        const uint64_t blocks =
+            std::max<uint64_t>(1, std::min<uint64_t>(tiles, static_cast<uint64_t>(2) * sp->num_sms));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+        cfg.blockDim = dim3(kTmaThreads);
+        cfg.dynamicSmemBytes = sizeof(TmaSmem);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl ? 1 : 0;
+        const uint64_t d_next = sp->plan.layers[static_cast<size_t>(t)].dense_size;
+        if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense_tma<true>, c, d_next));
+        else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense_tma<false>, c, d_next));
+        VCS_LAUNCHED();
+        return;
+    }
+    if (trace_enabled())
+        std::fprintf(stderr, "[vcs solve] cert layer %d: n=%llu key space=%llu %s [%llu, %llu)\n", t,
+                     static_cast<unsigned long long>(L.n), static_cast<unsigned long long>(L.dense_n),
+                     dense_order ? "dense" : "sparse", static_cast<unsigned long long>(L.d_lo),
+                     static_cast<unsigned long long>(L.d_hi));
     dispatch_words_solve(max_key_words(sp), [&](auto wm) {
         constexpr int WM = decltype(wm)::value;
         // 3 blocks per SM (80 registers, no spills): C4 0.68 ms vs 0.72 at 4, 0.74 at 2

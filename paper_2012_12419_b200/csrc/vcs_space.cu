@@ -1107,7 +1107,9 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
 // device cannot launch cooperative kernels.  VCS_BUILD_LAYERED forces the multi-kernel path.
 template <int WM, bool EXPLICIT>
 bool build_dense(vcs_space* sp, uint64_t state_cap) {
-    const bool layered = std::getenv("VCS_BUILD_LAYERED") != nullptr; // (read per build: tests)
+    // (read per build: tests.  VCS_BUILD_NO_PERSISTENT takes the layered implicit path.)
+    const bool layered = std::getenv("VCS_BUILD_LAYERED") != nullptr ||
+                         (!EXPLICIT && std::getenv("VCS_BUILD_NO_PERSISTENT") != nullptr);
     const LayerPlan& pl = sp->plan;
     const int H = pl.horizon;
     if (layered || H < 1) return false;
@@ -1273,10 +1275,33 @@ bool build_dense(vcs_space* sp, uint64_t state_cap) {
     return true;
 }
 
+// Rank table of transition t (the implicit form): key-space index of layer t+1 -> layer-local
+// BFS index (the rank of the successor's first edge), empty where no state was reached.
+__global__ void k_rank_table(const uint32_t* __restrict__ first_edge,
+                             const uint32_t* __restrict__ rank, uint32_t n,
+                             uint32_t* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t f = first_edge[i];
+    out[i] = f == kEmpty32 ? kEmpty32 : rank[f];
+}
+
+// The layered build can produce the implicit form too (IMPLICIT: every layer dense, <= 7 active
+// clouds): a layer's CSR lives in scratch only long enough to rank its successors, then the
+// rank table is extracted; only keys + rank tables + params stay resident.  This is the path
+// for spaces the persistent builder declines (more than 8 rounds of states per layer, e.g. C7's
+// 4.8 M-state layers).
+bool implicit_layered_ok(const LayerPlan& pl) {
+    if (pl.horizon < 1) return false;
+    for (const auto& L : pl.layers)
+        if (!L.dense_size || L.n_active > kDenseSlots - 1) return false;
+    return true;
+}
+
 // Per layer: count -> scan -> emit -> insert -> mark -> scan -> finalize -> counters, with the
 // edge-side launches sized by the host-known bound E_t <= n_t * max_degree_t (the kernels read
 // the exact E_t from device memory), and ONE stream synchronisation at the end of the layer.
-template <int WM>
+template <int WM, bool IMPLICIT = false>
 void build_layers(vcs_space* sp, uint64_t state_cap) {
     const double t_setup = trace_enabled() ? host_ms() : 0.0;
     const LayerPlan& pl = sp->plan;
@@ -1310,14 +1335,27 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
         }
     }
     const bool presize = e_bound < 0xffffffffull && s_bound < 0xffffffffull &&
-                         e_bound * 16 + s_bound * 4 + k_bound * 8 <= device_bytes(sp->device) / 8;
+                         (IMPLICIT ? 0 : e_bound * 16 + s_bound * 4) + k_bound * 8 <=
+                             device_bytes(sp->device) / 8;
     sp->keys.reserve(presize ? k_bound : 1u << 20, 0, s);
     VCS_CUDA(cudaMemcpyAsync(sp->keys.p, pl.init_key.data(), pl.words[0] * sizeof(uint64_t),
                              cudaMemcpyHostToDevice, s));
-    sp->row_ptr.reserve(presize ? s_bound + 1 : 1u << 20, 0, s);
-    sp->succ.reserve(presize ? e_bound : 1u << 20, 0, s);
-    sp->reward.reserve(presize ? e_bound : 1u << 20, 0, s);
-    sp->action.reserve(presize ? e_bound : 1u << 20, 0, s);
+    // IMPLICIT: one layer's CSR in scratch (rank_off: per transition, dense_size entries)
+    DevBuf<uint32_t> lay_row_ptr, lay_succ;
+    DevBuf<double> lay_reward;
+    DevBuf<int32_t> lay_action;
+    if (IMPLICIT) {
+        sp->rank_off.assign(static_cast<size_t>(H) + 1, 0);
+        for (int t = 0; t < H; ++t)
+            sp->rank_off[static_cast<size_t>(t) + 1] =
+                sp->rank_off[static_cast<size_t>(t)] + pl.layers[static_cast<size_t>(t)].dense_size;
+        sp->rank_tables.exact(std::max<uint64_t>(sp->rank_off.back(), 1), s);
+    } else {
+        sp->row_ptr.reserve(presize ? s_bound + 1 : 1u << 20, 0, s);
+        sp->succ.reserve(presize ? e_bound : 1u << 20, 0, s);
+        sp->reward.reserve(presize ? e_bound : 1u << 20, 0, s);
+        sp->action.reserve(presize ? e_bound : 1u << 20, 0, s);
+    }
 
     uint64_t S = 1, E = 0, n_t = 1;
     sp->max_layer = 1;
@@ -1348,26 +1386,48 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
         const uint32_t* e_dev = sc.off.p + n_t; // exact E_t on the device
 
         const uint64_t row0 = sp->layer_off[static_cast<size_t>(t)];
-        sp->row_ptr.reserve(row0 + n_t + 1, row0, s);
-        sp->succ.reserve(E + e_ub, E, s);
-        sp->reward.reserve(E + e_ub, E, s);
-        sp->action.reserve(E + e_ub, E, s);
+        // where this layer's CSR goes: the resident arrays, or (IMPLICIT) the layer scratch
+        uint32_t* rp_out;
+        uint32_t* succ_out;
+        double* rw_out;
+        int32_t* act_out;
+        uint32_t ebase;
+        if (IMPLICIT) {
+            lay_row_ptr.exact(n_t + 1, s);
+            lay_succ.exact(e_ub, s);
+            lay_reward.exact(e_ub, s);
+            lay_action.exact(e_ub, s);
+            rp_out = lay_row_ptr.p;
+            succ_out = lay_succ.p;
+            rw_out = lay_reward.p;
+            act_out = lay_action.p;
+            ebase = 0;
+        } else {
+            sp->row_ptr.reserve(row0 + n_t + 1, row0, s);
+            sp->succ.reserve(E + e_ub, E, s);
+            sp->reward.reserve(E + e_ub, E, s);
+            sp->action.reserve(E + e_ub, E, s);
+            rp_out = sp->row_ptr.p + row0;
+            succ_out = sp->succ.p + E;
+            rw_out = sp->reward.p;
+            act_out = sp->action.p;
+            ebase = static_cast<uint32_t>(E);
+        }
         const uint64_t key_next = sp->key_off[static_cast<size_t>(t) + 1];
         sp->keys.reserve(key_next + e_ub * static_cast<uint64_t>(L.next_words), key_next, s);
         const uint64_t cap = pow2_at_least(2 * e_ub);
         // dense successor indices when the next key space is small: a first-edge table of
         // dense_size words instead of a hash table of 2*E_t slots
-        const bool dense = L.dense_size != 0 &&
-                           static_cast<uint64_t>(L.dense_size) * 4 <=
-                               std::max<uint64_t>(16ull << 20, cap * 12);
+        const bool dense = IMPLICIT || (L.dense_size != 0 &&
+                                        static_cast<uint64_t>(L.dense_size) * 4 <=
+                                            std::max<uint64_t>(16ull << 20, cap * 12));
         if (dense) {
             sc.table.exact(L.dense_size, s);
             sc.eidx.exact(e_ub, s);
             VCS_CUDA(cudaMemsetAsync(sc.table.p, 0xff, L.dense_size * sizeof(uint32_t), s));
             k_emit_dense<WM><<<blocks_for(n_t, T), T, 0, s>>>(
-                static_cast<uint32_t>(n_t), sp->keys.p + key_t, sc.off.p, L,
-                static_cast<uint32_t>(E), sp->row_ptr.p + row0, sc.eidx.p, sp->reward.p,
-                sp->action.p, sc.table.p);
+                static_cast<uint32_t>(n_t), sp->keys.p + key_t, sc.off.p, L, ebase, rp_out,
+                sc.eidx.p, rw_out, act_out, sc.table.p);
             VCS_LAUNCHED();
             sc.rank.exact(e_ub + 1, s);
             exclusive_scan(sc,
@@ -1376,9 +1436,15 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
                                FirstEdgeOp{e_dev, sc.table.p, sc.eidx.p}),
                            sc.rank.p, e_ub + 1, s); // rank[E_t] = n_{t+1}
             k_finalize_dense<WM><<<blocks_for(e_ub, T), T, 0, s>>>(
-                e_dev, sc.table.p, sc.eidx.p, sc.rank.p, L, static_cast<uint32_t>(S),
-                sp->succ.p + E, sp->keys.p + key_next);
+                e_dev, sc.table.p, sc.eidx.p, sc.rank.p, L, static_cast<uint32_t>(S), succ_out,
+                sp->keys.p + key_next);
             VCS_LAUNCHED();
+            if (IMPLICIT) {
+                k_rank_table<<<blocks_for(L.dense_size, T), T, 0, s>>>(
+                    sc.table.p, sc.rank.p, L.dense_size,
+                    sp->rank_tables.p + sp->rank_off[static_cast<size_t>(t)]);
+                VCS_LAUNCHED();
+            }
         } else {
             sc.ekeys.exact(e_ub * static_cast<uint64_t>(L.next_words), s);
             k_emit<WM><<<blocks_for(n_t, T), T, 0, s>>>(
@@ -1439,6 +1505,18 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
     sp->layer_off[static_cast<size_t>(H) + 1] = S;
     sp->key_off[static_cast<size_t>(H) + 1] =
         sp->key_off[static_cast<size_t>(H)] + n_t * static_cast<uint64_t>(pl.words[H]);
+    if (IMPLICIT) {
+        sp->params_dev.exact(static_cast<size_t>(H), s); // the implicit-CSR solver reads it
+        VCS_CUDA(cudaMemcpyAsync(sp->params_dev.p, pl.layers.data(), H * sizeof(LayerParam),
+                                 cudaMemcpyHostToDevice, s));
+        VCS_CUDA(cudaStreamSynchronize(s));
+        sp->S = S;
+        sp->E = E;
+        sp->implicit = true;
+        sp->csr_ready = false;
+        if (trace_enabled()) std::fprintf(stderr, "[vcs build] final (implicit) %.3f ms\n", host_ms() - t_last);
+        return;
+    }
     // Terminal layer: no outgoing edges (mdp.cpp:207-209).
     const uint64_t rowH = sp->layer_off[static_cast<size_t>(H)];
     sp->row_ptr.reserve(S + 1, rowH, s);
@@ -1773,7 +1851,12 @@ int vcs_space_build(const vcs_instance* inst, uint64_t state_cap, int device, vc
             constexpr int WM = decltype(wm)::value;
             const bool dense = explicit_now ? vcs::build_dense<WM, true>(sp.get(), state_cap)
                                             : vcs::build_dense<WM, false>(sp.get(), state_cap);
-            if (!dense) vcs::build_layers<WM>(sp.get(), state_cap);
+            if (dense) return;
+            if (!explicit_now && !std::getenv("VCS_BUILD_LAYERED") &&
+                vcs::implicit_layered_ok(sp->plan))
+                vcs::build_layers<WM, true>(sp.get(), state_cap);
+            else
+                vcs::build_layers<WM>(sp.get(), state_cap);
         });
         const auto t1 = std::chrono::steady_clock::now();
         sp->build_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();

@@ -648,3 +648,36 @@ def test_concurrent_pinned_solves(gpu, golden):
     for tag in range(2):
         for vs, as_ in out[tag]:
             assert (vs, as_) == (g["values_sha"], g["actions_sha"])
+
+
+def test_layered_implicit_build_matches_golden(gpu, golden, monkeypatch):
+    """The layered builder's implicit form (the path of spaces too large for the persistent
+    builder, e.g. C7): forced on C3/C4 with VCS_BUILD_NO_PERSISTENT, the certified pass on its
+    keys + rank tables reproduces the reference digests, and the explicit CSR materialised from
+    it later (Jacobi) gives the same bits."""
+    monkeypatch.setenv("VCS_BUILD_NO_PERSISTENT", "1")
+    for name in ("C3", "C4"):
+        p = V.load_instance(str(GOLDEN / "instances" / f"{name.lower()}.txt"))
+        sp = V.StateSpace.build_native(V.NativeInstance(p.vcc, bots=p.bots), 10**9)
+        g = golden["cases"][name]["eps=1e-06"]
+        assert sp.size() == golden["cases"][name]["S"]
+        r = _solve(sp, method=N.VCS_METHOD_CERTIFIED)
+        assert r.values.report.method == N.VCS_METHOD_CERTIFIED
+        assert sha(r.values.raw_values()) == g["values_sha"]
+        assert sha(r.policy.raw_actions()) == g["actions_sha"]
+        if name == "C3":
+            r = _solve(sp, method=N.VCS_METHOD_JACOBI)
+            assert sha(r.values.raw_values()) == g["values_sha"]
+
+
+def test_certified_tma_kernel_matches_golden(gpu, golden, monkeypatch):
+    """The TMA-staged key-space walk (k_cert_dense_tma, VCS_CERT_TMA=1) gives the reference's
+    bits on C3 and C4 (its non-retiring layers; the retiring ones keep k_cert_dense)."""
+    monkeypatch.setenv("VCS_CERT_TMA", "1")
+    for name in ("C3", "C4"):
+        p = V.load_instance(str(GOLDEN / "instances" / f"{name.lower()}.txt"))
+        sp = V.StateSpace.build_native(V.NativeInstance(p.vcc, bots=p.bots), 10**9)
+        g = golden["cases"][name]["eps=1e-06"]
+        r = _solve(sp, method=N.VCS_METHOD_CERTIFIED)
+        assert sha(r.values.raw_values()) == g["values_sha"]
+        assert sha(r.policy.raw_actions()) == g["actions_sha"]
