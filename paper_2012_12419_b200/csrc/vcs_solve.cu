@@ -1550,8 +1550,7 @@ CertLayer cert_layer(const vcs_space* sp, int t, double2* xd, uint64_t half, boo
 // 0.52 ms, C7 5.6 vs 5.4 ms; its consumers wait on the bulk copies while the scattered
 // value/action stores, 27 % of the C7 time, stay.  DESIGN.md section 3.4.)
 bool cert_tma_ok(const vcs_space* sp, int t) {
-    static const bool on = std::getenv("VCS_CERT_TMA") != nullptr;
-    if (!on || t < 1 || t >= sp->H) return false;
+    if (t < 1 || t >= sp->H || !std::getenv("VCS_CERT_TMA")) return false;
     const LayerParam& P = sp->plan.layers[static_cast<size_t>(t)];
     if (P.n_keep != P.n_active || P.dense_size == 0 || P.self_size != P.dense_size) return false;
     for (int p = 0; p < P.n_active; ++p)
