@@ -379,6 +379,30 @@ def full_work_methods(space, args, stream):
     return out
 
 
+def early_stop_solve(N, space, eps):
+    """Side number: a C4 solve whose certificate FAILS (eps = 4: the reference stops at sweep 24
+    of 49, tests/test_gpu_solver.py pins the bits): the certified pass, then the wavefront
+    fallback inside vcs_solve_collect after materialising the explicit CSR.  Wall time of
+    vcs_solve (host arrays), the first call (CSR + version store allocated) and a warm one."""
+    import torch
+    S = space.size()
+    vals = np.empty(S, np.float64)
+    acts = np.empty(S, np.int32)
+    opts = N.vcs_solve_opts(eps, 1, 0, 1.0, N.VCS_METHOD_AUTO)
+    times = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = N.vcs_solve_report()
+        N.check(N.lib().vcs_solve(space.handle, C.byref(opts), N.ptr(vals, C.c_double),
+                                  N.ptr(acts, C.c_int32), C.byref(rep)))
+        times.append((time.perf_counter() - t0) * 1e3)
+    return {"epsilon": eps, "sweeps": rep.sweeps, "method": METHODS.get(rep.method),
+            "fallback_deferred": bool(rep.fallback_deferred), "first_call_ms": times[0],
+            "warm_ms": min(times[1:]), "fallback_device_ms": rep.sweep_ms + rep.extract_ms,
+            "note": "wall time of vcs_solve incl. the 232 MB download to pageable host memory"}
+
+
 def greedy_c2(V, N):
     """BASELINE configs[1] beside the headline: greedy first-fit placement of 10^5 tasks over
     10^3 clouds through the C ABI from host SoA arrays to host placements, next to
@@ -830,6 +854,8 @@ def run_b200(args):
     }
     if not sharded_path and not multi and not args.no_alt and method == N.VCS_METHOD_CERTIFIED:
         line["full_work_methods"] = full_work_methods(space, args, stream)
+        if workload == "c4":
+            line["early_stop"] = early_stop_solve(N, space, 4.0)
     if rank == 0 and not args.no_greedy:
         line["greedy"] = greedy_c2(V, N)
     if rank == 0 and world == 1 and not args.no_side:

@@ -206,7 +206,9 @@ typedef struct vcs_solve_report {
     double alg_bytes_done;     /* same formula over the performed backups */
     int32_t method;            /* the method that ran: VCS_METHOD_JACOBI, _WAVEFRONT, or _CERTIFIED
                                   (the certificate held: one backward pass was the whole solve) */
-    int32_t pad;
+    int32_t fallback_deferred; /* 1: the certificate failed on an implicit-form space and the
+                                  wavefront fallback ran inside vcs_solve_collect (see
+                                  vcs_solve_enqueue); 0 otherwise */
     double model_bytes;        /* minimum HBM bytes of the method that ran: Jacobi = alg_bytes_done
                                   with the u32 row_ptr layout; wavefront = CSR once + every
                                   version written and read once + the extraction pass */
@@ -223,9 +225,16 @@ typedef struct vcs_solve_report {
 int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int32_t* actions_out,
               vcs_solve_report* report);
 /* The same solve split in two for callers that overlap or time it on their own stream
- * (a cudaStream_t; NULL = the space's stream): vcs_solve_enqueue launches the whole solve (one
- * CUDA graph) without synchronising; vcs_solve_collect waits for it, downloads the results of
- * the LAST enqueued solve and fills the report.  vcs_solve = enqueue + collect. */
+ * (a cudaStream_t; NULL = the space's stream): vcs_solve_enqueue launches the solve (one CUDA
+ * graph) without synchronising; vcs_solve_collect waits for it, downloads the results of the
+ * LAST enqueued solve and fills the report.  vcs_solve = enqueue + collect.
+ * What enqueue launches: Jacobi / wavefront: the whole solve.  Certified pass on an explicit
+ * CSR: the pass plus, as a graph IF node, the wavefront fallback (the whole solve).  Certified
+ * pass on the IMPLICIT form (the default for dense spaces) and the multi-GPU pass: the pass and
+ * its certificate only; when the certificate fails (an early stop is possible, or a sweep cap
+ * below horizon+1), collect materialises the explicit CSR and runs the wavefront before it
+ * returns, and sets report->fallback_deferred = 1.  Timing enqueue alone is therefore exact
+ * only when the report says method == VCS_METHOD_CERTIFIED. */
 int vcs_solve_enqueue(vcs_space* sp, const vcs_solve_opts* opts, void* stream);
 int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
                       vcs_solve_report* report, void* stream);

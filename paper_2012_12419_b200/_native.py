@@ -129,7 +129,7 @@ class vcs_solve_report(C.Structure):
         ("alg_bytes", C.c_double),
         ("alg_bytes_done", C.c_double),
         ("method", C.c_int32),
-        ("pad", C.c_int32),
+        ("fallback_deferred", C.c_int32),
         ("model_bytes", C.c_double),
     ]
 

@@ -738,6 +738,65 @@ __global__ void __launch_bounds__(256, MINB) k_cert_rows(CertArgs a) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); // the next layer may launch
 }
 
+// The whole certified pass of a SMALL explicit space (every layer <= kCertSmallStates states) in
+// ONE block: the (V_{m-1}, V_m) pairs of two adjacent layers stay in shared memory, a layer is a
+// block barrier instead of a kernel launch (the canonical instance: 330 layers of <= 614 states).
+// Per state exactly k_cert_rows' operations (same edge order, same strict first maximum).
+constexpr int kCertSmallStates = 1280; // 2 x 20 KB of pairs (static shared memory)
+constexpr int kCertSmallThreads = 1024;
+
+template <bool DISC>
+__global__ void __launch_bounds__(kCertSmallThreads, 1)
+k_cert_small(CertArgs a, const uint64_t* __restrict__ layer_off, int H) {
+    __shared__ double2 xd[2][kCertSmallStates];
+    __shared__ unsigned long long s_lb;
+    const int tid = threadIdx.x;
+    {
+        const uint64_t rH = layer_off[H], nH = layer_off[H + 1] - rH;
+        for (uint64_t i = tid; i < nH; i += blockDim.x) xd[H & 1][i] = make_double2(0.0, 0.0);
+    }
+    for (int t = H - 1; t >= 0; --t) {
+        if (tid == 0) s_lb = 0ull;
+        __syncthreads(); // layer t+1's pairs are complete
+        const uint64_t row0 = layer_off[t], n = layer_off[t + 1] - row0, next0 = layer_off[t + 1];
+        const double2* nxt = xd[(t + 1) & 1];
+        double2* cur = xd[t & 1];
+        const int m = H - t;
+        double dmax = 0.0;
+        for (uint64_t i = tid; i < n; i += blockDim.x) {
+            const uint32_t eb = __ldg(a.row_ptr + row0 + i), ee = __ldg(a.row_ptr + row0 + i + 1);
+            double hi = -INFINITY, lo = -INFINITY;
+            uint32_t best_e = 0xffffffffu;
+            for (uint32_t e = eb; e < ee; ++e) {
+                const double rw = __ldg(a.reward + e);
+                const double2 x = nxt[__ldg(a.succ + e) - next0];
+                const double qx = DISC ? __dadd_rn(rw, __dmul_rn(a.discount, x.x)) : __dadd_rn(rw, x.x);
+                const double qy = DISC ? __dadd_rn(rw, __dmul_rn(a.discount, x.y)) : __dadd_rn(rw, x.y);
+                if (qy > hi) { // strict: the first maximal edge wins (mdp.cpp:254-260)
+                    hi = qy;
+                    best_e = e;
+                }
+                if (qx > lo) lo = qx;
+            }
+            if (m == 1) lo = 0.0; // V_0
+            cur[i] = make_double2(lo, hi);
+            a.values_out[row0 + i] = hi;
+            a.act_out[row0 + i] = best_e != 0xffffffffu ? __ldg(a.action + best_e) : -1;
+            const double d = fabs(hi - lo);
+            dmax = dmax < d ? d : dmax;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double other = __shfl_xor_sync(0xffffffffu, dmax, o);
+            dmax = dmax < other ? other : dmax;
+        }
+        if ((tid & 31) == 0 && dmax > 0.0)
+            atomicMax(&s_lb, static_cast<unsigned long long>(__double_as_longlong(dmax)));
+        __syncthreads();
+        if (tid == 0 && s_lb) a.lb[m] = __longlong_as_double(static_cast<long long>(s_lb));
+    }
+}
+
 // Certified layer on the implicit-CSR form of a dense space: a state's edges are
 // its valid slots (clouds in key order, paid last = the reference's edge order), the successor
 // of slot e is rank_t[idx_e], the reward is the layer's kept constant or the retirement formula
@@ -1725,7 +1784,16 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
     a.discount = key.discount;
     a.write_out = 1;
     int launches = 0;
-    for (int t = H - 1; t >= 0; --t) {
+    if (sp->max_layer <= static_cast<uint64_t>(kCertSmallStates) && !std::getenv("VCS_NO_SMALL_SOLVE")) {
+        // a small space: the whole pass in one block (layer pairs in shared memory)
+        if (sp->layer_off_dev.n < static_cast<size_t>(H) + 2) // (ensure_wave_buffers sets it)
+            raise(VCS_EINVAL, "layer offsets were not uploaded before the capture");
+        if (disc) k_cert_small<true><<<1, kCertSmallThreads, 0, s>>>(a, sp->layer_off_dev.p, H);
+        else k_cert_small<false><<<1, kCertSmallThreads, 0, s>>>(a, sp->layer_off_dev.p, H);
+        VCS_LAUNCHED();
+        launches = 1;
+    }
+    for (int t = launches ? -1 : H - 1; t >= 0; --t) {
         a.row0 = sp->layer_off[t];
         a.n = sp->layer_off[t + 1] - sp->layer_off[t];
         a.next_row0 = sp->layer_off[t + 1];
@@ -2990,7 +3058,7 @@ int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int
     // is allocated before the solve is enqueued so the download stream, which waits on the
     // solve's layer events, is ordered after the allocation
     const bool narrow = pinned_out && actions_out && sp->has_plan && sp->plan.n_clouds <= 127 &&
-                        !std::getenv("VCS_NO_NARROW");
+                        sp->S * 12 >= (32ull << 20) && !std::getenv("VCS_NO_NARROW");
     if (narrow) {
         const int rca = guarded([&] {
             vcs::bind_device(sp->device);
@@ -2999,7 +3067,10 @@ int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int
         });
         if (rca != VCS_OK) return rca;
     }
-    const int rc = enqueue_impl(sp, opts, nullptr, pinned_out ? 1 : 0);
+    // streaming the result behind per-layer events pays for large results only: a small one
+    // (< 32 MB) goes in one copy after the PDL-chained pass (canonical: 331 layers, 0.8 MB)
+    const bool stream_out = pinned_out && sp->S * 12 >= (32ull << 20);
+    const int rc = enqueue_impl(sp, opts, nullptr, stream_out ? 1 : 0);
     if (rc != VCS_OK) return rc;
     const vcs::CachedGraph& g = *sp->last_graph;
     const bool overlap = g.method != vcs::kMethodJacobi && !g.layer_ev.empty() && pinned_out;
@@ -3112,7 +3183,8 @@ int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
         vcs::SolveCtrl ctrl{};
         VCS_CUDA(cudaMemcpyAsync(&ctrl, sp->ctrl.p, sizeof ctrl, cudaMemcpyDeviceToHost, s));
         VCS_CUDA(cudaStreamSynchronize(s));
-        if (sp->last_graph->fallback_at_collect && !ctrl.certified) {
+        const bool deferred = sp->last_graph->fallback_at_collect && !ctrl.certified;
+        if (deferred) {
             // the proof failed (an early stop is possible): the layer wavefront on the explicit
             // CSR, materialised now, gives the reference's result
             if (std::getenv("VCS_PROFILE_NO_FALLBACK"))
@@ -3201,6 +3273,7 @@ int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
             report->method = g.method == vcs::kMethodCertified && !ctrl.certified
                                  ? vcs::kMethodWavefront // the proof failed: the wavefront ran
                                  : g.method;
+            report->fallback_deferred = deferred ? 1 : 0;
             report->alg_bytes = (24.0 + 12.0 * dbar) * static_cast<double>(report->backups_ref);
             report->alg_bytes_done = (24.0 + 12.0 * dbar) * static_cast<double>(done);
         }

@@ -1275,6 +1275,234 @@ bool build_dense(vcs_space* sp, uint64_t state_cap) {
     return true;
 }
 
+// ---- single-CTA builder for small spaces (every layer <= kSmallStates / WM states) ---------------
+// The whole layered BFS of mdp.cpp:81-214 in ONE block and ONE launch: the frontier keys, the
+// layer's successor keys and the first-occurrence hash table live in shared memory, so a layer
+// costs a handful of block barriers instead of a host round trip (the canonical instance: 330
+// layers of at most 614 states).  Same edge order (clouds by key position, paid last), same
+// first-insertion numbering (the lowest edge index of a successor ranks it), same reward
+// operations — the CSR it writes is bit-identical to the layered builder's.  A layer larger than
+// the shared-memory tables aborts with status 3 and the host takes the layered path.
+constexpr int kSmallThreads = 1024;
+constexpr int kSmallStates = 1024; // per layer, divided by the key words
+constexpr int kSmallEdges = 4096;  // per layer, divided by the key words
+
+struct SmallBuild {
+    const LayerParam* params; // H
+    uint64_t* keys;           // all layers' packed keys (the layer-0 key is preset)
+    uint32_t* row_ptr;
+    uint32_t* succ;
+    double* reward;
+    int32_t* action;
+    uint64_t* info;           // out: n_t for t = 0..H, then E_t for t = 0..H-1
+    int32_t* status;          // out: 0 ok, 1 state cap, 2 > 2^32-1, 3 a layer overflowed
+    uint64_t state_cap;
+    uint64_t edge_cap;        // room in succ / reward / action
+    uint64_t state_room;      // room in row_ptr / keys (states)
+    int H;
+};
+
+// exclusive scan of v over the block (every thread passes its value; returns its prefix; *total
+// = the sum).  Uses `warp_sums` (32 entries) and two barriers.
+__device__ __forceinline__ uint32_t block_exscan(uint32_t v, uint32_t* warp_sums, uint32_t* total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t s = lane < static_cast<int>(blockDim.x >> 5) ? warp_sums[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        warp_sums[lane] = s; // inclusive
+    }
+    __syncthreads();
+    const uint32_t before = w > 0 ? warp_sums[w - 1] : 0u;
+    *total = warp_sums[(blockDim.x >> 5) - 1];
+    __syncthreads(); // (the next scan may overwrite warp_sums)
+    return before + x - v;
+}
+
+template <int WM>
+__global__ void __launch_bounds__(kSmallThreads, 1) k_build_small(SmallBuild A) {
+    constexpr int NS = kSmallStates / WM;
+    constexpr int NE = kSmallEdges / WM;
+    constexpr int TC = 2 * NE; // table slots (power of two)
+    constexpr int RS = (NS + kSmallThreads - 1) / kSmallThreads; // states per thread
+    constexpr int RE = (NE + kSmallThreads - 1) / kSmallThreads; // edges per thread
+    extern __shared__ __align__(16) unsigned char small_raw[];
+    uint64_t* front = reinterpret_cast<uint64_t*>(small_raw);            // NS * WM
+    uint64_t* ekey = front + static_cast<size_t>(NS) * WM;               // NE * WM
+    uint32_t* table = reinterpret_cast<uint32_t*>(ekey + static_cast<size_t>(NE) * WM); // TC
+    uint32_t* trank = table + TC;                                        // TC
+    uint32_t* slot_of = trank + TC;                                      // NE
+    __shared__ uint32_t warp_sums[32];
+    __shared__ LayerParam Lbuf[2]; // layer t's parameters, and t+1's loaded behind it
+    const int tid = threadIdx.x;
+    constexpr int PW = static_cast<int>(sizeof(LayerParam) / 4);
+    static_assert(PW <= kSmallThreads, "one word of the layer parameters per thread");
+    for (int i = tid; i < PW; i += blockDim.x)
+        reinterpret_cast<uint32_t*>(&Lbuf[0])[i] = reinterpret_cast<const uint32_t*>(A.params)[i];
+    for (int i = tid; i < TC; i += blockDim.x) table[i] = kEmpty32;
+    for (int w = tid; w < WM; w += blockDim.x) front[w] = A.keys[w];
+    uint64_t S = 1, E = 0, key_base = 0; // states / edges before the current layer, its key offset
+    uint32_t n = 1;
+    if (tid == 0) A.info[0] = 1;
+    for (int t = 0; t < A.H; ++t) {
+        __syncthreads(); // (the previous layer's frontier / table / parameters are complete)
+        const LayerParam& L = Lbuf[t & 1];
+        uint32_t pf = 0; // the next layer's parameters: loaded now, stored at the layer's end
+        if (t + 1 < A.H && tid < PW) pf = __ldg(reinterpret_cast<const uint32_t*>(A.params + t + 1) + tid);
+        const int words = L.words, nw = L.next_words;
+        // 1. out-degrees and row offsets (a thread owns states tid, tid + 1024, ...)
+        uint32_t deg[RS], cnt = 0;
+#pragma unroll
+        for (int r = 0; r < RS; ++r) {
+            const uint32_t i = tid + r * kSmallThreads;
+            deg[r] = 0;
+            if (i < n) {
+                uint64_t k[WM];
+                load_key<WM>(front + static_cast<size_t>(i) * WM, words, k);
+                uint32_t d = 1;
+                for (int p = 0; p < L.n_active; ++p)
+                    if (L.attr[p] && get_field<WM>(k, L.bit_off[p], L.width[p]) >= L.demand) ++d;
+                deg[r] = d;
+            }
+            cnt += deg[r];
+        }
+        // edges are numbered state-major: thread blocks of states are interleaved, so scan per
+        // round (round r's states precede round r+1's)
+        uint32_t off[RS], E_t = 0;
+#pragma unroll
+        for (int r = 0; r < RS; ++r) {
+            uint32_t tot = 0;
+            off[r] = E_t + block_exscan(deg[r], warp_sums, &tot);
+            E_t += tot;
+        }
+        if (E_t > static_cast<uint32_t>(NE) || E + E_t > A.edge_cap) {
+            if (tid == 0) *A.status = 3;
+            return;
+        }
+        // 2. emit: successor keys to shared memory, rewards / actions / row offsets to HBM
+#pragma unroll
+        for (int r = 0; r < RS; ++r) {
+            const uint32_t i = tid + r * kSmallThreads;
+            if (i >= n) continue;
+            uint64_t k[WM];
+            load_key<WM>(front + static_cast<size_t>(i) * WM, words, k);
+            uint32_t j = off[r];
+            A.row_ptr[S - n + i] = static_cast<uint32_t>(E + j);
+            for (int p = 0; p < L.n_active; ++p) {
+                if (!L.attr[p] || get_field<WM>(k, L.bit_off[p], L.width[p]) < L.demand) continue;
+                emit_edge<WM>(k, p, L, ekey + static_cast<size_t>(j) * WM, A.reward + E + j,
+                              A.action + E + j);
+                ++j;
+            }
+            emit_edge<WM>(k, -1, L, ekey + static_cast<size_t>(j) * WM, A.reward + E + j,
+                          A.action + E + j);
+        }
+        __syncthreads();
+        // 3. first-occurrence table: the lowest edge index of every successor key
+#pragma unroll
+        for (int r = 0; r < RE; ++r) {
+            const uint32_t j = tid + r * kSmallThreads;
+            if (j >= E_t) continue;
+            uint64_t k[WM];
+            load_key<WM>(ekey + static_cast<size_t>(j) * WM, nw, k);
+            uint32_t h = static_cast<uint32_t>(hash_key<WM>(k, nw, 0)) & (TC - 1);
+            for (;;) {
+                uint32_t cur = table[h];
+                if (cur == kEmpty32) {
+                    const uint32_t prev = atomicCAS(&table[h], kEmpty32, j);
+                    if (prev == kEmpty32) break;
+                    cur = prev;
+                }
+                if (key_equal<WM>(ekey + static_cast<size_t>(cur) * WM, nw, k)) {
+                    if (cur > j) atomicMin(&table[h], j);
+                    break;
+                }
+                h = (h + 1) & (TC - 1);
+            }
+            slot_of[j] = h;
+        }
+        __syncthreads();
+        // 4. ranks of the first occurrences in edge order = the reference's insertion order
+        //    (a thread owns edges tid*RE .. tid*RE + RE - 1: contiguous, so one scan orders them)
+        uint32_t firsts = 0;
+        bool is_first[RE];
+#pragma unroll
+        for (int r = 0; r < RE; ++r) {
+            const uint32_t j = tid * RE + r;
+            is_first[r] = j < E_t && table[slot_of[j]] == j;
+            firsts += is_first[r] ? 1u : 0u;
+        }
+        uint32_t n_next = 0;
+        uint32_t rk = block_exscan(firsts, warp_sums, &n_next);
+        if (S + n_next > A.state_cap || S + n_next > A.state_room) {
+            if (tid == 0) *A.status = S + n_next > A.state_cap ? 1 : 3;
+            return;
+        }
+        if (n_next > static_cast<uint32_t>(NS)) {
+            if (tid == 0) *A.status = 3;
+            return;
+        }
+        const uint64_t next_key_base = key_base + static_cast<uint64_t>(n) * words;
+#pragma unroll
+        for (int r = 0; r < RE; ++r) {
+            const uint32_t j = tid * RE + r;
+            if (!is_first[r]) continue;
+            trank[slot_of[j]] = rk;
+            ++rk;
+        }
+        __syncthreads();
+        // 5. successor ids; first occurrences write the next frontier (shared + HBM)
+#pragma unroll
+        for (int r = 0; r < RE; ++r) {
+            const uint32_t j = tid + r * kSmallThreads;
+            if (j >= E_t) continue;
+            const uint32_t q = trank[slot_of[j]];
+            A.succ[E + j] = static_cast<uint32_t>(S + q);
+            if (table[slot_of[j]] == j) {
+                for (int w = 0; w < nw; ++w) A.keys[next_key_base + static_cast<uint64_t>(q) * nw + w] =
+                    ekey[static_cast<size_t>(j) * WM + w];
+            }
+        }
+        __syncthreads();
+        // the next frontier and a clean table
+#pragma unroll
+        for (int r = 0; r < RE; ++r) {
+            const uint32_t j = tid + r * kSmallThreads;
+            if (j >= E_t) continue;
+            if (table[slot_of[j]] == j) {
+                const uint32_t q = trank[slot_of[j]];
+                for (int w = 0; w < WM; ++w)
+                    front[static_cast<size_t>(q) * WM + w] = w < nw ? ekey[static_cast<size_t>(j) * WM + w] : 0ull;
+            }
+        }
+        __syncthreads();
+        for (int i = tid; i < TC; i += blockDim.x) table[i] = kEmpty32;
+        if (t + 1 < A.H && tid < PW) reinterpret_cast<uint32_t*>(&Lbuf[(t + 1) & 1])[tid] = pf;
+        if (tid == 0) {
+            A.info[t + 1] = n_next;
+            A.info[A.H + 1 + t] = E_t;
+        }
+        E += E_t;
+        S += n_next;
+        key_base = next_key_base;
+        n = n_next;
+    }
+    // the terminal layer's rows have no edges (mdp.cpp:207-209)
+    for (uint32_t i = tid; i <= n; i += blockDim.x) A.row_ptr[S - n + i] = static_cast<uint32_t>(E);
+    if (tid == 0) *A.status = 0;
+}
+
 // Rank table of transition t (the implicit form): key-space index of layer t+1 -> layer-local
 // BFS index (the rank of the successor's first edge), empty where no state was reached.
 __global__ void k_rank_table(const uint32_t* __restrict__ first_edge,
@@ -1284,6 +1512,99 @@ __global__ void k_rank_table(const uint32_t* __restrict__ first_edge,
     if (i >= n) return;
     const uint32_t f = first_edge[i];
     out[i] = f == kEmpty32 ? kEmpty32 : rank[f];
+}
+
+void raise_smem_limit_space(const void* fn, int device, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> set;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& cur = set[{fn, device}];
+    if (smem <= cur) return;
+    VCS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    cur = smem;
+}
+
+// Host side of k_build_small: returns false (nothing kept) when the space is not small.
+template <int WM>
+bool build_small(vcs_space* sp, uint64_t state_cap) {
+    const LayerPlan& pl = sp->plan;
+    const int H = pl.horizon;
+    if (H < 1 || H > 4096 || std::getenv("VCS_BUILD_LAYERED") || std::getenv("VCS_NO_SMALL_BUILD"))
+        return false;
+    constexpr int NS = kSmallStates / WM, NE = kSmallEdges / WM, TC = 2 * NE;
+    const size_t smem = static_cast<size_t>(NS) * WM * 8 + static_cast<size_t>(NE) * WM * 8 +
+                        static_cast<size_t>(TC) * 8 + static_cast<size_t>(NE) * 4;
+    const uint64_t state_room = std::min<uint64_t>(static_cast<uint64_t>(H) * NS + 1, state_cap + NS);
+    const uint64_t edge_room = static_cast<uint64_t>(H) * NE;
+    if (edge_room >= 0xffffffffull || state_room >= 0xffffffffull) return false;
+    cudaStream_t s = sp->stream;
+    const void* fn = reinterpret_cast<const void*>(k_build_small<WM>);
+    raise_smem_limit_space(fn, sp->device, smem);
+    sp->keys.reserve(state_room * WM, 0, s);
+    sp->row_ptr.reserve(state_room + 1, 0, s);
+    sp->succ.reserve(edge_room, 0, s);
+    sp->reward.reserve(edge_room, 0, s);
+    sp->action.reserve(edge_room, 0, s);
+    DevBuf<LayerParam> params;
+    DevBuf<uint64_t> info;
+    DevBuf<int32_t> status;
+    params.exact(static_cast<size_t>(H), s);
+    info.exact(2 * static_cast<size_t>(H) + 2, s);
+    status.exact(1, s);
+    VCS_CUDA(cudaMemcpyAsync(params.p, pl.layers.data(), H * sizeof(LayerParam),
+                             cudaMemcpyHostToDevice, s));
+    VCS_CUDA(cudaMemcpyAsync(sp->keys.p, pl.init_key.data(), pl.words[0] * sizeof(uint64_t),
+                             cudaMemcpyHostToDevice, s));
+    VCS_CUDA(cudaMemsetAsync(status.p, 0xff, sizeof(int32_t), s));
+    SmallBuild A{};
+    A.params = params.p;
+    A.keys = sp->keys.p;
+    A.row_ptr = sp->row_ptr.p;
+    A.succ = sp->succ.p;
+    A.reward = sp->reward.p;
+    A.action = sp->action.p;
+    A.info = info.p;
+    A.status = status.p;
+    A.state_cap = state_cap;
+    A.edge_cap = edge_room;
+    A.state_room = state_room;
+    A.H = H;
+    k_build_small<WM><<<1, kSmallThreads, smem, s>>>(A);
+    VCS_LAUNCHED();
+    std::vector<uint64_t> hinfo(2 * static_cast<size_t>(H) + 2);
+    int32_t hstatus = -1;
+    VCS_CUDA(cudaMemcpyAsync(hinfo.data(), info.p, hinfo.size() * sizeof(uint64_t),
+                             cudaMemcpyDeviceToHost, s));
+    VCS_CUDA(cudaMemcpyAsync(&hstatus, status.p, sizeof hstatus, cudaMemcpyDeviceToHost, s));
+    VCS_CUDA(cudaStreamSynchronize(s));
+    if (hstatus == 1)
+        raise(VCS_ECAP, "reachable state space exceeds cap of " + std::to_string(state_cap) +
+                            " states");
+    if (hstatus != 0) return false; // a layer outgrew the shared-memory tables
+    sp->layer_off.assign(static_cast<size_t>(H) + 2, 0);
+    sp->layer_edges.assign(static_cast<size_t>(H) + 1, 0);
+    sp->key_off.assign(static_cast<size_t>(H) + 2, 0);
+    sp->max_layer = 0;
+    uint64_t S = 0, E = 0;
+    for (int t = 0; t <= H; ++t) {
+        const uint64_t n = hinfo[static_cast<size_t>(t)];
+        sp->layer_off[static_cast<size_t>(t)] = S;
+        sp->key_off[static_cast<size_t>(t) + 1] =
+            sp->key_off[static_cast<size_t>(t)] + n * static_cast<uint64_t>(pl.words[static_cast<size_t>(t)]);
+        S += n;
+        sp->max_layer = std::max(sp->max_layer, n);
+        if (t < H) {
+            sp->layer_edges[static_cast<size_t>(t)] = hinfo[static_cast<size_t>(H) + 1 + t];
+            E += sp->layer_edges[static_cast<size_t>(t)];
+        }
+    }
+    sp->layer_off[static_cast<size_t>(H) + 1] = S;
+    sp->S = S;
+    sp->E = E;
+    sp->implicit = false;
+    sp->csr_ready = true;
+    return true;
 }
 
 // The layered build can produce the implicit form too (IMPLICIT: every layer dense, <= 7 active
@@ -1852,6 +2173,7 @@ int vcs_space_build(const vcs_instance* inst, uint64_t state_cap, int device, vc
             const bool dense = explicit_now ? vcs::build_dense<WM, true>(sp.get(), state_cap)
                                             : vcs::build_dense<WM, false>(sp.get(), state_cap);
             if (dense) return;
+            if (vcs::build_small<WM>(sp.get(), state_cap)) return;
             if (!explicit_now && !std::getenv("VCS_BUILD_LAYERED") &&
                 vcs::implicit_layered_ok(sp->plan))
                 vcs::build_layers<WM, true>(sp.get(), state_cap);

@@ -80,20 +80,18 @@ C5_SAMPLES = ((3, 6, "static1609"), (3, 6, "aaa"), (4, 10, "aaa"), (5, 9, "aaa")
               (6, 8, "static1609"), (7, 6, "aaa"))
 
 
-def main(argv):
-    ref = Reference()
-    out = {"generator": "tests/golden/make_golden.py", "reference": "oracle/_ref/libvcsref.so",
-           "cases": {}, "families": {}}
-    for name, (ni, eps_list) in named_cases().items():
-        out["cases"][name] = record(ref, ni, eps_list)
-        print(name, out["cases"][name]["S"], flush=True)
-    for fam, (seed, params, n, brute_ok) in FAMILIES.items():
-        recs = []
-        for trial in range(n):
-            ni = V.generate_instance(N.VCS_GEN_RANDOM, seed, trial, *params, as_objects=False)
-            recs.append(record(ref, ni, with_brute=brute_ok))
-        out["families"][fam] = recs
-        print(fam, len(recs), flush=True)
+def extra(ref, argv):
+    """Add digests to the existing golden.json without regenerating it (--early, --c5)."""
+    if "--early" in argv:  # early-stop digests for C3 (eps 3) and C4 (eps 4): the fallback path
+        old = json.loads((HERE / "golden.json").read_text())
+        for name, eps in (("C3", 3.0), ("C4", 4.0)):
+            p = V.load_instance(str(HERE / "instances" / f"{name.lower()}.txt"))
+            ni = V.MdpInstance.from_workload(p.vcc, p.bots).native()
+            rec = record(ref, ni, eps_list=(eps,))
+            old["cases"][name][f"eps={eps:g}"] = rec[f"eps={eps:g}"]
+            print(name, eps, rec[f"eps={eps:g}"]["sweeps"], flush=True)
+        (HERE / "golden.json").write_text(json.dumps(old, indent=1, sort_keys=True))
+        return
     if "--c5" in argv:  # add / refresh only the C5 sample points (bench_workloads.c5_text)
         import bench_workloads as W
         old = json.loads((HERE / "golden.json").read_text())
@@ -106,6 +104,24 @@ def main(argv):
         (HERE / "golden.json").write_text(json.dumps(old, indent=1, sort_keys=True))
         print("wrote", HERE / "golden.json")
         return
+
+
+def main(argv):
+    ref = Reference()
+    if "--early" in argv or "--c5" in argv:
+        return extra(ref, argv)
+    out = {"generator": "tests/golden/make_golden.py", "reference": "oracle/_ref/libvcsref.so",
+           "cases": {}, "families": {}}
+    for name, (ni, eps_list) in named_cases().items():
+        out["cases"][name] = record(ref, ni, eps_list)
+        print(name, out["cases"][name]["S"], flush=True)
+    for fam, (seed, params, n, brute_ok) in FAMILIES.items():
+        recs = []
+        for trial in range(n):
+            ni = V.generate_instance(N.VCS_GEN_RANDOM, seed, trial, *params, as_objects=False)
+            recs.append(record(ref, ni, with_brute=brute_ok))
+        out["families"][fam] = recs
+        print(fam, len(recs), flush=True)
     if "--big" in argv:
         for name, args in (("C3", (2012, 0, 5, 8, 40, 3)), ("C4", (2012, 0, 6, 8, 48, 3))):
             ni = V.generate_instance(N.VCS_GEN_HOMOG, *args, as_objects=False)

@@ -681,3 +681,47 @@ def test_certified_tma_kernel_matches_golden(gpu, golden, monkeypatch):
         r = _solve(sp, method=N.VCS_METHOD_CERTIFIED)
         assert sha(r.values.raw_values()) == g["values_sha"]
         assert sha(r.policy.raw_actions()) == g["actions_sha"]
+
+
+def test_small_builder_matches_layered_and_oracle(gpu, oracle, monkeypatch):
+    """The single-CTA small-space builder (k_build_small: the canonical instance's 330 hash-path
+    layers in one launch) writes the same CSR as the layered builder and the oracle; an instance
+    whose layers outgrow its shared-memory tables falls back to the layered path; the state cap
+    raises the reference's error from inside it."""
+    from cases import cloud
+    p = V.load_instance(str(GOLDEN / "canonical_instance.txt"))
+    ni = V.NativeInstance(p.vcc, bots=p.bots)
+    a = V.StateSpace.build_native(ni, 10**9)
+    monkeypatch.setenv("VCS_NO_SMALL_BUILD", "1")
+    b = V.StateSpace.build_native(ni, 10**9)
+    monkeypatch.delenv("VCS_NO_SMALL_BUILD")
+    assert np.array_equal(a.layer_offsets(), b.layer_offsets())
+    for x, y in zip(a.csr(), b.csr()):
+        assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
+    _csr_equal(a, oracle.build(ni.ref, 10**9))
+    with pytest.raises(N.StateCapacityError, match="exceeds cap of 50000 states"):
+        V.StateSpace.build_native(ni, 50000)
+    # 8 clouds x 300 VMs with 7 tasks: layers outgrow the tables -> layered fallback, same bits
+    vcc = V.VccModel([cloud(i + 1, 300, 100.0 + i, 5.0 + i) for i in range(8)], 1.0, 1.2, 0.5)
+    tasks = [V.Task(j + 1, 1 + (j * 7) % 3, 60.0, 90.0) for j in range(7)]
+    wide = V.NativeInstance(vcc, bots=[V.BagOfTasks(1, tasks)])
+    _csr_equal(V.StateSpace.build_native(wide, 10**9), oracle.build(wide.ref, 10**9))
+
+
+@pytest.mark.parametrize("name,eps", [("C3", 3.0), ("C4", 4.0)])
+def test_certificate_failure_at_scale(gpu, golden, name, eps):
+    """An early stop on a full-size implicit space (C3 at eps 3 stops at 39 of 41 sweeps, C4 at
+    eps 4 at 24 of 49): the certificate fails, the fallback runs inside collect (reported as
+    deferred), and the result is the reference's."""
+    p = V.load_instance(str(GOLDEN / "instances" / f"{name.lower()}.txt"))
+    sp = V.StateSpace.build_native(V.NativeInstance(p.vcc, bots=p.bots), 10**9)
+    g = golden["cases"][name][f"eps={eps:g}"]
+    r = _solve(sp, eps=eps, method=N.VCS_METHOD_AUTO)
+    rep = r.values.report
+    assert rep.method == N.VCS_METHOD_WAVEFRONT and rep.fallback_deferred == 1
+    assert r.values.sweeps() == g["sweeps"] < sp.task_count() + 1
+    assert sha(r.values.raw_values()) == g["values_sha"]
+    assert sha(r.policy.raw_actions()) == g["actions_sha"]
+    # and the certified case on the same space is not deferred
+    r = _solve(sp, eps=1e-6, method=N.VCS_METHOD_AUTO)
+    assert r.values.report.method == N.VCS_METHOD_CERTIFIED and r.values.report.fallback_deferred == 0
