@@ -24,7 +24,9 @@ SHIM      := $(PKG)/libvcsched_b200.so
 ORACLE    := oracle/liboracle.so
 REFLIB    := oracle/_ref/libvcsref.so
 
-all: $(LIB) $(SHIM) $(ORACLE) ref
+CLI       := $(PKG)/vcsched-b200
+
+all: $(LIB) $(SHIM) $(CLI) $(ORACLE) ref
 
 $(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJ)
@@ -42,6 +44,11 @@ SHIM_HDRS := $(wildcard $(PKG)/include/vcsched/*.hpp)
 $(SHIM): $(SRC)/vcsched_b200.cpp $(SHIM_HDRS) include/vcs_gpu.h $(LIB)
 	$(CXX) -O2 -std=c++20 -fPIC -shared -Wall -I$(PKG)/include -o $@ $(SRC)/vcsched_b200.cpp \
 	    -L$(PKG) -lvcs_gpu -Wl,-rpath,'$$ORIGIN'
+
+# the reference CLI's schedule / speedup subcommands over the shim (scheduler mdp-gpu added)
+$(CLI): $(SRC)/vcsched_cli.cpp $(SHIM) $(SHIM_HDRS)
+	$(CXX) -O2 -std=c++20 -Wall -I$(PKG)/include -o $@ $(SRC)/vcsched_cli.cpp \
+	    -L$(PKG) -lvcsched_b200 -lvcs_gpu -Wl,-rpath,'$$ORIGIN'
 
 $(ORACLE): oracle/vcs_oracle.c include/vcs_gpu.h
 	$(CC) -O2 -std=gnu11 -fPIC -shared -ffp-contract=off -pthread -o $@ $< -lm
@@ -79,7 +86,7 @@ oracle/_ref/ref_suite_on_b200: tests/cpp/doctest.h tests/cpp/doctest_main.cpp $(
 	    -L$(PKG) -lvcsched_b200 -lvcs_gpu -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
 
 clean:
-	rm -rf build $(LIB) $(SHIM) $(ORACLE) oracle/_ref
+	rm -rf build $(LIB) $(SHIM) $(CLI) $(ORACLE) oracle/_ref
 
 .PHONY: all ref clean
 

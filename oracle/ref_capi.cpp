@@ -21,6 +21,7 @@
 #include <chrono>
 #include <cstring>
 #include <memory>
+#include <optional>
 #include <random>
 #include <sstream>
 #include <stdexcept>
@@ -408,6 +409,34 @@ int ref_per_vehicle_kbps(int32_t n_vehicles, int32_t scheme, uint64_t seed, int6
         *out = per_vehicle_throughput(vc_throughput(tr), n_vehicles);
         return VCS_OK;
     });
+}
+
+// The reference CLI's run_schedule output file (tools/cli.cpp:43-61, 100-118; io.cpp:203-242)
+// for scheduler 0 = greedy, 1 = mdp; format 0 = csv, 1 = json.  Returns the text length.
+uint64_t ref_schedule_text(const char* path, int scheduler, double eps, int format, char* buf,
+                           uint64_t cap) {
+    std::string text;
+    const int rc = guarded([&] {
+        const auto p = load_instance(path);
+        ScheduleResult res;
+        std::optional<SolverDiagnostics> diag;
+        if (scheduler == 0) {
+            res = greedy_schedule(p.vcc, p.bots);
+        } else {
+            const auto mdp = MdpInstance::from_workload(p.vcc, p.bots);
+            ViOptions o;
+            o.epsilon = eps;
+            const ViResult vi = value_iteration(mdp, o);
+            res = rollout(vi.policy, mdp);
+            diag = SolverDiagnostics{vi.values.epsilon(), vi.values.sweeps(),
+                                     vi.values.states_explored()};
+        }
+        text = format == 1 ? schedule_json(res, p.vcc, diag) : schedule_csv(res, p.vcc, diag);
+        return VCS_OK;
+    });
+    if (rc != VCS_OK) return 0;
+    if (buf) std::memcpy(buf, text.data(), std::min<std::size_t>(cap, text.size()));
+    return text.size();
 }
 
 // The reference's own parser (io.cpp:51-101), for cross-checking the product parser.

@@ -12,8 +12,12 @@
 
 #include "../../include/vcs_gpu.h"
 
+#include <algorithm>
+#include <charconv>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <fstream>
 #include <istream>
 #include <iterator>
 #include <limits>
@@ -359,12 +363,18 @@ std::vector<int32_t> worker_devices(int first, int n_workers) {
 namespace detail {
 ViResult run_value_iteration(std::shared_ptr<const StateSpace> space, const ViOptions& options,
                              int n_workers) {
+    vcs_solve_report rep{};
+    return run_value_iteration(std::move(space), options, n_workers, &rep);
+}
+
+ViResult run_value_iteration(std::shared_ptr<const StateSpace> space, const ViOptions& options,
+                             int n_workers, vcs_solve_report* report) {
     if (n_workers < 1) throw std::invalid_argument("n_workers must be >= 1");
     // page-locked results: the solve streams them to the host behind the layer pass
     PinnedVector<double> values(space->size());
     PinnedVector<std::int32_t> actions(space->size());
     vcs_solve_opts opts{options.epsilon, 1, 0, 1.0, VCS_METHOD_AUTO};
-    vcs_solve_report rep{};
+    vcs_solve_report& rep = *report;
     const auto devs = worker_devices(space->device(), n_workers);
     if (devs.size() == 1)
         check(vcs_solve(space->handle(), &opts, values.data(), actions.data(), &rep));
@@ -516,6 +526,130 @@ ParsedInstance load_instance(const std::string& path) {
     vcs_instance_owned* h = nullptr;
     check(vcs_instance_load(path.c_str(), &h), 0, true);
     return from_owned(h);
+}
+
+// ---- io.hpp writers (io.cpp:103-118, 203-242, 351-357 formats) -------------------------------
+
+namespace {
+std::string fmt17(double v) { // io.cpp fmt: %.17g
+    char buf[40];
+    std::snprintf(buf, sizeof buf, "%.17g", v);
+    return buf;
+}
+std::string json_num(double v) { // nlohmann::json's shortest round-trip form
+    if (std::isnan(v) || std::isinf(v)) return "null";
+    char buf[64];
+    auto r = std::to_chars(buf, buf + sizeof buf, v);
+    std::string s(buf, r.ptr);
+    if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
+    return s;
+}
+std::string target_name(int target) { return target == kPaidCloud ? "tcc" : "vc:" + std::to_string(target); }
+double reward_total(const ScheduleResult& r, const VccModel& vcc) { // metrics.cpp:32-39
+    const double gain = vcc.reward_per_vc_vm * static_cast<double>(r.vc_placed_vms());
+    const double cost = vcc.cost_per_tcc_vm * static_cast<double>(r.paid_vms);
+    const double idle = vcc.penalty_per_idle_vm * static_cast<double>(r.unused_vms);
+    return gain - cost - idle;
+}
+} // namespace
+
+std::string instance_text(const ParsedInstance& instance) {
+    std::ostringstream out;
+    out << "beta_vc " << fmt17(instance.vcc.reward_per_vc_vm) << "\n";
+    out << "beta_tc " << fmt17(instance.vcc.cost_per_tcc_vm) << "\n";
+    out << "gamma_vc " << fmt17(instance.vcc.penalty_per_idle_vm) << "\n";
+    for (const auto& c : instance.vcc.clouds)
+        out << "cloud " << c.id << ' ' << c.vm_total << ' ' << fmt17(c.vm_throughput_kbps) << ' '
+            << fmt17(c.v2i_delay_ms) << "\n";
+    for (const auto& bot : instance.bots) {
+        out << "bot " << bot.id << "\n";
+        for (const auto& t : bot.tasks)
+            out << "task " << t.id << ' ' << t.vm_demand << ' ' << fmt17(t.max_delay_ms) << ' '
+                << fmt17(t.min_vm_throughput_kbps) << "\n";
+    }
+    return out.str();
+}
+
+std::string schedule_csv(const ScheduleResult& result, const VccModel& vcc,
+                         const std::optional<SolverDiagnostics>& diag) {
+    std::ostringstream out;
+    out << "task_id,target,vms_used\n";
+    for (const auto& p : result.placements)
+        out << p.task_id << ',' << target_name(p.target) << ',' << p.vms_used << "\n";
+    out << "\n";
+    out << "summary,key,value\n";
+    out << "summary,vc_placed_vms," << result.vc_placed_vms() << "\n";
+    out << "summary,paid_vms," << result.paid_vms << "\n";
+    out << "summary,unused_vms," << result.unused_vms << "\n";
+    out << "summary,total_reward," << fmt17(reward_total(result, vcc)) << "\n";
+    if (diag) {
+        out << "summary,epsilon," << fmt17(diag->epsilon) << "\n";
+        out << "summary,sweeps," << diag->sweeps << "\n";
+        out << "summary,states_explored," << diag->states_explored << "\n";
+        if (!diag->solver.empty()) {
+            out << "summary,solver," << diag->solver << "\n";
+            out << "summary,gpus," << diag->gpus << "\n";
+            out << "summary,device_ms," << fmt17(diag->device_ms) << "\n";
+            out << "summary,build_ms," << fmt17(diag->build_ms) << "\n";
+        }
+    }
+    return out.str();
+}
+
+std::string schedule_json(const ScheduleResult& result, const VccModel& vcc,
+                          const std::optional<SolverDiagnostics>& diag) {
+    // the layout of nlohmann::json::dump(2) (io.cpp:228-242): object keys in sorted order
+    std::ostringstream out;
+    out << "{\n  \"placements\": [";
+    for (std::size_t i = 0; i < result.placements.size(); ++i) {
+        const auto& p = result.placements[i];
+        out << (i ? ",\n" : "\n") << "    {\n      \"target\": \"" << target_name(p.target)
+            << "\",\n      \"task_id\": " << p.task_id << ",\n      \"vms_used\": " << p.vms_used
+            << "\n    }";
+    }
+    out << (result.placements.empty() ? "]" : "\n  ]") << ",\n  \"summary\": {\n";
+    std::vector<std::pair<std::string, std::string>> kv = {
+        {"paid_vms", std::to_string(result.paid_vms)},
+        {"total_reward", json_num(reward_total(result, vcc))},
+        {"unused_vms", std::to_string(result.unused_vms)},
+        {"vc_placed_vms", std::to_string(result.vc_placed_vms())}};
+    if (diag) {
+        kv.push_back({"epsilon", json_num(diag->epsilon)});
+        kv.push_back({"sweeps", std::to_string(diag->sweeps)});
+        kv.push_back({"states_explored", std::to_string(diag->states_explored)});
+        if (!diag->solver.empty()) {
+            kv.push_back({"solver", "\"" + diag->solver + "\""});
+            kv.push_back({"gpus", std::to_string(diag->gpus)});
+            kv.push_back({"device_ms", json_num(diag->device_ms)});
+            kv.push_back({"build_ms", json_num(diag->build_ms)});
+        }
+    }
+    std::sort(kv.begin(), kv.end());
+    for (std::size_t i = 0; i < kv.size(); ++i)
+        out << "    \"" << kv[i].first << "\": " << kv[i].second << (i + 1 < kv.size() ? ",\n" : "\n");
+    out << "  }\n}\n";
+    return out.str();
+}
+
+std::string speedup_csv(const std::vector<SpeedupRow>& rows) {
+    std::ostringstream out;
+    out << "workers,wall_ms,speedup_vs_one\n";
+    for (const auto& r : rows)
+        out << r.workers << ',' << fmt17(r.wall_ms) << ',' << fmt17(r.speedup_vs_one) << "\n";
+    return out.str();
+}
+
+std::string read_file(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw IoError("cannot read file: " + path);
+    return std::string((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+}
+
+void write_file(const std::string& path, const std::string& content) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw IoError("cannot write file: " + path);
+    out << content;
+    if (!out) throw IoError("write failed: " + path);
 }
 
 } // namespace vcsched
