@@ -314,6 +314,22 @@ class RefResult:
             raise OracleError(rc, self.space.ref.err())
         return out.value
 
+    def value_of(self, free_vms, t, terminal):
+        """ValueTable::value_of (mdp.cpp:269-271); None where the reference throws."""
+        fv = np.ascontiguousarray(free_vms, np.int32)
+        out = C.c_double()
+        rc = self.L.ref_res_value_of(self.h, _p(fv, C.c_int32), int(t), 1 if terminal else 0,
+                                     C.byref(out))
+        return None if rc != 0 else out.value
+
+    def action_for(self, free_vms, t, terminal):
+        """Policy::action_for (mdp.cpp:277-282); None where the reference throws."""
+        fv = np.ascontiguousarray(free_vms, np.int32)
+        out = C.c_int32()
+        rc = self.L.ref_res_action_for(self.h, _p(fv, C.c_int32), int(t), 1 if terminal else 0,
+                                       C.byref(out))
+        return None if rc != 0 else out.value
+
     def rollout(self, n_tasks, n_clouds):
         tg = np.empty(max(n_tasks, 1), np.int32)
         used = np.zeros(max(n_clouds, 1), np.int64)

@@ -537,16 +537,20 @@ def test_builder_paths_agree(gpu, oracle, monkeypatch):
         V.StateSpace.build_native(ni, 1000)
 
 
-def test_batched_policy_query(gpu):
+def test_batched_policy_query(gpu, reference):
     """vcs_policy_query: value_of / action_for for many full states at once on the
-    device, bit-identical to the per-state path; unreachable -> NaN / VCS_NO_ACTION (the
-    reference raises), terminal -> VCS_NO_ACTION; host and device buffers both accepted."""
+    device, bit-identical to the UNMODIFIED reference's ValueTable::value_of and
+    Policy::action_for (oracle/_ref ref_res_value_of / ref_res_action_for) on the same states;
+    unreachable -> NaN / VCS_NO_ACTION where the reference raises, terminal -> VCS_NO_ACTION;
+    host and device buffers both accepted."""
     import torch
     rng = np.random.default_rng(7)
     for trial in range(4):
         p = V.generate_instance(N.VCS_GEN_RANDOM, 61, trial, 3, 6, 10, 3)
         inst = V.MdpInstance.from_workload(p.vcc, p.bots)
         vi = V.value_iteration(inst)
+        ni = inst.native()
+        ref_vi = reference.build(ni.ref, 10**9).vi(eps=1e-6)
         states = []
         for walk in range(6):
             s = V.initial_state(inst)
@@ -563,16 +567,15 @@ def test_batched_policy_query(gpu):
         vals = vi.values.value_of_many(states)
         acts = vi.policy.action_for_many(states)
         for s, v, a in zip(states, vals, acts):
-            try:
-                ref_v = vi.values.value_of(s)
-            except N.OutOfRange:
+            ref_v = ref_vi.value_of(s.free_vms, s.next_task_index, s.terminal)
+            ref_a = ref_vi.action_for(s.free_vms, s.next_task_index, s.terminal)
+            if ref_v is None:  # the reference throws std::out_of_range
                 assert np.isnan(v) and a == N.VCS_NO_ACTION
                 continue
             assert np.float64(v).view(np.uint64) == np.float64(ref_v).view(np.uint64)
-            if s.terminal or s.next_task_index >= vi.values.space().task_count():
-                assert a == N.VCS_NO_ACTION
-            else:
-                assert a == vi.policy.action_for(s).target
+            assert a == (N.VCS_NO_ACTION if ref_a is None else ref_a)
+            # and the per-state device path agrees
+            assert np.float64(vi.values.value_of(s)).view(np.uint64) == np.float64(v).view(np.uint64)
         # device-resident inputs and outputs are used in place
         space = vi.values.space()
         fv, ti, te = space._state_arrays(states)
