@@ -379,6 +379,24 @@ def full_work_methods(space, args, stream):
     return out
 
 
+def e2e_cpp(workload, steps, gpus=1):
+    """The same end-to-end step through the reference's C++ API on the drop-in shim
+    (libvcsched_b200.so: load_instance + StateSpace::build + detail::run_value_iteration into
+    the ValueTable / Policy host storage + rollout), timed inside one C++ process
+    (paper_2012_12419_b200/vcsched-b200 e2e)."""
+    cli = ROOT / "paper_2012_12419_b200" / "vcsched-b200"
+    r = subprocess.run([str(cli), "e2e", "--instance", str(W.FILES[workload]), "--workers",
+                        str(steps), "--gpus", str(gpus), "--state-cap", str(10**9)],
+                       capture_output=True, text=True, timeout=600)
+    if r.returncode != 0:
+        return {"error": r.stderr.strip()[-300:]}
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    out["path"] = ("C++ reference API over libvcsched_b200.so: load_instance + StateSpace::build + "
+                   "detail::run_value_iteration (pinned ValueTable/Policy storage) + rollout "
+                   "(device policy walk)")
+    return out
+
+
 def early_stop_solve(N, space, eps):
     """Side number: a C4 solve whose certificate FAILS (eps = 4: the reference stops at sweep 24
     of 49, tests/test_gpu_solver.py pins the bits): the certified pass, then the wavefront
@@ -856,6 +874,8 @@ def run_b200(args):
         line["full_work_methods"] = full_work_methods(space, args, stream)
         if workload == "c4":
             line["early_stop"] = early_stop_solve(N, space, 4.0)
+    if rank == 0 and world == 1 and args.e2e_steps > 0 and workload in ("c1", "c3", "c4"):
+        line["e2e_cpp"] = e2e_cpp(workload, max(3, args.e2e_steps))
     if rank == 0 and not args.no_greedy:
         line["greedy"] = greedy_c2(V, N)
     if rank == 0 and world == 1 and not args.no_side:

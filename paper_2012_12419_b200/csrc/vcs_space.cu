@@ -462,6 +462,60 @@ __global__ void k_rollout(QueryArgs a, const int32_t* __restrict__ demand, int32
     *status = 0;
 }
 
+// The same walk without a key index (no locate table to build): on an explicit CSR the
+// successor under action a is the row's edge carrying a (edges are one per action); on the
+// implicit form the state's index is the rank table entry of its key-space index
+// d = sum_p free[cloud_p] * W_p.
+__global__ void k_rollout_csr(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ succ,
+                              const int32_t* __restrict__ action, const int32_t* __restrict__ actions,
+                              int H, int32_t* targets, int32_t* status) {
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    uint32_t s = 0; // the initial state is the root (mdp.cpp:81-92)
+    for (int t = 0; t < H; ++t) {
+        const int32_t a = actions[s];
+        targets[t] = a;
+        const uint32_t eb = row_ptr[s], ee = row_ptr[s + 1];
+        uint32_t nxt = 0xffffffffu;
+        for (uint32_t e = eb; e < ee; ++e)
+            if (action[e] == a) {
+                nxt = succ[e];
+                break;
+            }
+        if (nxt == 0xffffffffu) {
+            *status = 1;
+            return;
+        }
+        s = nxt;
+    }
+    *status = 0;
+}
+
+__global__ void k_rollout_rank(const LayerParam* __restrict__ params, const uint32_t* __restrict__ rank_tables,
+                               const uint64_t* __restrict__ rank_off, const uint64_t* __restrict__ layer_off,
+                               const int32_t* __restrict__ actions, const int32_t* __restrict__ demand,
+                               int32_t* fv, int H, int32_t* targets, int32_t* status) {
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    uint64_t idx = 0; // the root
+    for (int t = 0; t < H; ++t) {
+        if (t > 0) {
+            const LayerParam& L = params[t]; // layer t's own numbering (wself)
+            uint64_t d = 0;
+            for (int p = 0; p < L.n_active; ++p)
+                d += static_cast<uint64_t>(fv[L.cloud[p]]) * L.wself[p];
+            const uint32_t r = rank_tables[rank_off[t - 1] + d];
+            if (r == kEmpty32) {
+                *status = 1;
+                return;
+            }
+            idx = layer_off[t] + r;
+        }
+        const int32_t a = actions[idx];
+        targets[t] = a;
+        if (a >= 0) fv[a] -= demand[t];
+    }
+    *status = 0;
+}
+
 uint32_t blocks_for(uint64_t n, uint32_t threads) {
     return static_cast<uint32_t>((n + threads - 1) / threads);
 }
@@ -2477,27 +2531,47 @@ int vcs_rollout(vcs_space* sp, const vcs_instance* inst, int32_t* target_per_tas
         if (H == 0) return VCS_OK;
         vcs::bind_device(sp->device);
         const vcs::StreamUse s(sp, stream);
-        vcs::ensure_locate_index(sp);
-        vcs::QueryArgs a{};
-        ensure_query_meta(sp, a);
-        // one staging block: initial free counts, demands, scratch free counts, targets, status
+        // one staging block: initial free counts, demands, scratch free counts, targets, status,
+        // then (implicit form) the layer and rank-table offsets
         const size_t nk = static_cast<size_t>(std::max(K, 1)), nh = static_cast<size_t>(H);
-        std::vector<int32_t> host(2 * nk + 2 * nh + 1, 0);
+        const size_t n32 = (2 * nk + 2 * nh + 1 + 1) & ~size_t(1); // (u64 offsets stay aligned)
+        const bool rank_walk = sp->implicit && !sp->rank_off.empty() && !sp->csr_ready;
+        std::vector<int32_t> host(n32 + (rank_walk ? 2 * (nh + 2) * 2 : 0), 0);
         std::memcpy(host.data(), inst->cloud_vm_free, sizeof(int32_t) * static_cast<size_t>(K));
         std::memcpy(host.data() + nk, inst->task_demand, sizeof(int32_t) * nh);
+        if (rank_walk) {
+            std::memcpy(host.data() + n32, sp->layer_off.data(), sizeof(uint64_t) * (nh + 2));
+            std::memcpy(host.data() + n32 + 2 * (nh + 2), sp->rank_off.data(), sizeof(uint64_t) * (nh + 1));
+        }
         vcs::DevBuf<int32_t> buf;
         buf.exact(host.size(), s);
-        VCS_CUDA(cudaMemcpyAsync(buf.p, host.data(), sizeof(int32_t) * (nk + nh),
+        VCS_CUDA(cudaMemcpyAsync(buf.p, host.data(), sizeof(int32_t) * host.size(),
                                  cudaMemcpyHostToDevice, s));
-        a.free_vms = buf.p;
         int32_t* fv = buf.p + nk + nh;
         int32_t* tg = fv + nk;
         int32_t* st = tg + nh;
-        vcs::dispatch_words(vcs::max_words(sp), [&](auto wm) {
-            constexpr int WM = decltype(wm)::value;
-            vcs::k_rollout<WM><<<1, 32, 0, s>>>(a, buf.p + nk, fv, tg, st);
+        VCS_CUDA(cudaMemcpyAsync(fv, buf.p, sizeof(int32_t) * nk, cudaMemcpyDeviceToDevice, s));
+        if (rank_walk) {
+            const uint64_t* lo = reinterpret_cast<const uint64_t*>(buf.p + n32);
+            vcs::k_rollout_rank<<<1, 32, 0, s>>>(sp->params_dev.p, sp->rank_tables.p,
+                                                 lo + (nh + 2), lo, sp->result_actions, buf.p + nk,
+                                                 fv, H, tg, st);
             VCS_LAUNCHED();
-        });
+        } else if (sp->csr_ready) {
+            vcs::k_rollout_csr<<<1, 32, 0, s>>>(sp->row_ptr.p, sp->succ.p, sp->action.p,
+                                                sp->result_actions, H, tg, st);
+            VCS_LAUNCHED();
+        } else {
+            vcs::ensure_locate_index(sp);
+            vcs::QueryArgs a{};
+            ensure_query_meta(sp, a);
+            a.free_vms = buf.p;
+            vcs::dispatch_words(vcs::max_words(sp), [&](auto wm) {
+                constexpr int WM = decltype(wm)::value;
+                vcs::k_rollout<WM><<<1, 32, 0, s>>>(a, buf.p + nk, fv, tg, st);
+                VCS_LAUNCHED();
+            });
+        }
         VCS_CUDA(cudaMemcpyAsync(host.data() + 2 * nk + nh, tg, sizeof(int32_t) * (nh + 1),
                                  cudaMemcpyDeviceToHost, s));
         VCS_CUDA(cudaStreamSynchronize(s));

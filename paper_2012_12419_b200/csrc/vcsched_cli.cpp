@@ -8,6 +8,7 @@
 //   vcsched-b200 schedule --instance F [--scheduler greedy|mdp|mdp-parallel|mdp-gpu]
 //                [--workers N] [--gpus N] [--epsilon E] [--state-cap N] [--out F] [--format csv|json]
 //   vcsched-b200 speedup --instance F [--workers N] [--epsilon E] [--state-cap N] [--out F]
+//   vcsched-b200 e2e --instance F [--workers REPEAT] [--gpus N]   (timing of the API call path)
 #include "vcsched/greedy.hpp"
 #include "vcsched/io.hpp"
 #include "vcsched/mdp.hpp"
@@ -15,6 +16,7 @@
 
 #include "../../include/vcs_gpu.h"
 
+#include <algorithm>
 #include <chrono>
 #include <iostream>
 #include <map>
@@ -118,6 +120,51 @@ int run_schedule(const Config& c) {
     return kOk;
 }
 
+// `e2e`: the reference API call path end to end, repeated in one process (the CUDA context is
+// created once, outside the timing): load_instance + MdpInstance::from_workload +
+// StateSpace::build + detail::run_value_iteration (results into the ValueTable / Policy host
+// storage) + rollout.  Prints one JSON object with the per-repetition wall times (ms).
+int run_e2e(const Config& c, int repeat) {
+    std::vector<double> ms, build_ms, solve_ms, rollout_ms;
+    double v0 = 0.0;
+    int sweeps = 0;
+    long paid = 0;
+    for (int i = 0; i < repeat + 2; ++i) {
+        const auto t0 = std::chrono::steady_clock::now();
+        const ParsedInstance instance = load_instance(c.instance);
+        const auto mdp = MdpInstance::from_workload(instance.vcc, instance.bots);
+        ViOptions options;
+        options.epsilon = c.epsilon;
+        options.state_cap = c.state_cap;
+        auto space = StateSpace::build(mdp, options.state_cap);
+        const auto t1 = std::chrono::steady_clock::now();
+        const ViResult vi = detail::run_value_iteration(space, options, c.gpus);
+        const auto t2 = std::chrono::steady_clock::now();
+        const ScheduleResult r = rollout(vi.policy, mdp);
+        const auto t3 = std::chrono::steady_clock::now();
+        auto d = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        if (i >= 2) { // two warm-up repetitions (the device memory pool reaches its size)
+            ms.push_back(d(t0, t3));
+            build_ms.push_back(d(t0, t1));
+            solve_ms.push_back(d(t1, t2));
+            rollout_ms.push_back(d(t2, t3));
+        }
+        v0 = vi.values.raw_values()[0];
+        sweeps = vi.values.sweeps();
+        paid = r.paid_vms;
+    }
+    auto med = [](std::vector<double> v) {
+        std::sort(v.begin(), v.end());
+        return v.empty() ? 0.0 : v[v.size() / 2];
+    };
+    std::cout.precision(17);
+    std::cout << "{\"ms_per_step\": " << med(ms) << ", \"load_and_build_ms\": " << med(build_ms)
+              << ", \"solve_ms\": " << med(solve_ms) << ", \"rollout_ms\": " << med(rollout_ms)
+              << ", \"steps\": " << ms.size() << ", \"sweeps\": " << sweeps
+              << ", \"v0\": " << v0 << ", \"rollout_paid\": " << paid << "}\n";
+    return kOk;
+}
+
 int run_speedup(const Config& c) {
     const ParsedInstance instance = load_instance(c.instance);
     const auto mdp = MdpInstance::from_workload(instance.vcc, instance.bots);
@@ -141,6 +188,7 @@ int main(int argc, char** argv) {
         const Config c = parse(args);
         if (c.sub == "schedule") return run_schedule(c);
         if (c.sub == "speedup") return run_speedup(c);
+        if (c.sub == "e2e") return run_e2e(c, std::max(1, c.workers));
         if (c.sub == "simulate" || c.sub == "benchmark")
             throw ConfigError("subcommand '" + c.sub + "' drives the DSRC simulator, which is not "
                               "part of the B200 solver build");
