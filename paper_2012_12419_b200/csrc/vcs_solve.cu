@@ -1022,6 +1022,135 @@ __device__ __forceinline__ void cert_dense_layer(const CertImplArgs& a, const La
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// The key-space walk with TWO indices in flight per thread (d and d + stride, both stepped by
+// 2*stride): sixteen successor-pair gathers are issued before either evaluation, which hides
+// HBM latency on layers whose pair vectors do not fit in L2 (C7: 76 MB per layer).  Arithmetic,
+// slot order and the strict first maximum are cert_dense_layer's.
+template <int WM, bool DISC>
+__device__ __forceinline__ void cert_dense_layer2(const CertImplArgs& a, const LayerParam& L,
+                                                  unsigned long long& s_lb, uint64_t first,
+                                                  uint64_t stride) {
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int SL = kDenseSlots;
+    constexpr int NF = kDenseSlots - 1;
+    const bool retires = L.n_keep != L.n_active;
+    const SlotDecoder<WM> dec(L);
+    const double r_cloud = L.r_cloud_kept, r_paid = L.r_paid_kept;
+    const int na = L.n_active;
+    double dmax = 0.0;
+    const uint64_t d_hi = a.d_hi;
+    uint64_t d = a.d_lo + first;
+    const uint64_t step = 2 * stride;
+    uint32_t g0[NF], g1[NF], sd[NF], rad[NF];
+    {
+        uint32_t r0 = static_cast<uint32_t>(d < d_hi ? d : 0);
+        uint32_t r1 = static_cast<uint32_t>(d + stride < d_hi ? d + stride : 0);
+        uint32_t srem = static_cast<uint32_t>(step < a.dense_n ? step : 0);
+#pragma unroll
+        for (int p = 0; p < NF; ++p) {
+            rad[p] = p < na ? L.radix[p] : 1u;
+            g0[p] = r0 % rad[p];
+            r0 /= rad[p];
+            g1[p] = r1 % rad[p];
+            r1 /= rad[p];
+            sd[p] = srem % rad[p];
+            srem /= rad[p];
+        }
+    }
+    uint32_t retmask = 0;
+#pragma unroll
+    for (int p = 0; p < NF; ++p)
+        if (p < na && L.keep_idx[p] < 0) retmask |= 1u << p;
+    const double r_cl = L.r_cloud, r_pd = L.r_paid, gam = L.gamma;
+    const int dem = L.demand;
+    uint32_t rk0 = d < d_hi ? __ldg(a.rank_self + d) : kEmpty32;
+    uint32_t rk1 = d + stride < d_hi ? __ldg(a.rank_self + d + stride) : kEmpty32;
+    asm volatile("griddepcontrol.wait;" ::: "memory"); // (PDL) the previous layer's pairs
+    auto slots = [&](const uint32_t (&g)[NF], int& ret_all) {
+        uint32_t base = 0, mask = 0;
+        ret_all = 0;
+#pragma unroll
+        for (int p = 0; p < NF; ++p) {
+            base += g[p] * dec.wn[p];
+            if (((dec.sw[p] >> 16) & 1u) && g[p] >= dec.demand) mask |= 1u << p;
+            if ((retmask >> p) & 1u) ret_all += static_cast<int>(g[p]);
+        }
+        return Slots(static_cast<uint64_t>(base) | (static_cast<uint64_t>(mask) << 32));
+    };
+    auto advance = [&](uint32_t (&g)[NF]) {
+        uint32_t carry = 0;
+#pragma unroll
+        for (int p = 0; p < NF; ++p) {
+            const uint32_t v = g[p] + sd[p] + carry;
+            carry = v >= rad[p] ? 1u : 0u;
+            g[p] = carry ? v - rad[p] : v;
+        }
+    };
+    auto evaluate = [&](uint64_t dd, uint32_t r, const Slots& sl, int ret_all, const double2 (&x)[SL]) {
+        double hi = -INFINITY, lo = -INFINITY;
+        int best = -1;
+#pragma unroll
+        for (int e = 0; e < SL; ++e) {
+            const int pe = e == SL - 1 ? -1 : e;
+            double rw;
+            if (retires) {
+                const int ret = ret_all - ((pe >= 0 && ((retmask >> pe) & 1u)) ? dem : 0);
+                rw = __dsub_rn(pe < 0 ? r_pd : r_cl, __dmul_rn(gam, static_cast<double>(ret)));
+            } else {
+                rw = pe < 0 ? r_paid : r_cloud;
+            }
+            const double qx = DISC ? __dadd_rn(rw, __dmul_rn(a.discount, x[e].x)) : __dadd_rn(rw, x[e].x);
+            const double qy = DISC ? __dadd_rn(rw, __dmul_rn(a.discount, x[e].y)) : __dadd_rn(rw, x[e].y);
+            if (qy > hi) { // strict: the first maximal edge wins (mdp.cpp:254-260)
+                hi = qy;
+                best = pe;
+            }
+            if (qx > lo) lo = qx;
+        }
+        if (a.m == 1) lo = 0.0; // V_0
+        a.xd_cur[dd] = make_double2(lo, hi);
+        if (a.write_out) {
+            a.values_out[a.row0 + r] = hi;
+            a.act_out[a.row0 + r] = best < 0 ? -1 : L.cloud[best];
+        }
+        const double df = fabs(hi - lo);
+        dmax = dmax < df ? df : dmax;
+    };
+    for (; d < d_hi; d += step) {
+        const uint32_t r0 = rk0, r1 = rk1;
+        const bool has1 = d + stride < d_hi;
+        if (d + step < d_hi) rk0 = __ldg(a.rank_self + d + step);
+        if (d + step + stride < d_hi) rk1 = __ldg(a.rank_self + d + step + stride);
+        int ra0, ra1;
+        const Slots s0 = slots(g0, ra0);
+        const Slots s1 = slots(g1, ra1);
+        advance(g0);
+        advance(g1);
+        const bool v0 = r0 != kEmpty32, v1 = has1 && r1 != kEmpty32;
+        double2 x0[SL], x1[SL];
+#pragma unroll
+        for (int e = 0; e < SL; ++e) {
+            x0[e] = make_double2(-INFINITY, -INFINITY);
+            x1[e] = make_double2(-INFINITY, -INFINITY);
+            if (v0 && s0.valid(e)) x0[e] = __ldg(a.xd_next + dec.idx(s0, e));
+            if (v1 && s1.valid(e)) x1[e] = __ldg(a.xd_next + dec.idx(s1, e));
+        }
+        if (v0) evaluate(d, r0, s0, ra0, x0);
+        if (v1) evaluate(d + stride, r1, s1, ra1, x1);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double other = __shfl_xor_sync(FULL, dmax, o);
+        dmax = dmax < other ? other : dmax;
+    }
+    if ((threadIdx.x & 31) == 0 && dmax > 0.0)
+        atomicMax(&s_lb, static_cast<unsigned long long>(__double_as_longlong(dmax)));
+    __syncthreads();
+    if (threadIdx.x == 0 && s_lb)
+        atomicMax(reinterpret_cast<unsigned long long*>(a.lb + a.m), s_lb);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void load_layer_param(LayerParam& sL, const LayerParam* src,
                                                  unsigned long long& s_lb) {
     __syncthreads(); // the previous layer's readers of sL are done
@@ -1305,6 +1434,16 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_cert_dense_tma(CertImplArgs 
         atomicMax(reinterpret_cast<unsigned long long*>(a.lb + a.m),
                   static_cast<unsigned long long>(__double_as_longlong(dmax)));
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <int WM, bool DISC>
+__global__ void __launch_bounds__(256, 2) k_cert_dense2(CertImplArgs a) {
+    __shared__ LayerParam sL;
+    __shared__ unsigned long long s_lb;
+    load_layer_param(sL, a.L, s_lb);
+    cert_dense_layer2<WM, DISC>(a, sL, s_lb,
+                                static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x,
+                                static_cast<uint64_t>(gridDim.x) * blockDim.x);
 }
 
 // K* = H+1 is proven iff lb_k >= eps for k = 1..H (and no sweep cap below H+1).  Sets the graph
@@ -1670,6 +1809,40 @@ void launch_cert_layer(const vcs_space* sp, const CertData& data, const CertLaye
         if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense_tma<true>, c, d_next));
         else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense_tma<false>, c, d_next));
         VCS_LAUNCHED();
+        return;
+    }
+    // (opt-in, VCS_CERT_ILP2=1: two indices in flight per thread; measured no faster on the
+    // B200 — C7 5.58 vs 5.42 ms, C4 0.55 vs 0.52 ms — the gathers are not latency-per-thread
+    // bound)
+    const char* ilp_env = std::getenv("VCS_CERT_ILP2");
+    const bool ilp2 = dense_order && ks && ilp_env && std::atoi(ilp_env) != 0;
+    if (ilp2) {
+        dispatch_words_solve(max_key_words(sp), [&](auto wm) {
+            constexpr int WM = decltype(wm)::value;
+            const void* fn = disc ? reinterpret_cast<const void*>(k_cert_dense2<WM, true>)
+                                  : reinterpret_cast<const void*>(k_cert_dense2<WM, false>);
+            int dev = 0;
+            VCS_CUDA(cudaGetDevice(&dev));
+            static thread_local std::map<std::pair<const void*, int>, int> occ2;
+            int& per_sm = occ2[{fn, dev}];
+            if (!per_sm) VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
+            const uint64_t items = L.d_hi > L.d_lo ? L.d_hi - L.d_lo : 0;
+            const uint64_t blocks = std::max<uint64_t>(
+                1, std::min<uint64_t>((items + 511) / 512,
+                                      static_cast<uint64_t>(std::max(1, per_sm)) * sp->num_sms));
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+            cfg.blockDim = dim3(256);
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = pdl ? 1 : 0;
+            if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense2<WM, true>, c));
+            else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense2<WM, false>, c));
+            VCS_LAUNCHED();
+        });
         return;
     }
     if (trace_enabled())

@@ -728,3 +728,16 @@ def test_certificate_failure_at_scale(gpu, golden, name, eps):
     # and the certified case on the same space is not deferred
     r = _solve(sp, eps=1e-6, method=N.VCS_METHOD_AUTO)
     assert r.values.report.method == N.VCS_METHOD_CERTIFIED and r.values.report.fallback_deferred == 0
+
+
+def test_certified_ilp2_kernel_matches_golden(gpu, golden, monkeypatch):
+    """k_cert_dense2 (two key-space indices in flight per thread, VCS_CERT_ILP2=1) gives the
+    reference's bits on C3 and C4."""
+    monkeypatch.setenv("VCS_CERT_ILP2", "1")
+    for name in ("C3", "C4"):
+        p = V.load_instance(str(GOLDEN / "instances" / f"{name.lower()}.txt"))
+        sp = V.StateSpace.build_native(V.NativeInstance(p.vcc, bots=p.bots), 10**9)
+        g = golden["cases"][name]["eps=1e-06"]
+        r = _solve(sp, method=N.VCS_METHOD_CERTIFIED)
+        assert sha(r.values.raw_values()) == g["values_sha"]
+        assert sha(r.policy.raw_actions()) == g["actions_sha"]

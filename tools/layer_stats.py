@@ -1,4 +1,8 @@
-"""Layer sizes vs key-space sizes of a bench workload (which certified kernel walks each layer)."""
+"""Layer sizes vs key-space sizes of a bench workload (which certified kernel walks each layer);
+writes tools/<name>_layers.json for tools/ncu_cert_summary.py.
+
+    python tools/layer_stats.py [c4|c7|c3|c1]"""
+import json
 import sys
 from pathlib import Path
 
@@ -15,6 +19,11 @@ inst = V.MdpInstance.from_workload(p.vcc, p.bots)
 sp = V.StateSpace.build_native(inst.native(), 10**9, 0, inst)
 lo = sp.layer_offsets().astype(np.int64)
 n = np.diff(lo)
-caps = [c.vm_free + 1 for c in p.vcc.clouds]
-print(name, "S", sp.size(), "key space", int(np.prod(caps)))
-print("layer sizes:", n.tolist())
+key_space = int(np.prod([c.vm_free + 1 for c in p.vcc.clouds]))
+H = sp.task_count()
+doc = {"workload": name, "S": sp.size(), "H": H, "key_space": key_space,
+       "layers": [int(x) for x in n],
+       # k_cert_dense walks layer t >= 1 when at least half its key space is reached
+       "dense_layers_desc": [t for t in range(H - 1, 0, -1) if 2 * int(n[t]) >= key_space]}
+(ROOT / "tools" / f"{name}_layers.json").write_text(json.dumps(doc))
+print(name, "S", sp.size(), "key space", key_space, "dense layers", len(doc["dense_layers_desc"]))
