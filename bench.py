@@ -283,7 +283,7 @@ def run_reference(args):
 
 PARALLELISM = {
     "single": lambda n: "single GPU",
-    "multi": lambda n: f"one state space split across {n} GPUs of rank 0's process "
+    "multi": lambda n: f"one state space split across {n} ranks (GPUs) of rank 0's process "
                        "(vcs_solve_multi: per-layer key-space ranges, forward-halo peer copies "
                        "over NVLink, lower bounds max-reduced on the primary; the other ranks "
                        "only join the barriers)",
@@ -696,6 +696,7 @@ def run_b200(args):
     # multi: rank 0 drives every GPU of the node through vcs_solve_multi (one process owns the
     # whole state space); --ranks R > WORLD_SIZE puts several ranks on a GPU
     n_ranks = max(args.ranks, world) if multi else 1
+    multi_error = None
     devices = [r % max(1, world) for r in range(n_ranks)] if multi else None
     exchange = N.VCS_EXCHANGE_ALLGATHER if args.exchange == "allgather" else N.VCS_EXCHANGE_HALO
     use_dist = world > 1 or sharded_path or sharding == "instances"
@@ -724,6 +725,25 @@ def run_b200(args):
     sampler = ClockSampler(local)
     sampler.start()
 
+    if multi:
+        # probe the multi-GPU pass once (peer access, multi-device graph); if this node cannot
+        # run it, every rank falls back to one independent instance per GPU (weak scaling)
+        ok = torch.ones(1, dtype=torch.int32, device=dev)
+        if rank == 0:
+            try:
+                N.check(enqueue_fn(N, devices, exchange)(space, opts, C.c_void_p(stream.cuda_stream)))
+                probe = N.vcs_solve_report()
+                N.check(N.lib().vcs_solve_collect(space.handle, None, None, C.byref(probe),
+                                                  C.c_void_p(stream.cuda_stream)))
+            except N.VcsError as e:
+                multi_error = str(e)
+                log(f"multi-GPU solve unavailable ({e}); falling back to --sharding instances")
+                ok.zero_()
+        if world > 1:
+            dist.broadcast(ok, 0)
+        if not int(ok.item()):
+            multi, devices = False, None
+            sharding = "instances" if world > 1 else "single"
     if not sharded_path:
         if world > 1:
             dist.barrier()
@@ -835,7 +855,7 @@ def run_b200(args):
     if not sharded_path:
         roofline = roofline_for(N, method, model_bytes, alg_bytes_done, sweep_ms, S, sweeps, E / S)
 
-    multi_info = None
+    multi_info = {"error": multi_error} if multi_error else None
     if multi and rank == 0:
         mi = N.vcs_multi_report()
         if N.lib().vcs_multi_info(space.handle, C.byref(mi)) == 0:
@@ -858,7 +878,8 @@ def run_b200(args):
                     "solver (the reference) performs for the same result"},
         "solve": {"transitions": E, "method": METHODS.get(method, str(method)),
                   "backups_performed_per_step": backups_done, "layer_skip": not args.no_skip,
-                  "parallelism": PARALLELISM[sharding](world), "instances": n_instances,
+                  "parallelism": PARALLELISM[sharding](n_ranks if multi else world),
+                  "instances": n_instances,
                   "l2": "no flush between steps: the certified pass reads the 100 MB rank tables "
                         "+ 155 MB keys and writes 232 MB of results per solve (> 126 MB L2)",
                   "build_ms": space.info.build_ms, "build_wall_ms": build_wall_ms,

@@ -1852,12 +1852,15 @@ void launch_cert_layer(const vcs_space* sp, const CertData& data, const CertLaye
                      static_cast<unsigned long long>(L.d_hi));
     dispatch_words_solve(max_key_words(sp), [&](auto wm) {
         constexpr int WM = decltype(wm)::value;
+        // the key-walking kernel: 3 blocks per SM for keys of <= 2 words (80 registers, no
+        // spills); wide keys (4 / 8 words: many-cloud instances) take 2 so they do not spill
+        constexpr int IMB = WM <= 2 ? 3 : 2;
         // 3 blocks per SM (80 registers, no spills): C4 0.68 ms vs 0.72 at 4, 0.74 at 2
         const void* fn =
             dense_order ? (disc ? reinterpret_cast<const void*>(k_cert_dense<WM, true, 3>)
                                 : reinterpret_cast<const void*>(k_cert_dense<WM, false, 3>))
-                        : (disc ? reinterpret_cast<const void*>(k_cert_implicit<WM, true, 3, false>)
-                                : reinterpret_cast<const void*>(k_cert_implicit<WM, false, 3, false>));
+                        : (disc ? reinterpret_cast<const void*>(k_cert_implicit<WM, true, IMB, false>)
+                                : reinterpret_cast<const void*>(k_cert_implicit<WM, false, IMB, false>));
         static thread_local std::map<std::pair<const void*, int>, int> occ;
         int dev = 0;
         VCS_CUDA(cudaGetDevice(&dev));
@@ -1883,11 +1886,11 @@ void launch_cert_layer(const vcs_space* sp, const CertData& data, const CertLaye
             if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense<WM, true, 3>, c));
             else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense<WM, false, 3>, c));
         } else if (ks) {
-            if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, true, 3, true>, c));
-            else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, false, 3, true>, c));
+            if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, true, IMB, true>, c));
+            else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, false, IMB, true>, c));
         } else {
-            if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, true, 3, false>, c));
-            else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, false, 3, false>, c));
+            if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, true, IMB, false>, c));
+            else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, false, IMB, false>, c));
         }
         VCS_LAUNCHED();
     });

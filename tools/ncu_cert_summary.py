@@ -34,7 +34,7 @@ def main(rep, layers_json, skip, out):
             "dram_bytes": dram, "dram_over_alg": dram / alg, "ncu_time_us": tt * 1e6,
             "dram_GBps": dram / tt / 1e9, "alg_GBps": alg / tt / 1e9,
             "l2_hit_pct": pick("lts__t_sector_hit_rate.pct"),
-            "l2_bytes": g("lts__t_bytes.sum") if "lts__t_bytes.sum" in hdr else None,
+            "l2_bytes": 32.0 * pick("lts__t_sectors.sum") if "lts__t_sectors.sum" in hdr else None,
             "warps_active_pct": pick("sm__warps_active.avg.pct_of_peak_sustained_active"),
             "issue_active_pct": pick("smsp__issue_active.avg.pct_of_peak_sustained_active")})
     doc = {"kernel": "k_cert_dense (certified pass, key-space walk)", "workload": lay["workload"],
