@@ -192,6 +192,7 @@ struct vcs_space {
     std::vector<uint64_t> ver_off_host;
     // certified pass: (V_{m-1}, V_m) of every state, lower bounds lb[k] of the residuals
     vcs::DevBuf<double2> cert_xd;
+    vcs::DevBuf<int8_t> cert_act_ks; // (VCS_CERT_PERMUTE) winner slots by key-space index
     vcs::DevBuf<double> cert_lb;
     cudaStream_t aux_stream = nullptr; // captures the fallback body of the certified graph
     std::map<vcs::GraphKey, vcs::CachedGraph> graphs;

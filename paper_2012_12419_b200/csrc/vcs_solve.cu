@@ -820,6 +820,7 @@ struct CertImplArgs {
     uint64_t dense_n;                       // layer t's key-space size
     int write_own;
     int write_out;                          // 0: values/actions are written by another rank
+    int8_t* act_ks;                         // (VCS_CERT_PERMUTE) winner slot by key-space index
     // key-space order: the indices [d_lo, d_hi) of this launch (the whole key space on one GPU,
     // a rank's contiguous share when the layer is sharded across GPUs)
     uint64_t d_lo, d_hi;
@@ -1436,6 +1437,141 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_cert_dense_tma(CertImplArgs 
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// The key-space walk specialised for NON-RETIRING transitions (every full layer of C3/C4/C7
+// but the last): the successor of d through cloud slot p is d - demand*W_p and the paid one is
+// d itself, so the successor index needs no digit sum, every cloud edge has the same reward
+// (r_cloud_kept) and the paid edge r_paid_kept; the eligible slots and their byte offsets are
+// per-layer uniforms.  ~2x fewer instructions per index than the generic walk (390 SASS
+// instructions per iteration there); same operations on every edge, same strict first maximum.
+template <bool DISC>
+__global__ void __launch_bounds__(256, 3) k_cert_dense_nr(CertImplArgs a) {
+    __shared__ LayerParam sL;
+    __shared__ unsigned long long s_lb;
+    load_layer_param(sL, a.L, s_lb);
+    const LayerParam& L = sL;
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int NF = kDenseSlots - 1;
+    const int na = L.n_active;
+    const uint32_t dem = static_cast<uint32_t>(L.demand);
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const uint64_t d_hi = a.d_hi;
+    uint64_t d = a.d_lo + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    uint32_t g[NF], sd[NF], rad[NF], off[NF];
+    uint32_t elig = 0;
+    {
+        uint32_t rem = static_cast<uint32_t>(d < d_hi ? d : 0);
+        uint32_t srem = static_cast<uint32_t>(stride < a.dense_n ? stride : 0);
+#pragma unroll
+        for (int p = 0; p < NF; ++p) {
+            rad[p] = p < na ? L.radix[p] : 1u;
+            g[p] = rem % rad[p];
+            rem /= rad[p];
+            sd[p] = srem % rad[p];
+            srem /= rad[p];
+            off[p] = p < na ? dem * L.wnext[p] : 0u;
+            if (p < na && L.attr[p]) elig |= 1u << p;
+        }
+    }
+    const double r_cloud = L.r_cloud_kept, r_paid = L.r_paid_kept;
+    uint32_t rn = d < d_hi ? __ldg(a.rank_self + d) : kEmpty32;
+    double dmax = 0.0;
+    asm volatile("griddepcontrol.wait;" ::: "memory"); // (PDL) the previous layer's pairs
+    for (; d < d_hi; d += stride) {
+        const uint32_t r = rn;
+        if (d + stride < d_hi) rn = __ldg(a.rank_self + d + stride);
+        uint32_t mask = 0;
+#pragma unroll
+        for (int p = 0; p < NF; ++p) mask |= (g[p] >= dem ? 1u : 0u) << p;
+        mask &= elig;
+        {
+            uint32_t carry = 0;
+#pragma unroll
+            for (int p = 0; p < NF; ++p) {
+                const uint32_t v = g[p] + sd[p] + carry;
+                carry = v >= rad[p] ? 1u : 0u;
+                g[p] = carry ? v - rad[p] : v;
+            }
+        }
+        if (r == kEmpty32) continue;
+        const double2* P = a.xd_next + d;
+        double2 x[NF];
+#pragma unroll
+        for (int p = 0; p < NF; ++p)
+            if ((mask >> p) & 1u) x[p] = __ldg(P - off[p]);
+        const double2 xp = __ldg(P);
+        double hi = -INFINITY, lo = -INFINITY;
+        int best = -1;
+#pragma unroll
+        for (int p = 0; p < NF; ++p) {
+            if (!((mask >> p) & 1u)) continue;
+            const double qx = DISC ? __dadd_rn(r_cloud, __dmul_rn(a.discount, x[p].x)) : __dadd_rn(r_cloud, x[p].x);
+            const double qy = DISC ? __dadd_rn(r_cloud, __dmul_rn(a.discount, x[p].y)) : __dadd_rn(r_cloud, x[p].y);
+            if (qy > hi) { // strict: the first maximal edge wins (mdp.cpp:254-260)
+                hi = qy;
+                best = p;
+            }
+            if (qx > lo) lo = qx;
+        }
+        {
+            const double qx = DISC ? __dadd_rn(r_paid, __dmul_rn(a.discount, xp.x)) : __dadd_rn(r_paid, xp.x);
+            const double qy = DISC ? __dadd_rn(r_paid, __dmul_rn(a.discount, xp.y)) : __dadd_rn(r_paid, xp.y);
+            if (qy > hi) {
+                hi = qy;
+                best = -1;
+            }
+            if (qx > lo) lo = qx;
+        }
+        if (a.m == 1) lo = 0.0; // V_0
+        a.xd_cur[d] = make_double2(lo, hi);
+        if (a.act_ks) {
+            a.act_ks[d] = static_cast<int8_t>(best); // coalesced; k_cert_permute reorders
+        } else if (a.write_out) {
+            a.values_out[a.row0 + r] = hi;
+            a.act_out[a.row0 + r] = best < 0 ? -1 : L.cloud[best];
+        }
+        const double dd = fabs(hi - lo);
+        dmax = dmax < dd ? dd : dmax;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double other = __shfl_xor_sync(FULL, dmax, o);
+        dmax = dmax < other ? other : dmax;
+    }
+    if ((threadIdx.x & 31) == 0 && dmax > 0.0)
+        atomicMax(&s_lb, static_cast<unsigned long long>(__double_as_longlong(dmax)));
+    __syncthreads();
+    if (threadIdx.x == 0 && s_lb)
+        atomicMax(reinterpret_cast<unsigned long long*>(a.lb + a.m), s_lb);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// (VCS_CERT_PERMUTE experiment) layer t's results in BFS order from the key-space-ordered pairs
+// and winner slots: a thread per state decodes its key-space index from its packed key.
+template <int WM>
+__global__ void __launch_bounds__(256) k_cert_permute(const uint64_t* __restrict__ keys,
+                                                      const LayerParam* __restrict__ Lp,
+                                                      const double2* __restrict__ xd,
+                                                      const int8_t* __restrict__ act_ks, uint64_t n,
+                                                      uint64_t row0, double* values_out,
+                                                      int32_t* act_out) {
+    __shared__ LayerParam L;
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(LayerParam) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t*>(&L)[i] = __ldg(reinterpret_cast<const uint32_t*>(Lp) + i);
+    __syncthreads();
+    const int words = L.words;
+    for (uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+         r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        uint64_t k[WM];
+        load_key<WM>(keys + r * static_cast<uint64_t>(words), words, k);
+        uint32_t d = 0;
+        for (int p = 0; p < L.n_active; ++p)
+            d += static_cast<uint32_t>(get_field<WM>(k, L.bit_off[p], L.width[p])) * L.wself[p];
+        const int8_t b = act_ks[d];
+        values_out[row0 + r] = xd[d].y;
+        act_out[row0 + r] = b < 0 ? -1 : L.cloud[b];
+    }
+}
+
 template <int WM, bool DISC>
 __global__ void __launch_bounds__(256, 2) k_cert_dense2(CertImplArgs a) {
     __shared__ LayerParam sL;
@@ -1744,6 +1880,29 @@ CertLayer cert_layer(const vcs_space* sp, int t, double2* xd, uint64_t half, boo
 
 // Layer t's transition keeps every cloud with the same numbering (succ = d - demand*W_p): the
 // TMA-staged kernel applies.
+// Whether a full layer of this key-space size writes its results in key-space order and lets
+// k_cert_permute reorder them (VCS_CERT_PERMUTE=0/1 forces it).  Measured on the B200: the
+// scattered value/action stores are 48 % of C7's certified pass (76 MB pair vectors per layer);
+// the gather pass brings C7 from 5.36 to 4.91 ms, while on C4 (L2-resident, 8.5 MB) the extra
+// launches cost more than the scatter (0.71 vs 0.53 ms).
+bool cert_permute_layer(uint64_t key_space) {
+    if (const char* e = std::getenv("VCS_CERT_PERMUTE")) return std::atoi(e) != 0;
+    return 16 * key_space > (48ull << 20);
+}
+bool cert_permute_space(const vcs_space* sp) {
+    return cert_keyspace(sp) && cert_permute_layer(cert_half(sp));
+}
+
+// Layer t's transition keeps every cloud with the same numbering, so succ = d - demand*W_p.
+bool cert_nonretiring(const vcs_space* sp, int t) {
+    if (t < 1 || t >= sp->H) return false;
+    const LayerParam& P = sp->plan.layers[static_cast<size_t>(t)];
+    if (P.n_keep != P.n_active || P.dense_size == 0 || P.self_size != P.dense_size) return false;
+    for (int p = 0; p < P.n_active; ++p)
+        if (P.keep_idx[p] != p || P.wnext[p] != P.wself[p]) return false;
+    return P.n_active <= kDenseSlots - 1;
+}
+
 // (Opt-in, VCS_CERT_TMA=1: measured on the B200 it does not beat k_cert_dense — C4 0.63 vs
 // 0.52 ms, C7 5.6 vs 5.4 ms; its consumers wait on the bulk copies while the scattered
 // value/action stores, 27 % of the C7 time, stay.  DESIGN.md section 3.4.)
@@ -1785,6 +1944,53 @@ void launch_cert_layer(const vcs_space* sp, const CertData& data, const CertLaye
         c.d_hi = L.d_hi;
     }
     const bool dense_order = L.dense_order;
+    // the non-retiring walk pays with the gather pass on layers beyond L2 (C7); on L2-resident
+    // layers (C4) the generic walk measured as fast or faster (0.517 vs 0.530 ms)
+    if (dense_order && ks && cert_nonretiring(sp, t) && cert_permute_layer(L.dense_n) &&
+        !std::getenv("VCS_CERT_GENERIC") && !std::getenv("VCS_CERT_TMA") &&
+        !std::getenv("VCS_CERT_ILP2")) {
+        const void* fn = disc ? reinterpret_cast<const void*>(k_cert_dense_nr<true>)
+                              : reinterpret_cast<const void*>(k_cert_dense_nr<false>);
+        static thread_local std::map<std::pair<const void*, int>, int> occ_nr;
+        int dev = 0;
+        VCS_CUDA(cudaGetDevice(&dev));
+        int& per_sm = occ_nr[{fn, dev}];
+        if (!per_sm) VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
+        const uint64_t items = L.d_hi > L.d_lo ? L.d_hi - L.d_lo : 0;
+        const uint64_t blocks = std::max<uint64_t>(
+            1, std::min<uint64_t>((items + 255) / 256,
+                                  static_cast<uint64_t>(std::max(1, per_sm)) * sp->num_sms));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+        cfg.blockDim = dim3(256);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl ? 1 : 0;
+        CertImplArgs cx = c;
+        // pair vectors beyond L2 (C7): results in key-space order + a gather pass to BFS order
+        // (single GPU only: a rank of the multi-GPU pass holds only its range's pairs)
+        const bool permute = sp->cert_act_ks.p && c.write_out && L.d_lo == 0 &&
+                             L.d_hi == L.dense_n && cert_permute_layer(L.dense_n);
+        if (permute) cx.act_ks = sp->cert_act_ks.p;
+        if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense_nr<true>, cx));
+        else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense_nr<false>, cx));
+        if (permute) {
+            VCS_LAUNCHED();
+            dispatch_words_solve(max_key_words(sp), [&](auto wm) {
+                constexpr int WM = decltype(wm)::value;
+                const unsigned pb = static_cast<unsigned>(std::min<uint64_t>(
+                    (L.n + 255) / 256, static_cast<uint64_t>(sp->num_sms) * 8));
+                k_cert_permute<WM><<<std::max(1u, pb), 256, 0, s>>>(
+                    data.keys + sp->key_off[t], data.params + t, L.xd_cur, sp->cert_act_ks.p, L.n,
+                    L.row0, values_out, act_out);
+            });
+        }
+        VCS_LAUNCHED();
+        return;
+    }
     if (dense_order && ks && cert_tma_ok(sp, t)) {
         // the successor windows staged in shared memory by bulk copies (k_cert_dense_tma)
         const void* fn = disc ? reinterpret_cast<const void*>(k_cert_dense_tma<true>)
@@ -2776,6 +2982,11 @@ int enqueue_impl(vcs_space* sp, const vcs_solve_opts* opts, void* stream, int st
                 cudaGetLastError();
                 method = VCS_METHOD_JACOBI; // the version store does not fit right now
             }
+        }
+        if (method == VCS_METHOD_CERTIFIED && vcs::cert_permute_space(sp) &&
+            sp->cert_act_ks.n < vcs::cert_half(sp)) {
+            sp->cert_act_ks.exact(vcs::cert_half(sp), sp->stream);
+            VCS_CUDA(cudaStreamSynchronize(sp->stream));
         }
         if (method == VCS_METHOD_CERTIFIED && sp->cert_xd.n < vcs::cert_pairs_needed(sp)) {
             sp->cert_xd.exact(vcs::cert_pairs_needed(sp), sp->stream);

@@ -2158,6 +2158,7 @@ vcs_space::~vcs_space() {
     act8_dev.release_idle();
     ver.release_idle();
     cert_xd.release_idle();
+    cert_act_ks.release_idle();
     cert_lb.release_idle();
     band_ver.release_idle();
     ver_off.release_idle();

@@ -741,3 +741,40 @@ def test_certified_ilp2_kernel_matches_golden(gpu, golden, monkeypatch):
         r = _solve(sp, method=N.VCS_METHOD_CERTIFIED)
         assert sha(r.values.raw_values()) == g["values_sha"]
         assert sha(r.policy.raw_actions()) == g["actions_sha"]
+
+
+@pytest.mark.parametrize("kernel", ["generic", "permute"])
+def test_certified_kernel_variants_match_golden(gpu, golden, monkeypatch, kernel):
+    """The generic key-space walk (VCS_CERT_GENERIC=1, the retiring-capable kernel on every
+    layer) and the non-retiring walk with key-space-ordered results + gather pass
+    (VCS_CERT_PERMUTE=1, the default only for pair vectors beyond L2) reproduce the reference's
+    digests on C3 and C4."""
+    monkeypatch.setenv("VCS_CERT_GENERIC" if kernel == "generic" else "VCS_CERT_PERMUTE", "1")
+    for name in ("C3", "C4"):
+        p = V.load_instance(str(GOLDEN / "instances" / f"{name.lower()}.txt"))
+        sp = V.StateSpace.build_native(V.NativeInstance(p.vcc, bots=p.bots), 10**9)
+        g = golden["cases"][name]["eps=1e-06"]
+        r = _solve(sp, method=N.VCS_METHOD_CERTIFIED)
+        assert sha(r.values.raw_values()) == g["values_sha"]
+        assert sha(r.policy.raw_actions()) == g["actions_sha"]
+
+
+def test_c7_kernel_variants_agree(gpu, monkeypatch):
+    """C7 (190.7 M states, no reference digest: the reference cannot build it in a test's time)
+    is solved bit-identically by the default path (non-retiring walk + gather pass), the
+    generic walk and the scattered-store variant; the certificate holds (57 sweeps)."""
+    p = V.load_instance(str(GOLDEN / "instances" / "c7.txt"))
+    sp = V.StateSpace.build_native(V.NativeInstance(p.vcc, bots=p.bots), 10**9)
+    assert sp.size() == 190740125
+    digests = []
+    for env in ({}, {"VCS_CERT_GENERIC": "1"}, {"VCS_CERT_PERMUTE": "0"}):
+        for k in ("VCS_CERT_GENERIC", "VCS_CERT_PERMUTE"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        sp2 = V.StateSpace.build_native(V.NativeInstance(p.vcc, bots=p.bots), 10**9)
+        r = _solve(sp2, method=N.VCS_METHOD_CERTIFIED)
+        assert r.values.sweeps() == 57 and r.values.report.method == N.VCS_METHOD_CERTIFIED
+        digests.append((sha(r.values.raw_values()), sha(r.policy.raw_actions())))
+        del r, sp2
+    assert digests[0] == digests[1] == digests[2]
