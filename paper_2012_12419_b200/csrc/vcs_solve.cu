@@ -2147,7 +2147,13 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
         g.fallback_at_collect = true;
         return;
     }
-    if (!capturing) raise(VCS_EINVAL, "the certified solve is only recorded into a CUDA graph");
+    // uncaptured (the first solve of a small explicit space, see enqueue_solve): the pass and
+    // its certificate only; a failed certificate runs the fallback at collect
+    const bool small = sp->max_layer <= static_cast<uint64_t>(kCertSmallStates) &&
+                       !std::getenv("VCS_NO_SMALL_SOLVE");
+    if (!capturing && !small)
+        raise(VCS_EINVAL, "the certified solve is only recorded into a CUDA graph");
+    g.fallback_at_collect = !capturing;
     // explicit CSR: k_cert_rows, a thread per row, 4 edges in flight, 4 blocks per SM (C4:
     // 0.75 ms; a warp-cooperative form that staged q pairs in shared memory measured 0.83 ms,
     // more resident warps thrash L1)
@@ -2166,7 +2172,7 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
     a.discount = key.discount;
     a.write_out = 1;
     int launches = 0;
-    if (sp->max_layer <= static_cast<uint64_t>(kCertSmallStates) && !std::getenv("VCS_NO_SMALL_SOLVE")) {
+    if (small) {
         // a small space: the whole pass in one block (layer pairs in shared memory)
         if (sp->layer_off_dev.n < static_cast<size_t>(H) + 2) // (ensure_wave_buffers sets it)
             raise(VCS_EINVAL, "layer offsets were not uploaded before the capture");
@@ -2198,7 +2204,7 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
     // Profiling mode (ncu cannot profile kernels of graphs holding conditional nodes): no
     // fallback node; vcs_solve_collect raises if the proof did not hold.
     static const bool no_fallback = std::getenv("VCS_PROFILE_NO_FALLBACK") != nullptr;
-    if (no_fallback) {
+    if (no_fallback || !capturing) {
         k_cert_check<<<1, 64, 0, s>>>(sp->cert_lb.p, H, key.eps, key.max_sweeps, sp->ctrl.p, 0);
         VCS_LAUNCHED();
         record_event(g.ev[1], s, capturing);
@@ -2307,8 +2313,14 @@ CachedGraph& enqueue_solve(vcs_space* sp, const GraphKey& key, cudaStream_t s) {
     // (The explicit certified pass needs the graph: its fallback is a conditional node.)
     // (Not with the streamed download: measured on C4, direct launches interleaved with the
     // per-layer download events idle the GPU — e2e 6.1 vs 5.75 ms; C3 gains 1.58 -> 1.41 ms.)
-    const bool direct_ok = sp->implicit && key.method == kMethodCertified && key.stream_out == 0;
-    if (sp->implicit && key.method == kMethodCertified &&
+    // Small explicit spaces (k_cert_small, one launch) too: their graph would carry the whole
+    // layer wavefront as the fallback body (canonical: 330 layers, 1.9 ms to capture and
+    // instantiate, more than the solve); uncaptured, the fallback runs at collect.
+    const bool small_explicit = !sp->implicit && sp->max_layer <= static_cast<uint64_t>(kCertSmallStates) &&
+                                !std::getenv("VCS_NO_SMALL_SOLVE");
+    const bool direct_ok = (sp->implicit || small_explicit) && key.method == kMethodCertified &&
+                           key.stream_out == 0;
+    if ((sp->implicit || small_explicit) && key.method == kMethodCertified &&
         (std::getenv("VCS_NO_GRAPH") || (direct_ok && g.uses == 0 && !g.exec &&
                                                       !std::getenv("VCS_GRAPH_FIRST")))) {
         record_solve(sp, key, g, s, false); // (VCS_NO_GRAPH: always direct; VCS_SYNC_CHECK works)
