@@ -112,3 +112,29 @@ def test_multi_python_api_and_errors(gpu, golden):
     dv[1] = 99
     assert N.lib().vcs_solve_multi_enqueue(sp.handle, C.byref(opts), 2, N.ptr(dv, C.c_int32),
                                            0, None) == N.VCS_EINVAL
+
+
+@pytest.mark.parametrize("discount", [1.0, 0.9])
+def test_multi_random_instances_against_oracle(gpu, oracle, monkeypatch, discount):
+    """Random instances with retiring clouds (the transitions the halo cannot bound take the
+    whole-layer exchange) and the labelled discounted extension: the multi-GPU pass at 2-5
+    emulated ranks, every layer split, equals the oracle bit for bit."""
+    from conftest import bits
+    monkeypatch.setenv("VCS_MULTI_MIN_SPLIT", "1")
+    for trial in range(4):
+        ni = V.generate_instance(N.VCS_GEN_RANDOM, 41, trial, 5, 6, 18, 3, as_objects=False)
+        sp = V.StateSpace.build_native(ni, 10**9)
+        osp = oracle.build(ni.ref, 10**9)
+        v, a, sw, _, _ = osp.vi(discount=discount)
+        for ranks in (2, 5):
+            opts = N.vcs_solve_opts(1e-6, 1, 0, discount, N.VCS_METHOD_CERTIFIED)
+            vals = np.empty(sp.size())
+            acts = np.empty(sp.size(), np.int32)
+            rep = N.vcs_solve_report()
+            dv = np.zeros(ranks, np.int32)
+            N.check(N.lib().vcs_solve_multi(sp.handle, C.byref(opts), ranks, N.ptr(dv, C.c_int32),
+                                            N.VCS_EXCHANGE_HALO, N.ptr(vals, C.c_double),
+                                            N.ptr(acts, C.c_int32), C.byref(rep)))
+            assert rep.sweeps == sw, (trial, ranks)
+            assert np.array_equal(bits(vals), bits(v)), (trial, ranks)
+            assert np.array_equal(acts, a), (trial, ranks)
