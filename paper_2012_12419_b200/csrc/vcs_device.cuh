@@ -193,6 +193,9 @@ struct vcs_space {
     // certified pass: (V_{m-1}, V_m) of every state, lower bounds lb[k] of the residuals
     vcs::DevBuf<double2> cert_xd;
     vcs::DevBuf<int8_t> cert_act_ks; // (VCS_CERT_PERMUTE) winner slots by key-space index
+    vcs::DevBuf<unsigned char> stream_meta; // k_cert_stream's per-layer table
+    vcs::DevBuf<uint32_t> stream_sync;      // its tile flags, layer counters, work counter
+    uint32_t stream_tiles = 0;
     vcs::DevBuf<double> cert_lb;
     cudaStream_t aux_stream = nullptr; // captures the fallback body of the certified graph
     std::map<vcs::GraphKey, vcs::CachedGraph> graphs;

@@ -1582,6 +1582,326 @@ __global__ void __launch_bounds__(256, 2) k_cert_dense2(CertImplArgs a) {
                                 static_cast<uint64_t>(gridDim.x) * blockDim.x);
 }
 
+// ---- k_cert_stream: the whole certified pass as ONE persistent kernel --------------------------
+// Per-layer launches cost ~3 us each even chained by PDL (measured: 48 near-empty layer launches
+// take 0.15 ms of C4's 0.52), and every layer waits for the slowest block of the one before.
+// Here blocks pull tiles of T indices from one global counter, in layer order (t = H-1 .. 0, then
+// ascending within a layer), and a tile waits only for what it reads:
+//   * key-space walk on a non-retiring transition: the successor of d through slot p is
+//     d - demand*W_p, so tile k of layer t reads layer t+1's tiles covering
+//     [kT - demand*W_p, kT + T - demand*W_p) for its eligible slots and [kT, kT + T) (paid) — at
+//     most 16 per-tile flags;
+//   * key-space walk on a retiring transition, BFS walk (sparse layers): all of layer t+1.
+// Pairs rotate through THREE buffers (layer t in t % 3) and a tile of layer t also waits until
+// layer t+2 is complete — the last reader of the buffer it overwrites — so two layers are in
+// flight at once.  Deadlock-free without co-residency: a tile is handed out only to a running
+// block and waits only for tiles handed out before it.  Producer: stores, block barrier, fence,
+// release-store of the tile's flag, count into the layer's done counter.  Consumer: warp 0
+// spins (relaxed) on the tile's dependencies, one acquire fence (it invalidates the SM's L1, so
+// the pair loads after the block barrier, cached in L1 for the overlapping windows, are fresh).
+// Per index the arithmetic is cert_dense_layer's / cert_implicit_layer's, so are the bits.
+constexpr int kStreamT = 1024;       // indices (key-space walk) or states (BFS walk) per tile
+constexpr int kStreamThreads = 256;
+constexpr int kStreamBufs = 4;       // pair buffers in rotation (layer t in buffer t % 4)
+
+struct StreamLayer {
+    uint64_t row0, n;        // the layer's BFS rows
+    uint64_t dense_n;        // key-space size of the layer
+    uint64_t key_off;        // its packed keys (u64 words)
+    uint64_t rank_self_off;  // transition t-1's rank table (key-space walk)
+    uint32_t tile_start, n_tiles;
+    int32_t kind;            // 0: key-space walk, window deps; 1: key-space walk, whole-layer dep;
+                             // 2: BFS walk, whole-layer dep
+    int32_t m;               // H - t
+    uint32_t n_shift;
+    uint32_t shift[kDenseSlots]; // kind 0: the eligible slots' demand*W_p, and 0 (paid)
+};
+
+struct StreamArgs {
+    const StreamLayer* layers; // processing order o = 0..H-1 (t = H-1-o)
+    const LayerParam* params;  // by t
+    const uint64_t* keys;
+    const uint32_t* rank_tables;
+    double2* xd;               // 3 buffers of `third` pairs; layer t in buffer t % 3
+    uint64_t third;
+    double* values_out;
+    int32_t* act_out;
+    double* lb;
+    double discount;
+    uint32_t* sync;            // [total_tiles flags | H done counters | work counter]
+    uint32_t total_tiles;
+    int H;
+};
+
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// spin with relaxed loads (an acquire load per iteration would invalidate L1 every time), then
+// one acquire fence once the producer's release-store is seen
+__device__ __forceinline__ void wait_ge(const uint32_t* p, uint32_t target) {
+    while (ld_relaxed_u32(p) < target) {}
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int WM, bool DISC>
+__global__ void __launch_bounds__(kStreamThreads, 2) k_cert_stream(StreamArgs A) {
+    // per tile, everything that is latency rather than work is taken off the critical path: the
+    // NEXT tile id is fetched while this one computes, its layer's parameters are loaded into
+    // the other half of a double buffer behind the computation, and warp 0 checks the tile's
+    // (up to 17) dependencies with one lane each, so a satisfied check costs one L2 round trip
+    __shared__ LayerParam sLb[2];
+    __shared__ uint32_t s_tile[2];
+    __shared__ int s_o[2];
+    __shared__ unsigned long long s_lb;
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int SL = kDenseSlots;
+    constexpr int NF = kDenseSlots - 1;
+    constexpr int PW = static_cast<int>(sizeof(LayerParam) / 4);
+    constexpr int PPT = (PW + kStreamThreads - 1) / kStreamThreads; // param words per thread
+    const int tid = threadIdx.x, lane = tid & 31;
+    uint32_t* flags = A.sync;
+    uint32_t* done = A.sync + A.total_tiles;
+    uint32_t* counter = done + A.H;
+    auto layer_of = [&](uint32_t tile, int from) {
+        int o = from < 0 ? 0 : from;
+        while (tile >= A.layers[o].tile_start + A.layers[o].n_tiles) ++o;
+        return o;
+    };
+    if (tid == 0) {
+        s_tile[0] = atomicAdd(counter, 1u);
+        s_o[0] = s_tile[0] < A.total_tiles ? layer_of(s_tile[0], 0) : 0;
+    }
+    __syncthreads();
+    if (s_tile[0] < A.total_tiles) // the first tile's parameters, synchronously
+        for (int i = tid; i < PW; i += blockDim.x)
+            reinterpret_cast<uint32_t*>(&sLb[0])[i] =
+                __ldg(reinterpret_cast<const uint32_t*>(A.params + (A.H - 1 - s_o[0])) + i);
+    for (int it = 0;; ++it) {
+        const int bb = it & 1;
+        __syncthreads(); // s_tile[bb], s_o[bb], sLb[bb] are complete
+        const uint32_t tile = s_tile[bb];
+        if (tile >= A.total_tiles) break;
+        const int o = s_o[bb];
+        const int t = A.H - 1 - o;
+        const StreamLayer* Lp = A.layers + o;
+        const uint32_t k = tile - Lp->tile_start;
+        const int kind = Lp->kind, m = Lp->m;
+        if (tid == 0) {
+            s_lb = 0ull;
+            const uint32_t nx = atomicAdd(counter, 1u); // the next tile, behind this one
+            s_tile[bb ^ 1] = nx;
+            s_o[bb ^ 1] = nx < A.total_tiles ? layer_of(nx, o) : o;
+        }
+        // read-only inputs of the tile (rank entries / packed keys, build outputs) are loaded
+        // before the dependency wait, so their latency overlaps it
+        constexpr int JT = kStreamT / kStreamThreads;
+        constexpr int KP = WM <= 2 ? WM : 1; // keys prefetched for narrow keys only
+        uint32_t rr[JT];
+        uint64_t kpre[JT][KP];
+        if (kind != 2) {
+            const uint32_t* rank_self = A.rank_tables + Lp->rank_self_off;
+            const uint64_t dense_n = Lp->dense_n;
+#pragma unroll
+            for (int j = 0; j < JT; ++j) {
+                const uint64_t d = static_cast<uint64_t>(k) * kStreamT + j * kStreamThreads + tid;
+                rr[j] = d < dense_n ? __ldg(rank_self + d) : kEmpty32;
+            }
+        } else if (WM <= 2) {
+            const int words = sLb[bb].words;
+            const uint64_t n = Lp->n;
+            const uint64_t* keys = A.keys + Lp->key_off;
+#pragma unroll
+            for (int j = 0; j < JT; ++j) {
+                const uint64_t i = static_cast<uint64_t>(k) * kStreamT + j * kStreamThreads + tid;
+#pragma unroll
+                for (int w = 0; w < KP; ++w)
+                    kpre[j][w] = (i < n && w < words) ? __ldg(keys + i * static_cast<uint64_t>(words) + w) : 0ull;
+            }
+        }
+        if (tid < 32) { // dependencies: one lane per flag / counter
+            const uint32_t* wp = nullptr;
+            uint32_t want = 0;
+            if (lane == 0 && o >= kStreamBufs - 1) { // the last reader of buffer t % B is done
+                wp = done + o - (kStreamBufs - 1);
+                want = A.layers[o - (kStreamBufs - 1)].n_tiles;
+            } else if (lane == 1 && o >= 1 && kind != 0) { // all of layer t+1
+                wp = done + o - 1;
+                want = A.layers[o - 1].n_tiles;
+            } else if (lane >= 2 && o >= 1 && kind == 0) { // layer t+1's tiles under the windows
+                const int q = (lane - 2) >> 1, half_sel = (lane - 2) & 1;
+                if (q < static_cast<int>(Lp->n_shift)) {
+                    const int64_t D = static_cast<int64_t>(Lp->dense_n);
+                    const int64_t lo = static_cast<int64_t>(k) * kStreamT - Lp->shift[q];
+                    const int64_t a = lo < 0 ? 0 : lo;
+                    const int64_t b = (lo + kStreamT) > D ? D : (lo + kStreamT);
+                    if (b > a) {
+                        const int64_t j = half_sel ? (b - 1) / kStreamT : a / kStreamT;
+                        wp = flags + A.layers[o - 1].tile_start + j;
+                        want = 1u;
+                    }
+                }
+            }
+            if (wp) wait_ge(wp, want);
+            __syncwarp();
+            if (lane == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
+        __syncthreads();
+        // the next tile's layer parameters: loads issued now, stored after the computation
+        const int o_next = s_o[bb ^ 1];
+        const bool pf = s_tile[bb ^ 1] < A.total_tiles;
+        uint32_t pfw[PPT];
+#pragma unroll
+        for (int q = 0; q < PPT; ++q) {
+            const int i = tid + q * kStreamThreads;
+            pfw[q] = (pf && i < PW) ? __ldg(reinterpret_cast<const uint32_t*>(A.params + (A.H - 1 - o_next)) + i) : 0u;
+        }
+        const LayerParam& L = sLb[bb];
+        const double2* xn = A.xd + static_cast<uint64_t>((t + 1) % kStreamBufs) * A.third;
+        double2* xc = A.xd + static_cast<uint64_t>(t % kStreamBufs) * A.third;
+        const bool retires = L.n_keep != L.n_active;
+        const SlotDecoder<WM> dec(L);
+        double dmax = 0.0;
+        const uint64_t row0 = Lp->row0;
+        if (kind != 2) { // ---- key-space walk (cert_dense_layer's evaluation) -------------------
+            const int na = L.n_active;
+            const uint64_t dense_n = Lp->dense_n;
+            const uint32_t* rank_self = A.rank_tables + Lp->rank_self_off;
+            uint32_t retmask = 0;
+#pragma unroll
+            for (int p = 0; p < NF; ++p)
+                if (p < na && L.keep_idx[p] < 0) retmask |= 1u << p;
+            const double r_cl = L.r_cloud, r_pd = L.r_paid, gam = L.gamma;
+            const double r_cloud = L.r_cloud_kept, r_paid = L.r_paid_kept;
+            const int dem = L.demand;
+            (void)rank_self;
+#pragma unroll
+            for (int j = 0; j < JT; ++j) {
+                const uint64_t d = static_cast<uint64_t>(k) * kStreamT + j * kStreamThreads + tid;
+                if (d >= dense_n) break;
+                const uint32_t r = rr[j];
+                if (r == kEmpty32) continue;
+                uint32_t rem = static_cast<uint32_t>(d), base = 0, mask = 0;
+                int ret_all = 0;
+#pragma unroll
+                for (int p = 0; p < NF; ++p) {
+                    const uint32_t rad = p < na ? L.radix[p] : 1u;
+                    const uint32_t gp = rem % rad;
+                    rem /= rad;
+                    base += gp * dec.wn[p];
+                    if (((dec.sw[p] >> 16) & 1u) && gp >= dec.demand) mask |= 1u << p;
+                    if ((retmask >> p) & 1u) ret_all += static_cast<int>(gp);
+                }
+                const Slots sl(static_cast<uint64_t>(base) | (static_cast<uint64_t>(mask) << 32));
+                double2 x[SL];
+#pragma unroll
+                for (int e = 0; e < SL; ++e) {
+                    x[e] = make_double2(-INFINITY, -INFINITY);
+                    if (sl.valid(e)) x[e] = __ldca(xn + dec.idx(sl, e));
+                }
+                double hi = -INFINITY, lo = -INFINITY;
+                int best = -1;
+#pragma unroll
+                for (int e = 0; e < SL; ++e) {
+                    const int pe = e == SL - 1 ? -1 : e;
+                    double rw;
+                    if (retires) {
+                        const int ret = ret_all - ((pe >= 0 && ((retmask >> pe) & 1u)) ? dem : 0);
+                        rw = __dsub_rn(pe < 0 ? r_pd : r_cl, __dmul_rn(gam, static_cast<double>(ret)));
+                    } else {
+                        rw = pe < 0 ? r_paid : r_cloud;
+                    }
+                    const double qx = DISC ? __dadd_rn(rw, __dmul_rn(A.discount, x[e].x)) : __dadd_rn(rw, x[e].x);
+                    const double qy = DISC ? __dadd_rn(rw, __dmul_rn(A.discount, x[e].y)) : __dadd_rn(rw, x[e].y);
+                    if (qy > hi) { // strict: the first maximal edge wins (mdp.cpp:254-260)
+                        hi = qy;
+                        best = pe;
+                    }
+                    if (qx > lo) lo = qx;
+                }
+                if (m == 1) lo = 0.0; // V_0
+                xc[d] = make_double2(lo, hi);
+                A.values_out[row0 + r] = hi;
+                A.act_out[row0 + r] = best < 0 ? -1 : L.cloud[best];
+                const double dd = fabs(hi - lo);
+                dmax = dmax < dd ? dd : dmax;
+            }
+        } else { // ---- BFS walk (cert_implicit_layer's evaluation, pairs by key-space index) -------
+            const int words = L.words;
+            const double r_cloud = L.r_cloud_kept, r_paid = L.r_paid_kept;
+            const uint64_t n = Lp->n;
+            const uint64_t* keys = A.keys + Lp->key_off;
+#pragma unroll
+            for (int j = 0; j < JT; ++j) {
+                const uint64_t i = static_cast<uint64_t>(k) * kStreamT + j * kStreamThreads + tid;
+                if (i >= n) break;
+                uint64_t kk[WM];
+                if (WM <= 2) {
+#pragma unroll
+                    for (int w = 0; w < WM; ++w) kk[w] = kpre[j][w < KP ? w : 0];
+                } else {
+                    load_key<WM>(keys + i * static_cast<uint64_t>(words), words, kk);
+                }
+                const Slots sl = dec.decode(kk);
+                double2 x[SL];
+#pragma unroll
+                for (int e = 0; e < SL; ++e)
+                    if (sl.valid(e)) x[e] = __ldca(xn + dec.idx(sl, e));
+                double hi = -INFINITY, lo = -INFINITY;
+                int best = -1;
+#pragma unroll
+                for (int e = 0; e < SL; ++e) {
+                    if (!sl.valid(e)) continue;
+                    const int pe = e == SL - 1 ? -1 : e;
+                    const double rr = retires ? retiring_reward<WM>(kk, pe, L) : (pe < 0 ? r_paid : r_cloud);
+                    const double qx = DISC ? __dadd_rn(rr, __dmul_rn(A.discount, x[e].x)) : __dadd_rn(rr, x[e].x);
+                    const double qy = DISC ? __dadd_rn(rr, __dmul_rn(A.discount, x[e].y)) : __dadd_rn(rr, x[e].y);
+                    if (qy > hi) {
+                        hi = qy;
+                        best = pe;
+                    }
+                    if (qx > lo) lo = qx;
+                }
+                if (m == 1) lo = 0.0;
+                if (t >= 1) {
+                    uint32_t own = 0;
+                    for (int p = 0; p < L.n_active; ++p)
+                        own += static_cast<uint32_t>(get_field<WM>(kk, L.bit_off[p], L.width[p])) * L.wself[p];
+                    xc[own] = make_double2(lo, hi);
+                }
+                A.values_out[row0 + i] = hi;
+                A.act_out[row0 + i] = best < 0 ? -1 : L.cloud[best];
+                const double dd = fabs(hi - lo);
+                dmax = dmax < dd ? dd : dmax;
+            }
+        }
+#pragma unroll
+        for (int ofs = 16; ofs > 0; ofs >>= 1) {
+            const double other = __shfl_xor_sync(FULL, dmax, ofs);
+            dmax = dmax < other ? other : dmax;
+        }
+        if (lane == 0 && dmax > 0.0)
+            atomicMax(&s_lb, static_cast<unsigned long long>(__double_as_longlong(dmax)));
+        if (pf) { // (sLb[bb ^ 1] is not read by anyone this iteration)
+#pragma unroll
+            for (int q = 0; q < PPT; ++q) {
+                const int i = tid + q * kStreamThreads;
+                if (i < PW) reinterpret_cast<uint32_t*>(&sLb[bb ^ 1])[i] = pfw[q];
+            }
+        }
+        __syncthreads(); // the tile's stores are issued
+        if (tid == 0) {
+            if (s_lb) atomicMax(reinterpret_cast<unsigned long long*>(A.lb + m), s_lb);
+            __threadfence();
+            st_release_u32(flags + tile, 1u);
+            atomicAdd(done + o, 1u);
+        }
+    }
+}
+
 // K* = H+1 is proven iff lb_k >= eps for k = 1..H (and no sweep cap below H+1).  Sets the graph
 // conditional to run the wavefront fallback otherwise.
 __global__ void k_cert_check(const double* __restrict__ lb, int H, double eps, int max_sweeps,
@@ -1833,8 +2153,19 @@ uint64_t cert_half(const vcs_space* sp) {
         h = std::max<uint64_t>(h, sp->plan.layers[static_cast<size_t>(t - 1)].dense_size);
     return h;
 }
+bool cert_permute_layer(uint64_t key_space);
+// The persistent streaming pass (k_cert_stream, opt-in: VCS_CERT_STREAM=1) applies to key-space
+// spaces whose layers stay in L2 (the gather-pass layout of larger ones is per layer).
+// Measured on the B200 it is correct and deadlock-free but slower than the PDL-chained layer
+// launches: C4 0.75 vs 0.52 ms, C3 0.34 vs 0.18 ms.
+bool cert_stream_space(const vcs_space* sp) {
+    const char* e = std::getenv("VCS_CERT_STREAM");
+    if (!e || std::atoi(e) == 0) return false;
+    return cert_keyspace(sp) && !cert_permute_layer(cert_half(sp)) && sp->H >= 1;
+}
 uint64_t cert_pairs_needed(const vcs_space* sp) {
-    return cert_keyspace(sp) ? 2 * cert_half(sp) : sp->S;
+    // (the streaming pass rotates three buffers, the per-layer launches two)
+    return cert_keyspace(sp) ? (cert_stream_space(sp) ? 4 : 2) * cert_half(sp) : sp->S;
 }
 
 // Device pointers of the implicit form a certified layer reads (the space's own, or a replica
@@ -2102,6 +2433,56 @@ void launch_cert_layer(const vcs_space* sp, const CertData& data, const CertLaye
     });
 }
 
+// The streaming pass's per-layer table (processing order) and its sync words, built once per
+// space before any capture.
+void ensure_stream_plan(vcs_space* sp) {
+    if (sp->stream_meta.p && sp->stream_tiles) return;
+    const int H = sp->H;
+    const uint64_t half = cert_half(sp);
+    std::vector<StreamLayer> ly(static_cast<size_t>(H));
+    uint32_t tiles = 0;
+    for (int o = 0; o < H; ++o) {
+        const int t = H - 1 - o;
+        const CertLayer L = cert_layer(sp, t, nullptr, half, true);
+        StreamLayer& Y = ly[static_cast<size_t>(o)];
+        Y.row0 = L.row0;
+        Y.n = L.n;
+        Y.dense_n = L.dense_n;
+        Y.key_off = sp->key_off[static_cast<size_t>(t)];
+        Y.rank_self_off = t >= 1 ? sp->rank_off[static_cast<size_t>(t - 1)] : 0;
+        Y.m = H - t;
+        if (L.dense_order) {
+            // window deps need layer t+1 walked in the same key space (a key-space-walk layer
+            // of the same size) and a non-retiring transition
+            bool local = cert_nonretiring(sp, t) && o >= 1;
+            if (local) {
+                const CertLayer P = cert_layer(sp, t + 1, nullptr, half, true);
+                local = P.dense_order && P.dense_n == L.dense_n;
+            }
+            Y.kind = local ? 0 : 1;
+            Y.n_tiles = static_cast<uint32_t>((L.dense_n + kStreamT - 1) / kStreamT);
+            if (local) {
+                const LayerParam& P = sp->plan.layers[static_cast<size_t>(t)];
+                Y.n_shift = 0;
+                Y.shift[Y.n_shift++] = 0; // the paid successor: d itself
+                for (int p = 0; p < P.n_active && p < kDenseSlots - 1; ++p)
+                    if (P.attr[p]) Y.shift[Y.n_shift++] = static_cast<uint32_t>(P.demand) * P.wnext[p];
+            }
+        } else {
+            Y.kind = 2;
+            Y.n_tiles = static_cast<uint32_t>((L.n + kStreamT - 1) / kStreamT);
+        }
+        Y.tile_start = tiles;
+        tiles += Y.n_tiles;
+    }
+    const size_t bytes = ly.size() * sizeof(StreamLayer);
+    sp->stream_meta.exact(std::max<size_t>(bytes, 16), sp->stream);
+    sp->stream_sync.exact(static_cast<size_t>(tiles) + static_cast<size_t>(H) + 1, sp->stream);
+    VCS_CUDA(cudaMemcpyAsync(sp->stream_meta.p, ly.data(), bytes, cudaMemcpyHostToDevice, sp->stream));
+    VCS_CUDA(cudaStreamSynchronize(sp->stream));
+    sp->stream_tiles = tiles;
+}
+
 void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaStream_t s,
                       bool capturing) {
     const bool disc = is_discounted(key.discount);
@@ -2119,10 +2500,50 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
         const uint64_t rH = sp->layer_off[H], nH = sp->S - rH;
         VCS_CUDA(cudaMemsetAsync(sp->v[0].p + rH, 0, nH * sizeof(double), s));
         VCS_CUDA(cudaMemsetAsync(sp->actions_dev.p + rH, 0xff, nH * sizeof(int32_t), s));
-        if (ks) // the terminal layer's single state, key-space index 0
-            VCS_CUDA(cudaMemsetAsync(sp->cert_xd.p + (H & 1) * half, 0, sizeof(double2), s));
+        if (ks) // the terminal layer's single state, key-space index 0 (buffer H % 3 streaming)
+            VCS_CUDA(cudaMemsetAsync(sp->cert_xd.p + (key.stream_out == 0 && cert_stream_space(sp)
+                                                          ? (H % 4) : (H & 1)) * half,
+                                     0, sizeof(double2), s));
         else
             VCS_CUDA(cudaMemsetAsync(sp->cert_xd.p + rH, 0, nH * sizeof(double2), s)); // V_0 = 0
+    }
+    if (sp->implicit && ks && key.stream_out == 0 && cert_stream_space(sp) && sp->stream_tiles) {
+        // the whole pass as one persistent kernel (k_cert_stream)
+        VCS_CUDA(cudaMemsetAsync(sp->stream_sync.p, 0,
+                                 (static_cast<size_t>(sp->stream_tiles) + H + 1) * sizeof(uint32_t), s));
+        StreamArgs A{};
+        A.layers = reinterpret_cast<const StreamLayer*>(sp->stream_meta.p);
+        A.params = sp->params_dev.p;
+        A.keys = sp->keys.p;
+        A.rank_tables = sp->rank_tables.p;
+        A.xd = sp->cert_xd.p;
+        A.third = half;
+        A.values_out = sp->v[0].p;
+        A.act_out = sp->actions_dev.p;
+        A.lb = sp->cert_lb.p;
+        A.discount = key.discount;
+        A.sync = sp->stream_sync.p;
+        A.total_tiles = sp->stream_tiles;
+        A.H = H;
+        dispatch_words_solve(max_key_words(sp), [&](auto wm) {
+            constexpr int WM = decltype(wm)::value;
+            const void* fn = disc ? reinterpret_cast<const void*>(k_cert_stream<WM, true>)
+                                  : reinterpret_cast<const void*>(k_cert_stream<WM, false>);
+            int per_sm = 0;
+            VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kStreamThreads, 0));
+            const unsigned blocks = static_cast<unsigned>(std::max(1, per_sm) * sp->num_sms);
+            if (disc) k_cert_stream<WM, true><<<blocks, kStreamThreads, 0, s>>>(A);
+            else k_cert_stream<WM, false><<<blocks, kStreamThreads, 0, s>>>(A);
+            VCS_LAUNCHED();
+        });
+        k_cert_check<<<1, 64, 0, s>>>(sp->cert_lb.p, H, key.eps, key.max_sweeps, sp->ctrl.p, 0);
+        VCS_LAUNCHED();
+        record_event(g.ev[1], s, capturing);
+        record_event(g.ev[2], s, capturing);
+        g.launches = 2;
+        g.implicit = true;
+        g.fallback_at_collect = true;
+        return;
     }
     if (sp->implicit) { // implicit-CSR form: keys + rank tables; the fallback runs at collect
         const CertData data = cert_data_of(sp);
@@ -3015,6 +3436,8 @@ int enqueue_impl(vcs_space* sp, const vcs_solve_opts* opts, void* stream, int st
             sp->cert_lb.exact(static_cast<size_t>(sp->H) + 2, sp->stream);
             VCS_CUDA(cudaStreamSynchronize(sp->stream));
         }
+        if (method == VCS_METHOD_CERTIFIED && sp->implicit && vcs::cert_stream_space(sp))
+            vcs::ensure_stream_plan(sp);
         if (vcs::trace_enabled())
             std::fprintf(stderr, "[vcs solve] buffers %.3f ms\n", vcs::host_ms() - t0);
         const vcs::GraphKey key{o.epsilon, o.discount,

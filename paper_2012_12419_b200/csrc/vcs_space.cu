@@ -2159,6 +2159,8 @@ vcs_space::~vcs_space() {
     ver.release_idle();
     cert_xd.release_idle();
     cert_act_ks.release_idle();
+    stream_meta.release_idle();
+    stream_sync.release_idle();
     cert_lb.release_idle();
     band_ver.release_idle();
     ver_off.release_idle();

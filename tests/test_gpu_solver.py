@@ -778,3 +778,29 @@ def test_c7_kernel_variants_agree(gpu, monkeypatch):
         digests.append((sha(r.values.raw_values()), sha(r.policy.raw_actions())))
         del r, sp2
     assert digests[0] == digests[1] == digests[2]
+
+
+def test_certified_streaming_kernel_matches_golden(gpu, golden, monkeypatch):
+    """k_cert_stream (VCS_CERT_STREAM=1): the whole certified pass as one persistent kernel with
+    per-tile dependency flags (window deps on non-retiring transitions, whole-layer deps
+    otherwise, four rotating pair buffers) reproduces the reference's digests on C3, C4 and the
+    C5 sample points, and terminates (no tile waits on a later one)."""
+    import bench_workloads as W
+    monkeypatch.setenv("VCS_CERT_STREAM", "1")
+    for name in ("C3", "C4"):
+        p = V.load_instance(str(GOLDEN / "instances" / f"{name.lower()}.txt"))
+        sp = V.StateSpace.build_native(V.NativeInstance(p.vcc, bots=p.bots), 10**9)
+        g = golden["cases"][name]["eps=1e-06"]
+        for _ in range(2):  # direct first solve, then the captured graph
+            r = _solve(sp, method=N.VCS_METHOD_CERTIFIED)
+            assert sha(r.values.raw_values()) == g["values_sha"]
+            assert sha(r.policy.raw_actions()) == g["actions_sha"]
+    table = W.channel_table()
+    for key in [k for k in golden["cases"] if k.startswith("C5_")]:
+        _, K, c, scheme = key.split("_", 3)
+        p = V.parse_instance(W.c5_text(int(K[1:]), int(c[1:]), scheme, table))
+        sp = V.StateSpace.build_native(V.NativeInstance(p.vcc, bots=p.bots), 10**9)
+        r = _solve(sp, method=N.VCS_METHOD_CERTIFIED)
+        e = golden["cases"][key]["eps=1e-06"]
+        assert sha(r.values.raw_values()) == e["values_sha"], key
+        assert sha(r.policy.raw_actions()) == e["actions_sha"], key
