@@ -3340,7 +3340,10 @@ CachedGraph& enqueue_multi(vcs_space* sp, MultiState& ms, const GraphKey& key, c
     g.implicit = sp->implicit;
     g.fallback_at_collect = true;
     g.n_ranks = static_cast<int>(ms.ranks.size());
-    if (!g.exec && !ms.no_graph && !std::getenv("VCS_NO_GRAPH")) {
+    // the first solve of a space launches directly (a one-shot solve does not pay the capture
+    // and instantiation of the multi-device graph); the second captures it
+    if (!g.exec && !ms.no_graph && !std::getenv("VCS_NO_GRAPH") &&
+        (g.uses > 0 || std::getenv("VCS_GRAPH_FIRST"))) {
         cudaStream_t cs = sp->stream;
         if (cs != s) VCS_CUDA(cudaStreamSynchronize(s));
         VCS_CUDA(cudaSetDevice(sp->device));

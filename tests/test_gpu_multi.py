@@ -46,13 +46,14 @@ def test_multi_keyspace_matches_golden(gpu, golden, monkeypatch, name, gen):
     g = golden["cases"][name]["eps=1e-06"]
     for ranks in (2, 3, 8):
         for ex in (N.VCS_EXCHANGE_HALO, N.VCS_EXCHANGE_ALLGATHER):
-            vals, acts, rep, info = _multi(sp, ranks, exchange=ex)
-            assert rep.method == N.VCS_METHOD_CERTIFIED
-            assert rep.sweeps == g["sweeps"]
-            assert sha(vals) == g["values_sha"], (ranks, ex)
-            assert sha(acts) == g["actions_sha"], (ranks, ex)
-            assert info.n_ranks == ranks and info.split_layers > 0
-            assert info.graph == 1
+            for use in range(2):  # direct launches first, then the captured multi-device graph
+                vals, acts, rep, info = _multi(sp, ranks, exchange=ex)
+                assert rep.method == N.VCS_METHOD_CERTIFIED
+                assert rep.sweeps == g["sweeps"]
+                assert sha(vals) == g["values_sha"], (ranks, ex, use)
+                assert sha(acts) == g["actions_sha"], (ranks, ex, use)
+                assert info.n_ranks == ranks and info.split_layers > 0
+                assert info.graph == 1
         # the halo moves strictly less than the all-gather
         _, _, _, halo = _multi(sp, ranks, exchange=N.VCS_EXCHANGE_HALO)
         _, _, _, full = _multi(sp, ranks, exchange=N.VCS_EXCHANGE_ALLGATHER)
