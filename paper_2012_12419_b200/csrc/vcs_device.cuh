@@ -196,6 +196,9 @@ struct vcs_space {
     vcs::DevBuf<unsigned char> stream_meta; // k_cert_stream's per-layer table
     vcs::DevBuf<uint32_t> stream_sync;      // its tile flags, layer counters, work counter
     uint32_t stream_tiles = 0;
+    vcs::DevBuf<uint64_t> cert_tail_meta;   // k_cert_tail: row0 / n / key offset of layers 0..t
+    int cert_tail_t = -1;
+    bool cert_tail_ready = false;
     vcs::DevBuf<double> cert_lb;
     cudaStream_t aux_stream = nullptr; // captures the fallback body of the certified graph
     std::map<vcs::GraphKey, vcs::CachedGraph> graphs;

@@ -829,7 +829,7 @@ struct CertImplArgs {
 // One layer of the implicit certified pass over states first_i, first_i + stride, ... (the
 // block has loaded the layer's LayerParam into sL and zeroed s_lb).  DXD: the pairs are stored
 // by key-space index (one gather per edge, no rank-table hop); otherwise by BFS index.
-template <int WM, bool DISC, bool DXD>
+template <int WM, bool DISC, bool DXD, bool COHERENT = false>
 __device__ __forceinline__ void cert_implicit_layer(const CertImplArgs& a, const LayerParam& L,
                                                     unsigned long long& s_lb, uint64_t first_i,
                                                     uint64_t stride) {
@@ -856,7 +856,8 @@ __device__ __forceinline__ void cert_implicit_layer(const CertImplArgs& a, const
         if (DXD) {
 #pragma unroll
             for (int e = 0; e < SL; ++e)
-                if (sl.valid(e)) x[e] = __ldg(a.xd_next + dec.idx(sl, e));
+                if (sl.valid(e)) // (COHERENT: written earlier in this kernel, read from L2)
+                    x[e] = COHERENT ? __ldcg(a.xd_next + dec.idx(sl, e)) : __ldg(a.xd_next + dec.idx(sl, e));
         } else {
             uint32_t rk[SL];
 #pragma unroll
@@ -1171,6 +1172,35 @@ __global__ void __launch_bounds__(256, MINB) k_cert_implicit(CertImplArgs a) {
     cert_implicit_layer<WM, DISC, DXD>(a, sL, s_lb,
                                        static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x,
                                        static_cast<uint64_t>(gridDim.x) * blockDim.x);
+}
+
+// The small sparse layers at the bottom of the pass (C4: layers 0-6, 1 to 4,704 states) in ONE
+// block: a block barrier per layer instead of a kernel launch.  Per state cert_implicit_layer's
+// evaluation (pairs by key-space index, read through L2: the previous layer wrote them in this
+// kernel).  `meta`: per layer t <= t_hi its row0 / n / key offset (3 x u64).
+constexpr int kTailThreads = 512;
+constexpr uint64_t kTailMaxStates = 8192;
+
+template <int WM, bool DISC>
+__global__ void __launch_bounds__(kTailThreads, 1) k_cert_tail(CertImplArgs a, const uint64_t* meta,
+                                                              const uint64_t* keys,
+                                                              const LayerParam* params, double2* xd,
+                                                              uint64_t half, int t_hi, int H) {
+    __shared__ LayerParam sL;
+    __shared__ unsigned long long s_lb;
+    for (int t = t_hi; t >= 0; --t) {
+        load_layer_param(sL, params + t, s_lb); // (its barriers also order the layers)
+        CertImplArgs c = a;
+        c.row0 = meta[3 * t];
+        c.n = meta[3 * t + 1];
+        c.keys = keys + meta[3 * t + 2];
+        c.m = H - t;
+        c.xd_next = xd + ((t + 1) & 1) * half;
+        c.xd_cur = xd + (t & 1) * half;
+        c.write_own = t >= 1 ? 1 : 0;
+        cert_implicit_layer<WM, DISC, true, true>(c, sL, s_lb, threadIdx.x, blockDim.x);
+        __syncthreads(); // this layer's pairs are written before the next layer reads them
+    }
 }
 
 template <int WM, bool DISC, int MINB>
@@ -2433,6 +2463,37 @@ void launch_cert_layer(const vcs_space* sp, const CertData& data, const CertLaye
     });
 }
 
+// The bottom run of small sparse layers that k_cert_tail takes (every layer 0..t_tail walks its
+// states, none has more than kTailMaxStates), and their row / key offsets on the device; built
+// once per space before any capture.  cert_tail_t = -1: no tail.
+void ensure_cert_tail(vcs_space* sp) {
+    if (sp->cert_tail_ready) return;
+    sp->cert_tail_ready = true;
+    sp->cert_tail_t = -1;
+    // (opt-in, VCS_CERT_TAIL=1: measured slower on the B200 — C4 0.543 vs 0.518 ms; the
+    // PDL-chained launches of those layers overlap better than one block walking them)
+    if (!cert_keyspace(sp) || !std::getenv("VCS_CERT_TAIL")) return;
+    const uint64_t half = cert_half(sp);
+    int t_tail = -1;
+    for (int t = 0; t < sp->H; ++t) {
+        const CertLayer L = cert_layer(sp, t, nullptr, half, true);
+        if (L.dense_order || L.n > kTailMaxStates) break;
+        t_tail = t;
+    }
+    if (t_tail < 1) return; // a single layer gains nothing
+    std::vector<uint64_t> meta(3 * (static_cast<size_t>(t_tail) + 1));
+    for (int t = 0; t <= t_tail; ++t) {
+        meta[3 * t] = sp->layer_off[static_cast<size_t>(t)];
+        meta[3 * t + 1] = sp->layer_off[static_cast<size_t>(t) + 1] - sp->layer_off[static_cast<size_t>(t)];
+        meta[3 * t + 2] = sp->key_off[static_cast<size_t>(t)];
+    }
+    sp->cert_tail_meta.exact(meta.size(), sp->stream);
+    VCS_CUDA(cudaMemcpyAsync(sp->cert_tail_meta.p, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice,
+                             sp->stream));
+    VCS_CUDA(cudaStreamSynchronize(sp->stream));
+    sp->cert_tail_t = t_tail;
+}
+
 // The streaming pass's per-layer table (processing order) and its sync words, built once per
 // space before any capture.
 void ensure_stream_plan(vcs_space* sp) {
@@ -2549,7 +2610,31 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
         const CertData data = cert_data_of(sp);
         int launches = 0;
         const bool pdl = g.layer_ev.empty() && !std::getenv("VCS_NO_PDL");
+        // the small sparse layers at the bottom run as one single-block launch (k_cert_tail)
+        const int t_tail = ks ? sp->cert_tail_t : -1;
         for (int t = H - 1; t >= 0; --t) {
+            if (t == t_tail) {
+                CertImplArgs c{};
+                c.values_out = sp->v[0].p;
+                c.act_out = sp->actions_dev.p;
+                c.lb = sp->cert_lb.p;
+                c.discount = key.discount;
+                c.write_out = 1;
+                dispatch_words_solve(max_key_words(sp), [&](auto wm) {
+                    constexpr int WM = decltype(wm)::value;
+                    if (disc)
+                        k_cert_tail<WM, true><<<1, kTailThreads, 0, s>>>(
+                            c, sp->cert_tail_meta.p, sp->keys.p, sp->params_dev.p, sp->cert_xd.p, half, t, H);
+                    else
+                        k_cert_tail<WM, false><<<1, kTailThreads, 0, s>>>(
+                            c, sp->cert_tail_meta.p, sp->keys.p, sp->params_dev.p, sp->cert_xd.p, half, t, H);
+                    VCS_LAUNCHED();
+                });
+                ++launches;
+                if (!g.layer_ev.empty())
+                    for (int u = t; u >= 0; --u) record_event(g.layer_ev[static_cast<size_t>(u)], s, capturing);
+                break;
+            }
             CertLayer L = cert_layer(sp, t, sp->cert_xd.p, half, ks);
             L.d_hi = L.dense_order ? L.dense_n : 0;
             if (L.n) {
@@ -3441,6 +3526,7 @@ int enqueue_impl(vcs_space* sp, const vcs_solve_opts* opts, void* stream, int st
         }
         if (method == VCS_METHOD_CERTIFIED && sp->implicit && vcs::cert_stream_space(sp))
             vcs::ensure_stream_plan(sp);
+        if (method == VCS_METHOD_CERTIFIED && sp->implicit) vcs::ensure_cert_tail(sp);
         if (vcs::trace_enabled())
             std::fprintf(stderr, "[vcs solve] buffers %.3f ms\n", vcs::host_ms() - t0);
         const vcs::GraphKey key{o.epsilon, o.discount,

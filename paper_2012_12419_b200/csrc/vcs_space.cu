@@ -2161,6 +2161,7 @@ vcs_space::~vcs_space() {
     cert_act_ks.release_idle();
     stream_meta.release_idle();
     stream_sync.release_idle();
+    cert_tail_meta.release_idle();
     cert_lb.release_idle();
     band_ver.release_idle();
     ver_off.release_idle();

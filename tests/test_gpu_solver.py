@@ -804,3 +804,17 @@ def test_certified_streaming_kernel_matches_golden(gpu, golden, monkeypatch):
         e = golden["cases"][key]["eps=1e-06"]
         assert sha(r.values.raw_values()) == e["values_sha"], key
         assert sha(r.policy.raw_actions()) == e["actions_sha"], key
+
+
+def test_certified_tail_kernel_matches_golden(gpu, golden, monkeypatch):
+    """k_cert_tail (VCS_CERT_TAIL=1: the small sparse bottom layers in one block) gives the
+    reference's bits on C3 and C4."""
+    monkeypatch.setenv("VCS_CERT_TAIL", "1")
+    for name in ("C3", "C4"):
+        p = V.load_instance(str(GOLDEN / "instances" / f"{name.lower()}.txt"))
+        sp = V.StateSpace.build_native(V.NativeInstance(p.vcc, bots=p.bots), 10**9)
+        g = golden["cases"][name]["eps=1e-06"]
+        for _ in range(2):
+            r = _solve(sp, method=N.VCS_METHOD_CERTIFIED)
+            assert sha(r.values.raw_values()) == g["values_sha"]
+            assert sha(r.policy.raw_actions()) == g["actions_sha"]
