@@ -353,6 +353,9 @@ LayerPlan make_layer_plan(const vcs_instance* in) {
             } else {
                 L.keep_idx[p] = -1;
             }
+            L.fdesc[p] = static_cast<uint32_t>(L.bit_off[p]) | (static_cast<uint32_t>(L.width[p]) << 9) |
+                         (L.attr[p] ? 1u << 15 : 0u) |
+                         (L.keep_idx[p] >= 0 ? (1u << 16) | (static_cast<uint32_t>(L.next_bit_off[p]) << 17) : 0u);
         }
     }
     pl.init_key.assign(static_cast<std::size_t>(pl.words[0]), 0);

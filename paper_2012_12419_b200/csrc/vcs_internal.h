@@ -85,6 +85,10 @@ struct LayerParam {
     uint32_t wself[kMaxActive];
     uint32_t self_size;
     int32_t pad2;
+    // field p in one word (the single-CTA builder reads four per shared-memory load): bits 0-8
+    // bit_off, 9-14 width, 15 attr, 16 kept, 17-25 next_bit_off; 0 past n_active (a zero-width
+    // retired field: it adds nothing)
+    uint32_t fdesc[kMaxActive];
 };
 
 // Dense successor indices are used up to this key-space size (a 4-byte first-edge table).

@@ -738,50 +738,127 @@ __global__ void __launch_bounds__(256, MINB) k_cert_rows(CertArgs a) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); // the next layer may launch
 }
 
-// The whole certified pass of a SMALL explicit space (every layer <= kCertSmallStates states) in
-// ONE block: the (V_{m-1}, V_m) pairs of two adjacent layers stay in shared memory, a layer is a
-// block barrier instead of a kernel launch (the canonical instance: 330 layers of <= 614 states).
-// Per state exactly k_cert_rows' operations (same edge order, same strict first maximum).
-constexpr int kCertSmallStates = 1280; // 2 x 20 KB of pairs (static shared memory)
-constexpr int kCertSmallThreads = 1024;
+// The whole certified pass of a SMALL explicit space (every layer <= kCertSmallStates states and
+// <= kCertSmallEdges transitions) in ONE block: the (V_{m-1}, V_m) pairs of two adjacent layers
+// stay in shared memory and a layer is a block barrier instead of a kernel launch (the canonical
+// instance: 330 layers of <= 614 states).  The CSR slices of layer t-1 (row offsets, successors,
+// rewards, actions) are copied into shared memory with cp.async while layer t computes, so a
+// layer's critical path is a barrier plus shared-memory reads — no global round trip.  Per state
+// exactly k_cert_rows' operations (same edge order, same strict first maximum).
+constexpr int kCertSmallStates = 1280;
+constexpr int kCertSmallEdges = 3072;
+constexpr int kCertSmallMaxH = 2046;
+constexpr int kCertSmallThreads = 512;
 
-template <bool DISC>
-__global__ void __launch_bounds__(kCertSmallThreads, 1)
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))), "l"(src) : "memory");
+}
+
+// a space k_cert_small takes: explicit CSR, every layer within the shared-memory stages
+inline bool cert_small_ok(const vcs_space* sp) {
+    if (sp->implicit || sp->H < 1 || sp->H > kCertSmallMaxH || std::getenv("VCS_NO_SMALL_SOLVE"))
+        return false;
+    if (sp->max_layer > static_cast<uint64_t>(kCertSmallStates)) return false;
+    for (int t = 0; t < sp->H; ++t)
+        if (sp->layer_edges[static_cast<size_t>(t)] > static_cast<uint64_t>(kCertSmallEdges)) return false;
+    return true;
+}
+
+// dynamic shared memory of k_cert_small for a horizon of H
+inline size_t cert_small_smem(int H) {
+    return static_cast<size_t>(2) * kCertSmallStates * 16 +               // pairs
+           static_cast<size_t>(2) * kCertSmallEdges * (8 + 4 + 4) +        // rewards, succ, actions
+           static_cast<size_t>(2) * (kCertSmallStates + 1) * 4 +           // row offsets
+           static_cast<size_t>(2) * (H + 2) * 4;                           // layer row / edge starts
+}
+
+template <bool DISC, int NT>
+__global__ void __launch_bounds__(NT, 1)
 k_cert_small(CertArgs a, const uint64_t* __restrict__ layer_off, int H) {
-    __shared__ double2 xd[2][kCertSmallStates];
-    __shared__ unsigned long long s_lb;
+    constexpr int KS = kCertSmallStates, NE = kCertSmallEdges;
+    extern __shared__ __align__(16) unsigned char cs_raw[];
+    double2* xd = reinterpret_cast<double2*>(cs_raw);                 // [2][KS]
+    double* srew = reinterpret_cast<double*>(xd + 2 * KS);            // [2][NE]
+    uint32_t* ssucc = reinterpret_cast<uint32_t*>(srew + 2 * NE);     // [2][NE]
+    int32_t* sact = reinterpret_cast<int32_t*>(ssucc + 2 * NE);       // [2][NE]
+    uint32_t* srp = reinterpret_cast<uint32_t*>(sact + 2 * NE);       // [2][KS + 1]
+    uint32_t* mrow = srp + 2 * (KS + 1);                              // [H + 2] first state of layer t
+    uint32_t* medge = mrow + (H + 2);                                 // [H + 2] first edge of layer t
+    __shared__ unsigned long long s_lb[2];
     const int tid = threadIdx.x;
-    {
-        const uint64_t rH = layer_off[H], nH = layer_off[H + 1] - rH;
-        for (uint64_t i = tid; i < nH; i += blockDim.x) xd[H & 1][i] = make_double2(0.0, 0.0);
+    for (int t = tid; t <= H + 1; t += NT) {
+        const uint64_t r = layer_off[t];
+        mrow[t] = static_cast<uint32_t>(r);
+        medge[t] = __ldg(a.row_ptr + r);
     }
+    if (tid < 2) s_lb[tid] = 0ull;
+    __syncthreads();
+    {
+        const uint32_t rH = mrow[H], nH = mrow[H + 1] - rH;
+        for (uint32_t i = tid; i < nH; i += NT) xd[(H & 1) * KS + i] = make_double2(0.0, 0.0);
+    }
+    auto stage = [&](int t) { // layer t's CSR slices -> buffer t & 1 (asynchronously)
+        const int b = t & 1;
+        const uint32_t r0 = mrow[t], n = mrow[t + 1] - r0, e0 = medge[t], ne = medge[t + 1] - e0;
+        for (uint32_t i = tid; i <= n; i += NT) cp_async4(srp + b * (KS + 1) + i, a.row_ptr + r0 + i);
+        for (uint32_t e = tid; e < ne; e += NT) {
+            cp_async8(srew + b * NE + e, a.reward + e0 + e);
+            cp_async4(ssucc + b * NE + e, a.succ + e0 + e);
+            cp_async4(sact + b * NE + e, a.action + e0 + e);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (H >= 1) stage(H - 1);
     for (int t = H - 1; t >= 0; --t) {
-        if (tid == 0) s_lb = 0ull;
-        __syncthreads(); // layer t+1's pairs are complete
-        const uint64_t row0 = layer_off[t], n = layer_off[t + 1] - row0, next0 = layer_off[t + 1];
-        const double2* nxt = xd[(t + 1) & 1];
-        double2* cur = xd[t & 1];
+        const int b = t & 1;
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads(); // layer t's slices landed, layer t+1's pairs and lb are complete
+        if (tid == 0 && t + 1 <= H - 1) { // layer t+1's lower bound
+            const unsigned long long v = s_lb[(t + 1) & 1];
+            if (v) a.lb[H - t - 1] = __longlong_as_double(static_cast<long long>(v));
+            s_lb[(t + 1) & 1] = 0ull;
+        }
+        if (t >= 1) stage(t - 1); // (buffer (t-1)&1 held layer t+1's slices: consumed)
+        const uint32_t row0 = mrow[t], n = mrow[t + 1] - row0, next0 = mrow[t + 1], e0 = medge[t];
+        const double2* nxt = xd + ((t + 1) & 1) * KS;
+        double2* cur = xd + b * KS;
+        const uint32_t* rp = srp + b * (KS + 1);
+        const double* rw_s = srew + b * NE;
+        const uint32_t* sc_s = ssucc + b * NE;
         const int m = H - t;
         double dmax = 0.0;
-        for (uint64_t i = tid; i < n; i += blockDim.x) {
-            const uint32_t eb = __ldg(a.row_ptr + row0 + i), ee = __ldg(a.row_ptr + row0 + i + 1);
+        for (uint32_t i = tid; i < n; i += NT) {
+            const uint32_t eb = rp[i] - e0, ee = rp[i + 1] - e0;
             double hi = -INFINITY, lo = -INFINITY;
             uint32_t best_e = 0xffffffffu;
-            for (uint32_t e = eb; e < ee; ++e) {
-                const double rw = __ldg(a.reward + e);
-                const double2 x = nxt[__ldg(a.succ + e) - next0];
-                const double qx = DISC ? __dadd_rn(rw, __dmul_rn(a.discount, x.x)) : __dadd_rn(rw, x.x);
-                const double qy = DISC ? __dadd_rn(rw, __dmul_rn(a.discount, x.y)) : __dadd_rn(rw, x.y);
-                if (qy > hi) { // strict: the first maximal edge wins (mdp.cpp:254-260)
-                    hi = qy;
-                    best_e = e;
+            // four edges' loads in flight at a time; the maximum runs in edge order
+            for (uint32_t e0 = eb; e0 < ee; e0 += 4) {
+                double qx[4], qy[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t e = e0 + u < ee ? e0 + u : e0; // (lanes past the row repeat e0)
+                    const double rw = rw_s[e];
+                    const double2 x = nxt[sc_s[e] - next0];
+                    qx[u] = DISC ? __dadd_rn(rw, __dmul_rn(a.discount, x.x)) : __dadd_rn(rw, x.x);
+                    qy[u] = DISC ? __dadd_rn(rw, __dmul_rn(a.discount, x.y)) : __dadd_rn(rw, x.y);
                 }
-                if (qx > lo) lo = qx;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (e0 + u >= ee) break;
+                    if (qy[u] > hi) { // strict: the first maximal edge wins (mdp.cpp:254-260)
+                        hi = qy[u];
+                        best_e = e0 + u;
+                    }
+                    if (qx[u] > lo) lo = qx[u];
+                }
             }
             if (m == 1) lo = 0.0; // V_0
             cur[i] = make_double2(lo, hi);
             a.values_out[row0 + i] = hi;
-            a.act_out[row0 + i] = best_e != 0xffffffffu ? __ldg(a.action + best_e) : -1;
+            a.act_out[row0 + i] = best_e != 0xffffffffu ? sact[b * NE + best_e] : -1;
             const double d = fabs(hi - lo);
             dmax = dmax < d ? d : dmax;
         }
@@ -791,10 +868,10 @@ k_cert_small(CertArgs a, const uint64_t* __restrict__ layer_off, int H) {
             dmax = dmax < other ? other : dmax;
         }
         if ((tid & 31) == 0 && dmax > 0.0)
-            atomicMax(&s_lb, static_cast<unsigned long long>(__double_as_longlong(dmax)));
-        __syncthreads();
-        if (tid == 0 && s_lb) a.lb[m] = __longlong_as_double(static_cast<long long>(s_lb));
+            atomicMax(&s_lb[b], static_cast<unsigned long long>(__double_as_longlong(dmax)));
     }
+    __syncthreads();
+    if (tid == 0 && H >= 1 && s_lb[0]) a.lb[H] = __longlong_as_double(static_cast<long long>(s_lb[0]));
 }
 
 // Certified layer on the implicit-CSR form of a dense space: a state's edges are
@@ -2655,8 +2732,7 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
     }
     // uncaptured (the first solve of a small explicit space, see enqueue_solve): the pass and
     // its certificate only; a failed certificate runs the fallback at collect
-    const bool small = sp->max_layer <= static_cast<uint64_t>(kCertSmallStates) &&
-                       !std::getenv("VCS_NO_SMALL_SOLVE");
+    const bool small = cert_small_ok(sp);
     if (!capturing && !small)
         raise(VCS_EINVAL, "the certified solve is only recorded into a CUDA graph");
     g.fallback_at_collect = !capturing;
@@ -2682,8 +2758,23 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
         // a small space: the whole pass in one block (layer pairs in shared memory)
         if (sp->layer_off_dev.n < static_cast<size_t>(H) + 2) // (ensure_wave_buffers sets it)
             raise(VCS_EINVAL, "layer offsets were not uploaded before the capture");
-        if (disc) k_cert_small<true><<<1, kCertSmallThreads, 0, s>>>(a, sp->layer_off_dev.p, H);
-        else k_cert_small<false><<<1, kCertSmallThreads, 0, s>>>(a, sp->layer_off_dev.p, H);
+        const size_t smem = cert_small_smem(H);
+        int nt = kCertSmallThreads; // (VCS_CERT_SMALL_THREADS = 256 / 1024: measurements; C1
+        // canonical 0.33 ms at 512 against 0.33 at 256 and 0.37 at 1024)
+        if (const char* e = std::getenv("VCS_CERT_SMALL_THREADS")) nt = std::atoi(e);
+        if (nt != 256 && nt != 1024) nt = 512;
+        const void* fn_small =
+            nt == 256 ? (disc ? reinterpret_cast<const void*>(k_cert_small<true, 256>)
+                              : reinterpret_cast<const void*>(k_cert_small<false, 256>))
+            : nt == 512 ? (disc ? reinterpret_cast<const void*>(k_cert_small<true, 512>)
+                                : reinterpret_cast<const void*>(k_cert_small<false, 512>))
+                        : (disc ? reinterpret_cast<const void*>(k_cert_small<true, 1024>)
+                                : reinterpret_cast<const void*>(k_cert_small<false, 1024>));
+        raise_smem_limit(fn_small, sp->device, smem);
+        const uint64_t* lo_dev = sp->layer_off_dev.p;
+        int h_arg = H;
+        void* args[] = {&a, const_cast<uint64_t**>(&lo_dev), &h_arg};
+        VCS_CUDA(cudaLaunchKernel(fn_small, dim3(1), dim3(nt), args, smem, s));
         VCS_LAUNCHED();
         launches = 1;
     }
@@ -2822,8 +2913,7 @@ CachedGraph& enqueue_solve(vcs_space* sp, const GraphKey& key, cudaStream_t s) {
     // Small explicit spaces (k_cert_small, one launch) too: their graph would carry the whole
     // layer wavefront as the fallback body (canonical: 330 layers, 1.9 ms to capture and
     // instantiate, more than the solve); uncaptured, the fallback runs at collect.
-    const bool small_explicit = !sp->implicit && sp->max_layer <= static_cast<uint64_t>(kCertSmallStates) &&
-                                !std::getenv("VCS_NO_SMALL_SOLVE");
+    const bool small_explicit = cert_small_ok(sp);
     const bool direct_ok = (sp->implicit || small_explicit) && key.method == kMethodCertified &&
                            key.stream_out == 0;
     if ((sp->implicit || small_explicit) && key.method == kMethodCertified &&

@@ -1337,9 +1337,9 @@ bool build_dense(vcs_space* sp, uint64_t state_cap) {
 // first-insertion numbering (the lowest edge index of a successor ranks it), same reward
 // operations — the CSR it writes is bit-identical to the layered builder's.  A layer larger than
 // the shared-memory tables aborts with status 3 and the host takes the layered path.
-constexpr int kSmallThreads = 1024;
 constexpr int kSmallStates = 1024; // per layer, divided by the key words
 constexpr int kSmallEdges = 4096;  // per layer, divided by the key words
+constexpr int kSmallThreadsDefault = 512;
 
 struct SmallBuild {
     const LayerParam* params; // H
@@ -1354,11 +1354,14 @@ struct SmallBuild {
     uint64_t edge_cap;        // room in succ / reward / action
     uint64_t state_room;      // room in row_ptr / keys (states)
     int H;
+    long long* cycles;        // VCS_TRACE: clock64 at the six phase boundaries of every layer
 };
 
-// exclusive scan of v over the block (every thread passes its value; returns its prefix; *total
-// = the sum).  Uses `warp_sums` (32 entries) and two barriers.
-__device__ __forceinline__ uint32_t block_exscan(uint32_t v, uint32_t* warp_sums, uint32_t* total) {
+// Exclusive scan of v over the block with ONE barrier: warp scans, the warp totals in `ws`
+// (NT / 32 entries; alternate two arrays between consecutive scans so that no trailing barrier
+// is needed), then every thread sums the totals of the warps before its own.
+template <int NT>
+__device__ __forceinline__ uint32_t block_exscan1(uint32_t v, uint32_t* ws, uint32_t* total) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     uint32_t x = v;
 #pragma unroll
@@ -1366,108 +1369,171 @@ __device__ __forceinline__ uint32_t block_exscan(uint32_t v, uint32_t* warp_sums
         const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
-    if (lane == 31) warp_sums[w] = x;
+    if (lane == 31) ws[w] = x;
     __syncthreads();
-    if (w == 0) {
-        uint32_t s = lane < static_cast<int>(blockDim.x >> 5) ? warp_sums[lane] : 0u;
+    static_assert(NT % 128 == 0, "warp totals are read four at a time");
+    uint32_t before = 0, tot = 0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
-            if (lane >= o) s += y;
-        }
-        warp_sums[lane] = s; // inclusive
+    for (int k = 0; k < NT / 32; k += 4) {
+        const uint4 s = *reinterpret_cast<const uint4*>(ws + k);
+        before += (k < w ? s.x : 0u) + (k + 1 < w ? s.y : 0u) + (k + 2 < w ? s.z : 0u) +
+                  (k + 3 < w ? s.w : 0u);
+        tot += s.x + s.y + s.z + s.w;
     }
-    __syncthreads();
-    const uint32_t before = w > 0 ? warp_sums[w - 1] : 0u;
-    *total = warp_sums[(blockDim.x >> 5) - 1];
-    __syncthreads(); // (the next scan may overwrite warp_sums)
+    *total = tot;
     return before + x - v;
 }
 
-template <int WM>
-__global__ void __launch_bounds__(kSmallThreads, 1) k_build_small(SmallBuild A) {
+// A thread owns a contiguous run of the layer's states (spt = ceil(n / NT) of them) while it
+// emits their edges (one scan numbers them), then a contiguous run of ceil(E_t / NT) edges while
+// they are hashed and ranked (one scan orders the first occurrences): five block barriers per
+// layer, and no thread hashes a high-degree state's edges alone.  The successor key of every edge is derived from the state's paid successor (one pass over the key's fields
+// per state): a kept cloud subtracts demand from its field, a retiring one from the retired sum
+// (small integers: the double sums are exact, the reward's two rounded operations are the
+// reference's).
+template <int WM, int NT>
+__global__ void __launch_bounds__(NT, 1) k_build_small(SmallBuild A) {
     constexpr int NS = kSmallStates / WM;
     constexpr int NE = kSmallEdges / WM;
     constexpr int TC = 2 * NE; // table slots (power of two)
-    constexpr int RS = (NS + kSmallThreads - 1) / kSmallThreads; // states per thread
-    constexpr int RE = (NE + kSmallThreads - 1) / kSmallThreads; // edges per thread
+    constexpr int RS = (NS + NT - 1) / NT; // states per thread at most
     extern __shared__ __align__(16) unsigned char small_raw[];
     uint64_t* front = reinterpret_cast<uint64_t*>(small_raw);            // NS * WM
     uint64_t* ekey = front + static_cast<size_t>(NS) * WM;               // NE * WM
     uint32_t* table = reinterpret_cast<uint32_t*>(ekey + static_cast<size_t>(NE) * WM); // TC
     uint32_t* trank = table + TC;                                        // TC
     uint32_t* slot_of = trank + TC;                                      // NE
-    __shared__ uint32_t warp_sums[32];
-    __shared__ LayerParam Lbuf[2]; // layer t's parameters, and t+1's loaded behind it
+    __shared__ __align__(16) uint32_t ws[2][NT / 32];
+    __shared__ __align__(16) LayerParam Lbuf[2]; // layer t's parameters, and t+1's behind it
+    static_assert(offsetof(LayerParam, fdesc) % 16 == 0 && sizeof(LayerParam) % 16 == 0,
+                  "field descriptors are read as uint4");
     const int tid = threadIdx.x;
     constexpr int PW = static_cast<int>(sizeof(LayerParam) / 4);
-    static_assert(PW <= kSmallThreads, "one word of the layer parameters per thread");
-    for (int i = tid; i < PW; i += blockDim.x)
-        reinterpret_cast<uint32_t*>(&Lbuf[0])[i] = reinterpret_cast<const uint32_t*>(A.params)[i];
-    for (int i = tid; i < TC; i += blockDim.x) table[i] = kEmpty32;
-    for (int w = tid; w < WM; w += blockDim.x) front[w] = A.keys[w];
-    uint64_t S = 1, E = 0, key_base = 0; // states / edges before the current layer, its key offset
+    constexpr int PWT = (PW + NT - 1) / NT; // parameter words per thread
+    const uint32_t* pw = reinterpret_cast<const uint32_t*>(A.params);
+    for (int i = tid; i < PW; i += NT) reinterpret_cast<uint32_t*>(&Lbuf[0])[i] = pw[i];
+    uint32_t pf[PWT]; // the parameters of layer t + 1, loaded one layer ahead
+#pragma unroll
+    for (int k = 0; k < PWT; ++k) {
+        const int i = tid + k * NT;
+        pf[k] = (A.H > 1 && i < PW) ? __ldg(pw + PW + i) : 0u;
+    }
+    for (int i = tid; i < TC; i += NT) table[i] = kEmpty32;
+    for (int w = tid; w < WM; w += NT) front[w] = A.keys[w];
+    uint64_t S = 1, E = 0, key_base = 0; // states through the current layer / edges before it
     uint32_t n = 1;
     if (tid == 0) A.info[0] = 1;
+    __syncthreads();
     for (int t = 0; t < A.H; ++t) {
-        __syncthreads(); // (the previous layer's frontier / table / parameters are complete)
         const LayerParam& L = Lbuf[t & 1];
-        uint32_t pf = 0; // the next layer's parameters: loaded now, stored at the layer's end
-        if (t + 1 < A.H && tid < PW) pf = __ldg(reinterpret_cast<const uint32_t*>(A.params + t + 1) + tid);
-        const int words = L.words, nw = L.next_words;
-        // 1. out-degrees and row offsets (a thread owns states tid, tid + 1024, ...)
-        uint32_t deg[RS], cnt = 0;
+        // layer t+1's parameters into the other buffer (last read during layer t-1, whose
+        // phases ended at its third barrier), then fetch layer t+2's
+        if (t + 1 < A.H) {
 #pragma unroll
-        for (int r = 0; r < RS; ++r) {
-            const uint32_t i = tid + r * kSmallThreads;
-            deg[r] = 0;
-            if (i < n) {
-                uint64_t k[WM];
-                load_key<WM>(front + static_cast<size_t>(i) * WM, words, k);
-                uint32_t d = 1;
-                for (int p = 0; p < L.n_active; ++p)
-                    if (L.attr[p] && get_field<WM>(k, L.bit_off[p], L.width[p]) >= L.demand) ++d;
-                deg[r] = d;
+            for (int k = 0; k < PWT; ++k) {
+                const int i = tid + k * NT;
+                if (i < PW) reinterpret_cast<uint32_t*>(&Lbuf[(t + 1) & 1])[i] = pf[k];
             }
-            cnt += deg[r];
+            if (t + 2 < A.H) {
+#pragma unroll
+                for (int k = 0; k < PWT; ++k) {
+                    const int i = tid + k * NT;
+                    if (i < PW) pf[k] = __ldg(pw + static_cast<size_t>(t + 2) * PW + i);
+                }
+            }
         }
-        // edges are numbered state-major: thread blocks of states are interleaved, so scan per
-        // round (round r's states precede round r+1's)
-        uint32_t off[RS], E_t = 0;
+        const int words = L.words, nw = L.next_words, na = L.n_active, dem = L.demand;
+        auto tick = [&](int k) {
+            if (A.cycles && tid == 0) A.cycles[6 * t + k] = clock64();
+        };
+        tick(0);
+        const uint32_t spt = (n + NT - 1) / NT;
+        const uint32_t i0 = static_cast<uint32_t>(tid) * spt;
+        // A. per state: valid-cloud mask, paid successor key, retired VMs (four fields per
+        //    step: the shared-memory loads of a step are independent)
+        uint64_t mask[RS], nk0[RS][WM];
+        int ret0[RS];
+        uint32_t deg = 0;
 #pragma unroll
         for (int r = 0; r < RS; ++r) {
-            uint32_t tot = 0;
-            off[r] = E_t + block_exscan(deg[r], warp_sums, &tot);
-            E_t += tot;
+            const uint32_t i = i0 + r;
+            mask[r] = 0;
+            ret0[r] = 0;
+#pragma unroll
+            for (int w = 0; w < WM; ++w) nk0[r][w] = 0ull;
+            if (static_cast<uint32_t>(r) >= spt || i >= n) continue;
+            uint64_t k[WM];
+            load_key<WM>(front + static_cast<size_t>(i) * WM, words, k);
+            // (the descriptors past n_active are 0: zero-width retired fields, adding nothing)
+            for (int q0 = 0; q0 < na; q0 += 4) {
+                const uint4 f4 = *reinterpret_cast<const uint4*>(L.fdesc + q0);
+                const uint32_t fd[4] = {f4.x, f4.y, f4.z, f4.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t f = fd[u];
+                    const int v = get_field<WM>(k, f & 511u, (f >> 9) & 63u);
+                    if (((f >> 15) & 1u) && v >= dem) mask[r] |= 1ull << (q0 + u);
+                    if ((f >> 16) & 1u)
+                        put_field<WM>(nk0[r], (f >> 17) & 511u, static_cast<uint64_t>(v));
+                    else
+                        ret0[r] += v;
+                }
+            }
+            deg += static_cast<uint32_t>(__popcll(mask[r])) + 1u;
         }
+        uint32_t E_t = 0;
+        const uint32_t e0 = block_exscan1<NT>(deg, ws[0], &E_t); // barrier 1
+        tick(1);
         if (E_t > static_cast<uint32_t>(NE) || E + E_t > A.edge_cap) {
             if (tid == 0) *A.status = 3;
             return;
         }
-        // 2. emit: successor keys to shared memory, rewards / actions / row offsets to HBM
+        // B. emit: successor keys to shared memory, rewards / actions / row offsets to HBM
+        {
+            const double r_paid = L.r_paid, r_cloud = L.r_cloud, gam = L.gamma;
+            uint32_t j = e0;
 #pragma unroll
-        for (int r = 0; r < RS; ++r) {
-            const uint32_t i = tid + r * kSmallThreads;
-            if (i >= n) continue;
-            uint64_t k[WM];
-            load_key<WM>(front + static_cast<size_t>(i) * WM, words, k);
-            uint32_t j = off[r];
-            A.row_ptr[S - n + i] = static_cast<uint32_t>(E + j);
-            for (int p = 0; p < L.n_active; ++p) {
-                if (!L.attr[p] || get_field<WM>(k, L.bit_off[p], L.width[p]) < L.demand) continue;
-                emit_edge<WM>(k, p, L, ekey + static_cast<size_t>(j) * WM, A.reward + E + j,
-                              A.action + E + j);
-                ++j;
+            for (int r = 0; r < RS; ++r) {
+                const uint32_t i = i0 + r;
+                if (static_cast<uint32_t>(r) >= spt || i >= n) continue;
+                A.row_ptr[S - n + i] = static_cast<uint32_t>(E + j);
+                for (uint64_t m = mask[r];; m &= m - 1) {
+                    const int p = m ? __ffsll(static_cast<long long>(m)) - 1 : -1;
+                    uint64_t* dst = ekey + static_cast<size_t>(j) * WM;
+                    int ret = ret0[r];
+                    uint64_t nk[WM];
+#pragma unroll
+                    for (int w = 0; w < WM; ++w) nk[w] = nk0[r][w];
+                    int act = -1;
+                    if (p >= 0) {
+                        const uint32_t f = L.fdesc[p];
+                        act = L.cloud[p];
+                        if ((f >> 16) & 1u) {
+                            const int off = static_cast<int>((f >> 17) & 511u);
+#pragma unroll
+                            for (int w = 0; w < WM; ++w)
+                                if (w == (off >> 6)) nk[w] -= static_cast<uint64_t>(dem) << (off & 63);
+                        } else {
+                            ret -= dem;
+                        }
+                    }
+#pragma unroll
+                    for (int w = 0; w < WM; ++w) dst[w] = nk[w];
+                    A.reward[E + j] = __dsub_rn(p < 0 ? r_paid : r_cloud, __dmul_rn(gam, static_cast<double>(ret)));
+                    A.action[E + j] = act;
+                    ++j;
+                    if (p < 0) break;
+                }
             }
-            emit_edge<WM>(k, -1, L, ekey + static_cast<size_t>(j) * WM, A.reward + E + j,
-                          A.action + E + j);
         }
-        __syncthreads();
-        // 3. first-occurrence table: the lowest edge index of every successor key
-#pragma unroll
-        for (int r = 0; r < RE; ++r) {
-            const uint32_t j = tid + r * kSmallThreads;
-            if (j >= E_t) continue;
+        __syncthreads(); // barrier 2
+        tick(2);
+        // first-occurrence table: the lowest edge number of every successor key.  From here on
+        // a thread owns a contiguous run of ept edges (balanced, whatever the states' degrees)
+        const uint32_t ept = (E_t + NT - 1) / NT;
+        const uint32_t j0 = min(static_cast<uint32_t>(tid) * ept, E_t);
+        const uint32_t j1 = min(j0 + ept, E_t);
+        for (uint32_t j = j0; j < j1; ++j) {
             uint64_t k[WM];
             load_key<WM>(ekey + static_cast<size_t>(j) * WM, nw, k);
             uint32_t h = static_cast<uint32_t>(hash_key<WM>(k, nw, 0)) & (TC - 1);
@@ -1486,63 +1552,39 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_build_small(SmallBuild A) 
             }
             slot_of[j] = h;
         }
-        __syncthreads();
-        // 4. ranks of the first occurrences in edge order = the reference's insertion order
-        //    (a thread owns edges tid*RE .. tid*RE + RE - 1: contiguous, so one scan orders them)
+        __syncthreads(); // barrier 3
+        tick(3);
+        // C. ranks of the first occurrences in edge order = the reference's insertion order
         uint32_t firsts = 0;
-        bool is_first[RE];
-#pragma unroll
-        for (int r = 0; r < RE; ++r) {
-            const uint32_t j = tid * RE + r;
-            is_first[r] = j < E_t && table[slot_of[j]] == j;
-            firsts += is_first[r] ? 1u : 0u;
-        }
+        for (uint32_t j = j0; j < j1; ++j) firsts += table[slot_of[j]] == j ? 1u : 0u;
         uint32_t n_next = 0;
-        uint32_t rk = block_exscan(firsts, warp_sums, &n_next);
-        if (S + n_next > A.state_cap || S + n_next > A.state_room) {
+        uint32_t rk = block_exscan1<NT>(firsts, ws[1], &n_next); // barrier 4
+        tick(4);
+        if (S + n_next > A.state_cap || S + n_next > A.state_room || n_next > static_cast<uint32_t>(NS)) {
             if (tid == 0) *A.status = S + n_next > A.state_cap ? 1 : 3;
             return;
         }
-        if (n_next > static_cast<uint32_t>(NS)) {
-            if (tid == 0) *A.status = 3;
-            return;
-        }
         const uint64_t next_key_base = key_base + static_cast<uint64_t>(n) * words;
+        for (uint32_t j = j0; j < j1; ++j) {
+            const uint32_t h = slot_of[j];
+            if (table[h] != j) continue;
+            trank[h] = rk;
 #pragma unroll
-        for (int r = 0; r < RE; ++r) {
-            const uint32_t j = tid * RE + r;
-            if (!is_first[r]) continue;
-            trank[slot_of[j]] = rk;
+            for (int w = 0; w < WM; ++w) {
+                const uint64_t x = w < nw ? ekey[static_cast<size_t>(j) * WM + w] : 0ull;
+                front[static_cast<size_t>(rk) * WM + w] = x;
+                if (w < nw) A.keys[next_key_base + static_cast<uint64_t>(rk) * nw + w] = x;
+            }
             ++rk;
         }
-        __syncthreads();
-        // 5. successor ids; first occurrences write the next frontier (shared + HBM)
-#pragma unroll
-        for (int r = 0; r < RE; ++r) {
-            const uint32_t j = tid + r * kSmallThreads;
-            if (j >= E_t) continue;
-            const uint32_t q = trank[slot_of[j]];
-            A.succ[E + j] = static_cast<uint32_t>(S + q);
-            if (table[slot_of[j]] == j) {
-                for (int w = 0; w < nw; ++w) A.keys[next_key_base + static_cast<uint64_t>(q) * nw + w] =
-                    ekey[static_cast<size_t>(j) * WM + w];
-            }
+        __syncthreads(); // barrier 5
+        tick(5);
+        // D. successor ids; the first occurrences clear their table slots
+        for (uint32_t j = j0; j < j1; ++j) {
+            const uint32_t h = slot_of[j];
+            A.succ[E + j] = static_cast<uint32_t>(S + trank[h]);
+            if (table[h] == j) table[h] = kEmpty32;
         }
-        __syncthreads();
-        // the next frontier and a clean table
-#pragma unroll
-        for (int r = 0; r < RE; ++r) {
-            const uint32_t j = tid + r * kSmallThreads;
-            if (j >= E_t) continue;
-            if (table[slot_of[j]] == j) {
-                const uint32_t q = trank[slot_of[j]];
-                for (int w = 0; w < WM; ++w)
-                    front[static_cast<size_t>(q) * WM + w] = w < nw ? ekey[static_cast<size_t>(j) * WM + w] : 0ull;
-            }
-        }
-        __syncthreads();
-        for (int i = tid; i < TC; i += blockDim.x) table[i] = kEmpty32;
-        if (t + 1 < A.H && tid < PW) reinterpret_cast<uint32_t*>(&Lbuf[(t + 1) & 1])[tid] = pf;
         if (tid == 0) {
             A.info[t + 1] = n_next;
             A.info[A.H + 1 + t] = E_t;
@@ -1553,7 +1595,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_build_small(SmallBuild A) 
         n = n_next;
     }
     // the terminal layer's rows have no edges (mdp.cpp:207-209)
-    for (uint32_t i = tid; i <= n; i += blockDim.x) A.row_ptr[S - n + i] = static_cast<uint32_t>(E);
+    for (uint32_t i = tid; i <= n; i += NT) A.row_ptr[S - n + i] = static_cast<uint32_t>(E);
     if (tid == 0) *A.status = 0;
 }
 
@@ -1586,6 +1628,7 @@ bool build_small(vcs_space* sp, uint64_t state_cap) {
     const int H = pl.horizon;
     if (H < 1 || H > 4096 || std::getenv("VCS_BUILD_LAYERED") || std::getenv("VCS_NO_SMALL_BUILD"))
         return false;
+    const double t_setup = trace_enabled() ? host_ms() : 0.0;
     constexpr int NS = kSmallStates / WM, NE = kSmallEdges / WM, TC = 2 * NE;
     const size_t smem = static_cast<size_t>(NS) * WM * 8 + static_cast<size_t>(NE) * WM * 8 +
                         static_cast<size_t>(TC) * 8 + static_cast<size_t>(NE) * 4;
@@ -1593,7 +1636,15 @@ bool build_small(vcs_space* sp, uint64_t state_cap) {
     const uint64_t edge_room = static_cast<uint64_t>(H) * NE;
     if (edge_room >= 0xffffffffull || state_room >= 0xffffffffull) return false;
     cudaStream_t s = sp->stream;
-    const void* fn = reinterpret_cast<const void*>(k_build_small<WM>);
+    // block size: 512 threads (VCS_SMALL_THREADS = 128 / 256 / 1024 for measurements; C1
+    // canonical: 1.10 ms at 512 against 1.24 at 256 and 1.54 at 1024)
+    int nt = kSmallThreadsDefault;
+    if (const char* e = std::getenv("VCS_SMALL_THREADS")) nt = std::atoi(e);
+    if (nt != 1024 && nt != 256 && nt != 128) nt = 512;
+    const void* fn = nt == 1024 ? reinterpret_cast<const void*>(k_build_small<WM, 1024>)
+                     : nt == 256 ? reinterpret_cast<const void*>(k_build_small<WM, 256>)
+                     : nt == 128 ? reinterpret_cast<const void*>(k_build_small<WM, 128>)
+                                 : reinterpret_cast<const void*>(k_build_small<WM, 512>);
     raise_smem_limit_space(fn, sp->device, smem);
     sp->keys.reserve(state_room * WM, 0, s);
     sp->row_ptr.reserve(state_room + 1, 0, s);
@@ -1624,14 +1675,48 @@ bool build_small(vcs_space* sp, uint64_t state_cap) {
     A.edge_cap = edge_room;
     A.state_room = state_room;
     A.H = H;
-    k_build_small<WM><<<1, kSmallThreads, smem, s>>>(A);
+    DevBuf<long long> cycles;
+    if (trace_enabled()) {
+        cycles.exact(6 * static_cast<size_t>(H) + 6, s);
+        A.cycles = cycles.p;
+    }
+    void* args[] = {&A};
+    const double t_launch = trace_enabled() ? host_ms() : 0.0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (trace_enabled()) {
+        cudaEventCreate(&ev0);
+        cudaEventCreate(&ev1);
+        cudaEventRecord(ev0, s);
+    }
+    VCS_CUDA(cudaLaunchKernel(fn, dim3(1), dim3(nt), args, smem, s));
     VCS_LAUNCHED();
+    if (trace_enabled()) cudaEventRecord(ev1, s);
     std::vector<uint64_t> hinfo(2 * static_cast<size_t>(H) + 2);
     int32_t hstatus = -1;
     VCS_CUDA(cudaMemcpyAsync(hinfo.data(), info.p, hinfo.size() * sizeof(uint64_t),
                              cudaMemcpyDeviceToHost, s));
     VCS_CUDA(cudaMemcpyAsync(&hstatus, status.p, sizeof hstatus, cudaMemcpyDeviceToHost, s));
     VCS_CUDA(cudaStreamSynchronize(s));
+    if (trace_enabled()) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev0, ev1);
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+        std::fprintf(stderr, "[vcs build] small builder (%d threads): setup %.3f ms, kernel %.3f ms, "
+                     "launch to results %.3f ms, status %d\n", nt, t_launch - t_setup, ms,
+                     host_ms() - t_launch, hstatus);
+        if (hstatus == 0) {
+            std::vector<long long> c(6 * static_cast<size_t>(H));
+            VCS_CUDA(cudaMemcpy(c.data(), cycles.p, c.size() * 8, cudaMemcpyDeviceToHost));
+            double ph[6] = {};
+            for (int t = 0; t + 1 < H; ++t)
+                for (int k = 0; k < 6; ++k)
+                    ph[k] += static_cast<double>((k < 5 ? c[6 * t + k + 1] : c[6 * (t + 1)]) - c[6 * t + k]);
+            std::fprintf(stderr, "[vcs build] small builder kcycles: fields+scan %.0f emit %.0f hash %.0f "
+                         "firsts+scan %.0f ranks %.0f succ %.0f (layers 0..%d)\n", ph[0] * 1e-3,
+                         ph[1] * 1e-3, ph[2] * 1e-3, ph[3] * 1e-3, ph[4] * 1e-3, ph[5] * 1e-3, H - 2);
+        }
+    }
     if (hstatus == 1)
         raise(VCS_ECAP, "reachable state space exceeds cap of " + std::to_string(state_cap) +
                             " states");
