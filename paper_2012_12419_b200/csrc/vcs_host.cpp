@@ -358,6 +358,14 @@ LayerPlan make_layer_plan(const vcs_instance* in) {
                          (L.keep_idx[p] >= 0 ? (1u << 16) | (static_cast<uint32_t>(L.next_bit_off[p]) << 17) : 0u);
         }
     }
+    for (int t = 1; t < H; ++t) {
+        LayerParam& L = pl.layers[static_cast<std::size_t>(t)];
+        bool ok = L.n_keep == L.n_active && L.n_active <= 7 && L.dense_size != 0 &&
+                  L.dense_size == L.self_size;
+        for (int p = 0; ok && p < L.n_active; ++p)
+            ok = L.keep_idx[p] == p && L.wnext[p] == L.wself[p] && L.next_bit_off[p] == L.bit_off[p];
+        L.pull = ok ? 1 : 0;
+    }
     pl.init_key.assign(static_cast<std::size_t>(pl.words[0]), 0);
     for (std::size_t p = 0; p < pl.active[0].size(); ++p) {
         const int c = pl.active[0][p];

@@ -84,7 +84,9 @@ struct LayerParam {
     // idx = sum_p f_p * wself[p]; self_size = prod radix (0 = too large)
     uint32_t wself[kMaxActive];
     uint32_t self_size;
-    int32_t pad2;
+    int32_t pull;                // 1: transition t keeps every cloud and numbers layers t and t+1
+                                 // alike (wself == wnext): the builder may pull first edges
+                                 // from layer t's rank table instead of pushing them (t >= 1)
     // field p in one word (the single-CTA builder reads four per shared-memory load): bits 0-8
     // bit_off, 9-14 width, 15 attr, 16 kept, 17-25 next_bit_off; 0 past n_active (a zero-width
     // retired field: it adds nothing)

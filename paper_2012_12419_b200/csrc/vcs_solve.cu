@@ -4149,12 +4149,9 @@ int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int
             }
             chunk_end = r0;
         }
-        vcs_solve_report local{};
-        vcs_solve_report* rep = report ? report : &local;
-        const int rc3 = vcs_solve_collect(sp, nullptr, nullptr, rep, nullptr);
-        if (rc3 != VCS_OK) vcs::raise(rc3, vcs_last_error());
         // widen each int8 piece into the caller's int32 column as soon as it landed (the later
-        // pieces are still on the wire)
+        // pieces are still on the wire, the lower layers still solving): the host widening,
+        // not the wire, is the slower of the two on a 16-core host
         const bool tr = vcs::trace_enabled();
         const double tw0 = tr ? vcs::host_ms() : 0.0;
         for (const Piece& pc : pieces) {
@@ -4171,7 +4168,12 @@ int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int
                              static_cast<unsigned long long>(pc.r1 - pc.r0), tb - ta, vcs::host_ms() - tb,
                              vcs::host_ms() - tw0);
         }
+        vcs_solve_report local{};
+        vcs_solve_report* rep = report ? report : &local;
+        const int rc3 = vcs_solve_collect(sp, nullptr, nullptr, rep, nullptr);
+        if (rc3 != VCS_OK) vcs::raise(rc3, vcs_last_error());
         // an early stop (K* < H) rewrote the prefix of layers t < H - K* after their events
+        // (the pieces above may hold the certified pass's rows there: copied over now)
         const int K = rep->sweeps;
         if (sp->H - K > 0) {
             VCS_CUDA(cudaStreamSynchronize(d));

@@ -615,9 +615,11 @@ struct DenseBuild {
     uint32_t dense_max;
     int max_rounds;      // bsum holds max_rounds x gridDim.x entries
     int H;
+    int pull;            // the pull form may run on layers marked LayerParam::pull
 };
 
 constexpr int kDenseThreads = 256;
+constexpr int kPullMaxBlocks = 1024; // (round, block) prefixes of the pull form in shared memory
 
 // Successor key of the edge choosing key position p (-1 = paid), in layer t+1's packing.
 template <int WM>
@@ -712,6 +714,7 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
     uint64_t E = 0;     // edges of layers < t
     uint64_t key_t = 0; // first key word of layer t
     uint64_t rank_t = 0; // first entry of transition t's rank table
+    uint64_t rank_prev = 0; // transition t-1's (layer t's own index -> BFS index)
     uint32_t n_t = 1;
     if (b == 0 && tid == 0) A.info[0] = 1;
     auto publish_rounds = [&](int R) { // s_round -> bsum[r * G + b]
@@ -736,6 +739,183 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
             load_key<WM>(A.keys + key_t + static_cast<uint64_t>(i) * L.words, L.words, k);
         };
         stamp(A.stamps, 6 * t + 0);
+        if (!EXPLICIT && WM == 1 && A.pull && L.pull && t >= 1 &&
+            (L.dense_size + T - 1) / T <= 8 && (static_cast<uint64_t>(n_t) + 4 * T - 1) / (4 * T) <= 2) {
+            // Pull form (a non-retiring transition numbered alike on both sides): successor d'
+            // has the paid predecessor d' and, per eligible cloud p, the predecessor
+            // d' + demand*W_p (when that free count fits the cloud); the predecessors' BFS
+            // indices come from layer t's own rank table (transition t-1), read as shifted
+            // streams.  Its first edge is the minimum of (index << 3 | slot) over them — what the
+            // push form's atomicMin finds — without an atomic per edge.  The BFS numbering of
+            // layer t+1 is the order of those first edges: a bitmap over the edge keys (bit
+            // cleared = a first edge; the table starts all ones), popcount prefixes, and every
+            // reached d' looks up its rank.
+            constexpr int RB = 8;
+            constexpr int NF = kDenseSlots - 1;
+            const uint32_t Dn = L.dense_size;
+            const int R1 = static_cast<int>((Dn + T - 1) / T);
+            const uint32_t* __restrict__ rs = A.rank_tables + rank_prev; // layer t: index -> BFS index
+            uint32_t* bm = table;
+            const uint32_t dem = static_cast<uint32_t>(L.demand);
+            uint32_t g[NF], sd[NF], rad[NF], wp[NF], nbo[NF], elig = 0;
+            {
+                uint32_t rem = q < Dn ? q : 0u, srem = T < Dn ? static_cast<uint32_t>(T) : 0u;
+#pragma unroll
+                for (int p = 0; p < NF; ++p) {
+                    const bool on = p < L.n_active;
+                    rad[p] = on ? L.radix[p] : 1u;
+                    wp[p] = on ? L.wnext[p] : 0u;
+                    nbo[p] = on ? L.next_bit_off[p] : 0u;
+                    if (on && L.attr[p]) elig |= 1u << p;
+                    g[p] = rem % rad[p];
+                    rem /= rad[p];
+                    sd[p] = srem % rad[p];
+                    srem /= rad[p];
+                }
+            }
+            stamp(A.stamps, 6 * t + 1);
+            uint32_t fr[RB];
+            uint64_t kr[RB];
+            uint32_t dsum = 0;
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+                const uint32_t d = static_cast<uint32_t>(r) * T + q;
+                fr[r] = kEmpty32;
+                kr[r] = 0ull;
+                if (r >= R1 || d >= Dn) continue;
+                uint32_t rk[NF + 1];
+                rk[NF] = __ldcg(rs + d); // the paid predecessor: d itself
+#pragma unroll
+                for (int p = 0; p < NF; ++p)
+                    rk[p] = ((elig >> p) & 1u) && g[p] + dem < rad[p] ? __ldcg(rs + d + dem * wp[p]) : kEmpty32;
+                uint32_t best = kEmpty32;
+                uint64_t key = 0ull;
+#pragma unroll
+                for (int p = 0; p < NF; ++p) {
+                    key |= static_cast<uint64_t>(g[p]) << nbo[p];
+                    if (rk[p] != kEmpty32) {
+                        best = min(best, (rk[p] << 3) | static_cast<uint32_t>(p));
+                        ++dsum;
+                    }
+                }
+                if (rk[NF] != kEmpty32) {
+                    best = min(best, (rk[NF] << 3) | static_cast<uint32_t>(NF));
+                    ++dsum;
+                }
+                fr[r] = best;
+                kr[r] = key;
+                if (best != kEmpty32) atomicAnd(bm + (best >> 5), ~(1u << (best & 31u)));
+                // the next round's digits: d + T
+                uint32_t carry = 0;
+#pragma unroll
+                for (int p = 0; p < NF; ++p) {
+                    const uint32_t v = g[p] + sd[p] + carry;
+                    carry = v >= rad[p] ? 1u : 0u;
+                    g[p] = carry ? v - rad[p] : v;
+                }
+            }
+            dsum = __reduce_add_sync(0xffffffffu, dsum);
+            if ((tid & 31) == 0 && dsum)
+                atomicAdd(reinterpret_cast<unsigned long long*>(A.info + A.H + 1 + t),
+                          static_cast<unsigned long long>(dsum));
+            grid.sync();
+            stamp(A.stamps, 6 * t + 2);
+            // first edges per bitmap word; block-local exclusive prefixes of the words
+            uint32_t* wpre = reinterpret_cast<uint32_t*>(A.desc);
+            const uint32_t NW = (n_t + 3u) / 4u; // 8 * n_t edge keys
+            const int R2 = static_cast<int>((NW + T - 1) / T);
+            {
+                __shared__ uint32_t s_ws2[2][kDenseThreads / 32];
+                const int lane = tid & 31, warp = tid >> 5;
+                uint32_t c[2], wex[2];
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const uint32_t w = static_cast<uint32_t>(r) * T + q;
+                    c[r] = (r < R2 && w < NW) ? static_cast<uint32_t>(__popc(~__ldcg(bm + w))) : 0u;
+                    uint32_t incl = c[r];
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    wex[r] = incl - c[r];
+                    if (lane == 31) s_ws2[r][warp] = incl;
+                }
+                __syncthreads();
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const uint32_t w = static_cast<uint32_t>(r) * T + q;
+                    uint32_t before = wex[r], tot = 0;
+                    for (int k = 0; k < kDenseThreads / 32; ++k) {
+                        before += k < warp ? s_ws2[r][k] : 0u;
+                        tot += s_ws2[r][k];
+                    }
+                    if (r < R2 && w < NW) wpre[w] = before;
+                    if (tid == 0 && r < R2) s_round[r] = tot;
+                }
+            }
+            publish_rounds(R2);
+            grid.sync();
+            stamp(A.stamps, 6 * t + 3);
+            // global prefixes of every (round, block) of the words, in shared memory
+            __shared__ uint32_t s_gpre[2 * kPullMaxBlocks];
+            uint32_t n_next = 0;
+            {
+                const int M = R2 * G;
+                const int per = (M + kDenseThreads - 1) / kDenseThreads;
+                uint32_t loc = 0;
+                for (int k = 0; k < per; ++k) {
+                    const int i = tid * per + k;
+                    if (i < M) loc += __ldcg(A.bsum + i);
+                }
+                uint32_t ex;
+                Scan(scan_tmp).ExclusiveSum(loc, ex, n_next);
+                for (int k = 0; k < per; ++k) {
+                    const int i = tid * per + k;
+                    if (i < M) {
+                        s_gpre[i] = ex;
+                        ex += __ldcg(A.bsum + i);
+                    }
+                }
+                __syncthreads();
+            }
+            if (S_next + n_next > A.state_cap || S_next + n_next >= 0xffffffffull) {
+                if (b == 0 && tid == 0) {
+                    *A.status = S_next + n_next > A.state_cap ? 1 : 2;
+                    A.info[t + 1] = n_next;
+                }
+                return; // every block takes the same decision
+            }
+            // ranks: the rank table of transition t (coalesced, by d') and the next layer's keys
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+                const uint32_t d = static_cast<uint32_t>(r) * T + q;
+                if (r >= R1 || d >= Dn) continue;
+                const uint32_t f = fr[r];
+                uint32_t rank = kEmpty32;
+                if (f != kEmpty32) {
+                    const uint32_t w = f >> 5;
+                    const uint32_t rw = w >= T ? 1u : 0u;
+                    const uint32_t bw = (w - rw * static_cast<uint32_t>(T)) / kDenseThreads;
+                    const uint32_t word = ~__ldcg(bm + w);
+                    rank = s_gpre[rw * G + bw] + __ldcg(wpre + w) +
+                           static_cast<uint32_t>(__popc(word & ((1u << (f & 31u)) - 1u)));
+                    A.keys[key_next + rank] = kr[r];
+                }
+                A.rank_tables[rank_t + d] = rank;
+            }
+            if (b == 0 && tid == 0) A.info[t + 1] = n_next;
+            if (tid < 8) s_round[tid] = 0;
+            grid.sync();
+            stamp(A.stamps, 6 * t + 4);
+            for (uint32_t i = q; i < A.dense_max; i += T) table[i] = kEmpty32;
+            S_t = S_next;
+            key_t = key_next;
+            rank_prev = rank_t;
+            rank_t += L.dense_size;
+            n_t = n_next;
+            continue;
+        }
         if (!EXPLICIT && WM == 1) {
             // Implicit form, single-word keys, all of a thread's rounds at once: keys,
             // descriptors and first-edge masks stay in registers across the grid syncs, the
@@ -858,6 +1038,7 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
             for (uint32_t i = q; i < A.dense_max; i += T) table[i] = kEmpty32;
             S_t = S_next;
             key_t = key_next;
+            rank_prev = rank_t;
             rank_t += L.dense_size;
             n_t = n_next;
             continue;
@@ -973,6 +1154,7 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
             for (uint32_t i = q; i < A.dense_max; i += T) table[i] = kEmpty32;
             S_t = S_next;
             key_t = key_next;
+            rank_prev = rank_t;
             rank_t += L.dense_size;
             n_t = n_next;
             continue;
@@ -1148,6 +1330,7 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
         S_t = S_next;
         E += E_t;
         key_t = key_next;
+        rank_prev = rank_t;
         rank_t += L.dense_size;
         n_t = n_next;
     }
@@ -1269,6 +1452,7 @@ bool build_dense(vcs_space* sp, uint64_t state_cap) {
     A.dense_max = static_cast<uint32_t>(dense_max);
     A.max_rounds = max_rounds;
     A.H = H;
+    A.pull = (G <= kPullMaxBlocks && !std::getenv("VCS_BUILD_NO_PULL")) ? 1 : 0;
     void* args[] = {&A};
     const double t_launch = trace_enabled() ? host_ms() : 0.0;
     VCS_CUDA(cudaLaunchCooperativeKernel(fn, G, kDenseThreads, args, 0, s));

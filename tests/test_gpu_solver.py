@@ -818,3 +818,38 @@ def test_certified_tail_kernel_matches_golden(gpu, golden, monkeypatch):
             r = _solve(sp, method=N.VCS_METHOD_CERTIFIED)
             assert sha(r.values.raw_values()) == g["values_sha"]
             assert sha(r.policy.raw_actions()) == g["actions_sha"]
+
+
+@pytest.mark.parametrize("pull", [True, False])
+def test_pull_builder_matches_golden_and_oracle(gpu, golden, oracle, monkeypatch, pull):
+    """The persistent builder's pull form (first edges pulled from layer t's rank table on
+    non-retiring transitions, BFS ranks from a bitmap over the edge keys; the default) and its
+    push form (VCS_BUILD_NO_PULL: an atomicMin per edge) number every layer alike: C3 / C4 give
+    the reference digests through the certified pass and Jacobi on the materialised CSR, and
+    random instances with retiring clouds (pull and push layers interleaved) equal the oracle
+    bit for bit, layer sizes and policy queries included."""
+    from conftest import bits
+    if not pull:
+        monkeypatch.setenv("VCS_BUILD_NO_PULL", "1")
+    for name in ("C3", "C4"):
+        p = V.load_instance(str(GOLDEN / "instances" / f"{name.lower()}.txt"))
+        sp = V.StateSpace.build_native(V.NativeInstance(p.vcc, bots=p.bots), 10**9)
+        g = golden["cases"][name]["eps=1e-06"]
+        assert sp.size() == golden["cases"][name]["S"]
+        r = _solve(sp, method=N.VCS_METHOD_CERTIFIED)
+        assert sha(r.values.raw_values()) == g["values_sha"]
+        assert sha(r.policy.raw_actions()) == g["actions_sha"]
+        if name == "C3":
+            r = _solve(sp, method=N.VCS_METHOD_JACOBI)
+            assert sha(r.values.raw_values()) == g["values_sha"]
+    for trial in range(4):
+        ni = V.generate_instance(N.VCS_GEN_RANDOM, 43, trial, 5, 6, 18, 3, as_objects=False)
+        sp = V.StateSpace.build_native(ni, 10**9)
+        osp = oracle.build(ni.ref, 10**9)
+        assert sp.size() == osp.S
+        assert np.array_equal(sp.layer_offsets().astype(np.uint64), osp.csr()[0])
+        v, a, sw, _, _ = osp.vi()
+        r = _solve(sp, method=N.VCS_METHOD_CERTIFIED)
+        assert r.values.report.sweeps == sw
+        assert np.array_equal(bits(r.values.raw_values()), bits(v)), trial
+        assert np.array_equal(r.policy.raw_actions(), a), trial
