@@ -887,6 +887,14 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
                 return; // every block takes the same decision
             }
             // ranks: the rank table of transition t (coalesced, by d') and the next layer's keys
+            // (every round's two gathers first, then the stores)
+            uint32_t bmw[RB], wpv[RB];
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+                const uint32_t f = fr[r];
+                bmw[r] = f != kEmpty32 ? __ldcg(bm + (f >> 5)) : 0u;
+                wpv[r] = f != kEmpty32 ? __ldcg(wpre + (f >> 5)) : 0u;
+            }
 #pragma unroll
             for (int r = 0; r < RB; ++r) {
                 const uint32_t d = static_cast<uint32_t>(r) * T + q;
@@ -897,9 +905,8 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
                     const uint32_t w = f >> 5;
                     const uint32_t rw = w >= T ? 1u : 0u;
                     const uint32_t bw = (w - rw * static_cast<uint32_t>(T)) / kDenseThreads;
-                    const uint32_t word = ~__ldcg(bm + w);
-                    rank = s_gpre[rw * G + bw] + __ldcg(wpre + w) +
-                           static_cast<uint32_t>(__popc(word & ((1u << (f & 31u)) - 1u)));
+                    rank = s_gpre[rw * G + bw] + wpv[r] +
+                           static_cast<uint32_t>(__popc(~bmw[r] & ((1u << (f & 31u)) - 1u)));
                     A.keys[key_next + rank] = kr[r];
                 }
                 A.rank_tables[rank_t + d] = rank;
@@ -1805,6 +1812,22 @@ void raise_smem_limit_space(const void* fn, int device, size_t smem) {
     cur = smem;
 }
 
+// Every layer of a dense plan fits k_build_small's tables by its key-space bound (n_{t+1} <=
+// dense_size_t, E_t <= n_t * out-degree bound).
+template <int WM>
+bool small_dense_fits(const LayerPlan& pl) {
+    constexpr uint64_t NS = kSmallStates / WM, NE = kSmallEdges / WM;
+    uint64_t n = 1;
+    for (const LayerParam& L : pl.layers) {
+        if (!L.dense_size || L.dense_size > NS) return false;
+        int maxdeg = 1;
+        for (int p = 0; p < L.n_active; ++p) maxdeg += L.attr[p] ? 1 : 0;
+        if (n * static_cast<uint64_t>(maxdeg) > NE) return false;
+        n = L.dense_size;
+    }
+    return !pl.layers.empty();
+}
+
 // Host side of k_build_small: returns false (nothing kept) when the space is not small.
 template <int WM>
 bool build_small(vcs_space* sp, uint64_t state_cap) {
@@ -2497,6 +2520,11 @@ int vcs_space_build(const vcs_instance* inst, uint64_t state_cap, int device, vc
         const bool explicit_now = std::getenv("VCS_BUILD_EXPLICIT") != nullptr;
         vcs::dispatch_words(vcs::max_words(sp.get()), [&](auto wm) {
             constexpr int WM = decltype(wm)::value;
+            // a tiny dense space (every layer's key space within the single-CTA tables, e.g. the
+            // small C5 points) is built in one block: the cooperative grid's barriers cost more
+            // than its layers
+            if (vcs::small_dense_fits<WM>(sp->plan) && vcs::build_small<WM>(sp.get(), state_cap))
+                return;
             const bool dense = explicit_now ? vcs::build_dense<WM, true>(sp.get(), state_cap)
                                             : vcs::build_dense<WM, false>(sp.get(), state_cap);
             if (dense) return;

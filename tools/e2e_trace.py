@@ -1,7 +1,7 @@
 """e2e steps exactly as bench.py times them (parse + build + vcs_solve into pinned buffers),
 traced (VCS_TRACE=1 prints the library's phase timings on stderr).
 
-    python tools/e2e_trace.py [c4|c1|c3|c7] [steps]"""
+    python tools/e2e_trace.py [c4|c1|c3|c7|c5:K:c:scheme] [steps]"""
 import ctypes as C
 import os
 import sys
@@ -17,7 +17,11 @@ from paper_2012_12419_b200 import _native as N  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c4"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
-text = W.instance_text(name).encode()
+if name.startswith("c5:"):  # c5:K:c:scheme
+    _, K, c, scheme = name.split(":")
+    text = W.c5_text(int(K), int(c), scheme, W.channel_table()).encode()
+else:
+    text = W.instance_text(name).encode()
 vals = acts = None
 opts = N.vcs_solve_opts(1e-6, 1, 0, 1.0, 0)
 for it in range(steps):
