@@ -2500,9 +2500,16 @@ void launch_cert_layer(const vcs_space* sp, const CertData& data, const CertLaye
         // spills); wide keys (4 / 8 words: many-cloud instances) take 2 so they do not spill
         constexpr int IMB = WM <= 2 ? 3 : 2;
         // 3 blocks per SM (80 registers, no spills): C4 0.68 ms vs 0.72 at 4, 0.74 at 2
+        static const int cert_minb = [] {
+            const char* e = std::getenv("VCS_CERT_MINB"); // (measurements: 2 / 4 blocks per SM)
+            const int v = e ? std::atoi(e) : 3;
+            return v == 2 || v == 4 ? v : 3;
+        }();
         const void* fn =
             dense_order ? (disc ? reinterpret_cast<const void*>(k_cert_dense<WM, true, 3>)
-                                : reinterpret_cast<const void*>(k_cert_dense<WM, false, 3>))
+                                : cert_minb == 4 ? reinterpret_cast<const void*>(k_cert_dense<WM, false, 4>)
+                                : cert_minb == 2 ? reinterpret_cast<const void*>(k_cert_dense<WM, false, 2>)
+                                                 : reinterpret_cast<const void*>(k_cert_dense<WM, false, 3>))
                         : (disc ? reinterpret_cast<const void*>(k_cert_implicit<WM, true, IMB, false>)
                                 : reinterpret_cast<const void*>(k_cert_implicit<WM, false, IMB, false>));
         static thread_local std::map<std::pair<const void*, int>, int> occ;
@@ -2528,6 +2535,8 @@ void launch_cert_layer(const vcs_space* sp, const CertData& data, const CertLaye
         cfg.numAttrs = pdl ? 1 : 0;
         if (dense_order) {
             if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense<WM, true, 3>, c));
+            else if (cert_minb == 4) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense<WM, false, 4>, c));
+            else if (cert_minb == 2) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense<WM, false, 2>, c));
             else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense<WM, false, 3>, c));
         } else if (ks) {
             if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_implicit<WM, true, IMB, true>, c));
@@ -2945,12 +2954,13 @@ CachedGraph& enqueue_solve(vcs_space* sp, const GraphKey& key, cudaStream_t s) {
         }
         cudaGraph_t graph = nullptr;
         VCS_CUDA(cudaStreamEndCapture(cs, &graph));
+        const double t1 = trace_enabled() ? host_ms() : 0.0;
         const cudaError_t ierr = cudaGraphInstantiate(&g.exec, graph, 0);
         cudaGraphDestroy(graph);
         if (ierr != cudaSuccess)
             raise(VCS_ECUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ierr));
         if (trace_enabled())
-            std::fprintf(stderr, "[vcs solve] capture+instantiate %.3f ms\n", host_ms() - t0);
+            std::fprintf(stderr, "[vcs solve] capture %.3f + instantiate %.3f ms\n", t1 - t0, host_ms() - t1);
     }
     VCS_CUDA(cudaGraphLaunch(g.exec, s));
     note_launch(static_cast<uint64_t>(g.launches));
@@ -3985,8 +3995,8 @@ private:
     uint64_t gen_ = 0;
 };
 
-// int8 -> int32 widening of the action column on the host (plain stores: non-temporal stores
-// measured slower, they compete with the DMA writing the value column into host memory)
+// int8 -> int32 widening of the action column on the host (plain stores: AVX2 conversion with
+// non-temporal stores measured the same on the B200 box, 4.01-4.18 vs 4.02-4.05 ms C4 e2e)
 void widen(const int8_t* src, int32_t* dst, size_t n) {
     for (size_t i = 0; i < n; ++i) dst[i] = src[i];
 }
