@@ -10,6 +10,9 @@
 //                                   libstdc++ uniform_int_distribution draws)
 #include "vcs_internal.h"
 
+#include <cerrno>
+#include <climits>
+#include <string_view>
 #include <algorithm>
 #include <atomic>
 #include <cctype>
@@ -89,12 +92,123 @@ bool skippable(const std::string& line) {
     raise(VCS_EINVAL, "line " + std::to_string(lineno) + ": " + why + " in '" + line + "'");
 }
 
+// Fast path of one well-formed directive line: whitespace-separated tokens of plain decimal
+// numbers (the only forms it accepts; anything else — signs in odd places, hex, inf/nan,
+// overflow, a wrong field count, a task before any bot — returns false and the line goes through
+// the stream extraction below, which produces the reference's diagnostics).  For such tokens
+// strtol / strtod give exactly what `>> int` / `>> double` give.
+bool plain_number(const char* b, const char* e, bool integral) {
+    if (b < e && (*b == '+' || *b == '-')) ++b;
+    if (b == e) return false;
+    bool digit = false;
+    for (const char* c = b; c < e; ++c) {
+        if (*c >= '0' && *c <= '9') {
+            digit = true;
+        } else if (integral) {
+            return false;
+        } else if (*c == '.' || *c == 'e' || *c == 'E' || *c == '+' || *c == '-') {
+            continue;
+        } else {
+            return false;
+        }
+    }
+    return digit;
+}
+
+bool fast_line(const std::string& line, OwnedInstance& p) {
+    const char* tb[6];
+    const char* te[6];
+    int n = 0;
+    const char* c = line.data();
+    const char* end = c + line.size();
+    while (c < end) {
+        while (c < end && std::isspace(static_cast<unsigned char>(*c))) ++c;
+        if (c == end) break;
+        if (n == 6) return false;
+        tb[n] = c;
+        while (c < end && !std::isspace(static_cast<unsigned char>(*c))) ++c;
+        te[n++] = c;
+    }
+    if (n < 2) return false;
+    const std::string_view kind(tb[0], static_cast<size_t>(te[0] - tb[0]));
+    auto to_int = [&](int k, int& out) {
+        if (!plain_number(tb[k], te[k], true)) return false;
+        char* stop = nullptr;
+        errno = 0;
+        const long v = std::strtol(tb[k], &stop, 10);
+        if (stop != te[k] || errno == ERANGE || v < INT_MIN || v > INT_MAX) return false;
+        out = static_cast<int>(v);
+        return true;
+    };
+    auto to_double = [&](int k, double& out) {
+        // an integer of <= 15 digits is exact in a double: the value strtod would return
+        const char* b = tb[k];
+        const bool neg = *b == '-';
+        if (*b == '+' || *b == '-') ++b;
+        if (te[k] - b >= 1 && te[k] - b <= 15) {
+            int64_t v = 0;
+            const char* q = b;
+            for (; q < te[k] && *q >= '0' && *q <= '9'; ++q) v = v * 10 + (*q - '0');
+            if (q == te[k]) {
+                out = neg ? -static_cast<double>(v) : static_cast<double>(v);
+                return true;
+            }
+        }
+        if (!plain_number(tb[k], te[k], false)) return false;
+        char* stop = nullptr;
+        errno = 0;
+        const double v = std::strtod(tb[k], &stop);
+        if (stop != te[k] || errno == ERANGE) return false;
+        out = v;
+        return true;
+    };
+    if (kind == "task") {
+        int id, demand;
+        double dly, thr;
+        if (n != 5 || p.bot_id.empty() || !to_int(1, id) || !to_int(2, demand) || !to_double(3, dly) ||
+            !to_double(4, thr))
+            return false;
+        p.task_id.push_back(id);
+        p.task_demand.push_back(demand);
+        p.task_max_delay.push_back(dly);
+        p.task_min_thr.push_back(thr);
+        return true;
+    }
+    if (kind == "cloud") {
+        int id, total;
+        double thr, delay;
+        if (n != 5 || !to_int(1, id) || !to_int(2, total) || !to_double(3, thr) || !to_double(4, delay))
+            return false;
+        p.cloud_id.push_back(id);
+        p.cloud_vm_total.push_back(total);
+        p.cloud_vm_free.push_back(total);
+        p.cloud_thr.push_back(thr);
+        p.cloud_delay.push_back(delay);
+        return true;
+    }
+    if (kind == "bot") {
+        int id;
+        if (n != 2 || !to_int(1, id)) return false;
+        p.bot_id.push_back(id);
+        p.bot_off.push_back(static_cast<int32_t>(p.task_id.size()));
+        return true;
+    }
+    if (kind == "beta_vc" || kind == "beta_tc" || kind == "gamma_vc") {
+        double v;
+        if (n != 2 || !to_double(1, v)) return false;
+        (kind == "beta_vc" ? p.beta_vc : kind == "beta_tc" ? p.beta_tc : p.gamma_vc) = v;
+        return true;
+    }
+    return false;
+}
+
 void parse_into(std::istream& in, OwnedInstance& p) {
     std::string line;
     int lineno = 0;
     while (std::getline(in, line)) {
         ++lineno;
         if (skippable(line)) continue;
+        if (fast_line(line, p)) continue;
         std::istringstream ls(line);
         std::string kind;
         ls >> kind;
@@ -283,7 +397,12 @@ LayerPlan make_layer_plan(const vcs_instance* in) {
     pl.active.resize(static_cast<std::size_t>(H) + 1);
     pl.words.resize(static_cast<std::size_t>(H) + 1);
     pl.bit_off.resize(static_cast<std::size_t>(H) + 1);
+    pl.key_bits.reserve(static_cast<std::size_t>(H) + 1);
     for (int t = 0; t <= H; ++t) {
+        int na = 0;
+        for (int i = 0; i < K; ++i) na += pl.last_use[i] >= t ? 1 : 0;
+        pl.active[t].reserve(static_cast<std::size_t>(na)); // (one allocation per layer)
+        pl.bit_off[t].reserve(static_cast<std::size_t>(na));
         for (int i = 0; i < K; ++i)
             if (pl.last_use[i] >= t) pl.active[t].push_back(i);
         if (static_cast<int>(pl.active[t].size()) > kMaxActive)
@@ -305,8 +424,7 @@ LayerPlan make_layer_plan(const vcs_instance* in) {
     }
     pl.layers.resize(static_cast<std::size_t>(H));
     for (int t = 0; t < H; ++t) {
-        LayerParam& L = pl.layers[t];
-        std::memset(&L, 0, sizeof L);
+        LayerParam& L = pl.layers[t]; // (value-initialised by the resize: all zero)
         const auto& act = pl.active[t];
         L.n_active = static_cast<int32_t>(act.size());
         L.n_keep = static_cast<int32_t>(pl.active[t + 1].size());
@@ -321,10 +439,11 @@ LayerPlan make_layer_plan(const vcs_instance* in) {
         L.r_cloud_kept = L.r_cloud - L.gamma * 0.0;
         L.r_paid_kept = L.r_paid - L.gamma * 0.0;
         // mixed-radix weights of layer t+1's fields (dense successor index)
-        std::vector<uint32_t> wq;
+        uint32_t wq[kMaxActive];
+        int nwq = 0;
         uint64_t W = 1;
         for (int c : pl.active[t + 1]) {
-            wq.push_back(static_cast<uint32_t>(W));
+            wq[nwq++] = static_cast<uint32_t>(W);
             W *= static_cast<uint64_t>(std::max(0, in->cloud_vm_free[c])) + 1;
             if (W > kDenseMax) break;
         }

@@ -47,6 +47,27 @@ def test_parse_errors_match_reference_messages(text, msg):
     assert str(e.value) == msg
 
 
+@pytest.mark.parametrize("thr,delay", [
+    ("60", "10"), ("+60", "-0"), ("007", "1e1"), ("60.", ".5"), ("6.0e1", "1E-3"),
+    ("123456789012345", "0.1"), ("1234567890123456789", "2.5e-310"), ("1e400", "10"),
+    ("0x10", "10"), ("inf", "10"), ("60x", "10"), ("--1", "10"), ("1e", "10"), ("6-0", "10"),
+])
+def test_parser_fast_path_matches_reference(reference, thr, delay):
+    """Directive lines go through a strtol/strtod fast path when every field is a plain decimal
+    number, else through the stream extraction; either way the instance (or the error message)
+    is the reference parser's: same doubles bit for bit, same diagnostics."""
+    txt = (f"beta_vc {delay}\ncloud 1 5 {thr} {delay}\ncloud +2 007 {thr} 20\nbot 1\n"
+           f"task 1 2 {thr} {delay}\ntask -3 1 30 60\n")
+    try:
+        ref = reference.parse(txt).text()
+    except Exception as e:  # noqa: BLE001
+        with pytest.raises(V.ConfigError) as ours:
+            V.parse_instance(txt)
+        assert str(ours.value) in str(e), (str(ours.value), str(e))
+        return
+    assert V.instance_text(V.parse_instance(txt)) == ref
+
+
 def test_load_missing_file_is_io_error():
     with pytest.raises(V.IoError, match="cannot read instance file: /nonexistent/x.txt"):
         V.load_instance("/nonexistent/x.txt")
