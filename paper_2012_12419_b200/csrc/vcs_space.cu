@@ -655,10 +655,19 @@ __device__ __forceinline__ uint32_t round_prefixes(const uint32_t* __restrict__ 
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (w < R) {
         uint32_t part = 0, tot = 0;
-        for (int i = lane; i < G; i += 32) {
-            const uint32_t v = __ldcg(bsum + w * G + i);
-            tot += v;
-            if (i < b) part += v;
+        // eight loads in flight per lane (G <= 256 blocks: one batch)
+        for (int i0 = lane; i0 < G; i0 += 8 * 32) {
+            uint32_t v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int i = i0 + 32 * k;
+                v[k] = i < G ? __ldcg(bsum + w * G + i) : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                tot += v[k];
+                if (i0 + 32 * k < b) part += v[k];
+            }
         }
         part = __reduce_add_sync(0xffffffffu, part);
         tot = __reduce_add_sync(0xffffffffu, tot);
@@ -861,21 +870,24 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
             __shared__ uint32_t s_gpre[2 * kPullMaxBlocks];
             uint32_t n_next = 0;
             {
+                // (every thread's <= 8 sums loaded at once: M = R2 * G <= 2 * kPullMaxBlocks)
+                constexpr int PER = 2 * kPullMaxBlocks / kDenseThreads;
                 const int M = R2 * G;
                 const int per = (M + kDenseThreads - 1) / kDenseThreads;
-                uint32_t loc = 0;
-                for (int k = 0; k < per; ++k) {
+                uint32_t v[PER], loc = 0;
+#pragma unroll
+                for (int k = 0; k < PER; ++k) {
                     const int i = tid * per + k;
-                    if (i < M) loc += __ldcg(A.bsum + i);
+                    v[k] = (k < per && i < M) ? __ldcg(A.bsum + i) : 0u;
+                    loc += v[k];
                 }
                 uint32_t ex;
                 Scan(scan_tmp).ExclusiveSum(loc, ex, n_next);
-                for (int k = 0; k < per; ++k) {
+#pragma unroll
+                for (int k = 0; k < PER; ++k) {
                     const int i = tid * per + k;
-                    if (i < M) {
-                        s_gpre[i] = ex;
-                        ex += __ldcg(A.bsum + i);
-                    }
+                    if (k < per && i < M) s_gpre[i] = ex;
+                    ex += v[k];
                 }
                 __syncthreads();
             }
