@@ -2227,7 +2227,7 @@ void record_wavefront(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
         ++launches;
         // layer t's values/actions are final here (unless an early stop needs the fix-up):
         // lets vcs_solve stream them to the host while the remaining layers compute
-        if (events && !g.layer_ev.empty())
+        if (events && !g.layer_ev.empty() && g.layer_ev[static_cast<size_t>(t)])
             record_event(g.layer_ev[static_cast<size_t>(t)], s, capturing);
     }
     if (events) record_event(g.ev[1], s, capturing);
@@ -2695,7 +2695,8 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
     if (sp->implicit) { // implicit-CSR form: keys + rank tables; the fallback runs at collect
         const CertData data = cert_data_of(sp);
         int launches = 0;
-        const bool pdl = g.layer_ev.empty() && !std::getenv("VCS_NO_PDL");
+        // PDL chains the layer launches, except right behind a download event
+        const bool pdl = !std::getenv("VCS_NO_PDL");
         // the small sparse layers at the bottom run as one single-block launch (k_cert_tail)
         const int t_tail = ks ? sp->cert_tail_t : -1;
         for (int t = H - 1; t >= 0; --t) {
@@ -2718,17 +2719,22 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
                 });
                 ++launches;
                 if (!g.layer_ev.empty())
-                    for (int u = t; u >= 0; --u) record_event(g.layer_ev[static_cast<size_t>(u)], s, capturing);
+                    for (int u = t; u >= 0; --u)
+                        if (g.layer_ev[static_cast<size_t>(u)])
+                            record_event(g.layer_ev[static_cast<size_t>(u)], s, capturing);
                 break;
             }
             CertLayer L = cert_layer(sp, t, sp->cert_xd.p, half, ks);
             L.d_hi = L.dense_order ? L.dense_n : 0;
             if (L.n) {
+                const bool after_event = t + 1 < H && !g.layer_ev.empty() &&
+                                         g.layer_ev[static_cast<size_t>(t) + 1] != nullptr;
                 launch_cert_layer(sp, data, L, sp->v[0].p, sp->actions_dev.p, sp->cert_lb.p,
-                                  key.discount, 1, pdl && t < H - 1, s);
+                                  key.discount, 1, pdl && t < H - 1 && !after_event, s);
                 ++launches;
             }
-            if (!g.layer_ev.empty()) record_event(g.layer_ev[static_cast<size_t>(t)], s, capturing);
+            if (!g.layer_ev.empty() && g.layer_ev[static_cast<size_t>(t)])
+                record_event(g.layer_ev[static_cast<size_t>(t)], s, capturing);
         }
         k_cert_check<<<1, 64, 0, s>>>(sp->cert_lb.p, H, key.eps, key.max_sweeps, sp->ctrl.p, 0);
         VCS_LAUNCHED();
@@ -2805,7 +2811,8 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
             VCS_LAUNCHED();
             ++launches;
         }
-        if (!g.layer_ev.empty()) record_event(g.layer_ev[static_cast<size_t>(t)], s, capturing);
+        if (!g.layer_ev.empty() && g.layer_ev[static_cast<size_t>(t)])
+            record_event(g.layer_ev[static_cast<size_t>(t)], s, capturing);
     }
     // Profiling mode (ncu cannot profile kernels of graphs holding conditional nodes): no
     // fallback node; vcs_solve_collect raises if the proof did not hold.
@@ -2896,6 +2903,21 @@ void record_solve(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaStream
         record_jacobi(sp, key, g, s, capturing);
 }
 
+// Layers whose completion ends a piece of vcs_solve's streamed download (row_bytes per state):
+// rows are final layer by layer from the back; a piece closes once it holds >= 16 MB, the last
+// one at layer 0.  Only these layers get an event (the others keep their PDL chaining).
+std::vector<char> piece_layers(const vcs_space* sp, uint64_t row_bytes) {
+    std::vector<char> f(static_cast<size_t>(std::max(0, sp->H)), 0);
+    uint64_t chunk_end = sp->S;
+    for (int t = sp->H - 1; t >= 0; --t) {
+        const uint64_t r0 = sp->layer_off[static_cast<size_t>(t)];
+        if ((chunk_end - r0) * row_bytes < (16ull << 20) && t > 0) continue;
+        f[static_cast<size_t>(t)] = 1;
+        chunk_end = r0;
+    }
+    return f;
+}
+
 // Launch one solve on `s`: the first solve of a (space, options) pair captures the kernel
 // sequence into a CUDA graph, every solve replays it with one launch.
 CachedGraph& enqueue_solve(vcs_space* sp, const GraphKey& key, cudaStream_t s) {
@@ -2906,9 +2928,11 @@ CachedGraph& enqueue_solve(vcs_space* sp, const GraphKey& key, cudaStream_t s) {
         g.n_sweeps = key.max_sweeps;
         for (auto& e : g.ev) VCS_CUDA(cudaEventCreate(&e));
         if (key.stream_out && (key.method == kMethodWavefront || key.method == kMethodCertified)) {
-            g.layer_ev.assign(static_cast<size_t>(std::max(0, sp->H)), nullptr);
-            for (auto& e : g.layer_ev)
-                VCS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            // (stream_out = the download's bytes per state: events at its piece boundaries)
+            const std::vector<char> f = piece_layers(sp, static_cast<uint64_t>(key.stream_out));
+            g.layer_ev.assign(f.size(), nullptr);
+            for (size_t t = 0; t < f.size(); ++t)
+                if (f[t]) VCS_CUDA(cudaEventCreateWithFlags(&g.layer_ev[t], cudaEventDisableTiming));
         }
         it = sp->graphs.emplace(key, g).first;
     }
@@ -2917,14 +2941,15 @@ CachedGraph& enqueue_solve(vcs_space* sp, const GraphKey& key, cudaStream_t s) {
     // directly: a one-shot solve (build -> solve -> free, the e2e path) does not pay the capture
     // and instantiation; the second solve captures the graph every later one replays.
     // (The explicit certified pass needs the graph: its fallback is a conditional node.)
-    // (Not with the streamed download: measured on C4, direct launches interleaved with the
-    // per-layer download events idle the GPU — e2e 6.1 vs 5.75 ms; C3 gains 1.58 -> 1.41 ms.)
+    // With the streamed download too, since the download events sit only at piece boundaries
+    // and PDL chains the layers between them (C4 solve + download 4.39 vs 4.48-4.57 ms through
+    // the graph, C3 0.67 vs 0.87 ms; with an event after every layer and no PDL, direct
+    // launches had idled the GPU).
     // Small explicit spaces (k_cert_small, one launch) too: their graph would carry the whole
     // layer wavefront as the fallback body (canonical: 330 layers, 1.9 ms to capture and
     // instantiate, more than the solve); uncaptured, the fallback runs at collect.
     const bool small_explicit = cert_small_ok(sp);
-    const bool direct_ok = (sp->implicit || small_explicit) && key.method == kMethodCertified &&
-                           key.stream_out == 0;
+    const bool direct_ok = (sp->implicit || small_explicit) && key.method == kMethodCertified;
     if ((sp->implicit || small_explicit) && key.method == kMethodCertified &&
         (std::getenv("VCS_NO_GRAPH") || (direct_ok && g.uses == 0 && !g.exec &&
                                                       !std::getenv("VCS_GRAPH_FIRST")))) {
@@ -4091,7 +4116,8 @@ int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int
     // streaming the result behind per-layer events pays for large results only: a small one
     // (< 32 MB) goes in one copy after the PDL-chained pass (canonical: 331 layers, 0.8 MB)
     const bool stream_out = pinned_out && sp->S * 12 >= (32ull << 20);
-    const int rc = enqueue_impl(sp, opts, nullptr, stream_out ? 1 : 0);
+    const uint64_t row_bytes = (values_out ? 8 : 0) + (actions_out ? (narrow ? 1 : 4) : 0);
+    const int rc = enqueue_impl(sp, opts, nullptr, stream_out ? static_cast<int>(row_bytes) : 0);
     if (rc != VCS_OK) return rc;
     const vcs::CachedGraph& g = *sp->last_graph;
     const bool overlap = g.method != vcs::kMethodJacobi && !g.layer_ev.empty() && pinned_out;
@@ -4129,11 +4155,11 @@ int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int
         // Rows are final layer by layer, from the back: copy them in chunks of >= 16 MB (fewer,
         // larger DMA transfers), each after the event of its last (lowest) layer.  The terminal
         // layer's rows go with the first chunk: its memsets precede layer H-1's kernel.
-        const uint64_t row_bytes = (values_out ? 8 : 0) + (actions_out ? (narrow ? 1 : 4) : 0);
+        const std::vector<char> piece = vcs::piece_layers(sp, row_bytes);
         uint64_t chunk_end = sp->S;
         for (int t = sp->H - 1; t >= 0; --t) {
             const uint64_t r0 = sp->layer_off[t];
-            if ((chunk_end - r0) * row_bytes < (16ull << 20) && t > 0) continue;
+            if (!piece[static_cast<size_t>(t)]) continue;
             VCS_CUDA(cudaStreamWaitEvent(d, g.layer_ev[static_cast<size_t>(t)], 0));
             if (!narrow) {
                 copy_rows(r0, chunk_end, d);
