@@ -124,7 +124,9 @@ __global__ void k_emit_dense(uint32_t n, const uint64_t* __restrict__ keys,
         eidx[j] = idx;
         reward[edge_base + j] = r;
         action[edge_base + j] = a;
-        if (first_edge[idx] > j) atomicMin(&first_edge[idx], j);
+        // (the check reads L2: an SM's L1 copy of a hot entry, e.g. the single terminal state's,
+        // would stay stale and let every edge through to the serialised atomic)
+        if (__ldcg(first_edge + idx) > j) atomicMin(&first_edge[idx], j);
         ++j;
     };
     for (int p = 0; p < L.n_active; ++p) {
@@ -231,7 +233,7 @@ __global__ void k_insert_kv(const uint32_t* __restrict__ n_edges_dev,
         if (cur == kEmptyKey || cur == k) break; // claimed the slot, or the key is already there
         h = (h + 1) & mask;
     }
-    if (tidx[h] > j) atomicMin(&tidx[h], j); // the first occurrence (lowest edge index) wins
+    if (__ldcg(tidx + h) > j) atomicMin(&tidx[h], j); // the first occurrence (lowest edge index) wins
     slot_of[j] = h;
 }
 
@@ -547,6 +549,7 @@ std::vector<LayerCounters*> g_counters_free;
 
 struct Scratch {
     DevBuf<uint32_t> off, slot, rank, table, eidx;
+    DevBuf<unsigned long long> edge_count; // (pull form) E_t
     DevBuf<uint64_t> ekeys, tkey;
     DevBuf<LayerParam> params; // every layer's LayerParam (read by the degree scan)
     DevBuf<uint8_t> cub_tmp;
@@ -578,6 +581,109 @@ void exclusive_scan(Scratch& sc, InputIt in, uint32_t* out, uint64_t n, cudaStre
     sc.cub_tmp.exact(bytes, s);
     VCS_CUDA(cub::DeviceScan::ExclusiveSum(sc.cub_tmp.p, bytes, in, out, static_cast<int64_t>(n), s));
     note_launch();
+}
+
+// ---- pull form of the layered implicit builder (non-retiring transitions, see k_build_dense) --
+// k_pull_first: per successor index d' of layer t+1, the first edge min((BFS index << 3) | slot)
+// over its predecessors (the paid edge of d' itself, slot p of d' + demand*W_p), read from layer
+// t's own rank table; clears the first edge's bit in the edge-key bitmap (all ones before) and
+// sums the in-degrees (= E_t).  k_pull_rank: the BFS rank of every reached d' from the word
+// prefixes of the bitmap; rank table (coalesced) and next-layer keys (digits of d').
+__global__ void k_pull_first(const uint32_t* __restrict__ rank_self, const LayerParam* __restrict__ Lp,
+                             uint32_t Dn, uint32_t* __restrict__ first, uint32_t* bm,
+                             unsigned long long* edges) {
+    __shared__ LayerParam L;
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(LayerParam) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t*>(&L)[i] = __ldg(reinterpret_cast<const uint32_t*>(Lp) + i);
+    __syncthreads();
+    const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t deg = 0;
+    if (d < Dn) {
+        const uint32_t dem = static_cast<uint32_t>(L.demand);
+        uint32_t rk[kDenseSlots];
+        uint32_t rem = d;
+#pragma unroll
+        for (int p = 0; p < kDenseSlots - 1; ++p) {
+            rk[p] = kEmpty32;
+            if (p >= L.n_active) continue;
+            const uint32_t rad = L.radix[p];
+            const uint32_t g = rem % rad;
+            rem /= rad;
+            if (L.attr[p] && g + dem < rad) rk[p] = __ldg(rank_self + d + dem * L.wnext[p]);
+        }
+        rk[kDenseSlots - 1] = __ldg(rank_self + d); // the paid predecessor: d itself
+        uint32_t best = kEmpty32;
+#pragma unroll
+        for (int p = 0; p < kDenseSlots; ++p)
+            if (rk[p] != kEmpty32) {
+                best = min(best, (rk[p] << 3) | static_cast<uint32_t>(p));
+                ++deg;
+            }
+        first[d] = best;
+        if (best != kEmpty32) atomicAnd(bm + (best >> 5), ~(1u << (best & 31u)));
+    }
+    deg = __reduce_add_sync(0xffffffffu, deg);
+    if ((threadIdx.x & 31) == 0 && deg) atomicAdd(edges, static_cast<unsigned long long>(deg));
+}
+
+struct FirstBitsOp { // first edges in bitmap word w (the bitmap holds them as cleared bits)
+    const uint32_t* bm;
+    uint32_t nw;
+    __device__ uint32_t operator()(uint32_t w) const {
+        return w < nw ? static_cast<uint32_t>(__popc(~bm[w])) : 0u;
+    }
+};
+
+template <int WM>
+__global__ void k_pull_rank(const uint32_t* __restrict__ first, const uint32_t* __restrict__ bm,
+                            const uint32_t* __restrict__ wpre, const LayerParam* __restrict__ Lp,
+                            uint32_t Dn, uint32_t* __restrict__ rank_table,
+                            uint64_t* __restrict__ keys_next) {
+    __shared__ LayerParam L;
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(LayerParam) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t*>(&L)[i] = __ldg(reinterpret_cast<const uint32_t*>(Lp) + i);
+    __syncthreads();
+    const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= Dn) return;
+    const uint32_t f = first[d];
+    if (f == kEmpty32) {
+        rank_table[d] = kEmpty32;
+        return;
+    }
+    const uint32_t w = f >> 5;
+    const uint32_t rank = wpre[w] + static_cast<uint32_t>(__popc(~bm[w] & ((1u << (f & 31u)) - 1u)));
+    rank_table[d] = rank;
+    uint64_t nk[WM];
+#pragma unroll
+    for (int i = 0; i < WM; ++i) nk[i] = 0ull;
+    uint32_t rem = d;
+    for (int p = 0; p < L.n_active; ++p) {
+        const uint32_t rad = L.radix[p];
+        put_field<WM>(nk, L.next_bit_off[p], static_cast<uint64_t>(rem % rad));
+        rem /= rad;
+    }
+    const int nw = L.next_words;
+#pragma unroll
+    for (int i = 0; i < WM; ++i)
+        if (i < nw) keys_next[static_cast<uint64_t>(rank) * nw + i] = nk[i];
+}
+
+// A transition into a one-state layer (the terminal layer when every cloud retires): every edge
+// reaches index 0, whose first edge is the root-most state's first edge — rank 0; E_t = the
+// degree sum.
+__global__ void k_single_successor(const uint32_t* __restrict__ off_end, uint32_t* rank_table,
+                                   uint64_t* key_next, int next_words, LayerCounters* out) {
+    rank_table[0] = 0;
+    for (int w = 0; w < next_words; ++w) key_next[w] = 0ull;
+    out->n_edges = *off_end;
+    out->n_next = 1;
+}
+
+__global__ void k_pull_counters(const unsigned long long* __restrict__ edges,
+                                const uint32_t* __restrict__ wpre, uint32_t nw,
+                                LayerCounters* __restrict__ out) {
+    out->n_edges = static_cast<uint32_t>(*edges);
+    out->n_next = wpre[nw];
 }
 
 // ---- persistent dense builder ----------------------------------------------------------------
@@ -964,7 +1070,7 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
                     if (!sl.valid(e)) continue;
                     const uint32_t key = (i << 3) | static_cast<uint32_t>(e);
                     uint32_t* slot = &table[dec.idx(sl, e)];
-                    if (red || *slot > key) atomicMin(slot, key);
+                    if (red || __ldcg(slot) > key) atomicMin(slot, key);
                 }
             }
             dsum = __reduce_add_sync(0xffffffffu, dsum);
@@ -1089,7 +1195,7 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
                     uint32_t cur[SL];
 #pragma unroll
                     for (int e = 0; e < SL; ++e)
-                        if (sl.valid(e)) cur[e] = table[dec.idx(sl, e)];
+                        if (sl.valid(e)) cur[e] = __ldcg(table + dec.idx(sl, e));
 #pragma unroll
                     for (int e = 0; e < SL; ++e) {
                         const uint32_t key = (i << 3) | static_cast<uint32_t>(e);
@@ -1211,7 +1317,7 @@ __global__ void __launch_bounds__(kDenseThreads, MINB) k_build_dense(DenseBuild 
                 uint32_t cur[SL];
 #pragma unroll
                 for (int e = 0; e < SL; ++e)
-                    if (sl.valid(e)) cur[e] = table[dec.idx(sl, e)]; // the state's checks in flight
+                    if (sl.valid(e)) cur[e] = __ldcg(table + dec.idx(sl, e)); // the state's checks in flight
                 uint64_t k[WM];
                 if (EXPLICIT && retires) key_of(i, k);
 #pragma unroll
@@ -2039,6 +2145,7 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
     uint64_t S = 1, E = 0, n_t = 1;
     sp->max_layer = 1;
     constexpr uint32_t T = 256;
+    const bool pull = !std::getenv("VCS_BUILD_NO_PULL");
     double t_last = host_ms();
     if (trace_enabled())
         std::fprintf(stderr, "[vcs build] setup %.3f ms (presize %d: S<=%llu E<=%llu)\n",
@@ -2055,6 +2162,52 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
         if (E + e_ub >= 0xffffffffull)
             raise(VCS_EINVAL, "more than 2^32-1 transitions are not supported");
 
+        if (IMPLICIT && pull && L.pull && t >= 1) {
+            // pull form: no per-layer CSR scratch, no atomic per edge (see k_pull_first)
+            const uint32_t Dn = L.dense_size;
+            const uint64_t nw = (n_t * 8 + 31) / 32;
+            const uint64_t key_next = sp->key_off[static_cast<size_t>(t) + 1];
+            sp->keys.reserve(key_next + static_cast<uint64_t>(Dn) * L.next_words, key_next, s);
+            sc.table.exact(Dn, s); // first edge per successor index
+            sc.eidx.exact(nw, s);  // edge-key bitmap (a cleared bit = a first edge)
+            sc.rank.exact(nw + 1, s);
+            sc.edge_count.exact(1, s);
+            VCS_CUDA(cudaMemsetAsync(sc.eidx.p, 0xff, nw * sizeof(uint32_t), s));
+            VCS_CUDA(cudaMemsetAsync(sc.edge_count.p, 0, sizeof(unsigned long long), s));
+            k_pull_first<<<blocks_for(Dn, T), T, 0, s>>>(
+                sp->rank_tables.p + sp->rank_off[static_cast<size_t>(t) - 1], sc.params.p + t, Dn,
+                sc.table.p, sc.eidx.p, sc.edge_count.p);
+            VCS_LAUNCHED();
+            exclusive_scan(sc,
+                           thrust::make_transform_iterator(thrust::counting_iterator<uint32_t>(0),
+                                                           FirstBitsOp{sc.eidx.p, static_cast<uint32_t>(nw)}),
+                           sc.rank.p, nw + 1, s); // rank[nw] = n_{t+1}
+            k_pull_rank<WM><<<blocks_for(Dn, T), T, 0, s>>>(
+                sc.table.p, sc.eidx.p, sc.rank.p, sc.params.p + t, Dn,
+                sp->rank_tables.p + sp->rank_off[static_cast<size_t>(t)], sp->keys.p + key_next);
+            VCS_LAUNCHED();
+            k_pull_counters<<<1, 1, 0, s>>>(sc.edge_count.p, sc.rank.p, static_cast<uint32_t>(nw),
+                                            sc.counters_dev);
+            VCS_LAUNCHED();
+            VCS_CUDA(cudaStreamSynchronize(s)); // the layer's single host round trip
+        } else if (IMPLICIT && L.dense_size == 1 && pl.words[static_cast<size_t>(t) + 1] == 1 &&
+                   pl.key_bits[static_cast<size_t>(t) + 1] == 0) {
+            // into a single state (no field left): only the degree sum is needed
+            sc.off.exact(n_t + 1, s);
+            exclusive_scan(sc,
+                           thrust::make_transform_iterator(
+                               thrust::counting_iterator<uint32_t>(0),
+                               DegreeOp<WM>{sp->keys.p + key_t, static_cast<uint32_t>(n_t),
+                                            sc.params.p + t}),
+                           sc.off.p, n_t + 1, s);
+            const uint64_t key_next = sp->key_off[static_cast<size_t>(t) + 1];
+            sp->keys.reserve(key_next + 1, key_next, s);
+            k_single_successor<<<1, 1, 0, s>>>(sc.off.p + n_t,
+                                               sp->rank_tables.p + sp->rank_off[static_cast<size_t>(t)],
+                                               sp->keys.p + key_next, L.next_words, sc.counters_dev);
+            VCS_LAUNCHED();
+            VCS_CUDA(cudaStreamSynchronize(s));
+        } else {
         sc.off.exact(n_t + 1, s);
         exclusive_scan(sc,
                        thrust::make_transform_iterator(
@@ -2160,6 +2313,7 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
         k_counters<<<1, 1, 0, s>>>(e_dev, sc.rank.p, sc.counters_dev);
         VCS_LAUNCHED();
         VCS_CUDA(cudaStreamSynchronize(s)); // the layer's single host round trip
+        }
         const uint64_t E_t = sc.counters->n_edges;
         const uint64_t n_next = sc.counters->n_next;
         if (S + n_next > state_cap)

@@ -653,12 +653,17 @@ def test_concurrent_pinned_solves(gpu, golden):
             assert (vs, as_) == (g["values_sha"], g["actions_sha"])
 
 
-def test_layered_implicit_build_matches_golden(gpu, golden, monkeypatch):
+@pytest.mark.parametrize("pull", [True, False])
+def test_layered_implicit_build_matches_golden(gpu, golden, monkeypatch, pull):
     """The layered builder's implicit form (the path of spaces too large for the persistent
-    builder, e.g. C7): forced on C3/C4 with VCS_BUILD_NO_PERSISTENT, the certified pass on its
-    keys + rank tables reproduces the reference digests, and the explicit CSR materialised from
-    it later (Jacobi) gives the same bits."""
+    builder, e.g. C7), in its pull form (k_pull_first / k_pull_rank on non-retiring transitions,
+    the default) and its push form (VCS_BUILD_NO_PULL): forced on C3/C4 with
+    VCS_BUILD_NO_PERSISTENT, the certified pass on its keys + rank tables reproduces the
+    reference digests, and the explicit CSR materialised from it later (Jacobi) gives the same
+    bits."""
     monkeypatch.setenv("VCS_BUILD_NO_PERSISTENT", "1")
+    if not pull:
+        monkeypatch.setenv("VCS_BUILD_NO_PULL", "1")
     for name in ("C3", "C4"):
         p = V.load_instance(str(GOLDEN / "instances" / f"{name.lower()}.txt"))
         sp = V.StateSpace.build_native(V.NativeInstance(p.vcc, bots=p.bots), 10**9)
