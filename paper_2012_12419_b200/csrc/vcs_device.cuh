@@ -151,6 +151,7 @@ struct vcs_space {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t d2h_stream = nullptr; // result copies overlapped with the layer pass
+    cudaEvent_t order_ev = nullptr;    // a caller's solve stream waits for `stream` on it
     uint64_t S = 0, E = 0;
     int H = 0;
     int max_degree = 1;
@@ -268,4 +269,10 @@ void ensure_csr(vcs_space* sp); // materialise the explicit CSR of an implicit s
 double host_ms();
 void bind_device(int device);
 int sm_count(int device);
+// Streams and events recycled across spaces on the current device (creating and destroying them
+// costs tens of µs each: more than a tiny space's whole solve).  Released handles must be idle.
+cudaStream_t acquire_stream(int device);
+void release_stream(int device, cudaStream_t s);
+cudaEvent_t acquire_event(int device, bool timing);
+void release_event(int device, cudaEvent_t e, bool timing);
 }

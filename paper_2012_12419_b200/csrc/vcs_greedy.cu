@@ -822,12 +822,15 @@ int vcs_greedy(const vcs_instance* in, int device, int32_t* target_per_task,
         const double t0 = tr ? vcs::host_ms() : 0.0;
         const vcs::HostGreedy h = vcs::plan_greedy(in);
         const double t1 = tr ? vcs::host_ms() : 0.0;
-        cudaStream_t s = nullptr;
-        VCS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-        struct StreamGuard {
+        cudaStream_t s = vcs::acquire_stream(device);
+        struct StreamGuard { // (back to the pool once the stream-ordered frees ran)
             cudaStream_t s;
-            ~StreamGuard() { cudaStreamDestroy(s); }
-        } guard{s};
+            int device;
+            ~StreamGuard() {
+                cudaStreamSynchronize(s);
+                vcs::release_stream(device, s);
+            }
+        } guard{s, device};
         vcs::GreedyDev g;
         vcs::stage(in, h, g, s);
         vcs::launch_mask(h, g, vcs::sm_count(device), s);
@@ -871,12 +874,15 @@ int vcs_greedy_batch(int32_t n, const vcs_instance* insts, int device, int32_t**
     return guarded([&] {
         if (n <= 0) return VCS_OK;
         vcs::bind_device(device);
-        cudaStream_t s = nullptr;
-        VCS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-        struct StreamGuard {
+        cudaStream_t s = vcs::acquire_stream(device);
+        struct StreamGuard { // (back to the pool once the stream-ordered frees ran)
             cudaStream_t s;
-            ~StreamGuard() { cudaStreamDestroy(s); }
-        } guard{s};
+            int device;
+            ~StreamGuard() {
+                cudaStreamSynchronize(s);
+                vcs::release_stream(device, s);
+            }
+        } guard{s, device};
         std::vector<vcs::HostGreedy> hs;
         std::vector<std::unique_ptr<vcs::GreedyDev>> gs;
         std::vector<vcs::GreedyDesc> descs;

@@ -2061,7 +2061,7 @@ bool wavefront_fits(const vcs_space* sp) {
     return sp->ver.n >= wave_versions(sp) || need < device_bytes(sp->device) / 2;
 }
 
-void ensure_wave_buffers(vcs_space* sp) {
+void ensure_wave_buffers(vcs_space* sp, bool sync = true) {
     std::vector<uint64_t> off;
     const uint64_t nv = wave_versions(sp, &off);
     const double t0 = trace_enabled() ? host_ms() : 0.0;
@@ -2081,7 +2081,7 @@ void ensure_wave_buffers(vcs_space* sp) {
     VCS_CUDA(cudaMemcpyAsync(sp->layer_off_dev.p, sp->layer_off.data(), sp->layer_off.size() * 8,
                              cudaMemcpyHostToDevice, sp->stream));
     const double t3 = trace_enabled() ? host_ms() : 0.0;
-    VCS_CUDA(cudaStreamSynchronize(sp->stream)); // solves may run on a caller's stream
+    if (sync) VCS_CUDA(cudaStreamSynchronize(sp->stream)); // solves may run on a caller's stream
     if (trace_enabled())
         std::fprintf(stderr, "[vcs solve] offsets alloc %.3f copy %.3f sync %.3f ms\n", t2 - t1,
                      t3 - t2, host_ms() - t3);
@@ -2931,13 +2931,13 @@ CachedGraph& enqueue_solve(vcs_space* sp, const GraphKey& key, cudaStream_t s) {
         CachedGraph g;
         g.method = key.method;
         g.n_sweeps = key.max_sweeps;
-        for (auto& e : g.ev) VCS_CUDA(cudaEventCreate(&e));
+        for (auto& e : g.ev) e = acquire_event(sp->device, true);
         if (key.stream_out && (key.method == kMethodWavefront || key.method == kMethodCertified)) {
             // (stream_out = the download's bytes per state: events at its piece boundaries)
             const std::vector<char> f = piece_layers(sp, static_cast<uint64_t>(key.stream_out));
             g.layer_ev.assign(f.size(), nullptr);
             for (size_t t = 0; t < f.size(); ++t)
-                if (f[t]) VCS_CUDA(cudaEventCreateWithFlags(&g.layer_ev[t], cudaEventDisableTiming));
+                if (f[t]) g.layer_ev[t] = acquire_event(sp->device, false);
         }
         it = sp->graphs.emplace(key, g).first;
     }
@@ -2998,14 +2998,14 @@ CachedGraph& enqueue_solve(vcs_space* sp, const GraphKey& key, cudaStream_t s) {
     return g;
 }
 
-void ensure_solve_buffers(vcs_space* sp, int max_sweeps) {
+void ensure_solve_buffers(vcs_space* sp, int max_sweeps, bool sync = true) {
     const double t0 = trace_enabled() ? host_ms() : 0.0;
     sp->v[0].exact(sp->S, sp->stream);
     sp->v[1].exact(sp->S, sp->stream);
     sp->delta.exact(static_cast<size_t>(max_sweeps) + 2, sp->stream);
     sp->ctrl.exact(1, sp->stream);
     sp->actions_dev.exact(sp->S, sp->stream);
-    VCS_CUDA(cudaStreamSynchronize(sp->stream)); // pool allocations ready for any stream
+    if (sync) VCS_CUDA(cudaStreamSynchronize(sp->stream)); // pool allocations ready for any stream
     if (trace_enabled()) std::fprintf(stderr, "[vcs solve] solve buffers %.3f ms\n", host_ms() - t0);
 }
 
@@ -3626,7 +3626,9 @@ int enqueue_impl(vcs_space* sp, const vcs_solve_opts* opts, void* stream, int st
         int M = sp->H + 1; // delta_{H+1} == 0 on the layered DAG, so this is never binding
         if (o.max_sweeps > 0) M = std::min(M, o.max_sweeps);
         const double t0 = vcs::trace_enabled() ? vcs::host_ms() : 0.0;
-        vcs::ensure_solve_buffers(sp, sp->H + 1); // fixed size: cached graphs keep addresses
+        // (no host synchronisation per buffer: the solve's stream is ordered behind the space's
+        // stream once, below)
+        vcs::ensure_solve_buffers(sp, sp->H + 1, false); // fixed size: cached graphs keep addresses
         int method = o.method;
         if (method == VCS_METHOD_AUTO) // implicit spaces: the fallback's buffers come at collect
             method = sp->implicit || vcs::wavefront_fits(sp) ? VCS_METHOD_CERTIFIED
@@ -3637,7 +3639,7 @@ int enqueue_impl(vcs_space* sp, const vcs_solve_opts* opts, void* stream, int st
         if ((method == VCS_METHOD_WAVEFRONT || (method == VCS_METHOD_CERTIFIED && !sp->implicit)) &&
             sp->ver_off_host.empty()) {
             try {
-                vcs::ensure_wave_buffers(sp);
+                vcs::ensure_wave_buffers(sp, false);
             } catch (const vcs::Error&) {
                 if (o.method != VCS_METHOD_AUTO) throw;
                 cudaGetLastError();
@@ -3647,12 +3649,10 @@ int enqueue_impl(vcs_space* sp, const vcs_solve_opts* opts, void* stream, int st
         if (method == VCS_METHOD_CERTIFIED && vcs::cert_permute_space(sp) &&
             sp->cert_act_ks.n < vcs::cert_half(sp)) {
             sp->cert_act_ks.exact(vcs::cert_half(sp), sp->stream);
-            VCS_CUDA(cudaStreamSynchronize(sp->stream));
         }
         if (method == VCS_METHOD_CERTIFIED && sp->cert_xd.n < vcs::cert_pairs_needed(sp)) {
             sp->cert_xd.exact(vcs::cert_pairs_needed(sp), sp->stream);
             sp->cert_lb.exact(static_cast<size_t>(sp->H) + 2, sp->stream);
-            VCS_CUDA(cudaStreamSynchronize(sp->stream));
         }
         if (method == VCS_METHOD_CERTIFIED && sp->implicit && vcs::cert_stream_space(sp))
             vcs::ensure_stream_plan(sp);
@@ -3663,6 +3663,11 @@ int enqueue_impl(vcs_space* sp, const vcs_solve_opts* opts, void* stream, int st
                                 method == VCS_METHOD_JACOBI && o.skip_converged ? 1 : 0, M,
                                 method, method != VCS_METHOD_JACOBI ? stream_out : 0};
         const vcs::StreamUse s(sp, stream);
+        if (static_cast<cudaStream_t>(s) != sp->stream) { // the buffers above, then the solve
+            if (!sp->order_ev) sp->order_ev = vcs::acquire_event(sp->device, false);
+            VCS_CUDA(cudaEventRecord(sp->order_ev, sp->stream));
+            VCS_CUDA(cudaStreamWaitEvent(s, sp->order_ev, 0));
+        }
         auto& g = vcs::enqueue_solve(sp, key, s);
         sp->last_graph = &g;
         sp->last_key_skip = key.skip;
@@ -4130,8 +4135,7 @@ int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int
     // Stream each layer's values/actions to the (pinned) host buffers as soon as its layer
     // kernel finished — the 12 B/state download overlaps the rest of the layer pass.
     const int rc2 = guarded([&] {
-        if (!sp->d2h_stream)
-            VCS_CUDA(cudaStreamCreateWithFlags(&sp->d2h_stream, cudaStreamNonBlocking));
+        if (!sp->d2h_stream) sp->d2h_stream = vcs::acquire_stream(sp->device);
         cudaStream_t d = sp->d2h_stream;
         int8_t* staging = nullptr;
         size_t staging_bytes = 0;
@@ -4180,11 +4184,7 @@ int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int
                 VCS_LAUNCHED();
                 VCS_CUDA(cudaMemcpyAsync(staging + r0, sp->act8_dev.p + r0, n, cudaMemcpyDeviceToHost, d));
                 const size_t k = pieces.size();
-                if (sp->piece_ev.size() <= k) {
-                    cudaEvent_t e = nullptr;
-                    VCS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-                    sp->piece_ev.push_back(e);
-                }
+                if (sp->piece_ev.size() <= k) sp->piece_ev.push_back(vcs::acquire_event(sp->device, false));
                 VCS_CUDA(cudaEventRecord(sp->piece_ev[k], d));
                 pieces.push_back(Piece{r0, chunk_end, sp->piece_ev[k]});
             }

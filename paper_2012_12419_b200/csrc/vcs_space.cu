@@ -2577,6 +2577,79 @@ int sm_count(int device) {
     return v;
 }
 
+namespace {
+struct HandlePool {
+    std::mutex mu;
+    std::vector<std::pair<int, cudaStream_t>> streams;
+    std::vector<std::pair<int, cudaEvent_t>> events[2]; // [timing]
+};
+HandlePool& handle_pool() {
+    static HandlePool* p = new HandlePool; // never destroyed: handles die with the context
+    return *p;
+}
+constexpr size_t kPoolStreams = 32, kPoolEvents = 1024;
+} // namespace
+
+cudaStream_t acquire_stream(int device) {
+    {
+        HandlePool& P = handle_pool();
+        std::lock_guard<std::mutex> lock(P.mu);
+        for (size_t i = P.streams.size(); i-- > 0;)
+            if (P.streams[i].first == device) {
+                cudaStream_t s = P.streams[i].second;
+                P.streams.erase(P.streams.begin() + static_cast<std::ptrdiff_t>(i));
+                return s;
+            }
+    }
+    cudaStream_t s = nullptr;
+    VCS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    return s;
+}
+
+void release_stream(int device, cudaStream_t s) {
+    if (!s) return;
+    {
+        HandlePool& P = handle_pool();
+        std::lock_guard<std::mutex> lock(P.mu);
+        if (P.streams.size() < kPoolStreams) {
+            P.streams.emplace_back(device, s);
+            return;
+        }
+    }
+    cudaStreamDestroy(s);
+}
+
+cudaEvent_t acquire_event(int device, bool timing) {
+    {
+        HandlePool& P = handle_pool();
+        std::lock_guard<std::mutex> lock(P.mu);
+        auto& v = P.events[timing ? 1 : 0];
+        for (size_t i = v.size(); i-- > 0;)
+            if (v[i].first == device) {
+                cudaEvent_t e = v[i].second;
+                v.erase(v.begin() + static_cast<std::ptrdiff_t>(i));
+                return e;
+            }
+    }
+    cudaEvent_t e = nullptr;
+    VCS_CUDA(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+    return e;
+}
+
+void release_event(int device, cudaEvent_t e, bool timing) {
+    if (!e) return;
+    {
+        HandlePool& P = handle_pool();
+        std::lock_guard<std::mutex> lock(P.mu);
+        auto& v = P.events[timing ? 1 : 0];
+        if (v.size() < kPoolEvents) {
+            v.emplace_back(device, e);
+            return;
+        }
+    }
+    cudaEventDestroy(e);
+}
+
 } // namespace vcs
 
 vcs_space::~vcs_space() {
@@ -2589,17 +2662,15 @@ vcs_space::~vcs_space() {
         cudaEventDestroy(ev);
     }
     if (stream) cudaStreamSynchronize(stream);
+    if (d2h_stream) cudaStreamSynchronize(d2h_stream);
     for (auto& [k, g] : graphs) {
         if (g.exec) cudaGraphExecDestroy(g.exec);
-        for (auto& e : g.ev)
-            if (e) cudaEventDestroy(e);
-        for (auto& e : g.layer_ev)
-            if (e) cudaEventDestroy(e);
+        for (auto& e : g.ev) vcs::release_event(device, e, true);
+        for (auto& e : g.layer_ev) vcs::release_event(device, e, false);
     }
-    for (auto e : piece_ev)
-        if (e) cudaEventDestroy(e);
-    if (d2h_stream) cudaStreamSynchronize(d2h_stream);
-    if (d2h_stream) cudaStreamDestroy(d2h_stream);
+    for (auto e : piece_ev) vcs::release_event(device, e, false);
+    vcs::release_event(device, order_ev, false);
+    vcs::release_stream(device, d2h_stream);
     if (aux_stream) cudaStreamDestroy(aux_stream);
     // the stream is idle: big blocks go to the per-device cache for the next space, the rest
     // back to the pool (stream-ordered frees are issued while the stream is alive)
@@ -2632,7 +2703,7 @@ vcs_space::~vcs_space() {
     // destroyed stream below)
     if (stream) {
         cudaStreamSynchronize(stream);
-        cudaStreamDestroy(stream);
+        vcs::release_stream(device, stream);
     }
 }
 
@@ -2645,7 +2716,7 @@ std::unique_ptr<vcs_space> new_space(int device) {
     auto sp = std::make_unique<vcs_space>();
     sp->device = device;
     sp->num_sms = vcs::sm_count(device);
-    VCS_CUDA(cudaStreamCreateWithFlags(&sp->stream, cudaStreamNonBlocking));
+    sp->stream = vcs::acquire_stream(device);
     return sp;
 }
 } // namespace
