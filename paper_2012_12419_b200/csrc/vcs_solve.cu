@@ -1555,7 +1555,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_cert_dense_tma(CertImplArgs 
 // (r_cloud_kept) and the paid edge r_paid_kept; the eligible slots and their byte offsets are
 // per-layer uniforms.  ~2x fewer instructions per index than the generic walk (390 SASS
 // instructions per iteration there); same operations on every edge, same strict first maximum.
-template <bool DISC>
+template <bool DISC, bool EARLY = false>
 __global__ void __launch_bounds__(256, 3) k_cert_dense_nr(CertImplArgs a) {
     __shared__ LayerParam sL;
     __shared__ unsigned long long s_lb;
@@ -1588,6 +1588,7 @@ __global__ void __launch_bounds__(256, 3) k_cert_dense_nr(CertImplArgs a) {
     uint32_t rn = d < d_hi ? __ldg(a.rank_self + d) : kEmpty32;
     double dmax = 0.0;
     asm volatile("griddepcontrol.wait;" ::: "memory"); // (PDL) the previous layer's pairs
+    if (EARLY) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     for (; d < d_hi; d += stride) {
         const uint32_t r = rn;
         if (d + stride < d_hi) rn = __ldg(a.rank_self + d + stride);
@@ -1654,7 +1655,154 @@ __global__ void __launch_bounds__(256, 3) k_cert_dense_nr(CertImplArgs a) {
     __syncthreads();
     if (threadIdx.x == 0 && s_lb)
         atomicMax(reinterpret_cast<unsigned long long*>(a.lb + a.m), s_lb);
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); // (late: measured 4.91 vs 4.95 ms on C7 with the early trigger)
+    // (with the gather pass the late trigger measured better on C7: 4.91 vs 4.95 ms)
+    if (!EARLY) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// ---- k_cert_dense_win: the non-retiring key-space walk with the near successors in shared memory
+// The dense layers are bound by L2 (LTS) throughput: ~108 MB of sector traffic per C4 layer of
+// 531,441 indices against ~25 MB of algorithmic bytes, two thirds of it the eight shifted pair
+// gathers.  On a non-retiring transition the successor of d through cloud slot p is d - c_p
+// (c_p = demand * W_p) and the paid one d itself, so for a tile of 256 consecutive indices the
+// slots with small shifts (c_p <= kWinShift: W = 1, 9, 81 at radix 9) and the paid slot read ONE
+// window [d0 - c_max, d0 + 256) of layer t+1's pairs.  Each block stages its tile's window in
+// shared memory with cp.async (double-buffered: the next tile's window streams in while this one
+// computes) and gathers only the far slots from global memory.  Same operations, slot order and
+// strict first maximum as k_cert_dense_nr, so the same bits.
+constexpr int kWinT = 256;
+constexpr int kWinShift = 512; // largest shift served from shared memory
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+
+template <bool DISC>
+__global__ void __launch_bounds__(kWinT, 3) k_cert_dense_win(CertImplArgs a) {
+    __shared__ LayerParam sL;
+    __shared__ unsigned long long s_lb;
+    __shared__ __align__(16) double2 win[2][kWinT + kWinShift];
+    load_layer_param(sL, a.L, s_lb);
+    const LayerParam& L = sL;
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int NF = kDenseSlots - 1;
+    const int na = L.n_active;
+    const int tid = threadIdx.x;
+    const uint32_t dem = static_cast<uint32_t>(L.demand);
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWinT;
+    const uint64_t d_hi = a.d_hi;
+    uint64_t d0 = a.d_lo + static_cast<uint64_t>(blockIdx.x) * kWinT; // this tile's first index
+    uint64_t d = d0 + tid;
+    uint32_t g[NF], sd[NF], rad[NF], off[NF];
+    uint32_t elig = 0, near = 0, cmax = 0;
+    {
+        uint32_t rem = static_cast<uint32_t>(d < d_hi ? d : 0);
+        uint32_t srem = static_cast<uint32_t>(stride < a.dense_n ? stride : 0);
+#pragma unroll
+        for (int p = 0; p < NF; ++p) {
+            rad[p] = p < na ? L.radix[p] : 1u;
+            g[p] = rem % rad[p];
+            rem /= rad[p];
+            sd[p] = srem % rad[p];
+            srem /= rad[p];
+            off[p] = p < na ? dem * L.wnext[p] : 0u;
+            if (p < na && L.attr[p]) elig |= 1u << p;
+            if (p < na && off[p] <= static_cast<uint32_t>(kWinShift)) {
+                near |= 1u << p;
+                cmax = max(cmax, off[p]);
+            }
+        }
+    }
+    const uint32_t wlen = kWinT + cmax; // window [d0 - cmax, d0 + kWinT)
+    const double r_cloud = L.r_cloud_kept, r_paid = L.r_paid_kept;
+    uint32_t rn = d < d_hi ? __ldg(a.rank_self + d) : kEmpty32;
+    double dmax = 0.0;
+    // the window of the tile starting at t0 into buffer b (indices outside [0, d_hi) are not read)
+    auto stage = [&](uint64_t t0, int b) {
+        for (uint32_t i = tid; i < wlen; i += kWinT) {
+            const int64_t src = static_cast<int64_t>(t0) - static_cast<int64_t>(cmax) + i;
+            if (src >= 0 && static_cast<uint64_t>(src) < d_hi) cp_async16(&win[b][i], a.xd_next + src);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    asm volatile("griddepcontrol.wait;" ::: "memory"); // (PDL) the previous layer's pairs
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); // (early: see cert_implicit_layer)
+    if (d0 < d_hi) stage(d0, 0);
+    for (int k = 0; d0 < d_hi; ++k, d0 += stride, d += stride) {
+        const int b = k & 1;
+        if (d0 + stride < d_hi) {
+            stage(d0 + stride, b ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads(); // this tile's window is complete
+        const uint32_t r = rn;
+        if (d + stride < d_hi) rn = __ldg(a.rank_self + d + stride);
+        uint32_t mask = 0;
+#pragma unroll
+        for (int p = 0; p < NF; ++p) mask |= (g[p] >= dem ? 1u : 0u) << p;
+        mask &= elig;
+        {
+            uint32_t carry = 0;
+#pragma unroll
+            for (int p = 0; p < NF; ++p) {
+                const uint32_t v = g[p] + sd[p] + carry;
+                carry = v >= rad[p] ? 1u : 0u;
+                g[p] = carry ? v - rad[p] : v;
+            }
+        }
+        if (d < d_hi && r != kEmpty32) {
+            const double2* W = &win[b][tid + cmax]; // the pair of index d
+            double2 x[NF];
+#pragma unroll
+            for (int p = 0; p < NF; ++p)
+                if ((mask >> p) & 1u) x[p] = ((near >> p) & 1u) ? W[-static_cast<int>(off[p])]
+                                                                 : __ldg(a.xd_next + d - off[p]);
+            const double2 xp = W[0];
+            double hi = -INFINITY, lo = -INFINITY;
+            int best = -1;
+#pragma unroll
+            for (int p = 0; p < NF; ++p) {
+                if (!((mask >> p) & 1u)) continue;
+                const double qx = DISC ? __dadd_rn(r_cloud, __dmul_rn(a.discount, x[p].x)) : __dadd_rn(r_cloud, x[p].x);
+                const double qy = DISC ? __dadd_rn(r_cloud, __dmul_rn(a.discount, x[p].y)) : __dadd_rn(r_cloud, x[p].y);
+                if (qy > hi) { // strict: the first maximal edge wins (mdp.cpp:254-260)
+                    hi = qy;
+                    best = p;
+                }
+                if (qx > lo) lo = qx;
+            }
+            {
+                const double qx = DISC ? __dadd_rn(r_paid, __dmul_rn(a.discount, xp.x)) : __dadd_rn(r_paid, xp.x);
+                const double qy = DISC ? __dadd_rn(r_paid, __dmul_rn(a.discount, xp.y)) : __dadd_rn(r_paid, xp.y);
+                if (qy > hi) {
+                    hi = qy;
+                    best = -1;
+                }
+                if (qx > lo) lo = qx;
+            }
+            if (a.m == 1) lo = 0.0; // V_0
+            a.xd_cur[d] = make_double2(lo, hi);
+            if (a.write_out) {
+                a.values_out[a.row0 + r] = hi;
+                a.act_out[a.row0 + r] = best < 0 ? -1 : L.cloud[best];
+            }
+            const double dd = fabs(hi - lo);
+            dmax = dmax < dd ? dd : dmax;
+        }
+        __syncthreads(); // the window buffer is free for the tile after next
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double other = __shfl_xor_sync(FULL, dmax, o);
+        dmax = dmax < other ? other : dmax;
+    }
+    if ((tid & 31) == 0 && dmax > 0.0)
+        atomicMax(&s_lb, static_cast<unsigned long long>(__double_as_longlong(dmax)));
+    __syncthreads();
+    if (tid == 0 && s_lb) atomicMax(reinterpret_cast<unsigned long long*>(a.lb + a.m), s_lb);
 }
 
 // (VCS_CERT_PERMUTE experiment) layer t's results in BFS order from the key-space-ordered pairs
@@ -2389,7 +2537,38 @@ void launch_cert_layer(const vcs_space* sp, const CertData& data, const CertLaye
     const bool dense_order = L.dense_order;
     // the non-retiring walk pays with the gather pass on layers beyond L2 (C7); on L2-resident
     // layers (C4) the generic walk measured as fast or faster (0.517 vs 0.530 ms)
-    if (dense_order && ks && cert_nonretiring(sp, t) && cert_permute_layer(L.dense_n) &&
+    static const bool win_on = std::getenv("VCS_CERT_WIN") != nullptr;
+    if (dense_order && ks && cert_nonretiring(sp, t) && !cert_permute_layer(L.dense_n) && win_on &&
+        !std::getenv("VCS_CERT_GENERIC") && !std::getenv("VCS_CERT_TMA") &&
+        !std::getenv("VCS_CERT_ILP2")) {
+        // the near successors from a shared-memory window per tile (k_cert_dense_win)
+        const void* fn = disc ? reinterpret_cast<const void*>(k_cert_dense_win<true>)
+                              : reinterpret_cast<const void*>(k_cert_dense_win<false>);
+        static thread_local std::map<std::pair<const void*, int>, int> occ_win;
+        int dev = 0;
+        VCS_CUDA(cudaGetDevice(&dev));
+        int& per_sm = occ_win[{fn, dev}];
+        if (!per_sm) VCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kWinT, 0));
+        const uint64_t items = L.d_hi > L.d_lo ? L.d_hi - L.d_lo : 0;
+        const uint64_t blocks = std::max<uint64_t>(
+            1, std::min<uint64_t>((items + kWinT - 1) / kWinT,
+                                  static_cast<uint64_t>(std::max(1, per_sm)) * sp->num_sms));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+        cfg.blockDim = dim3(kWinT);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl ? 1 : 0;
+        if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense_win<true>, c));
+        else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense_win<false>, c));
+        VCS_LAUNCHED();
+        return;
+    }
+    static const bool nr_all = std::getenv("VCS_CERT_NR") != nullptr; // (measurement switch)
+    if (dense_order && ks && cert_nonretiring(sp, t) && (cert_permute_layer(L.dense_n) || nr_all) &&
         !std::getenv("VCS_CERT_GENERIC") && !std::getenv("VCS_CERT_TMA") &&
         !std::getenv("VCS_CERT_ILP2")) {
         const void* fn = disc ? reinterpret_cast<const void*>(k_cert_dense_nr<true>)
@@ -2418,8 +2597,13 @@ void launch_cert_layer(const vcs_space* sp, const CertData& data, const CertLaye
         const bool permute = sp->cert_act_ks.p && c.write_out && L.d_lo == 0 &&
                              L.d_hi == L.dense_n && cert_permute_layer(L.dense_n);
         if (permute) cx.act_ks = sp->cert_act_ks.p;
-        if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense_nr<true>, cx));
-        else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense_nr<false>, cx));
+        if (permute) {
+            if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense_nr<true, false>, cx));
+            else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense_nr<false, false>, cx));
+        } else {
+            if (disc) VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense_nr<true, true>, cx));
+            else VCS_CUDA(cudaLaunchKernelEx(&cfg, k_cert_dense_nr<false, true>, cx));
+        }
         if (permute) {
             VCS_LAUNCHED();
             dispatch_words_solve(max_key_words(sp), [&](auto wm) {

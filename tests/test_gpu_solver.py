@@ -748,13 +748,15 @@ def test_certified_ilp2_kernel_matches_golden(gpu, golden, monkeypatch):
         assert sha(r.policy.raw_actions()) == g["actions_sha"]
 
 
-@pytest.mark.parametrize("kernel", ["generic", "permute"])
+@pytest.mark.parametrize("kernel", ["generic", "permute", "nr", "win"])
 def test_certified_kernel_variants_match_golden(gpu, golden, monkeypatch, kernel):
     """The generic key-space walk (VCS_CERT_GENERIC=1, the retiring-capable kernel on every
-    layer) and the non-retiring walk with key-space-ordered results + gather pass
-    (VCS_CERT_PERMUTE=1, the default only for pair vectors beyond L2) reproduce the reference's
-    digests on C3 and C4."""
-    monkeypatch.setenv("VCS_CERT_GENERIC" if kernel == "generic" else "VCS_CERT_PERMUTE", "1")
+    layer), the non-retiring walk with key-space-ordered results + gather pass
+    (VCS_CERT_PERMUTE=1, the default only for pair vectors beyond L2), the non-retiring walk
+    writing at the BFS rank (VCS_CERT_NR=1) and its shared-memory-window form (VCS_CERT_WIN=1)
+    reproduce the reference's digests on C3 and C4."""
+    monkeypatch.setenv({"generic": "VCS_CERT_GENERIC", "permute": "VCS_CERT_PERMUTE",
+                        "nr": "VCS_CERT_NR", "win": "VCS_CERT_WIN"}[kernel], "1")
     for name in ("C3", "C4"):
         p = V.load_instance(str(GOLDEN / "instances" / f"{name.lower()}.txt"))
         sp = V.StateSpace.build_native(V.NativeInstance(p.vcc, bots=p.bots), 10**9)
