@@ -4281,6 +4281,17 @@ void vcs_host_free(void* p) {
 
 uint64_t vcs_space_result_generation(const vcs_space* sp) { return sp->result_gen; }
 
+namespace {
+// results of at least this many bytes (12 per state) stream behind the layer pass
+uint64_t stream_threshold() {
+    static const uint64_t v = [] {
+        const char* e = std::getenv("VCS_STREAM_MIN_MB");
+        return static_cast<uint64_t>(e ? std::atof(e) * (1 << 20) : 32.0 * (1 << 20));
+    }();
+    return v;
+}
+} // namespace
+
 int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int32_t* actions_out,
               vcs_solve_report* report) {
     std::lock_guard<std::recursive_mutex> space_lock(sp->mu);
@@ -4298,7 +4309,7 @@ int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int
     // is allocated before the solve is enqueued so the download stream, which waits on the
     // solve's layer events, is ordered after the allocation
     const bool narrow = pinned_out && actions_out && sp->has_plan && sp->plan.n_clouds <= 127 &&
-                        sp->S * 12 >= (32ull << 20) && !std::getenv("VCS_NO_NARROW");
+                        sp->S * 12 >= stream_threshold() && !std::getenv("VCS_NO_NARROW");
     if (narrow) {
         const int rca = guarded([&] {
             vcs::bind_device(sp->device);
@@ -4309,7 +4320,7 @@ int vcs_solve(vcs_space* sp, const vcs_solve_opts* opts, double* values_out, int
     }
     // streaming the result behind per-layer events pays for large results only: a small one
     // (< 32 MB) goes in one copy after the PDL-chained pass (canonical: 331 layers, 0.8 MB)
-    const bool stream_out = pinned_out && sp->S * 12 >= (32ull << 20);
+    const bool stream_out = pinned_out && sp->S * 12 >= stream_threshold();
     const uint64_t row_bytes = (values_out ? 8 : 0) + (actions_out ? (narrow ? 1 : 4) : 0);
     const int rc = enqueue_impl(sp, opts, nullptr, stream_out ? static_cast<int>(row_bytes) : 0);
     if (rc != VCS_OK) return rc;
