@@ -1532,8 +1532,26 @@ bool build_dense(vcs_space* sp, uint64_t state_cap) {
     }
     sp->rank_tables.exact(rank_total, s);
     // unreached successor indices read as kEmpty32 (the certified pass walks layers in key-space
-    // order and skips them)
-    if (rank_total) VCS_CUDA(cudaMemsetAsync(sp->rank_tables.p, 0xff, rank_total * sizeof(uint32_t), s));
+    // order and skips them).  The pull form writes every entry of its transitions' tables: only
+    // the push transitions' runs are cleared (C4: 6 of 48).
+    {
+        // (the kernel's own condition for the pull form, A.pull included)
+        const bool pull_on = !EXPLICIT && WM == 1 && G <= kPullMaxBlocks && !std::getenv("VCS_BUILD_NO_PULL");
+        uint64_t off = 0, run0 = 0, run = 0;
+        for (int t = 0; t < H; ++t) {
+            const LayerParam& L = pl.layers[static_cast<size_t>(t)];
+            const bool pulled = pull_on && L.pull && t >= 1 && L.dense_size <= 8 * T;
+            if (!pulled) {
+                if (!run) run0 = off;
+                run += L.dense_size;
+            }
+            if ((pulled || t + 1 == H) && run) {
+                VCS_CUDA(cudaMemsetAsync(sp->rank_tables.p + run0, 0xff, run * sizeof(uint32_t), s));
+                run = 0;
+            }
+            off += L.dense_size;
+        }
+    }
     DevBuf<uint32_t> tables, bsum;
     DevBuf<uint64_t> desc;
     DevBuf<uint32_t> jfirst;
@@ -1577,7 +1595,7 @@ bool build_dense(vcs_space* sp, uint64_t state_cap) {
     A.dense_max = static_cast<uint32_t>(dense_max);
     A.max_rounds = max_rounds;
     A.H = H;
-    A.pull = (G <= kPullMaxBlocks && !std::getenv("VCS_BUILD_NO_PULL")) ? 1 : 0;
+    A.pull = (G <= kPullMaxBlocks && !std::getenv("VCS_BUILD_NO_PULL")) ? 1 : 0; // (as above)
     void* args[] = {&A};
     const double t_launch = trace_enabled() ? host_ms() : 0.0;
     VCS_CUDA(cudaLaunchCooperativeKernel(fn, G, kDenseThreads, args, 0, s));
