@@ -201,6 +201,7 @@ struct vcs_space {
     int cert_tail_t = -1;
     bool cert_tail_ready = false;
     vcs::DevBuf<double> cert_lb;
+    vcs::DevBuf<unsigned long long> cert_tl; // (VCS_CERT_TIMELINE) per-layer timeline stamps
     cudaStream_t aux_stream = nullptr; // captures the fallback body of the certified graph
     std::map<vcs::GraphKey, vcs::CachedGraph> graphs;
     vcs::CachedGraph* last_graph = nullptr; // graph of the last vcs_solve_enqueue

@@ -901,7 +901,17 @@ struct CertImplArgs {
     // key-space order: the indices [d_lo, d_hi) of this launch (the whole key space on one GPU,
     // a rank's contiguous share when the layer is sharded across GPUs)
     uint64_t d_lo, d_hi;
+    // (VCS_CERT_TIMELINE) per layer m: globaltimer of the first block's entry, the first block
+    // past the PDL wait, and the last block's exit (stored inverted: all three by atomicMin)
+    unsigned long long* tl;
 };
+
+__device__ __forceinline__ void tl_stamp(unsigned long long* tl, int m, int k) {
+    if (!tl || threadIdx.x != 0) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(tl + 3 * m + k, k == 2 ? ~t : t);
+}
 
 // One layer of the implicit certified pass over states first_i, first_i + stride, ... (the
 // block has loaded the layer's LayerParam into sL and zeroed s_lb).  DXD: the pairs are stored
@@ -920,9 +930,11 @@ __device__ __forceinline__ void cert_implicit_layer(const CertImplArgs& a, const
     uint64_t i = first_i;
     uint64_t kn[WM] = {}; // the next state's key, loaded while the current state computes
     if (i < a.n) load_key<WM>(a.keys + i * static_cast<uint64_t>(words), words, kn);
+    tl_stamp(a.tl, a.m, 0);
     // programmatic dependent launch: everything above reads only build outputs; the previous
     // layer's pairs (and this layer's outputs) are touched after the wait
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    tl_stamp(a.tl, a.m, 1);
     // the next layer may launch now: its blocks take the slots this grid frees, run their
     // prologue and wait for this grid to complete (griddepcontrol.wait orders the data)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -988,6 +1000,7 @@ __device__ __forceinline__ void cert_implicit_layer(const CertImplArgs& a, const
     __syncthreads();
     if (threadIdx.x == 0 && s_lb)
         atomicMax(reinterpret_cast<unsigned long long*>(a.lb + a.m), s_lb);
+    tl_stamp(a.tl, a.m, 2);
     // (the next layer was allowed to launch right after the wait above)
 }
 
@@ -1031,7 +1044,9 @@ __device__ __forceinline__ void cert_dense_layer(const CertImplArgs& a, const La
         if (p < na && L.keep_idx[p] < 0) retmask |= 1u << p;
     const double r_cl = L.r_cloud, r_pd = L.r_paid, gam = L.gamma;
     const int dem = L.demand;
+    tl_stamp(a.tl, a.m, 0);
     asm volatile("griddepcontrol.wait;" ::: "memory"); // (PDL) the previous layer's pairs
+    tl_stamp(a.tl, a.m, 1);
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); // (as in cert_implicit_layer)
     for (; d < d_hi; d += stride) {
         const uint32_t r = rn;
@@ -1102,6 +1117,7 @@ __device__ __forceinline__ void cert_dense_layer(const CertImplArgs& a, const La
     __syncthreads();
     if (threadIdx.x == 0 && s_lb)
         atomicMax(reinterpret_cast<unsigned long long*>(a.lb + a.m), s_lb);
+    tl_stamp(a.tl, a.m, 2);
     // (the next layer was allowed to launch right after the wait above)
 }
 
@@ -2461,7 +2477,7 @@ CertLayer cert_layer(const vcs_space* sp, int t, double2* xd, uint64_t half, boo
         L.dense_n = t >= 1 ? sp->plan.layers[static_cast<size_t>(t - 1)].dense_size : 0;
         // walk the key space when at least half of it is reached (coalesced pair writes, no
         // key loads); sparse layers walk their states
-        L.dense_order = t >= 1 && L.n * 2 >= L.dense_n;
+        L.dense_order = t >= 1 && L.n * 2 >= L.dense_n; // (0.4 / 0.3 / 0.2 measured the same on C4)
     } else {
         L.xd_next = xd + sp->layer_off[t + 1];
         L.xd_cur = xd + L.row0;
@@ -2527,6 +2543,7 @@ void launch_cert_layer(const vcs_space* sp, const CertData& data, const CertLaye
     c.xd_next = L.xd_next;
     c.xd_cur = L.xd_cur;
     c.write_out = write_out;
+    c.tl = sp->cert_tl.n ? sp->cert_tl.p : nullptr;
     if (ks) {
         c.dense_n = L.dense_n;
         c.rank_self = t >= 1 ? data.rank_tables + sp->rank_off[static_cast<size_t>(t - 1)] : nullptr;
@@ -3846,6 +3863,12 @@ int enqueue_impl(vcs_space* sp, const vcs_solve_opts* opts, void* stream, int st
         const vcs::GraphKey key{o.epsilon, o.discount,
                                 method == VCS_METHOD_JACOBI && o.skip_converged ? 1 : 0, M,
                                 method, method != VCS_METHOD_JACOBI ? stream_out : 0};
+        static const bool timeline = std::getenv("VCS_CERT_TIMELINE") != nullptr;
+        if (timeline && method == VCS_METHOD_CERTIFIED) {
+            const size_t n_tl = 3 * (static_cast<size_t>(sp->H) + 2);
+            if (sp->cert_tl.n < n_tl) sp->cert_tl.exact(n_tl, sp->stream);
+            VCS_CUDA(cudaMemsetAsync(sp->cert_tl.p, 0xff, n_tl * sizeof(unsigned long long), sp->stream));
+        }
         const vcs::StreamUse s(sp, stream);
         if (static_cast<cudaStream_t>(s) != sp->stream) { // the buffers above, then the solve
             if (!sp->order_ev) sp->order_ev = vcs::acquire_event(sp->device, false);
@@ -4429,6 +4452,21 @@ int vcs_solve_collect(vcs_space* sp, double* values_out, int32_t* actions_out,
         if (!sp->last_graph) raise(VCS_EINVAL, "no solve was enqueued on this space");
         vcs::bind_device(sp->device);
         const vcs::StreamUse s(sp, stream);
+        if (sp->cert_tl.n && std::getenv("VCS_CERT_TIMELINE")) { // per-layer timeline, stderr
+            std::vector<unsigned long long> tl(sp->cert_tl.n);
+            VCS_CUDA(cudaMemcpyAsync(tl.data(), sp->cert_tl.p, tl.size() * 8, cudaMemcpyDeviceToHost, s));
+            VCS_CUDA(cudaStreamSynchronize(s));
+            unsigned long long t0 = ~0ull;
+            for (size_t m = 0; 3 * m + 2 < tl.size(); ++m) t0 = std::min(t0, tl[3 * m]);
+            std::fprintf(stderr, "[vcs timeline] layer: entry / past-wait / exit (us from the first entry)\n");
+            for (int m = sp->H; m >= 1; --m) {
+                const unsigned long long* e = tl.data() + 3 * static_cast<size_t>(m);
+                if (e[0] == ~0ull) continue;
+                std::fprintf(stderr, "[vcs timeline] t=%d n=%llu: %.2f / %.2f / %.2f\n", sp->H - m,
+                             static_cast<unsigned long long>(sp->layer_off[sp->H - m + 1] - sp->layer_off[sp->H - m]),
+                             (e[0] - t0) * 1e-3, (e[1] - t0) * 1e-3, (~e[2] - t0) * 1e-3);
+            }
+        }
         vcs::SolveCtrl ctrl{};
         VCS_CUDA(cudaMemcpyAsync(&ctrl, sp->ctrl.p, sizeof ctrl, cudaMemcpyDeviceToHost, s));
         VCS_CUDA(cudaStreamSynchronize(s));

@@ -2710,6 +2710,7 @@ vcs_space::~vcs_space() {
     stream_sync.release_idle();
     cert_tail_meta.release_idle();
     cert_lb.release_idle();
+    cert_tl.release_idle();
     band_ver.release_idle();
     ver_off.release_idle();
     layer_off_dev.release_idle();
