@@ -649,6 +649,16 @@ __global__ void __launch_bounds__(kWaveWarps * 32) k_wave_extract(WaveArgs a, in
 // lb_k >= eps for all k <= H proves K* = H+1 (delta_{H+1} = 0 ends the reference's loop): the
 // pass is then the whole solve, bit for bit.  Otherwise the full wavefront runs (graph IF node).
 
+// Warp maximum of a non-negative double as its bit pattern (the order of non-negative doubles is
+// the order of their bits): two integer reductions instead of five 64-bit shuffle rounds.
+__device__ __forceinline__ unsigned long long warp_max_nonneg_bits(double v) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+    const uint32_t hi = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(b >> 32));
+    const uint32_t lo = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(b >> 32) == hi
+                                                           ? static_cast<uint32_t>(b) : 0u);
+    return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
+
 struct CertArgs {
     const uint32_t* __restrict__ row_ptr;
     const uint32_t* __restrict__ succ;
@@ -862,13 +872,8 @@ k_cert_small(CertArgs a, const uint64_t* __restrict__ layer_off, int H) {
             const double d = fabs(hi - lo);
             dmax = dmax < d ? d : dmax;
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double other = __shfl_xor_sync(0xffffffffu, dmax, o);
-            dmax = dmax < other ? other : dmax;
-        }
-        if ((tid & 31) == 0 && dmax > 0.0)
-            atomicMax(&s_lb[b], static_cast<unsigned long long>(__double_as_longlong(dmax)));
+        const unsigned long long wm = warp_max_nonneg_bits(dmax);
+        if ((tid & 31) == 0 && wm) atomicMax(&s_lb[b], wm);
     }
     __syncthreads();
     if (tid == 0 && H >= 1 && s_lb[0]) a.lb[H] = __longlong_as_double(static_cast<long long>(s_lb[0]));
