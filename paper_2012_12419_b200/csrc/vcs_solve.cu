@@ -3003,6 +3003,9 @@ void record_certified(vcs_space* sp, const GraphKey& key, CachedGraph& g, cudaSt
         VCS_CUDA(cudaLaunchKernel(fn_small, dim3(1), dim3(nt), args, smem, s));
         VCS_LAUNCHED();
         launches = 1;
+        // every layer is final when the one launch is: the download's piece events follow it
+        for (cudaEvent_t e : g.layer_ev)
+            if (e) record_event(e, s, capturing);
     }
     for (int t = launches ? -1 : H - 1; t >= 0; --t) {
         a.row0 = sp->layer_off[t];
@@ -4311,12 +4314,9 @@ uint64_t vcs_space_result_generation(const vcs_space* sp) { return sp->result_ge
 
 namespace {
 // results of at least this many bytes (12 per state) stream behind the layer pass
-uint64_t stream_threshold() {
-    static const uint64_t v = [] {
-        const char* e = std::getenv("VCS_STREAM_MIN_MB");
-        return static_cast<uint64_t>(e ? std::atof(e) * (1 << 20) : 32.0 * (1 << 20));
-    }();
-    return v;
+uint64_t stream_threshold() { // (read per call: tests force the streamed path on small spaces)
+    const char* e = std::getenv("VCS_STREAM_MIN_MB");
+    return static_cast<uint64_t>(e ? std::atof(e) * (1 << 20) : 32.0 * (1 << 20));
 }
 } // namespace
 

@@ -206,14 +206,18 @@ def test_capped_sweeps_match_oracle(gpu, oracle):
 
 @pytest.mark.parametrize("method", ["WAVEFRONT", "AUTO"])
 @pytest.mark.parametrize("narrow", [True, False])
-def test_pinned_outputs_overlapped_download(gpu, golden, monkeypatch, method, narrow):
-    """vcs_solve into PINNED host buffers streams each layer's results while the layer pass
-    runs (int8 action column widened on the host, or int32 with VCS_NO_NARROW); an early stop
-    (eps = 5, 0.5) rewrites a prefix afterwards (AUTO: after the certified pass's fallback) —
-    all must be exact."""
+@pytest.mark.parametrize("streamed", [True, False])
+def test_pinned_outputs_overlapped_download(gpu, golden, monkeypatch, method, narrow, streamed):
+    """vcs_solve into PINNED host buffers: streamed (VCS_STREAM_MIN_MB=0 forces the path the
+    results >= 32 MB take: pieces behind the layer events, int8 action column widened on the
+    host, or int32 with VCS_NO_NARROW) or in one copy after the pass; an early stop (eps = 5,
+    0.5) rewrites a prefix afterwards (AUTO: after the certified pass's fallback) — all must be
+    exact."""
     import torch
     if not narrow:
         monkeypatch.setenv("VCS_NO_NARROW", "1")
+    if streamed:
+        monkeypatch.setenv("VCS_STREAM_MIN_MB", "0")
     p = V.load_instance(str(GOLDEN / "canonical_instance.txt"))
     ni = V.NativeInstance(p.vcc, bots=p.bots)
     sp = V.StateSpace.build_native(ni)
@@ -592,10 +596,14 @@ def test_batched_policy_query(gpu, reference):
         assert np.array_equal(dact.cpu().numpy(), acts)
 
 
-def test_pinned_download_large(gpu, golden):
+@pytest.mark.parametrize("streamed", [True, False])
+def test_pinned_download_large(gpu, golden, monkeypatch, streamed):
     """C3 (1.8 M states) into pinned buffers: the chunked download behind the layer events of the
-    certified pass is exact, on a fresh and on a re-used graph."""
+    certified pass (forced: C3's 21 MB is below the 32 MB default) and the single copy are exact,
+    on a fresh and on a re-used graph."""
     import torch
+    if streamed:
+        monkeypatch.setenv("VCS_STREAM_MIN_MB", "1")
     ni = V.generate_instance(N.VCS_GEN_HOMOG, 2012, 0, 5, 8, 40, 3, as_objects=False)
     sp = V.StateSpace.build_native(ni, 10**9)
     S = sp.size()
