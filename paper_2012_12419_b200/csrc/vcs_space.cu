@@ -2137,7 +2137,8 @@ void build_layers(vcs_space* sp, uint64_t state_cap) {
             k_bound += nb * static_cast<uint64_t>(L.next_words);
         }
     }
-    const bool presize = e_bound < 0xffffffffull && s_bound < 0xffffffffull &&
+    const bool presize = !std::getenv("VCS_BUILD_NO_PRESIZE") && // (tests: the growth path)
+                         e_bound < 0xffffffffull && s_bound < 0xffffffffull &&
                          (IMPLICIT ? 0 : e_bound * 16 + s_bound * 4) + k_bound * 8 <=
                              device_bytes(sp->device) / 8;
     sp->keys.reserve(presize ? k_bound : 1u << 20, 0, s);

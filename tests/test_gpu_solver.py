@@ -868,3 +868,44 @@ def test_pull_builder_matches_golden_and_oracle(gpu, golden, oracle, monkeypatch
         assert r.values.report.sweeps == sw
         assert np.array_equal(bits(r.values.raw_values()), bits(v)), trial
         assert np.array_equal(r.policy.raw_actions(), a), trial
+
+
+@pytest.mark.parametrize("env", [
+    {"VCS_NO_SMALL_SOLVE": "1"},                         # per-layer k_cert_rows + graph IF node
+    {"VCS_CERT_SMALL_THREADS": "256"}, {"VCS_CERT_SMALL_THREADS": "1024"},
+    {"VCS_SMALL_THREADS": "128"}, {"VCS_SMALL_THREADS": "256"}, {"VCS_SMALL_THREADS": "1024"},
+])
+def test_small_space_kernel_variants_match_golden(gpu, golden, monkeypatch, env):
+    """The single-CTA builder at every block size it is compiled for, the single-CTA certified
+    pass at every block size, and the per-layer certified pass on the same small explicit space
+    (the canonical instance) give the reference's digests at eps = 1e-6 (certified) and at
+    eps = 5 / 0.5 (early stops: the fallback), with the sweep counts."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    p = V.load_instance(str(GOLDEN / "canonical_instance.txt"))
+    sp = V.StateSpace.build_native(V.NativeInstance(p.vcc, bots=p.bots))
+    assert sha(sp.layer_offsets()) == golden["cases"]["canonical"]["layers_sha"]
+    for eps in (1e-6, 5.0, 0.5):
+        g = golden["cases"]["canonical"][f"eps={eps:g}"]
+        for _ in range(2):  # direct first solve, then the captured graph
+            r = _solve(sp, eps=eps, method=N.VCS_METHOD_CERTIFIED)
+            assert r.values.report.sweeps == g["sweeps"], (env, eps)
+            assert sha(r.values.raw_values()) == g["values_sha"], (env, eps)
+            assert sha(r.policy.raw_actions()) == g["actions_sha"], (env, eps)
+
+
+@pytest.mark.parametrize("form", ["explicit", "implicit"])
+def test_layered_builder_growth_path(gpu, golden, monkeypatch, form):
+    """The layered builder without its a-priori sizing (VCS_BUILD_NO_PRESIZE: the arrays grow
+    geometrically, as for spaces whose bound is unaffordable) builds C3 exactly: the explicit CSR
+    (VCS_BUILD_LAYERED) and the implicit form (VCS_BUILD_NO_PERSISTENT) both give the reference's
+    digests."""
+    monkeypatch.setenv("VCS_BUILD_NO_PRESIZE", "1")
+    monkeypatch.setenv("VCS_BUILD_LAYERED" if form == "explicit" else "VCS_BUILD_NO_PERSISTENT", "1")
+    p = V.load_instance(str(GOLDEN / "instances" / "c3.txt"))
+    sp = V.StateSpace.build_native(V.NativeInstance(p.vcc, bots=p.bots), 10**9)
+    g = golden["cases"]["C3"]["eps=1e-06"]
+    assert sp.size() == golden["cases"]["C3"]["S"]
+    r = _solve(sp, method=N.VCS_METHOD_CERTIFIED)
+    assert sha(r.values.raw_values()) == g["values_sha"]
+    assert sha(r.policy.raw_actions()) == g["actions_sha"]
