@@ -909,3 +909,30 @@ def test_layered_builder_growth_path(gpu, golden, monkeypatch, form):
     r = _solve(sp, method=N.VCS_METHOD_CERTIFIED)
     assert sha(r.values.raw_values()) == g["values_sha"]
     assert sha(r.policy.raw_actions()) == g["actions_sha"]
+
+
+@pytest.mark.parametrize("name", ["canonical", "C3"])
+def test_enqueue_collect_on_a_caller_stream(gpu, golden, name):
+    """vcs_solve_enqueue on a caller's stream right after the build (the solve buffers are
+    allocated on the space's stream in the same call and ordered by an event, not a host sync),
+    then vcs_solve_collect into host buffers on that stream: the reference's digests, on a fresh
+    space and on the replayed graph."""
+    import torch
+    path = GOLDEN / ("canonical_instance.txt" if name == "canonical" else "instances/c3.txt")
+    p = V.load_instance(str(path))
+    sp = V.StateSpace.build_native(V.NativeInstance(p.vcc, bots=p.bots), 10**9)
+    g = golden["cases"][name]["eps=1e-06"]
+    st = torch.cuda.Stream()
+    h = C.c_void_p(st.cuda_stream)
+    vals = np.empty(sp.size())
+    acts = np.empty(sp.size(), np.int32)
+    for _ in range(2):
+        opts = N.vcs_solve_opts(1e-6, 1, 0, 1.0, N.VCS_METHOD_CERTIFIED)
+        N.check(N.lib().vcs_solve_enqueue(sp.handle, C.byref(opts), h))
+        rep = N.vcs_solve_report()
+        N.check(N.lib().vcs_solve_collect(sp.handle, N.ptr(vals, C.c_double), N.ptr(acts, C.c_int32),
+                                          C.byref(rep), h))
+        st.synchronize()
+        assert rep.sweeps == g["sweeps"]
+        assert sha(vals) == g["values_sha"]
+        assert sha(acts) == g["actions_sha"]
