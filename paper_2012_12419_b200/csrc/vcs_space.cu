@@ -1863,7 +1863,10 @@ __global__ void __launch_bounds__(NT, 1) k_build_small(SmallBuild A) {
         for (uint32_t j = j0; j < j1; ++j) {
             uint64_t k[WM];
             load_key<WM>(ekey + static_cast<size_t>(j) * WM, nw, k);
-            uint32_t h = static_cast<uint32_t>(hash_key<WM>(k, nw, 0)) & (TC - 1);
+            // (single-word keys: one multiply-shift — the slot is table-internal, the numbering
+            // depends only on the minimum edge of each key)
+            uint32_t h = WM == 1 ? static_cast<uint32_t>((k[0] * 0x9e3779b97f4a7c15ull) >> 40) & (TC - 1)
+                                 : static_cast<uint32_t>(hash_key<WM>(k, nw, 0)) & (TC - 1);
             for (;;) {
                 uint32_t cur = table[h];
                 if (cur == kEmpty32) {
