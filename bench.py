@@ -181,7 +181,12 @@ def common_config(workload, S, H, sweeps, eps):
     """The `config` dict both arms print (identical keys and values)."""
     return {"workload": W.DESCRIPTIONS.get(workload, workload), "states": int(S),
             "horizon": int(H), "sweeps": int(sweeps), "epsilon": eps,
-            "instance": str(W.FILES[workload].relative_to(ROOT)) if workload in W.FILES else None}
+            "instance": str(W.FILES[workload].relative_to(ROOT)) if workload in W.FILES else None,
+            "l2": ("no flush between steps: inputs larger than L2 (a solve reads the keys and "
+                   "rank tables and writes 12 B/state of results: %.0f MB against 126 MB of L2)"
+                   % (S * 12 / 1e6 + S * 8 / 1e6)) if S * 20 > (126 << 20) else
+                  ("no flush between steps: this workload's working set (%.1f MB) is "
+                   "L2-resident; a side number, not the headline configuration" % (S * 20 / 1e6))}
 
 
 def _reference():
